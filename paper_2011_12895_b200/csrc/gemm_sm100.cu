@@ -1,0 +1,128 @@
+// Host launcher for the tcgen05 3xTF32 GEMM (see gemm_sm100.cuh).
+#include <cudaTypedefs.h>
+
+#include <cstring>
+#include <mutex>
+
+#include "gemm_sm100.cuh"
+
+namespace tlg::gemm {
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    TLG_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || p == nullptr)
+      throw CudaError("cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2D fp32 tensor map, 128-byte swizzle, box {32 (inner), box_rows}.
+CUtensorMap make_map(const float* base, long inner, long outer, long ld, int box_rows,
+                     CUtensorMapSwizzle swz) {
+  CUtensorMap m;
+  if (base == nullptr) {
+    std::memset(&m, 0, sizeof(m));
+    return m;
+  }
+  if ((reinterpret_cast<uintptr_t>(base) & 15) != 0 || (ld * 4) % 16 != 0)
+    throw CudaError("gemm operand must be 16-byte aligned with a row pitch multiple of 4 floats");
+  cuuint64_t dims[2] = {cuuint64_t(inner), cuuint64_t(outer)};
+  cuuint64_t strides[1] = {cuuint64_t(ld) * 4};
+  cuuint32_t box[2] = {32, cuuint32_t(box_rows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  return m;
+}
+
+CUtensorMap operand_map(const float* ptr, const Operand& op, long mn, long k, int box_mn) {
+  if (!op.mn_major)  // [mn][k]
+    return make_map(ptr, k, mn, op.ld, box_mn, CU_TENSOR_MAP_SWIZZLE_128B);
+  // [k][mn]: 32-byte swizzle atoms, the layout tcgen05 expects for MN-major tf32
+  return make_map(ptr, mn, k, op.ld, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+}
+
+template <int BN, bool A_MN, bool B_MN, bool A_LO, bool B_LO, int EPI>
+void run(const CUtensorMap& ah, const CUtensorMap& al, const CUtensorMap& bh,
+         const CUtensorMap& bl, const Params& p, dim3 grid, cudaStream_t stream) {
+  auto kern = gemm_tf32x3_kernel<BN, A_MN, B_MN, A_LO, B_LO, EPI>;
+  constexpr int bytes = Smem<BN, A_LO, B_LO>::kBytes;
+  static bool attr = false;  // one-time per instantiation
+  if (!attr) {
+    TLG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    attr = true;
+  }
+  kern<<<grid, kThreads, bytes, stream>>>(ah, al, bh, bl, p);
+  TLG_CHECK_LAUNCH();
+}
+
+template <int BN>
+void dispatch_bn(bool a_mn, bool b_mn, bool a_lo, bool b_lo, int epi, const CUtensorMap& ah,
+                 const CUtensorMap& al, const CUtensorMap& bh, const CUtensorMap& bl,
+                 const Params& p, dim3 grid, cudaStream_t s) {
+  // forward: A = activations (K-major), B = W (K-major)
+  if (!a_mn && !b_mn && b_lo && epi == kEpiFwdTanh) {
+    if (a_lo) return run<BN, false, false, true, true, kEpiFwdTanh>(ah, al, bh, bl, p, grid, s);
+    return run<BN, false, false, false, true, kEpiFwdTanh>(ah, al, bh, bl, p, grid, s);
+  }
+  // dX: A = dZ (K-major), B = W (MN-major)
+  if (!a_mn && b_mn && a_lo && b_lo && epi == kEpiBwdTanh)
+    return run<BN, false, true, true, true, kEpiBwdTanh>(ah, al, bh, bl, p, grid, s);
+  // dW: A = dZ^T (MN-major), B = H (MN-major), split-K partials
+  if (a_mn && b_mn && a_lo && epi == kEpiStore) {
+    if (b_lo) return run<BN, true, true, true, true, kEpiStore>(ah, al, bh, bl, p, grid, s);
+    return run<BN, true, true, true, false, kEpiStore>(ah, al, bh, bl, p, grid, s);
+  }
+  // generic K-major store (used by the testkit)
+  if (!a_mn && !b_mn && a_lo && b_lo && epi == kEpiStore)
+    return run<BN, false, false, true, true, kEpiStore>(ah, al, bh, bl, p, grid, s);
+  throw CudaError("gemm: unsupported operand/epilogue combination");
+}
+
+}  // namespace
+
+int pick_splits(int M, int N, int K, int max_splits) {
+  const int tiles = ceil_div(M, kBM) * ceil_div(N, N > 128 ? 256 : N > 64 ? 128 : 64);
+  const int kb = ceil_div(K, kBK);
+  int s = std::max(1, std::min(max_splits, 148 / std::max(1, tiles)));
+  s = std::min(s, std::max(1, kb / 4));  // keep >= 4 K blocks per split
+  return s;
+}
+
+void launch(const Operand& A, const Operand& B, int M, int N, int K, int epi, Params p,
+            int splits, cudaStream_t stream) {
+  if (M <= 0 || N <= 0 || K <= 0) throw CudaError("gemm: empty problem");
+  const int BN = N > 128 ? 256 : N > 64 ? 128 : 64;
+  const int kb_total = ceil_div(K, kBK);
+  if (splits < 1) splits = 1;
+  if (epi != kEpiStore) splits = 1;
+  p.kb_per_split = ceil_div(kb_total, splits);
+  splits = ceil_div(kb_total, p.kb_per_split);
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  const CUtensorMap ah = operand_map(A.hi, A, M, K, kBM);
+  const CUtensorMap al = operand_map(A.lo, A, M, K, kBM);
+  const CUtensorMap bh = operand_map(B.hi, B, N, K, BN);
+  const CUtensorMap bl = operand_map(B.lo, B, N, K, BN);
+  dim3 grid(ceil_div(M, kBM), ceil_div(N, BN), splits);
+  const bool a_lo = A.lo != nullptr, b_lo = B.lo != nullptr;
+  switch (BN) {
+    case 256: return dispatch_bn<256>(A.mn_major, B.mn_major, a_lo, b_lo, epi, ah, al, bh, bl, p, grid, stream);
+    case 128: return dispatch_bn<128>(A.mn_major, B.mn_major, a_lo, b_lo, epi, ah, al, bh, bl, p, grid, stream);
+    default: return dispatch_bn<64>(A.mn_major, B.mn_major, a_lo, b_lo, epi, ah, al, bh, bl, p, grid, stream);
+  }
+}
+
+}  // namespace tlg::gemm

@@ -1,0 +1,821 @@
+// B200 learner step + InfServer forward behind the C ABI of include/tlg_b200.h.
+//
+// One tlg_learner owns one GPU's shard of Learner::TrainStep (learner.cpp:104-158):
+//
+//   stage batch (H2D or device) -> obs tf32 residual
+//   forward trunk GEMMs   (tcgen05 3xTF32, tanh epilogue writes x and its residual)
+//   K3a heads             (logits, value, target logp)
+//   K1 returns            (GAE + lambda-return | V-trace), adv-norm statistics
+//   K3b loss + dlogits    (PPO / PG), head gradients, tanh' of the last layer
+//   backward trunk GEMMs  (dW split-K + fixed-order reduce, db column sums, dX with tanh')
+//   [NCCL sum-allreduce of the flat fp32 gradient + failure guard]
+//   K7 optimizer          (Adam | SGD; skipped on any rank's failure)
+//
+// All reductions have a fixed order, so a step is bit-reproducible run to run.
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/tlg_b200.h"
+#include "gemm_sm100.cuh"
+#include "learner_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+struct InvalidArg : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct RuntimeErr : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+template <typename F>
+int Guard(F&& f) {
+  try {
+    f();
+    return TLG_OK;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return TLG_INVALID_ARGUMENT;
+  } catch (const tlg::CudaError& e) {
+    g_err = e.what();
+    return TLG_CUDA_ERROR;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return TLG_RUNTIME_ERROR;
+  }
+}
+
+#define NCCL_CHECK(expr)                                                              \
+  do {                                                                                \
+    ncclResult_t _r = (expr);                                                         \
+    if (_r != ncclSuccess)                                                            \
+      throw tlg::CudaError(std::string(#expr) + ": " + ncclGetErrorString(_r));       \
+  } while (0)
+
+// Parameter layout of the three families (policy.cpp:23-27,78-104).
+struct Net {
+  uint32_t family, D, A, L;
+  std::vector<uint32_t> dims;
+  std::vector<long> w_off, b_off;
+  long P = 0;
+  tlg::HeadDesc head{};
+
+  explicit Net(const tlg_policy_shape& s) {
+    if (s.obs_dim == 0 || s.n_actions == 0)
+      throw InvalidArg("policy shape dimensions must be positive");
+    if (s.family > TLG_FAMILY_MLP) throw InvalidArg("unknown policy family");
+    if (s.n_actions + 1 > 32) throw InvalidArg("n_actions > 31 is not supported on the GPU path");
+    family = s.family;
+    D = s.obs_dim;
+    A = s.n_actions;
+    L = family == TLG_FAMILY_MLP ? s.n_hidden : 0;
+    if (L > 8) throw InvalidArg("at most 8 hidden layers");
+    dims.push_back(D);
+    long off = 0;
+    for (uint32_t l = 0; l < L; ++l) {
+      const uint32_t h = s.hidden[l];
+      if (h == 0) throw InvalidArg("hidden width must be positive");
+      if (h % 4 != 0 || dims.back() % 4 != 0)
+        throw InvalidArg("mlp widths (obs_dim and hidden) must be multiples of 4 on the GPU path");
+      w_off.push_back(off);
+      off += long(h) * dims.back();
+      b_off.push_back(off);
+      off += h;
+      dims.push_back(h);
+    }
+    const int H = int(dims.back());
+    head.family = int(family);
+    head.A = int(A);
+    head.H = H;
+    if (family == TLG_FAMILY_MLP) {
+      head.wpi = off; head.wk = H; head.wj = 1; off += long(A) * H;
+      head.bpi = off; off += A;
+      head.wv = off; off += H;
+      head.bv = off; off += 1;
+    } else {
+      head.wpi = 0;
+      head.wk = family == TLG_FAMILY_LINEAR ? int(D) : 1;   // linear W[k][j]  (policy.cpp:86)
+      head.wj = family == TLG_FAMILY_LINEAR ? 1 : int(A);   // tabular T[row][k] (policy.cpp:80)
+      head.bpi = -1;
+      head.wv = long(A) * D;
+      head.bv = -1;
+      off = long(A) * D + D;
+    }
+    P = off;
+  }
+};
+
+template <typename T>
+T* dalloc(size_t n) {
+  void* p = nullptr;
+  if (n == 0) n = 1;
+  TLG_CUDA(cudaMalloc(&p, n * sizeof(T)));
+  TLG_CUDA(cudaMemset(p, 0, n * sizeof(T)));
+  return static_cast<T*>(p);
+}
+
+struct DevFree {
+  std::vector<void*> ptrs;
+  ~DevFree() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+  template <typename T>
+  T* add(size_t n) {
+    T* p = dalloc<T>(n);
+    ptrs.push_back(p);
+    return p;
+  }
+};
+
+long pad4(long n) { return (n + 3) & ~3L; }
+
+}  // namespace
+
+// ===========================================================================
+struct tlg_learner {
+  tlg_learner_config cfg{};
+  Net net;
+  int S_max, T;
+  long F_max;
+  long P_pad;
+  cudaStream_t stream = nullptr;
+  DevFree mem;
+  // parameters / optimizer (flat, fp32); grad has 4 trailing guard slots
+  float *params, *params_lo, *grad, *adam_m, *adam_v;
+  // batch
+  float *obs, *obs_lo;
+  uint8_t* obs_u8;
+  int32_t* action;
+  float *reward, *blogp, *value;
+  uint8_t* done;
+  float* boot;
+  int32_t* valid;
+  // activations
+  std::vector<float*> act, act_lo, dz, dz_lo;
+  float *head_out, *tlogp, *adv, *target;
+  double* seg_partial;
+  tlg::StepStatsDev* stats;
+  int* err;
+  float* hg_partial;
+  double* loss_partial;
+  float* ws;
+  long ws_elems;
+  float* col_partial;
+  // host
+  tlg_hyper hp{};
+  bool hp_set = false;
+  uint64_t adam_t = 0;
+  uint64_t steps_done = 0;
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  tlg::StepStatsDev* h_stats = nullptr;
+  int* h_flags = nullptr;  // [0] err bits, [1..] guard as float bits
+  cudaEvent_t ev[8]{};
+  int launches = 0;
+  int S_last = 0;
+
+  tlg_learner(const tlg_learner_config& c, const tlg_policy_shape& s) : cfg(c), net(s) {
+    if (c.max_segments == 0 || c.unroll_len == 0)
+      throw InvalidArg("max_segments and unroll_len must be >= 1");
+    if (c.algo > TLG_ALGO_PPO_VTRACE) throw InvalidArg("unknown algo");
+    TLG_CUDA(cudaSetDevice(c.device));
+    S_max = int(c.max_segments);
+    T = int(c.unroll_len);
+    F_max = long(S_max) * T;
+    P_pad = pad4(net.P);
+    TLG_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    params = mem.add<float>(P_pad);
+    params_lo = mem.add<float>(P_pad);
+    grad = mem.add<float>(P_pad + 4);
+    adam_m = mem.add<float>(P_pad);
+    adam_v = mem.add<float>(P_pad);
+    const long D = net.D;
+    obs = mem.add<float>(F_max * D);
+    obs_lo = mem.add<float>(F_max * D);
+    obs_u8 = cfg.obs_dtype == TLG_OBS_U8 ? mem.add<uint8_t>(F_max * D + 16) : nullptr;
+    action = mem.add<int32_t>(F_max);
+    reward = mem.add<float>(F_max);
+    blogp = mem.add<float>(F_max);
+    value = mem.add<float>(F_max);
+    done = mem.add<uint8_t>(F_max);
+    boot = mem.add<float>(S_max);
+    valid = mem.add<int32_t>(S_max);
+    for (uint32_t l = 0; l < net.L; ++l) {
+      const long n = F_max * net.dims[l + 1];
+      act.push_back(mem.add<float>(n));
+      act_lo.push_back(mem.add<float>(n));
+      dz.push_back(mem.add<float>(n));
+      dz_lo.push_back(mem.add<float>(n));
+    }
+    const int A1 = int(net.A) + 1;
+    head_out = mem.add<float>(F_max * A1);
+    tlogp = mem.add<float>(F_max);
+    adv = mem.add<float>(F_max);
+    target = mem.add<float>(F_max);
+    seg_partial = mem.add<double>(2 * S_max);
+    stats = mem.add<tlg::StepStatsDev>(1);
+    err = mem.add<int>(4);
+    const long nblk = (F_max + tlg::kLossFrames - 1) / tlg::kLossFrames;
+    hg_partial = mem.add<float>(nblk * A1 * long(net.head.H) + nblk * A1);
+    loss_partial = mem.add<double>(nblk * 5);
+    ws_elems = 0;
+    long max_cols = 1;
+    for (uint32_t l = 0; l < net.L; ++l) {
+      const int out = int(net.dims[l + 1]), in = int(net.dims[l]);
+      const int sp = tlg::gemm::pick_splits(out, in, int(F_max), 16);
+      ws_elems = std::max(ws_elems, long(sp) * out * in);
+      max_cols = std::max<long>(max_cols, out);
+    }
+    ws = ws_elems ? mem.add<float>(ws_elems) : nullptr;
+    col_partial = mem.add<float>(((F_max + 255) / 256) * max_cols);
+    TLG_CUDA(cudaMallocHost(&h_stats, sizeof(tlg::StepStatsDev)));
+    TLG_CUDA(cudaMallocHost(&h_flags, 16));
+    for (auto& e : ev) TLG_CUDA(cudaEventCreate(&e));
+  }
+
+  ~tlg_learner() {
+    if (stream) cudaStreamSynchronize(stream);
+    if (comm) ncclCommDestroy(comm);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    if (h_stats) cudaFreeHost(h_stats);
+    if (h_flags) cudaFreeHost(h_flags);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  void mark(int i) {
+    if (cfg.timing) TLG_CUDA(cudaEventRecord(ev[i], stream));
+  }
+
+  void stage(const tlg_segment_batch& b, int on_device, tlg::BatchDev& bd, const float** obs_f32,
+             bool& obs_exact) {
+    if (b.n_segments == 0) throw InvalidArg("empty minibatch");
+    if (int(b.n_segments) > S_max) throw InvalidArg("batch exceeds the learner's max_segments");
+    if (int(b.unroll_len) != T) throw InvalidArg("unroll_len mismatch");
+    if (b.obs_dim != net.D) throw InvalidArg("observation size does not match policy shape");
+    if (b.obs_dtype != TLG_OBS_F32 && b.obs_dtype != TLG_OBS_U8)
+      throw InvalidArg("unknown obs dtype");
+    if (b.obs_dtype == TLG_OBS_U8 && obs_u8 == nullptr)
+      throw InvalidArg("learner not configured for uint8 observations");
+    const long S = b.n_segments, F = S * T, D = net.D;
+    bd.S = int(S);
+    bd.T = T;
+    if (on_device) {
+      bd.action = b.action;
+      bd.reward = b.reward;
+      bd.blogp = b.behavior_logp;
+      bd.value = b.value_est;
+      bd.done = b.done;
+      bd.boot = b.bootstrap;
+      bd.valid = b.valid_steps;
+      if (b.obs_dtype == TLG_OBS_U8) {
+        tlg::launch_expand_u8(static_cast<const uint8_t*>(b.obs), obs, F * D, stream);
+        ++launches;
+        *obs_f32 = obs;
+        obs_exact = true;
+      } else {
+        *obs_f32 = static_cast<const float*>(b.obs);
+        obs_exact = false;
+      }
+      return;
+    }
+    auto h2d = [&](void* dst, const void* src, size_t bytes) {
+      TLG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream));
+    };
+    if (b.obs_dtype == TLG_OBS_U8) {
+      h2d(obs_u8, b.obs, size_t(F * D));
+      tlg::launch_expand_u8(obs_u8, obs, F * D, stream);
+      ++launches;
+      obs_exact = true;
+    } else {
+      h2d(obs, b.obs, size_t(F * D) * 4);
+      obs_exact = false;
+    }
+    *obs_f32 = obs;
+    h2d(action, b.action, F * 4);
+    h2d(reward, b.reward, F * 4);
+    h2d(blogp, b.behavior_logp, F * 4);
+    h2d(value, b.value_est, F * 4);
+    h2d(done, b.done, F);
+    h2d(boot, b.bootstrap, S * 4);
+    h2d(valid, b.valid_steps, S * 4);
+    bd.action = action;
+    bd.reward = reward;
+    bd.blogp = blogp;
+    bd.value = value;
+    bd.done = done;
+    bd.boot = boot;
+    bd.valid = valid;
+  }
+
+  void step(const tlg_segment_batch& b, int on_device, tlg_step_stats* out) {
+    if (!hp_set) throw InvalidArg("hyperparameters not set");
+    launches = 0;
+    TLG_CUDA(cudaSetDevice(cfg.device));
+    mark(0);
+    tlg::BatchDev bd{};
+    const float* x0 = nullptr;
+    bool obs_exact = false;
+    stage(b, on_device, bd, &x0, obs_exact);
+    S_last = bd.S;
+    const long F = long(bd.S) * T;
+    const long D = net.D;
+    TLG_CUDA(cudaMemsetAsync(err, 0, 16, stream));
+    const float* x0_lo = nullptr;
+    if (net.L > 0 && !obs_exact) {
+      tlg::launch_split_lo(x0, obs_lo, F * D, stream);
+      ++launches;
+      x0_lo = obs_lo;
+    }
+    mark(1);
+    // ---- forward trunk
+    using tlg::gemm::Operand;
+    for (uint32_t l = 0; l < net.L; ++l) {
+      const int in = int(net.dims[l]), outw = int(net.dims[l + 1]);
+      Operand A{l == 0 ? x0 : act[l - 1], l == 0 ? x0_lo : act_lo[l - 1], in, false};
+      Operand B{params + net.w_off[l], params_lo + net.w_off[l], in, false};
+      tlg::gemm::Params p{};
+      p.out_hi = act[l];
+      p.out_lo = act_lo[l];
+      p.ldo = outw;
+      p.bias = params + net.b_off[l];
+      tlg::gemm::launch(A, B, int(F), outw, in, tlg::gemm::kEpiFwdTanh, p, 1, stream);
+      ++launches;
+    }
+    mark(2);
+    // ---- heads, returns, loss
+    const float* hL = net.L ? act[net.L - 1] : x0;
+    const long ldh = net.head.H;
+    tlg::launch_head_forward(net.head, params, hL, ldh, &bd, F, head_out, tlogp, nullptr, err,
+                             stream);
+    tlg::HyperDev hd{float(hp.gamma), float(hp.lam), float(hp.clip_eps), float(hp.vf_coef),
+                     float(hp.ent_coef), float(hp.rho_bar), float(hp.c_bar), hp.adv_norm};
+    const int algo = int(cfg.algo);
+    tlg::launch_returns(bd, algo, hd, tlogp, adv, target, seg_partial, err, stream);
+    tlg::launch_finalize_adv(seg_partial, bd, hp.adv_norm, stats, err, stream);
+    const int loss_kind = algo == TLG_ALGO_VTRACE ? 1 : 0;
+    const int nblk = tlg::launch_loss_backward(
+        net.head, params, hL, ldh, bd, head_out, adv, target, stats, hd, loss_kind,
+        net.L ? dz[net.L - 1] : nullptr, net.L ? dz_lo[net.L - 1] : nullptr, hg_partial,
+        loss_partial, stream);
+    tlg::launch_head_grad_reduce(net.head, hg_partial, loss_partial, nblk, grad, stats, stream);
+    launches += 5;
+    mark(3);
+    // ---- backward trunk
+    for (int l = int(net.L) - 1; l >= 0; --l) {
+      const int in = int(net.dims[l]), outw = int(net.dims[l + 1]);
+      const float* xin = l == 0 ? x0 : act[l - 1];
+      const float* xin_lo = l == 0 ? x0_lo : act_lo[l - 1];
+      // dW_l = dZ_l^T . X_{l-1}   (K = frames, split-K partials reduced in fixed order)
+      int sp = tlg::gemm::pick_splits(outw, in, int(F), 16);
+      while (long(sp) * outw * in > ws_elems && sp > 1) --sp;
+      Operand A{dz[l], dz_lo[l], outw, true};
+      Operand B{xin, xin_lo, in, true};
+      tlg::gemm::Params p{};
+      p.ws = ws;
+      p.ws_split_stride = long(outw) * in;
+      // launch() may shrink the split count so that no split is empty
+      const int kb = (int(F) + tlg::gemm::kBK - 1) / tlg::gemm::kBK;
+      const int per = (kb + sp - 1) / sp;
+      const int sp_eff = (kb + per - 1) / per;
+      tlg::gemm::launch(A, B, outw, in, int(F), tlg::gemm::kEpiStore, p, sp, stream);
+      tlg::launch_dw_reduce(ws, sp_eff, long(outw) * in, grad + net.w_off[l], stream);
+      // db_l = column sums of dZ_l
+      tlg::launch_colsum(dz[l], outw, F, outw, col_partial, grad + net.b_off[l], stream);
+      launches += 4;
+      if (l > 0) {
+        // dZ_{l-1} = (dZ_l . W_l) * (1 - X_{l-1}^2)
+        Operand A2{dz[l], dz_lo[l], outw, false};
+        Operand B2{params + net.w_off[l], params_lo + net.w_off[l], in, true};
+        tlg::gemm::Params p2{};
+        p2.out_hi = dz[l - 1];
+        p2.out_lo = dz_lo[l - 1];
+        p2.ldo = in;
+        p2.act_hi = act[l - 1];
+        p2.ld_act = in;
+        tlg::gemm::launch(A2, B2, int(F), in, outw, tlg::gemm::kEpiBwdTanh, p2, 1, stream);
+        ++launches;
+      }
+    }
+    mark(4);
+    // ---- failure guard + allreduce (learner.cpp:138-149)
+    set_guard();
+    if (nranks > 1) {
+      NCCL_CHECK(ncclAllReduce(grad, grad, size_t(P_pad + 4), ncclFloat, ncclSum, comm, stream));
+    }
+    mark(5);
+    // ---- optimizer (skipped on device when any rank failed)
+    const bool adam = cfg.optimizer == TLG_OPT_ADAM;
+    const uint64_t t = adam_t + 1;
+    const double bc1 = 1.0 - std::pow(cfg.adam_beta1, double(t));
+    const double bc2 = 1.0 - std::pow(cfg.adam_beta2, double(t));
+    launch_guarded_optimizer(adam, float(hp.learning_rate), float(hp.learning_rate / bc1),
+                             float(std::sqrt(bc2)));
+    mark(6);
+    // ---- results
+    TLG_CUDA(cudaMemcpyAsync(h_stats, stats, sizeof(tlg::StepStatsDev), cudaMemcpyDeviceToHost,
+                             stream));
+    TLG_CUDA(cudaMemcpyAsync(h_flags, err, 4, cudaMemcpyDeviceToHost, stream));
+    TLG_CUDA(cudaMemcpyAsync(h_flags + 1, grad + P_pad, 4, cudaMemcpyDeviceToHost, stream));
+    TLG_CUDA(cudaStreamSynchronize(stream));
+    const int e = h_flags[0];
+    float guard;
+    std::memcpy(&guard, &h_flags[1], 4);
+    const uint64_t k = steps_done + 1;
+    if (e & tlg::kErrValidSteps) throw InvalidArg("valid_steps exceeds unroll_len");
+    if (e & tlg::kErrEmptyBatch) throw InvalidArg("empty minibatch");
+    if (e & tlg::kErrNotOneHot) throw InvalidArg("tabular observation must be one-hot");
+    if (e & tlg::kErrActionRange) throw InvalidArg("action out of range");
+    if (e & tlg::kErrNonFiniteLogp) throw InvalidArg("non-finite log probability");
+    if (e & tlg::kErrNonFiniteAdv) throw InvalidArg("non-finite advantage");
+    if (!std::isfinite(h_stats->loss))
+      throw RuntimeErr("non-finite loss at update step " + std::to_string(k));
+    if (guard != 0.f)
+      throw RuntimeErr("learner shard failed on another rank at update step " + std::to_string(k));
+    if (adam) adam_t = t;
+    steps_done = k;
+    if (out) {
+      out->loss = h_stats->loss;
+      out->clip_fraction = algo == TLG_ALGO_VTRACE ? 0.0 : h_stats->clip;
+      out->mean_ratio = h_stats->ratio;
+      out->entropy = h_stats->entropy;
+      out->value_loss = h_stats->vloss;
+      out->n_samples = uint64_t(h_stats->n);
+    }
+  }
+
+  void set_guard();
+  void launch_guarded_optimizer(bool adam, float lr, float step_size, float bc2_sqrt);
+};
+
+namespace {
+
+__global__ void set_guard_kernel(const int* err, const tlg::StepStatsDev* st, float* guard) {
+  const bool bad = (*err != 0) || !isfinite(st->loss);
+  guard[0] = bad ? 1.f : 0.f;
+  guard[1] = guard[2] = guard[3] = 0.f;
+}
+
+__global__ void optimizer_guarded_kernel(float4* __restrict__ p, float4* __restrict__ plo,
+                                         const float4* __restrict__ g, float4* __restrict__ m,
+                                         float4* __restrict__ v, long n4, const float* guard,
+                                         float grad_scale, int adam, float lr, float step_size,
+                                         float bc2_sqrt, float b1, float b2, float eps) {
+  if (*guard != 0.f) return;  // some shard failed: parameters stay untouched
+  for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n4;
+       i += long(gridDim.x) * blockDim.x) {
+    float4 pp = p[i];
+    const float4 gg = g[i];
+    float* pe = &pp.x;
+    const float* ge = &gg.x;
+    if (adam) {
+      float4 mm = m[i], vv = v[i];
+      float* me = &mm.x;
+      float* ve = &vv.x;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float gq = ge[q] * grad_scale;
+        me[q] = b1 * me[q] + (1.f - b1) * gq;
+        ve[q] = b2 * ve[q] + (1.f - b2) * gq * gq;
+        const float denom = sqrtf(ve[q]) / bc2_sqrt + eps;
+        pe[q] -= step_size * me[q] / denom;
+      }
+      m[i] = mm;
+      v[i] = vv;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) pe[q] -= lr * (ge[q] * grad_scale);
+    }
+    p[i] = pp;
+    plo[i] = make_float4(pp.x - tlg::tf32_hi(pp.x), pp.y - tlg::tf32_hi(pp.y),
+                         pp.z - tlg::tf32_hi(pp.z), pp.w - tlg::tf32_hi(pp.w));
+  }
+}
+
+__global__ void split_lo_flat(const float* x, float* lo, long n) {
+  long i = blockIdx.x * long(blockDim.x) + threadIdx.x;
+  if (i < n) lo[i] = x[i] - tlg::tf32_hi(x[i]);
+}
+
+}  // namespace
+
+void tlg_learner::set_guard() {
+  set_guard_kernel<<<1, 1, 0, stream>>>(err, stats, grad + P_pad);
+  TLG_CHECK_LAUNCH();
+  ++launches;
+}
+
+void tlg_learner::launch_guarded_optimizer(bool adam, float lr, float step_size, float bc2_sqrt) {
+  const long n4 = P_pad / 4;
+  const int blocks = int(std::max<long>(1, std::min<long>((n4 + 255) / 256, 148L * 4)));
+  optimizer_guarded_kernel<<<blocks, 256, 0, stream>>>(
+      reinterpret_cast<float4*>(params), reinterpret_cast<float4*>(params_lo),
+      reinterpret_cast<const float4*>(grad), reinterpret_cast<float4*>(adam_m),
+      reinterpret_cast<float4*>(adam_v), n4, grad + P_pad, 1.f / float(nranks), adam ? 1 : 0, lr,
+      step_size, bc2_sqrt, float(cfg.adam_beta1), float(cfg.adam_beta2), float(cfg.adam_eps));
+  TLG_CHECK_LAUNCH();
+  ++launches;
+}
+
+// ===========================================================================
+struct tlg_policy {
+  Net net;
+  int device;
+  long max_batch;
+  cudaStream_t stream = nullptr;
+  DevFree mem;
+  float *params, *params_lo, *obs, *obs_lo, *head_out, *logits, *probs, *value;
+  std::vector<float*> act, act_lo;
+  int* err;
+  long P_pad;
+
+  tlg_policy(const tlg_policy_shape& s, int dev, long mb) : net(s), device(dev), max_batch(mb) {
+    if (mb <= 0) throw InvalidArg("max_batch must be >= 1");
+    TLG_CUDA(cudaSetDevice(dev));
+    TLG_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    P_pad = pad4(net.P);
+    params = mem.add<float>(P_pad);
+    params_lo = mem.add<float>(P_pad);
+    obs = mem.add<float>(mb * net.D);
+    obs_lo = mem.add<float>(mb * net.D);
+    head_out = mem.add<float>(mb * (net.A + 1));
+    logits = mem.add<float>(mb * net.A);
+    probs = mem.add<float>(mb * net.A);
+    value = mem.add<float>(mb);
+    err = mem.add<int>(4);
+    for (uint32_t l = 0; l < net.L; ++l) {
+      act.push_back(mem.add<float>(mb * net.dims[l + 1]));
+      act_lo.push_back(mem.add<float>(mb * net.dims[l + 1]));
+    }
+  }
+  ~tlg_policy() {
+    if (stream) {
+      cudaStreamSynchronize(stream);
+      cudaStreamDestroy(stream);
+    }
+  }
+};
+
+namespace {
+
+__global__ void unpack_head_kernel(const float* head_out, int A, long n, float* logits,
+                                   float* value) {
+  const long i = blockIdx.x * long(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  for (int k = 0; k < A; ++k) logits[i * A + k] = head_out[i * (A + 1) + k];
+  value[i] = head_out[i * (A + 1) + A];
+}
+
+void set_params_common(float* params, float* params_lo, long P, long P_pad, const double* values,
+                       size_t n, cudaStream_t stream) {
+  if (long(n) != P) throw InvalidArg("parameter count mismatch");
+  std::vector<float> h(P_pad, 0.f);
+  for (long i = 0; i < P; ++i) h[i] = float(values[i]);
+  TLG_CUDA(cudaMemcpyAsync(params, h.data(), P_pad * 4, cudaMemcpyHostToDevice, stream));
+  split_lo_flat<<<int((P_pad + 255) / 256), 256, 0, stream>>>(params, params_lo, P_pad);
+  TLG_CHECK_LAUNCH();
+  TLG_CUDA(cudaStreamSynchronize(stream));
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+const char* tlg_last_error(void) { return g_err.c_str(); }
+const char* tlg_version(void) { return "tlg_b200 0.1 (sm_100a, tcgen05 3xTF32)"; }
+
+int tlg_learner_create(const tlg_learner_config* cfg, const tlg_policy_shape* shape,
+                       tlg_learner** out) {
+  return Guard([&] {
+    if (!cfg || !shape || !out) throw InvalidArg("null argument");
+    *out = new tlg_learner(*cfg, *shape);
+  });
+}
+
+void tlg_learner_destroy(tlg_learner* l) { delete l; }
+
+size_t tlg_learner_param_count(const tlg_learner* l) { return l ? size_t(l->net.P) : 0; }
+
+int tlg_learner_set_params(tlg_learner* l, const double* values, size_t n) {
+  return Guard([&] {
+    TLG_CUDA(cudaSetDevice(l->cfg.device));
+    set_params_common(l->params, l->params_lo, l->net.P, l->P_pad, values, n, l->stream);
+    TLG_CUDA(cudaMemsetAsync(l->adam_m, 0, l->P_pad * 4, l->stream));
+    TLG_CUDA(cudaMemsetAsync(l->adam_v, 0, l->P_pad * 4, l->stream));
+    TLG_CUDA(cudaStreamSynchronize(l->stream));
+    l->adam_t = 0;
+  });
+}
+
+int tlg_learner_get_params(tlg_learner* l, double* values, size_t n) {
+  return Guard([&] {
+    if (long(n) != l->net.P) throw InvalidArg("parameter count mismatch");
+    std::vector<float> h(l->net.P);
+    TLG_CUDA(cudaMemcpyAsync(h.data(), l->params, l->net.P * 4, cudaMemcpyDeviceToHost,
+                             l->stream));
+    TLG_CUDA(cudaStreamSynchronize(l->stream));
+    for (long i = 0; i < l->net.P; ++i) values[i] = double(h[i]);
+  });
+}
+
+int tlg_learner_get_grad(tlg_learner* l, double* values, size_t n) {
+  return Guard([&] {
+    if (long(n) != l->net.P) throw InvalidArg("parameter count mismatch");
+    std::vector<float> h(l->net.P);
+    TLG_CUDA(cudaMemcpyAsync(h.data(), l->grad, l->net.P * 4, cudaMemcpyDeviceToHost,
+                             l->stream));
+    TLG_CUDA(cudaStreamSynchronize(l->stream));
+    const double inv = 1.0 / double(l->nranks);
+    for (long i = 0; i < l->net.P; ++i) values[i] = double(h[i]) * inv;
+  });
+}
+
+int tlg_learner_get_returns(tlg_learner* l, float* adv, float* target, size_t n_frames) {
+  return Guard([&] {
+    const long F = long(l->S_last) * l->T;
+    if (long(n_frames) < F) throw InvalidArg("buffer too small");
+    TLG_CUDA(cudaMemcpyAsync(adv, l->adv, F * 4, cudaMemcpyDeviceToHost, l->stream));
+    TLG_CUDA(cudaMemcpyAsync(target, l->target, F * 4, cudaMemcpyDeviceToHost, l->stream));
+    TLG_CUDA(cudaStreamSynchronize(l->stream));
+  });
+}
+
+int tlg_learner_set_hyper(tlg_learner* l, const tlg_hyper* hp) {
+  return Guard([&] {
+    // HyperParams::Validate subset (types.cpp:17-35)
+    if (!(std::isfinite(hp->learning_rate) && hp->learning_rate > 0))
+      throw InvalidArg("hyperparams: learning_rate must be > 0");
+    if (!(hp->gamma > 0 && hp->gamma <= 1)) throw InvalidArg("hyperparams: gamma must be in (0, 1]");
+    if (!(hp->lam >= 0 && hp->lam <= 1)) throw InvalidArg("hyperparams: lam must be in [0, 1]");
+    if (!(hp->clip_eps > 0)) throw InvalidArg("hyperparams: clip_eps must be > 0");
+    if (!(hp->rho_bar > 0) || !(hp->c_bar > 0) || hp->c_bar > hp->rho_bar)
+      throw InvalidArg("hyperparams: need 0 < c_bar <= rho_bar");
+    if (hp->kl_teacher_coef > 0)
+      throw InvalidArg("teacher params required when kl_teacher_coef > 0");
+    l->hp = *hp;
+    l->hp_set = true;
+  });
+}
+
+int tlg_comm_unique_id(uint8_t out[128]) {
+  return Guard([&] {
+    ncclUniqueId id;
+    NCCL_CHECK(ncclGetUniqueId(&id));
+    static_assert(sizeof(id) == 128, "ncclUniqueId size");
+    std::memcpy(out, &id, 128);
+  });
+}
+
+int tlg_learner_comm_init(tlg_learner* l, const uint8_t unique_id[128], int nranks, int rank) {
+  return Guard([&] {
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw InvalidArg("bad rank / nranks");
+    TLG_CUDA(cudaSetDevice(l->cfg.device));
+    if (l->comm) {
+      ncclCommDestroy(l->comm);
+      l->comm = nullptr;
+    }
+    l->nranks = nranks;
+    l->rank = rank;
+    if (nranks > 1) {
+      ncclUniqueId id;
+      std::memcpy(&id, unique_id, 128);
+      NCCL_CHECK(ncclCommInitRank(&l->comm, nranks, id, rank));
+    }
+  });
+}
+
+int tlg_learner_train_step(tlg_learner* l, const tlg_segment_batch* batch, int on_device,
+                           tlg_step_stats* stats) {
+  return Guard([&] {
+    if (!l || !batch) throw InvalidArg("null argument");
+    l->step(*batch, on_device, stats);
+  });
+}
+
+void* tlg_learner_stream(tlg_learner* l) { return l ? static_cast<void*>(l->stream) : nullptr; }
+
+int tlg_learner_phase_ms(tlg_learner* l, float* out, int n) {
+  return Guard([&] {
+    if (!l->cfg.timing) throw InvalidArg("learner created without timing");
+    const int pairs[7][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 4}, {4, 5}, {5, 6}, {0, 6}};
+    for (int i = 0; i < n && i < 7; ++i)
+      TLG_CUDA(cudaEventElapsedTime(&out[i], l->ev[pairs[i][0]], l->ev[pairs[i][1]]));
+  });
+}
+
+int tlg_learner_last_launches(tlg_learner* l) { return l ? l->launches : 0; }
+
+int tlg_policy_create(const tlg_policy_shape* shape, int32_t device, uint32_t max_batch,
+                      tlg_policy** out) {
+  return Guard([&] { *out = new tlg_policy(*shape, device, long(max_batch)); });
+}
+
+void tlg_policy_destroy(tlg_policy* p) { delete p; }
+
+int tlg_policy_set_params(tlg_policy* p, const double* values, size_t n) {
+  return Guard([&] {
+    TLG_CUDA(cudaSetDevice(p->device));
+    set_params_common(p->params, p->params_lo, p->net.P, p->P_pad, values, n, p->stream);
+  });
+}
+
+int tlg_policy_forward(tlg_policy* p, const float* obs, size_t n, float* logits, float* probs,
+                       float* value, int on_device) {
+  return Guard([&] {
+    if (n == 0) return;
+    if (long(n) > p->max_batch) throw InvalidArg("batch exceeds max_batch");
+    TLG_CUDA(cudaSetDevice(p->device));
+    const long D = p->net.D, A = p->net.A;
+    const float* x0 = obs;
+    if (!on_device) {
+      TLG_CUDA(cudaMemcpyAsync(p->obs, obs, n * D * 4, cudaMemcpyHostToDevice, p->stream));
+      x0 = p->obs;
+    }
+    const float* x0_lo = nullptr;
+    if (p->net.L > 0) {
+      tlg::launch_split_lo(x0, p->obs_lo, long(n) * D, p->stream);
+      x0_lo = p->obs_lo;
+    }
+    using tlg::gemm::Operand;
+    for (uint32_t l = 0; l < p->net.L; ++l) {
+      const int in = int(p->net.dims[l]), outw = int(p->net.dims[l + 1]);
+      Operand Aop{l == 0 ? x0 : p->act[l - 1], l == 0 ? x0_lo : p->act_lo[l - 1], in, false};
+      Operand Bop{p->params + p->net.w_off[l], p->params_lo + p->net.w_off[l], in, false};
+      tlg::gemm::Params gp{};
+      gp.out_hi = p->act[l];
+      gp.out_lo = p->act_lo[l];
+      gp.ldo = outw;
+      gp.bias = p->params + p->net.b_off[l];
+      tlg::gemm::launch(Aop, Bop, int(n), outw, in, tlg::gemm::kEpiFwdTanh, gp, 1, p->stream);
+    }
+    const float* hL = p->net.L ? p->act[p->net.L - 1] : x0;
+    float* lg = on_device ? logits : p->logits;
+    float* pr = on_device ? probs : p->probs;
+    float* vv = on_device ? value : p->value;
+    TLG_CUDA(cudaMemsetAsync(p->err, 0, 4, p->stream));
+    tlg::launch_head_forward(p->net.head, p->params, hL, p->net.head.H, nullptr, long(n),
+                             p->head_out, nullptr, pr, p->err, p->stream);
+    unpack_head_kernel<<<int((n + 255) / 256), 256, 0, p->stream>>>(p->head_out, int(A), long(n),
+                                                                     lg, vv);
+    TLG_CHECK_LAUNCH();
+    if (!on_device) {
+      TLG_CUDA(cudaMemcpyAsync(logits, p->logits, n * A * 4, cudaMemcpyDeviceToHost, p->stream));
+      TLG_CUDA(cudaMemcpyAsync(probs, p->probs, n * A * 4, cudaMemcpyDeviceToHost, p->stream));
+      TLG_CUDA(cudaMemcpyAsync(value, p->value, n * 4, cudaMemcpyDeviceToHost, p->stream));
+    }
+    int e = 0;
+    TLG_CUDA(cudaMemcpyAsync(&e, p->err, 4, cudaMemcpyDeviceToHost, p->stream));
+    TLG_CUDA(cudaStreamSynchronize(p->stream));
+    if (e & tlg::kErrNotOneHot) throw InvalidArg("tabular observation must be one-hot");
+  });
+}
+
+void* tlg_policy_stream(tlg_policy* p) { return p ? static_cast<void*>(p->stream) : nullptr; }
+
+int tlg_returns(uint32_t algo, const tlg_hyper* hp, uint32_t n_segments, uint32_t unroll_len,
+                const float* reward, const float* value_est, const uint8_t* done,
+                const float* bootstrap, const int32_t* valid_steps, const float* behavior_logp,
+                const float* target_logp, float* adv, float* target, void* stream) {
+  return Guard([&] {
+    if (n_segments == 0 || unroll_len == 0) throw InvalidArg("segment length must be >= 1");
+    if (algo != TLG_ALGO_PPO && target_logp == nullptr)
+      throw InvalidArg("V-trace needs target log-probabilities");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    tlg::BatchDev bd{};
+    bd.S = int(n_segments);
+    bd.T = int(unroll_len);
+    bd.reward = reward;
+    bd.value = value_est;
+    bd.done = done;
+    bd.boot = bootstrap;
+    bd.valid = valid_steps;
+    bd.blogp = behavior_logp;
+    tlg::HyperDev hd{float(hp->gamma), float(hp->lam), float(hp->clip_eps), float(hp->vf_coef),
+                     float(hp->ent_coef), float(hp->rho_bar), float(hp->c_bar), hp->adv_norm};
+    double* part = nullptr;
+    int* err = nullptr;
+    TLG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part), 16 * size_t(n_segments), s));
+    TLG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&err), 4, s));
+    TLG_CUDA(cudaMemsetAsync(err, 0, 4, s));
+    tlg::launch_returns(bd, int(algo == TLG_ALGO_PPO ? tlg::kAlgoPpo : tlg::kAlgoVtrace), hd,
+                        target_logp, adv, target, part, err, s);
+    int e = 0;
+    TLG_CUDA(cudaMemcpyAsync(&e, err, 4, cudaMemcpyDeviceToHost, s));
+    TLG_CUDA(cudaFreeAsync(part, s));
+    TLG_CUDA(cudaFreeAsync(err, s));
+    TLG_CUDA(cudaStreamSynchronize(s));
+    if (e & tlg::kErrNonFiniteLogp) throw InvalidArg("non-finite log probability");
+    if (e & tlg::kErrValidSteps) throw InvalidArg("valid_steps exceeds unroll_len");
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,665 @@
+// Non-GEMM kernels of the B200 learner step (see learner_kernels.cuh).
+#include <cmath>
+
+#include "learner_kernels.cuh"
+
+namespace tlg {
+
+namespace {
+
+constexpr int kMaxA1Limit = 32;  // n_actions + 1 (value) supported by the head kernels
+
+__device__ __forceinline__ bool frame_valid(const BatchDev* b, long f, int* t_out = nullptr) {
+  if (b == nullptr) return true;
+  const int s = int(f / b->T), t = int(f % b->T);
+  if (t_out) *t_out = t;
+  return t < b->valid[s];
+}
+
+// ---------------------------------------------------------------------------
+__global__ void expand_u8_kernel(const uchar4* __restrict__ in, float4* __restrict__ out, long n4) {
+  for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n4; i += long(gridDim.x) * blockDim.x) {
+    const uchar4 u = in[i];
+    out[i] = make_float4(u.x, u.y, u.z, u.w);
+  }
+}
+
+__global__ void split_lo_kernel(const float4* __restrict__ x, float4* __restrict__ lo, long n4) {
+  for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n4; i += long(gridDim.x) * blockDim.x) {
+    const float4 v = x[i];
+    lo[i] = make_float4(v.x - tf32_hi(v.x), v.y - tf32_hi(v.y), v.z - tf32_hi(v.z),
+                        v.w - tf32_hi(v.w));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3a: one warp per frame.  Distribution + ValueEstimate (policy.cpp:73-105) with a
+// max-shifted log-sum-exp; writes logits+value [F x (A+1)], the log-prob of the
+// taken action (V-trace target logp, learner.cpp:80-84) and optionally probs.
+template <int kMaxA1>
+__global__ void __launch_bounds__(256) head_forward_kernel(HeadDesc hd, const float* __restrict__ params,
+                                                         const float* __restrict__ h, long ldh,
+                                                         BatchDev bd, int has_batch, long F,
+                                                         float* __restrict__ head_out,
+                                                         float* __restrict__ tlogp,
+                                                         float* __restrict__ probs_out,
+                                                         int* __restrict__ err) {
+  const BatchDev* b = has_batch ? &bd : nullptr;
+  const int lane = threadIdx.x & 31;
+  const long warps = long(gridDim.x) * (blockDim.x >> 5);
+  const int A = hd.A, A1 = hd.A + 1;
+  for (long f = blockIdx.x * long(blockDim.x >> 5) + (threadIdx.x >> 5); f < F; f += warps) {
+    if (!frame_valid(b, f)) {
+      if (lane < A1) head_out[f * A1 + lane] = 0.f;
+      if (lane == 0 && tlogp) tlogp[f] = 0.f;
+      continue;
+    }
+    const float* hr = h + f * ldh;
+    float acc[kMaxA1];
+#pragma unroll
+    for (int k = 0; k < kMaxA1; ++k) acc[k] = 0.f;
+    int ones = 0, others = 0;
+    for (int j = lane; j < hd.H; j += 32) {
+      const float x = hr[j];
+      if (hd.family == 0) {
+        if (x == 1.f) { ++ones; } else if (x != 0.f) { ++others; }
+      }
+      const float* w = params + hd.wpi + long(j) * hd.wj;
+#pragma unroll
+      for (int k = 0; k < kMaxA1 - 1; ++k)
+        if (k < A) acc[k] = fmaf(__ldg(w + long(k) * hd.wk), x, acc[k]);
+      acc[kMaxA1 - 1] = fmaf(__ldg(params + hd.wv + j), x, acc[kMaxA1 - 1]);
+    }
+#pragma unroll
+    for (int k = 0; k < kMaxA1; ++k)
+      if (k < A || k == kMaxA1 - 1) acc[k] = warp_sum(acc[k]);
+    if (hd.family == 0) {
+      ones = __reduce_add_sync(0xffffffffu, ones);
+      others = __reduce_add_sync(0xffffffffu, others);
+      if (ones != 1 || others != 0) {
+        if (lane == 0) atomicOr(err, kErrNotOneHot);
+      }
+    }
+    if (lane == 0) {
+      float z[kMaxA1];
+      float mx = -INFINITY;
+#pragma unroll
+      for (int k = 0; k < kMaxA1 - 1; ++k)
+        if (k < A) {
+          z[k] = acc[k] + (hd.bpi >= 0 ? params[hd.bpi + k] : 0.f);
+          mx = fmaxf(mx, z[k]);
+        }
+      float se = 0.f;
+#pragma unroll
+      for (int k = 0; k < kMaxA1 - 1; ++k)
+        if (k < A) se += expf(z[k] - mx);
+      const float lse = mx + logf(se);
+      const float v = acc[kMaxA1 - 1] + (hd.bv >= 0 ? params[hd.bv] : 0.f);
+#pragma unroll
+      for (int k = 0; k < kMaxA1 - 1; ++k)
+        if (k < A) {
+          head_out[f * A1 + k] = z[k];
+          if (probs_out) probs_out[f * A + k] = expf(z[k] - lse);
+        }
+      head_out[f * A1 + A] = v;
+      if (b) {
+        const int a = b->action[f];
+        if (a < 0 || a >= A) {
+          atomicOr(err, kErrActionRange);
+          if (tlogp) tlogp[f] = 0.f;
+        } else if (tlogp) {
+          float za = 0.f;
+#pragma unroll
+          for (int k = 0; k < kMaxA1 - 1; ++k)
+            if (k == a) za = z[k];
+          tlogp[f] = za - lse;
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1: one warp per segment; lanes cover 32 consecutive steps, blocks of 32 steps are
+// processed from the end so every warp load/store is one coalesced 128-B row slice.
+// Each recursion x_t = a_t x_{t+1} + b_t is a suffix scan of affine maps.
+struct Aff {
+  float a, b;
+};
+
+__device__ __forceinline__ Aff suffix_scan(Aff m, int lane) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const float a2 = __shfl_down_sync(0xffffffffu, m.a, d);
+    const float b2 = __shfl_down_sync(0xffffffffu, m.b, d);
+    if (lane + d < 32) {
+      m.b = fmaf(m.a, b2, m.b);
+      m.a = m.a * a2;
+    }
+  }
+  return m;
+}
+
+__global__ void __launch_bounds__(256) returns_kernel(BatchDev b, int algo, HyperDev hp,
+                                                      const float* __restrict__ tlogp,
+                                                      float* __restrict__ adv,
+                                                      float* __restrict__ target,
+                                                      double* __restrict__ seg_partial,
+                                                      int* __restrict__ err) {
+  const int lane = threadIdx.x & 31;
+  const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (s >= b.S) return;
+  const int T = b.T;
+  int n = b.valid[s];
+  if (n > T || n < 0) {
+    if (lane == 0) atomicOr(err, kErrValidSteps);
+    n = min(max(n, 0), T);
+  }
+  const long base = long(s) * T;
+  const float boot = b.boot[s];
+  const float g = hp.gamma, gl = hp.gamma * hp.lam;
+  const int nblk = (T + 31) / 32;
+  // carries from the block after the current one (t = (jb+1)*32)
+  float carry_v = boot;    // V_{t+1} for lane 31 (bootstrap when t+1 >= n)
+  float carry_x = 0.f;     // GAE A / V-trace u at the block start after
+  float carry_g = boot;    // lambda-return G
+  float carry_vs = boot;   // V-trace vs_{t+1}
+  double s1 = 0.0, s2 = 0.0;
+  bool bad_adv = false, bad_logp = false;
+  for (int jb = nblk - 1; jb >= 0; --jb) {
+    const int t = jb * 32 + lane;
+    const bool in = t < n;
+    const long f = base + t;
+    const float r = in ? b.reward[f] : 0.f;
+    const float v = in ? b.value[f] : 0.f;
+    const float nt = (in && b.done[f]) ? 0.f : 1.f;
+    float v_next = __shfl_down_sync(0xffffffffu, v, 1);
+    if (lane == 31) v_next = carry_v;
+    if (t + 1 >= n) v_next = boot;
+    if (algo == kAlgoPpo) {
+      // GaeAdvantages (rlmath.cpp:62-78) and LambdaReturn (:45-60)
+      Aff ma{in ? gl * nt : 0.f, in ? (r + g * nt * v_next - v) : 0.f};
+      Aff mg{in ? gl * nt : 0.f, in ? (r + g * nt * (1.f - hp.lam) * v_next) : boot};
+      ma = suffix_scan(ma, lane);
+      mg = suffix_scan(mg, lane);
+      const float A_t = fmaf(ma.a, carry_x, ma.b);
+      const float G_t = fmaf(mg.a, carry_g, mg.b);
+      if (t < T) {
+        adv[f] = in ? A_t : 0.f;
+        target[f] = in ? G_t : 0.f;
+      }
+      if (in) {
+        bad_adv |= !isfinite(A_t);
+        s1 += double(A_t);
+        s2 += double(A_t) * double(A_t);
+      }
+      carry_x = __shfl_sync(0xffffffffu, A_t, 0);
+      carry_g = __shfl_sync(0xffffffffu, G_t, 0);
+    } else {
+      // VtraceTargets (rlmath.cpp:80-114): truncated importance weights fused in
+      float rho = 0.f, c = 0.f;
+      if (in) {
+        const float bl = b.blogp[f], tl = tlogp[f];
+        if (!isfinite(bl) || !isfinite(tl)) bad_logp = true;
+        const float w = expf(tl - bl);
+        rho = fminf(hp.rho_bar, w);
+        c = fminf(hp.c_bar, w);
+      }
+      const float delta = rho * (r + g * nt * v_next - v);
+      Aff mu{in ? g * nt * c : 0.f, in ? delta : 0.f};
+      mu = suffix_scan(mu, lane);
+      const float u = fmaf(mu.a, carry_x, mu.b);
+      const float vs = v + u;
+      float vs_next = __shfl_down_sync(0xffffffffu, vs, 1);
+      if (lane == 31) vs_next = carry_vs;
+      if (t + 1 >= n) vs_next = boot;
+      const float pg = rho * (r + g * nt * vs_next - v);
+      if (t < T) {
+        adv[f] = in ? pg : 0.f;
+        target[f] = in ? vs : 0.f;
+      }
+      if (in) {
+        bad_adv |= !isfinite(pg);
+        s1 += double(pg);
+        s2 += double(pg) * double(pg);
+      }
+      carry_x = __shfl_sync(0xffffffffu, u, 0);
+      carry_vs = __shfl_sync(0xffffffffu, vs, 0);
+    }
+    carry_v = __shfl_sync(0xffffffffu, v, 0);
+  }
+  s1 = warp_sum(s1);
+  s2 = warp_sum(s2);
+  const unsigned anybad = __ballot_sync(0xffffffffu, bad_adv);
+  const unsigned anylogp = __ballot_sync(0xffffffffu, bad_logp);
+  if (lane == 0) {
+    seg_partial[2 * s] = s1;
+    seg_partial[2 * s + 1] = s2;
+    if (anylogp) atomicOr(err, kErrNonFiniteLogp);
+    if (anybad) atomicOr(err, kErrNonFiniteAdv);
+  }
+}
+
+// EffectiveAdvantages statistics (rlmath.cpp:18-34), fixed-order fp64 reduction.
+__global__ void __launch_bounds__(1024) finalize_adv_kernel(const double* __restrict__ seg_partial,
+                                                            BatchDev b, int adv_norm,
+                                                            StepStatsDev* st, int* err) {
+  __shared__ double sh1[32], sh2[32];
+  __shared__ long long shn[32];
+  double s1 = 0.0, s2 = 0.0;
+  long long n = 0;
+  for (int s = threadIdx.x; s < b.S; s += blockDim.x) {
+    s1 += seg_partial[2 * s];
+    s2 += seg_partial[2 * s + 1];
+    n += min(max(b.valid[s], 0), b.T);
+  }
+  s1 = warp_sum(s1);
+  s2 = warp_sum(s2);
+  for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) { sh1[w] = s1; sh2[w] = s2; shn[w] = n; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, c = 0.0;
+    long long nn = 0;
+    for (int i = 0; i < int(blockDim.x >> 5); ++i) { a += sh1[i]; c += sh2[i]; nn += shn[i]; }
+    st->sum_adv = a;
+    st->sum_adv2 = c;
+    st->n = nn;
+    if (nn == 0) {
+      atomicOr(err, kErrEmptyBatch);
+      st->inv_n = 0.0; st->mean = 0.0; st->sd = 1.0;
+      return;
+    }
+    st->inv_n = 1.0 / double(nn);
+    if (adv_norm && nn >= 2) {
+      const double mean = a / double(nn);
+      double var = c / double(nn) - mean * mean;
+      if (var < 0.0) var = 0.0;
+      st->mean = mean;
+      st->sd = fmax(sqrt(var), 1e-8);
+    } else {
+      st->mean = 0.0;
+      st->sd = 1.0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3b.  Block = kLossFrames frames x 256 threads.
+//  phase 1 (thread per frame): per-sample PPO / PG body (rlmath.cpp:129-182 / 196-220)
+//          -> dlogits, dvalue in smem; loss/stat partials (fp64).
+//  phase 2 (thread per head-input column j): dZ_L[f][j] = (sum_k dz_k W_pi[k][j] +
+//          dV w_v[j]) * (1 - h^2) for the trunk, and the head weight gradient
+//          partials sum_f dz_k(f) h[f][j] (AccumulateGrad, policy.cpp:122-141).
+template <int kMaxA1>
+__global__ void __launch_bounds__(256) loss_backward_kernel(
+    HeadDesc hd, const float* __restrict__ params, const float* __restrict__ h, long ldh,
+    BatchDev b, const float* __restrict__ head_out, const float* __restrict__ adv,
+    const float* __restrict__ target, const StepStatsDev* __restrict__ st, HyperDev hp,
+    int loss_kind, float* __restrict__ dz, float* __restrict__ dz_lo,
+    float* __restrict__ hg_partial, double* __restrict__ loss_partial) {
+  extern __shared__ float sdz[];  // [kLossFrames][A1]
+  __shared__ double red[5][8];
+  const int A = hd.A, A1 = A + 1;
+  const long F = long(b.S) * b.T;
+  const long f0 = long(blockIdx.x) * kLossFrames;
+  const int tid = threadIdx.x;
+  const float inv_n = float(st->inv_n);
+  const double mean = st->mean, sd = st->sd;
+
+  // ---- phase 1
+  double l_loss = 0, l_ratio = 0, l_ent = 0, l_vl = 0, l_clip = 0;
+  for (int i = tid; i < kLossFrames; i += blockDim.x) {
+    const long f = f0 + i;
+    float* d = sdz + i * A1;
+    bool valid = false;
+    if (f < F) {
+      const int s = int(f / b.T), t = int(f % b.T);
+      valid = t < b.valid[s];
+    }
+    if (!valid) {
+      for (int k = 0; k < A1; ++k) d[k] = 0.f;
+      continue;
+    }
+    const float* z = head_out + f * A1;
+    float mx = -INFINITY;
+    for (int k = 0; k < A; ++k) mx = fmaxf(mx, z[k]);
+    float se = 0.f;
+    for (int k = 0; k < A; ++k) se += expf(z[k] - mx);
+    const float lse = mx + logf(se);
+    float ent = 0.f;
+    for (int k = 0; k < A; ++k) {
+      const float lp = z[k] - lse;
+      const float p = expf(lp);
+      if (p > 0.f) ent -= p * lp;  // Entropy (rlmath.cpp:36-41)
+    }
+    const int a = min(max(b.action[f], 0), A - 1);  // out-of-range is flagged by K3a
+    const float logp = z[a] - lse;
+    const float V = z[A];
+    const float verr = V - target[f];
+    const float ad = float((double(adv[f]) - mean) / sd);
+    const float ratio = expf(logp - b.blogp[f]);
+    float loss_i;
+    for (int k = 0; k < A; ++k) d[k] = 0.f;
+    if (loss_kind == 0) {
+      const float clipped = fminf(fmaxf(ratio, 1.f - hp.clip_eps), 1.f + hp.clip_eps);
+      const float t1 = ratio * ad, t2 = clipped * ad;
+      loss_i = -fminf(t1, t2) + hp.vf_coef * verr * verr - hp.ent_coef * ent;
+      if (t2 < t1) l_clip += 1.0;
+      if (t1 <= t2) {
+        for (int k = 0; k < A; ++k) {
+          const float p = expf(z[k] - lse);
+          d[k] += -ad * ratio * ((k == a ? 1.f : 0.f) - p) * inv_n;
+        }
+      }
+      for (int k = 0; k < A; ++k) {
+        const float lp = z[k] - lse;
+        const float p = expf(lp);
+        d[k] += hp.ent_coef * p * ((p > 0.f ? lp : 0.f) + ent) * inv_n;
+      }
+    } else {
+      loss_i = -ad * logp + hp.vf_coef * verr * verr - hp.ent_coef * ent;
+      for (int k = 0; k < A; ++k) {
+        const float lp = z[k] - lse;
+        const float p = expf(lp);
+        d[k] = (-ad * ((k == a ? 1.f : 0.f) - p) + hp.ent_coef * p * ((p > 0.f ? lp : 0.f) + ent)) * inv_n;
+      }
+    }
+    d[A] = 2.f * hp.vf_coef * verr * inv_n;
+    l_loss += double(loss_i);
+    l_ratio += double(ratio);
+    l_ent += double(ent);
+    l_vl += double(verr) * double(verr);
+  }
+  {
+    double v[5] = {l_loss, l_ratio, l_ent, l_vl, l_clip};
+    const int w = tid >> 5, lane = tid & 31;
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      v[q] = warp_sum(v[q]);
+      if (lane == 0) red[q][w] = v[q];
+    }
+  }
+  __syncthreads();
+  if (tid < 5) {
+    double acc = 0.0;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) acc += red[tid][w];
+    loss_partial[long(blockIdx.x) * 5 + tid] = acc;
+  }
+
+  // ---- phase 2
+  const int nf = int(F - f0 < long(kLossFrames) ? F - f0 : long(kLossFrames));
+  for (int j = tid; j < hd.H; j += blockDim.x) {
+    float w[kMaxA1];
+#pragma unroll
+    for (int k = 0; k < kMaxA1 - 1; ++k)
+      w[k] = (k < A) ? __ldg(params + hd.wpi + long(k) * hd.wk + long(j) * hd.wj) : 0.f;
+    const float wv = __ldg(params + hd.wv + j);
+    float acc[kMaxA1];
+#pragma unroll
+    for (int k = 0; k < kMaxA1; ++k) acc[k] = 0.f;
+    for (int i = 0; i < nf; ++i) {
+      const long f = f0 + i;
+      const float x = h[f * ldh + j];
+      const float* d = sdz + i * A1;
+      float dh = d[A] * wv;
+#pragma unroll
+      for (int k = 0; k < kMaxA1 - 1; ++k)
+        if (k < A) {
+          dh = fmaf(d[k], w[k], dh);
+          acc[k] = fmaf(d[k], x, acc[k]);
+        }
+      acc[kMaxA1 - 1] = fmaf(d[A], x, acc[kMaxA1 - 1]);
+      if (dz) {
+        const float o = dh * (1.f - x * x);
+        dz[f * hd.H + j] = o;
+        dz_lo[f * hd.H + j] = o - tf32_hi(o);
+      }
+    }
+    float* out = hg_partial + long(blockIdx.x) * A1 * hd.H;
+#pragma unroll
+    for (int k = 0; k < kMaxA1 - 1; ++k)
+      if (k < A) out[long(k) * hd.H + j] = acc[k];
+    out[long(A) * hd.H + j] = acc[kMaxA1 - 1];
+  }
+  // bias partials: sum over the block's frames of dz_k, stored after the weight partials
+  __syncthreads();
+  if (tid < A1) {
+    float acc = 0.f;
+    for (int i = 0; i < nf; ++i) acc += sdz[i * A1 + tid];
+    hg_partial[long(gridDim.x) * A1 * hd.H + long(blockIdx.x) * A1 + tid] = acc;
+  }
+}
+
+// Fixed-order sum of the head-gradient partials into the flat gradient, plus the
+// loss/stat partials into the step statistics (rlmath.cpp:237-263).
+__global__ void head_grad_reduce_kernel(HeadDesc hd, const float* __restrict__ hg_partial,
+                                        const double* __restrict__ loss_partial, int nblocks,
+                                        float* __restrict__ grad, StepStatsDev* st) {
+  const int A = hd.A, A1 = A + 1;
+  const long nw = long(A1) * hd.H;
+  const long idx = blockIdx.x * long(blockDim.x) + threadIdx.x;
+  if (idx < nw) {
+    float acc = 0.f;
+    for (int bk = 0; bk < nblocks; ++bk) acc += hg_partial[long(bk) * nw + idx];
+    const int k = int(idx / hd.H), j = int(idx % hd.H);
+    if (k < A)
+      grad[hd.wpi + long(k) * hd.wk + long(j) * hd.wj] = acc;
+    else
+      grad[hd.wv + j] = acc;
+  } else if (idx < nw + A1) {
+    const int k = int(idx - nw);
+    float acc = 0.f;
+    const float* bp = hg_partial + long(nblocks) * nw;
+    for (int bk = 0; bk < nblocks; ++bk) acc += bp[long(bk) * A1 + k];
+    if (k < A && hd.bpi >= 0) grad[hd.bpi + k] = acc;
+    if (k == A && hd.bv >= 0) grad[hd.bv] = acc;
+  } else if (idx == nw + A1) {
+    double v[5] = {0, 0, 0, 0, 0};
+    for (int bk = 0; bk < nblocks; ++bk)
+      for (int q = 0; q < 5; ++q) v[q] += loss_partial[long(bk) * 5 + q];
+    const double inv_n = st->inv_n;
+    st->loss = v[0] * inv_n;
+    st->ratio = v[1] * inv_n;
+    st->entropy = v[2] * inv_n;
+    st->vloss = v[3] * inv_n;
+    st->clip = v[4] * inv_n;
+  }
+}
+
+__global__ void dw_reduce_kernel(const float4* __restrict__ ws, int splits, long n4, long stride4,
+                                 float4* __restrict__ out) {
+  for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n4; i += long(gridDim.x) * blockDim.x) {
+    float4 a = ws[i];
+    for (int s = 1; s < splits; ++s) {
+      const float4 b = ws[s * stride4 + i];
+      a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+    }
+    out[i] = a;
+  }
+}
+
+__global__ void dw_reduce_scalar_kernel(const float* __restrict__ ws, int splits, long n,
+                                        float* __restrict__ out) {
+  for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
+    float a = ws[i];
+    for (int s = 1; s < splits; ++s) a += ws[s * n + i];
+    out[i] = a;
+  }
+}
+
+constexpr int kColRows = 256;  // rows per colsum chunk
+
+__global__ void colsum_partial_kernel(const float* __restrict__ x, long ld, long rows, int cols,
+                                      float* __restrict__ partial) {
+  const long r0 = long(blockIdx.y) * kColRows;
+  const long r1 = min(rows, r0 + kColRows);
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < cols; j += gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (long r = r0; r < r1; ++r) acc += x[r * ld + j];
+    partial[long(blockIdx.y) * cols + j] = acc;
+  }
+}
+
+__global__ void colsum_reduce_kernel(const float* __restrict__ partial, int chunks, int cols,
+                                     float* __restrict__ out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= cols) return;
+  float acc = 0.f;
+  for (int c = 0; c < chunks; ++c) acc += partial[long(c) * cols + j];
+  out[j] = acc;
+}
+
+// K7: fused optimizer over the flat fp32 parameter vector.  Reads p, g, (m, v) and
+// writes p, (m, v) and the tf32 residual plane the next step's GEMMs consume.
+//   SGD  (rlmath.cpp:229-230):     p -= lr * g
+//   Adam (torch.optim.Adam):       m = b1 m + (1-b1) g ; v = b2 v + (1-b2) g^2
+//                                  p -= step_size * m / (sqrt(v) / bc2_sqrt + eps)
+// g is the allreduced sum times grad_scale (= 1/G, learner.cpp:146-147).
+__global__ void optimizer_kernel(float4* __restrict__ p, float4* __restrict__ plo,
+                                 const float4* __restrict__ g, float4* __restrict__ m,
+                                 float4* __restrict__ v, long n4, float grad_scale, int adam,
+                                 float lr, float step_size, float bc2_sqrt, float b1, float b2,
+                                 float eps) {
+  for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n4; i += long(gridDim.x) * blockDim.x) {
+    float4 pp = p[i];
+    float4 gg = g[i];
+    float* pe = &pp.x;
+    float* ge = &gg.x;
+    if (adam) {
+      float4 mm = m[i], vv = v[i];
+      float* me = &mm.x;
+      float* ve = &vv.x;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float gq = ge[q] * grad_scale;
+        me[q] = b1 * me[q] + (1.f - b1) * gq;
+        ve[q] = b2 * ve[q] + (1.f - b2) * gq * gq;
+        const float denom = sqrtf(ve[q]) / bc2_sqrt + eps;
+        pe[q] -= step_size * me[q] / denom;
+      }
+      m[i] = mm;
+      v[i] = vv;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) pe[q] -= lr * (ge[q] * grad_scale);
+    }
+    p[i] = pp;
+    plo[i] = make_float4(pp.x - tf32_hi(pp.x), pp.y - tf32_hi(pp.y), pp.z - tf32_hi(pp.z),
+                         pp.w - tf32_hi(pp.w));
+  }
+}
+
+int grid_for(long n, int threads, int per_sm = 8) {
+  long b = (n + threads - 1) / threads;
+  return int(std::max<long>(1, std::min<long>(b, 148L * per_sm)));
+}
+
+}  // namespace
+
+void launch_expand_u8(const uint8_t* in, float* out, long n, cudaStream_t s) {
+  expand_u8_kernel<<<grid_for(n / 4, 256), 256, 0, s>>>(reinterpret_cast<const uchar4*>(in),
+                                                        reinterpret_cast<float4*>(out), n / 4);
+  TLG_CHECK_LAUNCH();
+}
+
+void launch_split_lo(const float* x, float* lo, long n, cudaStream_t s) {
+  split_lo_kernel<<<grid_for(n / 4, 256), 256, 0, s>>>(reinterpret_cast<const float4*>(x),
+                                                       reinterpret_cast<float4*>(lo), n / 4);
+  TLG_CHECK_LAUNCH();
+}
+
+void launch_head_forward(const HeadDesc& hd, const float* params, const float* h, long ldh,
+                         const BatchDev* b, long F, float* head_out, float* tlogp,
+                         float* probs_out, int* err, cudaStream_t s) {
+  if (hd.A + 1 > kMaxA1Limit) throw CudaError("n_actions exceeds the head kernel limit (31)");
+  BatchDev bd{};
+  if (b) bd = *b;
+  const int blocks = int(std::max<long>(1, std::min<long>((F + 7) / 8, 148L * 16)));
+  if (hd.A + 1 <= 8)
+    head_forward_kernel<8><<<blocks, 256, 0, s>>>(hd, params, h, ldh, bd, b ? 1 : 0, F, head_out,
+                                                  tlogp, probs_out, err);
+  else
+    head_forward_kernel<32><<<blocks, 256, 0, s>>>(hd, params, h, ldh, bd, b ? 1 : 0, F,
+                                                   head_out, tlogp, probs_out, err);
+  TLG_CHECK_LAUNCH();
+}
+
+void launch_returns(const BatchDev& b, int algo, const HyperDev& hp, const float* tlogp,
+                    float* adv, float* target, double* seg_partial, int* err, cudaStream_t s) {
+  returns_kernel<<<ceil_div(b.S, 8), 256, 0, s>>>(b, algo, hp, tlogp, adv, target, seg_partial,
+                                                  err);
+  TLG_CHECK_LAUNCH();
+}
+
+void launch_finalize_adv(const double* seg_partial, const BatchDev& b, int adv_norm,
+                         StepStatsDev* st, int* err, cudaStream_t s) {
+  finalize_adv_kernel<<<1, 1024, 0, s>>>(seg_partial, b, adv_norm, st, err);
+  TLG_CHECK_LAUNCH();
+}
+
+int launch_loss_backward(const HeadDesc& hd, const float* params, const float* h, long ldh,
+                         const BatchDev& b, const float* head_out, const float* adv,
+                         const float* target, const StepStatsDev* st, const HyperDev& hp,
+                         int loss_kind, float* dz, float* dz_lo, float* hg_partial,
+                         double* loss_partial, cudaStream_t s) {
+  if (hd.A + 1 > kMaxA1Limit) throw CudaError("n_actions exceeds the head kernel limit (31)");
+  const long F = long(b.S) * b.T;
+  const int blocks = ceil_div(F, kLossFrames);
+  const size_t smem = size_t(kLossFrames) * (hd.A + 1) * sizeof(float);
+  if (hd.A + 1 <= 8)
+    loss_backward_kernel<8><<<blocks, 256, smem, s>>>(hd, params, h, ldh, b, head_out, adv, target,
+                                                      st, hp, loss_kind, dz, dz_lo, hg_partial,
+                                                      loss_partial);
+  else
+    loss_backward_kernel<32><<<blocks, 256, smem, s>>>(hd, params, h, ldh, b, head_out, adv,
+                                                       target, st, hp, loss_kind, dz, dz_lo,
+                                                       hg_partial, loss_partial);
+  TLG_CHECK_LAUNCH();
+  return blocks;
+}
+
+void launch_head_grad_reduce(const HeadDesc& hd, const float* hg_partial,
+                             const double* loss_partial, int nblocks, float* grad,
+                             StepStatsDev* st, cudaStream_t s) {
+  const long n = long(hd.A + 1) * hd.H + hd.A + 1 + 1;
+  head_grad_reduce_kernel<<<ceil_div(n, 256), 256, 0, s>>>(hd, hg_partial, loss_partial, nblocks,
+                                                           grad, st);
+  TLG_CHECK_LAUNCH();
+}
+
+void launch_dw_reduce(const float* ws, int splits, long n, float* grad, cudaStream_t s) {
+  if ((n & 3) == 0 && (reinterpret_cast<uintptr_t>(grad) & 15) == 0) {
+    dw_reduce_kernel<<<grid_for(n / 4, 256), 256, 0, s>>>(reinterpret_cast<const float4*>(ws),
+                                                          splits, n / 4, n / 4,
+                                                          reinterpret_cast<float4*>(grad));
+  } else {
+    dw_reduce_scalar_kernel<<<grid_for(n, 256), 256, 0, s>>>(ws, splits, n, grad);
+  }
+  TLG_CHECK_LAUNCH();
+}
+
+void launch_colsum(const float* x, long ld, long rows, int cols, float* partial, float* grad,
+                   cudaStream_t s) {
+  const int chunks = ceil_div(rows, kColRows);
+  dim3 grid(ceil_div(cols, 256), chunks);
+  colsum_partial_kernel<<<grid, 256, 0, s>>>(x, ld, rows, cols, partial);
+  TLG_CHECK_LAUNCH();
+  colsum_reduce_kernel<<<ceil_div(cols, 256), 256, 0, s>>>(partial, chunks, cols, grad);
+  TLG_CHECK_LAUNCH();
+}
+
+void launch_optimizer(float* params, float* params_lo, const float* grad, float* m, float* v,
+                      long n, float grad_scale, int adam, float lr, float step_size,
+                      float bc2_sqrt, float b1, float b2, float eps, cudaStream_t s) {
+  // n is padded to a multiple of 4 by the allocator
+  optimizer_kernel<<<grid_for(n / 4, 256, 4), 256, 0, s>>>(
+      reinterpret_cast<float4*>(params), reinterpret_cast<float4*>(params_lo),
+      reinterpret_cast<const float4*>(grad), reinterpret_cast<float4*>(m),
+      reinterpret_cast<float4*>(v), n / 4, grad_scale, adam, lr, step_size, bc2_sqrt, b1, b2,
+      eps);
+  TLG_CHECK_LAUNCH();
+}
+
+}  // namespace tlg

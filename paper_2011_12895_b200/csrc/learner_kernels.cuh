@@ -1,0 +1,95 @@
+// Non-GEMM kernels of the B200 learner step and InfServer forward.
+//
+//   K1  returns_kernel      GAE + lambda-return | V-trace (rho/c clip fused), one warp per
+//                           segment, reverse affine warp scans over T      rlmath.cpp:45-114
+//   K3a head_forward        policy/value heads, log-softmax, target logp  policy.cpp:73-105
+//   K3b loss_backward       PPO / PG loss + dlogits/dvalue + head grads + tanh' of the
+//                           last trunk layer                               rlmath.cpp:116-222
+//   K7  optimizer_kernel    fused Adam (torch semantics) | SGD             rlmath.cpp:224-232
+// plus deterministic (fixed-order) reductions for advantage normalisation
+// (rlmath.cpp:18-34), split-K dW partials and bias column sums.
+#pragma once
+
+#include "common.cuh"
+
+namespace tlg {
+
+// Error bits raised on device, mapped to the reference's exceptions on the host.
+enum ErrBits : int {
+  kErrNonFiniteLogp = 1,    // rlmath.cpp:90-91   invalid_argument
+  kErrActionRange = 2,      // rlmath.cpp:133     invalid_argument
+  kErrNotOneHot = 4,        // policy.cpp:57-71   invalid_argument
+  kErrNonFiniteAdv = 8,     // rlmath.cpp:22      invalid_argument
+  kErrEmptyBatch = 16,      // rlmath.cpp:118     invalid_argument
+  kErrValidSteps = 32,      // valid_steps > unroll_len
+};
+
+enum Algo : int { kAlgoPpo = 0, kAlgoVtrace = 1, kAlgoPpoVtrace = 2 };
+
+// Policy/value head over the head input h (the last trunk activation, or the raw
+// observation for the tabular/linear families).
+struct HeadDesc {
+  int family;   // 0 tabular, 1 linear, 2 mlp
+  int A;        // n_actions
+  int H;        // head input width
+  long wpi;     // W_pi(k, j) = params[wpi + k*wk + j*wj]
+  int wk, wj;
+  long bpi;     // -1: no bias
+  long wv;      // w_v(j) = params[wv + j]
+  long bv;      // -1: no bias
+};
+
+struct BatchDev {
+  int S, T;
+  const int32_t* action;
+  const float* reward;
+  const float* blogp;
+  const float* value;
+  const uint8_t* done;
+  const float* boot;
+  const int32_t* valid;
+};
+
+struct HyperDev {
+  float gamma, lam, clip_eps, vf_coef, ent_coef, rho_bar, c_bar;
+  int adv_norm;
+};
+
+// Device-side per-step statistics (written by finalize kernels, read once by host).
+struct StepStatsDev {
+  double sum_adv, sum_adv2;
+  double mean, sd;
+  double inv_n;
+  long long n;
+  double loss, ratio, entropy, vloss, clip;
+};
+
+constexpr int kLossFrames = 128;  // frames per loss_backward block
+
+void launch_expand_u8(const uint8_t* in, float* out, long n, cudaStream_t s);
+void launch_split_lo(const float* x, float* lo, long n, cudaStream_t s);
+void launch_head_forward(const HeadDesc& hd, const float* params, const float* h, long ldh,
+                         const BatchDev* b, long F, float* head_out, float* tlogp,
+                         float* probs_out, int* err, cudaStream_t s);
+void launch_returns(const BatchDev& b, int algo, const HyperDev& hp, const float* tlogp,
+                    float* adv, float* target, double* seg_partial, int* err, cudaStream_t s);
+void launch_finalize_adv(const double* seg_partial, const BatchDev& b, int adv_norm,
+                         StepStatsDev* st, int* err, cudaStream_t s);
+// dz/dz_lo may be null (no trunk).  Returns the number of blocks (partials rows).
+int launch_loss_backward(const HeadDesc& hd, const float* params, const float* h, long ldh,
+                         const BatchDev& b, const float* head_out, const float* adv,
+                         const float* target, const StepStatsDev* st, const HyperDev& hp,
+                         int loss_kind, float* dz, float* dz_lo, float* hg_partial,
+                         double* loss_partial, cudaStream_t s);
+void launch_head_grad_reduce(const HeadDesc& hd, const float* hg_partial,
+                             const double* loss_partial, int nblocks, float* grad,
+                             StepStatsDev* st, cudaStream_t s);
+void launch_dw_reduce(const float* ws, int splits, long n, float* grad, cudaStream_t s);
+// grad[j] = sum over rows of x[row][j] (fixed order); partial: scratch [chunks x cols]
+void launch_colsum(const float* x, long ld, long rows, int cols, float* partial, float* grad,
+                   cudaStream_t s);
+void launch_optimizer(float* params, float* params_lo, const float* grad, float* m, float* v,
+                      long n, float grad_scale, int adam, float lr, float step_size,
+                      float bc2_sqrt, float b1, float b2, float eps, cudaStream_t s);
+
+}  // namespace tlg

@@ -1,0 +1,182 @@
+// Device self-test of the tcgen05 3xTF32 GEMM against an fp64 SIMT reference on the
+// same GPU (test tool; not part of the product library).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O2 gemm_selftest.cu ../gemm_sm100.cu
+#include <cmath>
+#include <cstdio>
+#include <random>
+#include <vector>
+
+#include "../gemm_sm100.cuh"
+
+using namespace tlg;
+
+// ref[m][n] = sum_k A(m,k) B(n,k), fp64; A(m,k) = a_mn ? A[k*lda+m] : A[m*lda+k]
+__global__ void ref_gemm(const float* A, long lda, bool a_mn, const float* B, long ldb, bool b_mn,
+                         int M, int N, int K, double* out, double* absout) {
+  int m = blockIdx.x * blockDim.x + threadIdx.x;
+  int n = blockIdx.y;
+  if (m >= M) return;
+  double s = 0, sa = 0;
+  for (int k = 0; k < K; ++k) {
+    double a = a_mn ? A[long(k) * lda + m] : A[long(m) * lda + k];
+    double b = b_mn ? B[long(k) * ldb + n] : B[long(n) * ldb + k];
+    s += a * b;
+    sa += fabs(a * b);
+  }
+  out[long(m) * N + n] = s;
+  absout[long(m) * N + n] = sa;
+}
+
+__global__ void split_kernel(const float* x, float* hi, float* lo, long n) {
+  long i = blockIdx.x * long(blockDim.x) + threadIdx.x;
+  if (i < n) {
+    float h = tf32_hi(x[i]);
+    hi[i] = h;
+    lo[i] = x[i] - h;
+  }
+}
+
+struct Buf {
+  float *x = nullptr, *hi = nullptr, *lo = nullptr;
+  long n = 0;
+  void init(long n_, std::mt19937& rng, bool binary = false) {
+    n = n_;
+    std::vector<float> h(n);
+    std::normal_distribution<float> nd(0.f, 1.f);
+    std::uniform_real_distribution<float> u(0.f, 1.f);
+    for (auto& v : h) v = binary ? (u(rng) < 0.1f ? 1.f : 0.f) : nd(rng);
+    TLG_CUDA(cudaMalloc(&x, n * 4));
+    TLG_CUDA(cudaMalloc(&hi, n * 4));
+    TLG_CUDA(cudaMalloc(&lo, n * 4));
+    TLG_CUDA(cudaMemcpy(x, h.data(), n * 4, cudaMemcpyHostToDevice));
+    split_kernel<<<(n + 255) / 256, 256>>>(x, hi, lo, n);
+  }
+};
+
+static int failures = 0;
+
+static bool g_fullhi = false;  // feed the full fp32 plane as "hi" (tests HW tf32 truncation)
+
+void check(const char* name, int M, int N, int K, bool a_mn, bool b_mn, bool a_exact, int epi,
+           int splits) {
+  std::mt19937 rng(M * 131 + N * 7 + K);
+  Buf A, B, act, bias;
+  // A stored [M][K] (K-major) or [K][M] (MN-major); same element count
+  A.init(long(M) * K, rng, a_exact);
+  B.init(long(N) * K, rng);
+  act.init(long(M) * N, rng);
+  bias.init(N, rng);
+  // tanh'd activations in (-1,1)
+  const long lda = a_mn ? M : K, ldb = b_mn ? N : K;
+  double *ref, *refabs;
+  TLG_CUDA(cudaMalloc(&ref, long(M) * N * 8));
+  TLG_CUDA(cudaMalloc(&refabs, long(M) * N * 8));
+  ref_gemm<<<dim3((M + 127) / 128, N), 128>>>(A.x, lda, a_mn, B.x, ldb, b_mn, M, N, K, ref,
+                                              refabs);
+  float *out_hi, *out_lo, *ws;
+  TLG_CUDA(cudaMalloc(&out_hi, long(M) * N * 4));
+  TLG_CUDA(cudaMalloc(&out_lo, long(M) * N * 4));
+  TLG_CUDA(cudaMalloc(&ws, long(splits) * M * N * 4));
+  TLG_CUDA(cudaMemset(ws, 0, long(splits) * M * N * 4));
+  gemm::Operand oa{g_fullhi ? A.x : A.hi, a_exact ? nullptr : A.lo, lda, a_mn};
+  gemm::Operand ob{g_fullhi ? B.x : B.hi, B.lo, ldb, b_mn};
+  gemm::Params p{};
+  p.out_hi = out_hi;
+  p.out_lo = out_lo;
+  p.ldo = N;
+  p.bias = bias.x;
+  // act planes: use act.x as h values (clip into (-1,1) by tanh on host side not needed)
+  p.act_hi = act.x;
+  p.ld_act = N;
+  p.ws = ws;
+  p.ws_split_stride = long(M) * N;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  gemm::launch(oa, ob, M, N, K, epi, p, splits, 0);
+  TLG_CUDA(cudaDeviceSynchronize());
+  cudaEventRecord(e0);
+  const int reps = 5;
+  for (int i = 0; i < reps; ++i) gemm::launch(oa, ob, M, N, K, epi, p, splits, 0);
+  cudaEventRecord(e1);
+  TLG_CUDA(cudaDeviceSynchronize());
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  ms /= reps;
+
+  std::vector<double> hr(long(M) * N), ha(long(M) * N);
+  std::vector<float> hh(long(M) * N), hl(long(M) * N), hact(long(M) * N), hb(N);
+  std::vector<float> hws(long(splits) * M * N);
+  TLG_CUDA(cudaMemcpy(hr.data(), ref, hr.size() * 8, cudaMemcpyDeviceToHost));
+  TLG_CUDA(cudaMemcpy(ha.data(), refabs, ha.size() * 8, cudaMemcpyDeviceToHost));
+  TLG_CUDA(cudaMemcpy(hh.data(), out_hi, hh.size() * 4, cudaMemcpyDeviceToHost));
+  TLG_CUDA(cudaMemcpy(hl.data(), out_lo, hl.size() * 4, cudaMemcpyDeviceToHost));
+  TLG_CUDA(cudaMemcpy(hact.data(), act.x, hact.size() * 4, cudaMemcpyDeviceToHost));
+  TLG_CUDA(cudaMemcpy(hb.data(), bias.x, hb.size() * 4, cudaMemcpyDeviceToHost));
+  TLG_CUDA(cudaMemcpy(hws.data(), ws, hws.size() * 4, cudaMemcpyDeviceToHost));
+  double worst = 0;
+  long bad = 0;
+  for (long i = 0; i < long(M) * N; ++i) {
+    const int n = int(i % N);
+    double want, got, scale;
+    if (epi == gemm::kEpiStore) {
+      got = 0;
+      for (int s = 0; s < splits; ++s) got += hws[long(s) * M * N + i];
+      want = hr[i];
+      scale = ha[i] + 1e-30;
+    } else if (epi == gemm::kEpiFwdTanh) {
+      got = double(hh[i]);
+      if (std::fabs(double(hh[i]) - double(hh[i] - hl[i])) > 1e-3 * std::fabs(hh[i]) + 1e-30) got = 1e9;
+      want = std::tanh(hr[i] + hb[n]);
+      scale = ha[i] + 1.0;
+    } else {
+      const double h = hact[i];
+      got = double(hh[i]);
+      want = hr[i] * (1 - h * h);
+      scale = (ha[i] + 1e-30) * std::max(1.0, std::fabs(1 - h * h));
+    }
+    const double err = std::fabs(got - want) / scale;
+    if (!(err <= (K > 20000 ? 1e-5 : 2e-6))) ++bad;
+    if (!(err <= worst)) worst = std::isfinite(err) ? std::max(worst, err) : 1e30;
+  }
+  const double tflops = 2.0 * M * N * K / (ms * 1e-3) / 1e12;
+  printf("%-34s M=%6d N=%5d K=%6d split=%d : worst rel %.3e bad %ld  %.3f ms %.1f TF/s  %s\n",
+         name, M, N, K, splits, worst, bad, ms, tflops, bad ? "FAIL" : "ok");
+  if (bad) ++failures;
+  cudaFree(ref); cudaFree(refabs); cudaFree(out_hi); cudaFree(out_lo); cudaFree(ws);
+  cudaFree(A.x); cudaFree(A.hi); cudaFree(A.lo); cudaFree(B.x); cudaFree(B.hi); cudaFree(B.lo);
+  cudaFree(act.x); cudaFree(act.hi); cudaFree(act.lo); cudaFree(bias.x); cudaFree(bias.hi);
+  cudaFree(bias.lo);
+}
+
+int main(int argc, char** argv) {
+  try {
+    using namespace gemm;
+    check("fwd tanh K/K", 300, 256, 200, false, false, false, kEpiFwdTanh, 1);
+    check("fwd tanh K/K exactA", 300, 256, 200, false, false, true, kEpiFwdTanh, 1);
+    check("fwd tanh K/K N=100", 257, 100, 96, false, false, false, kEpiFwdTanh, 1);
+    check("fwd tanh K/K N=64", 128, 64, 64, false, false, false, kEpiFwdTanh, 1);
+    check("dX bwd K/MN", 300, 256, 256, false, true, false, kEpiBwdTanh, 1);
+    check("dX bwd K/MN N=64", 200, 64, 256, false, true, false, kEpiBwdTanh, 1);
+    check("dW store MN/MN", 256, 200, 1000, true, true, false, kEpiStore, 1);
+    check("dW store MN/MN split4", 256, 200, 1000, true, true, false, kEpiStore, 4);
+    check("dW store MN/MN exactB", 256, 1936, 2048, true, true, false, kEpiStore, 2);
+    check("store K/K", 256, 256, 512, false, false, false, kEpiStore, 1);
+    g_fullhi = true;
+    check("FULLHI fwd tanh K/K", 300, 256, 200, false, false, false, kEpiFwdTanh, 1);
+    check("FULLHI dX bwd K/MN", 300, 256, 256, false, true, false, kEpiBwdTanh, 1);
+    check("FULLHI dW store MN/MN", 256, 200, 1000, true, true, false, kEpiStore, 1);
+    g_fullhi = false;
+    if (argc > 1) {
+      // throughput shapes (C3 layer 1 forward, C5 layer forward)
+      check("perf fwd C3 L1", 131072, 256, 1936, false, false, true, kEpiFwdTanh, 1);
+      check("perf fwd C5", 131072, 2048, 2048, false, false, false, kEpiFwdTanh, 1);
+      check("perf dW C3 L1", 256, 1936, 131072, true, true, false, kEpiStore, 8);
+    }
+  } catch (const std::exception& e) {
+    printf("EXCEPTION: %s\n", e.what());
+    return 2;
+  }
+  printf("%s\n", failures ? "GEMM SELFTEST FAILED" : "GEMM SELFTEST PASSED");
+  return failures ? 1 : 0;
+}
