@@ -1,0 +1,424 @@
+#!/usr/bin/env python
+"""Benchmark: learner frames/sec (+ InferenceServer actions/sec) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
+
+Workload (BASELINE.json): config C3 -- Pommerman-shaped obs (11x11x16 = 1936 binary
+planes), MLP 1936-256-256-(6,1), PPO + GAE, T=32, B=4096 segments per learner shard
+(HyperParams::batch_size is per shard, learner.cpp:108), Adam.  One step = one
+Learner::TrainStep on every rank: returns, loss fwd/bwd, NCCL gradient allreduce,
+optimizer.  N>1 is launched by torchrun, one rank per GPU (weak scaling: per-GPU
+work fixed).
+
+* value   : frames/s with the batch already resident in HBM (whole job, all ranks),
+            timed with CUDA events on the learner's stream, max over ranks.
+* e2e     : the same through the C ABI with HOST buffers (pinned): the per-step H2D
+            of the shard's segments and the D2H of the step statistics are inside
+            the timed region.
+* roofline: the dominant kernel (layer-1 forward GEMM, tcgen05 kind::tf32) --
+            algorithmic FLOPs / its own CUDA-event time, against MEASURED_PEAKS.json.
+* cpu_baseline / --impl reference: the reference's own Learner::TrainStep
+            (oracle/_ref, compiled from the reference sources) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return d, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, \
+            "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi style clock / throttle sampling during the timed region (NVML)."""
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, device_index):
+        self.samples, self.reasons, self.stop_flag = [], set(), threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self.stop_flag.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop_flag.set()
+        if self.nv:
+            self.t.join()
+
+    def result(self):
+        med = float(np.median(self.samples)) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+def reference_cpu(cfg, seconds=12.0, steps=None, warmup=0, segs_per_shard=None):
+    """The reference's own Learner::TrainStep (linear_softmax: the only policy family the
+    reference has, types.hpp:14) at the config's obs/A/T, num_shards = host cores, on a
+    bounded sample (segs_per_shard segments per shard per step)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_ffi import Hyper, RefLearner, RefLib, Segments
+    from paper_2011_12895_b200.synth import make_segments
+    ref = RefLib()
+    cores = os.cpu_count() or 1
+    T, D, A = cfg.unroll_len, cfg.obs_dim, cfg.n_actions
+    if segs_per_shard is None:
+        # keep one step's fp64 AoS segments around ~64 MB
+        segs_per_shard = max(1, min(cfg.batch_size, int(64e6 / (T * D * 8 * cores))))
+    hp = Hyper(learning_rate=3e-4, batch_size=segs_per_shard, unroll_len=T, max_reuse=1)
+    algo = 0 if cfg.algo == "ppo" else 1
+    lrn = RefLearner(ref, ShapeLin(D, A), hp, init_scale=0.05, num_shards=cores, algo=algo,
+                     publish_interval=1 << 30, replay_capacity=1 << 20, seed=7)
+    draw = segs_per_shard * cores
+    times, frames = [], []
+    k = 0
+    t_start = time.perf_counter()
+    while True:
+        b = make_segments(draw, T, D, A, seed=5000 + k, obs_kind=cfg.obs_kind)
+        seg = Segments(b.obs.astype(np.float64), b.action.astype(np.uint32),
+                       b.reward.astype(np.float64), b.behavior_logp.astype(np.float64),
+                       b.value_est.astype(np.float64), b.done, b.bootstrap.astype(np.float64),
+                       b.valid_steps.astype(np.uint32))
+        lrn.push(seg)
+        c0 = lrn.consumed()
+        t0 = time.perf_counter()
+        assert lrn.train_step()
+        dt = time.perf_counter() - t0
+        if k >= warmup:
+            times.append(dt)
+            frames.append(lrn.consumed() - c0)
+        k += 1
+        if steps is not None:
+            if k >= warmup + steps:
+                break
+        elif time.perf_counter() - t_start > seconds and len(times) >= 2:
+            break
+    fps = float(np.sum(frames) / np.sum(times))
+    sample = (f"reference Learner::TrainStep, linear_softmax obs {D} A {A} T {T}, "
+              f"{cores} shards x {segs_per_shard} segments per step, {len(times)} steps")
+    return fps, cores, sample, float(np.mean(times))
+
+
+def ShapeLin(D, A):
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_ffi import Shape
+    return Shape(1, D, A)
+
+
+def run_reference_arm(args, cfg):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    try:
+        fps, cores, sample, ms = reference_cpu(cfg, steps=args.steps, warmup=args.warmup)
+    except Exception as e:  # pragma: no cover - reported, not raised
+        print(json.dumps({"impl": "reference", "unavailable": f"{type(e).__name__}: {e}"}))
+        return 0
+    line = {
+        "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": cfg.name, "note": cfg.note, "policy": "linear_softmax (reference)"},
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+METRIC = "learner frames/sec at 1/2/4/8 B200 + InferenceServer actions/sec vs CPU ref"
+
+
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--obs", default="u8", choices=["u8", "f32"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-infer", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    from paper_2011_12895_b200.configs import CONFIGS
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference_arm(args, cfg)
+
+    import torch
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+    import paper_2011_12895_b200 as tlg
+
+    obs_u8 = args.obs == "u8" and cfg.obs_kind == "binary"
+    S, T, D, A, hidden = cfg.batch_size, cfg.unroll_len, cfg.obs_dim, cfg.n_actions, cfg.hidden
+    lrn = tlg.Learner("mlp", D, A, hidden, algo=cfg.algo, optimizer=cfg.optimizer,
+                      max_segments=S, unroll_len=T, device=local, obs_u8=obs_u8, timing=True)
+    lrn.set_hyper(learning_rate=3e-4, batch_size=S, unroll_len=T)
+    params = tlg.synth.init_params_f32(lrn.n_params, 0.05, seed=cfg.seed).astype(np.float64)
+    lrn.set_params(params)
+    if world > 1:
+        uid = [tlg.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        lrn.comm_init(uid[0], world, rank)
+
+    # two distinct resident batches per rank (each > L2: the obs alone is >= 254 MB)
+    host = [tlg.synth.make_segments(S, T, D, A, seed=cfg.seed * 100 + rank * 10 + i,
+                                    obs_kind=cfg.obs_kind, obs_u8=obs_u8) for i in range(2)]
+    dev = [tlg.DeviceSegmentBatch(h, local) for h in host]
+    frames_per_step = [int(h.valid_steps.sum()) for h in host]
+
+    stream = torch.cuda.ExternalStream(lrn.stream(), device=local)
+
+    def barrier():
+        if dist:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if not dist:
+            return x
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x):
+        if not dist:
+            return x
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    # ---- device-resident timed region
+    for i in range(args.warmup):
+        lrn.train_step(dev[i % 2], on_device=True)
+    barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    kern = {"fwd1": [], "dw1": [], "fwd2": [], "dw2": [], "dx2": [], "phases": []}
+    launches = 0
+    frames = 0
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for i in range(args.steps):
+            lrn.train_step(dev[i % 2], on_device=True)
+            frames += frames_per_step[i % 2]
+            launches += lrn.last_launches()
+            kern["fwd1"].append(lrn.kernel_ms("fwd", 0))
+            kern["dw1"].append(lrn.kernel_ms("dw", 0))
+            if len(hidden) > 1:
+                kern["fwd2"].append(lrn.kernel_ms("fwd", 1))
+                kern["dw2"].append(lrn.kernel_ms("dw", 1))
+                kern["dx2"].append(lrn.kernel_ms("dx", 1))
+            kern["phases"].append(lrn.phase_ms())
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms_local = ev0.elapsed_time(ev1)
+    ms_total = max_over_ranks(ms_local)
+    frames_all = sum_over_ranks(frames)
+    value = frames_all / (ms_total / 1e3)
+    ms_per_step = ms_total / args.steps
+
+    # ---- end to end through the C ABI with pinned host buffers
+    pinned = []
+    for h in host:
+        pv = tlg.SegmentBatchView(h)
+        for k, a in pv.arrs.items():
+            t = torch.empty(a.shape, dtype=getattr(torch, str(a.dtype)), pin_memory=True)
+            t.numpy()[...] = a
+            pv.arrs[k] = t.numpy()
+        pv.c = tlg._capi.SegmentBatchC(
+            h.n_segments, h.unroll_len, h.obs_dim, 1 if obs_u8 else 0,
+            *(pv.arrs[k].ctypes.data for k in ("obs", "action", "reward", "behavior_logp",
+                                                 "value_est", "done", "bootstrap",
+                                                 "valid_steps")))
+        pinned.append(pv)
+    h2d = sum(a.nbytes for a in pinned[0].arrs.values())
+    for i in range(2):
+        lrn.train_step(pinned[i % 2])
+    barrier()
+    torch.cuda.synchronize()
+    e2e_steps = max(3, args.steps // 2)
+    t0 = time.perf_counter()
+    e2e_frames = 0
+    for i in range(e2e_steps):
+        lrn.train_step(pinned[i % 2])  # H2D + step + D2H of stats, synchronous
+        e2e_frames += frames_per_step[i % 2]
+    dt = max_over_ranks(time.perf_counter() - t0)
+    e2e_value = sum_over_ranks(e2e_frames) / dt
+
+    # ---- roofline of the dominant kernel (layer-1 forward GEMM)
+    peaks, peak_src = measured_peaks()
+    F = S * T
+    flops_fwd1 = 2.0 * F * hidden[0] * D
+    t_fwd1 = float(np.mean(kern["fwd1"])) / 1e3
+    t_dw1 = float(np.mean(kern["dw1"])) / 1e3
+    achieved = flops_fwd1 / t_fwd1 / 1e12
+    peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+    ph = np.mean(np.array(kern["phases"]), axis=0)
+    step_ms = float(ph[6])
+    roofline = {
+        "kernel": "gemm_tf32x3_kernel fwd layer1 (tcgen05.mma kind::tf32, A exact -> 2 passes)",
+        "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+        "frac": achieved / peak, "traffic": None,
+        "peak_source": f"{peak_src} bf16_tflops_sustained (MEASURED_PEAKS.json)",
+        "algorithmic_flops_per_launch": flops_fwd1,
+        "ms_per_launch": t_fwd1 * 1e3,
+        "share_of_step": t_fwd1 * 1e3 / step_ms,
+        "note": "fp32-exact 3xTF32 split; the tf32 dense ceiling is half the bf16 peak and "
+                "each K step issues 2 (exact obs) or 3 MMA passes",
+    }
+    kernels = {
+        "fwd1_ms": t_fwd1 * 1e3, "dw1_ms": t_dw1 * 1e3,
+        "dw1_tflops": 2.0 * F * hidden[0] * D / t_dw1 / 1e12,
+        "phases_ms": {"stage": float(ph[0]), "fwd": float(ph[1]), "heads_returns_loss": float(ph[2]),
+                      "bwd": float(ph[3]), "allreduce": float(ph[4]), "optimizer": float(ph[5]),
+                      "step": step_ms},
+    }
+    if kern["fwd2"]:
+        kernels.update(fwd2_ms=float(np.mean(kern["fwd2"])), dw2_ms=float(np.mean(kern["dw2"])),
+                       dx2_ms=float(np.mean(kern["dx2"])))
+    total_flops = cfg.flops_per_frame() * F
+    kernels["step_tflops"] = total_flops / (ms_per_step / 1e3) / 1e12
+
+    # ---- InferenceServer batched forward (C4), replicas on every rank
+    infer = None
+    if not args.no_infer:
+        c4 = CONFIGS["C4"]
+        pol = tlg.Policy("mlp", c4.obs_dim, c4.n_actions, c4.hidden, device=local,
+                         max_batch=c4.batch_size)
+        n_p = (c4.obs_dim * c4.hidden[0] + c4.hidden[0] + c4.hidden[0] * c4.hidden[1] +
+               c4.hidden[1] + (c4.n_actions + 1) * c4.hidden[1] + c4.n_actions + 1)
+        pol.set_params(tlg.synth.init_params_f32(n_p, 0.05, seed=c4.seed).astype(np.float64))
+        obs = tlg.synth.make_obs(c4.batch_size, c4.obs_dim, seed=c4.seed + rank)
+        ob_t = torch.from_numpy(obs).cuda(local)
+        lg_t = torch.empty(c4.batch_size, c4.n_actions, device=f"cuda:{local}")
+        pr_t = torch.empty_like(lg_t)
+        v_t = torch.empty(c4.batch_size, device=f"cuda:{local}")
+        pstream = torch.cuda.ExternalStream(pol.stream(), device=local)
+        for _ in range(3):
+            pol.forward_device(ob_t, lg_t, pr_t, v_t)
+        barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(pstream)
+        reps = max(5, args.steps)
+        for _ in range(reps):
+            pol.forward_device(ob_t, lg_t, pr_t, v_t)
+        e1.record(pstream)
+        torch.cuda.synchronize()
+        ims = max_over_ranks(e0.elapsed_time(e1) / reps)
+        obs_pin = torch.from_numpy(obs).pin_memory().numpy()
+        pol.forward(obs_pin)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(3):
+            pol.forward(obs_pin)
+        idt = max_over_ranks((time.perf_counter() - t0) / 3)
+        infer = {"metric": "InferenceServer actions/sec", "config": c4.name, "note": c4.note,
+                 "value": world * c4.batch_size / (ims / 1e3), "unit": "actions/s",
+                 "ms_per_batch": ims,
+                 "tflops": 2.2426e6 * c4.batch_size / (ims / 1e3) / 1e12,
+                 "e2e": {"value": world * c4.batch_size / idt, "unit": "actions/s",
+                         "h2d_bytes_per_batch": obs.nbytes,
+                         "d2h_bytes_per_batch": c4.batch_size * (2 * c4.n_actions + 1) * 4}}
+
+    # ---- CPU baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            fps, cores, sample, _ = reference_cpu(cfg, seconds=10.0)
+            cpu = {"value": fps, "unit": "frames/s", "cores": cores, "kind": "reference",
+                   "sample": sample}
+        except Exception as e:
+            cpu = {"value": None, "unit": "frames/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {type(e).__name__}: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": cfg.name, "note": cfg.note, "algo": cfg.algo,
+                       "optimizer": cfg.optimizer, "obs_dim": D, "hidden": list(hidden),
+                       "n_actions": A, "unroll_len": T, "segments_per_gpu": S,
+                       "frames_per_gpu_step": F, "obs_format": "u8 planes" if obs_u8 else "f32",
+                       "parallelism": f"dp{world}", "gemm_precision": "3xTF32 (fp32-exact)",
+                       "l2": "inputs > L2 (obs >= 254 MB per batch, two alternating batches)"},
+            "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": 48 + 8},
+            "gpu_launches": launches,
+            "roofline": roofline,
+            "kernels": kernels,
+            "infserver": infer,
+            "cpu_baseline": cpu,
+            "clocks": clk.result(),
+        }
+        print(json.dumps(line))
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

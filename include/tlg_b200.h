@@ -155,6 +155,9 @@ void* tlg_learner_stream(tlg_learner* l);
 int tlg_learner_phase_ms(tlg_learner* l, float* out, int n);
 /* Kernel launches issued by the last train_step (this library's kernels only). */
 int tlg_learner_last_launches(tlg_learner* l);
+/* Device time (ms) of one trunk GEMM of the last step (timing mode): kind 0 = forward,
+ * 1 = dW (split-K, without its reduce), 2 = dX; layer is 0-based. */
+int tlg_learner_kernel_ms(tlg_learner* l, int kind, int layer, float* ms);
 
 /* ---- inference (InfServer batched forward) ----------------------------- */
 int tlg_policy_create(const tlg_policy_shape* shape, int32_t device, uint32_t max_batch,

@@ -117,6 +117,8 @@ def lib():
         L.tlg_learner_stream.argtypes = [C.c_void_p]
         L.tlg_learner_phase_ms.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
         L.tlg_learner_last_launches.argtypes = [C.c_void_p]
+        L.tlg_learner_kernel_ms.argtypes = [C.c_void_p, C.c_int, C.c_int,
+                                            C.POINTER(C.c_float)]
         L.tlg_policy_create.argtypes = [C.POINTER(PolicyShape), C.c_int32, C.c_uint32,
                                         C.POINTER(C.c_void_p)]
         L.tlg_policy_destroy.argtypes = [C.c_void_p]
@@ -148,6 +150,7 @@ EXPORTS = [
     "tlg_learner_set_hyper", "tlg_comm_unique_id", "tlg_learner_comm_init",
     "tlg_learner_train_step", "tlg_learner_get_grad", "tlg_learner_get_returns",
     "tlg_learner_stream", "tlg_learner_phase_ms", "tlg_learner_last_launches",
+    "tlg_learner_kernel_ms",
     "tlg_policy_create", "tlg_policy_destroy", "tlg_policy_set_params", "tlg_policy_forward",
     "tlg_policy_stream", "tlg_returns",
 ]
@@ -265,6 +268,13 @@ class Learner:
 
     def last_launches(self):
         return lib().tlg_learner_last_launches(self.h)
+
+    def kernel_ms(self, kind, layer):
+        """kind: 'fwd' | 'dw' | 'dx' (0-based layer)."""
+        ms = C.c_float()
+        check(lib().tlg_learner_kernel_ms(self.h, {"fwd": 0, "dw": 1, "dx": 2}[kind], layer,
+                                          C.byref(ms)))
+        return ms.value
 
 
 def comm_unique_id() -> bytes:

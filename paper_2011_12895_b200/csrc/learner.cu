@@ -179,6 +179,8 @@ struct tlg_learner {
   tlg::StepStatsDev* h_stats = nullptr;
   int* h_flags = nullptr;  // [0] err bits, [1..] guard as float bits
   cudaEvent_t ev[8]{};
+  // per-GEMM events (timing mode): [kind 0 fwd | 1 dW | 2 dX][layer][begin,end]
+  cudaEvent_t kev[3][8][2]{};
   int launches = 0;
   int S_last = 0;
 
@@ -239,6 +241,10 @@ struct tlg_learner {
     TLG_CUDA(cudaMallocHost(&h_stats, sizeof(tlg::StepStatsDev)));
     TLG_CUDA(cudaMallocHost(&h_flags, 16));
     for (auto& e : ev) TLG_CUDA(cudaEventCreate(&e));
+    if (cfg.timing)
+      for (auto& a : kev)
+        for (auto& b : a)
+          for (auto& e : b) TLG_CUDA(cudaEventCreate(&e));
   }
 
   ~tlg_learner() {
@@ -246,6 +252,10 @@ struct tlg_learner {
     if (comm) ncclCommDestroy(comm);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
+    for (auto& a : kev)
+      for (auto& b : a)
+        for (auto& e : b)
+          if (e) cudaEventDestroy(e);
     if (h_stats) cudaFreeHost(h_stats);
     if (h_flags) cudaFreeHost(h_flags);
     if (stream) cudaStreamDestroy(stream);
@@ -253,6 +263,9 @@ struct tlg_learner {
 
   void mark(int i) {
     if (cfg.timing) TLG_CUDA(cudaEventRecord(ev[i], stream));
+  }
+  void kmark(int kind, int layer, int end) {
+    if (cfg.timing) TLG_CUDA(cudaEventRecord(kev[kind][layer][end], stream));
   }
 
   void stage(const tlg_segment_batch& b, int on_device, tlg::BatchDev& bd, const float** obs_f32,
@@ -347,7 +360,9 @@ struct tlg_learner {
       p.out_lo = act_lo[l];
       p.ldo = outw;
       p.bias = params + net.b_off[l];
+      kmark(0, int(l), 0);
       tlg::gemm::launch(A, B, int(F), outw, in, tlg::gemm::kEpiFwdTanh, p, 1, stream);
+      kmark(0, int(l), 1);
       ++launches;
     }
     mark(2);
@@ -386,7 +401,9 @@ struct tlg_learner {
       const int kb = (int(F) + tlg::gemm::kBK - 1) / tlg::gemm::kBK;
       const int per = (kb + sp - 1) / sp;
       const int sp_eff = (kb + per - 1) / per;
+      kmark(1, l, 0);
       tlg::gemm::launch(A, B, outw, in, int(F), tlg::gemm::kEpiStore, p, sp, stream);
+      kmark(1, l, 1);
       tlg::launch_dw_reduce(ws, sp_eff, long(outw) * in, grad + net.w_off[l], stream);
       // db_l = column sums of dZ_l
       tlg::launch_colsum(dz[l], outw, F, outw, col_partial, grad + net.b_off[l], stream);
@@ -401,7 +418,9 @@ struct tlg_learner {
         p2.ldo = in;
         p2.act_hi = act[l - 1];
         p2.ld_act = in;
+        kmark(2, l, 0);
         tlg::gemm::launch(A2, B2, int(F), in, outw, tlg::gemm::kEpiBwdTanh, p2, 1, stream);
+        kmark(2, l, 1);
         ++launches;
       }
     }
@@ -713,6 +732,16 @@ int tlg_learner_phase_ms(tlg_learner* l, float* out, int n) {
 }
 
 int tlg_learner_last_launches(tlg_learner* l) { return l ? l->launches : 0; }
+
+int tlg_learner_kernel_ms(tlg_learner* l, int kind, int layer, float* ms) {
+  return Guard([&] {
+    if (!l->cfg.timing) throw InvalidArg("learner created without timing");
+    if (kind < 0 || kind > 2 || layer < 0 || layer >= int(l->net.L))
+      throw InvalidArg("no such GEMM");
+    if (kind == 2 && layer == 0) throw InvalidArg("layer 1 has no dX GEMM");
+    TLG_CUDA(cudaEventElapsedTime(ms, l->kev[kind][layer][0], l->kev[kind][layer][1]));
+  });
+}
 
 int tlg_policy_create(const tlg_policy_shape* shape, int32_t device, uint32_t max_batch,
                       tlg_policy** out) {
