@@ -121,6 +121,9 @@ typedef struct tlg_policy tlg_policy;
 
 const char* tlg_last_error(void);
 const char* tlg_version(void);
+/* Page-locked host staging memory for the host-pointer calls (NULL on failure). */
+void* tlg_host_alloc(size_t bytes);
+void tlg_host_free(void* p);
 
 /* ---- learner ------------------------------------------------------------ */
 int tlg_learner_create(const tlg_learner_config* cfg, const tlg_policy_shape* shape,
@@ -143,6 +146,13 @@ int tlg_learner_comm_init(tlg_learner* l, const uint8_t unique_id[128], int nran
  * then every rank applies the identical optimizer step. */
 int tlg_learner_train_step(tlg_learner* l, const tlg_segment_batch* batch, int on_device,
                            tlg_step_stats* stats);
+/* Learner::TrainStep with `n_shards` in-process shards on this GPU (the reference's
+ * num_shards shard threads, learner.cpp:117-134): shard r's gradient is computed over
+ * shards[r] with its own advantage normalisation and 1/n (rlmath.cpp:18-34,122), the
+ * shard gradients are summed in rank order, allreduced with the other ranks, and
+ * scaled by 1/(n_shards * nranks).  stats receives one entry per local shard. */
+int tlg_learner_train_step_shards(tlg_learner* l, const tlg_segment_batch* shards, int n_shards,
+                                  int on_device, tlg_step_stats* stats);
 /* The averaged gradient of the last step (f32 -> f64), for parity checks. */
 int tlg_learner_get_grad(tlg_learner* l, double* out, size_t n);
 /* Per-frame advantages / value targets of the last step ([S][T], f32, padding = 0). */

@@ -1,0 +1,288 @@
+// B200 drop-in implementation of tleague::learner::Learner (replaces the reference's
+// src/learner/learner.cpp).  Host control flow mirrors learner.cpp line for line; the
+// math of TrainStep (learner.cpp:117-152) runs on the GPU via include/tlg_b200.h.
+#include "tleague/learner/learner.hpp"
+
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <thread>
+
+#include "tlg_b200.h"
+
+namespace tleague::learner {
+
+namespace {
+
+// C-ABI status -> the reference's exception types (learner.cpp:129-144, rlmath.cpp).
+void Check(int rc) {
+  if (rc == TLG_OK) return;
+  const std::string msg = tlg_last_error();
+  if (rc == TLG_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+  throw std::runtime_error(msg);
+}
+
+template <typename T>
+struct Pinned {
+  T* p = nullptr;
+  std::size_t n = 0;
+  void ensure(std::size_t count) {
+    if (count <= n) return;
+    tlg_host_free(p);
+    p = static_cast<T*>(tlg_host_alloc(count * sizeof(T)));
+    if (!p) throw std::runtime_error("pinned host allocation failed");
+    n = count;
+  }
+  ~Pinned() { tlg_host_free(p); }
+};
+
+}  // namespace
+
+Algo ParseAlgo(const std::string& name) {
+  if (name == "ppo") return Algo::kPpo;
+  if (name == "vtrace") return Algo::kVtrace;
+  if (name == "ppo_vtrace") return Algo::kPpoVtrace;
+  throw std::invalid_argument("unknown algo: " + name);
+}
+
+// One GPU learner plus pinned SoA staging for `shards` slices of the replay draw.
+struct Learner::Gpu {
+  tlg_learner* h = nullptr;
+  tlg_policy_shape shape{};
+  std::uint32_t S = 0, T = 0, shards = 0;
+  std::size_t P = 0;
+  Pinned<float> obs, reward, blogp, value, boot;
+  Pinned<std::int32_t> action, valid;
+  Pinned<std::uint8_t> done;
+  std::vector<tlg_segment_batch> batches;
+  std::vector<tlg_step_stats> stats;
+
+  ~Gpu() { tlg_learner_destroy(h); }
+
+  bool Matches(const tlg_policy_shape& s, std::uint32_t S_, std::uint32_t T_,
+               std::uint32_t sh) const {
+    return h && std::memcmp(&s, &shape, sizeof(s)) == 0 && S_ == S && T_ == T && sh == shards;
+  }
+
+  // SoA packing of the reference's AoS segments (types.hpp:82-104), padding zeroed.
+  void Pack(const std::vector<TrajectorySegment>& segs) {
+    const std::size_t D = shape.obs_dim, F = std::size_t(S) * T * shards;
+    obs.ensure(F * D);
+    reward.ensure(F);
+    blogp.ensure(F);
+    value.ensure(F);
+    action.ensure(F);
+    done.ensure(F);
+    boot.ensure(std::size_t(S) * shards);
+    valid.ensure(std::size_t(S) * shards);
+    std::memset(obs.p, 0, F * D * sizeof(float));
+    for (std::size_t i = 0; i < segs.size(); ++i) {
+      const TrajectorySegment& seg = segs[i];
+      if (seg.valid_steps > T || seg.valid_steps > seg.steps.size())
+        throw std::invalid_argument("segment valid_steps exceeds its steps / unroll_len");
+      boot.p[i] = float(seg.bootstrap_value);
+      valid.p[i] = std::int32_t(seg.valid_steps);
+      for (std::uint32_t t = 0; t < T; ++t) {
+        const std::size_t f = i * T + t;
+        if (t < seg.valid_steps) {
+          const SegmentStep& st = seg.steps[t];
+          if (st.obs.size() != D)
+            throw std::invalid_argument("observation size does not match policy shape");
+          for (std::size_t j = 0; j < D; ++j) obs.p[f * D + j] = float(st.obs[j]);
+          action.p[f] = std::int32_t(st.action);
+          reward.p[f] = float(st.reward);
+          blogp.p[f] = float(st.behavior_logp);
+          value.p[f] = float(st.value_est);
+          done.p[f] = st.done ? 1 : 0;
+        } else {
+          action.p[f] = 0;
+          reward.p[f] = blogp.p[f] = value.p[f] = 0.f;
+          done.p[f] = 0;
+        }
+      }
+    }
+    batches.assign(shards, tlg_segment_batch{});
+    for (std::uint32_t r = 0; r < shards; ++r) {
+      tlg_segment_batch& b = batches[r];
+      const std::size_t f0 = std::size_t(r) * S * T, s0 = std::size_t(r) * S;
+      b.n_segments = S;
+      b.unroll_len = T;
+      b.obs_dim = shape.obs_dim;
+      b.obs_dtype = TLG_OBS_F32;
+      b.obs = obs.p + f0 * D;
+      b.action = action.p + f0;
+      b.reward = reward.p + f0;
+      b.behavior_logp = blogp.p + f0;
+      b.value_est = value.p + f0;
+      b.done = done.p + f0;
+      b.bootstrap = boot.p + s0;
+      b.valid_steps = valid.p + s0;
+    }
+  }
+};
+
+Learner::Learner(LearnerConfig config, league::LeagueIface& league, pool::ModelPoolIface& pool)
+    : config_(std::move(config)),
+      league_(league),
+      pool_(pool),
+      replay_(config_.replay_capacity, /*max_reuse set per task*/ 1, config_.seed),
+      gpu_(std::make_unique<Gpu>()) {
+  if (config_.num_shards == 0) throw std::invalid_argument("num_shards must be >= 1");
+  StartPeriod();
+}
+
+Learner::~Learner() = default;
+
+void Learner::StartPeriod() {
+  Task task = league_.RequestLearnerTask(config_.group, 0);
+  ModelRecord record = pool_.GetModel(task.learning_model_key);
+  std::lock_guard lock(task_mu_);
+  current_key_ = task.learning_model_key;
+  hyper_ = task.hyperparams;
+  params_ = std::move(record.params);
+  params_stale_ = false;
+  parent_key_ = record.parent_key;
+  created_at_us_ = record.created_at_us;
+  replay_.Clear();
+  replay_.SetMaxReuse(hyper_.max_reuse);
+
+  // (Re)configure the device learner for this period's blob and hyperparameters.
+  tlg_policy_shape s{};
+  s.family = config_.mlp_hidden.empty() ? std::uint32_t(params_.family) : TLG_FAMILY_MLP;
+  s.obs_dim = params_.shape.obs_dim;
+  s.n_actions = params_.shape.n_actions;
+  s.n_hidden = std::uint32_t(config_.mlp_hidden.size());
+  if (s.n_hidden > 8) throw std::invalid_argument("at most 8 hidden layers");
+  for (std::uint32_t l = 0; l < s.n_hidden; ++l) s.hidden[l] = config_.mlp_hidden[l];
+  const std::uint32_t S = hyper_.batch_size, T = hyper_.unroll_len;
+  if (!gpu_->Matches(s, S, T, config_.num_shards)) {
+    tlg_learner_destroy(gpu_->h);
+    gpu_->h = nullptr;
+    tlg_learner_config c{};
+    c.algo = config_.algo == Algo::kPpo      ? TLG_ALGO_PPO
+             : config_.algo == Algo::kVtrace ? TLG_ALGO_VTRACE
+                                             : TLG_ALGO_PPO_VTRACE;
+    c.optimizer = config_.optimizer == Optimizer::kAdam ? TLG_OPT_ADAM : TLG_OPT_SGD;
+    c.adam_beta1 = config_.adam_beta1;
+    c.adam_beta2 = config_.adam_beta2;
+    c.adam_eps = config_.adam_eps;
+    c.max_segments = S;
+    c.unroll_len = T;
+    c.device = config_.device;
+    c.obs_dtype = TLG_OBS_F32;
+    Check(tlg_learner_create(&c, &s, &gpu_->h));
+    gpu_->shape = s;
+    gpu_->S = S;
+    gpu_->T = T;
+    gpu_->shards = config_.num_shards;
+    gpu_->P = tlg_learner_param_count(gpu_->h);
+  }
+  tlg_hyper hp{hyper_.learning_rate, hyper_.gamma, hyper_.lam, hyper_.clip_eps,
+               hyper_.vf_coef, hyper_.ent_coef, hyper_.kl_teacher_coef, hyper_.rho_bar,
+               hyper_.c_bar, hyper_.batch_size, hyper_.unroll_len, hyper_.max_reuse,
+               hyper_.adv_norm ? 1 : 0};
+  Check(tlg_learner_set_hyper(gpu_->h, &hp));
+  Check(tlg_learner_set_params(gpu_->h, params_.values.data(), params_.values.size()));
+}
+
+void Learner::PushSegment(const TrajectorySegment& segment) {
+  {
+    std::lock_guard lock(task_mu_);
+    if (segment.model_key != current_key_) {
+      stale_dropped_.fetch_add(1, std::memory_order_relaxed);
+      return;
+    }
+  }
+  replay_.Push(segment);
+}
+
+bool Learner::TrainStep() {
+  if (config_.step_delay_ms > 0)
+    std::this_thread::sleep_for(std::chrono::milliseconds(config_.step_delay_ms));
+  const std::size_t per_shard = hyper_.batch_size;
+  auto segments = replay_.SampleBlocking(per_shard * config_.num_shards);
+  if (segments.empty()) return false;
+  gpu_->Pack(segments);
+  gpu_->stats.assign(config_.num_shards, tlg_step_stats{});
+  // Per-shard gradients, rank-ordered mean, optimizer: one device call.  Errors come
+  // back as the reference's exception types; on failure the parameters are unchanged.
+  Check(tlg_learner_train_step_shards(gpu_->h, gpu_->batches.data(), int(config_.num_shards),
+                                      /*on_device=*/0, gpu_->stats.data()));
+  ++update_steps_;
+  params_stale_ = true;
+  if (config_.publish_interval > 0 && update_steps_ % config_.publish_interval == 0) Publish();
+  return true;
+}
+
+void Learner::SyncParams() const {
+  if (!params_stale_) return;
+  Check(tlg_learner_get_params(gpu_->h, params_.values.data(), params_.values.size()));
+  params_stale_ = false;
+}
+
+const ParamBlob& Learner::params() const {
+  SyncParams();
+  return params_;
+}
+
+void Learner::Publish() {
+  SyncParams();
+  ModelRecord record;
+  record.model_key = current_key_;
+  record.params = params_;
+  record.hyperparams = hyper_;
+  record.parent_key = parent_key_;
+  record.created_at_us = created_at_us_;
+  record.frozen = false;
+  pool_.PutModel(record);
+}
+
+std::string Learner::FinishPeriod() {
+  Publish();  // the frozen pool member must be the final parameters
+  std::string successor = league_.EndLearningPeriod(config_.group);
+  StartPeriod();
+  return successor;
+}
+
+std::string Learner::RunPeriod() {
+  for (std::uint32_t k = 0; k < config_.period_steps; ++k)
+    if (!TrainStep()) return {};
+  return FinishPeriod();
+}
+
+ThroughputStats Learner::Counters() const {
+  ThroughputStats s;
+  s.rfps = double(replay_.received_steps());
+  s.cfps = double(replay_.consumed_steps());
+  s.update_steps = update_steps_;
+  s.stale_dropped = stale_dropped_.load(std::memory_order_relaxed);
+  return s;
+}
+
+void Learner::LogMetricsLine(std::string& out) {
+  using Clock = std::chrono::steady_clock;
+  const double now = std::chrono::duration<double>(Clock::now().time_since_epoch()).count();
+  const std::uint64_t recv = replay_.received_steps();
+  const std::uint64_t cons = replay_.consumed_steps();
+  double rfps = 0.0, cfps = 0.0;
+  if (last_metric_ts_ > 0.0 && now > last_metric_ts_) {
+    const double dt = now - last_metric_ts_;
+    rfps = double(recv - last_metric_recv_) / dt;
+    cfps = double(cons - last_metric_cons_) / dt;
+  }
+  last_metric_ts_ = now;
+  last_metric_recv_ = recv;
+  last_metric_cons_ = cons;
+  const auto wall = std::chrono::duration_cast<std::chrono::seconds>(
+                        std::chrono::system_clock::now().time_since_epoch())
+                        .count();
+  char buf[160];
+  std::snprintf(buf, sizeof(buf), "ts=%lld group=%u rfps=%.1f cfps=%.1f steps=%llu\n",
+                static_cast<long long>(wall), config_.group, rfps, cfps,
+                static_cast<unsigned long long>(update_steps_));
+  out += buf;
+}
+
+}  // namespace tleague::learner

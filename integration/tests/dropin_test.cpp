@@ -1,0 +1,501 @@
+// Drop-in acceptance of the B200 Learner / InfServer against the reference's own
+// services (LeagueState, ModelStore/DirectPool, ReplayMem, net, run::RunBench), in the
+// scenarios of the reference's learner_test.cpp and infserver_test.cpp.  Numeric
+// checks compare with the reference's fp64 rlmath/policy routines (linked unchanged)
+// in the reference's Close() metric (acceptance.cpp:439-441).
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <functional>
+#include <limits>
+#include <memory>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "tleague/infserver/inf_server.hpp"
+#include "tleague/league/league_state.hpp"
+#include "tleague/learner/learner.hpp"
+#include "tleague/policy/policy.hpp"
+#include "tleague/pool/model_store.hpp"
+#include "tleague/rlmath/rlmath.hpp"
+#include "tleague/run/bench.hpp"
+#include "tlg_b200.h"
+
+using namespace tleague;
+
+// ---------------------------------------------------------------------------
+// minimal test harness
+namespace {
+struct Case {
+  const char* name;
+  std::function<void()> fn;
+};
+std::vector<Case>& Cases() {
+  static std::vector<Case> c;
+  return c;
+}
+int g_fail = 0, g_checks = 0;
+struct Reg {
+  Reg(const char* n, std::function<void()> f) { Cases().push_back({n, std::move(f)}); }
+};
+#define TEST(name)                         \
+  static void name();                      \
+  static Reg reg_##name(#name, name);      \
+  static void name()
+#define CHECK(cond)                                                              \
+  do {                                                                           \
+    ++g_checks;                                                                  \
+    if (!(cond)) {                                                               \
+      ++g_fail;                                                                  \
+      std::printf("  CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #cond);       \
+    }                                                                            \
+  } while (0)
+#define CHECK_THROWS_AS(expr, type)                                              \
+  do {                                                                           \
+    ++g_checks;                                                                  \
+    bool ok_ = false;                                                            \
+    try {                                                                        \
+      expr;                                                                      \
+    } catch (const type&) {                                                      \
+      ok_ = true;                                                                \
+    } catch (...) {                                                              \
+    }                                                                            \
+    if (!ok_) {                                                                  \
+      ++g_fail;                                                                  \
+      std::printf("  CHECK_THROWS_AS failed %s:%d: %s\n", __FILE__, __LINE__, #expr); \
+    }                                                                            \
+  } while (0)
+
+bool Close(double a, double b, double tol) {
+  return std::abs(a - b) <= tol * std::max({1.0, std::abs(a), std::abs(b)});
+}
+bool AllClose(const std::vector<double>& a, const std::vector<double>& b, double tol,
+              double* worst = nullptr) {
+  if (a.size() != b.size()) return false;
+  double w = 0;
+  bool ok = true;
+  for (std::size_t i = 0; i < a.size(); ++i) {
+    const double e = std::abs(a[i] - b[i]) / std::max({1.0, std::abs(a[i]), std::abs(b[i])});
+    w = std::max(w, e);
+    ok &= Close(a[i], b[i], tol);
+  }
+  if (worst) *worst = w;
+  return ok;
+}
+
+// ---------------------------------------------------------------------------
+// learner_test.cpp-style rig and synthetic segments (3-step episodes, one state)
+struct Rig {
+  pool::ModelStore store;
+  pool::DirectPool pool{store};
+  league::LeagueState league;
+  explicit Rig(HyperParams hyper, std::uint64_t seed = 42) : league(Groups(hyper), pool, seed) {}
+  static std::vector<league::LearnerGroupConfig> Groups(HyperParams hyper) {
+    league::LearnerGroupConfig cfg;
+    cfg.shape = {1, 3};
+    cfg.init_scale = 0.3;
+    cfg.hyper = hyper;
+    return {cfg};
+  }
+};
+
+HyperParams TestHyper() {
+  HyperParams hp;
+  hp.learning_rate = 0.05;
+  hp.batch_size = 4;
+  hp.max_reuse = 1;
+  hp.unroll_len = 3;
+  return hp;
+}
+
+TrajectorySegment MakeSegment(const std::string& key, std::mt19937_64& rng, std::uint64_t seq) {
+  TrajectorySegment seg;
+  seg.model_key = key;
+  seg.segment_seq = seq;
+  seg.valid_steps = 3;
+  seg.steps.resize(3);
+  std::uniform_real_distribution<double> real(-1.0, 1.0);
+  for (auto& step : seg.steps) {
+    step.obs = {1.0};
+    step.action = static_cast<std::uint32_t>(rng() % 3);
+    // fp32-representable so the fp64 oracle and the fp32 device path see the same data
+    step.reward = double(float(real(rng)));
+    step.behavior_logp = double(float(std::log(1.0 / 3) + 0.1 * real(rng)));
+    step.value_est = double(float(real(rng)));
+  }
+  seg.steps.back().done = true;
+  return seg;
+}
+
+// the reference's consume-time batch assembly, run serially in fp64 (learner.cpp:56-102)
+rlmath::Minibatch OracleBatch(const std::vector<TrajectorySegment>& segments, bool vtrace,
+                              const ParamBlob& params, const HyperParams& hp) {
+  rlmath::Minibatch batch;
+  for (const auto& seg : segments) {
+    const std::size_t n = seg.valid_steps;
+    std::vector<double> r(n), v(n), bl(n), tl(n);
+    std::unique_ptr<bool[]> d(new bool[n]);
+    for (std::size_t t = 0; t < n; ++t) {
+      r[t] = seg.steps[t].reward;
+      v[t] = seg.steps[t].value_est;
+      bl[t] = seg.steps[t].behavior_logp;
+      d[t] = seg.steps[t].done;
+      if (vtrace)
+        tl[t] = std::log(policy::Distribution(params, seg.steps[t].obs).probs[seg.steps[t].action]);
+    }
+    std::span<const bool> dones(d.get(), n);
+    std::vector<double> adv, tgt;
+    if (!vtrace) {
+      adv = rlmath::GaeAdvantages(r, v, seg.bootstrap_value, dones, hp.gamma, hp.lam);
+      tgt = rlmath::LambdaReturn(r, v, seg.bootstrap_value, dones, hp.gamma, hp.lam);
+    } else {
+      auto vt = rlmath::VtraceTargets(bl, tl, r, v, seg.bootstrap_value, dones, hp.gamma,
+                                      hp.rho_bar, hp.c_bar);
+      adv = std::move(vt.pg_adv);
+      tgt = std::move(vt.vs);
+    }
+    for (std::size_t t = 0; t < n; ++t) {
+      rlmath::Sample s;
+      s.obs = seg.steps[t].obs;
+      s.action = seg.steps[t].action;
+      s.behavior_logp = bl[t];
+      s.advantage = adv[t];
+      s.value_target = tgt[t];
+      batch.samples.push_back(std::move(s));
+    }
+  }
+  return batch;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+TEST(stale_model_keys_are_dropped) {
+  Rig rig(TestHyper());
+  learner::LearnerConfig cfg;
+  cfg.seed = 7;
+  learner::Learner lrn(cfg, rig.league, rig.pool);
+  std::mt19937_64 rng(1);
+  lrn.PushSegment(MakeSegment("main:0099", rng, 0));
+  lrn.PushSegment(MakeSegment("other:0000", rng, 1));
+  CHECK(lrn.replay().size() == 0);
+  CHECK(lrn.Counters().stale_dropped == 2);
+  lrn.PushSegment(MakeSegment(lrn.current_key(), rng, 2));
+  CHECK(lrn.replay().size() == 1);
+}
+
+TEST(two_shards_match_the_serial_fp64_reference) {
+  for (auto algo : {learner::Algo::kPpo, learner::Algo::kVtrace}) {
+    HyperParams hyper = TestHyper();
+    const bool vtrace = algo == learner::Algo::kVtrace;
+    if (vtrace) hyper.max_reuse = 2;
+    Rig rig(hyper);
+    learner::LearnerConfig cfg;
+    cfg.num_shards = 2;
+    cfg.algo = algo;
+    cfg.publish_interval = 1;
+    cfg.seed = 99;
+    learner::Learner lrn(cfg, rig.league, rig.pool);
+    learner::ReplayMem oracle_replay(cfg.replay_capacity, hyper.max_reuse, cfg.seed);
+    ParamBlob oracle = rig.store.Get(lrn.current_key())->params;
+    CHECK(oracle == lrn.params());
+    std::mt19937_64 feed_a(2024), feed_b(2024);
+    std::uint64_t seq = 0;
+    const std::size_t draw = hyper.batch_size * 2;
+    double worst_all = 0;
+    for (int step = 0; step < 30; ++step) {
+      for (std::size_t i = 0; i < draw; ++i) {
+        lrn.PushSegment(MakeSegment(lrn.current_key(), feed_a, seq + i));
+        oracle_replay.Push(MakeSegment(lrn.current_key(), feed_b, seq + i));
+      }
+      seq += draw;
+      CHECK(lrn.TrainStep());
+      auto segs = oracle_replay.SampleBlocking(draw);  // same ring, same seed: same draw
+      std::vector<double> avg(oracle.values.size(), 0.0);
+      for (int r = 0; r < 2; ++r) {
+        std::vector<TrajectorySegment> slice(segs.begin() + r * hyper.batch_size,
+                                             segs.begin() + (r + 1) * hyper.batch_size);
+        auto batch = OracleBatch(slice, vtrace, oracle, hyper);
+        auto res = vtrace ? rlmath::PgLossAndGrad(oracle, batch, hyper)
+                          : rlmath::PpoLossAndGrad(oracle, nullptr, batch, hyper);
+        for (std::size_t i = 0; i < avg.size(); ++i) avg[i] += res.grad[i];
+      }
+      for (double& g : avg) g *= 0.5;
+      oracle = rlmath::SgdStep(oracle, avg, hyper.learning_rate);
+      double worst = 0;
+      CHECK(AllClose(lrn.params().values, oracle.values, 1e-4, &worst));
+      worst_all = std::max(worst_all, worst);
+      // publish_interval = 1: the pool copy is the learner's parameters
+      CHECK(rig.store.Get(lrn.current_key())->params.values == lrn.params().values);
+      CHECK(lrn.replay().consumed_steps() == oracle_replay.consumed_steps());
+    }
+    std::printf("  %s: 30 steps, worst Close() error vs fp64 reference %.2e\n",
+                vtrace ? "vtrace" : "ppo", worst_all);
+  }
+}
+
+TEST(publishing_follows_the_configured_cadence) {
+  Rig rig(TestHyper());
+  learner::LearnerConfig cfg;
+  cfg.publish_interval = 3;
+  cfg.seed = 5;
+  learner::Learner lrn(cfg, rig.league, rig.pool);
+  const ParamBlob seed_params = rig.store.Get(lrn.current_key())->params;
+  std::mt19937_64 rng(9);
+  std::uint64_t seq = 0;
+  auto feed_and_step = [&] {
+    for (int i = 0; i < 4; ++i) lrn.PushSegment(MakeSegment(lrn.current_key(), rng, seq++));
+    CHECK(lrn.TrainStep());
+  };
+  feed_and_step();
+  feed_and_step();
+  CHECK(lrn.params().values != seed_params.values);
+  CHECK(rig.store.Get(lrn.current_key())->params.values == seed_params.values);
+  feed_and_step();
+  CHECK(rig.store.Get(lrn.current_key())->params.values == lrn.params().values);
+  CHECK(lrn.update_steps() == 3);
+}
+
+TEST(finishing_a_period_freezes_rolls_the_key_and_clears_the_ring) {
+  Rig rig(TestHyper());
+  learner::LearnerConfig cfg;
+  cfg.publish_interval = 100;
+  cfg.seed = 6;
+  learner::Learner lrn(cfg, rig.league, rig.pool);
+  CHECK(lrn.current_key() == "main:0000");
+  std::mt19937_64 rng(13);
+  for (int i = 0; i < 4; ++i) lrn.PushSegment(MakeSegment("main:0000", rng, i));
+  CHECK(lrn.TrainStep());
+  lrn.PushSegment(MakeSegment("main:0000", rng, 99));
+  std::string successor = lrn.FinishPeriod();
+  CHECK(successor == "main:0001");
+  CHECK(lrn.current_key() == "main:0001");
+  CHECK(lrn.replay().size() == 0);
+  auto frozen = rig.store.Get("main:0000");
+  CHECK(frozen->frozen);
+  CHECK(frozen->params.values == lrn.params().values);
+  lrn.PushSegment(MakeSegment("main:0000", rng, 100));
+  CHECK(lrn.replay().size() == 0);
+  CHECK(lrn.Counters().stale_dropped == 1);
+}
+
+TEST(a_non_finite_loss_aborts_the_training_step_loudly) {
+  Rig rig(TestHyper());
+  learner::LearnerConfig cfg;
+  cfg.seed = 8;
+  learner::Learner lrn(cfg, rig.league, rig.pool);
+  const ParamBlob before = lrn.params();
+  std::mt19937_64 rng(3);
+  for (int i = 0; i < 4; ++i) {
+    auto seg = MakeSegment(lrn.current_key(), rng, i);
+    seg.steps[0].reward = std::numeric_limits<double>::quiet_NaN();
+    lrn.PushSegment(seg);
+  }
+  CHECK_THROWS_AS(lrn.TrainStep(), std::invalid_argument);  // "non-finite advantage"
+  CHECK(lrn.params() == before);
+  CHECK(lrn.update_steps() == 0);
+}
+
+TEST(shutdown_releases_a_blocked_train_step) {
+  Rig rig(TestHyper());
+  learner::LearnerConfig cfg;
+  cfg.seed = 9;
+  learner::Learner lrn(cfg, rig.league, rig.pool);
+  bool result = true;
+  std::thread trainer([&] { result = lrn.TrainStep(); });
+  std::this_thread::sleep_for(std::chrono::milliseconds(30));
+  lrn.Shutdown();
+  trainer.join();
+  CHECK(!result);
+}
+
+// ---------------------------------------------------------------------------
+namespace {
+ModelRecord LinearModel(const std::string& key, std::uint64_t seed) {
+  ModelRecord rec;
+  rec.model_key = key;
+  rec.params = policy::InitParams(PolicyFamily::kLinearSoftmax, {4, 3}, 1.0, seed);
+  for (double& v : rec.params.values) v = double(float(v));
+  return rec;
+}
+std::vector<double> RandomObs(std::mt19937_64& rng) {
+  std::normal_distribution<double> n(0.0, 1.0);
+  std::vector<double> obs(4);
+  for (double& x : obs) x = double(float(n(rng)));
+  return obs;
+}
+}  // namespace
+
+TEST(remote_inference_equals_local_gpu_bit_for_bit_and_fp64_within_tolerance) {
+  pool::ModelStore store;
+  pool::DirectPool pool(store);
+  auto rec = LinearModel("main:0000", 3);
+  pool.PutModel(rec);
+  infserver::InfServer server({"main:0000"}, pool, "127.0.0.1", 0);
+  infserver::InferenceClient client(server.endpoint());
+  std::mt19937_64 rng(17);
+  double worst = 0;
+  for (int i = 0; i < 2000; ++i) {
+    auto obs = RandomObs(rng);
+    auto reply = client.Infer(obs);
+    auto local = server.EvaluateLocal(obs);
+    CHECK(reply.logits == local.logits);
+    CHECK(reply.probs == local.probs);
+    CHECK(reply.value == local.value);
+    auto ref = policy::Distribution(rec.params, obs);
+    double w1 = 0, w2 = 0;
+    CHECK(AllClose(reply.logits, ref.logits, 1e-5, &w1));
+    CHECK(AllClose(reply.probs, ref.probs, 1e-5, &w2));
+    CHECK(Close(reply.value, policy::ValueEstimate(rec.params, obs), 1e-5));
+    worst = std::max({worst, w1, w2});
+  }
+  std::printf("  worst Close() error vs fp64 policy::Distribution %.2e\n", worst);
+  server.Stop();
+}
+
+TEST(batched_requests_from_many_clients_are_routed_to_the_right_caller) {
+  pool::ModelStore store;
+  pool::DirectPool pool(store);
+  auto rec = LinearModel("main:0000", 9);
+  pool.PutModel(rec);
+  infserver::InfServer::Config cfg{"main:0000"};
+  cfg.max_batch = 8;
+  cfg.flush_timeout_ms = 5.0;
+  infserver::InfServer server(cfg, pool, "127.0.0.1", 0);
+  std::atomic<int> mismatches{0};
+  std::vector<std::thread> threads;
+  for (int t = 0; t < 12; ++t) {
+    threads.emplace_back([&, t] {
+      infserver::InferenceClient client(server.endpoint());
+      std::mt19937_64 rng(1000 + t);
+      for (int i = 0; i < 200; ++i) {
+        auto obs = RandomObs(rng);
+        auto reply = client.Infer(obs);
+        auto local = server.EvaluateLocal(obs);  // batch invariance: same bits alone
+        if (reply.logits != local.logits || reply.value != local.value) mismatches.fetch_add(1);
+      }
+    });
+  }
+  for (auto& t : threads) t.join();
+  CHECK(mismatches.load() == 0);
+  server.Stop();
+}
+
+TEST(the_tracked_key_follows_pool_updates_with_a_monotonic_version) {
+  pool::ModelStore store;
+  pool::DirectPool pool(store);
+  pool.PutModel(LinearModel("main:0000", 1));
+  infserver::InfServer::Config cfg{"latest:main"};
+  cfg.refresh_interval_ms = 5;
+  infserver::InfServer server(cfg, pool, "127.0.0.1", 0);
+  const std::uint64_t v0 = server.model_version();
+  server.RefreshNow();
+  CHECK(server.model_version() == v0);
+  pool.PutModel(LinearModel("main:0001", 2));
+  server.RefreshNow();
+  CHECK(server.model_version() == v0 + 1);
+  pool.PutModel(LinearModel("main:0002", 3));
+  for (int i = 0; i < 200 && server.model_version() == v0 + 1; ++i)
+    std::this_thread::sleep_for(std::chrono::milliseconds(5));
+  CHECK(server.model_version() == v0 + 2);
+  server.Stop();
+}
+
+TEST(replies_stay_self_consistent_under_concurrent_blob_refresh) {
+  pool::ModelStore store;
+  pool::DirectPool pool(store);
+  auto rec_a = LinearModel("main:0000", 11);
+  auto rec_b = LinearModel("main:0000", 22);
+  // device evaluations of each blob alone (batch-invariant forward)
+  tlg_policy_shape s{};
+  s.family = TLG_FAMILY_LINEAR;
+  s.obs_dim = 4;
+  s.n_actions = 3;
+  tlg_policy *pa = nullptr, *pb = nullptr;
+  CHECK(tlg_policy_create(&s, 0, 1, &pa) == 0);
+  CHECK(tlg_policy_create(&s, 0, 1, &pb) == 0);
+  CHECK(tlg_policy_set_params(pa, rec_a.params.values.data(), rec_a.params.values.size()) == 0);
+  CHECK(tlg_policy_set_params(pb, rec_b.params.values.data(), rec_b.params.values.size()) == 0);
+  pool.PutModel(rec_a);
+  infserver::InfServer::Config cfg{"main:0000"};
+  cfg.refresh_interval_ms = 1;
+  infserver::InfServer server(cfg, pool, "127.0.0.1", 0);
+  std::atomic<bool> stop{false};
+  std::thread writer([&] {
+    bool a = false;
+    while (!stop.load()) {
+      pool.PutModel(a ? rec_a : rec_b);
+      a = !a;
+      std::this_thread::sleep_for(std::chrono::milliseconds(1));
+    }
+  });
+  infserver::InferenceClient client(server.endpoint());
+  std::mt19937_64 rng(5);
+  int matched_a = 0, matched_b = 0, torn = 0;
+  for (int i = 0; i < 2000; ++i) {
+    auto obs = RandomObs(rng);
+    auto reply = client.Infer(obs);
+    float o[4], la[3], pa_[3], va, lb[3], pb_[3], vb;
+    for (int j = 0; j < 4; ++j) o[j] = float(obs[j]);
+    tlg_policy_forward(pa, o, 1, la, pa_, &va, 0);
+    tlg_policy_forward(pb, o, 1, lb, pb_, &vb, 0);
+    auto eq = [&](const float* l, float v) {
+      for (int k = 0; k < 3; ++k)
+        if (reply.logits[k] != double(l[k])) return false;
+      return reply.value == double(v);
+    };
+    if (eq(la, va)) ++matched_a;
+    else if (eq(lb, vb)) ++matched_b;
+    else ++torn;
+  }
+  stop.store(true);
+  writer.join();
+  CHECK(torn == 0);
+  CHECK(matched_a > 0);
+  CHECK(matched_b > 0);
+  server.Stop();
+  tlg_policy_destroy(pa);
+  tlg_policy_destroy(pb);
+}
+
+TEST(constructing_against_a_missing_key_fails_fast) {
+  pool::ModelStore store;
+  pool::DirectPool pool(store);
+  CHECK_THROWS_AS(infserver::InfServer({"absent:0000"}, pool, "127.0.0.1", 0), std::exception);
+}
+
+TEST(reference_run_bench_runs_on_the_b200_learner) {
+  // run::RunBench (bench.cpp:60-162) builds learner::Learner -- here the B200 drop-in --
+  // next to the reference's own actors, league and pool.
+  run::BenchOptions opts;
+  opts.duration_s = 1.0;
+  opts.warmup_s = 0.3;
+  auto res = run::RunBench("grid-1x2x8", opts);
+  std::printf("  RunBench grid-1x2x8 on the B200 learner: rfps %.0f cfps %.0f\n", res.rfps,
+              res.cfps);
+  CHECK(res.cfps > 0.0);
+  CHECK(res.rfps > 0.0);
+}
+
+int main(int argc, char** argv) {
+  int ran = 0;
+  for (const auto& c : Cases()) {
+    if (argc > 1 && std::string(c.name).find(argv[1]) == std::string::npos) continue;
+    const int before = g_fail;
+    std::printf("[ RUN  ] %s\n", c.name);
+    try {
+      c.fn();
+    } catch (const std::exception& e) {
+      ++g_fail;
+      std::printf("  uncaught exception: %s\n", e.what());
+    }
+    std::printf("[ %s ] %s\n", g_fail == before ? " OK " : "FAIL", c.name);
+    ++ran;
+  }
+  std::printf("%d tests, %d checks, %d failures\n", ran, g_checks, g_fail);
+  return g_fail ? 1 : 0;
+}

@@ -112,6 +112,8 @@ def lib():
         L.tlg_learner_comm_init.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int]
         L.tlg_learner_train_step.argtypes = [C.c_void_p, C.POINTER(SegmentBatchC), C.c_int,
                                              C.POINTER(StepStats)]
+        L.tlg_learner_train_step_shards.argtypes = [C.c_void_p, C.POINTER(SegmentBatchC), C.c_int,
+                                                    C.c_int, C.POINTER(StepStats)]
         L.tlg_learner_get_returns.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t]
         L.tlg_learner_stream.restype = C.c_void_p
         L.tlg_learner_stream.argtypes = [C.c_void_p]
@@ -145,10 +147,10 @@ def check(rc):
 
 
 EXPORTS = [
-    "tlg_last_error", "tlg_version", "tlg_learner_create", "tlg_learner_destroy",
+    "tlg_last_error", "tlg_version", "tlg_host_alloc", "tlg_host_free", "tlg_learner_create", "tlg_learner_destroy",
     "tlg_learner_param_count", "tlg_learner_set_params", "tlg_learner_get_params",
     "tlg_learner_set_hyper", "tlg_comm_unique_id", "tlg_learner_comm_init",
-    "tlg_learner_train_step", "tlg_learner_get_grad", "tlg_learner_get_returns",
+    "tlg_learner_train_step", "tlg_learner_train_step_shards", "tlg_learner_get_grad", "tlg_learner_get_returns",
     "tlg_learner_stream", "tlg_learner_phase_ms", "tlg_learner_last_launches",
     "tlg_learner_kernel_ms",
     "tlg_policy_create", "tlg_policy_destroy", "tlg_policy_set_params", "tlg_policy_forward",
@@ -251,6 +253,16 @@ class Learner:
         check(lib().tlg_learner_train_step(self.h, C.byref(view.c), 1 if on_device else 0,
                                            C.byref(st)))
         return st.as_dict()
+
+    def train_step_shards(self, batches, on_device=False):
+        """Several in-process shards on this GPU (learner.cpp:117-149)."""
+        views = [b if isinstance(b, (SegmentBatchView, DeviceSegmentBatch)) else
+                 SegmentBatchView(b) for b in batches]
+        arr = (SegmentBatchC * len(views))(*[v.c for v in views])
+        sts = (StepStats * len(views))()
+        check(lib().tlg_learner_train_step_shards(self.h, arr, len(views), 1 if on_device else 0,
+                                                  sts))
+        return [s.as_dict() for s in sts]
 
     def get_returns(self, n_frames):
         adv = np.zeros(n_frames, np.float32)

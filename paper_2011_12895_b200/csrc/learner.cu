@@ -149,7 +149,10 @@ struct tlg_learner {
   cudaStream_t stream = nullptr;
   DevFree mem;
   // parameters / optimizer (flat, fp32); grad has 4 trailing guard slots
-  float *params, *params_lo, *grad, *adam_m, *adam_v;
+  static constexpr int kMaxLocalShards = 64;
+  static constexpr int kMaxSplits = 128;
+  float *params, *params_lo, *grad, *grad_tmp, *adam_m, *adam_v;
+  float grad_scale = 1.f;
   // batch
   float *obs, *obs_lo;
   uint8_t* obs_u8;
@@ -197,6 +200,7 @@ struct tlg_learner {
     params = mem.add<float>(P_pad);
     params_lo = mem.add<float>(P_pad);
     grad = mem.add<float>(P_pad + 4);
+    grad_tmp = mem.add<float>(P_pad + 4);
     adam_m = mem.add<float>(P_pad);
     adam_v = mem.add<float>(P_pad);
     const long D = net.D;
@@ -223,7 +227,7 @@ struct tlg_learner {
     adv = mem.add<float>(F_max);
     target = mem.add<float>(F_max);
     seg_partial = mem.add<double>(2 * S_max);
-    stats = mem.add<tlg::StepStatsDev>(1);
+    stats = mem.add<tlg::StepStatsDev>(kMaxLocalShards);
     err = mem.add<int>(4);
     const long nblk = (F_max + tlg::kLossFrames - 1) / tlg::kLossFrames;
     hg_partial = mem.add<float>(nblk * A1 * long(net.head.H) + nblk * A1);
@@ -232,13 +236,13 @@ struct tlg_learner {
     long max_cols = 1;
     for (uint32_t l = 0; l < net.L; ++l) {
       const int out = int(net.dims[l + 1]), in = int(net.dims[l]);
-      const int sp = tlg::gemm::pick_splits(out, in, int(F_max), 16);
+      const int sp = tlg::gemm::pick_splits(out, in, int(F_max), kMaxSplits);
       ws_elems = std::max(ws_elems, long(sp) * out * in);
       max_cols = std::max<long>(max_cols, out);
     }
     ws = ws_elems ? mem.add<float>(ws_elems) : nullptr;
     col_partial = mem.add<float>(((F_max + 255) / 256) * max_cols);
-    TLG_CUDA(cudaMallocHost(&h_stats, sizeof(tlg::StepStatsDev)));
+    TLG_CUDA(cudaMallocHost(&h_stats, kMaxLocalShards * sizeof(tlg::StepStatsDev)));
     TLG_CUDA(cudaMallocHost(&h_flags, 16));
     for (auto& e : ev) TLG_CUDA(cudaEventCreate(&e));
     if (cfg.timing)
@@ -329,11 +333,9 @@ struct tlg_learner {
     bd.valid = valid;
   }
 
-  void step(const tlg_segment_batch& b, int on_device, tlg_step_stats* out) {
-    if (!hp_set) throw InvalidArg("hyperparameters not set");
-    launches = 0;
-    TLG_CUDA(cudaSetDevice(cfg.device));
-    mark(0);
+  // One shard's forward/backward; its gradient lands in `gtarget` (learner.cpp:117-134).
+  void run_shard(const tlg_segment_batch& b, int on_device, int shard, float* gtarget) {
+    tlg::StepStatsDev* st = stats + shard;
     tlg::BatchDev bd{};
     const float* x0 = nullptr;
     bool obs_exact = false;
@@ -341,14 +343,13 @@ struct tlg_learner {
     S_last = bd.S;
     const long F = long(bd.S) * T;
     const long D = net.D;
-    TLG_CUDA(cudaMemsetAsync(err, 0, 16, stream));
     const float* x0_lo = nullptr;
     if (net.L > 0 && !obs_exact) {
       tlg::launch_split_lo(x0, obs_lo, F * D, stream);
       ++launches;
       x0_lo = obs_lo;
     }
-    mark(1);
+    if (shard == 0) mark(1);
     // ---- forward trunk
     using tlg::gemm::Operand;
     for (uint32_t l = 0; l < net.L; ++l) {
@@ -360,12 +361,12 @@ struct tlg_learner {
       p.out_lo = act_lo[l];
       p.ldo = outw;
       p.bias = params + net.b_off[l];
-      kmark(0, int(l), 0);
+      if (shard == 0) kmark(0, int(l), 0);
       tlg::gemm::launch(A, B, int(F), outw, in, tlg::gemm::kEpiFwdTanh, p, 1, stream);
-      kmark(0, int(l), 1);
+      if (shard == 0) kmark(0, int(l), 1);
       ++launches;
     }
-    mark(2);
+    if (shard == 0) mark(2);
     // ---- heads, returns, loss
     const float* hL = net.L ? act[net.L - 1] : x0;
     const long ldh = net.head.H;
@@ -375,38 +376,37 @@ struct tlg_learner {
                      float(hp.ent_coef), float(hp.rho_bar), float(hp.c_bar), hp.adv_norm};
     const int algo = int(cfg.algo);
     tlg::launch_returns(bd, algo, hd, tlogp, adv, target, seg_partial, err, stream);
-    tlg::launch_finalize_adv(seg_partial, bd, hp.adv_norm, stats, err, stream);
+    tlg::launch_finalize_adv(seg_partial, bd, hp.adv_norm, st, err, stream);
     const int loss_kind = algo == TLG_ALGO_VTRACE ? 1 : 0;
     const int nblk = tlg::launch_loss_backward(
-        net.head, params, hL, ldh, bd, head_out, adv, target, stats, hd, loss_kind,
+        net.head, params, hL, ldh, bd, head_out, adv, target, st, hd, loss_kind,
         net.L ? dz[net.L - 1] : nullptr, net.L ? dz_lo[net.L - 1] : nullptr, hg_partial,
         loss_partial, stream);
-    tlg::launch_head_grad_reduce(net.head, hg_partial, loss_partial, nblk, grad, stats, stream);
+    tlg::launch_head_grad_reduce(net.head, hg_partial, loss_partial, nblk, gtarget, st, stream);
     launches += 5;
-    mark(3);
+    if (shard == 0) mark(3);
     // ---- backward trunk
     for (int l = int(net.L) - 1; l >= 0; --l) {
       const int in = int(net.dims[l]), outw = int(net.dims[l + 1]);
       const float* xin = l == 0 ? x0 : act[l - 1];
       const float* xin_lo = l == 0 ? x0_lo : act_lo[l - 1];
       // dW_l = dZ_l^T . X_{l-1}   (K = frames, split-K partials reduced in fixed order)
-      int sp = tlg::gemm::pick_splits(outw, in, int(F), 16);
+      int sp = tlg::gemm::pick_splits(outw, in, int(F), kMaxSplits);
       while (long(sp) * outw * in > ws_elems && sp > 1) --sp;
       Operand A{dz[l], dz_lo[l], outw, true};
       Operand B{xin, xin_lo, in, true};
       tlg::gemm::Params p{};
       p.ws = ws;
       p.ws_split_stride = long(outw) * in;
-      // launch() may shrink the split count so that no split is empty
       const int kb = (int(F) + tlg::gemm::kBK - 1) / tlg::gemm::kBK;
       const int per = (kb + sp - 1) / sp;
-      const int sp_eff = (kb + per - 1) / per;
-      kmark(1, l, 0);
+      const int sp_eff = (kb + per - 1) / per;  // launch() drops empty splits the same way
+      if (shard == 0) kmark(1, l, 0);
       tlg::gemm::launch(A, B, outw, in, int(F), tlg::gemm::kEpiStore, p, sp, stream);
-      kmark(1, l, 1);
-      tlg::launch_dw_reduce(ws, sp_eff, long(outw) * in, grad + net.w_off[l], stream);
+      if (shard == 0) kmark(1, l, 1);
+      tlg::launch_dw_reduce(ws, sp_eff, long(outw) * in, gtarget + net.w_off[l], stream);
       // db_l = column sums of dZ_l
-      tlg::launch_colsum(dz[l], outw, F, outw, col_partial, grad + net.b_off[l], stream);
+      tlg::launch_colsum(dz[l], outw, F, outw, col_partial, gtarget + net.b_off[l], stream);
       launches += 4;
       if (l > 0) {
         // dZ_{l-1} = (dZ_l . W_l) * (1 - X_{l-1}^2)
@@ -418,30 +418,46 @@ struct tlg_learner {
         p2.ldo = in;
         p2.act_hi = act[l - 1];
         p2.ld_act = in;
-        kmark(2, l, 0);
+        if (shard == 0) kmark(2, l, 0);
         tlg::gemm::launch(A2, B2, int(F), in, outw, tlg::gemm::kEpiBwdTanh, p2, 1, stream);
-        kmark(2, l, 1);
+        if (shard == 0) kmark(2, l, 1);
         ++launches;
       }
     }
+    if (gtarget != grad) {
+      accumulate_grad();  // grad += shard gradient, in rank order (learner.cpp:145-147)
+    }
+    set_guard(shard);
+  }
+
+  // Learner::TrainStep over `n` local shards (+ the communicator's other ranks).
+  void step(const tlg_segment_batch* bs, int n, int on_device, tlg_step_stats* out) {
+    if (!hp_set) throw InvalidArg("hyperparameters not set");
+    if (n < 1 || n > kMaxLocalShards) throw InvalidArg("1..64 local shards per call");
+    launches = 0;
+    TLG_CUDA(cudaSetDevice(cfg.device));
+    mark(0);
+    TLG_CUDA(cudaMemsetAsync(err, 0, 16, stream));
+    TLG_CUDA(cudaMemsetAsync(grad + P_pad, 0, 16, stream));
+    for (int r = 0; r < n; ++r) run_shard(bs[r], on_device, r, r == 0 ? grad : grad_tmp);
     mark(4);
-    // ---- failure guard + allreduce (learner.cpp:138-149)
-    set_guard();
+    // ---- allreduce over ranks (learner.cpp:138-149); the guard slot rides along
     if (nranks > 1) {
       NCCL_CHECK(ncclAllReduce(grad, grad, size_t(P_pad + 4), ncclFloat, ncclSum, comm, stream));
     }
     mark(5);
-    // ---- optimizer (skipped on device when any rank failed)
+    // ---- optimizer (skipped on device when any shard of any rank failed)
     const bool adam = cfg.optimizer == TLG_OPT_ADAM;
     const uint64_t t = adam_t + 1;
     const double bc1 = 1.0 - std::pow(cfg.adam_beta1, double(t));
     const double bc2 = 1.0 - std::pow(cfg.adam_beta2, double(t));
+    grad_scale = 1.f / float(n * nranks);
     launch_guarded_optimizer(adam, float(hp.learning_rate), float(hp.learning_rate / bc1),
                              float(std::sqrt(bc2)));
     mark(6);
     // ---- results
-    TLG_CUDA(cudaMemcpyAsync(h_stats, stats, sizeof(tlg::StepStatsDev), cudaMemcpyDeviceToHost,
-                             stream));
+    TLG_CUDA(cudaMemcpyAsync(h_stats, stats, n * sizeof(tlg::StepStatsDev),
+                             cudaMemcpyDeviceToHost, stream));
     TLG_CUDA(cudaMemcpyAsync(h_flags, err, 4, cudaMemcpyDeviceToHost, stream));
     TLG_CUDA(cudaMemcpyAsync(h_flags + 1, grad + P_pad, 4, cudaMemcpyDeviceToHost, stream));
     TLG_CUDA(cudaStreamSynchronize(stream));
@@ -455,32 +471,48 @@ struct tlg_learner {
     if (e & tlg::kErrActionRange) throw InvalidArg("action out of range");
     if (e & tlg::kErrNonFiniteLogp) throw InvalidArg("non-finite log probability");
     if (e & tlg::kErrNonFiniteAdv) throw InvalidArg("non-finite advantage");
-    if (!std::isfinite(h_stats->loss))
-      throw RuntimeErr("non-finite loss at update step " + std::to_string(k));
+    for (int r = 0; r < n; ++r)
+      if (!std::isfinite(h_stats[r].loss))
+        throw RuntimeErr("non-finite loss at update step " + std::to_string(k));
     if (guard != 0.f)
       throw RuntimeErr("learner shard failed on another rank at update step " + std::to_string(k));
     if (adam) adam_t = t;
     steps_done = k;
     if (out) {
-      out->loss = h_stats->loss;
-      out->clip_fraction = algo == TLG_ALGO_VTRACE ? 0.0 : h_stats->clip;
-      out->mean_ratio = h_stats->ratio;
-      out->entropy = h_stats->entropy;
-      out->value_loss = h_stats->vloss;
-      out->n_samples = uint64_t(h_stats->n);
+      for (int r = 0; r < n; ++r) {
+        const tlg::StepStatsDev& h = h_stats[r];
+        out[r].loss = h.loss;
+        out[r].clip_fraction = cfg.algo == TLG_ALGO_VTRACE ? 0.0 : h.clip;
+        out[r].mean_ratio = h.ratio;
+        out[r].entropy = h.entropy;
+        out[r].value_loss = h.vloss;
+        out[r].n_samples = uint64_t(h.n);
+      }
     }
   }
 
-  void set_guard();
+  void accumulate_grad();
+  void set_guard(int shard);
   void launch_guarded_optimizer(bool adam, float lr, float step_size, float bc2_sqrt);
 };
 
 namespace {
 
+// guard[0] > 0 iff some shard raised an error bit or produced a non-finite loss; it is
+// summed by the allreduce together with the gradient, so every rank agrees to skip.
 __global__ void set_guard_kernel(const int* err, const tlg::StepStatsDev* st, float* guard) {
   const bool bad = (*err != 0) || !isfinite(st->loss);
-  guard[0] = bad ? 1.f : 0.f;
-  guard[1] = guard[2] = guard[3] = 0.f;
+  if (bad) guard[0] = 1.f;
+}
+
+__global__ void accumulate_kernel(float4* __restrict__ g, const float4* __restrict__ t, long n4) {
+  for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n4;
+       i += long(gridDim.x) * blockDim.x) {
+    float4 a = g[i];
+    const float4 b = t[i];
+    a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+    g[i] = a;
+  }
 }
 
 __global__ void optimizer_guarded_kernel(float4* __restrict__ p, float4* __restrict__ plo,
@@ -526,8 +558,17 @@ __global__ void split_lo_flat(const float* x, float* lo, long n) {
 
 }  // namespace
 
-void tlg_learner::set_guard() {
-  set_guard_kernel<<<1, 1, 0, stream>>>(err, stats, grad + P_pad);
+void tlg_learner::set_guard(int shard) {
+  set_guard_kernel<<<1, 1, 0, stream>>>(err, stats + shard, grad + P_pad);
+  TLG_CHECK_LAUNCH();
+  ++launches;
+}
+
+void tlg_learner::accumulate_grad() {
+  const long n4 = P_pad / 4;
+  accumulate_kernel<<<int(std::max<long>(1, std::min<long>((n4 + 255) / 256, 148L * 4))), 256, 0,
+                      stream>>>(reinterpret_cast<float4*>(grad),
+                                reinterpret_cast<const float4*>(grad_tmp), n4);
   TLG_CHECK_LAUNCH();
   ++launches;
 }
@@ -538,7 +579,7 @@ void tlg_learner::launch_guarded_optimizer(bool adam, float lr, float step_size,
   optimizer_guarded_kernel<<<blocks, 256, 0, stream>>>(
       reinterpret_cast<float4*>(params), reinterpret_cast<float4*>(params_lo),
       reinterpret_cast<const float4*>(grad), reinterpret_cast<float4*>(adam_m),
-      reinterpret_cast<float4*>(adam_v), n4, grad + P_pad, 1.f / float(nranks), adam ? 1 : 0, lr,
+      reinterpret_cast<float4*>(adam_v), n4, grad + P_pad, grad_scale, adam ? 1 : 0, lr,
       step_size, bc2_sqrt, float(cfg.adam_beta1), float(cfg.adam_beta2), float(cfg.adam_eps));
   TLG_CHECK_LAUNCH();
   ++launches;
@@ -612,6 +653,19 @@ extern "C" {
 const char* tlg_last_error(void) { return g_err.c_str(); }
 const char* tlg_version(void) { return "tlg_b200 0.1 (sm_100a, tcgen05 3xTF32)"; }
 
+void* tlg_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaMallocHost(&p, bytes ? bytes : 1) != cudaSuccess) {
+    g_err = "cudaMallocHost failed";
+    return nullptr;
+  }
+  return p;
+}
+
+void tlg_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
 int tlg_learner_create(const tlg_learner_config* cfg, const tlg_policy_shape* shape,
                        tlg_learner** out) {
   return Guard([&] {
@@ -653,8 +707,8 @@ int tlg_learner_get_grad(tlg_learner* l, double* values, size_t n) {
     TLG_CUDA(cudaMemcpyAsync(h.data(), l->grad, l->net.P * 4, cudaMemcpyDeviceToHost,
                              l->stream));
     TLG_CUDA(cudaStreamSynchronize(l->stream));
-    const double inv = 1.0 / double(l->nranks);
-    for (long i = 0; i < l->net.P; ++i) values[i] = double(h[i]) * inv;
+    // the summed gradient times 1/(local shards x ranks) of the last step
+    for (long i = 0; i < l->net.P; ++i) values[i] = double(h[i]) * double(l->grad_scale);
   });
 }
 
@@ -716,7 +770,15 @@ int tlg_learner_train_step(tlg_learner* l, const tlg_segment_batch* batch, int o
                            tlg_step_stats* stats) {
   return Guard([&] {
     if (!l || !batch) throw InvalidArg("null argument");
-    l->step(*batch, on_device, stats);
+    l->step(batch, 1, on_device, stats);
+  });
+}
+
+int tlg_learner_train_step_shards(tlg_learner* l, const tlg_segment_batch* shards, int n_shards,
+                                  int on_device, tlg_step_stats* stats) {
+  return Guard([&] {
+    if (!l || !shards) throw InvalidArg("null argument");
+    l->step(shards, n_shards, on_device, stats);
   });
 }
 

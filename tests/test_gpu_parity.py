@@ -291,3 +291,80 @@ def test_policy_forward_matches_oracle_and_is_batch_invariant(tlg, oracle, case)
     assert np.array_equal(v2, v[idx])
     lg3, _, v3 = pol.forward(obs[5:6])
     assert np.array_equal(lg3, lg[5:6]) and np.array_equal(v3, v[5:6])
+
+
+# ---------------------------------------------------------------------------
+# Multi-shard semantics (learner.cpp:117-149): per-shard normalisation and 1/n,
+# rank-ordered sum, 1/num_shards.
+@pytest.mark.parametrize("algo", ["ppo", "vtrace"])
+def test_local_shards_match_oracle(tlg, oracle, algo):
+    S, T, D, A, hidden = 6, 9, 16, 5, (32,)
+    shape = Shape(2, D, A, hidden)
+    hp = dict(learning_rate=0.05, batch_size=S, unroll_len=T)
+    lrn = tlg.Learner("mlp", D, A, hidden, algo=algo, optimizer="sgd", max_segments=S,
+                      unroll_len=T)
+    lrn.set_hyper(**hp)
+    p = init_params(oracle, shape, 21)
+    lrn.set_params(p)
+    for step in range(3):
+        shards = [make_batch(tlg, S, T, D, A, seed=1000 + 10 * step + r) for r in range(3)]
+        sts = lrn.train_step_shards(shards)
+        p_new, g, osts, _ = oracle.learner_step(shape, p, OHyper(**hp), ALGO[algo],
+                                                [to_oracle(b) for b in shards])
+        for st, ost in zip(sts, osts):
+            assert close(st["loss"], ost["loss"], 1e-4)
+        assert close(lrn.get_grad(), g, 1e-4)
+        assert close(lrn.get_params(), p_new, 1e-4), worst(lrn.get_params(), p_new)
+        p = p_new.astype(np.float32).astype(np.float64)
+        lrn.set_params(p)
+
+
+def _golden_batches(g, name, s, B):
+    from paper_2011_12895_b200.synth import SegmentBatch
+    return SegmentBatch(*(g[f"{name}_s{s}_{k}"] for k in (
+        "obs", "action", "reward", "behavior_logp", "value_est", "done", "bootstrap",
+        "valid_steps")))
+
+
+@pytest.mark.parametrize("name", ["tab_ppo", "tab_vtrace", "lin_ppo", "lin_vtrace"])
+def test_gpu_learner_follows_reference_learner_trajectory(tlg, golden, ref, name):
+    """The reference Learner's parameter trajectory (tests/golden/learner.npz, produced by
+    learner::Learner itself) reproduced by the GPU learner consuming the same replay draws
+    (drawn by the reference's own ReplayMem, replay_mem.cpp:28-49)."""
+    from paper_2011_12895_b200.synth import SegmentBatch
+    g = golden("learner")
+    meta = {int(m[0]): m for m in g["meta"]}
+    idx = ["tab_ppo", "tab_vtrace", "lin_ppo", "lin_vtrace"].index(name)
+    _, fam, D, A, T, B, shards, algo, reuse, steps = (int(x) for x in meta[idx])
+    family = ["tabular", "linear"][fam]
+    lrn = tlg.Learner(family, D, A, (), algo=["ppo", "vtrace"][algo], optimizer="sgd",
+                      max_segments=B, unroll_len=T)
+    lrn.set_hyper(learning_rate=0.05, batch_size=B, max_reuse=reuse, unroll_len=T)
+    lrn.set_params(g[f"{name}_p0"])
+    L = ref.L
+    h = L.ref_replay_create(4096, reuse, 99)
+    pending = {}
+    try:
+        for s in range(steps):
+            seg = _golden_batches(g, name, s, B)
+            for i in range(seg.action.shape[0]):
+                seq = s * B * shards + i
+                pending[seq] = seg.slice(i, i + 1)
+                L.ref_replay_push(h, seq, int(seg.valid_steps[i]))
+            o = np.zeros(B * shards, np.uint64)
+            assert L.ref_replay_sample(h, B * shards, o) == 0
+            drawn = [pending[int(q)] for q in o]
+            parts = []
+            for r in range(shards):
+                part = drawn[r * B:(r + 1) * B]
+                parts.append(SegmentBatch(*(np.concatenate([getattr(x, k) for x in part]).astype(
+                    np.float32 if k in ("obs", "reward", "behavior_logp", "value_est", "bootstrap")
+                    else (np.int32 if k in ("action", "valid_steps") else np.uint8)) for k in (
+                    "obs", "action", "reward", "behavior_logp", "value_est", "done", "bootstrap",
+                    "valid_steps"))))
+            lrn.train_step_shards(parts)
+            want = g[f"{name}_p{s + 1}"]
+            got = lrn.get_params()
+            assert close(got, want, 1e-4), (name, s, worst(got, want))
+    finally:
+        L.ref_replay_destroy(h)
