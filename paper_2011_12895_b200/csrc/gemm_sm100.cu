@@ -25,6 +25,23 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // 2D fp32 tensor map, 128-byte swizzle, box {32 (inner), box_rows}.
+// 3D map for the split-K workspace [splits][M][N], box {32, 32, 1}.
+CUtensorMap make_map3(const float* base, long n, long m, long splits) {
+  CUtensorMap t;
+  cuuint64_t dims[3] = {cuuint64_t(n), cuuint64_t(m), cuuint64_t(splits)};
+  cuuint64_t strides[2] = {cuuint64_t(n) * 4, cuuint64_t(n) * m * 4};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  if ((reinterpret_cast<uintptr_t>(base) & 15) != 0 || (n * 4) % 16 != 0)
+    throw CudaError("gemm workspace must be 16-byte aligned with N a multiple of 4");
+  CUresult r = encode_fn()(&t, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled(3d) failed: " + std::to_string(r));
+  return t;
+}
+
 CUtensorMap make_map(const float* base, long inner, long outer, long ld, int box_rows,
                      CUtensorMapSwizzle swz) {
   CUtensorMap m;
@@ -53,40 +70,69 @@ CUtensorMap operand_map(const float* ptr, const Operand& op, long mn, long k, in
   return make_map(ptr, mn, k, op.ld, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
 }
 
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    TLG_CUDA(cudaGetDevice(&dev));
+    TLG_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return n;
+}
+
+struct EpiMaps {
+  CUtensorMap out, out_lo, act;
+};
+
 template <int BN, bool A_MN, bool B_MN, bool A_LO, bool B_LO, int EPI>
 void run(const CUtensorMap& ah, const CUtensorMap& al, const CUtensorMap& bh,
-         const CUtensorMap& bl, const Params& p, dim3 grid, cudaStream_t stream) {
+         const CUtensorMap& bl, const EpiMaps& em, const Params& p, dim3 grid,
+         cudaStream_t stream) {
   auto kern = gemm_tf32x3_kernel<BN, A_MN, B_MN, A_LO, B_LO, EPI>;
-  constexpr int bytes = Smem<BN, A_LO, B_LO>::kBytes;
+  constexpr int bytes = Smem<BN, A_LO, B_LO, EPI>::kBytes;
+  static_assert(bytes <= 227 * 1024, "shared memory budget");
   static bool attr = false;  // one-time per instantiation
   if (!attr) {
     TLG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     attr = true;
   }
-  kern<<<grid, kThreads, bytes, stream>>>(ah, al, bh, bl, p);
+  const TileMap tm{int(grid.x), int(grid.y), int(grid.z)};
+  const int tiles = tm.m_tiles * tm.n_tiles * tm.splits;
+  kern<<<std::min(tiles, num_sms()), kThreads, bytes, stream>>>(ah, al, bh, bl, em.out,
+                                                                 em.out_lo, em.act, p, tm);
   TLG_CHECK_LAUNCH();
+}
+
+template <int BN, bool A_MN, bool B_MN, bool A_LO, bool B_LO, int EPI>
+void run_if_fits(const CUtensorMap& ah, const CUtensorMap& al, const CUtensorMap& bh,
+                 const CUtensorMap& bl, const EpiMaps& em, const Params& p, dim3 grid,
+                 cudaStream_t s) {
+  if constexpr (Smem<BN, A_LO, B_LO, EPI>::kFits)
+    run<BN, A_MN, B_MN, A_LO, B_LO, EPI>(ah, al, bh, bl, em, p, grid, s);
+  else
+    throw CudaError("gemm: tile does not fit shared memory");
 }
 
 template <int BN>
 void dispatch_bn(bool a_mn, bool b_mn, bool a_lo, bool b_lo, int epi, const CUtensorMap& ah,
                  const CUtensorMap& al, const CUtensorMap& bh, const CUtensorMap& bl,
-                 const Params& p, dim3 grid, cudaStream_t s) {
+                 const EpiMaps& em, const Params& p, dim3 grid, cudaStream_t s) {
   // forward: A = activations (K-major), B = W (K-major)
   if (!a_mn && !b_mn && b_lo && epi == kEpiFwdTanh) {
-    if (a_lo) return run<BN, false, false, true, true, kEpiFwdTanh>(ah, al, bh, bl, p, grid, s);
-    return run<BN, false, false, false, true, kEpiFwdTanh>(ah, al, bh, bl, p, grid, s);
+    if (a_lo) return run_if_fits<BN, false, false, true, true, kEpiFwdTanh>(ah, al, bh, bl, em, p, grid, s);
+    return run_if_fits<BN, false, false, false, true, kEpiFwdTanh>(ah, al, bh, bl, em, p, grid, s);
   }
   // dX: A = dZ (K-major), B = W (MN-major)
   if (!a_mn && b_mn && a_lo && b_lo && epi == kEpiBwdTanh)
-    return run<BN, false, true, true, true, kEpiBwdTanh>(ah, al, bh, bl, p, grid, s);
+    return run_if_fits<BN, false, true, true, true, kEpiBwdTanh>(ah, al, bh, bl, em, p, grid, s);
   // dW: A = dZ^T (MN-major), B = H (MN-major), split-K partials
   if (a_mn && b_mn && a_lo && epi == kEpiStore) {
-    if (b_lo) return run<BN, true, true, true, true, kEpiStore>(ah, al, bh, bl, p, grid, s);
-    return run<BN, true, true, true, false, kEpiStore>(ah, al, bh, bl, p, grid, s);
+    if (b_lo) return run_if_fits<BN, true, true, true, true, kEpiStore>(ah, al, bh, bl, em, p, grid, s);
+    return run_if_fits<BN, true, true, true, false, kEpiStore>(ah, al, bh, bl, em, p, grid, s);
   }
   // generic K-major store (used by the testkit)
   if (!a_mn && !b_mn && a_lo && b_lo && epi == kEpiStore)
-    return run<BN, false, false, true, true, kEpiStore>(ah, al, bh, bl, p, grid, s);
+    return run_if_fits<BN, false, false, true, true, kEpiStore>(ah, al, bh, bl, em, p, grid, s);
   throw CudaError("gemm: unsupported operand/epilogue combination");
 }
 
@@ -100,10 +146,19 @@ int pick_splits(int M, int N, int K, int max_splits) {
   return s;
 }
 
-void launch(const Operand& A, const Operand& B, int M, int N, int K, int epi, Params p,
-            int splits, cudaStream_t stream) {
+int launch(const Operand& A, const Operand& B, int M, int N, int K, int epi, Params p,
+           int splits, cudaStream_t stream) {
   if (M <= 0 || N <= 0 || K <= 0) throw CudaError("gemm: empty problem");
-  const int BN = N > 128 ? 256 : N > 64 ? 128 : 64;
+  int BN = N > 128 ? 256 : N > 64 ? 128 : 64;
+  // widest tile whose pipeline (>= 2 stages) + epilogue staging fits 227 KB
+  const bool a_lo0 = A.lo != nullptr, b_lo0 = B.lo != nullptr;
+  auto fits = [&](int bn) {
+    const int stage = kBM * kBK * 4 * (a_lo0 ? 2 : 1) + bn * kBK * 4 * (b_lo0 ? 2 : 1);
+    const int blocks = epi == kEpiStore ? 1 : epi == kEpiBwdTanh ? 3 : 2;
+    const int epib = 4 * blocks * 4096 + (epi == kEpiBwdTanh ? 4 * bn * 4 : 0);
+    return 2 * stage + 2048 + epib + 1024 <= 227 * 1024;
+  };
+  while (BN > 64 && !fits(BN)) BN /= 2;
   const int kb_total = ceil_div(K, kBK);
   if (splits < 1) splits = 1;
   if (epi != kEpiStore) splits = 1;
@@ -118,11 +173,22 @@ void launch(const Operand& A, const Operand& B, int M, int N, int K, int epi, Pa
   const CUtensorMap bl = operand_map(B.lo, B, N, K, BN);
   dim3 grid(ceil_div(M, kBM), ceil_div(N, BN), splits);
   const bool a_lo = A.lo != nullptr, b_lo = B.lo != nullptr;
-  switch (BN) {
-    case 256: return dispatch_bn<256>(A.mn_major, B.mn_major, a_lo, b_lo, epi, ah, al, bh, bl, p, grid, stream);
-    case 128: return dispatch_bn<128>(A.mn_major, B.mn_major, a_lo, b_lo, epi, ah, al, bh, bl, p, grid, stream);
-    default: return dispatch_bn<64>(A.mn_major, B.mn_major, a_lo, b_lo, epi, ah, al, bh, bl, p, grid, stream);
+  // epilogue maps: 32x32 fp32 blocks with the 128-B swizzle
+  EpiMaps em;
+  std::memset(&em, 0, sizeof(em));
+  if (epi == kEpiStore) {
+    em.out = make_map3(p.ws, N, M, splits);
+  } else {
+    em.out = make_map(p.out_hi, N, M, p.ldo, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+    em.out_lo = make_map(p.out_lo, N, M, p.ldo, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (epi == kEpiBwdTanh) em.act = make_map(p.act_hi, N, M, p.ld_act, 32, CU_TENSOR_MAP_SWIZZLE_128B);
   }
+  switch (BN) {
+    case 256: dispatch_bn<256>(A.mn_major, B.mn_major, a_lo, b_lo, epi, ah, al, bh, bl, em, p, grid, stream); break;
+    case 128: dispatch_bn<128>(A.mn_major, B.mn_major, a_lo, b_lo, epi, ah, al, bh, bl, em, p, grid, stream); break;
+    default: dispatch_bn<64>(A.mn_major, B.mn_major, a_lo, b_lo, epi, ah, al, bh, bl, em, p, grid, stream); break;
+  }
+  return BN;
 }
 
 }  // namespace tlg::gemm

@@ -13,12 +13,14 @@
 // transposes are ever materialised (the backward dW = dZ^T . H and
 // dX = dZ . W GEMMs read the forward's buffers in place).
 //
-// Warp roles (192 threads, one output tile of 128 x BN per CTA):
+// Persistent CTAs (one per SM), 192 threads, 128 x BN output tiles:
 //   warp 0      TMA producer (one elected lane), smem ring of STAGES stages
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 2..5  epilogue: tcgen05.ld TMEM -> registers -> fused op -> global
+//   warps 2..5  epilogue: tcgen05.ld TMEM -> registers -> fused op -> smem transpose ->
+//               coalesced 128-B row stores (+ fused per-tile column sums for dZ)
 // Pipelines: full[s] (TMA -> MMA, tx-count), empty[s] (tcgen05.commit -> TMA),
-// tmem_full (final commit -> epilogue).
+// tmem_full[2] / tmem_empty[2] (double-buffered accumulators: the epilogue of tile i
+// overlaps the MMAs of tile i+1).
 #pragma once
 
 #include "common.cuh"
@@ -47,6 +49,13 @@ struct Params {
   long ld_act;
   float* ws;
   long ws_split_stride;
+  float* colsum;  // kEpiBwdTanh: optional per-M-tile column sums [M/128][N] of the output
+  // kEpiFwdTanh on the last trunk layer: fused policy/value head partial dot products
+  //   head_part[n_tile][m][k] = sum_{n in tile} Whead[k][n] * out[m][n], k < head_k
+  const float* head_w;   // W_pi [head_k - 1][N] row-major
+  const float* head_wv;  // w_v [N]
+  int head_k;            // n_actions + 1 (<= 8), 0 = no fused head
+  float* head_part;
 };
 
 // ---------------------------------------------------------------------------
@@ -158,42 +167,103 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 #undef TLG_R32
 
 // ---------------------------------------------------------------------------
-template <int BN, bool A_LO, bool B_LO>
+constexpr int kEpiWarps = 4;
+constexpr int kStageBuf = 32 * 33;  // per-warp 32x32 transpose buffer (+1 pad: no bank conflicts)
+
+template <int BN, bool A_LO, bool B_LO, int EPI>
 struct Smem {
   static constexpr int kA = kBM * kBK * 4;  // 16 KB
   static constexpr int kB = BN * kBK * 4;
   static constexpr int kStage = kA * (A_LO ? 2 : 1) + kB * (B_LO ? 2 : 1);
-  static constexpr int kStages = (200 * 1024 / kStage) < 2 ? 2
-                                 : (200 * 1024 / kStage) > 6 ? 6
-                                                             : (200 * 1024 / kStage);
+  // per epilogue warp, 4 KB each: out (+ out_lo unless split-K store) (+ act for bwd)
+  static constexpr int kEpiBlocks = EPI == kEpiStore ? 1 : EPI == kEpiBwdTanh ? 3 : 2;
+  static constexpr int kEpiBytes =
+      kEpiWarps * kEpiBlocks * 4096 + (EPI == kEpiBwdTanh ? kEpiWarps * BN * 4 : 0);
+  static constexpr int kBudget = 225 * 1024 - kEpiBytes - 1024 - 256;
+  static constexpr int kStages = (kBudget / kStage) < 2 ? 2 : (kBudget / kStage) > 8 ? 8 : (kBudget / kStage);
   static constexpr int kBarOff = kStages * kStage;
-  static constexpr int kBytes = kBarOff + (2 * kStages + 2) * 8 + 16 + 1024;  // + align slack
-  static constexpr int kTmemCols = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+  // full/empty per stage, tmem full/empty x2, act-block full x4
+  static constexpr int kNumBars = 2 * kStages + 4 + kEpiWarps;
+  static constexpr int kEpiOff = (kBarOff + kNumBars * 8 + 16 + 1023) / 1024 * 1024;
+  static constexpr int kBytes = kEpiOff + kEpiBytes + 1024;  // + 1 KB alignment slack
+  static constexpr bool kFits = kBytes <= 227 * 1024;
+  static constexpr int kAccCols = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+  static constexpr int kTmemCols = 2 * kAccCols;  // double-buffered accumulators
 };
+
+struct TileMap {
+  int m_tiles, n_tiles, splits;
+  __device__ __forceinline__ void decode(int t, int& m, int& n, int& s) const {
+    n = t % n_tiles;  // n fastest: the N-tiles of one M row run together (A re-read hits L2)
+    const int r = t / n_tiles;
+    m = r % m_tiles;
+    s = r / m_tiles;
+  }
+};
+
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+// Persistent, warp-specialised: CTA b processes tiles b, b + grid, ...  The MMA warp
+// accumulates tile i into TMEM buffer (i & 1) while the epilogue drains tile i-1.
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int x, int y, uint32_t src) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(x), "r"(y), "r"(src)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, int x, int y, int z,
+                                             uint32_t src) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(x), "r"(y), "r"(z), "r"(src)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// byte offset of element (row r, col c) in a 32x32 fp32 block with the 128-B TMA swizzle
+__device__ __forceinline__ uint32_t swz(int r, int c4) { return uint32_t(r * 128 + ((c4 ^ (r & 7)) << 4)); }
 
 template <int BN, bool A_MN, bool B_MN, bool A_LO, bool B_LO, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap tmA_hi,
                        const __grid_constant__ CUtensorMap tmA_lo,
                        const __grid_constant__ CUtensorMap tmB_hi,
-                       const __grid_constant__ CUtensorMap tmB_lo, const Params p) {
-  using S = Smem<BN, A_LO, B_LO>;
+                       const __grid_constant__ CUtensorMap tmB_lo,
+                       const __grid_constant__ CUtensorMap tmOut,
+                       const __grid_constant__ CUtensorMap tmOutLo,
+                       const __grid_constant__ CUtensorMap tmAct, const Params p,
+                       const TileMap tm) {
+  using S = Smem<BN, A_LO, B_LO, EPI>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
   const uint32_t bar_full = sbase + S::kBarOff;
   const uint32_t bar_empty = bar_full + S::kStages * 8;
-  const uint32_t bar_tmem = bar_empty + S::kStages * 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + S::kBarOff + (2 * S::kStages + 2) * 8);
+  const uint32_t bar_tfull = bar_empty + S::kStages * 8;  // [2]
+  const uint32_t bar_tempty = bar_tfull + 16;               // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + S::kBarOff + S::kNumBars * 8);
+  const uint32_t bar_act = bar_tempty + 16;                 // [4]
+  float* colpart = reinterpret_cast<float*>(smem + S::kEpiOff + kEpiWarps * S::kEpiBlocks * 4096);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * kBM;
-  const int n0 = blockIdx.y * BN;
+  const int num_tiles = tm.m_tiles * tm.n_tiles * tm.splits;
   const int kb_total = (p.K + kBK - 1) / kBK;
-  const int kb_begin = blockIdx.z * p.kb_per_split;
-  const int kb_end = min(kb_total, kb_begin + p.kb_per_split);
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA_hi);
@@ -204,7 +274,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(bar_full + 8 * s, 1);
       mbar_init(bar_empty + 8 * s, 1);
     }
-    mbar_init(bar_tmem, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(bar_tfull + 8 * a, 1);
+      mbar_init(bar_tempty + 8 * a, kEpiWarps);
+    }
+    for (int w = 0; w < kEpiWarps; ++w) mbar_init(bar_act + 8 * w, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -223,39 +297,43 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ===== TMA producer =====
       int stage = 0;
       uint32_t phase = 0;
-      for (int kb = kb_begin; kb < kb_end; ++kb) {
-        mbar_wait(bar_empty + 8 * stage, phase ^ 1);
-        const uint32_t st = sbase + stage * S::kStage;
-        const uint32_t full = bar_full + 8 * stage;
-        mbar_expect_tx(full, S::kStage);
-        const int k0 = kb * kBK;
-        uint32_t off = st;
-        // A tile: 128 rows (M) x 32 (K)
-        if (!A_MN) {
-          tma_load_2d(off, &tmA_hi, k0, m0, full);
-          if (A_LO) tma_load_2d(off + S::kA, &tmA_lo, k0, m0, full);
-        } else {
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int mt, nt, sp;
+        tm.decode(t, mt, nt, sp);
+        const int m0 = mt * kBM, n0 = nt * BN;
+        const int kb0 = sp * p.kb_per_split, kb1 = min(kb_total, kb0 + p.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(bar_empty + 8 * stage, phase ^ 1);
+          const uint32_t st = sbase + stage * S::kStage;
+          const uint32_t full = bar_full + 8 * stage;
+          mbar_expect_tx(full, S::kStage);
+          const int k0 = kb * kBK;
+          uint32_t off = st;
+          if (!A_MN) {
+            tma_load_2d(off, &tmA_hi, k0, m0, full);
+            if (A_LO) tma_load_2d(off + S::kA, &tmA_lo, k0, m0, full);
+          } else {
 #pragma unroll
-          for (int j = 0; j < kBM / 32; ++j) {
-            tma_load_2d(off + j * 4096, &tmA_hi, m0 + 32 * j, k0, full);
-            if (A_LO) tma_load_2d(off + S::kA + j * 4096, &tmA_lo, m0 + 32 * j, k0, full);
+            for (int j = 0; j < kBM / 32; ++j) {
+              tma_load_2d(off + j * 4096, &tmA_hi, m0 + 32 * j, k0, full);
+              if (A_LO) tma_load_2d(off + S::kA + j * 4096, &tmA_lo, m0 + 32 * j, k0, full);
+            }
           }
-        }
-        off += S::kA * (A_LO ? 2 : 1);
-        // B tile: BN rows (N) x 32 (K)
-        if (!B_MN) {
-          tma_load_2d(off, &tmB_hi, k0, n0, full);
-          if (B_LO) tma_load_2d(off + S::kB, &tmB_lo, k0, n0, full);
-        } else {
+          off += S::kA * (A_LO ? 2 : 1);
+          if (!B_MN) {
+            tma_load_2d(off, &tmB_hi, k0, n0, full);
+            if (B_LO) tma_load_2d(off + S::kB, &tmB_lo, k0, n0, full);
+          } else {
 #pragma unroll
-          for (int j = 0; j < BN / 32; ++j) {
-            tma_load_2d(off + j * 4096, &tmB_hi, n0 + 32 * j, k0, full);
-            if (B_LO) tma_load_2d(off + S::kB + j * 4096, &tmB_lo, n0 + 32 * j, k0, full);
+            for (int j = 0; j < BN / 32; ++j) {
+              tma_load_2d(off + j * 4096, &tmB_hi, n0 + 32 * j, k0, full);
+              if (B_LO) tma_load_2d(off + S::kB + j * 4096, &tmB_lo, n0 + 32 * j, k0, full);
+            }
           }
-        }
-        if (++stage == S::kStages) {
-          stage = 0;
-          phase ^= 1;
+          if (++stage == S::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
       }
     }
@@ -265,101 +343,192 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t idesc = make_idesc<BN, A_MN, B_MN>();
       int stage = 0;
       uint32_t phase = 0;
-      for (int kb = kb_begin; kb < kb_end; ++kb) {
-        mbar_wait(bar_full + 8 * stage, phase);
+      int it = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+        int mt, nt, sp;
+        tm.decode(t, mt, nt, sp);
+        const int kb0 = sp * p.kb_per_split, kb1 = min(kb_total, kb0 + p.kb_per_split);
+        const int acc_buf = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(bar_tempty + 8 * acc_buf, acc_phase ^ 1);  // epilogue drained this buffer
         tc_fence_after();
-        const uint32_t a_hi = sbase + stage * S::kStage;
-        const uint32_t a_lo = a_hi + S::kA;
-        const uint32_t b_hi = a_hi + S::kA * (A_LO ? 2 : 1);
-        const uint32_t b_lo = b_hi + S::kB;
+        const uint32_t tmem_d = tmem_base + uint32_t(acc_buf * S::kAccCols);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(bar_full + 8 * stage, phase);
+          tc_fence_after();
+          const uint32_t a_hi = sbase + stage * S::kStage;
+          const uint32_t a_lo = a_hi + S::kA;
+          const uint32_t b_hi = a_hi + S::kA * (A_LO ? 2 : 1);
+          const uint32_t b_lo = b_hi + S::kB;
 #pragma unroll
-        for (int k = 0; k < kBK / 8; ++k) {
-          // K-major: +32 B per 8-element K step inside the 128-B swizzle row;
-          //   SBO = 1 KB between 8-row (MN) atoms.
-          // MN-major: +1 KB per 8 K rows (128 B each); SBO = 512 B between the
-          //   4-row swizzle atoms along K, LBO = 4 KB between 32-element MN chunks.
-          const uint32_t ao = A_MN ? k * 1024 : k * 32;
-          const uint32_t bo = B_MN ? k * 1024 : k * 32;
-          const uint32_t albo = A_MN ? 4096 : 16, asbo = A_MN ? 512 : 1024;
-          const uint32_t blbo = B_MN ? 4096 : 16, bsbo = B_MN ? 512 : 1024;
-          const uint64_t dah = make_sdesc<A_MN>(a_hi + ao, albo, asbo);
-          const uint64_t dbh = make_sdesc<B_MN>(b_hi + bo, blbo, bsbo);
-          const uint32_t acc = (kb > kb_begin || k > 0) ? 1u : 0u;
-          if (B_LO) mma_tf32(tmem_base, dah, make_sdesc<B_MN>(b_lo + bo, blbo, bsbo), idesc, acc);
-          if (A_LO)
-            mma_tf32(tmem_base, make_sdesc<A_MN>(a_lo + ao, albo, asbo), dbh, idesc,
-                     (B_LO || acc) ? 1u : 0u);
-          mma_tf32(tmem_base, dah, dbh, idesc, (A_LO || B_LO || acc) ? 1u : 0u);
+          for (int k = 0; k < kBK / 8; ++k) {
+            // K-major: +32 B per 8-element K step inside the 128-B swizzle row;
+            //   SBO = 1 KB between 8-row (MN) atoms.
+            // MN-major: +1 KB per 8 K rows (128 B each); SBO = 512 B between the
+            //   4-row swizzle atoms along K, LBO = 4 KB between 32-element MN chunks.
+            const uint32_t ao = A_MN ? k * 1024 : k * 32;
+            const uint32_t bo = B_MN ? k * 1024 : k * 32;
+            const uint32_t albo = A_MN ? 4096 : 16, asbo = A_MN ? 512 : 1024;
+            const uint32_t blbo = B_MN ? 4096 : 16, bsbo = B_MN ? 512 : 1024;
+            const uint64_t dah = make_sdesc<A_MN>(a_hi + ao, albo, asbo);
+            const uint64_t dbh = make_sdesc<B_MN>(b_hi + bo, blbo, bsbo);
+            const uint32_t acc = (kb > kb0 || k > 0) ? 1u : 0u;
+            if (B_LO) mma_tf32(tmem_d, dah, make_sdesc<B_MN>(b_lo + bo, blbo, bsbo), idesc, acc);
+            if (A_LO)
+              mma_tf32(tmem_d, make_sdesc<A_MN>(a_lo + ao, albo, asbo), dbh, idesc,
+                       (B_LO || acc) ? 1u : 0u);
+            mma_tf32(tmem_d, dah, dbh, idesc, (A_LO || B_LO || acc) ? 1u : 0u);
+          }
+          mma_commit(bar_empty + 8 * stage);
+          if (++stage == S::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
-        mma_commit(bar_empty + 8 * stage);
-        if (++stage == S::kStages) {
-          stage = 0;
-          phase ^= 1;
-        }
+        mma_commit(bar_tfull + 8 * acc_buf);
       }
-      mma_commit(bar_tmem);
     }
   } else {
-    // ===== Epilogue: warps 2..5 cover TMEM lane quadrants (warp % 4) =====
+    // ===== Epilogue: warps 2..5 own TMEM lane quadrants (warp % 4) =====
+    // Per 32-column chunk each warp handles a 32x32 block: TMEM -> registers (thread =
+    // row) -> fused op -> 128-B-swizzled smem staging -> TMA bulk store.  The bwd
+    // activation block is TMA-prefetched one chunk ahead into its own swizzled buffer.
     const int q = warp & 3;
-    const int row = m0 + q * 32 + lane;
-    mbar_wait(bar_tmem, 0);
-    tc_fence_after();
-    const bool row_ok = row < p.M;
-#pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
-      uint32_t r[32];
-      tmem_ld32(tmem_base + (uint32_t(q * 32) << 16) + uint32_t(c), r);
-      const int nb = n0 + c;
-      if (!row_ok || nb >= p.N) continue;
-      const int ncols = min(32, p.N - nb);
-      if (EPI == kEpiStore) {
-        float* dst = p.ws + long(blockIdx.z) * p.ws_split_stride + long(row) * p.N + nb;
-        if (ncols == 32 && (p.N & 3) == 0) {
+    const int ew = warp - 2;
+    const uint32_t blk = sbase + S::kEpiOff + uint32_t(ew * S::kEpiBlocks * 4096);
+    const uint32_t st_out = blk, st_lo = blk + 4096, st_act = blk + 8192;
+    uint8_t* blk_ptr = smem + S::kEpiOff + ew * S::kEpiBlocks * 4096;
+    float* cpart = colpart + q * BN;
+    const uint32_t abar = bar_act + 8 * ew;
+    uint32_t act_phase = 0;
+    // the (tile, chunk) sequence this warp walks, for the act prefetch
+    auto act_issue = [&](int t, int c) {
+      if (EPI != kEpiBwdTanh || t >= num_tiles) return;
+      int mt2, nt2, sp2;
+      tm.decode(t, mt2, nt2, sp2);
+      if (lane == 0) {
+        mbar_expect_tx(abar, 4096);
+        tma_load_2d(st_act, &tmAct, nt2 * BN + c, mt2 * kBM + q * 32, abar);
+      }
+    };
+    act_issue(blockIdx.x, 0);
+    constexpr int kHK = 8;  // fused head width limit (n_actions + 1)
+    const bool do_head = EPI == kEpiFwdTanh && p.head_k > 0;
+    int it = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+      int mt, nt, sp;
+      tm.decode(t, mt, nt, sp);
+      const int m0 = mt * kBM, n0 = nt * BN;
+      const int rbase = m0 + q * 32;  // first row of this warp's 32-row slab
+      const int acc_buf = it & 1;
+      mbar_wait(bar_tfull + 8 * acc_buf, (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + uint32_t(acc_buf * S::kAccCols) + (uint32_t(q * 32) << 16);
+      float zacc[kHK];
 #pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            *reinterpret_cast<float4*>(dst + j) =
-                make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
-                            __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
-        } else {
-          for (int j = 0; j < ncols; ++j) dst[j] = __uint_as_float(r[j]);
+      for (int k = 0; k < kHK; ++k) zacc[k] = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        const int nb = n0 + c;
+        float h[32];
+        if (EPI == kEpiBwdTanh) {
+          mbar_wait(abar, act_phase);
+          act_phase ^= 1;
+#pragma unroll
+          for (int j4 = 0; j4 < 8; ++j4) {
+            const float4 v = *reinterpret_cast<const float4*>(blk_ptr + 8192 + swz(lane, j4));
+            h[4 * j4] = v.x; h[4 * j4 + 1] = v.y; h[4 * j4 + 2] = v.z; h[4 * j4 + 3] = v.w;
+          }
+          __syncwarp();
+          if (c + 32 < BN) act_issue(t, c + 32);
+          else act_issue(t + gridDim.x, 0);
         }
-      } else {
-        // out = full fp32 value (the tensor core truncates it to tf32 itself when it is
-        // consumed as the next GEMM's "hi" operand); out_lo = exact residual.
-        float* dhi = p.out_hi + long(row) * p.ldo + nb;
-        float* dlo = p.out_lo + long(row) * p.ldo + nb;
+        uint32_t r[32];
+        tmem_ld32(tbase + uint32_t(c), r);
         float o[32];
         if (EPI == kEpiFwdTanh) {
+          const float bl = (nb + lane < p.N) ? __ldg(p.bias + nb + lane) : 0.f;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float b = (j < ncols) ? __ldg(p.bias + nb + j) : 0.f;
-            o[j] = tanhf(__uint_as_float(r[j]) + b);
+          for (int j = 0; j < 32; ++j)
+            o[j] = tanhf(__uint_as_float(r[j]) + __shfl_sync(0xffffffffu, bl, j));
+          if (do_head) {
+            // lane j holds Whead[k][nb + j]; broadcast column j to every row-thread
+#pragma unroll
+            for (int k = 0; k < kHK; ++k) {
+              if (k < p.head_k) {
+                const float* wrow = k < p.head_k - 1 ? p.head_w + long(k) * p.N : p.head_wv;
+                const float wk = (nb + lane < p.N) ? __ldg(wrow + nb + lane) : 0.f;
+                float z = zacc[k];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) z = fmaf(__shfl_sync(0xffffffffu, wk, j), o[j], z);
+                zacc[k] = z;
+              }
+            }
           }
+        } else if (EPI == kEpiBwdTanh) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) o[j] = __uint_as_float(r[j]) * (1.f - h[j] * h[j]);
         } else {
-          const float* ah = p.act_hi + long(row) * p.ld_act + nb;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float h = (j < ncols) ? __ldg(ah + j) : 0.f;
-            o[j] = __uint_as_float(r[j]) * (1.f - h * h);
-          }
+          for (int j = 0; j < 32; ++j) o[j] = __uint_as_float(r[j]);
         }
-        if (ncols == 32 && (p.ldo & 3) == 0) {
+        // staging buffers are free once the previous chunk's bulk store has read them
+        if (lane == 0) bulk_wait_read();
+        __syncwarp();
 #pragma unroll
-          for (int j = 0; j < 32; j += 4) {
-            *reinterpret_cast<float4*>(dhi + j) = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
-            *reinterpret_cast<float4*>(dlo + j) =
-                make_float4(o[j] - tf32_hi(o[j]), o[j + 1] - tf32_hi(o[j + 1]),
-                            o[j + 2] - tf32_hi(o[j + 2]), o[j + 3] - tf32_hi(o[j + 3]));
+        for (int j4 = 0; j4 < 8; ++j4) {
+          *reinterpret_cast<float4*>(blk_ptr + swz(lane, j4)) =
+              make_float4(o[4 * j4], o[4 * j4 + 1], o[4 * j4 + 2], o[4 * j4 + 3]);
+          if (EPI != kEpiStore)
+            *reinterpret_cast<float4*>(blk_ptr + 4096 + swz(lane, j4)) =
+                make_float4(o[4 * j4] - tf32_hi(o[4 * j4]), o[4 * j4 + 1] - tf32_hi(o[4 * j4 + 1]),
+                            o[4 * j4 + 2] - tf32_hi(o[4 * j4 + 2]),
+                            o[4 * j4 + 3] - tf32_hi(o[4 * j4 + 3]));
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          if (EPI == kEpiStore) {
+            tma_store_3d(&tmOut, nb, rbase, sp, st_out);
+          } else {
+            tma_store_2d(&tmOut, nb, rbase, st_out);
+            tma_store_2d(&tmOutLo, nb, rbase, st_lo);
           }
-        } else {
-          for (int j = 0; j < ncols; ++j) {
-            dhi[j] = o[j];
-            dlo[j] = o[j] - tf32_hi(o[j]);
-          }
+          bulk_commit();
+        }
+        if (EPI == kEpiBwdTanh) {
+          // column sums of this warp's 32 rows (rows past M are exact zeros)
+          float csum = 0.f;
+#pragma unroll 8
+          for (int rr = 0; rr < 32; ++rr)
+            csum += *reinterpret_cast<const float*>(blk_ptr + swz(rr, lane >> 2) + (lane & 3) * 4);
+          cpart[c + lane] = csum;
         }
       }
+      // TMEM buffer drained: hand it back to the MMA warp
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_tempty + 8 * acc_buf);
+      if (do_head && rbase + lane < p.M) {
+        float* hp = p.head_part + (long(nt) * p.M + rbase + lane) * p.head_k;
+#pragma unroll
+        for (int k = 0; k < kHK; ++k)
+          if (k < p.head_k) hp[k] = zacc[k];
+      }
+      if (EPI == kEpiBwdTanh && p.colsum != nullptr) {
+        // fixed-order sum of the 4 warps' column partials -> colsum[m_tile][n]
+        named_bar(1, kEpiWarps * 32);
+        const int tid = threadIdx.x - 64;
+        for (int cidx = tid; cidx < BN; cidx += kEpiWarps * 32) {
+          const int n = n0 + cidx;
+          if (n < p.N)
+            p.colsum[long(mt) * p.N + n] = colpart[cidx] + colpart[BN + cidx] +
+                                           colpart[2 * BN + cidx] + colpart[3 * BN + cidx];
+        }
+        named_bar(1, kEpiWarps * 32);
+      }
     }
+    if (lane == 0) bulk_wait_all();
   }
 
   tc_fence_before();
@@ -381,8 +550,9 @@ struct Operand {
 };
 
 // Launch C = A . B^T with the given epilogue on `stream`.  splits > 1 only for
-// kEpiStore (partials into p.ws).  Throws tlg::CudaError on misuse.
-void launch(const Operand& A, const Operand& B, int M, int N, int K, int epi, Params p,
+// kEpiStore (partials into p.ws).  Returns the N tile width used (the fused head writes
+// ceil(N / BN) partial rows).  Throws tlg::CudaError on misuse.
+int launch(const Operand& A, const Operand& B, int M, int N, int K, int epi, Params p,
             int splits, cudaStream_t stream);
 
 // Number of K splits that fills the GPU for a (M, N, K) problem, given a cap.

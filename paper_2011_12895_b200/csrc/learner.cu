@@ -163,7 +163,7 @@ struct tlg_learner {
   int32_t* valid;
   // activations
   std::vector<float*> act, act_lo, dz, dz_lo;
-  float *head_out, *tlogp, *adv, *target;
+  float *head_out, *head_part, *tlogp, *adv, *target;
   double* seg_partial;
   tlg::StepStatsDev* stats;
   int* err;
@@ -223,6 +223,7 @@ struct tlg_learner {
     }
     const int A1 = int(net.A) + 1;
     head_out = mem.add<float>(F_max * A1);
+    head_part = mem.add<float>(F_max * A1 * ((net.head.H + 63) / 64));
     tlogp = mem.add<float>(F_max);
     adv = mem.add<float>(F_max);
     target = mem.add<float>(F_max);
@@ -241,7 +242,8 @@ struct tlg_learner {
       max_cols = std::max<long>(max_cols, out);
     }
     ws = ws_elems ? mem.add<float>(ws_elems) : nullptr;
-    col_partial = mem.add<float>(((F_max + 255) / 256) * max_cols);
+    col_partial = mem.add<float>(((F_max + tlg::kLossFrames - 1) / tlg::kLossFrames + 1) *
+                                 std::max<long>(max_cols, net.head.H));
     TLG_CUDA(cudaMallocHost(&h_stats, kMaxLocalShards * sizeof(tlg::StepStatsDev)));
     TLG_CUDA(cudaMallocHost(&h_flags, 16));
     for (auto& e : ev) TLG_CUDA(cudaEventCreate(&e));
@@ -361,17 +363,30 @@ struct tlg_learner {
       p.out_lo = act_lo[l];
       p.ldo = outw;
       p.bias = params + net.b_off[l];
+      const bool fuse_head = l + 1 == net.L && fused_head();
+      if (fuse_head) {  // policy/value heads in the last trunk GEMM's epilogue
+        p.head_w = params + net.head.wpi;
+        p.head_wv = params + net.head.wv;
+        p.head_k = int(net.A) + 1;
+        p.head_part = head_part;
+      }
       if (shard == 0) kmark(0, int(l), 0);
-      tlg::gemm::launch(A, B, int(F), outw, in, tlg::gemm::kEpiFwdTanh, p, 1, stream);
+      const int bn = tlg::gemm::launch(A, B, int(F), outw, in, tlg::gemm::kEpiFwdTanh, p, 1,
+                                       stream);
       if (shard == 0) kmark(0, int(l), 1);
+      if (fuse_head) head_tiles = (outw + bn - 1) / bn;
       ++launches;
     }
     if (shard == 0) mark(2);
     // ---- heads, returns, loss
     const float* hL = net.L ? act[net.L - 1] : x0;
     const long ldh = net.head.H;
-    tlg::launch_head_forward(net.head, params, hL, ldh, &bd, F, head_out, tlogp, nullptr, err,
-                             stream);
+    if (net.L > 0 && fused_head())
+      tlg::launch_head_finalize(net.head, params, head_part, head_tiles, F, &bd, head_out, tlogp,
+                                nullptr, nullptr, nullptr, err, stream);
+    else
+      tlg::launch_head_forward(net.head, params, hL, ldh, &bd, F, head_out, tlogp, nullptr, err,
+                               stream);
     tlg::HyperDev hd{float(hp.gamma), float(hp.lam), float(hp.clip_eps), float(hp.vf_coef),
                      float(hp.ent_coef), float(hp.rho_bar), float(hp.c_bar), hp.adv_norm};
     const int algo = int(cfg.algo);
@@ -381,9 +396,14 @@ struct tlg_learner {
     const int nblk = tlg::launch_loss_backward(
         net.head, params, hL, ldh, bd, head_out, adv, target, st, hd, loss_kind,
         net.L ? dz[net.L - 1] : nullptr, net.L ? dz_lo[net.L - 1] : nullptr, hg_partial,
-        loss_partial, stream);
+        loss_partial, col_partial, stream);
     tlg::launch_head_grad_reduce(net.head, hg_partial, loss_partial, nblk, gtarget, st, stream);
-    launches += 5;
+    launches += 6;
+    if (net.L > 0) {  // db of the top trunk layer from the loss kernel's column partials
+      tlg::launch_rows_reduce(col_partial, nblk, net.head.H, net.head.H,
+                              gtarget + net.b_off[net.L - 1], stream);
+      ++launches;
+    }
     if (shard == 0) mark(3);
     // ---- backward trunk
     for (int l = int(net.L) - 1; l >= 0; --l) {
@@ -405,9 +425,14 @@ struct tlg_learner {
       tlg::gemm::launch(A, B, outw, in, int(F), tlg::gemm::kEpiStore, p, sp, stream);
       if (shard == 0) kmark(1, l, 1);
       tlg::launch_dw_reduce(ws, sp_eff, long(outw) * in, gtarget + net.w_off[l], stream);
-      // db_l = column sums of dZ_l
-      tlg::launch_colsum(dz[l], outw, F, outw, col_partial, gtarget + net.b_off[l], stream);
-      launches += 4;
+      // db_l = column sums of dZ_l, from the per-M-tile partials the dX epilogue of
+      // layer l+1 wrote (the top layer's came from the loss kernel)
+      if (l < int(net.L) - 1) {
+        const int m_tiles = int((F + tlg::gemm::kBM - 1) / tlg::gemm::kBM);
+        tlg::launch_rows_reduce(col_partial, m_tiles, outw, outw, gtarget + net.b_off[l], stream);
+        ++launches;
+      }
+      launches += 2;
       if (l > 0) {
         // dZ_{l-1} = (dZ_l . W_l) * (1 - X_{l-1}^2)
         Operand A2{dz[l], dz_lo[l], outw, false};
@@ -418,6 +443,7 @@ struct tlg_learner {
         p2.ldo = in;
         p2.act_hi = act[l - 1];
         p2.ld_act = in;
+        p2.colsum = col_partial;
         if (shard == 0) kmark(2, l, 0);
         tlg::gemm::launch(A2, B2, int(F), in, outw, tlg::gemm::kEpiBwdTanh, p2, 1, stream);
         if (shard == 0) kmark(2, l, 1);
@@ -492,6 +518,8 @@ struct tlg_learner {
   }
 
   void accumulate_grad();
+  bool fused_head() const { return net.A + 1 <= 8; }
+  int head_tiles = 1;
   void set_guard(int shard);
   void launch_guarded_optimizer(bool adam, float lr, float step_size, float bc2_sqrt);
 };
@@ -592,10 +620,11 @@ struct tlg_policy {
   long max_batch;
   cudaStream_t stream = nullptr;
   DevFree mem;
-  float *params, *params_lo, *obs, *obs_lo, *head_out, *logits, *probs, *value;
+  float *params, *params_lo, *obs, *obs_lo, *head_out, *head_part, *logits, *probs, *value;
   std::vector<float*> act, act_lo;
   int* err;
   long P_pad;
+  int head_tiles = 1;
 
   tlg_policy(const tlg_policy_shape& s, int dev, long mb) : net(s), device(dev), max_batch(mb) {
     if (mb <= 0) throw InvalidArg("max_batch must be >= 1");
@@ -607,6 +636,7 @@ struct tlg_policy {
     obs = mem.add<float>(mb * net.D);
     obs_lo = mem.add<float>(mb * net.D);
     head_out = mem.add<float>(mb * (net.A + 1));
+    head_part = mem.add<float>(mb * (net.A + 1) * ((net.head.H + 63) / 64));
     logits = mem.add<float>(mb * net.A);
     probs = mem.add<float>(mb * net.A);
     value = mem.add<float>(mb);
@@ -846,18 +876,32 @@ int tlg_policy_forward(tlg_policy* p, const float* obs, size_t n, float* logits,
       gp.out_lo = p->act_lo[l];
       gp.ldo = outw;
       gp.bias = p->params + p->net.b_off[l];
-      tlg::gemm::launch(Aop, Bop, int(n), outw, in, tlg::gemm::kEpiFwdTanh, gp, 1, p->stream);
+      const bool fuse = l + 1 == p->net.L && p->net.A + 1 <= 8;
+      if (fuse) {
+        gp.head_w = p->params + p->net.head.wpi;
+        gp.head_wv = p->params + p->net.head.wv;
+        gp.head_k = int(A) + 1;
+        gp.head_part = p->head_part;
+      }
+      const int bn = tlg::gemm::launch(Aop, Bop, int(n), outw, in, tlg::gemm::kEpiFwdTanh, gp, 1,
+                                       p->stream);
+      if (fuse) p->head_tiles = (outw + bn - 1) / bn;
     }
     const float* hL = p->net.L ? p->act[p->net.L - 1] : x0;
     float* lg = on_device ? logits : p->logits;
     float* pr = on_device ? probs : p->probs;
     float* vv = on_device ? value : p->value;
     TLG_CUDA(cudaMemsetAsync(p->err, 0, 4, p->stream));
-    tlg::launch_head_forward(p->net.head, p->params, hL, p->net.head.H, nullptr, long(n),
-                             p->head_out, nullptr, pr, p->err, p->stream);
-    unpack_head_kernel<<<int((n + 255) / 256), 256, 0, p->stream>>>(p->head_out, int(A), long(n),
-                                                                     lg, vv);
-    TLG_CHECK_LAUNCH();
+    if (p->net.L > 0 && p->net.A + 1 <= 8) {
+      tlg::launch_head_finalize(p->net.head, p->params, p->head_part, p->head_tiles, long(n),
+                                nullptr, nullptr, nullptr, lg, pr, vv, p->err, p->stream);
+    } else {
+      tlg::launch_head_forward(p->net.head, p->params, hL, p->net.head.H, nullptr, long(n),
+                               p->head_out, nullptr, pr, p->err, p->stream);
+      unpack_head_kernel<<<int((n + 255) / 256), 256, 0, p->stream>>>(p->head_out, int(A),
+                                                                       long(n), lg, vv);
+      TLG_CHECK_LAUNCH();
+    }
     if (!on_device) {
       TLG_CUDA(cudaMemcpyAsync(logits, p->logits, n * A * 4, cudaMemcpyDeviceToHost, p->stream));
       TLG_CUDA(cudaMemcpyAsync(probs, p->probs, n * A * 4, cudaMemcpyDeviceToHost, p->stream));

@@ -119,6 +119,67 @@ __global__ void __launch_bounds__(256) head_forward_kernel(HeadDesc hd, const fl
   }
 }
 
+// K3a (fused form): the last trunk GEMM's epilogue left per-N-tile partial head dot
+// products; add them in tile order, add the biases, log-softmax.  Thread per frame.
+__global__ void head_finalize_kernel(HeadDesc hd, const float* __restrict__ params,
+                                     const float* __restrict__ part, int n_tiles, long F,
+                                     BatchDev bd, int has_batch, float* __restrict__ head_out,
+                                     float* __restrict__ tlogp, float* __restrict__ logits_out,
+                                     float* __restrict__ probs_out, float* __restrict__ value_out,
+                                     int* __restrict__ err) {
+  const long f = blockIdx.x * long(blockDim.x) + threadIdx.x;
+  if (f >= F) return;
+  const int A = hd.A, A1 = A + 1;
+  const BatchDev* b = has_batch ? &bd : nullptr;
+  if (!frame_valid(b, f)) {
+    for (int k = 0; k < A1; ++k) head_out[f * A1 + k] = 0.f;
+    if (tlogp) tlogp[f] = 0.f;
+    return;
+  }
+  float z[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    if (k < A1) {
+      float acc = 0.f;
+      for (int t = 0; t < n_tiles; ++t) acc += part[(long(t) * F + f) * A1 + k];
+      const long boff = k < A ? (hd.bpi >= 0 ? hd.bpi + k : -1) : hd.bv;
+      z[k] = acc + (boff >= 0 ? params[boff] : 0.f);
+    }
+  }
+  float mx = -INFINITY;
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    if (k < A) mx = fmaxf(mx, z[k]);
+  float se = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    if (k < A) se += expf(z[k] - mx);
+  const float lse = mx + logf(se);
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    if (k < A1) {
+      if (head_out) head_out[f * A1 + k] = z[k];
+      if (k < A) {
+        if (logits_out) logits_out[f * A + k] = z[k];
+        if (probs_out) probs_out[f * A + k] = expf(z[k] - lse);
+      }
+    }
+  if (value_out) value_out[f] = z[A < 8 ? A : 7];
+  if (b) {
+    const int a = b->action[f];
+    if (a < 0 || a >= A) {
+      atomicOr(err, kErrActionRange);
+      if (tlogp) tlogp[f] = 0.f;
+    } else if (tlogp) {
+      float za = 0.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (k == a) za = z[k];
+      tlogp[f] = za - lse;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K1: one warp per segment; lanes cover 32 consecutive steps, blocks of 32 steps are
 // processed from the end so every warp load/store is one coalesced 128-B row slice.
@@ -298,7 +359,8 @@ __global__ void __launch_bounds__(256) loss_backward_kernel(
     BatchDev b, const float* __restrict__ head_out, const float* __restrict__ adv,
     const float* __restrict__ target, const StepStatsDev* __restrict__ st, HyperDev hp,
     int loss_kind, float* __restrict__ dz, float* __restrict__ dz_lo,
-    float* __restrict__ hg_partial, double* __restrict__ loss_partial) {
+    float* __restrict__ hg_partial, double* __restrict__ loss_partial,
+    float* __restrict__ db_partial) {
   extern __shared__ float sdz[];  // [kLossFrames][A1]
   __shared__ double red[5][8];
   const int A = hd.A, A1 = A + 1;
@@ -399,6 +461,7 @@ __global__ void __launch_bounds__(256) loss_backward_kernel(
     float acc[kMaxA1];
 #pragma unroll
     for (int k = 0; k < kMaxA1; ++k) acc[k] = 0.f;
+    float dbacc = 0.f;
     for (int i = 0; i < nf; ++i) {
       const long f = f0 + i;
       const float x = h[f * ldh + j];
@@ -415,8 +478,10 @@ __global__ void __launch_bounds__(256) loss_backward_kernel(
         const float o = dh * (1.f - x * x);
         dz[f * hd.H + j] = o;
         dz_lo[f * hd.H + j] = o - tf32_hi(o);
+        dbacc += o;
       }
     }
+    if (dz) db_partial[long(blockIdx.x) * hd.H + j] = dbacc;  // bias grad of the last layer
     float* out = hg_partial + long(blockIdx.x) * A1 * hd.H;
 #pragma unroll
     for (int k = 0; k < kMaxA1 - 1; ++k)
@@ -432,30 +497,63 @@ __global__ void __launch_bounds__(256) loss_backward_kernel(
   }
 }
 
-// Fixed-order sum of the head-gradient partials into the flat gradient, plus the
-// loss/stat partials into the step statistics (rlmath.cpp:237-263).
-__global__ void head_grad_reduce_kernel(HeadDesc hd, const float* __restrict__ hg_partial,
-                                        const double* __restrict__ loss_partial, int nblocks,
-                                        float* __restrict__ grad, StepStatsDev* st) {
+// out[c] (+ scatter) = sum over rows r of partial[r*stride + c], in a fixed order:
+// warp w of the block sums rows w, w+8, ... for 32 consecutive columns (lane = column,
+// coalesced), then the 8 warp sums are added in warp order.  Deterministic.
+template <typename Store>
+__device__ __forceinline__ void rows_reduce_block(const float* __restrict__ partial, int rows,
+                                                  long cols, long stride, Store store) {
+  __shared__ float sh[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const long c = long(blockIdx.x) * 32 + lane;
+  float acc = 0.f;
+  if (c < cols)
+    for (int r = w; r < rows; r += 8) acc += partial[long(r) * stride + c];
+  sh[w][lane] = acc;
+  __syncthreads();
+  if (w == 0 && c < cols) {
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t += sh[i][lane];
+    store(c, t);
+  }
+}
+
+__global__ void __launch_bounds__(256) rows_reduce_kernel(const float* __restrict__ partial,
+                                                          int rows, long cols, long stride,
+                                                          float* __restrict__ out) {
+  rows_reduce_block(partial, rows, cols, stride, [&](long c, float v) { out[c] = v; });
+}
+
+// Head-gradient partials [nblk][A1][H] -> flat gradient (layout-aware, AccumulateGrad
+// order of the families, policy.cpp:122-141).
+__global__ void __launch_bounds__(256) head_grad_reduce_kernel(HeadDesc hd,
+                                                               const float* __restrict__ hg_partial,
+                                                               int nblocks,
+                                                               float* __restrict__ grad) {
   const int A = hd.A, A1 = A + 1;
   const long nw = long(A1) * hd.H;
-  const long idx = blockIdx.x * long(blockDim.x) + threadIdx.x;
-  if (idx < nw) {
-    float acc = 0.f;
-    for (int bk = 0; bk < nblocks; ++bk) acc += hg_partial[long(bk) * nw + idx];
+  rows_reduce_block(hg_partial, nblocks, nw, nw, [&](long idx, float v) {
     const int k = int(idx / hd.H), j = int(idx % hd.H);
     if (k < A)
-      grad[hd.wpi + long(k) * hd.wk + long(j) * hd.wj] = acc;
+      grad[hd.wpi + long(k) * hd.wk + long(j) * hd.wj] = v;
     else
-      grad[hd.wv + j] = acc;
-  } else if (idx < nw + A1) {
-    const int k = int(idx - nw);
+      grad[hd.wv + j] = v;
+  });
+}
+
+// Bias partials [nblk][A1] and the loss/stat partials -> gradient + step statistics.
+__global__ void head_bias_stats_kernel(HeadDesc hd, const float* __restrict__ bias_partial,
+                                       const double* __restrict__ loss_partial, int nblocks,
+                                       float* __restrict__ grad, StepStatsDev* st) {
+  const int A = hd.A, A1 = A + 1;
+  const int t = threadIdx.x;
+  if (t < A1) {
     float acc = 0.f;
-    const float* bp = hg_partial + long(nblocks) * nw;
-    for (int bk = 0; bk < nblocks; ++bk) acc += bp[long(bk) * A1 + k];
-    if (k < A && hd.bpi >= 0) grad[hd.bpi + k] = acc;
-    if (k == A && hd.bv >= 0) grad[hd.bv] = acc;
-  } else if (idx == nw + A1) {
+    for (int bk = 0; bk < nblocks; ++bk) acc += bias_partial[long(bk) * A1 + t];
+    if (t < A && hd.bpi >= 0) grad[hd.bpi + t] = acc;
+    if (t == A && hd.bv >= 0) grad[hd.bv] = acc;
+  } else if (t == 32) {
     double v[5] = {0, 0, 0, 0, 0};
     for (int bk = 0; bk < nblocks; ++bk)
       for (int q = 0; q < 5; ++q) v[q] += loss_partial[long(bk) * 5 + q];
@@ -586,6 +684,19 @@ void launch_head_forward(const HeadDesc& hd, const float* params, const float* h
   TLG_CHECK_LAUNCH();
 }
 
+void launch_head_finalize(const HeadDesc& hd, const float* params, const float* part,
+                          int n_tiles, long F, const BatchDev* b, float* head_out, float* tlogp,
+                          float* logits_out, float* probs_out, float* value_out, int* err,
+                          cudaStream_t s) {
+  if (hd.A + 1 > 8) throw CudaError("fused head supports n_actions <= 7");
+  BatchDev bd{};
+  if (b) bd = *b;
+  head_finalize_kernel<<<ceil_div(F, 256), 256, 0, s>>>(hd, params, part, n_tiles, F, bd,
+                                                        b ? 1 : 0, head_out, tlogp, logits_out,
+                                                        probs_out, value_out, err);
+  TLG_CHECK_LAUNCH();
+}
+
 void launch_returns(const BatchDev& b, int algo, const HyperDev& hp, const float* tlogp,
                     float* adv, float* target, double* seg_partial, int* err, cudaStream_t s) {
   returns_kernel<<<ceil_div(b.S, 8), 256, 0, s>>>(b, algo, hp, tlogp, adv, target, seg_partial,
@@ -603,7 +714,7 @@ int launch_loss_backward(const HeadDesc& hd, const float* params, const float* h
                          const BatchDev& b, const float* head_out, const float* adv,
                          const float* target, const StepStatsDev* st, const HyperDev& hp,
                          int loss_kind, float* dz, float* dz_lo, float* hg_partial,
-                         double* loss_partial, cudaStream_t s) {
+                         double* loss_partial, float* db_partial, cudaStream_t s) {
   if (hd.A + 1 > kMaxA1Limit) throw CudaError("n_actions exceeds the head kernel limit (31)");
   const long F = long(b.S) * b.T;
   const int blocks = ceil_div(F, kLossFrames);
@@ -611,11 +722,11 @@ int launch_loss_backward(const HeadDesc& hd, const float* params, const float* h
   if (hd.A + 1 <= 8)
     loss_backward_kernel<8><<<blocks, 256, smem, s>>>(hd, params, h, ldh, b, head_out, adv, target,
                                                       st, hp, loss_kind, dz, dz_lo, hg_partial,
-                                                      loss_partial);
+                                                      loss_partial, db_partial);
   else
     loss_backward_kernel<32><<<blocks, 256, smem, s>>>(hd, params, h, ldh, b, head_out, adv,
                                                        target, st, hp, loss_kind, dz, dz_lo,
-                                                       hg_partial, loss_partial);
+                                                       hg_partial, loss_partial, db_partial);
   TLG_CHECK_LAUNCH();
   return blocks;
 }
@@ -623,9 +734,17 @@ int launch_loss_backward(const HeadDesc& hd, const float* params, const float* h
 void launch_head_grad_reduce(const HeadDesc& hd, const float* hg_partial,
                              const double* loss_partial, int nblocks, float* grad,
                              StepStatsDev* st, cudaStream_t s) {
-  const long n = long(hd.A + 1) * hd.H + hd.A + 1 + 1;
-  head_grad_reduce_kernel<<<ceil_div(n, 256), 256, 0, s>>>(hd, hg_partial, loss_partial, nblocks,
-                                                           grad, st);
+  const long nw = long(hd.A + 1) * hd.H;
+  head_grad_reduce_kernel<<<ceil_div(nw, 32), 256, 0, s>>>(hd, hg_partial, nblocks, grad);
+  TLG_CHECK_LAUNCH();
+  head_bias_stats_kernel<<<1, 64, 0, s>>>(hd, hg_partial + long(nblocks) * nw, loss_partial,
+                                          nblocks, grad, st);
+  TLG_CHECK_LAUNCH();
+}
+
+void launch_rows_reduce(const float* partial, int rows, long cols, long stride, float* out,
+                        cudaStream_t s) {
+  rows_reduce_kernel<<<ceil_div(cols, 32), 256, 0, s>>>(partial, rows, cols, stride, out);
   TLG_CHECK_LAUNCH();
 }
 

@@ -71,6 +71,13 @@ void launch_split_lo(const float* x, float* lo, long n, cudaStream_t s);
 void launch_head_forward(const HeadDesc& hd, const float* params, const float* h, long ldh,
                          const BatchDev* b, long F, float* head_out, float* tlogp,
                          float* probs_out, int* err, cudaStream_t s);
+// Fused-head finalisation (n_actions <= 7): part = [n_tiles][F][A+1] partial dot products
+// from the last trunk GEMM epilogue.  Writes head_out [F][A+1] (+ tlogp with a batch),
+// and/or logits/probs/value for inference.
+void launch_head_finalize(const HeadDesc& hd, const float* params, const float* part,
+                          int n_tiles, long F, const BatchDev* b, float* head_out, float* tlogp,
+                          float* logits_out, float* probs_out, float* value_out, int* err,
+                          cudaStream_t s);
 void launch_returns(const BatchDev& b, int algo, const HyperDev& hp, const float* tlogp,
                     float* adv, float* target, double* seg_partial, int* err, cudaStream_t s);
 void launch_finalize_adv(const double* seg_partial, const BatchDev& b, int adv_norm,
@@ -80,10 +87,13 @@ int launch_loss_backward(const HeadDesc& hd, const float* params, const float* h
                          const BatchDev& b, const float* head_out, const float* adv,
                          const float* target, const StepStatsDev* st, const HyperDev& hp,
                          int loss_kind, float* dz, float* dz_lo, float* hg_partial,
-                         double* loss_partial, cudaStream_t s);
+                         double* loss_partial, float* db_partial, cudaStream_t s);
 void launch_head_grad_reduce(const HeadDesc& hd, const float* hg_partial,
                              const double* loss_partial, int nblocks, float* grad,
                              StepStatsDev* st, cudaStream_t s);
+// out[c] = sum_r partial[r*stride + c] for c < cols, fixed order (deterministic).
+void launch_rows_reduce(const float* partial, int rows, long cols, long stride, float* out,
+                        cudaStream_t s);
 void launch_dw_reduce(const float* ws, int splits, long n, float* grad, cudaStream_t s);
 // grad[j] = sum over rows of x[row][j] (fixed order); partial: scratch [chunks x cols]
 void launch_colsum(const float* x, long ld, long rows, int cols, float* partial, float* grad,

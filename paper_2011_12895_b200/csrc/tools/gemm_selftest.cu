@@ -73,7 +73,9 @@ void check(const char* name, int M, int N, int K, bool a_mn, bool b_mn, bool a_e
   TLG_CUDA(cudaMalloc(&refabs, long(M) * N * 8));
   ref_gemm<<<dim3((M + 127) / 128, N), 128>>>(A.x, lda, a_mn, B.x, ldb, b_mn, M, N, K, ref,
                                               refabs);
-  float *out_hi, *out_lo, *ws;
+  float *out_hi, *out_lo, *ws, *colsum;
+  const int mt = (M + 127) / 128;
+  TLG_CUDA(cudaMalloc(&colsum, long(mt) * N * 4));
   TLG_CUDA(cudaMalloc(&out_hi, long(M) * N * 4));
   TLG_CUDA(cudaMalloc(&out_lo, long(M) * N * 4));
   TLG_CUDA(cudaMalloc(&ws, long(splits) * M * N * 4));
@@ -90,6 +92,7 @@ void check(const char* name, int M, int N, int K, bool a_mn, bool b_mn, bool a_e
   p.ld_act = N;
   p.ws = ws;
   p.ws_split_stride = long(M) * N;
+  p.colsum = epi == gemm::kEpiBwdTanh ? colsum : nullptr;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -116,6 +119,16 @@ void check(const char* name, int M, int N, int K, bool a_mn, bool b_mn, bool a_e
   TLG_CUDA(cudaMemcpy(hws.data(), ws, hws.size() * 4, cudaMemcpyDeviceToHost));
   double worst = 0;
   long bad = 0;
+  if (epi == gemm::kEpiBwdTanh) {
+    std::vector<float> hc(long(mt) * N);
+    TLG_CUDA(cudaMemcpy(hc.data(), colsum, hc.size() * 4, cudaMemcpyDeviceToHost));
+    for (int n = 0; n < N; ++n) {
+      double want = 0, got = 0, sa = 0;
+      for (int m = 0; m < M; ++m) { want += hh[long(m) * N + n]; sa += std::fabs(hh[long(m) * N + n]); }
+      for (int t = 0; t < mt; ++t) got += hc[long(t) * N + n];
+      if (std::fabs(got - want) > 1e-5 * (sa + 1e-30)) ++bad;
+    }
+  }
   for (long i = 0; i < long(M) * N; ++i) {
     const int n = int(i % N);
     double want, got, scale;
@@ -143,7 +156,7 @@ void check(const char* name, int M, int N, int K, bool a_mn, bool b_mn, bool a_e
   printf("%-34s M=%6d N=%5d K=%6d split=%d : worst rel %.3e bad %ld  %.3f ms %.1f TF/s  %s\n",
          name, M, N, K, splits, worst, bad, ms, tflops, bad ? "FAIL" : "ok");
   if (bad) ++failures;
-  cudaFree(ref); cudaFree(refabs); cudaFree(out_hi); cudaFree(out_lo); cudaFree(ws);
+  cudaFree(colsum); cudaFree(ref); cudaFree(refabs); cudaFree(out_hi); cudaFree(out_lo); cudaFree(ws);
   cudaFree(A.x); cudaFree(A.hi); cudaFree(A.lo); cudaFree(B.x); cudaFree(B.hi); cudaFree(B.lo);
   cudaFree(act.x); cudaFree(act.hi); cudaFree(act.lo); cudaFree(bias.x); cudaFree(bias.hi);
   cudaFree(bias.lo);
@@ -171,7 +184,11 @@ int main(int argc, char** argv) {
       // throughput shapes (C3 layer 1 forward, C5 layer forward)
       check("perf fwd C3 L1", 131072, 256, 1936, false, false, true, kEpiFwdTanh, 1);
       check("perf fwd C5", 131072, 2048, 2048, false, false, false, kEpiFwdTanh, 1);
-      check("perf dW C3 L1", 256, 1936, 131072, true, true, false, kEpiStore, 8);
+      check("perf dW C3 L1", 256, 1936, 131072, true, true, false, kEpiStore, 9);
+      check("perf dW C3 L2", 256, 256, 131072, true, true, false, kEpiStore, 74);
+      check("perf dX C3 L2", 131072, 256, 256, false, true, false, kEpiBwdTanh, 1);
+      check("perf fwd C3 L2", 131072, 256, 256, false, false, false, kEpiFwdTanh, 1);
+      check("perf fwd C4 L2", 65536, 1024, 1024, false, false, false, kEpiFwdTanh, 1);
     }
   } catch (const std::exception& e) {
     printf("EXCEPTION: %s\n", e.what());
