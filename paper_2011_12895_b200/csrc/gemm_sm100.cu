@@ -1,6 +1,7 @@
 // Host launcher for the tcgen05 3xTF32 GEMM (see gemm_sm100.cuh).
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -146,8 +147,8 @@ int pick_splits(int M, int N, int K, int max_splits) {
   return s;
 }
 
-int launch(const Operand& A, const Operand& B, int M, int N, int K, int epi, Params p,
-           int splits, cudaStream_t stream) {
+LaunchInfo launch(const Operand& A, const Operand& B, int M, int N, int K, int epi, Params p,
+                  int splits, cudaStream_t stream) {
   if (M <= 0 || N <= 0 || K <= 0) throw CudaError("gemm: empty problem");
   int BN = N > 128 ? 256 : N > 64 ? 128 : 64;
   // widest tile whose pipeline (>= 2 stages) + epilogue staging fits 227 KB
@@ -155,10 +156,16 @@ int launch(const Operand& A, const Operand& B, int M, int N, int K, int epi, Par
   auto fits = [&](int bn) {
     const int stage = kBM * kBK * 4 * (a_lo0 ? 2 : 1) + bn * kBK * 4 * (b_lo0 ? 2 : 1);
     const int blocks = epi == kEpiStore ? 1 : epi == kEpiBwdTanh ? 3 : 2;
-    const int epib = 4 * blocks * 4096 + (epi == kEpiBwdTanh ? 4 * bn * 4 : 0);
+    const int epib = 4 * blocks * 4096 + (epi == kEpiBwdTanh ? 4 * bn * 4 + kColMax * 4 : 0);
     return 2 * stage + 2048 + epib + 1024 <= 227 * 1024;
   };
   while (BN > 64 && !fits(BN)) BN /= 2;
+  if (epi == kEpiBwdTanh && p.colsum != nullptr && N > kColMax)
+    throw CudaError("gemm: fused column sums need N <= 2048");
+  if (const char* e = std::getenv("TLG_GEMM_MAX_BN")) {  // tuning experiments only
+    const int cap = std::atoi(e);
+    while (BN > 64 && BN > cap) BN /= 2;
+  }
   const int kb_total = ceil_div(K, kBK);
   if (splits < 1) splits = 1;
   if (epi != kEpiStore) splits = 1;
@@ -188,7 +195,7 @@ int launch(const Operand& A, const Operand& B, int M, int N, int K, int epi, Par
     case 128: dispatch_bn<128>(A.mn_major, B.mn_major, a_lo, b_lo, epi, ah, al, bh, bl, em, p, grid, stream); break;
     default: dispatch_bn<64>(A.mn_major, B.mn_major, a_lo, b_lo, epi, ah, al, bh, bl, em, p, grid, stream); break;
   }
-  return BN;
+  return {BN, std::min(int(grid.x * grid.y * grid.z), num_sms())};
 }
 
 }  // namespace tlg::gemm

@@ -49,7 +49,8 @@ struct Params {
   long ld_act;
   float* ws;
   long ws_split_stride;
-  float* colsum;  // kEpiBwdTanh: optional per-M-tile column sums [M/128][N] of the output
+  float* colsum;  // kEpiBwdTanh: optional column sums of the output, one row per CTA:
+                  // colsum[cta][n] (N <= kColMax); the caller sums the rows in order
   // kEpiFwdTanh on the last trunk layer: fused policy/value head partial dot products
   //   head_part[n_tile][m][k] = sum_{n in tile} Whead[k][n] * out[m][n], k < head_k
   const float* head_w;   // W_pi [head_k - 1][N] row-major
@@ -168,6 +169,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 
 // ---------------------------------------------------------------------------
 constexpr int kEpiWarps = 4;
+constexpr int kColMax = 2048;  // widest N with fused column sums
 constexpr int kStageBuf = 32 * 33;  // per-warp 32x32 transpose buffer (+1 pad: no bank conflicts)
 
 template <int BN, bool A_LO, bool B_LO, int EPI>
@@ -178,7 +180,7 @@ struct Smem {
   // per epilogue warp, 4 KB each: out (+ out_lo unless split-K store) (+ act for bwd)
   static constexpr int kEpiBlocks = EPI == kEpiStore ? 1 : EPI == kEpiBwdTanh ? 3 : 2;
   static constexpr int kEpiBytes =
-      kEpiWarps * kEpiBlocks * 4096 + (EPI == kEpiBwdTanh ? kEpiWarps * BN * 4 : 0);
+      kEpiWarps * kEpiBlocks * 4096 + (EPI == kEpiBwdTanh ? kEpiWarps * BN * 4 + kColMax * 4 : 0);
   static constexpr int kBudget = 225 * 1024 - kEpiBytes - 1024 - 256;
   static constexpr int kStages = (kBudget / kStage) < 2 ? 2 : (kBudget / kStage) > 8 ? 8 : (kBudget / kStage);
   static constexpr int kBarOff = kStages * kStage;
@@ -412,6 +414,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     };
     act_issue(blockIdx.x, 0);
+    float* csacc = colpart + kEpiWarps * BN;  // [kColMax] CTA-level column sums
+    if (EPI == kEpiBwdTanh && p.colsum != nullptr) {
+      for (int i = threadIdx.x - 64; i < p.N; i += kEpiWarps * 32) csacc[i] = 0.f;
+    }
     constexpr int kHK = 8;  // fused head width limit (n_actions + 1)
     const bool do_head = EPI == kEpiFwdTanh && p.head_k > 0;
     int it = 0;
@@ -516,17 +522,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (k < p.head_k) hp[k] = zacc[k];
       }
       if (EPI == kEpiBwdTanh && p.colsum != nullptr) {
-        // fixed-order sum of the 4 warps' column partials -> colsum[m_tile][n]
+        // fixed-order sum of the 4 warps' column partials into the CTA accumulator
         named_bar(1, kEpiWarps * 32);
         const int tid = threadIdx.x - 64;
         for (int cidx = tid; cidx < BN; cidx += kEpiWarps * 32) {
           const int n = n0 + cidx;
           if (n < p.N)
-            p.colsum[long(mt) * p.N + n] = colpart[cidx] + colpart[BN + cidx] +
-                                           colpart[2 * BN + cidx] + colpart[3 * BN + cidx];
+            csacc[n] += colpart[cidx] + colpart[BN + cidx] + colpart[2 * BN + cidx] +
+                        colpart[3 * BN + cidx];
         }
         named_bar(1, kEpiWarps * 32);
       }
+    }
+    if (EPI == kEpiBwdTanh && p.colsum != nullptr) {
+      for (int i = threadIdx.x - 64; i < p.N; i += kEpiWarps * 32)
+        p.colsum[long(blockIdx.x) * p.N + i] = csacc[i];
     }
     if (lane == 0) bulk_wait_all();
   }
@@ -549,10 +559,14 @@ struct Operand {
   bool mn_major = false;      // false: stored [MN rows][K cols]; true: stored [K rows][MN cols]
 };
 
+struct LaunchInfo {
+  int bn;    // N tile width (the fused head writes ceil(N / bn) partial rows)
+  int ctas;  // persistent CTAs (the fused column sums write this many rows)
+};
+
 // Launch C = A . B^T with the given epilogue on `stream`.  splits > 1 only for
-// kEpiStore (partials into p.ws).  Returns the N tile width used (the fused head writes
-// ceil(N / BN) partial rows).  Throws tlg::CudaError on misuse.
-int launch(const Operand& A, const Operand& B, int M, int N, int K, int epi, Params p,
+// kEpiStore (partials into p.ws).  Throws tlg::CudaError on misuse.
+LaunchInfo launch(const Operand& A, const Operand& B, int M, int N, int K, int epi, Params p,
             int splits, cudaStream_t stream);
 
 // Number of K splits that fills the GPU for a (M, N, K) problem, given a cap.

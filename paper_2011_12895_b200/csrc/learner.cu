@@ -372,7 +372,7 @@ struct tlg_learner {
       }
       if (shard == 0) kmark(0, int(l), 0);
       const int bn = tlg::gemm::launch(A, B, int(F), outw, in, tlg::gemm::kEpiFwdTanh, p, 1,
-                                       stream);
+                                       stream).bn;
       if (shard == 0) kmark(0, int(l), 1);
       if (fuse_head) head_tiles = (outw + bn - 1) / bn;
       ++launches;
@@ -428,8 +428,8 @@ struct tlg_learner {
       // db_l = column sums of dZ_l, from the per-M-tile partials the dX epilogue of
       // layer l+1 wrote (the top layer's came from the loss kernel)
       if (l < int(net.L) - 1) {
-        const int m_tiles = int((F + tlg::gemm::kBM - 1) / tlg::gemm::kBM);
-        tlg::launch_rows_reduce(col_partial, m_tiles, outw, outw, gtarget + net.b_off[l], stream);
+        tlg::launch_rows_reduce(col_partial, colsum_rows, outw, outw, gtarget + net.b_off[l],
+                                stream);
         ++launches;
       }
       launches += 2;
@@ -445,7 +445,8 @@ struct tlg_learner {
         p2.ld_act = in;
         p2.colsum = col_partial;
         if (shard == 0) kmark(2, l, 0);
-        tlg::gemm::launch(A2, B2, int(F), in, outw, tlg::gemm::kEpiBwdTanh, p2, 1, stream);
+        colsum_rows = tlg::gemm::launch(A2, B2, int(F), in, outw, tlg::gemm::kEpiBwdTanh, p2, 1,
+                                        stream).ctas;
         if (shard == 0) kmark(2, l, 1);
         ++launches;
       }
@@ -519,6 +520,7 @@ struct tlg_learner {
 
   void accumulate_grad();
   bool fused_head() const { return net.A + 1 <= 8; }
+  int colsum_rows = 0;
   int head_tiles = 1;
   void set_guard(int shard);
   void launch_guarded_optimizer(bool adam, float lr, float step_size, float bc2_sqrt);
@@ -884,7 +886,7 @@ int tlg_policy_forward(tlg_policy* p, const float* obs, size_t n, float* logits,
         gp.head_part = p->head_part;
       }
       const int bn = tlg::gemm::launch(Aop, Bop, int(n), outw, in, tlg::gemm::kEpiFwdTanh, gp, 1,
-                                       p->stream);
+                                       p->stream).bn;
       if (fuse) p->head_tiles = (outw + bn - 1) / bn;
     }
     const float* hL = p->net.L ? p->act[p->net.L - 1] : x0;

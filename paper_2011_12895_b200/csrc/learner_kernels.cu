@@ -347,13 +347,15 @@ __global__ void __launch_bounds__(1024) finalize_adv_kernel(const double* __rest
 }
 
 // ---------------------------------------------------------------------------
-// K3b.  Block = kLossFrames frames x 256 threads.
+// K3b.  Persistent blocks of 256 threads walk chunks of kLossFrames frames.
 //  phase 1 (thread per frame): per-sample PPO / PG body (rlmath.cpp:129-182 / 196-220)
-//          -> dlogits, dvalue in smem; loss/stat partials (fp64).
+//          -> dlogits, dvalue in smem; loss/stat sums (fp64, per thread).
 //  phase 2 (thread per head-input column j): dZ_L[f][j] = (sum_k dz_k W_pi[k][j] +
-//          dV w_v[j]) * (1 - h^2) for the trunk, and the head weight gradient
-//          partials sum_f dz_k(f) h[f][j] (AccumulateGrad, policy.cpp:122-141).
-template <int kMaxA1>
+//          dV w_v[j]) * (1 - h^2) for the trunk, the head weight gradient
+//          sum_f dz_k(f) h[f][j] (AccumulateGrad, policy.cpp:122-141) and the last
+//          layer's bias gradient sum_f dZ_L[f][j], accumulated in registers across all
+//          of the block's chunks.  Each block writes one partial row (fixed order).
+template <int kMaxA1, int kCPT>
 __global__ void __launch_bounds__(256) loss_backward_kernel(
     HeadDesc hd, const float* __restrict__ params, const float* __restrict__ h, long ldh,
     BatchDev b, const float* __restrict__ head_out, const float* __restrict__ adv,
@@ -365,135 +367,162 @@ __global__ void __launch_bounds__(256) loss_backward_kernel(
   __shared__ double red[5][8];
   const int A = hd.A, A1 = A + 1;
   const long F = long(b.S) * b.T;
-  const long f0 = long(blockIdx.x) * kLossFrames;
+  const long nchunks = (F + kLossFrames - 1) / kLossFrames;
   const int tid = threadIdx.x;
   const float inv_n = float(st->inv_n);
   const double mean = st->mean, sd = st->sd;
-
-  // ---- phase 1
   double l_loss = 0, l_ratio = 0, l_ent = 0, l_vl = 0, l_clip = 0;
-  for (int i = tid; i < kLossFrames; i += blockDim.x) {
-    const long f = f0 + i;
-    float* d = sdz + i * A1;
-    bool valid = false;
-    if (f < F) {
-      const int s = int(f / b.T), t = int(f % b.T);
-      valid = t < b.valid[s];
+  // per-column accumulators (columns j = tid + 256*c)
+  float acc[kCPT][kMaxA1];
+  float dbacc[kCPT];
+  float w[kCPT][kMaxA1];
+#pragma unroll
+  for (int c = 0; c < kCPT; ++c) {
+    const int j = tid + 256 * c;
+    dbacc[c] = 0.f;
+#pragma unroll
+    for (int k = 0; k < kMaxA1; ++k) {
+      acc[c][k] = 0.f;
+      float wk = 0.f;
+      if (j < hd.H) {
+        if (k < A) wk = __ldg(params + hd.wpi + long(k) * hd.wk + long(j) * hd.wj);
+        else if (k == A) wk = __ldg(params + hd.wv + j);
+      }
+      w[c][k] = wk;
     }
-    if (!valid) {
-      for (int k = 0; k < A1; ++k) d[k] = 0.f;
-      continue;
-    }
-    const float* z = head_out + f * A1;
-    float mx = -INFINITY;
-    for (int k = 0; k < A; ++k) mx = fmaxf(mx, z[k]);
-    float se = 0.f;
-    for (int k = 0; k < A; ++k) se += expf(z[k] - mx);
-    const float lse = mx + logf(se);
-    float ent = 0.f;
-    for (int k = 0; k < A; ++k) {
-      const float lp = z[k] - lse;
-      const float p = expf(lp);
-      if (p > 0.f) ent -= p * lp;  // Entropy (rlmath.cpp:36-41)
-    }
-    const int a = min(max(b.action[f], 0), A - 1);  // out-of-range is flagged by K3a
-    const float logp = z[a] - lse;
-    const float V = z[A];
-    const float verr = V - target[f];
-    const float ad = float((double(adv[f]) - mean) / sd);
-    const float ratio = expf(logp - b.blogp[f]);
-    float loss_i;
-    for (int k = 0; k < A; ++k) d[k] = 0.f;
-    if (loss_kind == 0) {
-      const float clipped = fminf(fmaxf(ratio, 1.f - hp.clip_eps), 1.f + hp.clip_eps);
-      const float t1 = ratio * ad, t2 = clipped * ad;
-      loss_i = -fminf(t1, t2) + hp.vf_coef * verr * verr - hp.ent_coef * ent;
-      if (t2 < t1) l_clip += 1.0;
-      if (t1 <= t2) {
+  }
+
+  for (long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const long f0 = ch * kLossFrames;
+    // ---- phase 1
+    for (int i = tid; i < kLossFrames; i += blockDim.x) {
+      const long f = f0 + i;
+      float* d = sdz + i * A1;
+      bool valid = false;
+      if (f < F) {
+        const int s = int(f / b.T), t = int(f % b.T);
+        valid = t < b.valid[s];
+      }
+      if (!valid) {
+        for (int k = 0; k < A1; ++k) d[k] = 0.f;
+        continue;
+      }
+      const float* z = head_out + f * A1;
+      float mx = -INFINITY;
+      for (int k = 0; k < A; ++k) mx = fmaxf(mx, z[k]);
+      float se = 0.f;
+      for (int k = 0; k < A; ++k) se += expf(z[k] - mx);
+      const float lse = mx + logf(se);
+      float ent = 0.f;
+      for (int k = 0; k < A; ++k) {
+        const float lp = z[k] - lse;
+        const float pk = expf(lp);
+        if (pk > 0.f) ent -= pk * lp;  // Entropy (rlmath.cpp:36-41)
+      }
+      const int a = min(max(b.action[f], 0), A - 1);  // out-of-range is flagged by K3a
+      const float logp = z[a] - lse;
+      const float V = z[A];
+      const float verr = V - target[f];
+      const float ad = float((double(adv[f]) - mean) / sd);
+      const float ratio = expf(logp - b.blogp[f]);
+      float loss_i;
+      for (int k = 0; k < A; ++k) d[k] = 0.f;
+      if (loss_kind == 0) {
+        const float clipped = fminf(fmaxf(ratio, 1.f - hp.clip_eps), 1.f + hp.clip_eps);
+        const float t1 = ratio * ad, t2 = clipped * ad;
+        loss_i = -fminf(t1, t2) + hp.vf_coef * verr * verr - hp.ent_coef * ent;
+        if (t2 < t1) l_clip += 1.0;
+        if (t1 <= t2) {
+          for (int k = 0; k < A; ++k) {
+            const float pk = expf(z[k] - lse);
+            d[k] += -ad * ratio * ((k == a ? 1.f : 0.f) - pk) * inv_n;
+          }
+        }
         for (int k = 0; k < A; ++k) {
-          const float p = expf(z[k] - lse);
-          d[k] += -ad * ratio * ((k == a ? 1.f : 0.f) - p) * inv_n;
+          const float lp = z[k] - lse;
+          const float pk = expf(lp);
+          d[k] += hp.ent_coef * pk * ((pk > 0.f ? lp : 0.f) + ent) * inv_n;
+        }
+      } else {
+        loss_i = -ad * logp + hp.vf_coef * verr * verr - hp.ent_coef * ent;
+        for (int k = 0; k < A; ++k) {
+          const float lp = z[k] - lse;
+          const float pk = expf(lp);
+          d[k] = (-ad * ((k == a ? 1.f : 0.f) - pk) +
+                  hp.ent_coef * pk * ((pk > 0.f ? lp : 0.f) + ent)) * inv_n;
         }
       }
-      for (int k = 0; k < A; ++k) {
-        const float lp = z[k] - lse;
-        const float p = expf(lp);
-        d[k] += hp.ent_coef * p * ((p > 0.f ? lp : 0.f) + ent) * inv_n;
-      }
-    } else {
-      loss_i = -ad * logp + hp.vf_coef * verr * verr - hp.ent_coef * ent;
-      for (int k = 0; k < A; ++k) {
-        const float lp = z[k] - lse;
-        const float p = expf(lp);
-        d[k] = (-ad * ((k == a ? 1.f : 0.f) - p) + hp.ent_coef * p * ((p > 0.f ? lp : 0.f) + ent)) * inv_n;
+      d[A] = 2.f * hp.vf_coef * verr * inv_n;
+      l_loss += double(loss_i);
+      l_ratio += double(ratio);
+      l_ent += double(ent);
+      l_vl += double(verr) * double(verr);
+    }
+    __syncthreads();
+    // ---- phase 2
+    const int nf = int(F - f0 < long(kLossFrames) ? F - f0 : long(kLossFrames));
+#pragma unroll
+    for (int c = 0; c < kCPT; ++c) {
+      const int j = tid + 256 * c;
+      if (j >= hd.H) continue;
+#pragma unroll 4
+      for (int i = 0; i < nf; ++i) {
+        const long f = f0 + i;
+        const float x = h[f * ldh + j];
+        const float* d = sdz + i * A1;
+        float dh = d[A] * w[c][A < kMaxA1 ? A : kMaxA1 - 1];
+#pragma unroll
+        for (int k = 0; k < kMaxA1; ++k)
+          if (k < A) {
+            dh = fmaf(d[k], w[c][k], dh);
+            acc[c][k] = fmaf(d[k], x, acc[c][k]);
+          }
+#pragma unroll
+        for (int k = 0; k < kMaxA1; ++k)
+          if (k == A) acc[c][k] = fmaf(d[A], x, acc[c][k]);
+        if (dz) {
+          const float o = dh * (1.f - x * x);
+          dz[f * hd.H + j] = o;
+          dz_lo[f * hd.H + j] = o - tf32_hi(o);
+          dbacc[c] += o;
+        }
       }
     }
-    d[A] = 2.f * hp.vf_coef * verr * inv_n;
-    l_loss += double(loss_i);
-    l_ratio += double(ratio);
-    l_ent += double(ent);
-    l_vl += double(verr) * double(verr);
+    // bias partials of the heads: sum over the chunk's frames of dz_k
+    if (tid < A1) {
+      float bacc = 0.f;
+      for (int i = 0; i < nf; ++i) bacc += sdz[i * A1 + tid];
+      // stored after the weight partials: [gridDim][A1]
+      float* bp = hg_partial + long(gridDim.x) * A1 * hd.H + long(blockIdx.x) * A1 + tid;
+      *bp = (ch == blockIdx.x ? 0.f : *bp) + bacc;
+    }
+    __syncthreads();
+  }
+  // ---- per-block partial rows
+#pragma unroll
+  for (int c = 0; c < kCPT; ++c) {
+    const int j = tid + 256 * c;
+    if (j >= hd.H) continue;
+    float* out = hg_partial + long(blockIdx.x) * A1 * hd.H;
+#pragma unroll
+    for (int k = 0; k < kMaxA1; ++k)
+      if (k <= A) out[long(k) * hd.H + j] = acc[c][k];
+    if (dz) db_partial[long(blockIdx.x) * hd.H + j] = dbacc[c];
   }
   {
     double v[5] = {l_loss, l_ratio, l_ent, l_vl, l_clip};
-    const int w = tid >> 5, lane = tid & 31;
+    const int wi = tid >> 5, lane = tid & 31;
 #pragma unroll
     for (int q = 0; q < 5; ++q) {
       v[q] = warp_sum(v[q]);
-      if (lane == 0) red[q][w] = v[q];
+      if (lane == 0) red[q][wi] = v[q];
     }
   }
   __syncthreads();
   if (tid < 5) {
-    double acc = 0.0;
-    for (int w = 0; w < int(blockDim.x >> 5); ++w) acc += red[tid][w];
-    loss_partial[long(blockIdx.x) * 5 + tid] = acc;
-  }
-
-  // ---- phase 2
-  const int nf = int(F - f0 < long(kLossFrames) ? F - f0 : long(kLossFrames));
-  for (int j = tid; j < hd.H; j += blockDim.x) {
-    float w[kMaxA1];
-#pragma unroll
-    for (int k = 0; k < kMaxA1 - 1; ++k)
-      w[k] = (k < A) ? __ldg(params + hd.wpi + long(k) * hd.wk + long(j) * hd.wj) : 0.f;
-    const float wv = __ldg(params + hd.wv + j);
-    float acc[kMaxA1];
-#pragma unroll
-    for (int k = 0; k < kMaxA1; ++k) acc[k] = 0.f;
-    float dbacc = 0.f;
-    for (int i = 0; i < nf; ++i) {
-      const long f = f0 + i;
-      const float x = h[f * ldh + j];
-      const float* d = sdz + i * A1;
-      float dh = d[A] * wv;
-#pragma unroll
-      for (int k = 0; k < kMaxA1 - 1; ++k)
-        if (k < A) {
-          dh = fmaf(d[k], w[k], dh);
-          acc[k] = fmaf(d[k], x, acc[k]);
-        }
-      acc[kMaxA1 - 1] = fmaf(d[A], x, acc[kMaxA1 - 1]);
-      if (dz) {
-        const float o = dh * (1.f - x * x);
-        dz[f * hd.H + j] = o;
-        dz_lo[f * hd.H + j] = o - tf32_hi(o);
-        dbacc += o;
-      }
-    }
-    if (dz) db_partial[long(blockIdx.x) * hd.H + j] = dbacc;  // bias grad of the last layer
-    float* out = hg_partial + long(blockIdx.x) * A1 * hd.H;
-#pragma unroll
-    for (int k = 0; k < kMaxA1 - 1; ++k)
-      if (k < A) out[long(k) * hd.H + j] = acc[k];
-    out[long(A) * hd.H + j] = acc[kMaxA1 - 1];
-  }
-  // bias partials: sum over the block's frames of dz_k, stored after the weight partials
-  __syncthreads();
-  if (tid < A1) {
-    float acc = 0.f;
-    for (int i = 0; i < nf; ++i) acc += sdz[i * A1 + tid];
-    hg_partial[long(gridDim.x) * A1 * hd.H + long(blockIdx.x) * A1 + tid] = acc;
+    double t = 0.0;
+    for (int wi = 0; wi < int(blockDim.x >> 5); ++wi) t += red[tid][wi];
+    loss_partial[long(blockIdx.x) * 5 + tid] = t;
   }
 }
 
@@ -543,26 +572,34 @@ __global__ void __launch_bounds__(256) head_grad_reduce_kernel(HeadDesc hd,
 }
 
 // Bias partials [nblk][A1] and the loss/stat partials -> gradient + step statistics.
+// Warp w < A1 reduces bias column w; warps A1.. reduce the 5 loss sums; each warp sums a
+// strided subset then a fixed shuffle tree (deterministic).
 __global__ void head_bias_stats_kernel(HeadDesc hd, const float* __restrict__ bias_partial,
                                        const double* __restrict__ loss_partial, int nblocks,
                                        float* __restrict__ grad, StepStatsDev* st) {
   const int A = hd.A, A1 = A + 1;
-  const int t = threadIdx.x;
-  if (t < A1) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (w < A1) {
     float acc = 0.f;
-    for (int bk = 0; bk < nblocks; ++bk) acc += bias_partial[long(bk) * A1 + t];
-    if (t < A && hd.bpi >= 0) grad[hd.bpi + t] = acc;
-    if (t == A && hd.bv >= 0) grad[hd.bv] = acc;
-  } else if (t == 32) {
-    double v[5] = {0, 0, 0, 0, 0};
-    for (int bk = 0; bk < nblocks; ++bk)
-      for (int q = 0; q < 5; ++q) v[q] += loss_partial[long(bk) * 5 + q];
-    const double inv_n = st->inv_n;
-    st->loss = v[0] * inv_n;
-    st->ratio = v[1] * inv_n;
-    st->entropy = v[2] * inv_n;
-    st->vloss = v[3] * inv_n;
-    st->clip = v[4] * inv_n;
+    for (int bk = lane; bk < nblocks; bk += 32) acc += bias_partial[long(bk) * A1 + w];
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      if (w < A && hd.bpi >= 0) grad[hd.bpi + w] = acc;
+      if (w == A && hd.bv >= 0) grad[hd.bv] = acc;
+    }
+  } else if (w < A1 + 5) {
+    const int q = w - A1;
+    double acc = 0.0;
+    for (int bk = lane; bk < nblocks; bk += 32) acc += loss_partial[long(bk) * 5 + q];
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      const double v = acc * st->inv_n;
+      if (q == 0) st->loss = v;
+      else if (q == 1) st->ratio = v;
+      else if (q == 2) st->entropy = v;
+      else if (q == 3) st->vloss = v;
+      else st->clip = v;
+    }
   }
 }
 
@@ -715,18 +752,27 @@ int launch_loss_backward(const HeadDesc& hd, const float* params, const float* h
                          const float* target, const StepStatsDev* st, const HyperDev& hp,
                          int loss_kind, float* dz, float* dz_lo, float* hg_partial,
                          double* loss_partial, float* db_partial, cudaStream_t s) {
-  if (hd.A + 1 > kMaxA1Limit) throw CudaError("n_actions exceeds the head kernel limit (31)");
   const long F = long(b.S) * b.T;
-  const int blocks = ceil_div(F, kLossFrames);
+  const long nchunks = (F + kLossFrames - 1) / kLossFrames;
+  const int blocks = int(std::min<long>(nchunks, kLossBlocks));
   const size_t smem = size_t(kLossFrames) * (hd.A + 1) * sizeof(float);
-  if (hd.A + 1 <= 8)
-    loss_backward_kernel<8><<<blocks, 256, smem, s>>>(hd, params, h, ldh, b, head_out, adv, target,
-                                                      st, hp, loss_kind, dz, dz_lo, hg_partial,
-                                                      loss_partial, db_partial);
-  else
-    loss_backward_kernel<32><<<blocks, 256, smem, s>>>(hd, params, h, ldh, b, head_out, adv,
-                                                       target, st, hp, loss_kind, dz, dz_lo,
-                                                       hg_partial, loss_partial, db_partial);
+#define TLG_LOSS(MA, CPT)                                                                 \
+  loss_backward_kernel<MA, CPT><<<blocks, 256, smem, s>>>(hd, params, h, ldh, b, head_out, adv, \
+                                                         target, st, hp, loss_kind, dz, dz_lo, \
+                                                         hg_partial, loss_partial, db_partial)
+  const int cpt = (hd.H + 255) / 256;
+  if (hd.A + 1 <= 8) {
+    if (cpt <= 1) TLG_LOSS(8, 1);
+    else if (cpt <= 2) TLG_LOSS(8, 2);
+    else if (cpt <= 4) TLG_LOSS(8, 4);
+    else if (cpt <= 8) TLG_LOSS(8, 8);
+    else throw CudaError("head input wider than 2048 with the fused loss kernel");
+  } else if (hd.A + 1 <= kMaxA1Limit && cpt <= 1) {
+    TLG_LOSS(32, 1);
+  } else {
+    throw CudaError("n_actions > 7 needs a head input width <= 256");
+  }
+#undef TLG_LOSS
   TLG_CHECK_LAUNCH();
   return blocks;
 }
@@ -737,8 +783,8 @@ void launch_head_grad_reduce(const HeadDesc& hd, const float* hg_partial,
   const long nw = long(hd.A + 1) * hd.H;
   head_grad_reduce_kernel<<<ceil_div(nw, 32), 256, 0, s>>>(hd, hg_partial, nblocks, grad);
   TLG_CHECK_LAUNCH();
-  head_bias_stats_kernel<<<1, 64, 0, s>>>(hd, hg_partial + long(nblocks) * nw, loss_partial,
-                                          nblocks, grad, st);
+  head_bias_stats_kernel<<<1, 32 * (hd.A + 1 + 5), 0, s>>>(hd, hg_partial + long(nblocks) * nw,
+                                                          loss_partial, nblocks, grad, st);
   TLG_CHECK_LAUNCH();
 }
 
@@ -749,6 +795,10 @@ void launch_rows_reduce(const float* partial, int rows, long cols, long stride, 
 }
 
 void launch_dw_reduce(const float* ws, int splits, long n, float* grad, cudaStream_t s) {
+  if (splits > 8) {  // many partial rows: warp-parallel fixed-order reduction
+    launch_rows_reduce(ws, splits, n, n, grad, s);
+    return;
+  }
   if ((n & 3) == 0 && (reinterpret_cast<uintptr_t>(grad) & 15) == 0) {
     dw_reduce_kernel<<<grid_for(n / 4, 256), 256, 0, s>>>(reinterpret_cast<const float4*>(ws),
                                                           splits, n / 4, n / 4,

@@ -74,8 +74,9 @@ void check(const char* name, int M, int N, int K, bool a_mn, bool b_mn, bool a_e
   ref_gemm<<<dim3((M + 127) / 128, N), 128>>>(A.x, lda, a_mn, B.x, ldb, b_mn, M, N, K, ref,
                                               refabs);
   float *out_hi, *out_lo, *ws, *colsum;
-  const int mt = (M + 127) / 128;
+  const int mt = std::max((M + 127) / 128, 160);  // rows: one per CTA (<= #SMs)
   TLG_CUDA(cudaMalloc(&colsum, long(mt) * N * 4));
+  TLG_CUDA(cudaMemset(colsum, 0, long(mt) * N * 4));
   TLG_CUDA(cudaMalloc(&out_hi, long(M) * N * 4));
   TLG_CUDA(cudaMalloc(&out_lo, long(M) * N * 4));
   TLG_CUDA(cudaMalloc(&ws, long(splits) * M * N * 4));
@@ -98,6 +99,7 @@ void check(const char* name, int M, int N, int K, bool a_mn, bool b_mn, bool a_e
   cudaEventCreate(&e1);
   gemm::launch(oa, ob, M, N, K, epi, p, splits, 0);
   TLG_CUDA(cudaDeviceSynchronize());
+  p.colsum = nullptr;  // timed reps below must not rewrite the checked column sums
   cudaEventRecord(e0);
   const int reps = 5;
   for (int i = 0; i < reps; ++i) gemm::launch(oa, ob, M, N, K, epi, p, splits, 0);
