@@ -26,6 +26,24 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // 2D fp32 tensor map, 128-byte swizzle, box {32 (inner), box_rows}.
+// uint8 2D map, no swizzle (the converter warps lay the tile out for the MMA).
+CUtensorMap make_u8_map(const uint8_t* base, long inner, long outer, long ld, int box_inner,
+                        int box_outer) {
+  CUtensorMap m;
+  if ((reinterpret_cast<uintptr_t>(base) & 15) != 0 || ld % 16 != 0)
+    throw CudaError("uint8 operand must be 16-byte aligned with a row pitch multiple of 16");
+  cuuint64_t dims[2] = {cuuint64_t(inner), cuuint64_t(outer)};
+  cuuint64_t strides[1] = {cuuint64_t(ld)};
+  cuuint32_t box[2] = {cuuint32_t(box_inner), cuuint32_t(box_outer)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(base), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled(u8) failed: " + std::to_string(r));
+  return m;
+}
+
 // 3D map for the split-K workspace [splits][M][N], box {32, 32, 1}.
 CUtensorMap make_map3(const float* base, long n, long m, long splits) {
   CUtensorMap t;
@@ -85,12 +103,12 @@ struct EpiMaps {
   CUtensorMap out, out_lo, act;
 };
 
-template <int BN, bool A_MN, bool B_MN, bool A_LO, bool B_LO, int EPI>
+template <int BN, bool A_MN, bool B_MN, bool A_LO, bool B_LO, int EPI, int U8 = 0>
 void run(const CUtensorMap& ah, const CUtensorMap& al, const CUtensorMap& bh,
          const CUtensorMap& bl, const EpiMaps& em, const Params& p, dim3 grid,
          cudaStream_t stream) {
-  auto kern = gemm_tf32x3_kernel<BN, A_MN, B_MN, A_LO, B_LO, EPI>;
-  constexpr int bytes = Smem<BN, A_LO, B_LO, EPI>::kBytes;
+  auto kern = gemm_tf32x3_kernel<BN, A_MN, B_MN, A_LO, B_LO, EPI, U8>;
+  constexpr int bytes = Smem<BN, A_LO, B_LO, EPI, U8>::kBytes;
   static_assert(bytes <= 227 * 1024, "shared memory budget");
   static bool attr = false;  // one-time per instantiation
   if (!attr) {
@@ -99,25 +117,32 @@ void run(const CUtensorMap& ah, const CUtensorMap& al, const CUtensorMap& bh,
   }
   const TileMap tm{int(grid.x), int(grid.y), int(grid.z)};
   const int tiles = tm.m_tiles * tm.n_tiles * tm.splits;
-  kern<<<std::min(tiles, num_sms()), kThreads, bytes, stream>>>(ah, al, bh, bl, em.out,
+  kern<<<std::min(tiles, num_sms()), U8 ? kThreadsU8 : kThreads, bytes, stream>>>(ah, al, bh, bl, em.out,
                                                                  em.out_lo, em.act, p, tm);
   TLG_CHECK_LAUNCH();
 }
 
-template <int BN, bool A_MN, bool B_MN, bool A_LO, bool B_LO, int EPI>
+template <int BN, bool A_MN, bool B_MN, bool A_LO, bool B_LO, int EPI, int U8 = 0>
 void run_if_fits(const CUtensorMap& ah, const CUtensorMap& al, const CUtensorMap& bh,
                  const CUtensorMap& bl, const EpiMaps& em, const Params& p, dim3 grid,
                  cudaStream_t s) {
-  if constexpr (Smem<BN, A_LO, B_LO, EPI>::kFits)
-    run<BN, A_MN, B_MN, A_LO, B_LO, EPI>(ah, al, bh, bl, em, p, grid, s);
+  if constexpr (Smem<BN, A_LO, B_LO, EPI, U8>::kFits)
+    run<BN, A_MN, B_MN, A_LO, B_LO, EPI, U8>(ah, al, bh, bl, em, p, grid, s);
   else
     throw CudaError("gemm: tile does not fit shared memory");
 }
 
 template <int BN>
-void dispatch_bn(bool a_mn, bool b_mn, bool a_lo, bool b_lo, int epi, const CUtensorMap& ah,
-                 const CUtensorMap& al, const CUtensorMap& bh, const CUtensorMap& bl,
-                 const EpiMaps& em, const Params& p, dim3 grid, cudaStream_t s) {
+void dispatch_bn(bool a_mn, bool b_mn, bool a_lo, bool b_lo, int epi, int u8,
+                 const CUtensorMap& ah, const CUtensorMap& al, const CUtensorMap& bh,
+                 const CUtensorMap& bl, const EpiMaps& em, const Params& p, dim3 grid,
+                 cudaStream_t s) {
+  // uint8 observation planes: forward (A = obs) and dW of layer 1 (B = obs)
+  if (u8 == 1 && !a_mn && !b_mn && b_lo && epi == kEpiFwdTanh)
+    return run_if_fits<BN, false, false, false, true, kEpiFwdTanh, 1>(ah, al, bh, bl, em, p, grid, s);
+  if (u8 == 2 && a_mn && b_mn && a_lo && epi == kEpiStore)
+    return run_if_fits<BN, true, true, true, false, kEpiStore, 2>(ah, al, bh, bl, em, p, grid, s);
+  if (u8) throw CudaError("gemm: unsupported uint8 operand combination");
   // forward: A = activations (K-major), B = W (K-major)
   if (!a_mn && !b_mn && b_lo && epi == kEpiFwdTanh) {
     if (a_lo) return run_if_fits<BN, false, false, true, true, kEpiFwdTanh>(ah, al, bh, bl, em, p, grid, s);
@@ -152,9 +177,10 @@ LaunchInfo launch(const Operand& A, const Operand& B, int M, int N, int K, int e
   if (M <= 0 || N <= 0 || K <= 0) throw CudaError("gemm: empty problem");
   int BN = N > 128 ? 256 : N > 64 ? 128 : 64;
   // widest tile whose pipeline (>= 2 stages) + epilogue staging fits 227 KB
-  const bool a_lo0 = A.lo != nullptr, b_lo0 = B.lo != nullptr;
+  const bool a_lo0 = A.lo != nullptr && !A.u8, b_lo0 = B.lo != nullptr && !B.u8;
   auto fits = [&](int bn) {
-    const int stage = kBM * kBK * 4 * (a_lo0 ? 2 : 1) + bn * kBK * 4 * (b_lo0 ? 2 : 1);
+    const int stage = kBM * kBK * 4 * (a_lo0 ? 2 : 1) + bn * kBK * 4 * (b_lo0 ? 2 : 1) +
+                      (A.u8 ? kBM * kBK : B.u8 ? bn * kBK : 0);
     const int blocks = epi == kEpiStore ? 1 : epi == kEpiBwdTanh ? 3 : 2;
     const int epib = 4 * blocks * 4096 + (epi == kEpiBwdTanh ? 4 * bn * 4 + kColMax * 4 : 0);
     return 2 * stage + 2048 + epib + 1024 <= 227 * 1024;
@@ -174,12 +200,15 @@ LaunchInfo launch(const Operand& A, const Operand& B, int M, int N, int K, int e
   p.M = M;
   p.N = N;
   p.K = K;
-  const CUtensorMap ah = operand_map(A.hi, A, M, K, kBM);
+  const int u8 = A.u8 ? 1 : B.u8 ? 2 : 0;
+  if (A.u8 && (A.mn_major || A.ld % 16)) throw CudaError("gemm: uint8 A must be K-major, ld % 16 == 0");
+  if (B.u8 && (!B.mn_major || B.ld % 16)) throw CudaError("gemm: uint8 B must be MN-major, ld % 16 == 0");
+  const CUtensorMap ah = A.u8 ? make_u8_map(A.u8, K, M, A.ld, 32, kBM) : operand_map(A.hi, A, M, K, kBM);
   const CUtensorMap al = operand_map(A.lo, A, M, K, kBM);
-  const CUtensorMap bh = operand_map(B.hi, B, N, K, BN);
+  const CUtensorMap bh = B.u8 ? make_u8_map(B.u8, N, K, B.ld, BN, 32) : operand_map(B.hi, B, N, K, BN);
   const CUtensorMap bl = operand_map(B.lo, B, N, K, BN);
   dim3 grid(ceil_div(M, kBM), ceil_div(N, BN), splits);
-  const bool a_lo = A.lo != nullptr, b_lo = B.lo != nullptr;
+  const bool a_lo = A.lo != nullptr && !A.u8, b_lo = B.lo != nullptr && !B.u8;
   // epilogue maps: 32x32 fp32 blocks with the 128-B swizzle
   EpiMaps em;
   std::memset(&em, 0, sizeof(em));
@@ -189,11 +218,12 @@ LaunchInfo launch(const Operand& A, const Operand& B, int M, int N, int K, int e
     em.out = make_map(p.out_hi, N, M, p.ldo, 32, CU_TENSOR_MAP_SWIZZLE_128B);
     em.out_lo = make_map(p.out_lo, N, M, p.ldo, 32, CU_TENSOR_MAP_SWIZZLE_128B);
     if (epi == kEpiBwdTanh) em.act = make_map(p.act_hi, N, M, p.ld_act, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (A.u8 && p.a_expand) em.act = make_map(p.a_expand, K, M, A.ld, kBM, CU_TENSOR_MAP_SWIZZLE_128B);
   }
   switch (BN) {
-    case 256: dispatch_bn<256>(A.mn_major, B.mn_major, a_lo, b_lo, epi, ah, al, bh, bl, em, p, grid, stream); break;
-    case 128: dispatch_bn<128>(A.mn_major, B.mn_major, a_lo, b_lo, epi, ah, al, bh, bl, em, p, grid, stream); break;
-    default: dispatch_bn<64>(A.mn_major, B.mn_major, a_lo, b_lo, epi, ah, al, bh, bl, em, p, grid, stream); break;
+    case 256: dispatch_bn<256>(A.mn_major, B.mn_major, a_lo, b_lo, epi, u8, ah, al, bh, bl, em, p, grid, stream); break;
+    case 128: dispatch_bn<128>(A.mn_major, B.mn_major, a_lo, b_lo, epi, u8, ah, al, bh, bl, em, p, grid, stream); break;
+    default: dispatch_bn<64>(A.mn_major, B.mn_major, a_lo, b_lo, epi, u8, ah, al, bh, bl, em, p, grid, stream); break;
   }
   return {BN, std::min(int(grid.x * grid.y * grid.z), num_sms())};
 }

@@ -36,6 +36,7 @@ enum Epi : int {
 constexpr int kBM = 128;
 constexpr int kBK = 32;  // fp32 elements per 128-byte swizzle row
 constexpr int kThreads = 192;
+constexpr int kThreadsU8 = 320;  // + 4 converter warps for uint8 operands
 
 struct Params {
   int M, N, K;
@@ -57,6 +58,9 @@ struct Params {
   const float* head_wv;  // w_v [N]
   int head_k;            // n_actions + 1 (<= 8), 0 = no fused head
   float* head_part;
+  // U8 == 1: also write the expanded fp32 A operand (exact) to this [M][K] buffer
+  // (tmAct map) from the n_tile == 0 CTAs, so a later GEMM can read it as plain fp32
+  float* a_expand;
 };
 
 // ---------------------------------------------------------------------------
@@ -172,11 +176,16 @@ constexpr int kEpiWarps = 4;
 constexpr int kColMax = 2048;  // widest N with fused column sums
 constexpr int kStageBuf = 32 * 33;  // per-warp 32x32 transpose buffer (+1 pad: no bank conflicts)
 
-template <int BN, bool A_LO, bool B_LO, int EPI>
+// U8: 0 = fp32 operands; 1 = A arrives as uint8 planes (K-major); 2 = B arrives as uint8
+// planes (MN-major).  A uint8 operand is TMA-loaded into a byte staging tile and expanded
+// to fp32 in the MMA's swizzled layout by 4 converter warps (exact: 0..255).
+template <int BN, bool A_LO, bool B_LO, int EPI, int U8 = 0>
 struct Smem {
   static constexpr int kA = kBM * kBK * 4;  // 16 KB
   static constexpr int kB = BN * kBK * 4;
-  static constexpr int kStage = kA * (A_LO ? 2 : 1) + kB * (B_LO ? 2 : 1);
+  static constexpr int kU8 = U8 == 1 ? kBM * kBK : U8 == 2 ? BN * kBK : 0;  // byte staging
+  static constexpr int kStage = kA * (A_LO ? 2 : 1) + kB * (B_LO ? 2 : 1) + kU8;
+  static constexpr int kTmaBytes = kStage - kU8 - (U8 == 1 ? kA : U8 == 2 ? kB : 0);
   // per epilogue warp, 4 KB each: out (+ out_lo unless split-K store) (+ act for bwd)
   static constexpr int kEpiBlocks = EPI == kEpiStore ? 1 : EPI == kEpiBwdTanh ? 3 : 2;
   static constexpr int kEpiBytes =
@@ -184,8 +193,8 @@ struct Smem {
   static constexpr int kBudget = 225 * 1024 - kEpiBytes - 1024 - 256;
   static constexpr int kStages = (kBudget / kStage) < 2 ? 2 : (kBudget / kStage) > 8 ? 8 : (kBudget / kStage);
   static constexpr int kBarOff = kStages * kStage;
-  // full/empty per stage, tmem full/empty x2, act-block full x4
-  static constexpr int kNumBars = 2 * kStages + 4 + kEpiWarps;
+  // full/empty per stage, tmem full/empty x2, act-block full x4, u8 full/converted per stage
+  static constexpr int kNumBars = 2 * kStages + 4 + kEpiWarps + (U8 ? 2 * kStages : 0);
   static constexpr int kEpiOff = (kBarOff + kNumBars * 8 + 16 + 1023) / 1024 * 1024;
   static constexpr int kBytes = kEpiOff + kEpiBytes + 1024;  // + 1 KB alignment slack
   static constexpr bool kFits = kBytes <= 227 * 1024;
@@ -232,15 +241,29 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read_n() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+// Four uint8 -> four exact fp32 without I2F: byte b placed in the mantissa of 2^23 gives
+// 2^23 + b; subtracting 2^23 is exact (PRMT + FADD at full ALU rate).
+__device__ __forceinline__ float4 u8x4_to_f32(uint32_t v) {
+  const float k = 8388608.f;
+  return make_float4(__uint_as_float(__byte_perm(v, 0x4B000000u, 0x7440)) - k,
+                     __uint_as_float(__byte_perm(v, 0x4B000000u, 0x7441)) - k,
+                     __uint_as_float(__byte_perm(v, 0x4B000000u, 0x7442)) - k,
+                     __uint_as_float(__byte_perm(v, 0x4B000000u, 0x7443)) - k);
+}
+
 // byte offset of element (row r, col c) in a 32x32 fp32 block with the 128-B TMA swizzle
 __device__ __forceinline__ uint32_t swz(int r, int c4) { return uint32_t(r * 128 + ((c4 ^ (r & 7)) << 4)); }
 
-template <int BN, bool A_MN, bool B_MN, bool A_LO, bool B_LO, int EPI>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int BN, bool A_MN, bool B_MN, bool A_LO, bool B_LO, int EPI, int U8>
+__global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
     gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap tmA_hi,
                        const __grid_constant__ CUtensorMap tmA_lo,
                        const __grid_constant__ CUtensorMap tmB_hi,
@@ -249,7 +272,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                        const __grid_constant__ CUtensorMap tmOutLo,
                        const __grid_constant__ CUtensorMap tmAct, const Params p,
                        const TileMap tm) {
-  using S = Smem<BN, A_LO, B_LO, EPI>;
+  using S = Smem<BN, A_LO, B_LO, EPI, U8>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -260,6 +283,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t bar_tempty = bar_tfull + 16;               // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + S::kBarOff + S::kNumBars * 8);
   const uint32_t bar_act = bar_tempty + 16;                 // [4]
+  const uint32_t bar_ufull = bar_act + 8 * kEpiWarps;       // [stages] (U8)
+  const uint32_t bar_conv = bar_ufull + 8 * S::kStages;     // [stages] (U8)
   float* colpart = reinterpret_cast<float*>(smem + S::kEpiOff + kEpiWarps * S::kEpiBlocks * 4096);
 
   const int warp = threadIdx.x >> 5;
@@ -281,6 +306,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(bar_tempty + 8 * a, kEpiWarps);
     }
     for (int w = 0; w < kEpiWarps; ++w) mbar_init(bar_act + 8 * w, 1);
+    if (U8)
+      for (int st = 0; st < S::kStages; ++st) {
+        mbar_init(bar_ufull + 8 * st, 1);
+        mbar_init(bar_conv + 8 * st, 4);  // one arrive per converter warp
+      }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -308,10 +338,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(bar_empty + 8 * stage, phase ^ 1);
           const uint32_t st = sbase + stage * S::kStage;
           const uint32_t full = bar_full + 8 * stage;
-          mbar_expect_tx(full, S::kStage);
+          mbar_expect_tx(full, S::kTmaBytes);
           const int k0 = kb * kBK;
           uint32_t off = st;
-          if (!A_MN) {
+          const uint32_t ust = st + S::kStage - S::kU8;  // byte staging of the u8 operand
+          if (U8) mbar_expect_tx(bar_ufull + 8 * stage, S::kU8);
+          if (U8 == 1) {
+            tma_load_2d(ust, &tmA_hi, k0, m0, bar_ufull + 8 * stage);  // u8 box {32 k, 128 m}
+          } else if (!A_MN) {
             tma_load_2d(off, &tmA_hi, k0, m0, full);
             if (A_LO) tma_load_2d(off + S::kA, &tmA_lo, k0, m0, full);
           } else {
@@ -322,7 +356,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           off += S::kA * (A_LO ? 2 : 1);
-          if (!B_MN) {
+          if (U8 == 2) {
+            tma_load_2d(ust, &tmB_hi, n0, k0, bar_ufull + 8 * stage);  // u8 box {BN n, 32 k}
+          } else if (!B_MN) {
             tma_load_2d(off, &tmB_hi, k0, n0, full);
             if (B_LO) tma_load_2d(off + S::kB, &tmB_lo, k0, n0, full);
           } else {
@@ -357,6 +393,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t tmem_d = tmem_base + uint32_t(acc_buf * S::kAccCols);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(bar_full + 8 * stage, phase);
+          if (U8) mbar_wait(bar_conv + 8 * stage, phase);
           tc_fence_after();
           const uint32_t a_hi = sbase + stage * S::kStage;
           const uint32_t a_lo = a_hi + S::kA;
@@ -390,6 +427,73 @@ __global__ void __launch_bounds__(kThreads, 1)
         mma_commit(bar_tfull + 8 * acc_buf);
       }
     }
+  } else if (U8 && warp >= 2 + kEpiWarps) {
+    // ===== Converter warps 6..9: uint8 staging -> fp32 operand tile (MMA layout) =====
+    const int ct = threadIdx.x - (2 + kEpiWarps) * 32;  // 0..127
+    const bool expand = U8 == 1 && p.a_expand != nullptr;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      int mt, nt, sp;
+      tm.decode(t, mt, nt, sp);
+      const int kb0 = sp * p.kb_per_split, kb1 = min(kb_total, kb0 + p.kb_per_split);
+      for (int kb = kb0; kb < kb1; ++kb) {
+        if (expand) {  // the bulk store issued from this stage's tile last round must be done
+          if (ct == 0) bulk_wait_read_n<S::kStages - 1>();
+          named_bar(2, 128);
+        }
+        mbar_wait(bar_ufull + 8 * stage, phase);
+        uint8_t* st = smem + stage * S::kStage;
+        const uint8_t* us = st + S::kStage - S::kU8;
+        if (U8 == 1) {
+          // K-major SW128: row r (128 B) holds k = 0..31; 16-B chunk c stored at c ^ (r & 7)
+          const int r = ct;
+          const uint4 u0 = *reinterpret_cast<const uint4*>(us + r * 32);
+          const uint4 u1 = *reinterpret_cast<const uint4*>(us + r * 32 + 16);
+          const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const uint32_t v = w[c];
+            *reinterpret_cast<float4*>(st + r * 128 + ((c ^ (r & 7)) << 4)) = u8x4_to_f32(v);
+          }
+        } else {
+          // MN-major SW128_BASE32B: 32-element n chunk j at j*4 KB, k row at k*128 B,
+          // 32-B atom a = (n & 31) >> 3 stored at a ^ (k & 3)
+          uint8_t* bt = st + S::kA * (A_LO ? 2 : 1);
+          // lane -> (row k within a group of 4, 16-B slot c of the 128-B row): the 8 lanes
+          // of a row cover all 8 slots, so each float4 store is one conflict-free wavefront
+          // per row.  Warp w converts k rows [8w, 8w + 8).
+          const int lane = threadIdx.x & 31, w = ct >> 5;
+          const int c = lane & 7;
+          const int a = c >> 1;  // 32-B atom of n_local = 4c
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk) {
+            const int k = 8 * w + 4 * kk + (lane >> 3);
+            const uint32_t row_off = uint32_t(k * 128 + ((a ^ (k & 3)) << 5) + (c & 1) * 16);
+#pragma unroll
+            for (int j = 0; j < BN / 32; ++j) {
+              const uint32_t v = *reinterpret_cast<const uint32_t*>(us + k * BN + j * 32 + c * 4);
+              *reinterpret_cast<float4*>(bt + j * 4096 + row_off) = u8x4_to_f32(v);
+            }
+          }
+        }
+        fence_async_smem();  // generic-proxy writes -> visible to the tensor core
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mbar_arrive(bar_conv + 8 * stage);
+        if (expand && nt == 0) {
+          named_bar(2, 128);
+          if (ct == 0) {
+            tma_store_2d(&tmAct, kb * kBK, mt * kBM, sbase + stage * S::kStage);
+            bulk_commit();
+          }
+        }
+        if (++stage == S::kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    if (expand && ct == 0) bulk_wait_all();
   } else {
     // ===== Epilogue: warps 2..5 own TMEM lane quadrants (warp % 4) =====
     // Per 32-column chunk each warp handles a 32x32 block: TMEM -> registers (thread =
@@ -557,6 +661,8 @@ struct Operand {
   const float* lo = nullptr;  // null: exact in tf32, the lo pass is skipped
   long ld = 0;                // row pitch (elements) of the stored matrix
   bool mn_major = false;      // false: stored [MN rows][K cols]; true: stored [K rows][MN cols]
+  const uint8_t* u8 = nullptr;  // set: the operand is uint8 planes (exact), hi/lo unused;
+                                // A must be K-major, B must be MN-major; ld % 16 == 0
 };
 
 struct LaunchInfo {

@@ -274,8 +274,13 @@ struct tlg_learner {
     if (cfg.timing) TLG_CUDA(cudaEventRecord(kev[kind][layer][end], stream));
   }
 
+  // uint8 observations feed the first trunk GEMM and its dW directly (converted in smem)
+  bool direct_u8() const { return net.L > 0 && net.D % 16 == 0; }
+  const uint8_t* x0_u8 = nullptr;
+
   void stage(const tlg_segment_batch& b, int on_device, tlg::BatchDev& bd, const float** obs_f32,
              bool& obs_exact) {
+    x0_u8 = nullptr;
     if (b.n_segments == 0) throw InvalidArg("empty minibatch");
     if (int(b.n_segments) > S_max) throw InvalidArg("batch exceeds the learner's max_segments");
     if (int(b.unroll_len) != T) throw InvalidArg("unroll_len mismatch");
@@ -296,8 +301,12 @@ struct tlg_learner {
       bd.boot = b.bootstrap;
       bd.valid = b.valid_steps;
       if (b.obs_dtype == TLG_OBS_U8) {
-        tlg::launch_expand_u8(static_cast<const uint8_t*>(b.obs), obs, F * D, stream);
-        ++launches;
+        if (direct_u8() && (reinterpret_cast<uintptr_t>(b.obs) & 15) == 0) {
+          x0_u8 = static_cast<const uint8_t*>(b.obs);
+        } else {
+          tlg::launch_expand_u8(static_cast<const uint8_t*>(b.obs), obs, F * D, stream);
+          ++launches;
+        }
         *obs_f32 = obs;
         obs_exact = true;
       } else {
@@ -311,8 +320,12 @@ struct tlg_learner {
     };
     if (b.obs_dtype == TLG_OBS_U8) {
       h2d(obs_u8, b.obs, size_t(F * D));
-      tlg::launch_expand_u8(obs_u8, obs, F * D, stream);
-      ++launches;
+      if (direct_u8()) {
+        x0_u8 = obs_u8;
+      } else {
+        tlg::launch_expand_u8(obs_u8, obs, F * D, stream);
+        ++launches;
+      }
       obs_exact = true;
     } else {
       h2d(obs, b.obs, size_t(F * D) * 4);
@@ -356,13 +369,15 @@ struct tlg_learner {
     using tlg::gemm::Operand;
     for (uint32_t l = 0; l < net.L; ++l) {
       const int in = int(net.dims[l]), outw = int(net.dims[l + 1]);
-      Operand A{l == 0 ? x0 : act[l - 1], l == 0 ? x0_lo : act_lo[l - 1], in, false};
+      Operand A{l == 0 ? x0 : act[l - 1], l == 0 ? x0_lo : act_lo[l - 1], in, false,
+                l == 0 ? x0_u8 : nullptr};
       Operand B{params + net.w_off[l], params_lo + net.w_off[l], in, false};
       tlg::gemm::Params p{};
       p.out_hi = act[l];
       p.out_lo = act_lo[l];
       p.ldo = outw;
       p.bias = params + net.b_off[l];
+      if (l == 0 && x0_u8) p.a_expand = obs;  // fp32 copy of the planes for dW of layer 1
       const bool fuse_head = l + 1 == net.L && fused_head();
       if (fuse_head) {  // policy/value heads in the last trunk GEMM's epilogue
         p.head_w = params + net.head.wpi;
@@ -414,7 +429,8 @@ struct tlg_learner {
       int sp = tlg::gemm::pick_splits(outw, in, int(F), kMaxSplits);
       while (long(sp) * outw * in > ws_elems && sp > 1) --sp;
       Operand A{dz[l], dz_lo[l], outw, true};
-      Operand B{xin, xin_lo, in, true};
+      // layer 1 reads the fp32 planes the forward's converter warps wrote (exact, no residual)
+      Operand B{l == 0 && x0_u8 ? obs : xin, xin_lo, in, true};
       tlg::gemm::Params p{};
       p.ws = ws;
       p.ws_split_stride = long(outw) * in;

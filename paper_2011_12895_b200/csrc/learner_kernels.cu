@@ -465,26 +465,35 @@ __global__ void __launch_bounds__(256) loss_backward_kernel(
     for (int c = 0; c < kCPT; ++c) {
       const int j = tid + 256 * c;
       if (j >= hd.H) continue;
-#pragma unroll 4
-      for (int i = 0; i < nf; ++i) {
-        const long f = f0 + i;
-        const float x = h[f * ldh + j];
-        const float* d = sdz + i * A1;
-        float dh = d[A] * w[c][A < kMaxA1 ? A : kMaxA1 - 1];
+      for (int i0 = 0; i0 < nf; i0 += 8) {
+        // batch the 8 (independent, coalesced) loads ahead of the math: memory-level
+        // parallelism is what this HBM-bound loop needs
+        float xs[8];
 #pragma unroll
-        for (int k = 0; k < kMaxA1; ++k)
-          if (k < A) {
-            dh = fmaf(d[k], w[c][k], dh);
-            acc[c][k] = fmaf(d[k], x, acc[c][k]);
+        for (int u = 0; u < 8; ++u)
+          xs[u] = (i0 + u < nf) ? __ldg(h + (f0 + i0 + u) * ldh + j) : 0.f;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (i0 + u >= nf) break;
+          const long f = f0 + i0 + u;
+          const float x = xs[u];
+          const float* d = sdz + (i0 + u) * A1;
+          float dh = d[A] * w[c][A < kMaxA1 ? A : kMaxA1 - 1];
+#pragma unroll
+          for (int k = 0; k < kMaxA1; ++k)
+            if (k < A) {
+              dh = fmaf(d[k], w[c][k], dh);
+              acc[c][k] = fmaf(d[k], x, acc[c][k]);
+            }
+#pragma unroll
+          for (int k = 0; k < kMaxA1; ++k)
+            if (k == A) acc[c][k] = fmaf(d[A], x, acc[c][k]);
+          if (dz) {
+            const float o = dh * (1.f - x * x);
+            dz[f * hd.H + j] = o;
+            dz_lo[f * hd.H + j] = o - tf32_hi(o);
+            dbacc[c] += o;
           }
-#pragma unroll
-        for (int k = 0; k < kMaxA1; ++k)
-          if (k == A) acc[c][k] = fmaf(d[A], x, acc[c][k]);
-        if (dz) {
-          const float o = dh * (1.f - x * x);
-          dz[f * hd.H + j] = o;
-          dz_lo[f * hd.H + j] = o - tf32_hi(o);
-          dbacc[c] += o;
         }
       }
     }

@@ -65,7 +65,7 @@ struct StepStatsDev {
 };
 
 constexpr int kLossFrames = 128;  // frames per loss_backward chunk
-constexpr int kLossBlocks = 296;  // persistent loss_backward blocks (2 per SM): partial rows
+constexpr int kLossBlocks = 444;  // persistent loss_backward blocks (3 per SM): partial rows
 
 void launch_expand_u8(const uint8_t* in, float* out, long n, cudaStream_t s);
 void launch_split_lo(const float* x, float* lo, long n, cudaStream_t s);

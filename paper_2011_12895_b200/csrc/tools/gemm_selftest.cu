@@ -56,14 +56,26 @@ struct Buf {
 static int failures = 0;
 
 static bool g_fullhi = false;  // feed the full fp32 plane as "hi" (tests HW tf32 truncation)
+static int g_u8 = 0;           // 1: A as uint8 planes, 2: B as uint8 planes
+
+uint8_t* to_u8(const float* d, long n) {
+  std::vector<float> h(n);
+  std::vector<uint8_t> u(n);
+  TLG_CUDA(cudaMemcpy(h.data(), d, n * 4, cudaMemcpyDeviceToHost));
+  for (long i = 0; i < n; ++i) u[i] = uint8_t(h[i]);
+  uint8_t* p;
+  TLG_CUDA(cudaMalloc(&p, n));
+  TLG_CUDA(cudaMemcpy(p, u.data(), n, cudaMemcpyHostToDevice));
+  return p;
+}
 
 void check(const char* name, int M, int N, int K, bool a_mn, bool b_mn, bool a_exact, int epi,
            int splits) {
   std::mt19937 rng(M * 131 + N * 7 + K);
   Buf A, B, act, bias;
   // A stored [M][K] (K-major) or [K][M] (MN-major); same element count
-  A.init(long(M) * K, rng, a_exact);
-  B.init(long(N) * K, rng);
+  A.init(long(M) * K, rng, a_exact || g_u8 == 1);
+  B.init(long(N) * K, rng, g_u8 == 2);
   act.init(long(M) * N, rng);
   bias.init(N, rng);
   // tanh'd activations in (-1,1)
@@ -83,6 +95,13 @@ void check(const char* name, int M, int N, int K, bool a_mn, bool b_mn, bool a_e
   TLG_CUDA(cudaMemset(ws, 0, long(splits) * M * N * 4));
   gemm::Operand oa{g_fullhi ? A.x : A.hi, a_exact ? nullptr : A.lo, lda, a_mn};
   gemm::Operand ob{g_fullhi ? B.x : B.hi, B.lo, ldb, b_mn};
+  float* expand = nullptr;
+  if (g_u8 == 1) {
+    oa.u8 = to_u8(A.x, long(M) * K);
+    TLG_CUDA(cudaMalloc(&expand, long(M) * K * 4));
+    TLG_CUDA(cudaMemset(expand, 0xff, long(M) * K * 4));
+  }
+  if (g_u8 == 2) { ob.u8 = to_u8(B.x, long(N) * K); ob.lo = nullptr; }
   gemm::Params p{};
   p.out_hi = out_hi;
   p.out_lo = out_lo;
@@ -94,6 +113,7 @@ void check(const char* name, int M, int N, int K, bool a_mn, bool b_mn, bool a_e
   p.ws = ws;
   p.ws_split_stride = long(M) * N;
   p.colsum = epi == gemm::kEpiBwdTanh ? colsum : nullptr;
+  p.a_expand = expand;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -121,6 +141,15 @@ void check(const char* name, int M, int N, int K, bool a_mn, bool b_mn, bool a_e
   TLG_CUDA(cudaMemcpy(hws.data(), ws, hws.size() * 4, cudaMemcpyDeviceToHost));
   double worst = 0;
   long bad = 0;
+  if (expand) {  // the converter's fp32 copy of the uint8 A operand must be exact
+    std::vector<float> he(long(M) * K), ha(long(M) * K);
+    TLG_CUDA(cudaMemcpy(he.data(), expand, he.size() * 4, cudaMemcpyDeviceToHost));
+    TLG_CUDA(cudaMemcpy(ha.data(), A.x, ha.size() * 4, cudaMemcpyDeviceToHost));
+    for (long i = 0; i < long(M) * K; ++i)
+      if (he[i] != ha[i]) { ++bad; }
+    if (bad) printf("  expanded A copy mismatches: %ld\n", bad);
+    cudaFree(expand);
+  }
   if (epi == gemm::kEpiBwdTanh) {
     std::vector<float> hc(long(mt) * N);
     TLG_CUDA(cudaMemcpy(hc.data(), colsum, hc.size() * 4, cudaMemcpyDeviceToHost));
@@ -182,7 +211,19 @@ int main(int argc, char** argv) {
     check("FULLHI dX bwd K/MN", 300, 256, 256, false, true, false, kEpiBwdTanh, 1);
     check("FULLHI dW store MN/MN", 256, 200, 1000, true, true, false, kEpiStore, 1);
     g_fullhi = false;
+    g_u8 = 1;
+    check("U8A fwd tanh K/K", 300, 256, 208, false, false, true, kEpiFwdTanh, 1);
+    check("U8A fwd tanh K/K N=100", 257, 100, 1936, false, false, true, kEpiFwdTanh, 1);
+    g_u8 = 2;
+    check("U8B dW store MN/MN", 256, 1936, 1000, true, true, false, kEpiStore, 3);
+    check("U8B dW store MN/MN N=64", 200, 64, 300, true, true, false, kEpiStore, 1);
+    g_u8 = 0;
     if (argc > 1) {
+      g_u8 = 1;
+      check("perf U8 fwd C3 L1", 131072, 256, 1936, false, false, true, kEpiFwdTanh, 1);
+      g_u8 = 2;
+      check("perf U8 dW C3 L1", 256, 1936, 131072, true, true, false, kEpiStore, 9);
+      g_u8 = 0;
       // throughput shapes (C3 layer 1 forward, C5 layer forward)
       check("perf fwd C3 L1", 131072, 256, 1936, false, false, true, kEpiFwdTanh, 1);
       check("perf fwd C5", 131072, 2048, 2048, false, false, false, kEpiFwdTanh, 1);
