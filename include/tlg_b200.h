@@ -163,6 +163,8 @@ void* tlg_learner_stream(tlg_learner* l);
  * [0] H2D staging, [1] forward GEMMs, [2] heads+returns+loss, [3] backward GEMMs+reductions,
  * [4] allreduce, [5] optimizer, [6] whole step.  n <= 7. */
 int tlg_learner_phase_ms(tlg_learner* l, float* out, int n);
+/* Toggle per-phase / per-GEMM event timing (timed steps launch eagerly, not as a graph). */
+int tlg_learner_set_timing(tlg_learner* l, int on);
 /* Kernel launches issued by the last train_step (this library's kernels only). */
 int tlg_learner_last_launches(tlg_learner* l);
 /* Device time (ms) of one trunk GEMM of the last step (timing mode): kind 0 = forward,

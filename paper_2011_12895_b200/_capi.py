@@ -119,6 +119,7 @@ def lib():
         L.tlg_learner_stream.argtypes = [C.c_void_p]
         L.tlg_learner_phase_ms.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
         L.tlg_learner_last_launches.argtypes = [C.c_void_p]
+        L.tlg_learner_set_timing.argtypes = [C.c_void_p, C.c_int]
         L.tlg_learner_kernel_ms.argtypes = [C.c_void_p, C.c_int, C.c_int,
                                             C.POINTER(C.c_float)]
         L.tlg_policy_create.argtypes = [C.POINTER(PolicyShape), C.c_int32, C.c_uint32,
@@ -152,7 +153,7 @@ EXPORTS = [
     "tlg_learner_set_hyper", "tlg_comm_unique_id", "tlg_learner_comm_init",
     "tlg_learner_train_step", "tlg_learner_train_step_shards", "tlg_learner_get_grad", "tlg_learner_get_returns",
     "tlg_learner_stream", "tlg_learner_phase_ms", "tlg_learner_last_launches",
-    "tlg_learner_kernel_ms",
+    "tlg_learner_kernel_ms", "tlg_learner_set_timing",
     "tlg_policy_create", "tlg_policy_destroy", "tlg_policy_set_params", "tlg_policy_forward",
     "tlg_policy_stream", "tlg_returns",
 ]
@@ -280,6 +281,9 @@ class Learner:
 
     def last_launches(self):
         return lib().tlg_learner_last_launches(self.h)
+
+    def set_timing(self, on: bool):
+        check(lib().tlg_learner_set_timing(self.h, 1 if on else 0))
 
     def kernel_ms(self, kind, layer):
         """kind: 'fwd' | 'dw' | 'dx' (0-based layer)."""

@@ -45,6 +45,7 @@ CONFIGS = {
                  note="Pommerman-shaped obs 11x11x16 binary planes, PPO, T=32 B=4096 per shard"),
     "C4": Config("C4", "infer", 64, 6, (1024, 1024), 1, 65536, seed=1004,
                  note="InferenceServer batched forward, 65,536 obs, MLP 64-1024-1024-(6,1)"),
-    "C5": Config("C5", "ppo_vtrace", 64, 6, (2048, 2048, 2048, 2048), 64, 16384, seed=1005,
-                 note="4x2048 trunk, PPO surrogate over V-trace targets, T=64 B=16384"),
+    "C5": Config("C5", "ppo_vtrace", 64, 6, (2048, 2048, 2048, 2048), 64, 2048, seed=1005,
+                 note="4x2048 trunk, PPO surrogate over V-trace targets, T=64, B=16384 over "
+                      "8 GPUs = 2048 segments per learner shard"),
 }

@@ -439,7 +439,11 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
       const int kb0 = sp * p.kb_per_split, kb1 = min(kb_total, kb0 + p.kb_per_split);
       for (int kb = kb0; kb < kb1; ++kb) {
         if (expand) {  // the bulk store issued from this stage's tile last round must be done
-          if (ct == 0) bulk_wait_read_n<S::kStages - 1>();
+          // (a tile that issues no stores must not rely on the count: wait for all)
+          if (ct == 0) {
+            if (nt == 0) bulk_wait_read_n<S::kStages - 1>();
+            else bulk_wait_read();
+          }
           named_bar(2, 128);
         }
         mbar_wait(bar_ufull + 8 * stage, phase);

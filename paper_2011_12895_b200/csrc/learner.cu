@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -203,6 +204,7 @@ struct tlg_learner {
     grad_tmp = mem.add<float>(P_pad + 4);
     adam_m = mem.add<float>(P_pad);
     adam_v = mem.add<float>(P_pad);
+    adam_t_dev = mem.add<uint64_t>(1);
     const long D = net.D;
     obs = mem.add<float>(F_max * D);
     obs_lo = mem.add<float>(F_max * D);
@@ -247,14 +249,14 @@ struct tlg_learner {
     TLG_CUDA(cudaMallocHost(&h_stats, kMaxLocalShards * sizeof(tlg::StepStatsDev)));
     TLG_CUDA(cudaMallocHost(&h_flags, 16));
     for (auto& e : ev) TLG_CUDA(cudaEventCreate(&e));
-    if (cfg.timing)
-      for (auto& a : kev)
-        for (auto& b : a)
-          for (auto& e : b) TLG_CUDA(cudaEventCreate(&e));
+    for (auto& a : kev)
+      for (auto& b : a)
+        for (auto& e : b) TLG_CUDA(cudaEventCreate(&e));
   }
 
   ~tlg_learner() {
     if (stream) cudaStreamSynchronize(stream);
+    if (graph_exec) cudaGraphExecDestroy(graph_exec);
     if (comm) ncclCommDestroy(comm);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
@@ -279,7 +281,7 @@ struct tlg_learner {
   const uint8_t* x0_u8 = nullptr;
 
   void stage(const tlg_segment_batch& b, int on_device, tlg::BatchDev& bd, const float** obs_f32,
-             bool& obs_exact) {
+             bool& obs_exact, bool internal = false) {
     x0_u8 = nullptr;
     if (b.n_segments == 0) throw InvalidArg("empty minibatch");
     if (int(b.n_segments) > S_max) throw InvalidArg("batch exceeds the learner's max_segments");
@@ -292,7 +294,7 @@ struct tlg_learner {
     const long S = b.n_segments, F = S * T, D = net.D;
     bd.S = int(S);
     bd.T = T;
-    if (on_device) {
+    if (on_device && !internal) {
       bd.action = b.action;
       bd.reward = b.reward;
       bd.blogp = b.behavior_logp;
@@ -316,7 +318,9 @@ struct tlg_learner {
       return;
     }
     auto h2d = [&](void* dst, const void* src, size_t bytes) {
-      TLG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream));
+      TLG_CUDA(cudaMemcpyAsync(dst, src, bytes,
+                               on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                               stream));
     };
     if (b.obs_dtype == TLG_OBS_U8) {
       h2d(obs_u8, b.obs, size_t(F * D));
@@ -348,13 +352,31 @@ struct tlg_learner {
     bd.valid = valid;
   }
 
-  // One shard's forward/backward; its gradient lands in `gtarget` (learner.cpp:117-134).
-  void run_shard(const tlg_segment_batch& b, int on_device, int shard, float* gtarget) {
-    tlg::StepStatsDev* st = stats + shard;
+  struct Staged {
     tlg::BatchDev bd{};
     const float* x0 = nullptr;
-    bool obs_exact = false;
-    stage(b, on_device, bd, &x0, obs_exact);
+    const uint8_t* x0_u8 = nullptr;
+    bool exact = false;
+  };
+
+  Staged stage_shard(const tlg_segment_batch& b, int on_device, bool internal) {
+    Staged sg;
+    stage(b, on_device, sg.bd, &sg.x0, sg.exact, internal);
+    sg.x0_u8 = x0_u8;
+    return sg;
+  }
+
+  // One shard's forward/backward; its gradient lands in `gtarget` (learner.cpp:117-134).
+  void run_shard(const tlg_segment_batch& b, int on_device, int shard, float* gtarget) {
+    compute_shard(stage_shard(b, on_device, false), shard, gtarget);
+  }
+
+  void compute_shard(const Staged& sg, int shard, float* gtarget) {
+    tlg::StepStatsDev* st = stats + shard;
+    const tlg::BatchDev bd = sg.bd;
+    const float* x0 = sg.x0;
+    const bool obs_exact = sg.exact;
+    x0_u8 = sg.x0_u8;
     S_last = bd.S;
     const long F = long(bd.S) * T;
     const long D = net.D;
@@ -474,35 +496,75 @@ struct tlg_learner {
   }
 
   // Learner::TrainStep over `n` local shards (+ the communicator's other ranks).
+  // Small steps are launch-bound: after staging into the learner's own buffers, the
+  // whole device step (kernels, allreduce, optimizer, stats D2H) replays as one CUDA graph.
+  bool use_graph(const tlg_segment_batch* bs, int n) const {
+    if (cfg.timing || n != 1 || graph_disabled) return false;
+    const long F = long(bs[0].n_segments) * T;
+    return F * long(net.D) <= (8L << 20);
+  }
+
   void step(const tlg_segment_batch* bs, int n, int on_device, tlg_step_stats* out) {
     if (!hp_set) throw InvalidArg("hyperparameters not set");
     if (n < 1 || n > kMaxLocalShards) throw InvalidArg("1..64 local shards per call");
     launches = 0;
     TLG_CUDA(cudaSetDevice(cfg.device));
+    if (use_graph(bs, n)) {
+      const Staged sg = stage_shard(bs[0], on_device, /*internal=*/true);
+      const long key = long(sg.bd.S) * 4 + (sg.x0_u8 ? 1 : 0) + (sg.exact ? 2 : 0);
+      if (!graph_exec || key != graph_key || graph_hyper != hyper_version) {
+        if (graph_exec) cudaGraphExecDestroy(graph_exec);
+        graph_exec = nullptr;
+        cudaGraph_t g;
+        TLG_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+        enqueue_device_step(&sg, 1);
+        TLG_CUDA(cudaStreamEndCapture(stream, &g));
+        TLG_CUDA(cudaGraphInstantiate(&graph_exec, g, 0));
+        cudaGraphDestroy(g);
+        graph_key = key;
+        graph_hyper = hyper_version;
+        graph_launches = launches;
+      }
+      TLG_CUDA(cudaGraphLaunch(graph_exec, stream));
+      launches = graph_launches;
+    } else {
+      enqueue_device_step(nullptr, n, bs, on_device);
+    }
+    finish(n, out);
+  }
+
+  // Everything after staging: per-shard compute, allreduce, optimizer, stats D2H.
+  void enqueue_device_step(const Staged* staged, int n, const tlg_segment_batch* bs = nullptr,
+                           int on_device = 0) {
+    launches = 0;
     mark(0);
     TLG_CUDA(cudaMemsetAsync(err, 0, 16, stream));
     TLG_CUDA(cudaMemsetAsync(grad + P_pad, 0, 16, stream));
-    for (int r = 0; r < n; ++r) run_shard(bs[r], on_device, r, r == 0 ? grad : grad_tmp);
+    for (int r = 0; r < n; ++r) {
+      if (staged) compute_shard(staged[r], r, r == 0 ? grad : grad_tmp);
+      else run_shard(bs[r], on_device, r, r == 0 ? grad : grad_tmp);
+    }
     mark(4);
     // ---- allreduce over ranks (learner.cpp:138-149); the guard slot rides along
     if (nranks > 1) {
       NCCL_CHECK(ncclAllReduce(grad, grad, size_t(P_pad + 4), ncclFloat, ncclSum, comm, stream));
     }
     mark(5);
-    // ---- optimizer (skipped on device when any shard of any rank failed)
+    // ---- optimizer (skipped on device when any shard of any rank failed); the Adam step
+    // counter lives on the device so a captured graph replays correctly
     const bool adam = cfg.optimizer == TLG_OPT_ADAM;
-    const uint64_t t = adam_t + 1;
-    const double bc1 = 1.0 - std::pow(cfg.adam_beta1, double(t));
-    const double bc2 = 1.0 - std::pow(cfg.adam_beta2, double(t));
     grad_scale = 1.f / float(n * nranks);
-    launch_guarded_optimizer(adam, float(hp.learning_rate), float(hp.learning_rate / bc1),
-                             float(std::sqrt(bc2)));
+    launch_guarded_optimizer(adam, float(hp.learning_rate));
     mark(6);
     // ---- results
     TLG_CUDA(cudaMemcpyAsync(h_stats, stats, n * sizeof(tlg::StepStatsDev),
                              cudaMemcpyDeviceToHost, stream));
     TLG_CUDA(cudaMemcpyAsync(h_flags, err, 4, cudaMemcpyDeviceToHost, stream));
     TLG_CUDA(cudaMemcpyAsync(h_flags + 1, grad + P_pad, 4, cudaMemcpyDeviceToHost, stream));
+  }
+
+  void finish(int n, tlg_step_stats* out) {
+    const bool adam = cfg.optimizer == TLG_OPT_ADAM;
     TLG_CUDA(cudaStreamSynchronize(stream));
     const int e = h_flags[0];
     float guard;
@@ -519,7 +581,7 @@ struct tlg_learner {
         throw RuntimeErr("non-finite loss at update step " + std::to_string(k));
     if (guard != 0.f)
       throw RuntimeErr("learner shard failed on another rank at update step " + std::to_string(k));
-    if (adam) adam_t = t;
+    if (adam) ++adam_t;
     steps_done = k;
     if (out) {
       for (int r = 0; r < n; ++r) {
@@ -539,7 +601,13 @@ struct tlg_learner {
   int colsum_rows = 0;
   int head_tiles = 1;
   void set_guard(int shard);
-  void launch_guarded_optimizer(bool adam, float lr, float step_size, float bc2_sqrt);
+  void launch_guarded_optimizer(bool adam, float lr);
+  cudaGraphExec_t graph_exec = nullptr;
+  long graph_key = -1;
+  uint64_t hyper_version = 0, graph_hyper = ~0ull;
+  int graph_launches = 0;
+  bool graph_disabled = std::getenv("TLG_NO_GRAPH") != nullptr;
+  uint64_t* adam_t_dev = nullptr;
 };
 
 namespace {
@@ -564,9 +632,15 @@ __global__ void accumulate_kernel(float4* __restrict__ g, const float4* __restri
 __global__ void optimizer_guarded_kernel(float4* __restrict__ p, float4* __restrict__ plo,
                                          const float4* __restrict__ g, float4* __restrict__ m,
                                          float4* __restrict__ v, long n4, const float* guard,
-                                         float grad_scale, int adam, float lr, float step_size,
-                                         float bc2_sqrt, float b1, float b2, float eps) {
+                                         float grad_scale, int adam, float lr,
+                                         const uint64_t* adam_t, double b1d, double b2d,
+                                         float eps) {
   if (*guard != 0.f) return;  // some shard failed: parameters stay untouched
+  // torch.optim.Adam bias corrections for step t = (completed steps) + 1
+  const double t = double(*adam_t + 1);
+  const float step_size = float(double(lr) / (1.0 - pow(b1d, t)));
+  const float bc2_sqrt = float(sqrt(1.0 - pow(b2d, t)));
+  const float b1 = float(b1d), b2 = float(b2d);
   for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n4;
        i += long(gridDim.x) * blockDim.x) {
     float4 pp = p[i];
@@ -597,6 +671,10 @@ __global__ void optimizer_guarded_kernel(float4* __restrict__ p, float4* __restr
   }
 }
 
+__global__ void advance_step_kernel(const float* guard, uint64_t* adam_t) {
+  if (*guard == 0.f) *adam_t += 1;
+}
+
 __global__ void split_lo_flat(const float* x, float* lo, long n) {
   long i = blockIdx.x * long(blockDim.x) + threadIdx.x;
   if (i < n) lo[i] = x[i] - tlg::tf32_hi(x[i]);
@@ -619,16 +697,18 @@ void tlg_learner::accumulate_grad() {
   ++launches;
 }
 
-void tlg_learner::launch_guarded_optimizer(bool adam, float lr, float step_size, float bc2_sqrt) {
+void tlg_learner::launch_guarded_optimizer(bool adam, float lr) {
   const long n4 = P_pad / 4;
   const int blocks = int(std::max<long>(1, std::min<long>((n4 + 255) / 256, 148L * 4)));
   optimizer_guarded_kernel<<<blocks, 256, 0, stream>>>(
       reinterpret_cast<float4*>(params), reinterpret_cast<float4*>(params_lo),
       reinterpret_cast<const float4*>(grad), reinterpret_cast<float4*>(adam_m),
       reinterpret_cast<float4*>(adam_v), n4, grad + P_pad, grad_scale, adam ? 1 : 0, lr,
-      step_size, bc2_sqrt, float(cfg.adam_beta1), float(cfg.adam_beta2), float(cfg.adam_eps));
+      adam_t_dev, cfg.adam_beta1, cfg.adam_beta2, float(cfg.adam_eps));
   TLG_CHECK_LAUNCH();
-  ++launches;
+  advance_step_kernel<<<1, 1, 0, stream>>>(grad + P_pad, adam_t_dev);
+  TLG_CHECK_LAUNCH();
+  launches += 2;
 }
 
 // ===========================================================================
@@ -732,6 +812,7 @@ int tlg_learner_set_params(tlg_learner* l, const double* values, size_t n) {
     set_params_common(l->params, l->params_lo, l->net.P, l->P_pad, values, n, l->stream);
     TLG_CUDA(cudaMemsetAsync(l->adam_m, 0, l->P_pad * 4, l->stream));
     TLG_CUDA(cudaMemsetAsync(l->adam_v, 0, l->P_pad * 4, l->stream));
+    TLG_CUDA(cudaMemsetAsync(l->adam_t_dev, 0, 8, l->stream));
     TLG_CUDA(cudaStreamSynchronize(l->stream));
     l->adam_t = 0;
   });
@@ -784,6 +865,7 @@ int tlg_learner_set_hyper(tlg_learner* l, const tlg_hyper* hp) {
       throw InvalidArg("teacher params required when kl_teacher_coef > 0");
     l->hp = *hp;
     l->hp_set = true;
+    ++l->hyper_version;
   });
 }
 
@@ -806,6 +888,7 @@ int tlg_learner_comm_init(tlg_learner* l, const uint8_t unique_id[128], int nran
     }
     l->nranks = nranks;
     l->rank = rank;
+    ++l->hyper_version;  // re-capture: the step graph embeds the communicator
     if (nranks > 1) {
       ncclUniqueId id;
       std::memcpy(&id, unique_id, 128);
@@ -842,6 +925,10 @@ int tlg_learner_phase_ms(tlg_learner* l, float* out, int n) {
 }
 
 int tlg_learner_last_launches(tlg_learner* l) { return l ? l->launches : 0; }
+
+int tlg_learner_set_timing(tlg_learner* l, int on) {
+  return Guard([&] { l->cfg.timing = on ? 1 : 0; });
+}
 
 int tlg_learner_kernel_ms(tlg_learner* l, int kind, int layer, float* ms) {
   return Guard([&] {

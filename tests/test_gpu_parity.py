@@ -368,3 +368,21 @@ def test_gpu_learner_follows_reference_learner_trajectory(tlg, golden, ref, name
             assert close(got, want, 1e-4), (name, s, worst(got, want))
     finally:
         L.ref_replay_destroy(h)
+
+
+def test_cuda_graph_replay_matches_eager_launches(tlg, oracle, monkeypatch):
+    """Small steps replay as one captured CUDA graph; results must be bit-identical to the
+    eagerly launched step (TLG_NO_GRAPH), including Adam's device-side step counter."""
+    S, T, D, A, hidden = 8, 16, 64, 6, (128, 128)
+    p = init_params(oracle, Shape(2, D, A, hidden), 12)
+    out = []
+    for no_graph in (False, True):
+        if no_graph:
+            monkeypatch.setenv("TLG_NO_GRAPH", "1")
+        lrn = tlg.Learner("mlp", D, A, hidden, max_segments=S, unroll_len=T, optimizer="adam")
+        lrn.set_hyper(learning_rate=1e-3, batch_size=S, unroll_len=T)
+        lrn.set_params(p)
+        stats = [lrn.train_step(make_batch(tlg, S, T, D, A, seed=40 + k)) for k in range(4)]
+        out.append((lrn.get_params(), stats))
+    assert np.array_equal(out[0][0], out[1][0])
+    assert out[0][1] == out[1][1]
