@@ -64,6 +64,7 @@ extern "C" {
 
 #define TLG_OBS_F32 0
 #define TLG_OBS_U8 1 /* exact integer planes (e.g. Pommerman 0/1 features) */
+#define TLG_OBS_BITS 2 /* 0/1 planes bit-packed LSB-first, ceil(obs_dim/8) bytes per frame */
 
 /* Flat layout (family MLP): [W_1 (h1 x d), b_1, ..., W_L, b_L | W_pi (A x hL), b_pi |
  * w_v (hL), b_v], W row-major [out x in].  Tabular/linear keep the reference layout
@@ -153,6 +154,12 @@ int tlg_learner_train_step(tlg_learner* l, const tlg_segment_batch* batch, int o
  * scaled by 1/(n_shards * nranks).  stats receives one entry per local shard. */
 int tlg_learner_train_step_shards(tlg_learner* l, const tlg_segment_batch* shards, int n_shards,
                                   int on_device, tlg_step_stats* stats);
+/* Pipelined host input: tlg_learner_stage queues an asynchronous H2D copy of a host
+ * batch (pinned memory; it must stay valid until the step that consumes it returns)
+ * into one of two device staging slots on a copy stream, so the transfer of step k+1
+ * overlaps step k; tlg_learner_train_staged runs one step on the oldest staged batch. */
+int tlg_learner_stage(tlg_learner* l, const tlg_segment_batch* host_batch);
+int tlg_learner_train_staged(tlg_learner* l, tlg_step_stats* stats);
 /* The averaged gradient of the last step (f32 -> f64), for parity checks. */
 int tlg_learner_get_grad(tlg_learner* l, double* out, size_t n);
 /* Per-frame advantages / value targets of the last step ([S][T], f32, padding = 0). */

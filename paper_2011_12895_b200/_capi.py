@@ -114,6 +114,8 @@ def lib():
                                              C.POINTER(StepStats)]
         L.tlg_learner_train_step_shards.argtypes = [C.c_void_p, C.POINTER(SegmentBatchC), C.c_int,
                                                     C.c_int, C.POINTER(StepStats)]
+        L.tlg_learner_stage.argtypes = [C.c_void_p, C.POINTER(SegmentBatchC)]
+        L.tlg_learner_train_staged.argtypes = [C.c_void_p, C.POINTER(StepStats)]
         L.tlg_learner_get_returns.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t]
         L.tlg_learner_stream.restype = C.c_void_p
         L.tlg_learner_stream.argtypes = [C.c_void_p]
@@ -151,7 +153,8 @@ EXPORTS = [
     "tlg_last_error", "tlg_version", "tlg_host_alloc", "tlg_host_free", "tlg_learner_create", "tlg_learner_destroy",
     "tlg_learner_param_count", "tlg_learner_set_params", "tlg_learner_get_params",
     "tlg_learner_set_hyper", "tlg_comm_unique_id", "tlg_learner_comm_init",
-    "tlg_learner_train_step", "tlg_learner_train_step_shards", "tlg_learner_get_grad", "tlg_learner_get_returns",
+    "tlg_learner_train_step", "tlg_learner_train_step_shards", "tlg_learner_get_grad",
+    "tlg_learner_stage", "tlg_learner_train_staged", "tlg_learner_get_returns",
     "tlg_learner_stream", "tlg_learner_phase_ms", "tlg_learner_last_launches",
     "tlg_learner_kernel_ms", "tlg_learner_set_timing",
     "tlg_policy_create", "tlg_policy_destroy", "tlg_policy_set_params", "tlg_policy_forward",
@@ -164,9 +167,10 @@ def _ptr(a):
 
 
 class SegmentBatchView:
-    """Keeps host arrays alive and exposes the C struct (host pointers)."""
+    """Keeps host arrays alive and exposes the C struct (host pointers).  `bits=True`:
+    b.obs holds 0/1 planes bit-packed LSB-first (synth.pack_bits), obs_dim given."""
 
-    def __init__(self, b):
+    def __init__(self, b, bits=False, obs_dim=None):
         self.arrs = dict(
             obs=np.ascontiguousarray(b.obs),
             action=np.ascontiguousarray(b.action, np.int32),
@@ -180,7 +184,8 @@ class SegmentBatchView:
         if o.dtype not in (np.float32, np.uint8):
             self.arrs["obs"] = o = o.astype(np.float32)
         S, T = self.arrs["action"].shape
-        self.c = SegmentBatchC(S, T, o.shape[2], 1 if o.dtype == np.uint8 else 0,
+        self.c = SegmentBatchC(S, T, obs_dim if bits else o.shape[2],
+                               2 if bits else (1 if o.dtype == np.uint8 else 0),
                                *(self.arrs[k].ctypes.data for k in (
                                    "obs", "action", "reward", "behavior_logp", "value_est",
                                    "done", "bootstrap", "valid_steps")))
@@ -264,6 +269,15 @@ class Learner:
         check(lib().tlg_learner_train_step_shards(self.h, arr, len(views), 1 if on_device else 0,
                                                   sts))
         return [s.as_dict() for s in sts]
+
+    def stage(self, batch_view):
+        """Queue the async H2D of a host batch (keep `batch_view` alive until trained)."""
+        check(lib().tlg_learner_stage(self.h, C.byref(batch_view.c)))
+
+    def train_staged(self):
+        st = StepStats()
+        check(lib().tlg_learner_train_staged(self.h, C.byref(st)))
+        return st.as_dict()
 
     def get_returns(self, n_frames):
         adv = np.zeros(n_frames, np.float32)

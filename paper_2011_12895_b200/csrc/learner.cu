@@ -157,6 +157,7 @@ struct tlg_learner {
   // batch
   float *obs, *obs_lo;
   uint8_t* obs_u8;
+  uint8_t* obs_bits;
   int32_t* action;
   float *reward, *blogp, *value;
   uint8_t* done;
@@ -208,7 +209,9 @@ struct tlg_learner {
     const long D = net.D;
     obs = mem.add<float>(F_max * D);
     obs_lo = mem.add<float>(F_max * D);
-    obs_u8 = cfg.obs_dtype == TLG_OBS_U8 ? mem.add<uint8_t>(F_max * D + 16) : nullptr;
+    obs_u8 = cfg.obs_dtype != TLG_OBS_F32 ? mem.add<uint8_t>(F_max * D + 16) : nullptr;
+    obs_bits = cfg.obs_dtype != TLG_OBS_F32 ? mem.add<uint8_t>(F_max * ((D + 7) / 8) + 16)
+                                            : nullptr;
     action = mem.add<int32_t>(F_max);
     reward = mem.add<float>(F_max);
     blogp = mem.add<float>(F_max);
@@ -257,6 +260,14 @@ struct tlg_learner {
   ~tlg_learner() {
     if (stream) cudaStreamSynchronize(stream);
     if (graph_exec) cudaGraphExecDestroy(graph_exec);
+    if (copy_stream) {
+      cudaStreamSynchronize(copy_stream);
+      cudaStreamDestroy(copy_stream);
+    }
+    for (auto& sl : slots) {
+      if (sl.ready) cudaEventDestroy(sl.ready);
+      if (sl.consumed) cudaEventDestroy(sl.consumed);
+    }
     if (comm) ncclCommDestroy(comm);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
@@ -287,13 +298,36 @@ struct tlg_learner {
     if (int(b.n_segments) > S_max) throw InvalidArg("batch exceeds the learner's max_segments");
     if (int(b.unroll_len) != T) throw InvalidArg("unroll_len mismatch");
     if (b.obs_dim != net.D) throw InvalidArg("observation size does not match policy shape");
-    if (b.obs_dtype != TLG_OBS_F32 && b.obs_dtype != TLG_OBS_U8)
+    if (b.obs_dtype != TLG_OBS_F32 && b.obs_dtype != TLG_OBS_U8 && b.obs_dtype != TLG_OBS_BITS)
       throw InvalidArg("unknown obs dtype");
-    if (b.obs_dtype == TLG_OBS_U8 && obs_u8 == nullptr)
-      throw InvalidArg("learner not configured for uint8 observations");
+    if (b.obs_dtype != TLG_OBS_F32 && obs_u8 == nullptr)
+      throw InvalidArg("learner not configured for uint8 / bit-packed observations");
     const long S = b.n_segments, F = S * T, D = net.D;
     bd.S = int(S);
     bd.T = T;
+    if (b.obs_dtype == TLG_OBS_BITS) {
+      // bit-packed 0/1 planes (LSB first, ceil(D/8) bytes per frame): unpack to uint8
+      const long rowb = (D + 7) / 8;
+      const uint8_t* bits = static_cast<const uint8_t*>(b.obs);
+      if (!on_device) {
+        TLG_CUDA(cudaMemcpyAsync(obs_bits, bits, size_t(F * rowb), cudaMemcpyHostToDevice, stream));
+        bits = obs_bits;
+      }
+      tlg::launch_unpack_bits(bits, rowb, F, D, obs_u8, stream);
+      ++launches;
+      tlg_segment_batch u = b;
+      u.obs_dtype = TLG_OBS_U8;
+      u.obs = obs_u8;
+      // the remaining arrays follow the caller's residency; obs now lives on the device
+      stage_rest(u, on_device, internal, bd, obs_f32, obs_exact, /*obs_on_device=*/true);
+      return;
+    }
+    stage_rest(b, on_device, internal, bd, obs_f32, obs_exact, on_device != 0);
+  }
+
+  void stage_rest(const tlg_segment_batch& b, int on_device, bool internal, tlg::BatchDev& bd,
+                  const float** obs_f32, bool& obs_exact, bool obs_on_device) {
+    const long S = b.n_segments, F = S * T, D = net.D;
     if (on_device && !internal) {
       bd.action = b.action;
       bd.reward = b.reward;
@@ -323,7 +357,10 @@ struct tlg_learner {
                                stream));
     };
     if (b.obs_dtype == TLG_OBS_U8) {
-      h2d(obs_u8, b.obs, size_t(F * D));
+      if (b.obs != obs_u8)
+        TLG_CUDA(cudaMemcpyAsync(obs_u8, b.obs, size_t(F * D),
+                                 obs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                 stream));
       if (direct_u8()) {
         x0_u8 = obs_u8;
       } else {
@@ -504,7 +541,8 @@ struct tlg_learner {
     return F * long(net.D) <= (8L << 20);
   }
 
-  void step(const tlg_segment_batch* bs, int n, int on_device, tlg_step_stats* out) {
+  void step(const tlg_segment_batch* bs, int n, int on_device, tlg_step_stats* out,
+            cudaEvent_t consumed = nullptr) {
     if (!hp_set) throw InvalidArg("hyperparameters not set");
     if (n < 1 || n > kMaxLocalShards) throw InvalidArg("1..64 local shards per call");
     launches = 0;
@@ -530,7 +568,83 @@ struct tlg_learner {
     } else {
       enqueue_device_step(nullptr, n, bs, on_device);
     }
+    if (consumed) TLG_CUDA(cudaEventRecord(consumed, stream));
     finish(n, out);
+  }
+
+  // ---- asynchronous staging: H2D of the next batch overlaps the current step
+  struct Slot {
+    void* obs = nullptr;
+    size_t obs_bytes = 0;
+    int32_t* action = nullptr;
+    float *reward = nullptr, *blogp = nullptr, *value = nullptr, *boot = nullptr;
+    uint8_t* done = nullptr;
+    int32_t* valid = nullptr;
+    cudaEvent_t ready = nullptr, consumed = nullptr;
+    tlg_segment_batch dev{};
+  };
+  Slot slots[2];
+  int slot_next = 0, slot_count = 0, slot_head = 0;
+  cudaStream_t copy_stream = nullptr;
+
+  void stage_async(const tlg_segment_batch& b) {
+    if (slot_count == 2) throw InvalidArg("both staging slots hold untrained batches");
+    if (int(b.n_segments) > S_max || b.n_segments == 0) throw InvalidArg("bad batch size");
+    if (int(b.unroll_len) != T) throw InvalidArg("unroll_len mismatch");
+    if (!copy_stream) TLG_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+    Slot& sl = slots[slot_next];
+    const long S = b.n_segments, F = S * T, D = net.D;
+    const size_t ob = b.obs_dtype == TLG_OBS_F32 ? size_t(F * D) * 4
+                      : b.obs_dtype == TLG_OBS_U8 ? size_t(F * D)
+                                                  : size_t(F * ((D + 7) / 8));
+    if (!sl.ready) {
+      TLG_CUDA(cudaEventCreateWithFlags(&sl.ready, cudaEventDisableTiming));
+      TLG_CUDA(cudaEventCreateWithFlags(&sl.consumed, cudaEventDisableTiming));
+      sl.action = mem.add<int32_t>(F_max);
+      sl.reward = mem.add<float>(F_max);
+      sl.blogp = mem.add<float>(F_max);
+      sl.value = mem.add<float>(F_max);
+      sl.done = mem.add<uint8_t>(F_max);
+      sl.boot = mem.add<float>(S_max);
+      sl.valid = mem.add<int32_t>(S_max);
+    }
+    if (sl.obs_bytes < ob) {
+      sl.obs = mem.add<uint8_t>(ob + 16);
+      sl.obs_bytes = ob;
+    }
+    TLG_CUDA(cudaStreamWaitEvent(copy_stream, sl.consumed, 0));
+    auto cp = [&](void* dst, const void* src, size_t bytes) {
+      TLG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, copy_stream));
+    };
+    cp(sl.obs, b.obs, ob);
+    cp(sl.action, b.action, F * 4);
+    cp(sl.reward, b.reward, F * 4);
+    cp(sl.blogp, b.behavior_logp, F * 4);
+    cp(sl.value, b.value_est, F * 4);
+    cp(sl.done, b.done, F);
+    cp(sl.boot, b.bootstrap, S * 4);
+    cp(sl.valid, b.valid_steps, S * 4);
+    TLG_CUDA(cudaEventRecord(sl.ready, copy_stream));
+    sl.dev = b;
+    sl.dev.obs = sl.obs;
+    sl.dev.action = sl.action;
+    sl.dev.reward = sl.reward;
+    sl.dev.behavior_logp = sl.blogp;
+    sl.dev.value_est = sl.value;
+    sl.dev.done = sl.done;
+    sl.dev.bootstrap = sl.boot;
+    sl.dev.valid_steps = sl.valid;
+    slot_next ^= 1;
+    ++slot_count;
+  }
+
+  void train_staged(tlg_step_stats* out) {
+    if (slot_count == 0) throw InvalidArg("no staged batch");
+    Slot& sl = slots[slot_head];
+    slot_head ^= 1;
+    --slot_count;
+    TLG_CUDA(cudaStreamWaitEvent(stream, sl.ready, 0));
+    step(&sl.dev, 1, /*on_device=*/1, out, sl.consumed);
   }
 
   // Everything after staging: per-shard compute, allreduce, optimizer, stats D2H.
@@ -910,6 +1024,20 @@ int tlg_learner_train_step_shards(tlg_learner* l, const tlg_segment_batch* shard
   return Guard([&] {
     if (!l || !shards) throw InvalidArg("null argument");
     l->step(shards, n_shards, on_device, stats);
+  });
+}
+
+int tlg_learner_stage(tlg_learner* l, const tlg_segment_batch* host_batch) {
+  return Guard([&] {
+    TLG_CUDA(cudaSetDevice(l->cfg.device));
+    l->stage_async(*host_batch);
+  });
+}
+
+int tlg_learner_train_staged(tlg_learner* l, tlg_step_stats* stats) {
+  return Guard([&] {
+    TLG_CUDA(cudaSetDevice(l->cfg.device));
+    l->train_staged(stats);
   });
 }
 

@@ -24,6 +24,25 @@ __global__ void expand_u8_kernel(const uchar4* __restrict__ in, float4* __restri
   }
 }
 
+// Bit-packed 0/1 observation planes -> uint8 (one thread per packed byte).
+__global__ void unpack_bits_kernel(const uint8_t* __restrict__ bits, long rowb, long F, long D,
+                                   uint8_t* __restrict__ out) {
+  for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < F * rowb;
+       i += long(gridDim.x) * blockDim.x) {
+    const long f = i / rowb, j = i % rowb;
+    const uint32_t v = bits[i];
+    uint8_t* o = out + f * D + 8 * j;
+    if (8 * j + 8 <= D && ((reinterpret_cast<uintptr_t>(o) & 7) == 0)) {
+      uint2 w;
+      w.x = (v & 1u) | ((v >> 1) & 1u) << 8 | ((v >> 2) & 1u) << 16 | ((v >> 3) & 1u) << 24;
+      w.y = ((v >> 4) & 1u) | ((v >> 5) & 1u) << 8 | ((v >> 6) & 1u) << 16 | ((v >> 7) & 1u) << 24;
+      *reinterpret_cast<uint2*>(o) = w;
+    } else {
+      for (int q = 0; q < 8 && 8 * j + q < D; ++q) o[q] = (v >> q) & 1u;
+    }
+  }
+}
+
 __global__ void split_lo_kernel(const float4* __restrict__ x, float4* __restrict__ lo, long n4) {
   for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n4; i += long(gridDim.x) * blockDim.x) {
     const float4 v = x[i];
@@ -705,6 +724,12 @@ int grid_for(long n, int threads, int per_sm = 8) {
 void launch_expand_u8(const uint8_t* in, float* out, long n, cudaStream_t s) {
   expand_u8_kernel<<<grid_for(n / 4, 256), 256, 0, s>>>(reinterpret_cast<const uchar4*>(in),
                                                         reinterpret_cast<float4*>(out), n / 4);
+  TLG_CHECK_LAUNCH();
+}
+
+void launch_unpack_bits(const uint8_t* bits, long rowb, long F, long D, uint8_t* out,
+                        cudaStream_t s) {
+  unpack_bits_kernel<<<grid_for(F * rowb, 256), 256, 0, s>>>(bits, rowb, F, D, out);
   TLG_CHECK_LAUNCH();
 }
 

@@ -118,3 +118,8 @@ def init_params_f32(n_params: int, scale: float, seed: int) -> np.ndarray:
     host layer for the tabular/linear families)."""
     rng = np.random.default_rng(seed)
     return rng.uniform(-scale, scale, size=n_params).astype(np.float32)
+
+
+def pack_bits(obs_u8: np.ndarray) -> np.ndarray:
+    """0/1 planes [..., D] -> LSB-first packed bytes [..., ceil(D/8)] (TLG_OBS_BITS)."""
+    return np.ascontiguousarray(np.packbits(obs_u8.astype(np.uint8), axis=-1, bitorder="little"))

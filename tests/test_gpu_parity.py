@@ -386,3 +386,40 @@ def test_cuda_graph_replay_matches_eager_launches(tlg, oracle, monkeypatch):
         out.append((lrn.get_params(), stats))
     assert np.array_equal(out[0][0], out[1][0])
     assert out[0][1] == out[1][1]
+
+
+@pytest.mark.parametrize("D", [64, 1936, 40])
+def test_bit_packed_and_staged_inputs_match(tlg, oracle, D):
+    """TLG_OBS_BITS planes and the pipelined stage/train_staged path give bit-identical
+    steps to plain uint8 host batches."""
+    from paper_2011_12895_b200._capi import SegmentBatchView
+    S, T, A, hidden = 8, 8, 6, (32,)
+    p = init_params(oracle, Shape(2, D, A, hidden), 3)
+    batches = [tlg.synth.make_segments(S, T, D, A, seed=70 + k, obs_kind="binary", obs_u8=True)
+               for k in range(3)]
+    res = []
+    for mode in ("u8", "bits", "staged"):
+        lrn = tlg.Learner("mlp", D, A, hidden, max_segments=S, unroll_len=T, obs_u8=True,
+                          optimizer="adam")
+        lrn.set_hyper(learning_rate=1e-3, batch_size=S, unroll_len=T)
+        lrn.set_params(p)
+        views = []
+        for b in batches:
+            if mode == "u8":
+                lrn.train_step(b)
+            else:
+                pb = b.slice(0, S)
+                pb.obs = tlg.synth.pack_bits(b.obs)
+                v = SegmentBatchView(pb, bits=True, obs_dim=D)
+                views.append(v)
+                if mode == "bits":
+                    lrn.train_step(v)
+        if mode == "staged":
+            lrn.stage(views[0])
+            for k in range(len(views)):
+                if k + 1 < len(views):
+                    lrn.stage(views[k + 1])
+                lrn.train_staged()
+        res.append(lrn.get_params())
+    assert np.array_equal(res[0], res[1])
+    assert np.array_equal(res[0], res[2])
