@@ -89,6 +89,8 @@ CUtensorMap operand_map(const float* ptr, const Operand& op, long mn, long k, in
   return make_map(ptr, mn, k, op.ld, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
 }
 
+thread_local int g_cg = 1;  // CTA-pair mode chosen by launch() for the current call
+
 int num_sms() {
   static int n = 0;
   if (n == 0) {
@@ -103,22 +105,38 @@ struct EpiMaps {
   CUtensorMap out, out_lo, act;
 };
 
-template <int BN, bool A_MN, bool B_MN, bool A_LO, bool B_LO, int EPI, int U8 = 0>
+template <int BN, bool A_MN, bool B_MN, bool A_LO, bool B_LO, int EPI, int U8 = 0, int CG = 1>
 void run(const CUtensorMap& ah, const CUtensorMap& al, const CUtensorMap& bh,
          const CUtensorMap& bl, const EpiMaps& em, const Params& p, dim3 grid,
          cudaStream_t stream) {
-  auto kern = gemm_tf32x3_kernel<BN, A_MN, B_MN, A_LO, B_LO, EPI, U8>;
-  constexpr int bytes = Smem<BN, A_LO, B_LO, EPI, U8>::kBytes;
+  auto kern = gemm_tf32x3_kernel<BN, A_MN, B_MN, A_LO, B_LO, EPI, U8, CG>;
+  constexpr int bytes = Smem<BN, A_LO, B_LO, EPI, U8, CG>::kBytes;
   static_assert(bytes <= 227 * 1024, "shared memory budget");
   static bool attr = false;  // one-time per instantiation
   if (!attr) {
     TLG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     attr = true;
   }
-  const TileMap tm{int(grid.x), int(grid.y), int(grid.z)};
+  const TileMap tm{int(grid.x), int(grid.y), int(grid.z)};  // grid.x counts (128*CG)-row tiles
   const int tiles = tm.m_tiles * tm.n_tiles * tm.splits;
-  kern<<<std::min(tiles, num_sms()), U8 ? kThreadsU8 : kThreads, bytes, stream>>>(ah, al, bh, bl, em.out,
-                                                                 em.out_lo, em.act, p, tm);
+  if (CG == 1) {
+    kern<<<std::min(tiles, num_sms()), U8 ? kThreadsU8 : kThreads, bytes, stream>>>(
+        ah, al, bh, bl, em.out, em.out_lo, em.act, p, tm);
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * std::min(tiles, num_sms() / 2));
+    cfg.blockDim = dim3(U8 ? kThreadsU8 : kThreads);
+    cfg.dynamicSmemBytes = bytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    TLG_CUDA(cudaLaunchKernelEx(&cfg, kern, ah, al, bh, bl, em.out, em.out_lo, em.act, p, tm));
+  }
   TLG_CHECK_LAUNCH();
 }
 
@@ -126,6 +144,11 @@ template <int BN, bool A_MN, bool B_MN, bool A_LO, bool B_LO, int EPI, int U8 = 
 void run_if_fits(const CUtensorMap& ah, const CUtensorMap& al, const CUtensorMap& bh,
                  const CUtensorMap& bl, const EpiMaps& em, const Params& p, dim3 grid,
                  cudaStream_t s) {
+  if (g_cg == 2) {
+    if constexpr (Smem<BN, A_LO, B_LO, EPI, U8, 2>::kFits && BN >= 128)
+      return run<BN, A_MN, B_MN, A_LO, B_LO, EPI, U8, 2>(ah, al, bh, bl, em, p, grid, s);
+    throw CudaError("gemm: pair tile does not fit shared memory");
+  }
   if constexpr (Smem<BN, A_LO, B_LO, EPI, U8>::kFits)
     run<BN, A_MN, B_MN, A_LO, B_LO, EPI, U8>(ah, al, bh, bl, em, p, grid, s);
   else
@@ -200,14 +223,26 @@ LaunchInfo launch(const Operand& A, const Operand& B, int M, int N, int K, int e
   p.M = M;
   p.N = N;
   p.K = K;
+  // CTA pairs (cta_group::2) when there are enough 256-row tiles to fill the GPU
+  int cg = 1;
+  {
+    const long tiles2 = long(ceil_div(M, 2 * kBM)) * ceil_div(N, BN) * splits;
+    // (the uint8 converter path measured slower as a pair: keep it on single CTAs)
+    const int kb_tile = ceil_div(ceil_div(K, kBK), splits);  // K blocks per tile
+    if (BN >= 128 && M >= 2 * kBM && tiles2 >= num_sms() / 2 && kb_tile >= 8 && !A.u8 && !B.u8)
+      cg = 2;
+    if (const char* e = std::getenv("TLG_GEMM_CG")) cg = std::atoi(e) == 2 && BN >= 128 ? 2 : 1;
+  }
   const int u8 = A.u8 ? 1 : B.u8 ? 2 : 0;
   if (A.u8 && (A.mn_major || A.ld % 16)) throw CudaError("gemm: uint8 A must be K-major, ld % 16 == 0");
   if (B.u8 && (!B.mn_major || B.ld % 16)) throw CudaError("gemm: uint8 B must be MN-major, ld % 16 == 0");
   const CUtensorMap ah = A.u8 ? make_u8_map(A.u8, K, M, A.ld, 32, kBM) : operand_map(A.hi, A, M, K, kBM);
   const CUtensorMap al = operand_map(A.lo, A, M, K, kBM);
-  const CUtensorMap bh = B.u8 ? make_u8_map(B.u8, N, K, B.ld, BN, 32) : operand_map(B.hi, B, N, K, BN);
-  const CUtensorMap bl = operand_map(B.lo, B, N, K, BN);
-  dim3 grid(ceil_div(M, kBM), ceil_div(N, BN), splits);
+  const CUtensorMap bh = B.u8 ? make_u8_map(B.u8, N, K, B.ld, BN / cg, 32)
+                              : operand_map(B.hi, B, N, K, BN / cg);
+  const CUtensorMap bl = operand_map(B.lo, B, N, K, BN / cg);
+  dim3 grid(ceil_div(M, kBM * cg), ceil_div(N, BN), splits);
+  g_cg = cg;
   const bool a_lo = A.lo != nullptr && !A.u8, b_lo = B.lo != nullptr && !B.u8;
   // epilogue maps: 32x32 fp32 blocks with the 128-B swizzle
   EpiMaps em;
@@ -225,7 +260,8 @@ LaunchInfo launch(const Operand& A, const Operand& B, int M, int N, int K, int e
     case 128: dispatch_bn<128>(A.mn_major, B.mn_major, a_lo, b_lo, epi, u8, ah, al, bh, bl, em, p, grid, stream); break;
     default: dispatch_bn<64>(A.mn_major, B.mn_major, a_lo, b_lo, epi, u8, ah, al, bh, bl, em, p, grid, stream); break;
   }
-  return {BN, std::min(int(grid.x * grid.y * grid.z), num_sms())};
+  const int tiles = int(grid.x * grid.y * grid.z);
+  return {BN, cg == 2 ? 2 * std::min(tiles, num_sms() / 2) : std::min(tiles, num_sms())};
 }
 
 }  // namespace tlg::gemm

@@ -119,8 +119,8 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uin
   return d;
 }
 
-// Instruction descriptor for kind::tf32, fp32 accumulate, M=128.
-template <int BN, bool A_MN, bool B_MN>
+// Instruction descriptor for kind::tf32, fp32 accumulate, M = 128 * CG.
+template <int BN, bool A_MN, bool B_MN, int CG = 1>
 __device__ __forceinline__ constexpr uint32_t make_idesc() {
   return (1u << 4)                        // D format: f32
          | (2u << 7)                      // A format: tf32
@@ -128,7 +128,7 @@ __device__ __forceinline__ constexpr uint32_t make_idesc() {
          | (uint32_t(A_MN) << 15)         // A major (0 = K, 1 = MN)
          | (uint32_t(B_MN) << 16)         // B major
          | (uint32_t(BN >> 3) << 17)      // N >> 3
-         | (uint32_t(kBM >> 4) << 24);    // M >> 4
+         | (uint32_t((kBM * CG) >> 4) << 24);  // M >> 4
 }
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
@@ -140,6 +140,54 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
       "}\n" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+// ---- CTA-pair (cta_group::2) helpers
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of the same smem offset in CTA rank 0 of the pair
+__device__ __forceinline__ uint32_t map_rank0(uint32_t addr) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(addr));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+// TMA into this CTA's smem, completion counted on the pair leader's mbarrier
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, int x, int y,
+                                                 uint32_t leader_bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(leader_bar)
+      : "memory");
+}
+__device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t a, uint64_t b,
+                                              uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+// arrive on the barrier at this smem offset in both CTAs of the pair
+__device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(bar),
+      "h"(uint16_t(3))
+      : "memory");
 }
 
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
@@ -179,11 +227,12 @@ constexpr int kStageBuf = 32 * 33;  // per-warp 32x32 transpose buffer (+1 pad: 
 // U8: 0 = fp32 operands; 1 = A arrives as uint8 planes (K-major); 2 = B arrives as uint8
 // planes (MN-major).  A uint8 operand is TMA-loaded into a byte staging tile and expanded
 // to fp32 in the MMA's swizzled layout by 4 converter warps (exact: 0..255).
-template <int BN, bool A_LO, bool B_LO, int EPI, int U8 = 0>
+template <int BN, bool A_LO, bool B_LO, int EPI, int U8 = 0, int CG = 1>
 struct Smem {
   static constexpr int kA = kBM * kBK * 4;  // 16 KB
-  static constexpr int kB = BN * kBK * 4;
-  static constexpr int kU8 = U8 == 1 ? kBM * kBK : U8 == 2 ? BN * kBK : 0;  // byte staging
+  static constexpr int kBN = BN / CG;       // B rows held by this CTA (a pair splits N)
+  static constexpr int kB = kBN * kBK * 4;
+  static constexpr int kU8 = U8 == 1 ? kBM * kBK : U8 == 2 ? kBN * kBK : 0;  // byte staging
   static constexpr int kStage = kA * (A_LO ? 2 : 1) + kB * (B_LO ? 2 : 1) + kU8;
   static constexpr int kTmaBytes = kStage - kU8 - (U8 == 1 ? kA : U8 == 2 ? kB : 0);
   // per epilogue warp, 4 KB each: out (+ out_lo unless split-K store) (+ act for bwd)
@@ -262,7 +311,7 @@ __device__ __forceinline__ float4 u8x4_to_f32(uint32_t v) {
 // byte offset of element (row r, col c) in a 32x32 fp32 block with the 128-B TMA swizzle
 __device__ __forceinline__ uint32_t swz(int r, int c4) { return uint32_t(r * 128 + ((c4 ^ (r & 7)) << 4)); }
 
-template <int BN, bool A_MN, bool B_MN, bool A_LO, bool B_LO, int EPI, int U8>
+template <int BN, bool A_MN, bool B_MN, bool A_LO, bool B_LO, int EPI, int U8, int CG>
 __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
     gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap tmA_hi,
                        const __grid_constant__ CUtensorMap tmA_lo,
@@ -272,7 +321,13 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
                        const __grid_constant__ CUtensorMap tmOutLo,
                        const __grid_constant__ CUtensorMap tmAct, const Params p,
                        const TileMap tm) {
-  using S = Smem<BN, A_LO, B_LO, EPI, U8>;
+  using S = Smem<BN, A_LO, B_LO, EPI, U8, CG>;
+  // CG == 2: a cluster of two CTAs shares each (256 x BN) tile; rank r owns rows
+  // [128 r, 128 r + 128) of A / D and B rows [r BN/2, (r+1) BN/2).  Only rank 0 issues
+  // the MMAs (cta_group::2), reading both CTAs' smem and writing both CTAs' TMEM.
+  const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
+  const int cl_id = CG == 2 ? int(blockIdx.x >> 1) : int(blockIdx.x);
+  const int n_cl = CG == 2 ? int(gridDim.x >> 1) : int(gridDim.x);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -303,42 +358,57 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(bar_tfull + 8 * a, 1);
-      mbar_init(bar_tempty + 8 * a, kEpiWarps);
+      mbar_init(bar_tempty + 8 * a, kEpiWarps * CG);  // both CTAs' epilogues drain
     }
     for (int w = 0; w < kEpiWarps; ++w) mbar_init(bar_act + 8 * w, 1);
     if (U8)
       for (int st = 0; st < S::kStages; ++st) {
         mbar_init(bar_ufull + 8 * st, 1);
-        mbar_init(bar_conv + 8 * st, 4);  // one arrive per converter warp
+        mbar_init(bar_conv + 8 * st, 4 * CG);  // one arrive per converter warp (x CTAs)
       }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "n"(S::kTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (CG == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "n"(S::kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "n"(S::kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2) cluster_sync_all();  // the peer's barriers exist before any remote arrive
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
     if (lane == 0) {
       // ===== TMA producer =====
+#define TMA_FP32(dst, map, x, y, bar)                                   \
+  do {                                                                 \
+    if (CG == 2) tma_load_2d_pair(dst, map, x, y, bar);                \
+    else tma_load_2d(dst, map, x, y, bar);                             \
+  } while (0)
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int t = cl_id; t < num_tiles; t += n_cl) {
         int mt, nt, sp;
         tm.decode(t, mt, nt, sp);
-        const int m0 = mt * kBM, n0 = nt * BN;
+        const int m0 = mt * kBM * CG + int(rank) * kBM;
+        const int n0 = nt * BN + int(rank) * S::kBN;
         const int kb0 = sp * p.kb_per_split, kb1 = min(kb_total, kb0 + p.kb_per_split);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(bar_empty + 8 * stage, phase ^ 1);
           const uint32_t st = sbase + stage * S::kStage;
-          const uint32_t full = bar_full + 8 * stage;
-          mbar_expect_tx(full, S::kTmaBytes);
+          // CG == 2: both CTAs' fp32 tiles complete on the leader's full barrier
+          const uint32_t full = CG == 2 ? map_rank0(bar_full + 8 * stage) : bar_full + 8 * stage;
+          if (rank == 0) mbar_expect_tx(bar_full + 8 * stage, S::kTmaBytes * CG);
           const int k0 = kb * kBK;
           uint32_t off = st;
           const uint32_t ust = st + S::kStage - S::kU8;  // byte staging of the u8 operand
@@ -346,26 +416,26 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
           if (U8 == 1) {
             tma_load_2d(ust, &tmA_hi, k0, m0, bar_ufull + 8 * stage);  // u8 box {32 k, 128 m}
           } else if (!A_MN) {
-            tma_load_2d(off, &tmA_hi, k0, m0, full);
-            if (A_LO) tma_load_2d(off + S::kA, &tmA_lo, k0, m0, full);
+            TMA_FP32(off, &tmA_hi, k0, m0, full);
+            if (A_LO) TMA_FP32(off + S::kA, &tmA_lo, k0, m0, full);
           } else {
 #pragma unroll
             for (int j = 0; j < kBM / 32; ++j) {
-              tma_load_2d(off + j * 4096, &tmA_hi, m0 + 32 * j, k0, full);
-              if (A_LO) tma_load_2d(off + S::kA + j * 4096, &tmA_lo, m0 + 32 * j, k0, full);
+              TMA_FP32(off + j * 4096, &tmA_hi, m0 + 32 * j, k0, full);
+              if (A_LO) TMA_FP32(off + S::kA + j * 4096, &tmA_lo, m0 + 32 * j, k0, full);
             }
           }
           off += S::kA * (A_LO ? 2 : 1);
           if (U8 == 2) {
             tma_load_2d(ust, &tmB_hi, n0, k0, bar_ufull + 8 * stage);  // u8 box {BN n, 32 k}
           } else if (!B_MN) {
-            tma_load_2d(off, &tmB_hi, k0, n0, full);
-            if (B_LO) tma_load_2d(off + S::kB, &tmB_lo, k0, n0, full);
+            TMA_FP32(off, &tmB_hi, k0, n0, full);
+            if (B_LO) TMA_FP32(off + S::kB, &tmB_lo, k0, n0, full);
           } else {
 #pragma unroll
-            for (int j = 0; j < BN / 32; ++j) {
-              tma_load_2d(off + j * 4096, &tmB_hi, n0 + 32 * j, k0, full);
-              if (B_LO) tma_load_2d(off + S::kB + j * 4096, &tmB_lo, n0 + 32 * j, k0, full);
+            for (int j = 0; j < S::kBN / 32; ++j) {
+              TMA_FP32(off + j * 4096, &tmB_hi, n0 + 32 * j, k0, full);
+              if (B_LO) TMA_FP32(off + S::kB + j * 4096, &tmB_lo, n0 + 32 * j, k0, full);
             }
           }
           if (++stage == S::kStages) {
@@ -376,13 +446,14 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ===== MMA issuer =====
-      constexpr uint32_t idesc = make_idesc<BN, A_MN, B_MN>();
+#undef TMA_FP32
+    if (lane == 0 && rank == 0) {
+      // ===== MMA issuer (pair leader) =====
+      constexpr uint32_t idesc = make_idesc<BN, A_MN, B_MN, CG>();
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+      for (int t = cl_id; t < num_tiles; t += n_cl, ++it) {
         int mt, nt, sp;
         tm.decode(t, mt, nt, sp);
         const int kb0 = sp * p.kb_per_split, kb1 = min(kb_total, kb0 + p.kb_per_split);
@@ -412,19 +483,23 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
             const uint64_t dah = make_sdesc<A_MN>(a_hi + ao, albo, asbo);
             const uint64_t dbh = make_sdesc<B_MN>(b_hi + bo, blbo, bsbo);
             const uint32_t acc = (kb > kb0 || k > 0) ? 1u : 0u;
-            if (B_LO) mma_tf32(tmem_d, dah, make_sdesc<B_MN>(b_lo + bo, blbo, bsbo), idesc, acc);
-            if (A_LO)
-              mma_tf32(tmem_d, make_sdesc<A_MN>(a_lo + ao, albo, asbo), dbh, idesc,
-                       (B_LO || acc) ? 1u : 0u);
-            mma_tf32(tmem_d, dah, dbh, idesc, (A_LO || B_LO || acc) ? 1u : 0u);
+            auto mma = [&](uint64_t da, uint64_t db, uint32_t ac) {
+              if (CG == 2) mma_tf32_pair(tmem_d, da, db, idesc, ac);
+              else mma_tf32(tmem_d, da, db, idesc, ac);
+            };
+            if (B_LO) mma(dah, make_sdesc<B_MN>(b_lo + bo, blbo, bsbo), acc);
+            if (A_LO) mma(make_sdesc<A_MN>(a_lo + ao, albo, asbo), dbh, (B_LO || acc) ? 1u : 0u);
+            mma(dah, dbh, (A_LO || B_LO || acc) ? 1u : 0u);
           }
-          mma_commit(bar_empty + 8 * stage);
+          if (CG == 2) mma_commit_pair(bar_empty + 8 * stage);
+          else mma_commit(bar_empty + 8 * stage);
           if (++stage == S::kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        mma_commit(bar_tfull + 8 * acc_buf);
+        if (CG == 2) mma_commit_pair(bar_tfull + 8 * acc_buf);
+        else mma_commit(bar_tfull + 8 * acc_buf);
       }
     }
   } else if (U8 && warp >= 2 + kEpiWarps) {
@@ -433,7 +508,7 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
     const bool expand = U8 == 1 && p.a_expand != nullptr;
     int stage = 0;
     uint32_t phase = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    for (int t = cl_id; t < num_tiles; t += n_cl) {
       int mt, nt, sp;
       tm.decode(t, mt, nt, sp);
       const int kb0 = sp * p.kb_per_split, kb1 = min(kb_total, kb0 + p.kb_per_split);
@@ -475,19 +550,22 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
             const int k = 8 * w + 4 * kk + (lane >> 3);
             const uint32_t row_off = uint32_t(k * 128 + ((a ^ (k & 3)) << 5) + (c & 1) * 16);
 #pragma unroll
-            for (int j = 0; j < BN / 32; ++j) {
-              const uint32_t v = *reinterpret_cast<const uint32_t*>(us + k * BN + j * 32 + c * 4);
+            for (int j = 0; j < S::kBN / 32; ++j) {
+              const uint32_t v = *reinterpret_cast<const uint32_t*>(us + k * S::kBN + j * 32 + c * 4);
               *reinterpret_cast<float4*>(bt + j * 4096 + row_off) = u8x4_to_f32(v);
             }
           }
         }
         fence_async_smem();  // generic-proxy writes -> visible to the tensor core
         __syncwarp();
-        if ((threadIdx.x & 31) == 0) mbar_arrive(bar_conv + 8 * stage);
+        if ((threadIdx.x & 31) == 0) {
+          if (CG == 2) mbar_arrive_cluster(map_rank0(bar_conv + 8 * stage));
+          else mbar_arrive(bar_conv + 8 * stage);
+        }
         if (expand && nt == 0) {
           named_bar(2, 128);
           if (ct == 0) {
-            tma_store_2d(&tmAct, kb * kBK, mt * kBM, sbase + stage * S::kStage);
+            tma_store_2d(&tmAct, kb * kBK, mt * kBM * CG + int(rank) * kBM, sbase + stage * S::kStage);
             bulk_commit();
           }
         }
@@ -518,10 +596,10 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
       tm.decode(t, mt2, nt2, sp2);
       if (lane == 0) {
         mbar_expect_tx(abar, 4096);
-        tma_load_2d(st_act, &tmAct, nt2 * BN + c, mt2 * kBM + q * 32, abar);
+        tma_load_2d(st_act, &tmAct, nt2 * BN + c, mt2 * kBM * CG + int(rank) * kBM + q * 32, abar);
       }
     };
-    act_issue(blockIdx.x, 0);
+    act_issue(cl_id, 0);
     float* csacc = colpart + kEpiWarps * BN;  // [kColMax] CTA-level column sums
     if (EPI == kEpiBwdTanh && p.colsum != nullptr) {
       for (int i = threadIdx.x - 64; i < p.N; i += kEpiWarps * 32) csacc[i] = 0.f;
@@ -529,10 +607,10 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
     constexpr int kHK = 8;  // fused head width limit (n_actions + 1)
     const bool do_head = EPI == kEpiFwdTanh && p.head_k > 0;
     int it = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+    for (int t = cl_id; t < num_tiles; t += n_cl, ++it) {
       int mt, nt, sp;
       tm.decode(t, mt, nt, sp);
-      const int m0 = mt * kBM, n0 = nt * BN;
+      const int m0 = mt * kBM * CG + int(rank) * kBM, n0 = nt * BN;
       const int rbase = m0 + q * 32;  // first row of this warp's 32-row slab
       const int acc_buf = it & 1;
       mbar_wait(bar_tfull + 8 * acc_buf, (it >> 1) & 1);
@@ -555,7 +633,7 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
           }
           __syncwarp();
           if (c + 32 < BN) act_issue(t, c + 32);
-          else act_issue(t + gridDim.x, 0);
+          else act_issue(t + n_cl, 0);
         }
         uint32_t r[32];
         tmem_ld32(tbase + uint32_t(c), r);
@@ -622,7 +700,10 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
       // TMEM buffer drained: hand it back to the MMA warp
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(bar_tempty + 8 * acc_buf);
+      if (lane == 0) {
+        if (CG == 2) mbar_arrive_cluster(map_rank0(bar_tempty + 8 * acc_buf));
+        else mbar_arrive(bar_tempty + 8 * acc_buf);
+      }
       if (do_head && rbase + lane < p.M) {
         float* hp = p.head_part + (long(nt) * p.M + rbase + lane) * p.head_k;
 #pragma unroll
@@ -650,11 +731,16 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2) cluster_sync_all();  // no CTA leaves while its pair may still touch its smem/TMEM
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "n"(S::kTmemCols));
+    if (CG == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "n"(S::kTmemCols));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "n"(S::kTmemCols));
   }
 }
 
