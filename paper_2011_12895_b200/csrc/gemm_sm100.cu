@@ -232,6 +232,8 @@ LaunchInfo launch(const Operand& A, const Operand& B, int M, int N, int K, int e
     if (BN >= 128 && M >= 2 * kBM && tiles2 >= num_sms() / 2 && kb_tile >= 8 && !A.u8 && !B.u8)
       cg = 2;
     if (const char* e = std::getenv("TLG_GEMM_CG")) cg = std::atoi(e) == 2 && BN >= 128 ? 2 : 1;
+    if (const char* e = std::getenv("TLG_GEMM_CG_U8"))  // tuning experiments only
+      if ((A.u8 || B.u8) && std::atoi(e) == 2 && BN >= 128) cg = 2;
   }
   const int u8 = A.u8 ? 1 : B.u8 ? 2 : 0;
   if (A.u8 && (A.mn_major || A.ld % 16)) throw CudaError("gemm: uint8 A must be K-major, ld % 16 == 0");

@@ -232,18 +232,33 @@ struct Smem {
   static constexpr int kA = kBM * kBK * 4;  // 16 KB
   static constexpr int kBN = BN / CG;       // B rows held by this CTA (a pair splits N)
   static constexpr int kB = kBN * kBK * 4;
-  static constexpr int kU8 = U8 == 1 ? kBM * kBK : U8 == 2 ? kBN * kBK : 0;  // byte staging
-  static constexpr int kStage = kA * (A_LO ? 2 : 1) + kB * (B_LO ? 2 : 1) + kU8;
-  static constexpr int kTmaBytes = kStage - kU8 - (U8 == 1 ? kA : U8 == 2 ? kB : 0);
-  // per epilogue warp, 4 KB each: out (+ out_lo unless split-K store) (+ act for bwd)
-  static constexpr int kEpiBlocks = EPI == kEpiStore ? 1 : EPI == kEpiBwdTanh ? 3 : 2;
-  static constexpr int kEpiBytes =
-      kEpiWarps * kEpiBlocks * 4096 + (EPI == kEpiBwdTanh ? kEpiWarps * BN * 4 + kColMax * 4 : 0);
-  static constexpr int kBudget = 225 * 1024 - kEpiBytes - 1024 - 256;
-  static constexpr int kStages = (kBudget / kStage) < 2 ? 2 : (kBudget / kStage) > 8 ? 8 : (kBudget / kStage);
-  static constexpr int kBarOff = kStages * kStage;
-  // full/empty per stage, tmem full/empty x2, act-block full x4, u8 full/converted per stage
-  static constexpr int kNumBars = 2 * kStages + 4 + kEpiWarps + (U8 ? 2 * kStages : 0);
+  // uint8 operand: its byte tiles stream through their own ring (kU8Ring slots), filled
+  // by the producer up to kU8Ring k-blocks ahead of the fp32 stages, so only the
+  // conversion itself sits on the MMA's critical path.
+  static constexpr int kU8 = U8 == 1 ? kBM * kBK : U8 == 2 ? kBN * kBK : 0;  // bytes per slot
+  static constexpr int kU8Ring = U8 == 0 ? 0 : (32768 / kU8) < 2 ? 2 : (32768 / kU8) > 8 ? 8 : (32768 / kU8);
+  static constexpr int kStage = kA * (A_LO ? 2 : 1) + kB * (B_LO ? 2 : 1);
+  static constexpr int kTmaBytes = kStage - (U8 == 1 ? kA : U8 == 2 ? kB : 0);
+  // per epilogue warp, 4 KB each: out (+ out_lo unless split-K store) (+ act for bwd).
+  // out and out_lo share one block (stored one after the other) whenever the freed
+  // 16 KB buys the mainloop another pipeline stage.
+  static constexpr int kExtra = EPI == kEpiBwdTanh ? kEpiWarps * BN * 4 + kColMax * 4 : 0;
+  static constexpr int stages_for(int blocks) {
+    const int b =
+        (225 * 1024 - (kEpiWarps * blocks * 4096 + kExtra) - kU8Ring * kU8 - 1024 - 256) / kStage;
+    return b < 2 ? 2 : b > 8 ? 8 : b;
+  }
+  static constexpr int kFullBlocks = EPI == kEpiStore ? 1 : EPI == kEpiBwdTanh ? 3 : 2;
+  static constexpr bool kShareLo =
+      EPI != kEpiStore && stages_for(kFullBlocks - 1) > stages_for(kFullBlocks);
+  static constexpr int kEpiBlocks = kFullBlocks - (kShareLo ? 1 : 0);
+  static constexpr int kEpiBytes = kEpiWarps * kEpiBlocks * 4096 + kExtra;
+  static constexpr int kStages = stages_for(kEpiBlocks);
+  static constexpr int kRingOff = kStages * kStage;
+  static constexpr int kBarOff = kRingOff + kU8Ring * kU8;
+  // full/empty per stage, tmem full/empty x2, act-block full x4, converted per stage,
+  // u8 ring full/empty per slot
+  static constexpr int kNumBars = 2 * kStages + 4 + kEpiWarps + (U8 ? kStages + 2 * kU8Ring : 0);
   static constexpr int kEpiOff = (kBarOff + kNumBars * 8 + 16 + 1023) / 1024 * 1024;
   static constexpr int kBytes = kEpiOff + kEpiBytes + 1024;  // + 1 KB alignment slack
   static constexpr bool kFits = kBytes <= 227 * 1024;
@@ -258,6 +273,29 @@ struct TileMap {
     const int r = t / n_tiles;
     m = r % m_tiles;
     s = r / m_tiles;
+  }
+};
+
+// (tile, k-block) walk of one CTA (or CTA pair) through its persistent work list.
+struct KCursor {
+  int t, kb, kb1, mt, nt, sp;
+  __device__ __forceinline__ void load(const TileMap& tm, int kb_per_split, int kb_total) {
+    tm.decode(t, mt, nt, sp);
+    kb = sp * kb_per_split;
+    kb1 = min(kb_total, kb + kb_per_split);
+  }
+  __device__ __forceinline__ void init(int t0, int, int num_tiles, const TileMap& tm,
+                                       int kb_per_split, int kb_total) {
+    t = t0;
+    if (t < num_tiles) load(tm, kb_per_split, kb_total);
+  }
+  __device__ __forceinline__ bool valid(int num_tiles) const { return t < num_tiles; }
+  __device__ __forceinline__ void next(int n_cl, int num_tiles, const TileMap& tm,
+                                       int kb_per_split, int kb_total) {
+    if (++kb >= kb1) {
+      t += n_cl;
+      if (t < num_tiles) load(tm, kb_per_split, kb_total);
+    }
   }
 };
 
@@ -338,8 +376,9 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
   const uint32_t bar_tempty = bar_tfull + 16;               // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + S::kBarOff + S::kNumBars * 8);
   const uint32_t bar_act = bar_tempty + 16;                 // [4]
-  const uint32_t bar_ufull = bar_act + 8 * kEpiWarps;       // [stages] (U8)
-  const uint32_t bar_conv = bar_ufull + 8 * S::kStages;     // [stages] (U8)
+  const uint32_t bar_conv = bar_act + 8 * kEpiWarps;        // [stages] (U8)
+  const uint32_t bar_ufull = bar_conv + 8 * S::kStages;     // [ring] (U8)
+  const uint32_t bar_uempty = bar_ufull + 8 * S::kU8Ring;   // [ring] (U8)
   float* colpart = reinterpret_cast<float*>(smem + S::kEpiOff + kEpiWarps * S::kEpiBlocks * 4096);
 
   const int warp = threadIdx.x >> 5;
@@ -361,11 +400,14 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
       mbar_init(bar_tempty + 8 * a, kEpiWarps * CG);  // both CTAs' epilogues drain
     }
     for (int w = 0; w < kEpiWarps; ++w) mbar_init(bar_act + 8 * w, 1);
-    if (U8)
-      for (int st = 0; st < S::kStages; ++st) {
-        mbar_init(bar_ufull + 8 * st, 1);
+    if (U8) {
+      for (int st = 0; st < S::kStages; ++st)
         mbar_init(bar_conv + 8 * st, 4 * CG);  // one arrive per converter warp (x CTAs)
+      for (int u = 0; u < S::kU8Ring; ++u) {
+        mbar_init(bar_ufull + 8 * u, 1);
+        mbar_init(bar_uempty + 8 * u, 4);  // the 4 local converter warps
       }
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -397,13 +439,38 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
   } while (0)
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = cl_id; t < num_tiles; t += n_cl) {
-        int mt, nt, sp;
-        tm.decode(t, mt, nt, sp);
-        const int m0 = mt * kBM * CG + int(rank) * kBM;
-        const int n0 = nt * BN + int(rank) * S::kBN;
-        const int kb0 = sp * p.kb_per_split, kb1 = min(kb_total, kb0 + p.kb_per_split);
-        for (int kb = kb0; kb < kb1; ++kb) {
+      // u8 ring cursor, running up to kU8Ring k-blocks ahead of the fp32 stages
+      KCursor cu;
+      cu.init(cl_id, n_cl, num_tiles, tm, p.kb_per_split, kb_total);
+      int ui = 0;
+      uint32_t uph = 0;
+      long issued_u8 = 0, done_fp32 = 0;
+      KCursor cf;
+      cf.init(cl_id, n_cl, num_tiles, tm, p.kb_per_split, kb_total);
+      for (; cf.valid(num_tiles); cf.next(n_cl, num_tiles, tm, p.kb_per_split, kb_total), ++done_fp32) {
+        if (U8) {
+          while (cu.valid(num_tiles) && issued_u8 < done_fp32 + S::kU8Ring) {
+            mbar_wait(bar_uempty + 8 * ui, uph ^ 1);
+            mbar_expect_tx(bar_ufull + 8 * ui, S::kU8);
+            const uint32_t dst = sbase + S::kRingOff + ui * S::kU8;
+            if (U8 == 1)  // u8 box {32 k, 128 m}
+              tma_load_2d(dst, &tmA_hi, cu.kb * kBK, cu.mt * kBM * CG + int(rank) * kBM,
+                          bar_ufull + 8 * ui);
+            else          // u8 box {BN/CG n, 32 k}
+              tma_load_2d(dst, &tmB_hi, cu.nt * BN + int(rank) * S::kBN, cu.kb * kBK,
+                          bar_ufull + 8 * ui);
+            cu.next(n_cl, num_tiles, tm, p.kb_per_split, kb_total);
+            ++issued_u8;
+            if (++ui == S::kU8Ring) {
+              ui = 0;
+              uph ^= 1;
+            }
+          }
+        }
+        const int m0 = cf.mt * kBM * CG + int(rank) * kBM;
+        const int n0 = cf.nt * BN + int(rank) * S::kBN;
+        const int kb = cf.kb;
+        {
           mbar_wait(bar_empty + 8 * stage, phase ^ 1);
           const uint32_t st = sbase + stage * S::kStage;
           // CG == 2: both CTAs' fp32 tiles complete on the leader's full barrier
@@ -411,10 +478,8 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
           if (rank == 0) mbar_expect_tx(bar_full + 8 * stage, S::kTmaBytes * CG);
           const int k0 = kb * kBK;
           uint32_t off = st;
-          const uint32_t ust = st + S::kStage - S::kU8;  // byte staging of the u8 operand
-          if (U8) mbar_expect_tx(bar_ufull + 8 * stage, S::kU8);
           if (U8 == 1) {
-            tma_load_2d(ust, &tmA_hi, k0, m0, bar_ufull + 8 * stage);  // u8 box {32 k, 128 m}
+            // converted by the converter warps
           } else if (!A_MN) {
             TMA_FP32(off, &tmA_hi, k0, m0, full);
             if (A_LO) TMA_FP32(off + S::kA, &tmA_lo, k0, m0, full);
@@ -427,7 +492,7 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
           }
           off += S::kA * (A_LO ? 2 : 1);
           if (U8 == 2) {
-            tma_load_2d(ust, &tmB_hi, n0, k0, bar_ufull + 8 * stage);  // u8 box {BN n, 32 k}
+            // converted by the converter warps
           } else if (!B_MN) {
             TMA_FP32(off, &tmB_hi, k0, n0, full);
             if (B_LO) TMA_FP32(off + S::kB, &tmB_lo, k0, n0, full);
@@ -508,11 +573,13 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
     const bool expand = U8 == 1 && p.a_expand != nullptr;
     int stage = 0;
     uint32_t phase = 0;
-    for (int t = cl_id; t < num_tiles; t += n_cl) {
-      int mt, nt, sp;
-      tm.decode(t, mt, nt, sp);
-      const int kb0 = sp * p.kb_per_split, kb1 = min(kb_total, kb0 + p.kb_per_split);
-      for (int kb = kb0; kb < kb1; ++kb) {
+    int ui = 0;
+    uint32_t uph = 0;
+    KCursor cc;
+    cc.init(cl_id, n_cl, num_tiles, tm, p.kb_per_split, kb_total);
+    for (; cc.valid(num_tiles); cc.next(n_cl, num_tiles, tm, p.kb_per_split, kb_total)) {
+      const int mt = cc.mt, nt = cc.nt, kb = cc.kb;
+      {
         if (expand) {  // the bulk store issued from this stage's tile last round must be done
           // (a tile that issues no stores must not rely on the count: wait for all)
           if (ct == 0) {
@@ -521,9 +588,10 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
           }
           named_bar(2, 128);
         }
-        mbar_wait(bar_ufull + 8 * stage, phase);
+        mbar_wait(bar_ufull + 8 * ui, uph);
+        mbar_wait(bar_empty + 8 * stage, phase ^ 1);  // the MMA released this stage's tile
         uint8_t* st = smem + stage * S::kStage;
-        const uint8_t* us = st + S::kStage - S::kU8;
+        const uint8_t* us = smem + S::kRingOff + ui * S::kU8;
         if (U8 == 1) {
           // K-major SW128: row r (128 B) holds k = 0..31; 16-B chunk c stored at c ^ (r & 7)
           const int r = ct;
@@ -569,6 +637,11 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
             bulk_commit();
           }
         }
+        if ((threadIdx.x & 31) == 0) mbar_arrive(bar_uempty + 8 * ui);  // byte slot consumed
+        if (++ui == S::kU8Ring) {
+          ui = 0;
+          uph ^= 1;
+        }
         if (++stage == S::kStages) {
           stage = 0;
           phase ^= 1;
@@ -584,7 +657,9 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
     const int q = warp & 3;
     const int ew = warp - 2;
     const uint32_t blk = sbase + S::kEpiOff + uint32_t(ew * S::kEpiBlocks * 4096);
-    const uint32_t st_out = blk, st_lo = blk + 4096, st_act = blk + 8192;
+    const uint32_t st_out = blk, st_lo = S::kShareLo ? blk : blk + 4096;
+    const uint32_t st_act = blk + (S::kEpiBlocks - 1) * 4096;
+    const int act_off = (S::kEpiBlocks - 1) * 4096;
     uint8_t* blk_ptr = smem + S::kEpiOff + ew * S::kEpiBlocks * 4096;
     float* cpart = colpart + q * BN;
     const uint32_t abar = bar_act + 8 * ew;
@@ -628,7 +703,7 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
           act_phase ^= 1;
 #pragma unroll
           for (int j4 = 0; j4 < 8; ++j4) {
-            const float4 v = *reinterpret_cast<const float4*>(blk_ptr + 8192 + swz(lane, j4));
+            const float4 v = *reinterpret_cast<const float4*>(blk_ptr + act_off + swz(lane, j4));
             h[4 * j4] = v.x; h[4 * j4 + 1] = v.y; h[4 * j4 + 2] = v.z; h[4 * j4 + 3] = v.w;
           }
           __syncwarp();
@@ -671,7 +746,7 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
         for (int j4 = 0; j4 < 8; ++j4) {
           *reinterpret_cast<float4*>(blk_ptr + swz(lane, j4)) =
               make_float4(o[4 * j4], o[4 * j4 + 1], o[4 * j4 + 2], o[4 * j4 + 3]);
-          if (EPI != kEpiStore)
+          if (EPI != kEpiStore && !S::kShareLo)
             *reinterpret_cast<float4*>(blk_ptr + 4096 + swz(lane, j4)) =
                 make_float4(o[4 * j4] - tf32_hi(o[4 * j4]), o[4 * j4 + 1] - tf32_hi(o[4 * j4 + 1]),
                             o[4 * j4 + 2] - tf32_hi(o[4 * j4 + 2]),
@@ -684,7 +759,7 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
             tma_store_3d(&tmOut, nb, rbase, sp, st_out);
           } else {
             tma_store_2d(&tmOut, nb, rbase, st_out);
-            tma_store_2d(&tmOutLo, nb, rbase, st_lo);
+            if (!S::kShareLo) tma_store_2d(&tmOutLo, nb, rbase, st_lo);
           }
           bulk_commit();
         }
@@ -695,6 +770,23 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
           for (int rr = 0; rr < 32; ++rr)
             csum += *reinterpret_cast<const float*>(blk_ptr + swz(rr, lane >> 2) + (lane & 3) * 4);
           cpart[c + lane] = csum;
+        }
+        if (EPI != kEpiStore && S::kShareLo) {
+          // residual plane through the same block once the full-value store has read it
+          if (lane == 0) bulk_wait_read();
+          __syncwarp();
+#pragma unroll
+          for (int j4 = 0; j4 < 8; ++j4)
+            *reinterpret_cast<float4*>(blk_ptr + swz(lane, j4)) =
+                make_float4(o[4 * j4] - tf32_hi(o[4 * j4]), o[4 * j4 + 1] - tf32_hi(o[4 * j4 + 1]),
+                            o[4 * j4 + 2] - tf32_hi(o[4 * j4 + 2]),
+                            o[4 * j4 + 3] - tf32_hi(o[4 * j4 + 3]));
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmOutLo, nb, rbase, st_lo);
+            bulk_commit();
+          }
         }
       }
       // TMEM buffer drained: hand it back to the MMA warp

@@ -436,7 +436,6 @@ struct tlg_learner {
       p.out_lo = act_lo[l];
       p.ldo = outw;
       p.bias = params + net.b_off[l];
-      if (l == 0 && x0_u8) p.a_expand = obs;  // fp32 copy of the planes for dW of layer 1
       const bool fuse_head = l + 1 == net.L && fused_head();
       if (fuse_head) {  // policy/value heads in the last trunk GEMM's epilogue
         p.head_w = params + net.head.wpi;
@@ -488,8 +487,8 @@ struct tlg_learner {
       int sp = tlg::gemm::pick_splits(outw, in, int(F), kMaxSplits);
       while (long(sp) * outw * in > ws_elems && sp > 1) --sp;
       Operand A{dz[l], dz_lo[l], outw, true};
-      // layer 1 reads the fp32 planes the forward's converter warps wrote (exact, no residual)
-      Operand B{l == 0 && x0_u8 ? obs : xin, xin_lo, in, true};
+      // layer 1 reads the uint8 planes directly (converted in smem, exact, no residual)
+      Operand B{xin, xin_lo, in, true, l == 0 ? x0_u8 : nullptr};
       tlg::gemm::Params p{};
       p.ws = ws;
       p.ws_split_stride = long(outw) * in;

@@ -2,6 +2,7 @@
 // same GPU (test tool; not part of the product library).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O2 gemm_selftest.cu ../gemm_sm100.cu
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <random>
 #include <vector>
@@ -98,6 +99,8 @@ void check(const char* name, int M, int N, int K, bool a_mn, bool b_mn, bool a_e
   float* expand = nullptr;
   if (g_u8 == 1) {
     oa.u8 = to_u8(A.x, long(M) * K);
+  }
+  if (g_u8 == 1 && !std::getenv("TLG_ST_NOEXPAND")) {
     TLG_CUDA(cudaMalloc(&expand, long(M) * K * 4));
     TLG_CUDA(cudaMemset(expand, 0xff, long(M) * K * 4));
   }
