@@ -12,7 +12,7 @@
 //   K7 optimizer          (Adam | SGD; skipped on any rank's failure)
 //
 // All reductions have a fixed order, so a step is bit-reproducible run to run.
-#include <nccl.h>
+#include "nccl_dyn.h"
 
 #include <algorithm>
 #include <cmath>
@@ -58,7 +58,7 @@ int Guard(F&& f) {
   do {                                                                                \
     ncclResult_t _r = (expr);                                                         \
     if (_r != ncclSuccess)                                                            \
-      throw tlg::CudaError(std::string(#expr) + ": " + ncclGetErrorString(_r));       \
+      throw tlg::CudaError(std::string(#expr) + ": " + tlg::nccl::api().GetErrorString(_r)); \
   } while (0)
 
 // Parameter layout of the three families (policy.cpp:23-27,78-104).
@@ -268,7 +268,7 @@ struct tlg_learner {
       if (sl.ready) cudaEventDestroy(sl.ready);
       if (sl.consumed) cudaEventDestroy(sl.consumed);
     }
-    if (comm) ncclCommDestroy(comm);
+    if (comm) tlg::nccl::api().CommDestroy(comm);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     for (auto& a : kev)
@@ -660,7 +660,7 @@ struct tlg_learner {
     mark(4);
     // ---- allreduce over ranks (learner.cpp:138-149); the guard slot rides along
     if (nranks > 1) {
-      NCCL_CHECK(ncclAllReduce(grad, grad, size_t(P_pad + 4), ncclFloat, ncclSum, comm, stream));
+      NCCL_CHECK(tlg::nccl::api().AllReduce(grad, grad, size_t(P_pad + 4), ncclFloat, ncclSum, comm, stream));
     }
     mark(5);
     // ---- optimizer (skipped on device when any shard of any rank failed); the Adam step
@@ -985,7 +985,7 @@ int tlg_learner_set_hyper(tlg_learner* l, const tlg_hyper* hp) {
 int tlg_comm_unique_id(uint8_t out[128]) {
   return Guard([&] {
     ncclUniqueId id;
-    NCCL_CHECK(ncclGetUniqueId(&id));
+    NCCL_CHECK(tlg::nccl::api().GetUniqueId(&id));
     static_assert(sizeof(id) == 128, "ncclUniqueId size");
     std::memcpy(out, &id, 128);
   });
@@ -996,7 +996,7 @@ int tlg_learner_comm_init(tlg_learner* l, const uint8_t unique_id[128], int nran
     if (nranks < 1 || rank < 0 || rank >= nranks) throw InvalidArg("bad rank / nranks");
     TLG_CUDA(cudaSetDevice(l->cfg.device));
     if (l->comm) {
-      ncclCommDestroy(l->comm);
+      tlg::nccl::api().CommDestroy(l->comm);
       l->comm = nullptr;
     }
     l->nranks = nranks;
@@ -1005,7 +1005,7 @@ int tlg_learner_comm_init(tlg_learner* l, const uint8_t unique_id[128], int nran
     if (nranks > 1) {
       ncclUniqueId id;
       std::memcpy(&id, unique_id, 128);
-      NCCL_CHECK(ncclCommInitRank(&l->comm, nranks, id, rank));
+      NCCL_CHECK(tlg::nccl::api().CommInitRank(&l->comm, nranks, id, rank));
     }
   });
 }
