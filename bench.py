@@ -178,6 +178,16 @@ def run_reference_arm(args, cfg):
 METRIC = "learner frames/sec at 1/2/4/8 B200 + InferenceServer actions/sec vs CPU ref"
 
 
+def _ncu_traffic():
+    """dram__bytes_read + dram__bytes_write of the dominant kernel per launch, from the
+    committed ncu --set full capture (profiles/r01_fwd1_ncu.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_fwd1_ncu.json")) as f:
+            return json.load(f)["traffic_bytes_per_launch"]
+    except Exception:
+        return None
+
+
 # ---------------------------------------------------------------------------
 def main():
     ap = argparse.ArgumentParser()
@@ -339,9 +349,11 @@ def main():
     ph = np.mean(np.array(kern["phases"]), axis=0)
     step_ms = float(ph[6])
     roofline = {
-        "kernel": "gemm_tf32x3_kernel fwd layer1 (tcgen05.mma kind::tf32, A exact -> 2 passes)",
+        "kernel": "gemm_tf32x3_kernel fwd layer1 (tcgen05.mma kind::tf32; uint8 obs planes "
+                  "converted in smem, exact -> 2 MMA passes)",
+        "algorithmic_bytes_per_launch": F * D + 4 * 2 * hidden[0] * D + 2 * 4 * F * hidden[0],
         "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-        "frac": achieved / peak, "traffic": None,
+        "frac": achieved / peak, "traffic": _ncu_traffic(),
         "peak_source": f"{peak_src} bf16_tflops_sustained (MEASURED_PEAKS.json)",
         "algorithmic_flops_per_launch": flops_fwd1,
         "ms_per_launch": t_fwd1 * 1e3,
