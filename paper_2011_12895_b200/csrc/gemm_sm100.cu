@@ -204,8 +204,8 @@ LaunchInfo launch(const Operand& A, const Operand& B, int M, int N, int K, int e
   auto fits = [&](int bn) {
     const int stage = kBM * kBK * 4 * (a_lo0 ? 2 : 1) + bn * kBK * 4 * (b_lo0 ? 2 : 1) +
                       (A.u8 ? kBM * kBK : B.u8 ? bn * kBK : 0);
-    const int blocks = epi == kEpiStore ? 1 : epi == kEpiBwdTanh ? 3 : 2;
-    const int epib = 4 * blocks * 4096 + (epi == kEpiBwdTanh ? 4 * bn * 4 + kColMax * 4 : 0);
+    const int blocks = epi == kEpiStore ? 1 : (A.u8 ? 1 : 2) + (epi == kEpiBwdTanh ? 1 : 0);
+    const int epib = 4 * blocks * 4096 + (epi == kEpiBwdTanh ? 4 * bn * 4 + kColMax * 4 : 4096);
     return 2 * stage + 2048 + epib + 1024 <= 227 * 1024;
   };
   while (BN > 64 && !fits(BN)) BN /= 2;

@@ -236,24 +236,24 @@ struct Smem {
   // by the producer up to kU8Ring k-blocks ahead of the fp32 stages, so only the
   // conversion itself sits on the MMA's critical path.
   static constexpr int kU8 = U8 == 1 ? kBM * kBK : U8 == 2 ? kBN * kBK : 0;  // bytes per slot
-  static constexpr int kU8Ring = U8 == 0 ? 0 : (32768 / kU8) < 2 ? 2 : (32768 / kU8) > 8 ? 8 : (32768 / kU8);
+  static constexpr int kU8Ring = U8 == 0 ? 0 : (16384 / kU8) < 2 ? 2 : (16384 / kU8) > 8 ? 8 : (16384 / kU8);
   static constexpr int kStage = kA * (A_LO ? 2 : 1) + kB * (B_LO ? 2 : 1);
   static constexpr int kTmaBytes = kStage - (U8 == 1 ? kA : U8 == 2 ? kB : 0);
-  // per epilogue warp, 4 KB each: out (+ out_lo unless split-K store) (+ act for bwd).
-  // out and out_lo share one block (stored one after the other) whenever the freed
-  // 16 KB buys the mainloop another pipeline stage.
+  // per epilogue warp: 4 KB TMA-store staging for out, another for out_lo (the obs-input
+  // forward, whose long K loop hides the serialisation, shares one block to afford more
+  // pipeline stages), + a 4 KB TMA-prefetched activation block (bwd), + 1 KB of head
+  // weights (fwd).
+  static constexpr bool kShareLo = U8 == 1;
   static constexpr int kExtra = EPI == kEpiBwdTanh ? kEpiWarps * BN * 4 + kColMax * 4 : 0;
-  static constexpr int stages_for(int blocks) {
-    const int b =
-        (225 * 1024 - (kEpiWarps * blocks * 4096 + kExtra) - kU8Ring * kU8 - 1024 - 256) / kStage;
+  static constexpr int kEpiBlocks =
+      EPI == kEpiStore ? 1 : (kShareLo ? 1 : 2) + (EPI == kEpiBwdTanh ? 1 : 0);
+  static constexpr int kWarpEpi = kEpiBlocks * 4096 + (EPI == kEpiFwdTanh ? 1024 : 0);
+  static constexpr int kEpiBytes = kEpiWarps * kWarpEpi + kExtra;
+  static constexpr int stages_for() {
+    const int b = (225 * 1024 - kEpiBytes - kU8Ring * kU8 - 1024 - 256) / kStage;
     return b < 2 ? 2 : b > 8 ? 8 : b;
   }
-  static constexpr int kFullBlocks = EPI == kEpiStore ? 1 : EPI == kEpiBwdTanh ? 3 : 2;
-  static constexpr bool kShareLo =
-      EPI != kEpiStore && stages_for(kFullBlocks - 1) > stages_for(kFullBlocks);
-  static constexpr int kEpiBlocks = kFullBlocks - (kShareLo ? 1 : 0);
-  static constexpr int kEpiBytes = kEpiWarps * kEpiBlocks * 4096 + kExtra;
-  static constexpr int kStages = stages_for(kEpiBlocks);
+  static constexpr int kStages = stages_for();
   static constexpr int kRingOff = kStages * kStage;
   static constexpr int kBarOff = kRingOff + kU8Ring * kU8;
   // full/empty per stage, tmem full/empty x2, act-block full x4, converted per stage,
@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
   const uint32_t bar_conv = bar_act + 8 * kEpiWarps;        // [stages] (U8)
   const uint32_t bar_ufull = bar_conv + 8 * S::kStages;     // [ring] (U8)
   const uint32_t bar_uempty = bar_ufull + 8 * S::kU8Ring;   // [ring] (U8)
-  float* colpart = reinterpret_cast<float*>(smem + S::kEpiOff + kEpiWarps * S::kEpiBlocks * 4096);
+  float* colpart = reinterpret_cast<float*>(smem + S::kEpiOff + kEpiWarps * S::kWarpEpi);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -656,11 +656,12 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
     // activation block is TMA-prefetched one chunk ahead into its own swizzled buffer.
     const int q = warp & 3;
     const int ew = warp - 2;
-    const uint32_t blk = sbase + S::kEpiOff + uint32_t(ew * S::kEpiBlocks * 4096);
+    const uint32_t blk = sbase + S::kEpiOff + uint32_t(ew * S::kWarpEpi);
     const uint32_t st_out = blk, st_lo = S::kShareLo ? blk : blk + 4096;
     const uint32_t st_act = blk + (S::kEpiBlocks - 1) * 4096;
     const int act_off = (S::kEpiBlocks - 1) * 4096;
-    uint8_t* blk_ptr = smem + S::kEpiOff + ew * S::kEpiBlocks * 4096;
+    uint8_t* blk_ptr = smem + S::kEpiOff + ew * S::kWarpEpi;
+    float* wsm = reinterpret_cast<float*>(blk_ptr + S::kEpiBlocks * 4096);  // fwd head W [8][32]
     float* cpart = colpart + q * BN;
     const uint32_t abar = bar_act + 8 * ew;
     uint32_t act_phase = 0;
@@ -719,18 +720,33 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
           for (int j = 0; j < 32; ++j)
             o[j] = tanhf(__uint_as_float(r[j]) + __shfl_sync(0xffffffffu, bl, j));
           if (do_head) {
-            // lane j holds Whead[k][nb + j]; broadcast column j to every row-thread
+            // head weights of this chunk's 32 columns -> smem, then broadcast LDS.128
+#pragma unroll
+            for (int k = 0; k < kHK; ++k) {
+              float wk = 0.f;
+              if (k < p.head_k && nb + lane < p.N) {
+                const float* wrow = k < p.head_k - 1 ? p.head_w + long(k) * p.N : p.head_wv;
+                wk = __ldg(wrow + nb + lane);
+              }
+              wsm[k * 32 + lane] = wk;
+            }
+            __syncwarp();
 #pragma unroll
             for (int k = 0; k < kHK; ++k) {
               if (k < p.head_k) {
-                const float* wrow = k < p.head_k - 1 ? p.head_w + long(k) * p.N : p.head_wv;
-                const float wk = (nb + lane < p.N) ? __ldg(wrow + nb + lane) : 0.f;
                 float z = zacc[k];
 #pragma unroll
-                for (int j = 0; j < 32; ++j) z = fmaf(__shfl_sync(0xffffffffu, wk, j), o[j], z);
+                for (int j4 = 0; j4 < 8; ++j4) {
+                  const float4 w4 = *reinterpret_cast<const float4*>(wsm + k * 32 + 4 * j4);
+                  z = fmaf(w4.x, o[4 * j4], z);
+                  z = fmaf(w4.y, o[4 * j4 + 1], z);
+                  z = fmaf(w4.z, o[4 * j4 + 2], z);
+                  z = fmaf(w4.w, o[4 * j4 + 3], z);
+                }
                 zacc[k] = z;
               }
             }
+            __syncwarp();
           }
         } else if (EPI == kEpiBwdTanh) {
 #pragma unroll

@@ -165,7 +165,7 @@ struct tlg_learner {
   int32_t* valid;
   // activations
   std::vector<float*> act, act_lo, dz, dz_lo;
-  float *head_out, *head_part, *tlogp, *adv, *target;
+  float *head_out, *head_part, *tlogp, *adv, *target, *dzh;
   double* seg_partial;
   tlg::StepStatsDev* stats;
   int* err;
@@ -238,6 +238,7 @@ struct tlg_learner {
     const long nblk = (F_max + tlg::kLossFrames - 1) / tlg::kLossFrames;
     hg_partial = mem.add<float>(nblk * A1 * long(net.head.H) + nblk * A1);
     loss_partial = mem.add<double>(nblk * 5);
+    dzh = mem.add<float>(F_max * A1);
     ws_elems = 0;
     long max_cols = 1;
     for (uint32_t l = 0; l < net.L; ++l) {
@@ -466,14 +467,14 @@ struct tlg_learner {
     tlg::launch_returns(bd, algo, hd, tlogp, adv, target, seg_partial, err, stream);
     tlg::launch_finalize_adv(seg_partial, bd, hp.adv_norm, st, err, stream);
     const int loss_kind = algo == TLG_ALGO_VTRACE ? 1 : 0;
-    const int nblk = tlg::launch_loss_backward(
-        net.head, params, hL, ldh, bd, head_out, adv, target, st, hd, loss_kind,
+    const tlg::LossLaunch ll = tlg::launch_loss_backward(
+        net.head, params, hL, ldh, bd, head_out, adv, target, st, hd, loss_kind, dzh,
         net.L ? dz[net.L - 1] : nullptr, net.L ? dz_lo[net.L - 1] : nullptr, hg_partial,
         loss_partial, col_partial, stream);
-    tlg::launch_head_grad_reduce(net.head, hg_partial, loss_partial, nblk, gtarget, st, stream);
-    launches += 6;
+    tlg::launch_head_grad_reduce(net.head, hg_partial, loss_partial, ll, gtarget, st, stream);
+    launches += 7;
     if (net.L > 0) {  // db of the top trunk layer from the loss kernel's column partials
-      tlg::launch_rows_reduce(col_partial, nblk, net.head.H, net.head.H,
+      tlg::launch_rows_reduce(col_partial, ll.stream_blocks, net.head.H, net.head.H,
                               gtarget + net.b_off[net.L - 1], stream);
       ++launches;
     }

@@ -366,32 +366,136 @@ __global__ void __launch_bounds__(1024) finalize_adv_kernel(const double* __rest
 }
 
 // ---------------------------------------------------------------------------
-// K3b.  Persistent blocks of 256 threads walk chunks of kLossFrames frames.
-//  phase 1 (thread per frame): per-sample PPO / PG body (rlmath.cpp:129-182 / 196-220)
-//          -> dlogits, dvalue in smem; loss/stat sums (fp64, per thread).
-//  phase 2 (thread per head-input column j): dZ_L[f][j] = (sum_k dz_k W_pi[k][j] +
-//          dV w_v[j]) * (1 - h^2) for the trunk, the head weight gradient
-//          sum_f dz_k(f) h[f][j] (AccumulateGrad, policy.cpp:122-141) and the last
-//          layer's bias gradient sum_f dZ_L[f][j], accumulated in registers across all
-//          of the block's chunks.  Each block writes one partial row (fixed order).
-template <int kMaxA1, int kCPT>
-__global__ void __launch_bounds__(256) loss_backward_kernel(
-    HeadDesc hd, const float* __restrict__ params, const float* __restrict__ h, long ldh,
-    BatchDev b, const float* __restrict__ head_out, const float* __restrict__ adv,
+// K3b, part 1 (thread per frame): the per-sample PPO / PG body (rlmath.cpp:129-182 /
+// 196-220) -> dlogits, dvalue [F][A1]; per-block fp64 loss/stat sums and per-block
+// bias-gradient sums (fixed-order warp trees).
+template <int kMaxA1>
+__global__ void __launch_bounds__(256) loss_math_kernel(
+    HeadDesc hd, BatchDev b, const float* __restrict__ head_out, const float* __restrict__ adv,
     const float* __restrict__ target, const StepStatsDev* __restrict__ st, HyperDev hp,
-    int loss_kind, float* __restrict__ dz, float* __restrict__ dz_lo,
-    float* __restrict__ hg_partial, double* __restrict__ loss_partial,
-    float* __restrict__ db_partial) {
-  extern __shared__ float sdz[];  // [kLossFrames][A1]
+    int loss_kind, float* __restrict__ dzh, double* __restrict__ loss_partial,
+    float* __restrict__ bias_partial) {
   __shared__ double red[5][8];
+  __shared__ float bred[kMaxA1][8];
   const int A = hd.A, A1 = A + 1;
   const long F = long(b.S) * b.T;
-  const long nchunks = (F + kLossFrames - 1) / kLossFrames;
-  const int tid = threadIdx.x;
+  const long f = blockIdx.x * long(blockDim.x) + threadIdx.x;
   const float inv_n = float(st->inv_n);
   const double mean = st->mean, sd = st->sd;
+  float d[kMaxA1];
+#pragma unroll
+  for (int k = 0; k < kMaxA1; ++k) d[k] = 0.f;
   double l_loss = 0, l_ratio = 0, l_ent = 0, l_vl = 0, l_clip = 0;
-  // per-column accumulators (columns j = tid + 256*c)
+  bool valid = false;
+  if (f < F) {
+    const int s = int(f / b.T), t = int(f % b.T);
+    valid = t < b.valid[s];
+  }
+  if (valid) {
+    float z[kMaxA1];
+#pragma unroll
+    for (int k = 0; k < kMaxA1; ++k) z[k] = k < A1 ? head_out[f * A1 + k] : 0.f;
+    float mx = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < kMaxA1; ++k)
+      if (k < A) mx = fmaxf(mx, z[k]);
+    float se = 0.f;
+#pragma unroll
+    for (int k = 0; k < kMaxA1; ++k)
+      if (k < A) se += expf(z[k] - mx);
+    const float lse = mx + logf(se);
+    float pk[kMaxA1], lpk[kMaxA1];
+    float ent = 0.f;
+#pragma unroll
+    for (int k = 0; k < kMaxA1; ++k) {
+      lpk[k] = z[k] - lse;
+      pk[k] = k < A ? expf(lpk[k]) : 0.f;
+      if (k < A && pk[k] > 0.f) ent -= pk[k] * lpk[k];  // Entropy (rlmath.cpp:36-41)
+    }
+    const int a = min(max(b.action[f], 0), A - 1);  // out-of-range is flagged by K3a
+    float logp = 0.f, V = 0.f;
+#pragma unroll
+    for (int k = 0; k < kMaxA1; ++k) {
+      if (k == a) logp = lpk[k];
+      if (k == A) V = z[k];
+    }
+    const float verr = V - target[f];
+    const float ad = float((double(adv[f]) - mean) / sd);
+    const float ratio = expf(logp - b.blogp[f]);
+    float loss_i;
+    if (loss_kind == 0) {
+      const float clipped = fminf(fmaxf(ratio, 1.f - hp.clip_eps), 1.f + hp.clip_eps);
+      const float t1 = ratio * ad, t2 = clipped * ad;
+      loss_i = -fminf(t1, t2) + hp.vf_coef * verr * verr - hp.ent_coef * ent;
+      if (t2 < t1) l_clip = 1.0;
+      const bool surr = t1 <= t2;  // gradient only when the unclipped term is active
+#pragma unroll
+      for (int k = 0; k < kMaxA1; ++k)
+        if (k < A) {
+          float g = hp.ent_coef * pk[k] * ((pk[k] > 0.f ? lpk[k] : 0.f) + ent);
+          if (surr) g += -ad * ratio * ((k == a ? 1.f : 0.f) - pk[k]);
+          d[k] = g * inv_n;
+        }
+    } else {
+      loss_i = -ad * logp + hp.vf_coef * verr * verr - hp.ent_coef * ent;
+#pragma unroll
+      for (int k = 0; k < kMaxA1; ++k)
+        if (k < A)
+          d[k] = (-ad * ((k == a ? 1.f : 0.f) - pk[k]) +
+                  hp.ent_coef * pk[k] * ((pk[k] > 0.f ? lpk[k] : 0.f) + ent)) * inv_n;
+    }
+#pragma unroll
+    for (int k = 0; k < kMaxA1; ++k)
+      if (k == A) d[k] = 2.f * hp.vf_coef * verr * inv_n;
+    l_loss = loss_i;
+    l_ratio = ratio;
+    l_ent = ent;
+    l_vl = double(verr) * double(verr);
+  }
+  if (f < F) {
+#pragma unroll
+    for (int k = 0; k < kMaxA1; ++k)
+      if (k < A1) dzh[f * A1 + k] = d[k];
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double v[5] = {l_loss, l_ratio, l_ent, l_vl, l_clip};
+#pragma unroll
+  for (int q = 0; q < 5; ++q) {
+    v[q] = warp_sum(v[q]);
+    if (lane == 0) red[q][w] = v[q];
+  }
+#pragma unroll
+  for (int k = 0; k < kMaxA1; ++k) {
+    const float t = warp_sum(d[k]);
+    if (lane == 0) bred[k][w] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x < 5) {
+    double t = 0.0;
+    for (int i = 0; i < 8; ++i) t += red[threadIdx.x][i];
+    loss_partial[long(blockIdx.x) * 5 + threadIdx.x] = t;
+  } else if (threadIdx.x >= 32 && threadIdx.x < 32 + A1) {
+    const int k = threadIdx.x - 32;
+    float t = 0.f;
+    for (int i = 0; i < 8; ++i) t += bred[k][i];
+    bias_partial[long(blockIdx.x) * A1 + k] = t;
+  }
+}
+
+// K3b, part 2: persistent blocks of 256 threads stream chunks of kLossFrames frames
+// (thread per head-input column j): dZ_L[f][j] = (sum_k dz_k W_pi[k][j] + dV w_v[j]) *
+// (1 - h^2), the head weight gradient sum_f dz_k(f) h[f][j] (AccumulateGrad,
+// policy.cpp:122-141) and the last layer's bias gradient sum_f dZ_L[f][j], accumulated in
+// registers across the block's chunks; one partial row per block (fixed order).
+template <int kMaxA1, int kCPT>
+__global__ void __launch_bounds__(256) loss_stream_kernel(
+    HeadDesc hd, const float* __restrict__ params, const float* __restrict__ h, long ldh,
+    long F, const float* __restrict__ dzh, float* __restrict__ dz, float* __restrict__ dz_lo,
+    float* __restrict__ hg_partial, float* __restrict__ db_partial) {
+  extern __shared__ float sdz[];  // [kLossFrames][A1]
+  const int A = hd.A, A1 = A + 1;
+  const long nchunks = (F + kLossFrames - 1) / kLossFrames;
+  const int tid = threadIdx.x;
   float acc[kCPT][kMaxA1];
   float dbacc[kCPT];
   float w[kCPT][kMaxA1];
@@ -410,103 +514,34 @@ __global__ void __launch_bounds__(256) loss_backward_kernel(
       w[c][k] = wk;
     }
   }
-
   for (long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
     const long f0 = ch * kLossFrames;
-    // ---- phase 1
-    for (int i = tid; i < kLossFrames; i += blockDim.x) {
-      const long f = f0 + i;
-      float* d = sdz + i * A1;
-      bool valid = false;
-      if (f < F) {
-        const int s = int(f / b.T), t = int(f % b.T);
-        valid = t < b.valid[s];
-      }
-      if (!valid) {
-        for (int k = 0; k < A1; ++k) d[k] = 0.f;
-        continue;
-      }
-      const float* z = head_out + f * A1;
-      float mx = -INFINITY;
-      for (int k = 0; k < A; ++k) mx = fmaxf(mx, z[k]);
-      float se = 0.f;
-      for (int k = 0; k < A; ++k) se += expf(z[k] - mx);
-      const float lse = mx + logf(se);
-      float ent = 0.f;
-      for (int k = 0; k < A; ++k) {
-        const float lp = z[k] - lse;
-        const float pk = expf(lp);
-        if (pk > 0.f) ent -= pk * lp;  // Entropy (rlmath.cpp:36-41)
-      }
-      const int a = min(max(b.action[f], 0), A - 1);  // out-of-range is flagged by K3a
-      const float logp = z[a] - lse;
-      const float V = z[A];
-      const float verr = V - target[f];
-      const float ad = float((double(adv[f]) - mean) / sd);
-      const float ratio = expf(logp - b.blogp[f]);
-      float loss_i;
-      for (int k = 0; k < A; ++k) d[k] = 0.f;
-      if (loss_kind == 0) {
-        const float clipped = fminf(fmaxf(ratio, 1.f - hp.clip_eps), 1.f + hp.clip_eps);
-        const float t1 = ratio * ad, t2 = clipped * ad;
-        loss_i = -fminf(t1, t2) + hp.vf_coef * verr * verr - hp.ent_coef * ent;
-        if (t2 < t1) l_clip += 1.0;
-        if (t1 <= t2) {
-          for (int k = 0; k < A; ++k) {
-            const float pk = expf(z[k] - lse);
-            d[k] += -ad * ratio * ((k == a ? 1.f : 0.f) - pk) * inv_n;
-          }
-        }
-        for (int k = 0; k < A; ++k) {
-          const float lp = z[k] - lse;
-          const float pk = expf(lp);
-          d[k] += hp.ent_coef * pk * ((pk > 0.f ? lp : 0.f) + ent) * inv_n;
-        }
-      } else {
-        loss_i = -ad * logp + hp.vf_coef * verr * verr - hp.ent_coef * ent;
-        for (int k = 0; k < A; ++k) {
-          const float lp = z[k] - lse;
-          const float pk = expf(lp);
-          d[k] = (-ad * ((k == a ? 1.f : 0.f) - pk) +
-                  hp.ent_coef * pk * ((pk > 0.f ? lp : 0.f) + ent)) * inv_n;
-        }
-      }
-      d[A] = 2.f * hp.vf_coef * verr * inv_n;
-      l_loss += double(loss_i);
-      l_ratio += double(ratio);
-      l_ent += double(ent);
-      l_vl += double(verr) * double(verr);
-    }
-    __syncthreads();
-    // ---- phase 2
     const int nf = int(F - f0 < long(kLossFrames) ? F - f0 : long(kLossFrames));
+    for (int i = tid; i < nf * A1; i += blockDim.x) sdz[i] = dzh[f0 * A1 + i];
+    __syncthreads();
 #pragma unroll
     for (int c = 0; c < kCPT; ++c) {
       const int j = tid + 256 * c;
       if (j >= hd.H) continue;
-      for (int i0 = 0; i0 < nf; i0 += 8) {
-        // batch the 8 (independent, coalesced) loads ahead of the math: memory-level
-        // parallelism is what this HBM-bound loop needs
-        float xs[8];
+      for (int i0 = 0; i0 < nf; i0 += 16) {
+        // 16 independent coalesced loads in flight before the math
+        float xs[16];
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
+        for (int u = 0; u < 16; ++u)
           xs[u] = (i0 + u < nf) ? __ldg(h + (f0 + i0 + u) * ldh + j) : 0.f;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < 16; ++u) {
           if (i0 + u >= nf) break;
           const long f = f0 + i0 + u;
           const float x = xs[u];
           const float* d = sdz + (i0 + u) * A1;
-          float dh = d[A] * w[c][A < kMaxA1 ? A : kMaxA1 - 1];
+          float dh = 0.f;
 #pragma unroll
           for (int k = 0; k < kMaxA1; ++k)
-            if (k < A) {
+            if (k <= A) {
               dh = fmaf(d[k], w[c][k], dh);
               acc[c][k] = fmaf(d[k], x, acc[c][k]);
             }
-#pragma unroll
-          for (int k = 0; k < kMaxA1; ++k)
-            if (k == A) acc[c][k] = fmaf(d[A], x, acc[c][k]);
           if (dz) {
             const float o = dh * (1.f - x * x);
             dz[f * hd.H + j] = o;
@@ -516,17 +551,8 @@ __global__ void __launch_bounds__(256) loss_backward_kernel(
         }
       }
     }
-    // bias partials of the heads: sum over the chunk's frames of dz_k
-    if (tid < A1) {
-      float bacc = 0.f;
-      for (int i = 0; i < nf; ++i) bacc += sdz[i * A1 + tid];
-      // stored after the weight partials: [gridDim][A1]
-      float* bp = hg_partial + long(gridDim.x) * A1 * hd.H + long(blockIdx.x) * A1 + tid;
-      *bp = (ch == blockIdx.x ? 0.f : *bp) + bacc;
-    }
     __syncthreads();
   }
-  // ---- per-block partial rows
 #pragma unroll
   for (int c = 0; c < kCPT; ++c) {
     const int j = tid + 256 * c;
@@ -536,21 +562,6 @@ __global__ void __launch_bounds__(256) loss_backward_kernel(
     for (int k = 0; k < kMaxA1; ++k)
       if (k <= A) out[long(k) * hd.H + j] = acc[c][k];
     if (dz) db_partial[long(blockIdx.x) * hd.H + j] = dbacc[c];
-  }
-  {
-    double v[5] = {l_loss, l_ratio, l_ent, l_vl, l_clip};
-    const int wi = tid >> 5, lane = tid & 31;
-#pragma unroll
-    for (int q = 0; q < 5; ++q) {
-      v[q] = warp_sum(v[q]);
-      if (lane == 0) red[q][wi] = v[q];
-    }
-  }
-  __syncthreads();
-  if (tid < 5) {
-    double t = 0.0;
-    for (int wi = 0; wi < int(blockDim.x >> 5); ++wi) t += red[tid][wi];
-    loss_partial[long(blockIdx.x) * 5 + tid] = t;
   }
 }
 
@@ -781,44 +792,58 @@ void launch_finalize_adv(const double* seg_partial, const BatchDev& b, int adv_n
   TLG_CHECK_LAUNCH();
 }
 
-int launch_loss_backward(const HeadDesc& hd, const float* params, const float* h, long ldh,
-                         const BatchDev& b, const float* head_out, const float* adv,
-                         const float* target, const StepStatsDev* st, const HyperDev& hp,
-                         int loss_kind, float* dz, float* dz_lo, float* hg_partial,
-                         double* loss_partial, float* db_partial, cudaStream_t s) {
+LossLaunch launch_loss_backward(const HeadDesc& hd, const float* params, const float* h,
+                                long ldh, const BatchDev& b, const float* head_out,
+                                const float* adv, const float* target, const StepStatsDev* st,
+                                const HyperDev& hp, int loss_kind, float* dzh, float* dz,
+                                float* dz_lo, float* hg_partial, double* loss_partial,
+                                float* db_partial, cudaStream_t s) {
   const long F = long(b.S) * b.T;
+  const int A1 = hd.A + 1;
+  const long nw = long(A1) * hd.H;
   const long nchunks = (F + kLossFrames - 1) / kLossFrames;
-  const int blocks = int(std::min<long>(nchunks, kLossBlocks));
-  const size_t smem = size_t(kLossFrames) * (hd.A + 1) * sizeof(float);
-#define TLG_LOSS(MA, CPT)                                                                 \
-  loss_backward_kernel<MA, CPT><<<blocks, 256, smem, s>>>(hd, params, h, ldh, b, head_out, adv, \
-                                                         target, st, hp, loss_kind, dz, dz_lo, \
-                                                         hg_partial, loss_partial, db_partial)
+  LossLaunch ll;
+  ll.stream_blocks = int(std::min<long>(nchunks, kLossBlocks));
+  ll.math_blocks = ceil_div(F, 256);
+  float* bias_partial = hg_partial + long(ll.stream_blocks) * nw;
+  if (A1 <= 8)
+    loss_math_kernel<8><<<ll.math_blocks, 256, 0, s>>>(hd, b, head_out, adv, target, st, hp,
+                                                       loss_kind, dzh, loss_partial, bias_partial);
+  else
+    loss_math_kernel<32><<<ll.math_blocks, 256, 0, s>>>(hd, b, head_out, adv, target, st, hp,
+                                                        loss_kind, dzh, loss_partial,
+                                                        bias_partial);
+  TLG_CHECK_LAUNCH();
+  const size_t smem = size_t(kLossFrames) * A1 * sizeof(float);
+#define TLG_LOSS(MA, CPT)                                                                  \
+  loss_stream_kernel<MA, CPT><<<ll.stream_blocks, 256, smem, s>>>(hd, params, h, ldh, F, dzh, dz, \
+                                                                 dz_lo, hg_partial, db_partial)
   const int cpt = (hd.H + 255) / 256;
-  if (hd.A + 1 <= 8) {
+  if (A1 <= 8) {
     if (cpt <= 1) TLG_LOSS(8, 1);
     else if (cpt <= 2) TLG_LOSS(8, 2);
     else if (cpt <= 4) TLG_LOSS(8, 4);
     else if (cpt <= 8) TLG_LOSS(8, 8);
     else throw CudaError("head input wider than 2048 with the fused loss kernel");
-  } else if (hd.A + 1 <= kMaxA1Limit && cpt <= 1) {
+  } else if (A1 <= kMaxA1Limit && cpt <= 1) {
     TLG_LOSS(32, 1);
   } else {
     throw CudaError("n_actions > 7 needs a head input width <= 256");
   }
 #undef TLG_LOSS
   TLG_CHECK_LAUNCH();
-  return blocks;
+  return ll;
 }
 
 void launch_head_grad_reduce(const HeadDesc& hd, const float* hg_partial,
-                             const double* loss_partial, int nblocks, float* grad,
+                             const double* loss_partial, const LossLaunch& ll, float* grad,
                              StepStatsDev* st, cudaStream_t s) {
   const long nw = long(hd.A + 1) * hd.H;
-  head_grad_reduce_kernel<<<ceil_div(nw, 32), 256, 0, s>>>(hd, hg_partial, nblocks, grad);
+  head_grad_reduce_kernel<<<ceil_div(nw, 32), 256, 0, s>>>(hd, hg_partial, ll.stream_blocks,
+                                                           grad);
   TLG_CHECK_LAUNCH();
-  head_bias_stats_kernel<<<1, 32 * (hd.A + 1 + 5), 0, s>>>(hd, hg_partial + long(nblocks) * nw,
-                                                          loss_partial, nblocks, grad, st);
+  head_bias_stats_kernel<<<1, 32 * (hd.A + 1 + 5), 0, s>>>(
+      hd, hg_partial + long(ll.stream_blocks) * nw, loss_partial, ll.math_blocks, grad, st);
   TLG_CHECK_LAUNCH();
 }
 

@@ -85,14 +85,19 @@ void launch_returns(const BatchDev& b, int algo, const HyperDev& hp, const float
                     float* adv, float* target, double* seg_partial, int* err, cudaStream_t s);
 void launch_finalize_adv(const double* seg_partial, const BatchDev& b, int adv_norm,
                          StepStatsDev* st, int* err, cudaStream_t s);
-// dz/dz_lo may be null (no trunk).  Returns the number of blocks (partials rows).
-int launch_loss_backward(const HeadDesc& hd, const float* params, const float* h, long ldh,
-                         const BatchDev& b, const float* head_out, const float* adv,
-                         const float* target, const StepStatsDev* st, const HyperDev& hp,
-                         int loss_kind, float* dz, float* dz_lo, float* hg_partial,
-                         double* loss_partial, float* db_partial, cudaStream_t s);
+struct LossLaunch {
+  int stream_blocks;  // rows of the head-weight / last-layer-bias partials
+  int math_blocks;    // rows of the loss/stat and head-bias partials
+};
+// dz/dz_lo may be null (no trunk).  dzh: scratch [F][A+1] (dlogits, dvalue).
+LossLaunch launch_loss_backward(const HeadDesc& hd, const float* params, const float* h,
+                                long ldh, const BatchDev& b, const float* head_out,
+                                const float* adv, const float* target, const StepStatsDev* st,
+                                const HyperDev& hp, int loss_kind, float* dzh, float* dz,
+                                float* dz_lo, float* hg_partial, double* loss_partial,
+                                float* db_partial, cudaStream_t s);
 void launch_head_grad_reduce(const HeadDesc& hd, const float* hg_partial,
-                             const double* loss_partial, int nblocks, float* grad,
+                             const double* loss_partial, const LossLaunch& ll, float* grad,
                              StepStatsDev* st, cudaStream_t s);
 // out[c] = sum_r partial[r*stride + c] for c < cols, fixed order (deterministic).
 void launch_rows_reduce(const float* partial, int rows, long cols, long stride, float* out,
