@@ -198,23 +198,10 @@ int pick_splits(int M, int N, int K, int max_splits) {
 LaunchInfo launch(const Operand& A, const Operand& B, int M, int N, int K, int epi, Params p,
                   int splits, cudaStream_t stream) {
   if (M <= 0 || N <= 0 || K <= 0) throw CudaError("gemm: empty problem");
-  int BN = N > 128 ? 256 : N > 64 ? 128 : 64;
-  // widest tile whose pipeline (>= 2 stages) + epilogue staging fits 227 KB
   const bool a_lo0 = A.lo != nullptr && !A.u8, b_lo0 = B.lo != nullptr && !B.u8;
-  auto fits = [&](int bn) {
-    const int stage = kBM * kBK * 4 * (a_lo0 ? 2 : 1) + bn * kBK * 4 * (b_lo0 ? 2 : 1) +
-                      (A.u8 ? kBM * kBK : B.u8 ? bn * kBK : 0);
-    const int blocks = epi == kEpiStore ? 1 : (A.u8 ? 1 : 2) + (epi == kEpiBwdTanh ? 1 : 0);
-    const int epib = 4 * blocks * 4096 + (epi == kEpiBwdTanh ? 4 * bn * 4 + kColMax * 4 : 4096);
-    return 2 * stage + 2048 + epib + 1024 <= 227 * 1024;
-  };
-  while (BN > 64 && !fits(BN)) BN /= 2;
+  const int u8_0 = A.u8 ? 1 : B.u8 ? 2 : 0;
   if (epi == kEpiBwdTanh && p.colsum != nullptr && N > kColMax)
     throw CudaError("gemm: fused column sums need N <= 2048");
-  if (const char* e = std::getenv("TLG_GEMM_MAX_BN")) {  // tuning experiments only
-    const int cap = std::atoi(e);
-    while (BN > 64 && BN > cap) BN /= 2;
-  }
   const int kb_total = ceil_div(K, kBK);
   if (splits < 1) splits = 1;
   if (epi != kEpiStore) splits = 1;
@@ -223,17 +210,29 @@ LaunchInfo launch(const Operand& A, const Operand& B, int M, int N, int K, int e
   p.M = M;
   p.N = N;
   p.K = K;
-  // CTA pairs (cta_group::2) when there are enough 256-row tiles to fill the GPU
+  // Tile width: 256 columns when the K loop is long enough to hide the wider epilogue,
+  // else 128 (short-K fused epilogues are the critical path; narrower tiles balance).
+  int BN = N > 128 ? 256 : N > 64 ? 128 : 64;
+  const int kb_tile = p.kb_per_split;  // K blocks per tile
+  if (BN == 256 && epi != kEpiStore && kb_tile < 16) BN = 128;
+  if (const char* e = std::getenv("TLG_GEMM_MAX_BN")) {  // tuning experiments only
+    const int cap = std::atoi(e);
+    while (BN > 64 && BN > cap) BN /= 2;
+  }
+  // CTA pairs (cta_group::2) when there are enough 256-row tiles to fill the GPU; then
+  // the widest tile whose pipeline (>= 2 stages) + epilogue staging fits 227 KB.
   int cg = 1;
-  {
+  for (;;) {
+    cg = 1;
     const long tiles2 = long(ceil_div(M, 2 * kBM)) * ceil_div(N, BN) * splits;
     // (the uint8 converter path measured slower as a pair: keep it on single CTAs)
-    const int kb_tile = ceil_div(ceil_div(K, kBK), splits);  // K blocks per tile
     if (BN >= 128 && M >= 2 * kBM && tiles2 >= num_sms() / 2 && kb_tile >= 8 && !A.u8 && !B.u8)
       cg = 2;
     if (const char* e = std::getenv("TLG_GEMM_CG")) cg = std::atoi(e) == 2 && BN >= 128 ? 2 : 1;
     if (const char* e = std::getenv("TLG_GEMM_CG_U8"))  // tuning experiments only
       if ((A.u8 || B.u8) && std::atoi(e) == 2 && BN >= 128) cg = 2;
+    if (BN == 64 || smem_plan(BN, a_lo0, b_lo0, epi, u8_0, cg).bytes <= 227 * 1024) break;
+    BN /= 2;
   }
   const int u8 = A.u8 ? 1 : B.u8 ? 2 : 0;
   if (A.u8 && (A.mn_major || A.ld % 16)) throw CudaError("gemm: uint8 A must be K-major, ld % 16 == 0");

@@ -227,40 +227,77 @@ constexpr int kStageBuf = 32 * 33;  // per-warp 32x32 transpose buffer (+1 pad: 
 // U8: 0 = fp32 operands; 1 = A arrives as uint8 planes (K-major); 2 = B arrives as uint8
 // planes (MN-major).  A uint8 operand is TMA-loaded into a byte staging tile and expanded
 // to fp32 in the MMA's swizzled layout by 4 converter warps (exact: 0..255).
-template <int BN, bool A_LO, bool B_LO, int EPI, int U8 = 0, int CG = 1>
-struct Smem {
-  static constexpr int kA = kBM * kBK * 4;  // 16 KB
-  static constexpr int kBN = BN / CG;       // B rows held by this CTA (a pair splits N)
-  static constexpr int kB = kBN * kBK * 4;
-  // uint8 operand: its byte tiles stream through their own ring (kU8Ring slots), filled
-  // by the producer up to kU8Ring k-blocks ahead of the fp32 stages, so only the
+// Shared-memory plan of one instantiation, constexpr so the host launcher picks tiles
+// with exactly the arithmetic the kernel is compiled with.
+struct SmemPlan {
+  int stage, tma_bytes, u8_slot, u8_ring, epi_blocks, warp_epi, extra, stages;
+  bool share_lo;
+  int ring_off, bar_off, num_bars, epi_off, bytes;
+};
+constexpr int plan_stages(int stage, int epi_bytes, int ring_bytes) {
+  const int b = (225 * 1024 - epi_bytes - ring_bytes - 1024 - 256) / stage;
+  return b < 2 ? 2 : b > 8 ? 8 : b;
+}
+constexpr SmemPlan smem_plan(int BN, bool a_lo, bool b_lo, int epi, int u8, int cg) {
+  SmemPlan q{};
+  const int kA = kBM * kBK * 4;          // 16 KB
+  const int kB = (BN / cg) * kBK * 4;    // B rows held by this CTA (a pair splits N)
+  q.stage = kA * (a_lo ? 2 : 1) + kB * (b_lo ? 2 : 1);
+  q.tma_bytes = q.stage - (u8 == 1 ? kA : u8 == 2 ? kB : 0);
+  // a uint8 operand's byte tiles stream through their own ring (u8_ring slots), filled
+  // by the producer up to u8_ring k-blocks ahead of the fp32 stages, so only the
   // conversion itself sits on the MMA's critical path.
-  static constexpr int kU8 = U8 == 1 ? kBM * kBK : U8 == 2 ? kBN * kBK : 0;  // bytes per slot
-  static constexpr int kU8Ring = U8 == 0 ? 0 : (16384 / kU8) < 2 ? 2 : (16384 / kU8) > 8 ? 8 : (16384 / kU8);
-  static constexpr int kStage = kA * (A_LO ? 2 : 1) + kB * (B_LO ? 2 : 1);
-  static constexpr int kTmaBytes = kStage - (U8 == 1 ? kA : U8 == 2 ? kB : 0);
-  // per epilogue warp: 4 KB TMA-store staging for out, another for out_lo (the obs-input
-  // forward, whose long K loop hides the serialisation, shares one block to afford more
-  // pipeline stages), + a 4 KB TMA-prefetched activation block (bwd), + 1 KB of head
-  // weights (fwd).
-  static constexpr bool kShareLo = U8 == 1;
-  static constexpr int kExtra = EPI == kEpiBwdTanh ? kEpiWarps * BN * 4 + kColMax * 4 : 0;
-  static constexpr int kEpiBlocks =
-      EPI == kEpiStore ? 1 : (kShareLo ? 1 : 2) + (EPI == kEpiBwdTanh ? 1 : 0);
-  static constexpr int kWarpEpi = kEpiBlocks * 4096 + (EPI == kEpiFwdTanh ? 1024 : 0);
-  static constexpr int kEpiBytes = kEpiWarps * kWarpEpi + kExtra;
-  static constexpr int stages_for() {
-    const int b = (225 * 1024 - kEpiBytes - kU8Ring * kU8 - 1024 - 256) / kStage;
-    return b < 2 ? 2 : b > 8 ? 8 : b;
-  }
-  static constexpr int kStages = stages_for();
-  static constexpr int kRingOff = kStages * kStage;
-  static constexpr int kBarOff = kRingOff + kU8Ring * kU8;
+  q.u8_slot = u8 == 1 ? kBM * kBK : u8 == 2 ? (BN / cg) * kBK : 0;
+  q.u8_ring = u8 == 0 ? 0 : (16384 / q.u8_slot) < 2 ? 2 : (16384 / q.u8_slot) > 8 ? 8
+                                                                                 : (16384 / q.u8_slot);
+  // per epilogue warp: 4 KB TMA-store staging for out, another for out_lo, + a 4 KB
+  // TMA-prefetched activation block (bwd), + 1 KB of head weights (fwd).  out and out_lo
+  // share one block (stores serialised) when that buys the pipeline a third stage: the
+  // uint8-input forward and the wide 3-pass tiles, whose long K loops hide it.
+  q.extra = epi == kEpiBwdTanh ? kEpiWarps * BN * 4 + kColMax * 4 : 0;
+  const int head = epi == kEpiFwdTanh ? 1024 : 0;
+  const int ring = q.u8_ring * q.u8_slot;
+  auto epi_bytes = [&](int blocks) { return kEpiWarps * (blocks * 4096 + head) + q.extra; };
+  const int sep_blocks = epi == kEpiStore ? 1 : 2 + (epi == kEpiBwdTanh ? 1 : 0);
+  const int sep = plan_stages(q.stage, epi_bytes(sep_blocks), ring);
+  const int shr = plan_stages(q.stage, epi_bytes(sep_blocks - 1), ring);
+  q.share_lo = epi != kEpiStore && (u8 == 1 || (sep < 3 && shr > sep));
+  q.epi_blocks = q.share_lo ? sep_blocks - 1 : sep_blocks;
+  q.warp_epi = q.epi_blocks * 4096 + head;
+  q.stages = q.share_lo ? shr : sep;
+  q.ring_off = q.stages * q.stage;
+  q.bar_off = q.ring_off + ring;
   // full/empty per stage, tmem full/empty x2, act-block full x4, converted per stage,
   // u8 ring full/empty per slot
-  static constexpr int kNumBars = 2 * kStages + 4 + kEpiWarps + (U8 ? kStages + 2 * kU8Ring : 0);
-  static constexpr int kEpiOff = (kBarOff + kNumBars * 8 + 16 + 1023) / 1024 * 1024;
-  static constexpr int kBytes = kEpiOff + kEpiBytes + 1024;  // + 1 KB alignment slack
+  q.num_bars = 2 * q.stages + 4 + kEpiWarps + (u8 ? q.stages + 2 * q.u8_ring : 0);
+  q.epi_off = (q.bar_off + q.num_bars * 8 + 16 + 1023) / 1024 * 1024;
+  q.bytes = q.epi_off + kEpiWarps * q.warp_epi + q.extra + 1024;  // + 1 KB alignment slack
+  return q;
+}
+
+// U8: 0 = fp32 operands; 1 = A arrives as uint8 planes (K-major); 2 = B arrives as uint8
+// planes (MN-major).  A uint8 operand is TMA-loaded into a byte staging tile and expanded
+// to fp32 in the MMA's swizzled layout by 4 converter warps (exact: 0..255).
+template <int BN, bool A_LO, bool B_LO, int EPI, int U8 = 0, int CG = 1>
+struct Smem {
+  static constexpr SmemPlan P = smem_plan(BN, A_LO, B_LO, EPI, U8, CG);
+  static constexpr int kA = kBM * kBK * 4;
+  static constexpr int kBN = BN / CG;
+  static constexpr int kB = kBN * kBK * 4;
+  static constexpr int kU8 = P.u8_slot;
+  static constexpr int kU8Ring = P.u8_ring;
+  static constexpr int kStage = P.stage;
+  static constexpr int kTmaBytes = P.tma_bytes;
+  static constexpr bool kShareLo = P.share_lo;
+  static constexpr int kExtra = P.extra;
+  static constexpr int kEpiBlocks = P.epi_blocks;
+  static constexpr int kWarpEpi = P.warp_epi;
+  static constexpr int kStages = P.stages;
+  static constexpr int kRingOff = P.ring_off;
+  static constexpr int kBarOff = P.bar_off;
+  static constexpr int kNumBars = P.num_bars;
+  static constexpr int kEpiOff = P.epi_off;
+  static constexpr int kBytes = P.bytes;
   static constexpr bool kFits = kBytes <= 227 * 1024;
   static constexpr int kAccCols = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
   static constexpr int kTmemCols = 2 * kAccCols;  // double-buffered accumulators

@@ -568,6 +568,109 @@ __global__ void __launch_bounds__(256) loss_stream_kernel(
 // out[c] (+ scatter) = sum over rows r of partial[r*stride + c], in a fixed order:
 // warp w of the block sums rows w, w+8, ... for 32 consecutive columns (lane = column,
 // coalesced), then the 8 warp sums are added in warp order.  Deterministic.
+// K3b, part 2, vectorised (A+1 <= 8, H % 4 == 0): a block owns a contiguous, balanced
+// frame range and a slab of up to 1024 columns (blockIdx.y); each thread owns 4 adjacent
+// columns (float4) of one frame lane and keeps kU 16-byte loads of h in flight.  The
+// frame lanes of a block are folded in shared memory (fixed order) before the block's
+// partial row is written, so results do not depend on timing.
+template <int kU>
+__global__ void __launch_bounds__(256, 2) loss_stream4_kernel(
+    HeadDesc hd, const float* __restrict__ params, const float* __restrict__ h, long ldh,
+    long F, const float* __restrict__ dzh, float* __restrict__ dz, float* __restrict__ dz_lo,
+    float* __restrict__ hg_partial, float* __restrict__ db_partial) {
+  constexpr int kA1 = 8;
+  __shared__ float sdz[kLossFrames * kA1];
+  __shared__ float red[256 * 4];
+  const int A = hd.A, A1 = A + 1;
+  const int quads = min(hd.H / 4, 256);            // column quads per slab
+  const int lanes = 256 / quads;                    // frame lanes per block (1,2,4,...)
+  const int tid = threadIdx.x;
+  const int q = tid % quads, lane = tid / quads;
+  const bool active = lane < lanes;
+  const int j0 = blockIdx.y * quads * 4 + q * 4;    // first column of this thread
+  const long fb = F * blockIdx.x / gridDim.x, fe = F * (blockIdx.x + 1) / gridDim.x;
+  float w[4][kA1], acc[4][kA1], db[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    db[c] = 0.f;
+#pragma unroll
+    for (int k = 0; k < kA1; ++k) {
+      acc[c][k] = 0.f;
+      float wk = 0.f;
+      if (active && k < A) wk = __ldg(params + hd.wpi + long(k) * hd.wk + long(j0 + c) * hd.wj);
+      else if (active && k == A) wk = __ldg(params + hd.wv + j0 + c);
+      w[c][k] = wk;
+    }
+  }
+  for (long f0 = fb; f0 < fe; f0 += kLossFrames) {
+    const int nf = int(fe - f0 < long(kLossFrames) ? fe - f0 : long(kLossFrames));
+    __syncthreads();
+    for (int i = tid; i < nf * kA1; i += 256) {
+      const int fi = i / kA1, k = i % kA1;
+      sdz[i] = k < A1 ? dzh[(f0 + fi) * A1 + k] : 0.f;
+    }
+    __syncthreads();
+    if (!active) continue;
+    for (int i0 = lane; i0 < nf; i0 += lanes * kU) {
+      float4 xs[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int i = i0 + u * lanes;
+        xs[u] = i < nf ? __ldg(reinterpret_cast<const float4*>(h + (f0 + i) * ldh + j0))
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int i = i0 + u * lanes;
+        if (i >= nf) break;
+        const float* d = sdz + i * kA1;
+        float dk[kA1];
+#pragma unroll
+        for (int k = 0; k < kA1; ++k) dk[k] = d[k];
+        const float x[4] = {xs[u].x, xs[u].y, xs[u].z, xs[u].w};
+        float o[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          float dh = 0.f;
+#pragma unroll
+          for (int k = 0; k < kA1; ++k) {
+            dh = fmaf(dk[k], w[c][k], dh);
+            acc[c][k] = fmaf(dk[k], x[c], acc[c][k]);
+          }
+          o[c] = dh * (1.f - x[c] * x[c]);
+          db[c] += o[c];
+        }
+        if (dz) {
+          const long off = (f0 + i) * hd.H + j0;
+          *reinterpret_cast<float4*>(dz + off) = make_float4(o[0], o[1], o[2], o[3]);
+          *reinterpret_cast<float4*>(dz_lo + off) =
+              make_float4(o[0] - tf32_hi(o[0]), o[1] - tf32_hi(o[1]), o[2] - tf32_hi(o[2]),
+                          o[3] - tf32_hi(o[3]));
+        }
+      }
+    }
+  }
+  // fold the frame lanes (lane 0 + lane 1 + ... in order), one output at a time
+  float* out = hg_partial + long(blockIdx.x) * A1 * hd.H;
+#pragma unroll
+  for (int k = 0; k <= kA1; ++k) {  // k == kA1: the last layer's bias partial
+    if (k < kA1 && k >= A1) continue;
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < 4; ++c) red[tid * 4 + c] = k < kA1 ? acc[c][k] : db[c];
+    __syncthreads();
+    if (lane == 0) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float t = red[q * 4 + c];
+        for (int l = 1; l < lanes; ++l) t += red[(l * quads + q) * 4 + c];
+        if (k < kA1) out[long(k) * hd.H + j0 + c] = t;
+        else if (dz) db_partial[long(blockIdx.x) * hd.H + j0 + c] = t;
+      }
+    }
+  }
+}
+
 template <typename Store>
 __device__ __forceinline__ void rows_reduce_block(const float* __restrict__ partial, int rows,
                                                   long cols, long stride, Store store) {
@@ -803,7 +906,12 @@ LossLaunch launch_loss_backward(const HeadDesc& hd, const float* params, const f
   const long nw = long(A1) * hd.H;
   const long nchunks = (F + kLossFrames - 1) / kLossFrames;
   LossLaunch ll;
-  ll.stream_blocks = int(std::min<long>(nchunks, kLossBlocks));
+  const bool vec = A1 <= 8 && hd.H % 4 == 0 && ldh % 4 == 0 &&
+                   (reinterpret_cast<uintptr_t>(h) & 15) == 0 && hd.H <= 4096;
+  const int slabs = ceil_div(hd.H, 1024);
+  // vectorised: 2 resident blocks per SM over all slabs, no more rows than 128-frame chunks
+  ll.stream_blocks = vec ? int(std::max<long>(1, std::min<long>(nchunks, 2 * 148 / slabs)))
+                         : int(std::min<long>(nchunks, kLossBlocks));
   ll.math_blocks = ceil_div(F, 256);
   float* bias_partial = hg_partial + long(ll.stream_blocks) * nw;
   if (A1 <= 8)
@@ -814,6 +922,12 @@ LossLaunch launch_loss_backward(const HeadDesc& hd, const float* params, const f
                                                         loss_kind, dzh, loss_partial,
                                                         bias_partial);
   TLG_CHECK_LAUNCH();
+  if (vec) {
+    loss_stream4_kernel<8><<<dim3(ll.stream_blocks, slabs), 256, 0, s>>>(
+        hd, params, h, ldh, F, dzh, dz, dz_lo, hg_partial, db_partial);
+    TLG_CHECK_LAUNCH();
+    return ll;
+  }
   const size_t smem = size_t(kLossFrames) * A1 * sizeof(float);
 #define TLG_LOSS(MA, CPT)                                                                  \
   loss_stream_kernel<MA, CPT><<<ll.stream_blocks, 256, smem, s>>>(hd, params, h, ldh, F, dzh, dz, \
