@@ -178,11 +178,11 @@ def run_reference_arm(args, cfg):
 METRIC = "learner frames/sec at 1/2/4/8 B200 + InferenceServer actions/sec vs CPU ref"
 
 
-def _ncu_traffic():
+def _ncu_traffic(kernel="fwd1"):
     """dram__bytes_read + dram__bytes_write of the dominant kernel per launch, from the
-    committed ncu --set full capture (profiles/r01_fwd1_ncu.json)."""
+    committed ncu --set full capture (profiles/r01_<kernel>_ncu.json)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_fwd1_ncu.json")) as f:
+        with open(os.path.join(ROOT, "profiles", f"r01_{kernel}_ncu.json")) as f:
             return json.load(f)["traffic_bytes_per_launch"]
     except Exception:
         return None
@@ -196,7 +196,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="C3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--obs", default="u8", choices=["u8", "f32"])
+    ap.add_argument("--obs", default="bits", choices=["bits", "u8", "f32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-infer", action="store_true")
     args = ap.parse_args()
@@ -216,7 +216,8 @@ def main():
         dist.init_process_group("gloo")
     import paper_2011_12895_b200 as tlg
 
-    obs_u8 = args.obs == "u8" and cfg.obs_kind == "binary"
+    obs_u8 = args.obs in ("u8", "bits") and cfg.obs_kind == "binary"
+    obs_bits = obs_u8 and args.obs == "bits"
     S, T, D, A, hidden = cfg.batch_size, cfg.unroll_len, cfg.obs_dim, cfg.n_actions, cfg.hidden
     lrn = tlg.Learner("mlp", D, A, hidden, algo=cfg.algo, optimizer=cfg.optimizer,
                       max_segments=S, unroll_len=T, device=local, obs_u8=obs_u8, timing=False)
@@ -228,11 +229,22 @@ def main():
         dist.broadcast_object_list(uid, src=0)
         lrn.comm_init(uid[0], world, rank)
 
-    # two distinct resident batches per rank (each > L2: the obs alone is >= 254 MB)
+    # distinct resident batches per rank, cycled so the inputs exceed L2 (126 MB): two
+    # u8/f32 batches (obs >= 254 MB each) or four bit-packed ones (34 MB each)
+    nb = 4 if obs_bits else 2
     host = [tlg.synth.make_segments(S, T, D, A, seed=cfg.seed * 100 + rank * 10 + i,
-                                    obs_kind=cfg.obs_kind, obs_u8=obs_u8) for i in range(2)]
-    dev = [tlg.DeviceSegmentBatch(h, local) for h in host]
+                                    obs_kind=cfg.obs_kind, obs_u8=obs_u8) for i in range(nb)]
+    if obs_bits:
+        packed = []
+        for h in host:
+            hb = h.slice(0, h.n_segments)
+            hb.obs = tlg.synth.pack_bits(h.obs)
+            packed.append(hb)
+        dev = [tlg.DeviceSegmentBatch(h, local, bits=True, obs_dim=D) for h in packed]
+    else:
+        dev = [tlg.DeviceSegmentBatch(h, local) for h in host]
     frames_per_step = [int(h.valid_steps.sum()) for h in host]
+    resident_bytes = sum(sum(t.numel() * t.element_size() for t in d.t.values()) for d in dev)
 
     stream = torch.cuda.ExternalStream(lrn.stream(), device=local)
 
@@ -256,7 +268,7 @@ def main():
 
     # ---- device-resident timed region (no instrumentation: small steps replay as graphs)
     for i in range(args.warmup):
-        lrn.train_step(dev[i % 2], on_device=True)
+        lrn.train_step(dev[i % nb], on_device=True)
     barrier()
     torch.cuda.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)
@@ -266,8 +278,8 @@ def main():
     with ClockSampler(local) as clk:
         ev0.record(stream)
         for i in range(args.steps):
-            lrn.train_step(dev[i % 2], on_device=True)
-            frames += frames_per_step[i % 2]
+            lrn.train_step(dev[i % nb], on_device=True)
+            frames += frames_per_step[i % nb]
             launches += lrn.last_launches()
         ev1.record(stream)
         torch.cuda.synchronize()
@@ -282,7 +294,7 @@ def main():
     lrn.set_timing(True)
     kern = {"fwd1": [], "dw1": [], "fwd2": [], "dw2": [], "dx2": [], "phases": []}
     for i in range(max(5, args.steps // 2)):
-        lrn.train_step(dev[i % 2], on_device=True)
+        lrn.train_step(dev[i % nb], on_device=True)
         kern["fwd1"].append(lrn.kernel_ms("fwd", 0))
         kern["dw1"].append(lrn.kernel_ms("dw", 0))
         if len(hidden) > 1:
@@ -328,15 +340,16 @@ def main():
         dt = max_over_ranks(time.perf_counter() - t0)
         return sum_over_ranks(fr) / dt
 
-    pinned = [pinned_view(h) for h in host]
+    # main e2e in the run's obs format; binary planes also reported as uint8 planes
+    pinned = [pinned_view(h, bits=obs_bits) for h in host[:2]]
     h2d = sum(a.nbytes for a in pinned[0].arrs.values())
     e2e_value = e2e_run(pinned)
-    e2e_bits = None
-    if obs_u8:  # binary planes also cross PCIe bit-packed (TLG_OBS_BITS), 8x fewer obs bytes
-        pb = [pinned_view(h, bits=True) for h in host]
-        e2e_bits = {"value": e2e_run(pb), "unit": "frames/s",
-                    "h2d_bytes_per_step": sum(a.nbytes for a in pb[0].arrs.values()),
-                    "d2h_bytes_per_step": 48 + 8, "obs_format": "bit-packed planes"}
+    e2e_alt = None
+    if obs_bits:
+        pu = [pinned_view(h) for h in host[:2]]
+        e2e_alt = {"value": e2e_run(pu), "unit": "frames/s",
+                   "h2d_bytes_per_step": sum(a.nbytes for a in pu[0].arrs.values()),
+                   "d2h_bytes_per_step": 48 + 8, "obs_format": "uint8 planes"}
 
     # ---- roofline of the dominant kernel (layer-1 forward GEMM)
     peaks, peak_src = measured_peaks()
@@ -344,22 +357,37 @@ def main():
     flops_fwd1 = 2.0 * F * hidden[0] * D
     t_fwd1 = float(np.mean(kern["fwd1"])) / 1e3
     t_dw1 = float(np.mean(kern["dw1"])) / 1e3
-    achieved = flops_fwd1 / t_fwd1 / 1e12
     peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
     ph = np.mean(np.array(kern["phases"]), axis=0)
     step_ms = float(ph[6])
+    # the dominant kernel of the step: the layer-1 forward or the layer-1 weight gradient
+    # (same algorithmic FLOPs, 2 F h1 D)
+    dom = "dw1" if t_dw1 >= t_fwd1 else "fwd1"
+    t_dom = max(t_dw1, t_fwd1)
+    achieved = flops_fwd1 / t_dom / 1e12
+    desc = {
+        "fwd1": ("gemm_i8_bits_fwd_kernel layer-1 forward (tcgen05.mma kind::i8: bit-packed "
+                 "binary planes x 3 fixed-point int8 weight pieces, exact int32 accumulate)"
+                 if obs_bits else
+                 "gemm_tf32x3_kernel layer-1 forward (tcgen05.mma kind::tf32, obs exact -> "
+                 "2 MMA passes)"),
+        "dw1": "gemm_tf32x3_kernel layer-1 dW = dZ1^T X (tcgen05.mma kind::tf32, MN-major "
+               "operands, uint8 planes converted in smem, 2 MMA passes, split-K)",
+    }[dom]
+    bytes_dom = (F * D // (8 if obs_bits else 1) + 3 * hidden[0] * D + 2 * 4 * F * hidden[0]
+                 if dom == "fwd1" else
+                 2 * 4 * F * hidden[0] + F * D + 4 * hidden[0] * D)
     roofline = {
-        "kernel": "gemm_tf32x3_kernel fwd layer1 (tcgen05.mma kind::tf32; uint8 obs planes "
-                  "converted in smem, exact -> 2 MMA passes)",
-        "algorithmic_bytes_per_launch": F * D + 4 * 2 * hidden[0] * D + 2 * 4 * F * hidden[0],
+        "kernel": desc,
+        "algorithmic_bytes_per_launch": bytes_dom,
         "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-        "frac": achieved / peak, "traffic": _ncu_traffic(),
+        "frac": achieved / peak, "traffic": _ncu_traffic(dom),
         "peak_source": f"{peak_src} bf16_tflops_sustained (MEASURED_PEAKS.json)",
         "algorithmic_flops_per_launch": flops_fwd1,
-        "ms_per_launch": t_fwd1 * 1e3,
-        "share_of_step": t_fwd1 * 1e3 / step_ms,
-        "note": "fp32-exact 3xTF32 split; the tf32 dense ceiling is half the bf16 peak and "
-                "each K step issues 2 (exact obs) or 3 MMA passes",
+        "ms_per_launch": t_dom * 1e3,
+        "share_of_step": t_dom * 1e3 / step_ms,
+        "note": "fp32-exact: 3xTF32 split (tf32 dense ceiling = half the bf16 peak, 2-3 MMA "
+                "passes per K step) or exact int8 fixed point for binary planes",
     }
     kernels = {
         "fwd1_ms": t_fwd1 * 1e3, "dw1_ms": t_dw1 * 1e3,
@@ -437,14 +465,20 @@ def main():
             "config": {"workload": cfg.name, "note": cfg.note, "algo": cfg.algo,
                        "optimizer": cfg.optimizer, "obs_dim": D, "hidden": list(hidden),
                        "n_actions": A, "unroll_len": T, "segments_per_gpu": S,
-                       "frames_per_gpu_step": F, "obs_format": "u8 planes" if obs_u8 else "f32",
-                       "parallelism": f"dp{world}", "gemm_precision": "3xTF32 (fp32-exact)",
-                       "l2": "inputs > L2 (obs >= 254 MB per batch, two alternating batches)"},
+                       "frames_per_gpu_step": F,
+                       "obs_format": ("bit-packed binary planes" if obs_bits else
+                                      "u8 planes" if obs_u8 else "f32"),
+                       "parallelism": f"dp{world}",
+                       "gemm_precision": ("layer 1 exact int8 fixed point (binary planes), "
+                                          "other GEMMs 3xTF32 (fp32-exact)" if obs_bits else
+                                          "3xTF32 (fp32-exact)"),
+                       "l2": f"inputs > L2: {nb} resident batches cycled, "
+                             f"{resident_bytes / 1e6:.0f} MB in total"},
             "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": 48 + 8,
-                    "note": "pinned host SoA batch (u8 planes) H2D each step, pipelined "
-                            "one step ahead on a copy stream; stats D2H each step"},
-            "e2e_bitpacked": e2e_bits,
+                    "note": "pinned host SoA batch H2D each step (same obs format as value), "
+                            "pipelined one step ahead on a copy stream; stats D2H each step"},
+            "e2e_alt_format": e2e_alt,
             "gpu_launches": launches,
             "roofline": roofline,
             "kernels": kernels,

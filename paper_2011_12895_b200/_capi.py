@@ -194,14 +194,15 @@ class SegmentBatchView:
 class DeviceSegmentBatch:
     """The same batch resident in HBM (torch tensors as device allocations)."""
 
-    def __init__(self, b, device=0):
+    def __init__(self, b, device=0, bits=False, obs_dim=None):
         import torch
         dev = torch.device("cuda", device)
-        v = SegmentBatchView(b)
+        v = SegmentBatchView(b, bits=bits, obs_dim=obs_dim)
         self.t = {k: torch.from_numpy(a).to(dev) for k, a in v.arrs.items()}
         o = self.t["obs"]
         S, T = self.t["action"].shape
-        self.c = SegmentBatchC(S, T, o.shape[2], 1 if o.dtype == torch.uint8 else 0,
+        self.c = SegmentBatchC(S, T, obs_dim if bits else o.shape[2],
+                               2 if bits else (1 if o.dtype == torch.uint8 else 0),
                                *(self.t[k].data_ptr() for k in (
                                    "obs", "action", "reward", "behavior_logp", "value_est",
                                    "done", "bootstrap", "valid_steps")))

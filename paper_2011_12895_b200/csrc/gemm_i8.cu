@@ -1,0 +1,147 @@
+// Host side of the exact-integer binary-plane GEMM (gemm_i8.cuh) + the weight quantizer.
+#include <cstdlib>
+#include <cstring>
+
+#include "gemm_i8.cuh"
+
+namespace tlg::gemm {
+
+namespace {
+
+CUtensorMap make_bytes_map(const void* base, long inner, long outer, long ld, int box_inner,
+                           int box_outer, CUtensorMapSwizzle swz) {
+  CUtensorMap m;
+  if ((reinterpret_cast<uintptr_t>(base) & 15) != 0 || ld % 16 != 0)
+    throw CudaError("int8 operand must be 16-byte aligned with a row pitch multiple of 16");
+  cuuint64_t dims[2] = {cuuint64_t(inner), cuuint64_t(outer)};
+  cuuint64_t strides[1] = {cuuint64_t(ld)};
+  cuuint32_t box[2] = {cuuint32_t(box_inner), cuuint32_t(box_outer)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled(i8) failed: " + std::to_string(r));
+  return m;
+}
+
+CUtensorMap make_f32_out_map(float* base, long n, long m, long ld) {
+  CUtensorMap t;
+  if ((reinterpret_cast<uintptr_t>(base) & 15) != 0 || (ld * 4) % 16 != 0)
+    throw CudaError("gemm output must be 16-byte aligned with a row pitch multiple of 4 floats");
+  cuuint64_t dims[2] = {cuuint64_t(n), cuuint64_t(m)};
+  cuuint64_t strides[1] = {cuuint64_t(ld) * 4};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&t, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled(out) failed: " + std::to_string(r));
+  return t;
+}
+
+template <int BN, int CG>
+void run_i8_fwd(const CUtensorMap& tb, const CUtensorMap& tq, const CUtensorMap& to,
+                const CUtensorMap& tl, const I8Params& p, const TileMap& tm, cudaStream_t stream) {
+  auto kern = gemm_i8_bits_fwd_kernel<BN, CG>;
+  constexpr int bytes = SmemI8<BN, CG>::kBytes;
+  static_assert(bytes <= 227 * 1024, "shared memory budget");
+  static bool attr = false;
+  if (!attr) {
+    TLG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    attr = true;
+  }
+  const int tiles = tm.m_tiles * tm.n_tiles;
+  if (CG == 1) {
+    kern<<<std::min(tiles, num_sms()), kThreadsI8, bytes, stream>>>(tb, tq, to, tl, p, tm);
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * std::min(tiles, num_sms() / 2));
+    cfg.blockDim = dim3(kThreadsI8);
+    cfg.dynamicSmemBytes = bytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    TLG_CUDA(cudaLaunchKernelEx(&cfg, kern, tb, tq, to, tl, p, tm));
+  }
+  TLG_CHECK_LAUNCH();
+}
+
+// one block per row: max |W[n][:]| (fixed-order tree), then the three pieces
+__global__ void __launch_bounds__(256) quantize_rows_kernel(const float* __restrict__ W, int K,
+                                                            long ldw, int8_t* __restrict__ q,
+                                                            long Kp, long plane,
+                                                            float* __restrict__ scale) {
+  __shared__ float red[8];
+  const int n = blockIdx.x;
+  const float* w = W + long(n) * ldw;
+  float mx = 0.f;
+  for (int k = threadIdx.x; k < K; k += blockDim.x) mx = fmaxf(mx, fabsf(w[k]));
+  mx = warp_max(mx);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    v = warp_max(v);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const float s = red[0] > 0.f ? red[0] / 127.f : 1.f;
+  if (threadIdx.x == 0) scale[n] = s;
+  const double inv = 1.0 / double(s);
+  int8_t* q0 = q + long(n) * Kp;
+  for (long k = threadIdx.x; k < Kp; k += blockDim.x) {
+    int a = 0, b = 0, c = 0;
+    if (k < K) {
+      const double x = double(w[k]) * inv;  // |x| <= 127 (+ rounding of s)
+      const double r0 = rint(x);
+      const double x1 = (x - r0) * 128.0;  // |x1| <= 64
+      const double r1 = rint(x1);
+      const double x2 = (x1 - r1) * 128.0;
+      a = int(r0);
+      b = int(r1);
+      c = int(rint(x2));
+      a = a > 127 ? 127 : a < -127 ? -127 : a;
+    }
+    q0[k] = int8_t(a);
+    q0[plane + k] = int8_t(b);
+    q0[2 * plane + k] = int8_t(c);
+  }
+}
+
+}  // namespace
+
+void launch_quantize_rows(const float* W, int N, int K, long ldw, int8_t* q, long Kp, float* s,
+                          cudaStream_t stream) {
+  if (Kp % 16 != 0 || Kp < K) throw CudaError("quantize_rows: Kp must be >= K and a multiple of 16");
+  quantize_rows_kernel<<<N, 256, 0, stream>>>(W, K, ldw, q, Kp, long(N) * Kp, s);
+  TLG_CHECK_LAUNCH();
+}
+
+LaunchInfo launch_i8_bits_fwd(const uint8_t* bits, long rowb, const int8_t* q, long Kp,
+                              const float* scale, const float* bias, int M, int N, int K,
+                              float* out, float* out_lo, int ldo, cudaStream_t stream) {
+  if (M <= 0 || N <= 0 || K <= 0) throw CudaError("gemm_i8: empty problem");
+  if (rowb * 8 < K || Kp < K) throw CudaError("gemm_i8: K exceeds the operand rows");
+  constexpr int BN = 128;
+  // CTA pairs (256-row tiles) whenever there are enough of them to fill the GPU
+  int cg = (M >= 2 * kBM && long(ceil_div(M, 2 * kBM)) * ceil_div(N, BN) >= num_sms() / 2) ? 2 : 1;
+  if (const char* e = std::getenv("TLG_I8_CG")) cg = std::atoi(e) == 2 ? 2 : 1;
+  I8Params p{M, N, K, scale, bias, N};
+  const TileMap tm{ceil_div(M, kBM * cg), ceil_div(N, BN), 1};
+  // bit rows: box {16 bytes = 128 elements, 128 rows}; pieces: box {128, BN / cg}, SW128
+  const CUtensorMap tb = make_bytes_map(bits, rowb, M, rowb, kBKi / 8, kBM, CU_TENSOR_MAP_SWIZZLE_NONE);
+  const CUtensorMap tq = make_bytes_map(q, Kp, 3L * N, Kp, kBKi, BN / cg, CU_TENSOR_MAP_SWIZZLE_128B);
+  const CUtensorMap to = make_f32_out_map(out, N, M, ldo);
+  const CUtensorMap tl = make_f32_out_map(out_lo, N, M, ldo);
+  if (cg == 2) run_i8_fwd<BN, 2>(tb, tq, to, tl, p, tm, stream);
+  else run_i8_fwd<BN, 1>(tb, tq, to, tl, p, tm, stream);
+  const int tiles = tm.m_tiles * tm.n_tiles;
+  return {BN, cg == 2 ? 2 * std::min(tiles, num_sms() / 2) : std::min(tiles, num_sms())};
+}
+
+}  // namespace tlg::gemm

@@ -1,0 +1,356 @@
+// Exact-integer tcgen05 GEMM for binary observation planes (kind::i8, sm_100a).
+//
+// The first trunk layer of the Pommerman-shaped configs multiplies {0,1} observation
+// planes by fp32 weights.  The planes are exact integers, so the product can run on the
+// int8 tensor cores (4x the tf32 rate) without losing the fp32-exact contract of the
+// 3xTF32 path, once the weights are written as fixed-point pieces:
+//
+//   W[n][k] = s_n (q0 + q1 / 2^7 + q2 / 2^14) + e,   q_i int8,   |e| <= s_n 2^-15,
+//   s_n = max_k |W[n][k]| / 127                         (quantize_rows_kernel)
+//
+// and the planes arrive LSB-first bit-packed (TLG_OBS_BITS: 1 bit per plane element,
+// 8x fewer bytes than uint8 in HBM and over PCIe).  Per 128-element k-block the
+// converter warps expand the 16-byte bit rows into two int8 operand tiles in the MMA's
+// 128-B swizzled layout: x (0/1) and x << 7 (0/128).  Two int32 TMEM accumulators
+//
+//   acc_a = sum_k (x<<7) q0 + x q1 = 2^7 sum x q0 + sum x q1,     acc_b = sum_k x q2
+//
+// are exact; the epilogue forms s_n (acc_a 2^-7 + acc_b 2^-14) in fp32 (one rounding)
+// and applies the fused bias + tanh.  Error vs the fp32 product: <= s_n 2^-15 per weight
+// (2.4e-7 of the row's largest weight), the same order as the 3xTF32 split's 2^-22.
+//
+// Layout, per CTA (pair mode: cta_group::2, 256-row tiles, each CTA holds half of the
+// piece rows; one elected thread of rank 0 issues the MMAs for both):
+//   warp 0      TMA producer: bit rows (local barrier), 3 piece tiles (leader barrier)
+//   warp 1      TMEM allocator + MMA issuer
+//   warps 2..5  epilogue: TMEM -> registers -> s (a/128 + b/16384) + bias -> tanh ->
+//               hi / tf32-residual planes -> swizzled smem -> TMA store
+//   warps 6..9  converters: bits -> x, x<<7 tiles
+#pragma once
+
+#include "gemm_sm100.cuh"
+
+namespace tlg::gemm {
+
+constexpr int kBKi = 128;  // int8 K elements per k-block (one 128-B swizzle row)
+constexpr int kConvWarps = 4;
+constexpr int kThreadsI8 = 32 * (2 + kEpiWarps + kConvWarps);
+
+struct I8Params {
+  int M, N, K;
+  const float* scale;  // [N] piece scale per output column
+  const float* bias;   // [N]
+  long q_rows;         // rows per piece in the stacked [3][q_rows][Kp] piece array
+};
+
+template <int BN, int CG>
+struct SmemI8 {
+  static constexpr int kX = kBM * kBKi;         // 16 KB operand tile (x, x<<7)
+  static constexpr int kBits = kBM * kBKi / 8;  // 2 KB packed source rows
+  static constexpr int kBN = BN / CG;           // piece rows held by this CTA
+  static constexpr int kQ = kBN * kBKi;         // bytes per piece tile
+  static constexpr int kStage = 2 * kX + 3 * kQ + kBits;
+  static constexpr int kEpi = kEpiWarps * 2 * 4096;
+  static constexpr int kStagesRaw = (225 * 1024 - kEpi - 2048) / kStage;
+  static constexpr int kStages = kStagesRaw > 6 ? 6 : kStagesRaw;
+  static constexpr int kBarOff = kStages * kStage;
+  // full (pieces, leader), xfull (bits, local), conv (leader), empty; tfull[2], tempty[2]
+  static constexpr int kNumBars = 4 * kStages + 4;
+  static constexpr int kEpiOff = (kBarOff + kNumBars * 8 + 16 + 1023) / 1024 * 1024;
+  static constexpr int kBytes = kEpiOff + kEpi + 1024;
+  static constexpr int kTmemCols = 4 * BN;  // 2 accumulators x double buffer
+  static_assert(kStage % 1024 == 0, "stages must keep the 1 KB swizzle alignment");
+  static_assert(kStages >= 2, "pipeline needs two stages");
+  static_assert(kTmemCols <= 512, "TMEM has 512 columns");
+};
+
+// kind::i8 instruction descriptor: s32 accumulate, A u8 (x planes), B s8 (pieces), both
+// K-major, M = 128 * CG.
+template <int BN, int CG>
+__device__ __forceinline__ constexpr uint32_t make_idesc_i8() {
+  return (2u << 4)                          // D format: s32
+         | (0u << 7)                        // A format: unsigned 8-bit
+         | (1u << 10)                       // B format: signed 8-bit
+         | (uint32_t(BN >> 3) << 17)        // N >> 3
+         | (uint32_t((kBM * CG) >> 4) << 24);  // M >> 4
+}
+
+template <int CG>
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                       uint32_t accumulate) {
+  if (CG == 2)
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+  else
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+// 4 bits (LSB first) -> 4 bytes of 0/1
+__device__ __forceinline__ uint32_t spread4(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
+
+template <int BN, int CG>
+__global__ void __launch_bounds__(kThreadsI8, 1)
+    gemm_i8_bits_fwd_kernel(const __grid_constant__ CUtensorMap tmBits,
+                            const __grid_constant__ CUtensorMap tmQ,
+                            const __grid_constant__ CUtensorMap tmOut,
+                            const __grid_constant__ CUtensorMap tmOutLo, const I8Params p,
+                            const TileMap tm) {
+  using S = SmemI8<BN, CG>;
+  const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
+  const int cl_id = CG == 2 ? int(blockIdx.x >> 1) : int(blockIdx.x);
+  const int n_cl = CG == 2 ? int(gridDim.x >> 1) : int(gridDim.x);
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t bar_full = sbase + S::kBarOff;
+  const uint32_t bar_xfull = bar_full + 8 * S::kStages;
+  const uint32_t bar_conv = bar_xfull + 8 * S::kStages;
+  const uint32_t bar_empty = bar_conv + 8 * S::kStages;
+  const uint32_t bar_tfull = bar_empty + 8 * S::kStages;  // [2]
+  const uint32_t bar_tempty = bar_tfull + 16;             // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + S::kBarOff + S::kNumBars * 8);
+  constexpr int kOffX128 = S::kX, kOffQ = 2 * S::kX, kOffBits = 2 * S::kX + 3 * S::kQ;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int num_tiles = tm.m_tiles * tm.n_tiles;
+  const int kb_total = (p.K + kBKi - 1) / kBKi;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmBits);
+    prefetch_tmap(&tmQ);
+    for (int s = 0; s < S::kStages; ++s) {
+      mbar_init(bar_full + 8 * s, 1);
+      mbar_init(bar_xfull + 8 * s, 1);
+      mbar_init(bar_conv + 8 * s, kConvWarps * CG);
+      mbar_init(bar_empty + 8 * s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(bar_tfull + 8 * a, 1);
+      mbar_init(bar_tempty + 8 * a, kEpiWarps * CG);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    if (CG == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "n"(S::kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "n"(S::kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+  }
+  tc_fence_before();
+  if (CG == 2) cluster_sync_all();
+  else __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer =====
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cl_id; t < num_tiles; t += n_cl) {
+        const int nt = t % tm.n_tiles, mt = t / tm.n_tiles;
+        const int m0 = mt * kBM * CG + int(rank) * kBM;
+        const int n0 = nt * BN + int(rank) * S::kBN;
+        for (int kb = 0; kb < kb_total; ++kb) {
+          mbar_wait(bar_empty + 8 * stage, phase ^ 1);
+          const uint32_t st = sbase + stage * S::kStage;
+          mbar_expect_tx(bar_xfull + 8 * stage, S::kBits);
+          tma_load_2d(st + kOffBits, &tmBits, kb * (kBKi / 8), m0, bar_xfull + 8 * stage);
+          const uint32_t full = CG == 2 ? map_rank0(bar_full + 8 * stage) : bar_full + 8 * stage;
+          if (rank == 0) mbar_expect_tx(bar_full + 8 * stage, 3 * S::kQ * CG);
+#pragma unroll
+          for (int pc = 0; pc < 3; ++pc) {
+            const int row = pc * int(p.q_rows) + n0;
+            if (CG == 2) tma_load_2d_pair(st + kOffQ + pc * S::kQ, &tmQ, kb * kBKi, row, full);
+            else tma_load_2d(st + kOffQ + pc * S::kQ, &tmQ, kb * kBKi, row, full);
+          }
+          if (++stage == S::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // ===== MMA issuer =====
+      constexpr uint32_t idesc = make_idesc_i8<BN, CG>();
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = cl_id; t < num_tiles; t += n_cl, ++it) {
+        const int acc_buf = it & 1;
+        mbar_wait(bar_tempty + 8 * acc_buf, ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t tacc_a = tmem_base + uint32_t(acc_buf * 2 * BN);
+        const uint32_t tacc_b = tacc_a + uint32_t(BN);
+        for (int kb = 0; kb < kb_total; ++kb) {
+          mbar_wait(bar_full + 8 * stage, phase);
+          mbar_wait(bar_conv + 8 * stage, phase);
+          tc_fence_after();
+          const uint32_t st = sbase + stage * S::kStage;
+#pragma unroll
+          for (int k = 0; k < kBKi / 32; ++k) {
+            // K-major SW128: +32 B per 32-element K step; SBO = 1 KB between 8-row atoms
+            const uint64_t dx = make_sdesc<false>(st + k * 32, 16, 1024);
+            const uint64_t dx7 = make_sdesc<false>(st + kOffX128 + k * 32, 16, 1024);
+            const uint64_t dq0 = make_sdesc<false>(st + kOffQ + k * 32, 16, 1024);
+            const uint64_t dq1 = make_sdesc<false>(st + kOffQ + S::kQ + k * 32, 16, 1024);
+            const uint64_t dq2 = make_sdesc<false>(st + kOffQ + 2 * S::kQ + k * 32, 16, 1024);
+            const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
+            mma_i8<CG>(tacc_a, dx7, dq0, idesc, acc);
+            mma_i8<CG>(tacc_a, dx, dq1, idesc, 1u);
+            mma_i8<CG>(tacc_b, dx, dq2, idesc, acc);
+          }
+          if (CG == 2) mma_commit_pair(bar_empty + 8 * stage);
+          else mma_commit(bar_empty + 8 * stage);
+          if (++stage == S::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (CG == 2) mma_commit_pair(bar_tfull + 8 * acc_buf);
+        else mma_commit(bar_tfull + 8 * acc_buf);
+      }
+    }
+  } else if (warp >= 2 + kEpiWarps) {
+    // ===== converters: 16-B bit row -> 128-B x row and x<<7 row (SW128 K-major) =====
+    const int r = threadIdx.x - (2 + kEpiWarps) * 32;  // tile row 0..127
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = cl_id; t < num_tiles; t += n_cl) {
+      for (int kb = 0; kb < kb_total; ++kb) {
+        mbar_wait(bar_xfull + 8 * stage, phase);
+        uint8_t* st = smem + stage * S::kStage;
+        const uint4 b = *reinterpret_cast<const uint4*>(st + kOffBits + r * 16);
+        const uint32_t bw[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          // chunk c: elements 16c..16c+15 = bytes 2c, 2c+1 of the bit row
+          const uint32_t two = (bw[c >> 1] >> ((c & 1) * 16)) & 0xFFFFu;
+          const uint4 x = make_uint4(spread4(two & 15u), spread4((two >> 4) & 15u),
+                                     spread4((two >> 8) & 15u), spread4(two >> 12));
+          const uint32_t off = uint32_t(r * 128 + ((c ^ (r & 7)) << 4));
+          *reinterpret_cast<uint4*>(st + off) = x;
+          *reinterpret_cast<uint4*>(st + kOffX128 + off) =
+              make_uint4(x.x << 7, x.y << 7, x.z << 7, x.w << 7);
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          if (CG == 2) mbar_arrive_cluster(map_rank0(bar_conv + 8 * stage));
+          else mbar_arrive(bar_conv + 8 * stage);
+        }
+        if (++stage == S::kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ===== epilogue: warps 2..5 own TMEM lane quadrants (warp % 4) =====
+    const int q = warp & 3;
+    const int ew = warp - 2;
+    const uint32_t blk = sbase + S::kEpiOff + uint32_t(ew * 2 * 4096);
+    uint8_t* blk_ptr = smem + S::kEpiOff + ew * 2 * 4096;
+    int it = 0;
+    for (int t = cl_id; t < num_tiles; t += n_cl, ++it) {
+      const int nt = t % tm.n_tiles, mt = t / tm.n_tiles;
+      const int m0 = mt * kBM * CG + int(rank) * kBM, n0 = nt * BN;
+      const int rbase = m0 + q * 32;
+      const int acc_buf = it & 1;
+      mbar_wait(bar_tfull + 8 * acc_buf, (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t ta = tmem_base + uint32_t(acc_buf * 2 * BN) + (uint32_t(q * 32) << 16);
+      const uint32_t tb = ta + uint32_t(BN);
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        const int nb = n0 + c;
+        uint32_t ra[32], rb[32];
+        tmem_ld32(ta + uint32_t(c), ra);
+        tmem_ld32(tb + uint32_t(c), rb);
+        const bool colok = nb + lane < p.N;
+        const float sc = colok ? __ldg(p.scale + nb + lane) : 0.f;
+        const float bi = colok ? __ldg(p.bias + nb + lane) : 0.f;
+        float o[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float s = __shfl_sync(0xffffffffu, sc, j);
+          const float bj = __shfl_sync(0xffffffffu, bi, j);
+          const float z = fmaf(float(int(ra[j])), s * 0.0078125f,
+                               float(int(rb[j])) * (s * 6.103515625e-05f));
+          o[j] = tanhf(z + bj);
+        }
+        if (lane == 0) bulk_wait_read();
+        __syncwarp();
+#pragma unroll
+        for (int j4 = 0; j4 < 8; ++j4) {
+          *reinterpret_cast<float4*>(blk_ptr + swz(lane, j4)) =
+              make_float4(o[4 * j4], o[4 * j4 + 1], o[4 * j4 + 2], o[4 * j4 + 3]);
+          *reinterpret_cast<float4*>(blk_ptr + 4096 + swz(lane, j4)) =
+              make_float4(o[4 * j4] - tf32_hi(o[4 * j4]), o[4 * j4 + 1] - tf32_hi(o[4 * j4 + 1]),
+                          o[4 * j4 + 2] - tf32_hi(o[4 * j4 + 2]),
+                          o[4 * j4 + 3] - tf32_hi(o[4 * j4 + 3]));
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tmOut, nb, rbase, blk);
+          tma_store_2d(&tmOutLo, nb, rbase, blk + 4096);
+          bulk_commit();
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (CG == 2) mbar_arrive_cluster(map_rank0(bar_tempty + 8 * acc_buf));
+        else mbar_arrive(bar_tempty + 8 * acc_buf);
+      }
+    }
+    if (lane == 0) bulk_wait_all();
+  }
+
+  tc_fence_before();
+  if (CG == 2) cluster_sync_all();
+  else __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    if (CG == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "n"(S::kTmemCols));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "n"(S::kTmemCols));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Host side
+
+// W [N][K] (row pitch ldw floats) -> pieces q [3][N][Kp] (int8, zero past K) and per-row
+// scales s [N] (see the header comment).  Kp % 16 == 0.
+void launch_quantize_rows(const float* W, int N, int K, long ldw, int8_t* q, long Kp, float* s,
+                          cudaStream_t stream);
+
+// out = tanh(X . W^T + b) with X binary planes bit-packed LSB first ([M] rows of `rowb`
+// bytes, rowb % 16 == 0, bits past K ignored) and W given as launch_quantize_rows pieces.
+// Writes the full fp32 plane and the tf32 residual plane (row pitch ldo).
+LaunchInfo launch_i8_bits_fwd(const uint8_t* bits, long rowb, const int8_t* q, long Kp,
+                              const float* scale, const float* bias, int M, int N, int K,
+                              float* out, float* out_lo, int ldo, cudaStream_t stream);
+
+}  // namespace tlg::gemm

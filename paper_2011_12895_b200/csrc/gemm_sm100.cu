@@ -9,8 +9,6 @@
 
 namespace tlg::gemm {
 
-namespace {
-
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -24,6 +22,18 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   });
   return fn;
 }
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    TLG_CUDA(cudaGetDevice(&dev));
+    TLG_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return n;
+}
+
+namespace {
 
 // 2D fp32 tensor map, 128-byte swizzle, box {32 (inner), box_rows}.
 // uint8 2D map, no swizzle (the converter warps lay the tile out for the MMA).
@@ -90,16 +100,6 @@ CUtensorMap operand_map(const float* ptr, const Operand& op, long mn, long k, in
 }
 
 thread_local int g_cg = 1;  // CTA-pair mode chosen by launch() for the current call
-
-int num_sms() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    TLG_CUDA(cudaGetDevice(&dev));
-    TLG_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
-  }
-  return n;
-}
 
 struct EpiMaps {
   CUtensorMap out, out_lo, act;
@@ -225,9 +225,7 @@ LaunchInfo launch(const Operand& A, const Operand& B, int M, int N, int K, int e
   for (;;) {
     cg = 1;
     const long tiles2 = long(ceil_div(M, 2 * kBM)) * ceil_div(N, BN) * splits;
-    // (the uint8 converter path measured slower as a pair: keep it on single CTAs)
-    if (BN >= 128 && M >= 2 * kBM && tiles2 >= num_sms() / 2 && kb_tile >= 8 && !A.u8 && !B.u8)
-      cg = 2;
+    if (BN >= 128 && M >= 2 * kBM && tiles2 >= num_sms() / 2 && kb_tile >= 8) cg = 2;
     if (const char* e = std::getenv("TLG_GEMM_CG")) cg = std::atoi(e) == 2 && BN >= 128 ? 2 : 1;
     if (const char* e = std::getenv("TLG_GEMM_CG_U8"))  // tuning experiments only
       if ((A.u8 || B.u8) && std::atoi(e) == 2 && BN >= 128) cg = 2;

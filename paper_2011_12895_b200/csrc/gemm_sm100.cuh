@@ -23,6 +23,8 @@
 // overlaps the MMAs of tile i+1).
 #pragma once
 
+#include <cudaTypedefs.h>
+
 #include "common.cuh"
 
 namespace tlg::gemm {
@@ -158,9 +160,10 @@ __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
                    : "memory");
 }
+// (default .release.cta semantics, as CUTLASS's ClusterBarrier::arrive: the explicit
+// .release.cluster form compiles to MEMBAR.ALL.GPU + ERRBAR, ~1 us per arrive)
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-               : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // TMA into this CTA's smem, completion counted on the pair leader's mbarrier
 __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, int x, int y,
@@ -912,5 +915,9 @@ LaunchInfo launch(const Operand& A, const Operand& B, int M, int N, int K, int e
 
 // Number of K splits that fills the GPU for a (M, N, K) problem, given a cap.
 int pick_splits(int M, int N, int K, int max_splits);
+
+int num_sms();
+// cuTensorMapEncodeTiled through the runtime's driver entry point
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn();
 
 }  // namespace tlg::gemm

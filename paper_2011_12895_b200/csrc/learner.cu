@@ -23,7 +23,7 @@
 #include <vector>
 
 #include "../../include/tlg_b200.h"
-#include "gemm_sm100.cuh"
+#include "gemm_i8.cuh"
 #include "learner_kernels.cuh"
 
 namespace {
@@ -157,7 +157,15 @@ struct tlg_learner {
   // batch
   float *obs, *obs_lo;
   uint8_t* obs_u8;
-  uint8_t* obs_bits;
+  uint8_t* obs_bits;       // bit planes, row pitch bits_pitch (16-B aligned rows)
+  long bits_pitch = 0;
+  uint8_t* obs_bits_lin;    // host bit rows as shipped (ceil(D/8) bytes per frame)
+  // layer-1 weights as fixed-point int8 pieces for the exact binary-plane GEMM
+  int8_t* wq = nullptr;
+  float* wq_scale = nullptr;
+  long wq_kp = 0;
+  const bool i8_disabled = std::getenv("TLG_NO_I8") != nullptr;
+  bool wq_fresh = false;
   int32_t* action;
   float *reward, *blogp, *value;
   uint8_t* done;
@@ -210,8 +218,16 @@ struct tlg_learner {
     obs = mem.add<float>(F_max * D);
     obs_lo = mem.add<float>(F_max * D);
     obs_u8 = cfg.obs_dtype != TLG_OBS_F32 ? mem.add<uint8_t>(F_max * D + 16) : nullptr;
-    obs_bits = cfg.obs_dtype != TLG_OBS_F32 ? mem.add<uint8_t>(F_max * ((D + 7) / 8) + 16)
-                                            : nullptr;
+    bits_pitch = ((D + 7) / 8 + 15) / 16 * 16;
+    obs_bits = cfg.obs_dtype != TLG_OBS_F32 ? mem.add<uint8_t>(F_max * bits_pitch + 16) : nullptr;
+    if (obs_bits) TLG_CUDA(cudaMemset(obs_bits, 0, F_max * bits_pitch + 16));
+    obs_bits_lin = cfg.obs_dtype != TLG_OBS_F32 ? mem.add<uint8_t>(F_max * ((D + 7) / 8) + 16)
+                                                : nullptr;
+    if (obs_bits && net.L >= 2) {
+      wq_kp = (D + 15) / 16 * 16;
+      wq = mem.add<int8_t>(3 * long(net.dims[1]) * wq_kp);
+      wq_scale = mem.add<float>(net.dims[1]);
+    }
     action = mem.add<int32_t>(F_max);
     reward = mem.add<float>(F_max);
     blogp = mem.add<float>(F_max);
@@ -291,10 +307,16 @@ struct tlg_learner {
   // uint8 observations feed the first trunk GEMM and its dW directly (converted in smem)
   bool direct_u8() const { return net.L > 0 && net.D % 16 == 0; }
   const uint8_t* x0_u8 = nullptr;
+  const uint8_t* x0_bits = nullptr;  // bit planes (pitch bits_pitch) for the int8 layer-1 GEMM
+
+  // binary planes take the exact int8 tensor-core path for layer 1 (L >= 2: the fused
+  // heads stay on the last trunk layer's tf32 epilogue)
+  bool i8_layer1() const { return wq != nullptr && !i8_disabled; }
 
   void stage(const tlg_segment_batch& b, int on_device, tlg::BatchDev& bd, const float** obs_f32,
              bool& obs_exact, bool internal = false) {
     x0_u8 = nullptr;
+    x0_bits = nullptr;
     if (b.n_segments == 0) throw InvalidArg("empty minibatch");
     if (int(b.n_segments) > S_max) throw InvalidArg("batch exceeds the learner's max_segments");
     if (int(b.unroll_len) != T) throw InvalidArg("unroll_len mismatch");
@@ -311,10 +333,15 @@ struct tlg_learner {
       const long rowb = (D + 7) / 8;
       const uint8_t* bits = static_cast<const uint8_t*>(b.obs);
       if (!on_device) {
-        TLG_CUDA(cudaMemcpyAsync(obs_bits, bits, size_t(F * rowb), cudaMemcpyHostToDevice, stream));
-        bits = obs_bits;
+        TLG_CUDA(cudaMemcpyAsync(obs_bits_lin, bits, size_t(F * rowb), cudaMemcpyHostToDevice,
+                                 stream));
+        bits = obs_bits_lin;
       }
-      tlg::launch_unpack_bits(bits, rowb, F, D, obs_u8, stream);
+      // one pass: rows re-pitched to 16 B for the int8 GEMM's TMA (pad bytes zero) and
+      // expanded to the uint8 planes the layer-1 dW reads
+      tlg::launch_unpack_bits(bits, rowb, F, D, obs_u8, i8_layer1() ? obs_bits : nullptr,
+                              bits_pitch, stream);
+      if (i8_layer1()) x0_bits = obs_bits;
       ++launches;
       tlg_segment_batch u = b;
       u.obs_dtype = TLG_OBS_U8;
@@ -394,6 +421,7 @@ struct tlg_learner {
     tlg::BatchDev bd{};
     const float* x0 = nullptr;
     const uint8_t* x0_u8 = nullptr;
+    const uint8_t* x0_bits = nullptr;
     bool exact = false;
   };
 
@@ -401,6 +429,7 @@ struct tlg_learner {
     Staged sg;
     stage(b, on_device, sg.bd, &sg.x0, sg.exact, internal);
     sg.x0_u8 = x0_u8;
+    sg.x0_bits = x0_bits;
     return sg;
   }
 
@@ -445,8 +474,20 @@ struct tlg_learner {
         p.head_part = head_part;
       }
       if (shard == 0) kmark(0, int(l), 0);
-      const int bn = tlg::gemm::launch(A, B, int(F), outw, in, tlg::gemm::kEpiFwdTanh, p, 1,
-                                       stream).bn;
+      int bn;
+      if (l == 0 && sg.x0_bits != nullptr) {
+        if (!wq_fresh) {  // this step's layer-1 weights -> pieces (once per step)
+          tlg::gemm::launch_quantize_rows(params + net.w_off[0], outw, in, in, wq, wq_kp, wq_scale,
+                                          stream);
+          wq_fresh = true;
+          ++launches;
+        }
+        // binary planes x int8 weight pieces: exact integer tensor-core GEMM
+        bn = tlg::gemm::launch_i8_bits_fwd(sg.x0_bits, bits_pitch, wq, wq_kp, wq_scale, p.bias,
+                                           int(F), outw, in, act[0], act_lo[0], outw, stream).bn;
+      } else {
+        bn = tlg::gemm::launch(A, B, int(F), outw, in, tlg::gemm::kEpiFwdTanh, p, 1, stream).bn;
+      }
       if (shard == 0) kmark(0, int(l), 1);
       if (fuse_head) head_tiles = (outw + bn - 1) / bn;
       ++launches;
@@ -549,7 +590,8 @@ struct tlg_learner {
     TLG_CUDA(cudaSetDevice(cfg.device));
     if (use_graph(bs, n)) {
       const Staged sg = stage_shard(bs[0], on_device, /*internal=*/true);
-      const long key = long(sg.bd.S) * 4 + (sg.x0_u8 ? 1 : 0) + (sg.exact ? 2 : 0);
+      const long key = long(sg.bd.S) * 8 + (sg.x0_u8 ? 1 : 0) + (sg.exact ? 2 : 0) +
+                       (sg.x0_bits ? 4 : 0);
       if (!graph_exec || key != graph_key || graph_hyper != hyper_version) {
         if (graph_exec) cudaGraphExecDestroy(graph_exec);
         graph_exec = nullptr;
@@ -651,6 +693,7 @@ struct tlg_learner {
   void enqueue_device_step(const Staged* staged, int n, const tlg_segment_batch* bs = nullptr,
                            int on_device = 0) {
     launches = 0;
+    wq_fresh = false;
     mark(0);
     TLG_CUDA(cudaMemsetAsync(err, 0, 16, stream));
     TLG_CUDA(cudaMemsetAsync(grad + P_pad, 0, 16, stream));

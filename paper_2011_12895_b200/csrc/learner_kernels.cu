@@ -24,13 +24,17 @@ __global__ void expand_u8_kernel(const uchar4* __restrict__ in, float4* __restri
   }
 }
 
-// Bit-packed 0/1 observation planes -> uint8 (one thread per packed byte).
+// Bit-packed 0/1 observation planes -> uint8 (one thread per packed byte); optionally
+// also the same bit rows re-pitched to `pitch` bytes (16-B aligned rows for TMA).
 __global__ void unpack_bits_kernel(const uint8_t* __restrict__ bits, long rowb, long F, long D,
-                                   uint8_t* __restrict__ out) {
+                                   uint8_t* __restrict__ out, uint8_t* __restrict__ pitched,
+                                   long pitch) {
   for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < F * rowb;
        i += long(gridDim.x) * blockDim.x) {
     const long f = i / rowb, j = i % rowb;
     const uint32_t v = bits[i];
+    if (pitched) pitched[f * pitch + j] = uint8_t(v);
+    if (!out) continue;
     uint8_t* o = out + f * D + 8 * j;
     if (8 * j + 8 <= D && ((reinterpret_cast<uintptr_t>(o) & 7) == 0)) {
       uint2 w;
@@ -842,8 +846,10 @@ void launch_expand_u8(const uint8_t* in, float* out, long n, cudaStream_t s) {
 }
 
 void launch_unpack_bits(const uint8_t* bits, long rowb, long F, long D, uint8_t* out,
+                        uint8_t* pitched, long pitch,
                         cudaStream_t s) {
-  unpack_bits_kernel<<<grid_for(F * rowb, 256), 256, 0, s>>>(bits, rowb, F, D, out);
+  unpack_bits_kernel<<<grid_for(F * rowb, 256), 256, 0, s>>>(bits, rowb, F, D, out, pitched,
+                                                             pitch);
   TLG_CHECK_LAUNCH();
 }
 

@@ -70,6 +70,7 @@ constexpr int kLossBlocks = 444;  // persistent loss_backward blocks (3 per SM):
 void launch_expand_u8(const uint8_t* in, float* out, long n, cudaStream_t s);
 void launch_split_lo(const float* x, float* lo, long n, cudaStream_t s);
 void launch_unpack_bits(const uint8_t* bits, long rowb, long F, long D, uint8_t* out,
+                        uint8_t* pitched, long pitch,
                         cudaStream_t s);
 void launch_head_forward(const HeadDesc& hd, const float* params, const float* h, long ldh,
                          const BatchDev* b, long F, float* head_out, float* tlogp,

@@ -4,10 +4,11 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
+#include <cstring>
 #include <random>
 #include <vector>
 
-#include "../gemm_sm100.cuh"
+#include "../gemm_i8.cuh"
 
 using namespace tlg;
 
@@ -196,6 +197,80 @@ void check(const char* name, int M, int N, int K, bool a_mn, bool b_mn, bool a_e
   cudaFree(bias.lo);
 }
 
+// Binary planes (bit-packed) x fixed-point int8 pieces of W (kind::i8), fused bias + tanh.
+void check_i8(const char* name, int M, int N, int K) {
+  std::mt19937 rng(M * 17 + N * 3 + K);
+  Buf A, B, bias;
+  A.init(long(M) * K, rng, true);
+  B.init(long(N) * K, rng);
+  bias.init(N, rng);
+  double *ref, *refabs;
+  TLG_CUDA(cudaMalloc(&ref, long(M) * N * 8));
+  TLG_CUDA(cudaMalloc(&refabs, long(M) * N * 8));
+  ref_gemm<<<dim3((M + 127) / 128, N), 128>>>(A.x, K, false, B.x, K, false, M, N, K, ref, refabs);
+  const long rowb = ((K + 7) / 8 + 15) / 16 * 16, Kp = (K + 15) / 16 * 16;
+  std::vector<float> ha(long(M) * K);
+  TLG_CUDA(cudaMemcpy(ha.data(), A.x, ha.size() * 4, cudaMemcpyDeviceToHost));
+  std::vector<uint8_t> hb(long(M) * rowb, 0);
+  for (long m = 0; m < M; ++m)
+    for (long k = 0; k < K; ++k)
+      if (ha[m * K + k] != 0.f) hb[m * rowb + k / 8] |= uint8_t(1u << (k % 8));
+  uint8_t* bits;
+  int8_t* q;
+  float *scale, *out, *out_lo;
+  TLG_CUDA(cudaMalloc(&bits, hb.size()));
+  TLG_CUDA(cudaMemcpy(bits, hb.data(), hb.size(), cudaMemcpyHostToDevice));
+  TLG_CUDA(cudaMalloc(&q, 3 * long(N) * Kp));
+  TLG_CUDA(cudaMalloc(&scale, N * 4));
+  TLG_CUDA(cudaMalloc(&out, long(M) * N * 4));
+  TLG_CUDA(cudaMalloc(&out_lo, long(M) * N * 4));
+  gemm::launch_quantize_rows(B.x, N, K, K, q, Kp, scale, 0);
+  gemm::launch_i8_bits_fwd(bits, rowb, q, Kp, scale, bias.x, M, N, K, out, out_lo, N, 0);
+  TLG_CUDA(cudaDeviceSynchronize());
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  const int reps = 5;
+  for (int i = 0; i < reps; ++i)
+    gemm::launch_i8_bits_fwd(bits, rowb, q, Kp, scale, bias.x, M, N, K, out, out_lo, N, 0);
+  cudaEventRecord(e1);
+  TLG_CUDA(cudaDeviceSynchronize());
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  ms /= reps;
+  std::vector<double> hr(long(M) * N), hab(long(M) * N);
+  std::vector<float> hh(long(M) * N), hl(long(M) * N), hbias(N);
+  TLG_CUDA(cudaMemcpy(hr.data(), ref, hr.size() * 8, cudaMemcpyDeviceToHost));
+  TLG_CUDA(cudaMemcpy(hab.data(), refabs, hab.size() * 8, cudaMemcpyDeviceToHost));
+  TLG_CUDA(cudaMemcpy(hh.data(), out, hh.size() * 4, cudaMemcpyDeviceToHost));
+  TLG_CUDA(cudaMemcpy(hl.data(), out_lo, hl.size() * 4, cudaMemcpyDeviceToHost));
+  TLG_CUDA(cudaMemcpy(hbias.data(), bias.x, N * 4, cudaMemcpyDeviceToHost));
+  double worst = 0;
+  long bad = 0;
+  for (long i = 0; i < long(M) * N; ++i) {
+    const int n = int(i % N);
+    double got = hh[i];
+    uint32_t u;
+    std::memcpy(&u, &hh[i], 4);
+    u &= 0xFFFFE000u;
+    float th;
+    std::memcpy(&th, &u, 4);
+    if (hl[i] != hh[i] - th) got = 1e9;  // residual plane = x - trunc_tf32(x)
+    const double want = std::tanh(hr[i] + hbias[n]);
+    const double err = std::fabs(got - want) / (hab[i] + 1.0);
+    if (!(err <= 2e-6)) ++bad;
+    if (!(err <= worst)) worst = std::isfinite(err) ? std::max(worst, err) : 1e30;
+  }
+  const double tflops = 2.0 * M * N * K / (ms * 1e-3) / 1e12;
+  printf("%-34s M=%6d N=%5d K=%6d split=1 : worst rel %.3e bad %ld  %.3f ms %.1f TF/s  %s\n",
+         name, M, N, K, worst, bad, ms, tflops, bad ? "FAIL" : "ok");
+  if (bad) ++failures;
+  cudaFree(ref); cudaFree(refabs); cudaFree(bits); cudaFree(q); cudaFree(scale); cudaFree(out);
+  cudaFree(out_lo); cudaFree(A.x); cudaFree(A.hi); cudaFree(A.lo); cudaFree(B.x); cudaFree(B.hi);
+  cudaFree(B.lo); cudaFree(bias.x); cudaFree(bias.hi); cudaFree(bias.lo);
+}
+
 int main(int argc, char** argv) {
   try {
     using namespace gemm;
@@ -221,7 +296,11 @@ int main(int argc, char** argv) {
     check("U8B dW store MN/MN", 256, 1936, 1000, true, true, false, kEpiStore, 3);
     check("U8B dW store MN/MN N=64", 200, 64, 300, true, true, false, kEpiStore, 1);
     g_u8 = 0;
+    check_i8("I8 bits fwd", 300, 256, 200);
+    check_i8("I8 bits fwd N=100 K=1936", 700, 100, 1936);
+    check_i8("I8 bits fwd pair", 4096, 256, 1936);
     if (argc > 1) {
+      check_i8("perf I8 bits fwd C3 L1", 131072, 256, 1936);
       g_u8 = 1;
       check("perf U8 fwd C3 L1", 131072, 256, 1936, false, false, true, kEpiFwdTanh, 1);
       g_u8 = 2;
