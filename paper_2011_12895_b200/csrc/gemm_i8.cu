@@ -113,7 +113,133 @@ __global__ void __launch_bounds__(256) quantize_rows_kernel(const float* __restr
   }
 }
 
+template <int CG>
+void run_i8_dw(const CUtensorMap& tp, const CUtensorMap& tb, const CUtensorMap& tw,
+               const I8DwParams& p, const TileMap& tm, cudaStream_t stream) {
+  auto kern = gemm_i8_bits_dw_kernel<CG>;
+  constexpr int bytes = SmemI8Dw<CG>::kBytes;
+  static_assert(bytes <= 227 * 1024, "shared memory budget");
+  static bool attr = false;
+  if (!attr) {
+    TLG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    attr = true;
+  }
+  const int tiles = tm.m_tiles * tm.n_tiles * tm.splits;
+  if (CG == 1) {
+    kern<<<std::min(tiles, num_sms()), kThreadsI8, bytes, stream>>>(tp, tb, tw, p, tm);
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * std::min(tiles, num_sms() / 2));
+    cfg.blockDim = dim3(kThreadsI8);
+    cfg.dynamicSmemBytes = bytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    TLG_CUDA(cudaLaunchKernelEx(&cfg, kern, tp, tb, tw, p, tm));
+  }
+  TLG_CHECK_LAUNCH();
+}
+
+// dZ -> three int8 pieces per element, scale per (split, column) from the dX epilogue's
+// column maxima.  A block covers kQRows frames (never straddling a split) x all columns:
+// thread = (4-column quad, frame lane), scale inverses computed once per thread.
+constexpr int kQRows = 64;
+__global__ void __launch_bounds__(256) quantize_cols_kernel(const float* __restrict__ Z, long F,
+                                                            int M, long ldz,
+                                                            const unsigned* __restrict__ colmax,
+                                                            long rows_per_split,
+                                                            int8_t* __restrict__ P) {
+  const int quads = M / 4;
+  const int lanes = max(1, 256 / quads);
+  const int per_pass = (256 / quads) > 0 ? quads : 256;  // quads handled per pass
+  const long plane = F * M;
+  const long f0 = long(blockIdx.x) * kQRows;
+  const long g = f0 / rows_per_split;
+  for (int q0 = 0; q0 < quads; q0 += per_pass) {
+    const int qi = q0 + int(threadIdx.x) % per_pass;
+    const int lane = int(threadIdx.x) / per_pass;
+    if (qi >= quads || lane >= lanes) continue;
+    const int m = qi * 4;
+    float inv[4], lim[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float mx = __uint_as_float(colmax[g * M + m + j]);
+      inv[j] = mx > 0.f ? 127.f / mx : 1.f;  // the GEMM epilogue multiplies by mx / 127
+      lim[j] = 127.f;
+    }
+    for (long f = f0 + lane; f < min(F, f0 + kQRows); f += lanes) {
+      const float4 z = *reinterpret_cast<const float4*>(Z + f * ldz + m);
+      const float zv[4] = {z.x, z.y, z.z, z.w};
+      uint32_t w0 = 0, w1 = 0, w2 = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        // x = z * (127 / max) rounds once (|x| <= 127 (1 + 2^-23)); the residual steps
+        // are exact (Sterbenz, power-of-two scaling)
+        const float x = zv[j] * inv[j];
+        const float r0 = fminf(fmaxf(rintf(x), -lim[j]), lim[j]);
+        const float x1 = (x - r0) * 128.f;
+        const float r1 = rintf(x1);
+        const int a = int(r0), b = int(r1), c = int(rintf((x1 - r1) * 128.f));
+        w0 |= uint32_t(a & 0xFF) << (8 * j);
+        w1 |= uint32_t(b & 0xFF) << (8 * j);
+        w2 |= uint32_t(c & 0xFF) << (8 * j);
+      }
+      const long o = f * M + m;
+      *reinterpret_cast<uint32_t*>(P + o) = w0;
+      *reinterpret_cast<uint32_t*>(P + plane + o) = w1;
+      *reinterpret_cast<uint32_t*>(P + 2 * plane + o) = w2;
+    }
+  }
+}
+
+CUtensorMap make_ws_map(float* base, long n, long m, long splits) {
+  CUtensorMap t;
+  cuuint64_t dims[3] = {cuuint64_t(n), cuuint64_t(m), cuuint64_t(splits)};
+  cuuint64_t strides[2] = {cuuint64_t(n) * 4, cuuint64_t(n) * m * 4};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  if ((reinterpret_cast<uintptr_t>(base) & 15) != 0 || (n * 4) % 16 != 0)
+    throw CudaError("gemm workspace must be 16-byte aligned with N a multiple of 4");
+  CUresult r = encode_fn()(&t, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled(ws) failed: " + std::to_string(r));
+  return t;
+}
+
 }  // namespace
+
+void launch_quantize_cols(const float* Z, long F, int M, long ldz, const unsigned* colmax,
+                          long rows_per_split, int8_t* P, cudaStream_t stream) {
+  if (M % 4 != 0 || ldz % 4 != 0) throw CudaError("quantize_cols: M and ldz must be multiples of 4");
+  if (rows_per_split % kQRows != 0) throw CudaError("quantize_cols: split rows % 64 != 0");
+  quantize_cols_kernel<<<ceil_div(F, kQRows), 256, 0, stream>>>(Z, F, M, ldz, colmax,
+                                                                rows_per_split, P);
+  TLG_CHECK_LAUNCH();
+}
+
+void launch_i8_bits_dw(const int8_t* P, const uint8_t* bits, long rowb, const unsigned* colmax,
+                       int M, int N, int K, int kb_per_split, float* ws, cudaStream_t stream) {
+  if (M <= 0 || N <= 0 || K <= 0) throw CudaError("gemm_i8_dw: empty problem");
+  if (long(kb_per_split) * kBKi > 131072) throw CudaError("gemm_i8_dw: split too long for int32");
+  if (M % 16 != 0) throw CudaError("gemm_i8_dw: M must be a multiple of 16");
+  int cg = M >= 2 * kBM ? 2 : 1;
+  if (const char* e = std::getenv("TLG_I8_CG")) cg = std::atoi(e) == 2 ? 2 : 1;
+  const int kb_total = ceil_div(K, kBKi);
+  const int splits = ceil_div(kb_total, kb_per_split);
+  const TileMap tm{ceil_div(M, kBM * cg), ceil_div(N, 128 * cg), splits};
+  I8DwParams p{M, N, K, kb_per_split, long(K), colmax};
+  const CUtensorMap tp = make_bytes_map(P, M, 3L * K, M, kBM, kBKi, CU_TENSOR_MAP_SWIZZLE_128B);
+  const CUtensorMap tb = make_bytes_map(bits, rowb, K, rowb, 16, kBKi, CU_TENSOR_MAP_SWIZZLE_NONE);
+  const CUtensorMap tw = make_ws_map(ws, N, M, splits);
+  if (cg == 2) run_i8_dw<2>(tp, tb, tw, p, tm, stream);
+  else run_i8_dw<1>(tp, tb, tw, p, tm, stream);
+}
 
 void launch_quantize_rows(const float* W, int N, int K, long ldw, int8_t* q, long Kp, float* s,
                           cudaStream_t stream) {

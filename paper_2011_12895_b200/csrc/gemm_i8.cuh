@@ -93,6 +93,25 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t a, uint64_t b, 
 // 4 bits (LSB first) -> 4 bytes of 0/1
 __device__ __forceinline__ uint32_t spread4(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
 
+// One 16-byte bit row (128 elements) -> row r of the x tile (0/1) and of the x<<7 tile
+// (0/128), 128 bytes each, 16-B chunk c stored at chunk c ^ (r & 7) (the 128-B swizzle;
+// the same byte layout serves a K-major row and an MN-major row).
+__device__ __forceinline__ void expand_bit_row(const uint8_t* src, uint8_t* x_tile,
+                                               uint8_t* x7_tile, int r) {
+  const uint4 b = *reinterpret_cast<const uint4*>(src);
+  const uint32_t bw[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    // chunk c: elements 16c..16c+15 = bytes 2c, 2c+1 of the bit row
+    const uint32_t two = (bw[c >> 1] >> ((c & 1) * 16)) & 0xFFFFu;
+    const uint4 x = make_uint4(spread4(two & 15u), spread4((two >> 4) & 15u),
+                               spread4((two >> 8) & 15u), spread4(two >> 12));
+    const uint32_t off = uint32_t(r * 128 + ((c ^ (r & 7)) << 4));
+    *reinterpret_cast<uint4*>(x_tile + off) = x;
+    *reinterpret_cast<uint4*>(x7_tile + off) = make_uint4(x.x << 7, x.y << 7, x.z << 7, x.w << 7);
+  }
+}
+
 template <int BN, int CG>
 __global__ void __launch_bounds__(kThreadsI8, 1)
     gemm_i8_bits_fwd_kernel(const __grid_constant__ CUtensorMap tmBits,
@@ -236,19 +255,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
       for (int kb = 0; kb < kb_total; ++kb) {
         mbar_wait(bar_xfull + 8 * stage, phase);
         uint8_t* st = smem + stage * S::kStage;
-        const uint4 b = *reinterpret_cast<const uint4*>(st + kOffBits + r * 16);
-        const uint32_t bw[4] = {b.x, b.y, b.z, b.w};
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          // chunk c: elements 16c..16c+15 = bytes 2c, 2c+1 of the bit row
-          const uint32_t two = (bw[c >> 1] >> ((c & 1) * 16)) & 0xFFFFu;
-          const uint4 x = make_uint4(spread4(two & 15u), spread4((two >> 4) & 15u),
-                                     spread4((two >> 8) & 15u), spread4(two >> 12));
-          const uint32_t off = uint32_t(r * 128 + ((c ^ (r & 7)) << 4));
-          *reinterpret_cast<uint4*>(st + off) = x;
-          *reinterpret_cast<uint4*>(st + kOffX128 + off) =
-              make_uint4(x.x << 7, x.y << 7, x.z << 7, x.w << 7);
-        }
+        expand_bit_row(st + kOffBits + r * 16, st, st + kOffX128, r);
         fence_async_smem();
         __syncwarp();
         if (lane == 0) {
@@ -339,6 +346,285 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
 }
 
 // ---------------------------------------------------------------------------
+// Weight gradient of a binary-plane layer:  dW[m][n] = sum_f dZ[f][m] X[f][n]
+//   A = dZ as fixed-point int8 pieces, MN-major [3][F][M] (quantize_cols_kernel, one
+//       scale per (K split, m): s = colmax / 127, colmax from the dX epilogue);
+//   B = X bit rows [F][pitch] (MN-major after expansion);  K = frames, split-K.
+// Each CTA holds 128 rows of M (a pair: 256) and 128 columns of N; per split the int32
+// accumulators are exact (|acc| < 2^31 for <= 131072 frames per split) and the epilogue
+// writes s_m (acc_a / 2^7 + acc_b / 2^14) into the fp32 split-K workspace.
+template <int CG>
+struct SmemI8Dw {
+  static constexpr int kPiece = kBM * kBKi;     // 16 KB: 128 k rows x 128 m bytes
+  static constexpr int kX = kBKi * 128;         // 16 KB: 128 k rows x 128 n
+  static constexpr int kBits = kBKi * 16;       // 2 KB
+  static constexpr int kStage = 3 * kPiece + 2 * kX + kBits;
+  static constexpr int kEpi = kEpiWarps * 4096;
+  static constexpr int kStagesRaw = (225 * 1024 - kEpi - 2048) / kStage;
+  static constexpr int kStages = kStagesRaw > 4 ? 4 : kStagesRaw;
+  static constexpr int kBarOff = kStages * kStage;
+  static constexpr int kNumBars = 4 * kStages + 2;  // full, xfull, conv, empty; tfull, tempty
+  static constexpr int kEpiOff = (kBarOff + kNumBars * 8 + 16 + 1023) / 1024 * 1024;
+  static constexpr int kBytes = kEpiOff + kEpi + 1024;
+  static constexpr int BN = 128 * CG;
+  static constexpr int kTmemCols = 2 * BN;  // 2 accumulators, single-buffered
+  static_assert(kStage % 1024 == 0, "stages must keep the 1 KB swizzle alignment");
+  static_assert(kStages >= 2, "pipeline needs two stages");
+};
+
+struct I8DwParams {
+  int M, N, K;          // M = out features (dZ columns), N = in features (planes), K = frames
+  int kb_per_split;     // 128-frame k-blocks per split (colmax group = kb_per_split * 128 rows)
+  long f_rows;          // rows per piece in the stacked [3][f_rows][M] piece array
+  const unsigned* colmax;  // [splits][M] float bits
+};
+
+template <int CG>
+__device__ __forceinline__ constexpr uint32_t make_idesc_i8_dw() {
+  return (2u << 4)       // D: s32
+         | (1u << 7)     // A: signed 8-bit (dZ pieces)
+         | (0u << 10)    // B: unsigned 8-bit (planes)
+         | (1u << 15)    // A MN-major
+         | (1u << 16)    // B MN-major
+         | (uint32_t((128 * CG) >> 3) << 17)  // N = 128 * CG
+         | (uint32_t((kBM * CG) >> 4) << 24);
+}
+
+template <int CG>
+__global__ void __launch_bounds__(kThreadsI8, 1)
+    gemm_i8_bits_dw_kernel(const __grid_constant__ CUtensorMap tmP,
+                           const __grid_constant__ CUtensorMap tmBits,
+                           const __grid_constant__ CUtensorMap tmWs, const I8DwParams p,
+                           const TileMap tm) {
+  using S = SmemI8Dw<CG>;
+  constexpr int BN = S::BN;
+  const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
+  const int cl_id = CG == 2 ? int(blockIdx.x >> 1) : int(blockIdx.x);
+  const int n_cl = CG == 2 ? int(gridDim.x >> 1) : int(gridDim.x);
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t bar_full = sbase + S::kBarOff;
+  const uint32_t bar_xfull = bar_full + 8 * S::kStages;
+  const uint32_t bar_conv = bar_xfull + 8 * S::kStages;
+  const uint32_t bar_empty = bar_conv + 8 * S::kStages;
+  const uint32_t bar_tfull = bar_empty + 8 * S::kStages;
+  const uint32_t bar_tempty = bar_tfull + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + S::kBarOff + S::kNumBars * 8);
+  constexpr int kOffX = 3 * S::kPiece, kOffX128 = kOffX + S::kX, kOffBits = kOffX + 2 * S::kX;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int num_tiles = tm.m_tiles * tm.n_tiles * tm.splits;
+  const int kb_total = (p.K + kBKi - 1) / kBKi;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmP);
+    prefetch_tmap(&tmBits);
+    for (int s = 0; s < S::kStages; ++s) {
+      mbar_init(bar_full + 8 * s, 1);
+      mbar_init(bar_xfull + 8 * s, 1);
+      mbar_init(bar_conv + 8 * s, kConvWarps * CG);
+      mbar_init(bar_empty + 8 * s, 1);
+    }
+    mbar_init(bar_tfull, 1);
+    mbar_init(bar_tempty, kEpiWarps * CG);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    if (CG == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "n"(S::kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "n"(S::kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+  }
+  tc_fence_before();
+  if (CG == 2) cluster_sync_all();
+  else __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  auto decode = [&](int t, int& mt, int& nt, int& sp) {
+    nt = t % tm.n_tiles;
+    const int r = t / tm.n_tiles;
+    mt = r % tm.m_tiles;
+    sp = r / tm.m_tiles;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cl_id; t < num_tiles; t += n_cl) {
+        int mt, nt, sp;
+        decode(t, mt, nt, sp);
+        const int m0 = mt * kBM * CG + int(rank) * kBM;
+        const int n0 = nt * BN + int(rank) * 128;
+        const int kb0 = sp * p.kb_per_split, kb1 = min(kb_total, kb0 + p.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(bar_empty + 8 * stage, phase ^ 1);
+          const uint32_t st = sbase + stage * S::kStage;
+          mbar_expect_tx(bar_xfull + 8 * stage, S::kBits);
+          tma_load_2d(st + kOffBits, &tmBits, n0 / 8, kb * kBKi, bar_xfull + 8 * stage);
+          const uint32_t full = CG == 2 ? map_rank0(bar_full + 8 * stage) : bar_full + 8 * stage;
+          if (rank == 0) mbar_expect_tx(bar_full + 8 * stage, 3 * S::kPiece * CG);
+#pragma unroll
+          for (int pc = 0; pc < 3; ++pc) {
+            const int row = int(pc * p.f_rows) + kb * kBKi;
+            if (CG == 2) tma_load_2d_pair(st + pc * S::kPiece, &tmP, m0, row, full);
+            else tma_load_2d(st + pc * S::kPiece, &tmP, m0, row, full);
+          }
+          if (++stage == S::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = make_idesc_i8_dw<CG>();
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = cl_id; t < num_tiles; t += n_cl, ++it) {
+        int mt, nt, sp;
+        decode(t, mt, nt, sp);
+        const int kb0 = sp * p.kb_per_split, kb1 = min(kb_total, kb0 + p.kb_per_split);
+        mbar_wait(bar_tempty, (it & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t tacc_a = tmem_base, tacc_b = tmem_base + uint32_t(BN);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(bar_full + 8 * stage, phase);
+          mbar_wait(bar_conv + 8 * stage, phase);
+          tc_fence_after();
+          const uint32_t st = sbase + stage * S::kStage;
+#pragma unroll
+          for (int k = 0; k < kBKi / 32; ++k) {
+            // MN-major int8 SW128 (layout type 2 as K-major; the major-ness is in the
+            // instruction descriptor): 32 k rows of 128 B per K=32 step, SBO = 1 KB per
+            // 8 rows; one 128-element MN chunk per CTA, so LBO is never used
+            const uint32_t ko = uint32_t(k) * 4096u;
+            const uint64_t dp0 = make_sdesc<false>(st + ko, 16384, 1024);
+            const uint64_t dp1 = make_sdesc<false>(st + S::kPiece + ko, 16384, 1024);
+            const uint64_t dp2 = make_sdesc<false>(st + 2 * S::kPiece + ko, 16384, 1024);
+            const uint64_t dx = make_sdesc<false>(st + kOffX + ko, 16384, 1024);
+            const uint64_t dx7 = make_sdesc<false>(st + kOffX128 + ko, 16384, 1024);
+            const uint32_t acc = (kb > kb0 || k > 0) ? 1u : 0u;
+            mma_i8<CG>(tacc_a, dp0, dx7, idesc, acc);
+            mma_i8<CG>(tacc_a, dp1, dx, idesc, 1u);
+            mma_i8<CG>(tacc_b, dp2, dx, idesc, acc);
+          }
+          if (CG == 2) mma_commit_pair(bar_empty + 8 * stage);
+          else mma_commit(bar_empty + 8 * stage);
+          if (++stage == S::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (CG == 2) mma_commit_pair(bar_tfull);
+        else mma_commit(bar_tfull);
+      }
+    }
+  } else if (warp >= 2 + kEpiWarps) {
+    const int r = threadIdx.x - (2 + kEpiWarps) * 32;  // k row 0..127
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = cl_id; t < num_tiles; t += n_cl) {
+      int mt, nt, sp;
+      decode(t, mt, nt, sp);
+      const int kb0 = sp * p.kb_per_split, kb1 = min(kb_total, kb0 + p.kb_per_split);
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(bar_xfull + 8 * stage, phase);
+        uint8_t* st = smem + stage * S::kStage;
+        expand_bit_row(st + kOffBits + r * 16, st + kOffX, st + kOffX128, r);
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          if (CG == 2) mbar_arrive_cluster(map_rank0(bar_conv + 8 * stage));
+          else mbar_arrive(bar_conv + 8 * stage);
+        }
+        if (++stage == S::kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const int ew = warp - 2;
+    const uint32_t blk = sbase + S::kEpiOff + uint32_t(ew * 4096);
+    uint8_t* blk_ptr = smem + S::kEpiOff + ew * 4096;
+    int it = 0;
+    for (int t = cl_id; t < num_tiles; t += n_cl, ++it) {
+      int mt, nt, sp;
+      decode(t, mt, nt, sp);
+      const int m0 = mt * kBM * CG + int(rank) * kBM, n0 = nt * BN;
+      const int rbase = m0 + q * 32;
+      const int m = rbase + lane;
+      float sc = 0.f;
+      if (m < p.M) {
+        const float mx = __uint_as_float(p.colmax[long(sp) * p.M + m]);
+        sc = mx > 0.f ? mx / 127.f : 1.f;
+      }
+      const float sa = sc * 0.0078125f, sb = sc * 6.103515625e-05f;
+      mbar_wait(bar_tfull, it & 1);
+      tc_fence_after();
+      const uint32_t ta = tmem_base + (uint32_t(q * 32) << 16);
+      const uint32_t tb = ta + uint32_t(BN);
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t ra[32], rb[32];
+        tmem_ld32(ta + uint32_t(c), ra);
+        tmem_ld32(tb + uint32_t(c), rb);
+        float o[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) o[j] = fmaf(float(int(ra[j])), sa, float(int(rb[j])) * sb);
+        if (lane == 0) bulk_wait_read();
+        __syncwarp();
+#pragma unroll
+        for (int j4 = 0; j4 < 8; ++j4)
+          *reinterpret_cast<float4*>(blk_ptr + swz(lane, j4)) =
+              make_float4(o[4 * j4], o[4 * j4 + 1], o[4 * j4 + 2], o[4 * j4 + 3]);
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_3d(&tmWs, n0 + c, rbase, sp, blk);
+          bulk_commit();
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (CG == 2) mbar_arrive_cluster(map_rank0(bar_tempty));
+        else mbar_arrive(bar_tempty);
+      }
+    }
+    if (lane == 0) bulk_wait_all();
+  }
+
+  tc_fence_before();
+  if (CG == 2) cluster_sync_all();
+  else __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    if (CG == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "n"(S::kTmemCols));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "n"(S::kTmemCols));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Host side
 
 // W [N][K] (row pitch ldw floats) -> pieces q [3][N][Kp] (int8, zero past K) and per-row
@@ -352,5 +638,16 @@ void launch_quantize_rows(const float* W, int N, int K, long ldw, int8_t* q, lon
 LaunchInfo launch_i8_bits_fwd(const uint8_t* bits, long rowb, const int8_t* q, long Kp,
                               const float* scale, const float* bias, int M, int N, int K,
                               float* out, float* out_lo, int ldo, cudaStream_t stream);
+
+// dZ [F][M] (row pitch ldz floats) -> pieces P [3][F][M] int8 with one scale per
+// (split, column): s = colmax[f / rows_per_split][m] / 127.  M % 4 == 0.
+void launch_quantize_cols(const float* Z, long F, int M, long ldz, const unsigned* colmax,
+                          long rows_per_split, int8_t* P, cudaStream_t stream);
+
+// ws[split][m][n] = sum over the split's frames of dZ[f][m] X[f][n]  (X bit rows, pitch
+// `rowb` bytes; dZ as launch_quantize_cols pieces).  M % 128 == 0, N % 128 == 0 not
+// required (TMA clips), rows_per_split = kb_per_split * 128 and <= 131072.
+void launch_i8_bits_dw(const int8_t* P, const uint8_t* bits, long rowb, const unsigned* colmax,
+                       int M, int N, int K, int kb_per_split, float* ws, cudaStream_t stream);
 
 }  // namespace tlg::gemm

@@ -54,6 +54,12 @@ struct Params {
   long ws_split_stride;
   float* colsum;  // kEpiBwdTanh: optional column sums of the output, one row per CTA:
                   // colsum[cta][n] (N <= kColMax); the caller sums the rows in order
+  // kEpiBwdTanh: optional column max |out| per group of colmax_rows rows (rows of a
+  // group never straddle a 256-row tile): colmax[m / colmax_rows][n], as float bits
+  // (atomicMax on non-negative floats); zeroed by the caller.  Feeds the fixed-point
+  // scales of the int8 weight-gradient GEMM (gemm_i8.cuh).
+  unsigned* colmax;
+  int colmax_rows;
   // kEpiFwdTanh on the last trunk layer: fused policy/value head partial dot products
   //   head_part[n_tile][m][k] = sum_{n in tile} Whead[k][n] * out[m][n], k < head_k
   const float* head_w;   // W_pi [head_k - 1][N] row-major
@@ -802,7 +808,7 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
         for (int j4 = 0; j4 < 8; ++j4) {
           *reinterpret_cast<float4*>(blk_ptr + swz(lane, j4)) =
               make_float4(o[4 * j4], o[4 * j4 + 1], o[4 * j4 + 2], o[4 * j4 + 3]);
-          if (EPI != kEpiStore && !S::kShareLo)
+          if (EPI != kEpiStore && !S::kShareLo && p.out_lo != nullptr)
             *reinterpret_cast<float4*>(blk_ptr + 4096 + swz(lane, j4)) =
                 make_float4(o[4 * j4] - tf32_hi(o[4 * j4]), o[4 * j4 + 1] - tf32_hi(o[4 * j4 + 1]),
                             o[4 * j4 + 2] - tf32_hi(o[4 * j4 + 2]),
@@ -815,19 +821,24 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
             tma_store_3d(&tmOut, nb, rbase, sp, st_out);
           } else {
             tma_store_2d(&tmOut, nb, rbase, st_out);
-            if (!S::kShareLo) tma_store_2d(&tmOutLo, nb, rbase, st_lo);
+            if (!S::kShareLo && p.out_lo != nullptr) tma_store_2d(&tmOutLo, nb, rbase, st_lo);
           }
           bulk_commit();
         }
         if (EPI == kEpiBwdTanh) {
           // column sums of this warp's 32 rows (rows past M are exact zeros)
-          float csum = 0.f;
+          float csum = 0.f, cmax = 0.f;
 #pragma unroll 8
-          for (int rr = 0; rr < 32; ++rr)
-            csum += *reinterpret_cast<const float*>(blk_ptr + swz(rr, lane >> 2) + (lane & 3) * 4);
+          for (int rr = 0; rr < 32; ++rr) {
+            const float v = *reinterpret_cast<const float*>(blk_ptr + swz(rr, lane >> 2) + (lane & 3) * 4);
+            csum += v;
+            cmax = fmaxf(cmax, fabsf(v));
+          }
           cpart[c + lane] = csum;
+          if (p.colmax != nullptr && nb + lane < p.N)
+            atomicMax(p.colmax + long(rbase / p.colmax_rows) * p.N + nb + lane, __float_as_uint(cmax));
         }
-        if (EPI != kEpiStore && S::kShareLo) {
+        if (EPI != kEpiStore && S::kShareLo && p.out_lo != nullptr) {
           // residual plane through the same block once the full-value store has read it
           if (lane == 0) bulk_wait_read();
           __syncwarp();

@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -165,6 +166,11 @@ struct tlg_learner {
   float* wq_scale = nullptr;
   long wq_kp = 0;
   const bool i8_disabled = std::getenv("TLG_NO_I8") != nullptr;
+  const bool i8_dw_disabled = std::getenv("TLG_NO_I8_DW") != nullptr;
+  // layer-1 dW on the int8 tensor cores: dZ_1 as per-split fixed-point pieces
+  int8_t* dzq = nullptr;
+  unsigned* colmax = nullptr;
+  static constexpr int kMaxI8Splits = 148;
   bool wq_fresh = false;
   int32_t* action;
   float *reward, *blogp, *value;
@@ -227,6 +233,10 @@ struct tlg_learner {
       wq_kp = (D + 15) / 16 * 16;
       wq = mem.add<int8_t>(3 * long(net.dims[1]) * wq_kp);
       wq_scale = mem.add<float>(net.dims[1]);
+      if (net.dims[1] % 16 == 0) {
+        dzq = mem.add<int8_t>(3 * F_max * long(net.dims[1]));
+        colmax = mem.add<unsigned>(long(kMaxI8Splits) * net.dims[1]);
+      }
     }
     action = mem.add<int32_t>(F_max);
     reward = mem.add<float>(F_max);
@@ -263,6 +273,7 @@ struct tlg_learner {
       ws_elems = std::max(ws_elems, long(sp) * out * in);
       max_cols = std::max<long>(max_cols, out);
     }
+    if (dzq) ws_elems = std::max(ws_elems, long(kMaxI8Splits) * net.dims[1] * net.D);
     ws = ws_elems ? mem.add<float>(ws_elems) : nullptr;
     col_partial = mem.add<float>(((F_max + tlg::kLossFrames - 1) / tlg::kLossFrames + 1) *
                                  std::max<long>(max_cols, net.head.H));
@@ -312,6 +323,22 @@ struct tlg_learner {
   // binary planes take the exact int8 tensor-core path for layer 1 (L >= 2: the fused
   // heads stay on the last trunk layer's tf32 epilogue)
   bool i8_layer1() const { return wq != nullptr && !i8_disabled; }
+  bool i8_dw1() const { return i8_layer1() && dzq != nullptr && !i8_dw_disabled; }
+
+  // split-K plan of the int8 layer-1 dW: as many splits as fill one wave of CTA pairs,
+  // an even number of 128-frame k-blocks per split (the dX epilogue's 256-row tiles
+  // never straddle a split), <= 1024 k-blocks per split (exact int32 accumulators)
+  void i8_dw_plan(long F, int& splits, int& kb_per_split) const {
+    const int kb_total = int((F + 127) / 128);
+    const int cg = net.dims[1] >= 256 ? 2 : 1;
+    const int tiles = ((int(net.dims[1]) + 128 * cg - 1) / (128 * cg)) *
+                      ((int(net.D) + 128 * cg - 1) / (128 * cg));
+    const int units = cg == 2 ? tlg::gemm::num_sms() / 2 : tlg::gemm::num_sms();
+    splits = std::max(1, std::min(units / std::max(1, tiles), kMaxI8Splits));
+    kb_per_split = (kb_total + splits - 1) / splits;
+    kb_per_split = std::max(2, std::min(1024, (kb_per_split + 1) / 2 * 2));
+    splits = (kb_total + kb_per_split - 1) / kb_per_split;
+  }
 
   void stage(const tlg_segment_batch& b, int on_device, tlg::BatchDev& bd, const float** obs_f32,
              bool& obs_exact, bool internal = false) {
@@ -339,8 +366,9 @@ struct tlg_learner {
       }
       // one pass: rows re-pitched to 16 B for the int8 GEMM's TMA (pad bytes zero) and
       // expanded to the uint8 planes the layer-1 dW reads
-      tlg::launch_unpack_bits(bits, rowb, F, D, obs_u8, i8_layer1() ? obs_bits : nullptr,
-                              bits_pitch, stream);
+      // (the uint8 planes are only needed by the tf32 layer-1 dW)
+      tlg::launch_unpack_bits(bits, rowb, F, D, i8_dw1() ? nullptr : obs_u8,
+                              i8_layer1() ? obs_bits : nullptr, bits_pitch, stream);
       if (i8_layer1()) x0_bits = obs_bits;
       ++launches;
       tlg_segment_batch u = b;
@@ -525,6 +553,25 @@ struct tlg_learner {
       const int in = int(net.dims[l]), outw = int(net.dims[l + 1]);
       const float* xin = l == 0 ? x0 : act[l - 1];
       const float* xin_lo = l == 0 ? x0_lo : act_lo[l - 1];
+      if (l == 0 && sg.x0_bits != nullptr && i8_dw1()) {
+        // dW_1 = dZ_1^T . X on the int8 tensor cores (exact int32 per split)
+        int sp_i8, kbps;
+        i8_dw_plan(F, sp_i8, kbps);
+        tlg::gemm::launch_quantize_cols(dz[0], F, outw, outw, colmax, long(kbps) * 128, dzq,
+                                        stream);
+        if (shard == 0) kmark(1, l, 0);
+        tlg::gemm::launch_i8_bits_dw(dzq, sg.x0_bits, bits_pitch, colmax, outw, in, int(F), kbps,
+                                     ws, stream);
+        if (shard == 0) kmark(1, l, 1);
+        tlg::launch_dw_reduce(ws, sp_i8, long(outw) * in, gtarget + net.w_off[0], stream);
+        if (net.L > 1) {
+          tlg::launch_rows_reduce(col_partial, colsum_rows, outw, outw, gtarget + net.b_off[0],
+                                  stream);
+          ++launches;
+        }
+        launches += 3;
+        continue;
+      }
       // dW_l = dZ_l^T . X_{l-1}   (K = frames, split-K partials reduced in fixed order)
       int sp = tlg::gemm::pick_splits(outw, in, int(F), kMaxSplits);
       while (long(sp) * outw * in > ws_elems && sp > 1) --sp;
@@ -560,6 +607,15 @@ struct tlg_learner {
         p2.act_hi = act[l - 1];
         p2.ld_act = in;
         p2.colsum = col_partial;
+        if (l == 1 && sg.x0_bits != nullptr && i8_dw1()) {
+          // dZ_1 feeds only the int8 dW: column maxima per split instead of a residual plane
+          int sp_i8, kbps;
+          i8_dw_plan(F, sp_i8, kbps);
+          TLG_CUDA(cudaMemsetAsync(colmax, 0, size_t(sp_i8) * in * sizeof(unsigned), stream));
+          p2.colmax = colmax;
+          p2.colmax_rows = kbps * 128;
+          p2.out_lo = nullptr;
+        }
         if (shard == 0) kmark(2, l, 0);
         colsum_rows = tlg::gemm::launch(A2, B2, int(F), in, outw, tlg::gemm::kEpiBwdTanh, p2, 1,
                                         stream).ctas;
@@ -688,6 +744,7 @@ struct tlg_learner {
     TLG_CUDA(cudaStreamWaitEvent(stream, sl.ready, 0));
     step(&sl.dev, 1, /*on_device=*/1, out, sl.consumed);
   }
+
 
   // Everything after staging: per-shard compute, allreduce, optimizer, stats D2H.
   void enqueue_device_step(const Staged* staged, int n, const tlg_segment_batch* bs = nullptr,

@@ -271,6 +271,84 @@ void check_i8(const char* name, int M, int N, int K) {
   cudaFree(B.lo); cudaFree(bias.x); cudaFree(bias.hi); cudaFree(bias.lo);
 }
 
+// dW = dZ^T X with X bit-packed binary planes and dZ as per-split fixed-point pieces.
+void check_i8_dw(const char* name, int M, int N, int K, int kb_per_split) {
+  std::mt19937 rng(M * 5 + N * 11 + K);
+  Buf Z, X;
+  Z.init(long(K) * M, rng);        // dZ stored [K=frames][M]
+  X.init(long(K) * N, rng, true);  // planes stored [K][N]
+  double *ref, *refabs;
+  TLG_CUDA(cudaMalloc(&ref, long(M) * N * 8));
+  TLG_CUDA(cudaMalloc(&refabs, long(M) * N * 8));
+  ref_gemm<<<dim3((M + 127) / 128, N), 128>>>(Z.x, M, true, X.x, N, true, M, N, K, ref, refabs);
+  const long rowb = ((N + 7) / 8 + 15) / 16 * 16;
+  const int rows_split = kb_per_split * 128;
+  const int splits = (K + rows_split - 1) / rows_split;
+  std::vector<float> hz(long(K) * M), hx(long(K) * N);
+  TLG_CUDA(cudaMemcpy(hz.data(), Z.x, hz.size() * 4, cudaMemcpyDeviceToHost));
+  TLG_CUDA(cudaMemcpy(hx.data(), X.x, hx.size() * 4, cudaMemcpyDeviceToHost));
+  std::vector<uint8_t> hb(long(K) * rowb, 0);
+  for (long f = 0; f < K; ++f)
+    for (long n = 0; n < N; ++n)
+      if (hx[f * N + n] != 0.f) hb[f * rowb + n / 8] |= uint8_t(1u << (n % 8));
+  std::vector<float> cm(long(splits) * M, 0.f);
+  for (long f = 0; f < K; ++f)
+    for (int m = 0; m < M; ++m) {
+      float& c = cm[(f / rows_split) * M + m];
+      c = std::max(c, std::fabs(hz[f * M + m]));
+    }
+  uint8_t* bits;
+  int8_t* P;
+  unsigned* colmax;
+  float* ws;
+  TLG_CUDA(cudaMalloc(&bits, hb.size()));
+  TLG_CUDA(cudaMemcpy(bits, hb.data(), hb.size(), cudaMemcpyHostToDevice));
+  TLG_CUDA(cudaMalloc(&colmax, cm.size() * 4));
+  TLG_CUDA(cudaMemcpy(colmax, cm.data(), cm.size() * 4, cudaMemcpyHostToDevice));
+  TLG_CUDA(cudaMalloc(&P, 3L * K * M));
+  TLG_CUDA(cudaMalloc(&ws, long(splits) * M * N * 4));
+  gemm::launch_quantize_cols(Z.x, K, M, M, colmax, rows_split, P, 0);
+  gemm::launch_i8_bits_dw(P, bits, rowb, colmax, M, N, K, kb_per_split, ws, 0);
+  TLG_CUDA(cudaDeviceSynchronize());
+  cudaEvent_t e0, e1, e2;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventCreate(&e2);
+  const int reps = 5;
+  cudaEventRecord(e0);
+  for (int i = 0; i < reps; ++i) gemm::launch_quantize_cols(Z.x, K, M, M, colmax, rows_split, P, 0);
+  cudaEventRecord(e1);
+  for (int i = 0; i < reps; ++i)
+    gemm::launch_i8_bits_dw(P, bits, rowb, colmax, M, N, K, kb_per_split, ws, 0);
+  cudaEventRecord(e2);
+  TLG_CUDA(cudaDeviceSynchronize());
+  float msq = 0, ms = 0;
+  cudaEventElapsedTime(&msq, e0, e1);
+  cudaEventElapsedTime(&ms, e1, e2);
+  msq /= reps;
+  ms /= reps;
+  std::vector<double> hr(long(M) * N), ha(long(M) * N);
+  std::vector<float> hw(long(splits) * M * N);
+  TLG_CUDA(cudaMemcpy(hr.data(), ref, hr.size() * 8, cudaMemcpyDeviceToHost));
+  TLG_CUDA(cudaMemcpy(ha.data(), refabs, ha.size() * 8, cudaMemcpyDeviceToHost));
+  TLG_CUDA(cudaMemcpy(hw.data(), ws, hw.size() * 4, cudaMemcpyDeviceToHost));
+  double worst = 0;
+  long bad = 0;
+  for (long i = 0; i < long(M) * N; ++i) {
+    double got = 0;
+    for (int sp = 0; sp < splits; ++sp) got += hw[long(sp) * M * N + i];
+    const double err = std::fabs(got - hr[i]) / (ha[i] + 1e-30);
+    if (!(err <= 2e-6)) ++bad;
+    if (!(err <= worst)) worst = std::isfinite(err) ? std::max(worst, err) : 1e30;
+  }
+  const double tflops = 2.0 * M * N * K / (ms * 1e-3) / 1e12;
+  printf("%-34s M=%6d N=%5d K=%6d split=%d : worst rel %.3e bad %ld  %.3f ms %.1f TF/s (quantize %.3f ms)  %s\n",
+         name, M, N, K, splits, worst, bad, ms, tflops, msq, bad ? "FAIL" : "ok");
+  if (bad) ++failures;
+  cudaFree(ref); cudaFree(refabs); cudaFree(bits); cudaFree(P); cudaFree(colmax); cudaFree(ws);
+  cudaFree(Z.x); cudaFree(Z.hi); cudaFree(Z.lo); cudaFree(X.x); cudaFree(X.hi); cudaFree(X.lo);
+}
+
 int main(int argc, char** argv) {
   try {
     using namespace gemm;
@@ -299,8 +377,12 @@ int main(int argc, char** argv) {
     check_i8("I8 bits fwd", 300, 256, 200);
     check_i8("I8 bits fwd N=100 K=1936", 700, 100, 1936);
     check_i8("I8 bits fwd pair", 4096, 256, 1936);
+    check_i8_dw("I8 bits dW", 128, 200, 1000, 2);
+    check_i8_dw("I8 bits dW pair", 256, 1936, 4096, 8);
+    check_i8_dw("I8 bits dW ragged", 256, 300, 1300, 4);
     if (argc > 1) {
       check_i8("perf I8 bits fwd C3 L1", 131072, 256, 1936);
+      check_i8_dw("perf I8 bits dW C3 L1", 256, 1936, 131072, 114);
       g_u8 = 1;
       check("perf U8 fwd C3 L1", 131072, 256, 1936, false, false, true, kEpiFwdTanh, 1);
       g_u8 = 2;

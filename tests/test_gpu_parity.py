@@ -401,9 +401,11 @@ def test_bit_packed_and_staged_inputs_match(tlg, oracle, D, hidden):
                for k in range(3)]
     res = []
     for mode in ("u8", "bits", "staged"):
+        # SGD: parameter differences stay proportional to gradient differences (Adam's
+        # normalised first steps turn a sign flip of a ~0 gradient into a full lr move)
         lrn = tlg.Learner("mlp", D, A, hidden, max_segments=S, unroll_len=T, obs_u8=True,
-                          optimizer="adam")
-        lrn.set_hyper(learning_rate=1e-3, batch_size=S, unroll_len=T)
+                          optimizer="sgd")
+        lrn.set_hyper(learning_rate=0.05, batch_size=S, unroll_len=T)
         lrn.set_params(p)
         views = []
         for b in batches:
@@ -427,7 +429,7 @@ def test_bit_packed_and_staged_inputs_match(tlg, oracle, D, hidden):
     if len(hidden) == 1:
         assert np.array_equal(res[0], res[1])
     else:
-        assert close(res[0], res[1], 1e-4), worst(res[0], res[1])
+        assert close(res[0], res[1], 1e-5), worst(res[0], res[1])
 
 
 @pytest.mark.parametrize("optimizer", ["sgd", "adam"])
