@@ -491,7 +491,8 @@ struct tlg_learner {
       Operand B{params + net.w_off[l], params_lo + net.w_off[l], in, false};
       tlg::gemm::Params p{};
       p.out_hi = act[l];
-      p.out_lo = act_lo[l];
+      // the top layer's residual plane has no reader (heads and loss read the full plane)
+      p.out_lo = l + 1 == net.L ? nullptr : act_lo[l];
       p.ldo = outw;
       p.bias = params + net.b_off[l];
       const bool fuse_head = l + 1 == net.L && fused_head();
@@ -1206,7 +1207,7 @@ int tlg_policy_forward(tlg_policy* p, const float* obs, size_t n, float* logits,
       Operand Bop{p->params + p->net.w_off[l], p->params_lo + p->net.w_off[l], in, false};
       tlg::gemm::Params gp{};
       gp.out_hi = p->act[l];
-      gp.out_lo = p->act_lo[l];
+      gp.out_lo = l + 1 == p->net.L ? nullptr : p->act_lo[l];
       gp.ldo = outw;
       gp.bias = p->params + p->net.b_off[l];
       const bool fuse = l + 1 == p->net.L && p->net.A + 1 <= 8;

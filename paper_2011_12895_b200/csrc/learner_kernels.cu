@@ -24,6 +24,24 @@ __global__ void expand_u8_kernel(const uchar4* __restrict__ in, float4* __restri
   }
 }
 
+// Bit rows of rowb bytes -> rows of `pitch` bytes (zero padded), 8 output bytes per thread.
+__global__ void repitch_bits_kernel(const uint8_t* __restrict__ bits, long rowb, long F,
+                                    uint8_t* __restrict__ out, long pitch) {
+  const long per_row = pitch / 8;
+  for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < F * per_row;
+       i += long(gridDim.x) * blockDim.x) {
+    const long f = i / per_row, j = (i % per_row) * 8;
+    const uint8_t* src = bits + f * rowb + j;
+    uint32_t lo = 0, hi = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (j + q < rowb) lo |= uint32_t(src[q]) << (8 * q);
+      if (j + 4 + q < rowb) hi |= uint32_t(src[4 + q]) << (8 * q);
+    }
+    *reinterpret_cast<uint2*>(out + f * pitch + j) = make_uint2(lo, hi);
+  }
+}
+
 // Bit-packed 0/1 observation planes -> uint8 (one thread per packed byte); optionally
 // also the same bit rows re-pitched to `pitch` bytes (16-B aligned rows for TMA).
 __global__ void unpack_bits_kernel(const uint8_t* __restrict__ bits, long rowb, long F, long D,
@@ -848,6 +866,12 @@ void launch_expand_u8(const uint8_t* in, float* out, long n, cudaStream_t s) {
 void launch_unpack_bits(const uint8_t* bits, long rowb, long F, long D, uint8_t* out,
                         uint8_t* pitched, long pitch,
                         cudaStream_t s) {
+  if (out == nullptr) {  // only the re-pitched bit rows
+    if (pitch % 8 != 0) throw CudaError("bit-row pitch must be a multiple of 8");
+    repitch_bits_kernel<<<grid_for(F * (pitch / 8), 256), 256, 0, s>>>(bits, rowb, F, pitched, pitch);
+    TLG_CHECK_LAUNCH();
+    return;
+  }
   unpack_bits_kernel<<<grid_for(F * rowb, 256), 256, 0, s>>>(bits, rowb, F, D, out, pitched,
                                                              pitch);
   TLG_CHECK_LAUNCH();
@@ -974,7 +998,9 @@ void launch_rows_reduce(const float* partial, int rows, long cols, long stride, 
 }
 
 void launch_dw_reduce(const float* ws, int splits, long n, float* grad, cudaStream_t s) {
-  if (splits > 8) {  // many partial rows: warp-parallel fixed-order reduction
+  // few columns per partial row: warp-parallel fixed-order reduction over the rows;
+  // otherwise one float4 per thread walks the splits in order
+  if (splits > 32 || (splits > 8 && n < 4L * 148 * 256)) {
     launch_rows_reduce(ws, splits, n, n, grad, s);
     return;
   }
