@@ -176,18 +176,22 @@ __global__ void __launch_bounds__(256) quantize_cols_kernel(const float* __restr
       const float4 z = *reinterpret_cast<const float4*>(Z + f * ldz + m);
       const float zv[4] = {z.x, z.y, z.z, z.w};
       uint32_t w0 = 0, w1 = 0, w2 = 0;
+      // round-to-nearest-even via the 1.5 * 2^23 magic constant: the sum's low mantissa
+      // bits are the integer in two's complement (no F2I / FRND on the quarter-rate pipe)
+      constexpr float kMagic = 12582912.f;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         // x = z * (127 / max) rounds once (|x| <= 127 (1 + 2^-23)); the residual steps
         // are exact (Sterbenz, power-of-two scaling)
-        const float x = zv[j] * inv[j];
-        const float r0 = fminf(fmaxf(rintf(x), -lim[j]), lim[j]);
-        const float x1 = (x - r0) * 128.f;
-        const float r1 = rintf(x1);
-        const int a = int(r0), b = int(r1), c = int(rintf((x1 - r1) * 128.f));
-        w0 |= uint32_t(a & 0xFF) << (8 * j);
-        w1 |= uint32_t(b & 0xFF) << (8 * j);
-        w2 |= uint32_t(c & 0xFF) << (8 * j);
+        const float x = fminf(fmaxf(zv[j] * inv[j], -lim[j]), lim[j]);
+        const float m0 = x + kMagic;
+        const float x1 = (x - (m0 - kMagic)) * 128.f;
+        const float m1 = x1 + kMagic;
+        const float x2 = (x1 - (m1 - kMagic)) * 128.f;
+        const float m2 = x2 + kMagic;
+        w0 |= (__float_as_uint(m0) & 0xFFu) << (8 * j);
+        w1 |= (__float_as_uint(m1) & 0xFFu) << (8 * j);
+        w2 |= (__float_as_uint(m2) & 0xFFu) << (8 * j);
       }
       const long o = f * M + m;
       *reinterpret_cast<uint32_t*>(P + o) = w0;

@@ -49,13 +49,18 @@ struct SmemI8 {
   static constexpr int kBits = kBM * kBKi / 8;  // 2 KB packed source rows
   static constexpr int kBN = BN / CG;           // piece rows held by this CTA
   static constexpr int kQ = kBN * kBKi;         // bytes per piece tile
-  static constexpr int kStage = 2 * kX + 3 * kQ + kBits;
+  static constexpr int kStage = 2 * kX + 3 * kQ;
+  // the bit rows stream through their own ring, kRing k-blocks ahead of the stages
+  // (they come from HBM; the pieces are L2-resident)
+  static constexpr int kRing = 8;
   static constexpr int kEpi = kEpiWarps * 2 * 4096;
-  static constexpr int kStagesRaw = (225 * 1024 - kEpi - 2048) / kStage;
+  static constexpr int kStagesRaw = (225 * 1024 - kEpi - kRing * kBits - 2048) / kStage;
   static constexpr int kStages = kStagesRaw > 6 ? 6 : kStagesRaw;
-  static constexpr int kBarOff = kStages * kStage;
-  // full (pieces, leader), xfull (bits, local), conv (leader), empty; tfull[2], tempty[2]
-  static constexpr int kNumBars = 4 * kStages + 4;
+  static constexpr int kRingOff = kStages * kStage;
+  static constexpr int kBarOff = kRingOff + kRing * kBits;
+  // full (pieces, leader), conv (leader), empty per stage; ufull/uempty per ring slot;
+  // tfull[2], tempty[2]
+  static constexpr int kNumBars = 3 * kStages + 2 * kRing + 4;
   static constexpr int kEpiOff = (kBarOff + kNumBars * 8 + 16 + 1023) / 1024 * 1024;
   static constexpr int kBytes = kEpiOff + kEpi + 1024;
   static constexpr int kTmemCols = 4 * BN;  // 2 accumulators x double buffer
@@ -128,13 +133,14 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                                              ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
   const uint32_t bar_full = sbase + S::kBarOff;
-  const uint32_t bar_xfull = bar_full + 8 * S::kStages;
-  const uint32_t bar_conv = bar_xfull + 8 * S::kStages;
+  const uint32_t bar_conv = bar_full + 8 * S::kStages;
   const uint32_t bar_empty = bar_conv + 8 * S::kStages;
-  const uint32_t bar_tfull = bar_empty + 8 * S::kStages;  // [2]
-  const uint32_t bar_tempty = bar_tfull + 16;             // [2]
+  const uint32_t bar_ufull = bar_empty + 8 * S::kStages;   // [ring]
+  const uint32_t bar_uempty = bar_ufull + 8 * S::kRing;    // [ring]
+  const uint32_t bar_tfull = bar_uempty + 8 * S::kRing;    // [2]
+  const uint32_t bar_tempty = bar_tfull + 16;              // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + S::kBarOff + S::kNumBars * 8);
-  constexpr int kOffX128 = S::kX, kOffQ = 2 * S::kX, kOffBits = 2 * S::kX + 3 * S::kQ;
+  constexpr int kOffX128 = S::kX, kOffQ = 2 * S::kX;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -146,9 +152,12 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
     prefetch_tmap(&tmQ);
     for (int s = 0; s < S::kStages; ++s) {
       mbar_init(bar_full + 8 * s, 1);
-      mbar_init(bar_xfull + 8 * s, 1);
       mbar_init(bar_conv + 8 * s, kConvWarps * CG);
       mbar_init(bar_empty + 8 * s, 1);
+    }
+    for (int u = 0; u < S::kRing; ++u) {
+      mbar_init(bar_ufull + 8 * u, 1);
+      mbar_init(bar_uempty + 8 * u, kConvWarps);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(bar_tfull + 8 * a, 1);
@@ -180,15 +189,33 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
       // ===== TMA producer =====
       int stage = 0;
       uint32_t phase = 0;
+      // bit-row ring cursor, running up to kRing k-blocks ahead of the stages
+      int bt = cl_id, bkb = 0, ui = 0;
+      uint32_t uph = 0;
+      long issued = 0, done = 0;
       for (int t = cl_id; t < num_tiles; t += n_cl) {
         const int nt = t % tm.n_tiles, mt = t / tm.n_tiles;
         const int m0 = mt * kBM * CG + int(rank) * kBM;
         const int n0 = nt * BN + int(rank) * S::kBN;
-        for (int kb = 0; kb < kb_total; ++kb) {
+        for (int kb = 0; kb < kb_total; ++kb, ++done) {
+          while (bt < num_tiles && issued < done + S::kRing) {
+            mbar_wait(bar_uempty + 8 * ui, uph ^ 1);
+            mbar_expect_tx(bar_ufull + 8 * ui, S::kBits);
+            const int bm0 = (bt / tm.n_tiles) * kBM * CG + int(rank) * kBM;
+            tma_load_2d(sbase + S::kRingOff + ui * S::kBits, &tmBits, bkb * (kBKi / 8), bm0,
+                        bar_ufull + 8 * ui);
+            ++issued;
+            if (++bkb == kb_total) {
+              bkb = 0;
+              bt += n_cl;
+            }
+            if (++ui == S::kRing) {
+              ui = 0;
+              uph ^= 1;
+            }
+          }
           mbar_wait(bar_empty + 8 * stage, phase ^ 1);
           const uint32_t st = sbase + stage * S::kStage;
-          mbar_expect_tx(bar_xfull + 8 * stage, S::kBits);
-          tma_load_2d(st + kOffBits, &tmBits, kb * (kBKi / 8), m0, bar_xfull + 8 * stage);
           const uint32_t full = CG == 2 ? map_rank0(bar_full + 8 * stage) : bar_full + 8 * stage;
           if (rank == 0) mbar_expect_tx(bar_full + 8 * stage, 3 * S::kQ * CG);
 #pragma unroll
@@ -251,16 +278,24 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
     const int r = threadIdx.x - (2 + kEpiWarps) * 32;  // tile row 0..127
     int stage = 0;
     uint32_t phase = 0;
+    int ui = 0;
+    uint32_t uph = 0;
     for (int t = cl_id; t < num_tiles; t += n_cl) {
       for (int kb = 0; kb < kb_total; ++kb) {
-        mbar_wait(bar_xfull + 8 * stage, phase);
+        mbar_wait(bar_ufull + 8 * ui, uph);           // bit rows arrived
+        mbar_wait(bar_empty + 8 * stage, phase ^ 1);  // the MMA released this stage
         uint8_t* st = smem + stage * S::kStage;
-        expand_bit_row(st + kOffBits + r * 16, st, st + kOffX128, r);
+        expand_bit_row(smem + S::kRingOff + ui * S::kBits + r * 16, st, st + kOffX128, r);
         fence_async_smem();
         __syncwarp();
         if (lane == 0) {
           if (CG == 2) mbar_arrive_cluster(map_rank0(bar_conv + 8 * stage));
           else mbar_arrive(bar_conv + 8 * stage);
+          mbar_arrive(bar_uempty + 8 * ui);
+        }
+        if (++ui == S::kRing) {
+          ui = 0;
+          uph ^= 1;
         }
         if (++stage == S::kStages) {
           stage = 0;
