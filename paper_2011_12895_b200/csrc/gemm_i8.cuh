@@ -129,8 +129,9 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
   const int cl_id = CG == 2 ? int(blockIdx.x >> 1) : int(blockIdx.x);
   const int n_cl = CG == 2 ? int(gridDim.x >> 1) : int(gridDim.x);
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  // 1 KB-aligned base by pointer arithmetic on the __shared__ array (an integer round
+  // trip would turn every staging access into a generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t sbase = smem_u32(smem);
   const uint32_t bar_full = sbase + S::kBarOff;
   const uint32_t bar_conv = bar_full + 8 * S::kStages;
@@ -437,8 +438,9 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
   const int cl_id = CG == 2 ? int(blockIdx.x >> 1) : int(blockIdx.x);
   const int n_cl = CG == 2 ? int(gridDim.x >> 1) : int(gridDim.x);
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  // 1 KB-aligned base by pointer arithmetic on the __shared__ array (an integer round
+  // trip would turn every staging access into a generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t sbase = smem_u32(smem);
   const uint32_t bar_full = sbase + S::kBarOff;
   const uint32_t bar_xfull = bar_full + 8 * S::kStages;
