@@ -312,9 +312,11 @@ def main():
         if bits:
             hb.obs = tlg.synth.pack_bits(h.obs)
         pv = tlg.SegmentBatchView(hb, bits=bits, obs_dim=D)
+        pv.pinned = []  # the pinned tensors must outlive the numpy views handed to the C ABI
         for k, a in pv.arrs.items():
             t = torch.empty(a.shape, dtype=getattr(torch, str(a.dtype)), pin_memory=True)
             t.numpy()[...] = a
+            pv.pinned.append(t)
             pv.arrs[k] = t.numpy()
         pv.c = tlg._capi.SegmentBatchC(
             h.n_segments, h.unroll_len, D, 2 if bits else (1 if obs_u8 else 0),
@@ -324,6 +326,10 @@ def main():
         return pv
 
     def e2e_run(views):
+        if os.environ.get("TLG_BENCH_DEBUG"):
+            for v in views:
+                print("DBG", {k: (a.dtype, a.shape, float(a.min()), float(a.max())) for k, a in v.arrs.items()},
+                      v.c.n_segments, v.c.unroll_len, v.c.obs_dim, v.c.obs_dtype, file=sys.stderr)
         nsteps = max(3, args.steps // 2)
         lrn.stage(views[0])
         lrn.train_staged()  # warm the staged path
@@ -430,7 +436,8 @@ def main():
         e1.record(pstream)
         torch.cuda.synchronize()
         ims = max_over_ranks(e0.elapsed_time(e1) / reps)
-        obs_pin = torch.from_numpy(obs).pin_memory().numpy()
+        obs_pin_t = torch.from_numpy(obs).pin_memory()  # kept alive while the view is used
+        obs_pin = obs_pin_t.numpy()
         pol.forward(obs_pin)
         barrier()
         t0 = time.perf_counter()

@@ -275,8 +275,11 @@ struct tlg_learner {
     }
     if (dzq) ws_elems = std::max(ws_elems, long(kMaxI8Splits) * net.dims[1] * net.D);
     ws = ws_elems ? mem.add<float>(ws_elems) : nullptr;
-    col_partial = mem.add<float>(((F_max + tlg::kLossFrames - 1) / tlg::kLossFrames + 1) *
-                                 std::max<long>(max_cols, net.head.H));
+    // rows: the loss kernel's blocks, or one per persistent GEMM CTA (the dX epilogue's
+    // fused column sums), whichever is more
+    const long cp_rows = std::max<long>((F_max + tlg::kLossFrames - 1) / tlg::kLossFrames + 1,
+                                        tlg::gemm::num_sms());
+    col_partial = mem.add<float>(cp_rows * std::max<long>(max_cols, net.head.H));
     TLG_CUDA(cudaMallocHost(&h_stats, kMaxLocalShards * sizeof(tlg::StepStatsDev)));
     TLG_CUDA(cudaMallocHost(&h_flags, 16));
     for (auto& e : ev) TLG_CUDA(cudaEventCreate(&e));

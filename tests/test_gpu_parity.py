@@ -474,3 +474,37 @@ def test_bit_planes_int8_layer1_match_oracle(tlg, oracle, shape_case, optimizer)
             assert close(got, p_new, 1e-4), (step, worst(got, p_new))
             p = p_new.astype(np.float32).astype(np.float64)
             lrn.set_params(p)
+
+
+@pytest.mark.parametrize("no_graph", [False, True])
+def test_staged_f32_inputs_match_train_step(tlg, oracle, monkeypatch, no_graph):
+    """The pipelined stage/train_staged path with fp32 observations (graph-replayed small
+    steps) equals plain train_step calls."""
+    if no_graph:
+        monkeypatch.setenv("TLG_NO_GRAPH", "1")
+    # C1's shape: its dX epilogue writes more column-sum rows (one per persistent CTA)
+    # than the loss kernel has blocks, which once overran into the staging slots
+    S, T, D, A, hidden = 64, 32, 64, 6, (256, 256)
+    p = init_params(oracle, Shape(2, D, A, hidden), 11)
+    batches = [make_batch(tlg, S, T, D, A, seed=300 + k) for k in range(4)]
+    res = []
+    for mode in ("plain", "staged"):
+        lrn = tlg.Learner("mlp", D, A, hidden, max_segments=S, unroll_len=T, optimizer="sgd")
+        lrn.set_hyper(learning_rate=0.05, batch_size=S, unroll_len=T)
+        lrn.set_params(p)
+        if mode == "plain":
+            stats = [lrn.train_step(b) for b in batches]
+        else:
+            from paper_2011_12895_b200._capi import SegmentBatchView
+            views = [SegmentBatchView(b) for b in batches]
+            # train one, then keep two batches staged (the bench's e2e pattern)
+            lrn.stage(views[0])
+            stats = [lrn.train_staged()]
+            lrn.stage(views[1])
+            for k in range(2, len(views)):
+                lrn.stage(views[k])
+                stats.append(lrn.train_staged())
+            stats.append(lrn.train_staged())
+        res.append((lrn.get_params(), stats))
+    assert np.array_equal(res[0][0], res[1][0])
+    assert res[0][1] == res[1][1]

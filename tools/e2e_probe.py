@@ -23,9 +23,11 @@ for h in hs:
     hb = h.slice(0, S)
     hb.obs = tlg.synth.pack_bits(h.obs)
     v = tlg.SegmentBatchView(hb, bits=True, obs_dim=D)
+    v.pinned = []
     for k, a in v.arrs.items():
         t = torch.empty(a.shape, dtype=getattr(torch, str(a.dtype)), pin_memory=True)
         t.numpy()[...] = a
+        v.pinned.append(t)
         v.arrs[k] = t.numpy()
     v.c = tlg._capi.SegmentBatchC(S, T, D, 2, *(v.arrs[k].ctypes.data for k in (
         "obs", "action", "reward", "behavior_logp", "value_est", "done", "bootstrap", "valid_steps")))
