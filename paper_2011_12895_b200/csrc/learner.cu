@@ -290,7 +290,8 @@ struct tlg_learner {
 
   ~tlg_learner() {
     if (stream) cudaStreamSynchronize(stream);
-    if (graph_exec) cudaGraphExecDestroy(graph_exec);
+    for (auto& g : graphs)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
     if (copy_stream) {
       cudaStreamSynchronize(copy_stream);
       cudaStreamDestroy(copy_stream);
@@ -649,24 +650,33 @@ struct tlg_learner {
     launches = 0;
     TLG_CUDA(cudaSetDevice(cfg.device));
     if (use_graph(bs, n)) {
-      const Staged sg = stage_shard(bs[0], on_device, /*internal=*/true);
+      // a batch staged by stage_async is read in place (its slot's graph); any other batch
+      // is first copied into the learner's own buffers (binding 0)
+      int bind = 0;
+      if (on_device)
+        for (int k = 0; k < 2; ++k)
+          if (slots[k].ready && bs[0].action == slots[k].action) bind = 1 + k;
+      const Staged sg = stage_shard(bs[0], on_device, /*internal=*/bind == 0);
       const long key = long(sg.bd.S) * 8 + (sg.x0_u8 ? 1 : 0) + (sg.exact ? 2 : 0) +
                        (sg.x0_bits ? 4 : 0);
-      if (!graph_exec || key != graph_key || graph_hyper != hyper_version) {
-        if (graph_exec) cudaGraphExecDestroy(graph_exec);
-        graph_exec = nullptr;
+      Graph& gr = graphs[bind];
+      if (!gr.exec || key != gr.key || gr.hyper != hyper_version ||
+          (bind && gr.obs != slots[bind - 1].obs)) {
+        if (gr.exec) cudaGraphExecDestroy(gr.exec);
+        gr.exec = nullptr;
         cudaGraph_t g;
         TLG_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
         enqueue_device_step(&sg, 1);
         TLG_CUDA(cudaStreamEndCapture(stream, &g));
-        TLG_CUDA(cudaGraphInstantiate(&graph_exec, g, 0));
+        TLG_CUDA(cudaGraphInstantiate(&gr.exec, g, 0));
         cudaGraphDestroy(g);
-        graph_key = key;
-        graph_hyper = hyper_version;
-        graph_launches = launches;
+        gr.key = key;
+        gr.hyper = hyper_version;
+        gr.launches = launches;
+        gr.obs = bind ? slots[bind - 1].obs : nullptr;
       }
-      TLG_CUDA(cudaGraphLaunch(graph_exec, stream));
-      launches = graph_launches;
+      TLG_CUDA(cudaGraphLaunch(gr.exec, stream));
+      launches = gr.launches;
     } else {
       enqueue_device_step(nullptr, n, bs, on_device);
     }
@@ -820,10 +830,15 @@ struct tlg_learner {
   int head_tiles = 1;
   void set_guard(int shard);
   void launch_guarded_optimizer(bool adam, float lr);
-  cudaGraphExec_t graph_exec = nullptr;
-  long graph_key = -1;
-  uint64_t hyper_version = 0, graph_hyper = ~0ull;
-  int graph_launches = 0;
+  struct Graph {
+    cudaGraphExec_t exec = nullptr;
+    long key = -1;
+    uint64_t hyper = ~0ull;
+    int launches = 0;
+    const void* obs = nullptr;  // slot obs buffer the graph reads (slot bindings)
+  };
+  Graph graphs[3];  // learner's own buffers, staging slot 0, staging slot 1
+  uint64_t hyper_version = 0;
   bool graph_disabled = std::getenv("TLG_NO_GRAPH") != nullptr;
   uint64_t* adam_t_dev = nullptr;
 };
