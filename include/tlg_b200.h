@@ -99,7 +99,8 @@ typedef struct tlg_learner_config {
 /* One shard's slice of the replay draw, SoA [S][T]. */
 typedef struct tlg_segment_batch {
   uint32_t n_segments, unroll_len, obs_dim, obs_dtype;
-  const void* obs;              /* [S][T][obs_dim] f32 or u8 */
+  const void* obs;              /* [S][T][obs_dim] f32 or u8, or TLG_OBS_BITS: [S][T] rows of
+                                   ceil(obs_dim / 8) bytes, 0/1 planes LSB first */
   const int32_t* action;        /* [S][T] */
   const float* reward;          /* [S][T] */
   const float* behavior_logp;   /* [S][T] */

@@ -3,6 +3,7 @@
 // math of TrainStep (learner.cpp:117-152) runs on the GPU via include/tlg_b200.h.
 #include "tleague/learner/learner.hpp"
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -55,7 +56,8 @@ struct Learner::Gpu {
   std::size_t P = 0;
   Pinned<float> obs, reward, blogp, value, boot;
   Pinned<std::int32_t> action, valid;
-  Pinned<std::uint8_t> done;
+  Pinned<std::uint8_t> done, bits;
+  bool binary = false;  // this draw's observations are all 0/1: shipped bit-packed
   std::vector<tlg_segment_batch> batches;
   std::vector<tlg_step_stats> stats;
 
@@ -67,9 +69,29 @@ struct Learner::Gpu {
   }
 
   // SoA packing of the reference's AoS segments (types.hpp:82-104), padding zeroed.
+  // Observations made only of 0/1 planes (Pommerman-style) travel bit-packed
+  // (TLG_OBS_BITS, exact, 32x fewer bytes than fp32) and take the int8 tensor-core
+  // layer-1 path; anything else travels as fp32.
   void Pack(const std::vector<TrajectorySegment>& segs) {
     const std::size_t D = shape.obs_dim, F = std::size_t(S) * T * shards;
-    obs.ensure(F * D);
+    const std::size_t rowb = (D + 7) / 8;
+    binary = true;
+    for (const TrajectorySegment& seg : segs) {
+      const std::uint32_t n = std::min<std::uint32_t>(seg.valid_steps, std::uint32_t(seg.steps.size()));
+      for (std::uint32_t t = 0; t < n && binary; ++t)
+        for (double x : seg.steps[t].obs)
+          if (x != 0.0 && x != 1.0) {
+            binary = false;
+            break;
+          }
+      if (!binary) break;
+    }
+    if (binary) {
+      bits.ensure(F * rowb);
+      std::memset(bits.p, 0, F * rowb);
+    } else {
+      obs.ensure(F * D);
+    }
     reward.ensure(F);
     blogp.ensure(F);
     value.ensure(F);
@@ -77,7 +99,7 @@ struct Learner::Gpu {
     done.ensure(F);
     boot.ensure(std::size_t(S) * shards);
     valid.ensure(std::size_t(S) * shards);
-    std::memset(obs.p, 0, F * D * sizeof(float));
+    if (!binary) std::memset(obs.p, 0, F * D * sizeof(float));
     for (std::size_t i = 0; i < segs.size(); ++i) {
       const TrajectorySegment& seg = segs[i];
       if (seg.valid_steps > T || seg.valid_steps > seg.steps.size())
@@ -90,7 +112,13 @@ struct Learner::Gpu {
           const SegmentStep& st = seg.steps[t];
           if (st.obs.size() != D)
             throw std::invalid_argument("observation size does not match policy shape");
-          for (std::size_t j = 0; j < D; ++j) obs.p[f * D + j] = float(st.obs[j]);
+          if (binary) {
+            std::uint8_t* row = bits.p + f * rowb;
+            for (std::size_t j = 0; j < D; ++j)
+              if (st.obs[j] != 0.0) row[j >> 3] |= std::uint8_t(1u << (j & 7));
+          } else {
+            for (std::size_t j = 0; j < D; ++j) obs.p[f * D + j] = float(st.obs[j]);
+          }
           action.p[f] = std::int32_t(st.action);
           reward.p[f] = float(st.reward);
           blogp.p[f] = float(st.behavior_logp);
@@ -110,8 +138,9 @@ struct Learner::Gpu {
       b.n_segments = S;
       b.unroll_len = T;
       b.obs_dim = shape.obs_dim;
-      b.obs_dtype = TLG_OBS_F32;
-      b.obs = obs.p + f0 * D;
+      b.obs_dtype = binary ? TLG_OBS_BITS : TLG_OBS_F32;
+      b.obs = binary ? static_cast<const void*>(bits.p + f0 * rowb)
+                     : static_cast<const void*>(obs.p + f0 * D);
       b.action = action.p + f0;
       b.reward = reward.p + f0;
       b.behavior_logp = blogp.p + f0;
@@ -171,7 +200,7 @@ void Learner::StartPeriod() {
     c.max_segments = S;
     c.unroll_len = T;
     c.device = config_.device;
-    c.obs_dtype = TLG_OBS_F32;
+    c.obs_dtype = TLG_OBS_BITS;  // accepts fp32 and bit-packed batches
     Check(tlg_learner_create(&c, &s, &gpu_->h));
     gpu_->shape = s;
     gpu_->S = S;
