@@ -245,6 +245,69 @@ void launch_i8_bits_dw(const int8_t* P, const uint8_t* bits, long rowb, const un
   else run_i8_dw<1>(tp, tb, tw, p, tm, stream);
 }
 
+template <int BN, int CG>
+void run_i8x2_fwd(const CUtensorMap& ta, const CUtensorMap& tq, const CUtensorMap& to,
+                  const CUtensorMap& tl, const I8x2Params& p, const TileMap& tm,
+                  cudaStream_t stream) {
+  auto kern = gemm_i8x2_fwd_kernel<BN, CG>;
+  constexpr int bytes = SmemI8x2<BN, CG>::kBytes;
+  static_assert(bytes <= 227 * 1024, "shared memory budget");
+  static bool attr = false;
+  if (!attr) {
+    TLG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    attr = true;
+  }
+  const int tiles = tm.m_tiles * tm.n_tiles;
+  constexpr int threads = 32 * (2 + kEpiWarps);
+  if (CG == 1) {
+    kern<<<std::min(tiles, num_sms()), threads, bytes, stream>>>(ta, tq, to, tl, p, tm);
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * std::min(tiles, num_sms() / 2));
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = bytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    TLG_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tq, to, tl, p, tm));
+  }
+  TLG_CHECK_LAUNCH();
+}
+
+LaunchInfo launch_i8x2_fwd(const int8_t* a, const int8_t* q, long Kp, const float* scale,
+                           const float* bias, int M, int N, int K, float* out, float* out_lo,
+                           int ldo, const float* head_w, const float* head_wv, int head_k,
+                           float* head_part, cudaStream_t stream) {
+  if (M <= 0 || N <= 0 || K <= 0) throw CudaError("gemm_i8x2: empty problem");
+  if (K % 16 != 0 || Kp < K) throw CudaError("gemm_i8x2: K must be a multiple of 16");
+  if (head_k > 8) throw CudaError("gemm_i8x2: fused heads need n_actions + 1 <= 8");
+  // 64-column tiles: three accumulators double-buffered in TMEM (the epilogue of one tile
+  // overlaps the MMAs of the next).  CTA pairs only (a single CTA's six piece tiles
+  // would leave one pipeline stage)
+  int BN = 64;
+  if (const char* e = std::getenv("TLG_I8X2_BN")) BN = std::atoi(e) == 128 ? 128 : 64;
+  if (M < 2 * kBM) throw CudaError("gemm_i8x2: needs M >= 256");
+  constexpr int cg = 2;
+  I8x2Params p{M, N, K, scale, bias, long(M), long(N), head_w, head_wv, head_k, head_part,
+               out_lo != nullptr ? 1 : 0};
+  const TileMap tm{ceil_div(M, kBM * cg), ceil_div(N, BN), 1};
+  const CUtensorMap ta = make_bytes_map(a, K, 3L * M, K, kBKi, kBM, CU_TENSOR_MAP_SWIZZLE_128B);
+  const CUtensorMap tq = make_bytes_map(q, Kp, 3L * N, Kp, kBKi, BN / cg, CU_TENSOR_MAP_SWIZZLE_128B);
+  const CUtensorMap to = make_f32_out_map(out, N, M, ldo);
+  CUtensorMap tl;
+  if (out_lo) tl = make_f32_out_map(out_lo, N, M, ldo);
+  else std::memset(&tl, 0, sizeof(tl));
+  if (BN == 128) run_i8x2_fwd<128, 2>(ta, tq, to, tl, p, tm, stream);
+  else run_i8x2_fwd<64, 2>(ta, tq, to, tl, p, tm, stream);
+  const int tiles = tm.m_tiles * tm.n_tiles;
+  return {BN, 2 * std::min(tiles, num_sms() / 2)};
+}
+
 void launch_quantize_rows(const float* W, int N, int K, long ldw, int8_t* q, long Kp, float* s,
                           cudaStream_t stream) {
   if (Kp % 16 != 0 || Kp < K) throw CudaError("quantize_rows: Kp must be >= K and a multiple of 16");
@@ -254,14 +317,17 @@ void launch_quantize_rows(const float* W, int N, int K, long ldw, int8_t* q, lon
 
 LaunchInfo launch_i8_bits_fwd(const uint8_t* bits, long rowb, const int8_t* q, long Kp,
                               const float* scale, const float* bias, int M, int N, int K,
-                              float* out, float* out_lo, int ldo, cudaStream_t stream) {
+                              float* out, float* out_lo, int ldo, cudaStream_t stream,
+                              int8_t* out_q) {
   if (M <= 0 || N <= 0 || K <= 0) throw CudaError("gemm_i8: empty problem");
   if (rowb * 8 < K || Kp < K) throw CudaError("gemm_i8: K exceeds the operand rows");
   constexpr int BN = 128;
   // CTA pairs (256-row tiles) whenever there are enough of them to fill the GPU
   int cg = (M >= 2 * kBM && long(ceil_div(M, 2 * kBM)) * ceil_div(N, BN) >= num_sms() / 2) ? 2 : 1;
   if (const char* e = std::getenv("TLG_I8_CG")) cg = std::atoi(e) == 2 ? 2 : 1;
-  I8Params p{M, N, K, scale, bias, N};
+  if (out_q != nullptr && (N % 32 != 0 || (reinterpret_cast<uintptr_t>(out_q) & 15) != 0))
+    throw CudaError("gemm_i8: int8 activation pieces need N % 32 == 0 and 16-B alignment");
+  I8Params p{M, N, K, scale, bias, N, out_q};
   const TileMap tm{ceil_div(M, kBM * cg), ceil_div(N, BN), 1};
   // bit rows: box {16 bytes = 128 elements, 128 rows}; pieces: box {128, BN / cg}, SW128
   const CUtensorMap tb = make_bytes_map(bits, rowb, M, rowb, kBKi / 8, kBM, CU_TENSOR_MAP_SWIZZLE_NONE);

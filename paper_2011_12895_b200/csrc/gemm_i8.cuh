@@ -41,7 +41,27 @@ struct I8Params {
   const float* scale;  // [N] piece scale per output column
   const float* bias;   // [N]
   long q_rows;         // rows per piece in the stacked [3][q_rows][Kp] piece array
+  int8_t* out_q;       // optional: tanh outputs as int8 pieces [3][M][N] (scale 1/127)
 };
+
+// tanh output o in (-1, 1) -> three int8 pieces of o * 127 (fixed scale 1/127), packed
+// four columns per word; magic-constant rounding (exact residual steps)
+__device__ __forceinline__ void act_pieces4(const float* o, uint32_t& w0, uint32_t& w1,
+                                            uint32_t& w2) {
+  constexpr float kMagic = 12582912.f;
+  w0 = w1 = w2 = 0u;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float x = o[j] * 127.f;
+    const float m0 = x + kMagic;
+    const float x1 = (x - (m0 - kMagic)) * 128.f;
+    const float m1 = x1 + kMagic;
+    const float m2 = (x1 - (m1 - kMagic)) * 128.f + kMagic;
+    w0 |= (__float_as_uint(m0) & 0xFFu) << (8 * j);
+    w1 |= (__float_as_uint(m1) & 0xFFu) << (8 * j);
+    w2 |= (__float_as_uint(m2) & 0xFFu) << (8 * j);
+  }
+}
 
 template <int BN, int CG>
 struct SmemI8 {
@@ -338,6 +358,21 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                                float(int(rb[j])) * (s * 6.103515625e-05f));
           o[j] = tanhf(z + bj);
         }
+        if (p.out_q != nullptr && rbase + lane < p.M) {
+          // the same activations as int8 pieces for the next layer's int8 GEMM
+          const long plane = long(p.M) * p.N;
+          int8_t* q = p.out_q + long(rbase + lane) * p.N + nb;
+#pragma unroll
+          for (int j16 = 0; j16 < 2; ++j16) {
+            uint32_t a[4], b[4], c4[4];
+#pragma unroll
+            for (int w = 0; w < 4; ++w) act_pieces4(o + 16 * j16 + 4 * w, a[w], b[w], c4[w]);
+            *reinterpret_cast<uint4*>(q + 16 * j16) = make_uint4(a[0], a[1], a[2], a[3]);
+            *reinterpret_cast<uint4*>(q + plane + 16 * j16) = make_uint4(b[0], b[1], b[2], b[3]);
+            *reinterpret_cast<uint4*>(q + 2 * plane + 16 * j16) =
+                make_uint4(c4[0], c4[1], c4[2], c4[3]);
+          }
+        }
         if (lane == 0) bulk_wait_read();
         __syncwarp();
 #pragma unroll
@@ -362,6 +397,306 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
       if (lane == 0) {
         if (CG == 2) mbar_arrive_cluster(map_rank0(bar_tempty + 8 * acc_buf));
         else mbar_arrive(bar_tempty + 8 * acc_buf);
+      }
+    }
+    if (lane == 0) bulk_wait_all();
+  }
+
+  tc_fence_before();
+  if (CG == 2) cluster_sync_all();
+  else __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    if (CG == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "n"(S::kTmemCols));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "n"(S::kTmemCols));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Forward of a layer whose input activations are int8 pieces (fixed scale 1/127, from the
+// int8 layer-1 epilogue) and whose weights are int8 row pieces (scale s_n):
+//   A = a0 + a1/2^7 + a2/2^14 (x 1/127),  B = s_n (b0 + b1/2^7 + b2/2^14)
+//   sum_k A B = s_n/127 [acc0 + acc1/2^7 + acc2/2^14],
+//   acc0 = a0.b0,  acc1 = a0.b1 + a1.b0,  acc2 = a0.b2 + a1.b1 + a2.b0  (six int8 MMAs;
+// the dropped a1.b2 + a2.b1 + a2.b2 terms are < 2^-21 of a0.b0's scale).
+// Three int32 TMEM accumulators (single-buffered); epilogue as the tf32 forward: bias +
+// tanh, optional fused policy/value heads, full fp32 plane (+ optional residual plane).
+struct I8x2Params {
+  int M, N, K;
+  const float* scale;  // [N] weight piece scales
+  const float* bias;   // [N]
+  long a_rows;         // rows per piece of the stacked activation pieces [3][a_rows][K]
+  long q_rows;         // rows per piece of the stacked weight pieces [3][q_rows][Kp]
+  const float* head_w;   // fused heads as in Params (gemm_sm100.cuh)
+  const float* head_wv;
+  int head_k;
+  float* head_part;
+  int has_lo;
+};
+
+template <int BN_, int CG>
+struct SmemI8x2 {
+  static constexpr int BN = BN_;
+  // three accumulators; double-buffered when they fit TMEM twice (BN = 64)
+  static constexpr int kBufs = 6 * BN <= 512 ? 2 : 1;
+  static constexpr int kA = kBM * kBKi;          // 16 KB per activation piece tile
+  static constexpr int kBN = BN / CG;
+  static constexpr int kQ = kBN * kBKi;          // per weight piece tile
+  static constexpr int kStage = 3 * kA + 3 * kQ;
+  static constexpr int kEpi = kEpiWarps * (2 * 4096 + 1024);
+  static constexpr int kStagesRaw = (225 * 1024 - kEpi - 2048) / kStage;
+  static constexpr int kStages = kStagesRaw > 4 ? 4 : kStagesRaw;
+  static constexpr int kBarOff = kStages * kStage;
+  static constexpr int kNumBars = 2 * kStages + 4;  // full, empty; tfull[2], tempty[2]
+  static constexpr int kEpiOff = (kBarOff + kNumBars * 8 + 16 + 1023) / 1024 * 1024;
+  static constexpr int kBytes = kEpiOff + kEpi + 1024;
+  static constexpr int kTmemCols = 512;  // 3 x 128 accumulator columns
+  static_assert(kStage % 1024 == 0, "stages must keep the 1 KB swizzle alignment");
+  static_assert(kStages >= 2, "pipeline needs two stages");
+};
+
+template <int BN, int CG>
+__device__ __forceinline__ constexpr uint32_t make_idesc_i8x2() {
+  return (2u << 4) | (1u << 7) | (1u << 10)  // s32 <- s8 x s8, both K-major
+         | (uint32_t(BN >> 3) << 17) | (uint32_t((kBM * CG) >> 4) << 24);
+}
+
+template <int BN_, int CG>
+__global__ void __launch_bounds__(32 * (2 + kEpiWarps), 1)
+    gemm_i8x2_fwd_kernel(const __grid_constant__ CUtensorMap tmA,
+                         const __grid_constant__ CUtensorMap tmQ,
+                         const __grid_constant__ CUtensorMap tmOut,
+                         const __grid_constant__ CUtensorMap tmOutLo, const I8x2Params p,
+                         const TileMap tm) {
+  using S = SmemI8x2<BN_, CG>;
+  constexpr int BN = S::BN;
+  const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
+  const int cl_id = CG == 2 ? int(blockIdx.x >> 1) : int(blockIdx.x);
+  const int n_cl = CG == 2 ? int(gridDim.x >> 1) : int(gridDim.x);
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t bar_full = sbase + S::kBarOff;
+  const uint32_t bar_empty = bar_full + 8 * S::kStages;
+  const uint32_t bar_tfull = bar_empty + 8 * S::kStages;  // [2]
+  const uint32_t bar_tempty = bar_tfull + 16;              // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + S::kBarOff + S::kNumBars * 8);
+  constexpr int kOffQ = 3 * S::kA;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int num_tiles = tm.m_tiles * tm.n_tiles;
+  const int kb_total = (p.K + kBKi - 1) / kBKi;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmQ);
+    for (int s = 0; s < S::kStages; ++s) {
+      mbar_init(bar_full + 8 * s, 1);
+      mbar_init(bar_empty + 8 * s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(bar_tfull + 8 * b, 1);
+      mbar_init(bar_tempty + 8 * b, kEpiWarps * CG);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    if (CG == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "n"(S::kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "n"(S::kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+  }
+  tc_fence_before();
+  if (CG == 2) cluster_sync_all();
+  else __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cl_id; t < num_tiles; t += n_cl) {
+        const int nt = t % tm.n_tiles, mt = t / tm.n_tiles;
+        const int m0 = mt * kBM * CG + int(rank) * kBM;
+        const int n0 = nt * BN + int(rank) * S::kBN;
+        for (int kb = 0; kb < kb_total; ++kb) {
+          mbar_wait(bar_empty + 8 * stage, phase ^ 1);
+          const uint32_t st = sbase + stage * S::kStage;
+          const uint32_t full = CG == 2 ? map_rank0(bar_full + 8 * stage) : bar_full + 8 * stage;
+          if (rank == 0) mbar_expect_tx(bar_full + 8 * stage, (3 * S::kA + 3 * S::kQ) * CG);
+#pragma unroll
+          for (int pc = 0; pc < 3; ++pc) {
+            const int arow = int(pc * p.a_rows) + m0, qrow = int(pc * p.q_rows) + n0;
+            if (CG == 2) {
+              tma_load_2d_pair(st + pc * S::kA, &tmA, kb * kBKi, arow, full);
+              tma_load_2d_pair(st + kOffQ + pc * S::kQ, &tmQ, kb * kBKi, qrow, full);
+            } else {
+              tma_load_2d(st + pc * S::kA, &tmA, kb * kBKi, arow, full);
+              tma_load_2d(st + kOffQ + pc * S::kQ, &tmQ, kb * kBKi, qrow, full);
+            }
+          }
+          if (++stage == S::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = make_idesc_i8x2<BN, CG>();
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = cl_id; t < num_tiles; t += n_cl, ++it) {
+        const int buf = S::kBufs == 2 ? (it & 1) : 0;
+        const uint32_t tph = S::kBufs == 2 ? ((it >> 1) & 1) : (it & 1);
+        mbar_wait(bar_tempty + 8 * buf, tph ^ 1);
+        tc_fence_after();
+        const uint32_t t0 = tmem_base + uint32_t(buf * 3 * BN), t1 = t0 + uint32_t(BN),
+                       t2 = t0 + uint32_t(2 * BN);
+        for (int kb = 0; kb < kb_total; ++kb) {
+          mbar_wait(bar_full + 8 * stage, phase);
+          tc_fence_after();
+          const uint32_t st = sbase + stage * S::kStage;
+#pragma unroll
+          for (int k = 0; k < kBKi / 32; ++k) {
+            uint64_t da[3], dq[3];
+#pragma unroll
+            for (int pc = 0; pc < 3; ++pc) {
+              da[pc] = make_sdesc<false>(st + pc * S::kA + k * 32, 16, 1024);
+              dq[pc] = make_sdesc<false>(st + kOffQ + pc * S::kQ + k * 32, 16, 1024);
+            }
+            const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
+            mma_i8<CG>(t0, da[0], dq[0], idesc, acc);
+            mma_i8<CG>(t1, da[0], dq[1], idesc, acc);
+            mma_i8<CG>(t1, da[1], dq[0], idesc, 1u);
+            mma_i8<CG>(t2, da[0], dq[2], idesc, acc);
+            mma_i8<CG>(t2, da[1], dq[1], idesc, 1u);
+            mma_i8<CG>(t2, da[2], dq[0], idesc, 1u);
+          }
+          if (CG == 2) mma_commit_pair(bar_empty + 8 * stage);
+          else mma_commit(bar_empty + 8 * stage);
+          if (++stage == S::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (CG == 2) mma_commit_pair(bar_tfull + 8 * buf);
+        else mma_commit(bar_tfull + 8 * buf);
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const int ew = warp - 2;
+    const uint32_t blk = sbase + S::kEpiOff + uint32_t(ew * (2 * 4096 + 1024));
+    uint8_t* blk_ptr = smem + S::kEpiOff + ew * (2 * 4096 + 1024);
+    float* wsm = reinterpret_cast<float*>(blk_ptr + 2 * 4096);  // head weights [8][32]
+    constexpr int kHK = 8;
+    const bool do_head = p.head_k > 0;
+    int it = 0;
+    for (int t = cl_id; t < num_tiles; t += n_cl, ++it) {
+      const int nt = t % tm.n_tiles, mt = t / tm.n_tiles;
+      const int m0 = mt * kBM * CG + int(rank) * kBM, n0 = nt * BN;
+      const int rbase = m0 + q * 32;
+      const int buf = S::kBufs == 2 ? (it & 1) : 0;
+      mbar_wait(bar_tfull + 8 * buf, S::kBufs == 2 ? ((it >> 1) & 1) : (it & 1));
+      tc_fence_after();
+      const uint32_t ta = tmem_base + uint32_t(buf * 3 * BN) + (uint32_t(q * 32) << 16);
+      float zacc[kHK];
+#pragma unroll
+      for (int k = 0; k < kHK; ++k) zacc[k] = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        const int nb = n0 + c;
+        uint32_t r0[32], r1[32], r2[32];
+        tmem_ld32(ta + uint32_t(c), r0);
+        tmem_ld32(ta + uint32_t(BN + c), r1);
+        tmem_ld32(ta + uint32_t(2 * BN + c), r2);
+        const bool colok = nb + lane < p.N;
+        const float sc = colok ? __ldg(p.scale + nb + lane) * (1.f / 127.f) : 0.f;
+        const float bi = colok ? __ldg(p.bias + nb + lane) : 0.f;
+        float o[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float s = __shfl_sync(0xffffffffu, sc, j);
+          const float bj = __shfl_sync(0xffffffffu, bi, j);
+          const float v = fmaf(float(int(r2[j])), 6.103515625e-05f,
+                               fmaf(float(int(r1[j])), 0.0078125f, float(int(r0[j]))));
+          o[j] = tanhf(fmaf(v, s, bj));
+        }
+        if (do_head) {
+#pragma unroll
+          for (int k = 0; k < kHK; ++k) {
+            float wk = 0.f;
+            if (k < p.head_k && colok) {
+              const float* wrow = k < p.head_k - 1 ? p.head_w + long(k) * p.N : p.head_wv;
+              wk = __ldg(wrow + nb + lane);
+            }
+            wsm[k * 32 + lane] = wk;
+          }
+          __syncwarp();
+#pragma unroll
+          for (int k = 0; k < kHK; ++k) {
+            if (k < p.head_k) {
+              float z = zacc[k];
+#pragma unroll
+              for (int j4 = 0; j4 < 8; ++j4) {
+                const float4 w4 = *reinterpret_cast<const float4*>(wsm + k * 32 + 4 * j4);
+                z = fmaf(w4.x, o[4 * j4], z);
+                z = fmaf(w4.y, o[4 * j4 + 1], z);
+                z = fmaf(w4.z, o[4 * j4 + 2], z);
+                z = fmaf(w4.w, o[4 * j4 + 3], z);
+              }
+              zacc[k] = z;
+            }
+          }
+          __syncwarp();
+        }
+        if (lane == 0) bulk_wait_read();
+        __syncwarp();
+#pragma unroll
+        for (int j4 = 0; j4 < 8; ++j4) {
+          *reinterpret_cast<float4*>(blk_ptr + swz(lane, j4)) =
+              make_float4(o[4 * j4], o[4 * j4 + 1], o[4 * j4 + 2], o[4 * j4 + 3]);
+          if (p.has_lo)
+            *reinterpret_cast<float4*>(blk_ptr + 4096 + swz(lane, j4)) =
+                make_float4(o[4 * j4] - tf32_hi(o[4 * j4]), o[4 * j4 + 1] - tf32_hi(o[4 * j4 + 1]),
+                            o[4 * j4 + 2] - tf32_hi(o[4 * j4 + 2]),
+                            o[4 * j4 + 3] - tf32_hi(o[4 * j4 + 3]));
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tmOut, nb, rbase, blk);
+          if (p.has_lo) tma_store_2d(&tmOutLo, nb, rbase, blk + 4096);
+          bulk_commit();
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (CG == 2) mbar_arrive_cluster(map_rank0(bar_tempty + 8 * buf));
+        else mbar_arrive(bar_tempty + 8 * buf);
+      }
+      if (do_head && rbase + lane < p.M) {
+        float* hp = p.head_part + (long(nt) * p.M + rbase + lane) * p.head_k;
+#pragma unroll
+        for (int k = 0; k < kHK; ++k)
+          if (k < p.head_k) hp[k] = zacc[k];
       }
     }
     if (lane == 0) bulk_wait_all();
@@ -674,7 +1009,16 @@ void launch_quantize_rows(const float* W, int N, int K, long ldw, int8_t* q, lon
 // Writes the full fp32 plane and the tf32 residual plane (row pitch ldo).
 LaunchInfo launch_i8_bits_fwd(const uint8_t* bits, long rowb, const int8_t* q, long Kp,
                               const float* scale, const float* bias, int M, int N, int K,
-                              float* out, float* out_lo, int ldo, cudaStream_t stream);
+                              float* out, float* out_lo, int ldo, cudaStream_t stream,
+                              int8_t* out_q = nullptr);
+
+// out = tanh(A . W^T + b) with A given as int8 pieces [3][M][K] (scale 1/127, e.g. the
+// out_q of launch_i8_bits_fwd) and W as launch_quantize_rows pieces.  Optional fused
+// heads (Params::head_* semantics) and residual plane (out_lo may be null).  K % 16 == 0.
+LaunchInfo launch_i8x2_fwd(const int8_t* a, const int8_t* q, long Kp, const float* scale,
+                           const float* bias, int M, int N, int K, float* out, float* out_lo,
+                           int ldo, const float* head_w, const float* head_wv, int head_k,
+                           float* head_part, cudaStream_t stream);
 
 // dZ [F][M] (row pitch ldz floats) -> pieces P [3][F][M] int8 with one scale per
 // (split, column): s = colmax[f / rows_per_split][m] / 127.  M % 4 == 0.

@@ -172,6 +172,13 @@ struct tlg_learner {
   unsigned* colmax = nullptr;
   static constexpr int kMaxI8Splits = 148;
   bool wq_fresh = false;
+  // layer 2 on int8 x int8 (tanh activations as pieces, W_2 as row pieces).  Opt-in
+  // (TLG_I8X2=1): measured at C3 its forward is L2->SM-bound at 64-column tiles and the
+  // extra piece plane costs layer 1 more than layer 2 saves (profiles/r01_ncu_i8x2.md)
+  const bool i8x2_disabled = std::getenv("TLG_I8X2") == nullptr;
+  int8_t* act_q = nullptr;  // [3][F][h_1]
+  int8_t* w2q = nullptr;    // [3][h_2][h_1]
+  float* w2_scale = nullptr;
   int32_t* action;
   float *reward, *blogp, *value;
   uint8_t* done;
@@ -236,6 +243,11 @@ struct tlg_learner {
       if (net.dims[1] % 16 == 0) {
         dzq = mem.add<int8_t>(3 * F_max * long(net.dims[1]));
         colmax = mem.add<unsigned>(long(kMaxI8Splits) * net.dims[1]);
+      }
+      if (net.dims[1] % 32 == 0 && net.A + 1 <= 8) {
+        act_q = mem.add<int8_t>(3 * F_max * long(net.dims[1]));
+        w2q = mem.add<int8_t>(3 * long(net.dims[2]) * net.dims[1]);
+        w2_scale = mem.add<float>(net.dims[2]);
       }
     }
     action = mem.add<int32_t>(F_max);
@@ -328,6 +340,7 @@ struct tlg_learner {
   // heads stay on the last trunk layer's tf32 epilogue)
   bool i8_layer1() const { return wq != nullptr && !i8_disabled; }
   bool i8_dw1() const { return i8_layer1() && dzq != nullptr && !i8_dw_disabled; }
+  bool i8_fwd2(long F) const { return i8_layer1() && act_q != nullptr && !i8x2_disabled && F >= 256; }
 
   // split-K plan of the int8 layer-1 dW: as many splits as fill one wave of CTA pairs,
   // an even number of 128-frame k-blocks per split (the dX epilogue's 256-row tiles
@@ -515,9 +528,18 @@ struct tlg_learner {
           wq_fresh = true;
           ++launches;
         }
-        // binary planes x int8 weight pieces: exact integer tensor-core GEMM
+        // binary planes x int8 weight pieces: exact integer tensor-core GEMM (+ the
+        // activations as int8 pieces when layer 2 takes the int8 path too)
         bn = tlg::gemm::launch_i8_bits_fwd(sg.x0_bits, bits_pitch, wq, wq_kp, wq_scale, p.bias,
-                                           int(F), outw, in, act[0], act_lo[0], outw, stream).bn;
+                                           int(F), outw, in, act[0], act_lo[0], outw, stream,
+                                           i8_fwd2(F) ? act_q : nullptr).bn;
+      } else if (l == 1 && sg.x0_bits != nullptr && i8_fwd2(F)) {
+        tlg::gemm::launch_quantize_rows(params + net.w_off[1], outw, in, in, w2q, in, w2_scale,
+                                        stream);
+        ++launches;
+        bn = tlg::gemm::launch_i8x2_fwd(act_q, w2q, in, w2_scale, p.bias, int(F), outw, in,
+                                        act[1], p.out_lo, outw, p.head_w, p.head_wv, p.head_k,
+                                        p.head_part, stream).bn;
       } else {
         bn = tlg::gemm::launch(A, B, int(F), outw, in, tlg::gemm::kEpiFwdTanh, p, 1, stream).bn;
       }

@@ -349,6 +349,103 @@ void check_i8_dw(const char* name, int M, int N, int K, int kb_per_split) {
   cudaFree(Z.x); cudaFree(Z.hi); cudaFree(Z.lo); cudaFree(X.x); cudaFree(X.hi); cudaFree(X.lo);
 }
 
+// tanh activations as int8 pieces (scale 1/127) x int8 weight pieces (kind::i8, 6 MMAs)
+static void host_act_pieces(const std::vector<float>& o, long M, long K, std::vector<int8_t>& q) {
+  const float kMagic = 12582912.f;
+  q.assign(3 * M * K, 0);
+  for (long i = 0; i < M * K; ++i) {
+    volatile float x = o[i] * 127.f;
+    volatile float m0 = x + kMagic;
+    volatile float r0 = m0 - kMagic;
+    volatile float x1 = (x - r0) * 128.f;
+    volatile float m1 = x1 + kMagic;
+    volatile float r1 = m1 - kMagic;
+    volatile float x2 = (x1 - r1) * 128.f;
+    volatile float m2 = x2 + kMagic;
+    float f0 = m0, f1 = m1, f2 = m2;
+    uint32_t u0, u1, u2;
+    std::memcpy(&u0, &f0, 4); std::memcpy(&u1, &f1, 4); std::memcpy(&u2, &f2, 4);
+    q[i] = int8_t(u0 & 0xFF);
+    q[M * K + i] = int8_t(u1 & 0xFF);
+    q[2 * M * K + i] = int8_t(u2 & 0xFF);
+  }
+}
+
+void check_i8x2(const char* name, int M, int N, int K) {
+  std::mt19937 rng(M * 3 + N * 7 + K);
+  std::uniform_real_distribution<float> u(-0.999f, 0.999f);
+  std::vector<float> ha(long(M) * K);
+  for (auto& v : ha) v = u(rng);
+  float* A;
+  TLG_CUDA(cudaMalloc(&A, ha.size() * 4));
+  TLG_CUDA(cudaMemcpy(A, ha.data(), ha.size() * 4, cudaMemcpyHostToDevice));
+  Buf B, bias;
+  B.init(long(N) * K, rng);
+  bias.init(N, rng);
+  double *ref, *refabs;
+  TLG_CUDA(cudaMalloc(&ref, long(M) * N * 8));
+  TLG_CUDA(cudaMalloc(&refabs, long(M) * N * 8));
+  ref_gemm<<<dim3((M + 127) / 128, N), 128>>>(A, K, false, B.x, K, false, M, N, K, ref, refabs);
+  std::vector<int8_t> hq;
+  host_act_pieces(ha, M, K, hq);
+  int8_t *aq, *wq;
+  float *scale, *out, *out_lo;
+  const long Kp = (K + 15) / 16 * 16;
+  TLG_CUDA(cudaMalloc(&aq, hq.size()));
+  TLG_CUDA(cudaMemcpy(aq, hq.data(), hq.size(), cudaMemcpyHostToDevice));
+  TLG_CUDA(cudaMalloc(&wq, 3 * long(N) * Kp));
+  TLG_CUDA(cudaMalloc(&scale, N * 4));
+  TLG_CUDA(cudaMalloc(&out, long(M) * N * 4));
+  TLG_CUDA(cudaMalloc(&out_lo, long(M) * N * 4));
+  gemm::launch_quantize_rows(B.x, N, K, K, wq, Kp, scale, 0);
+  auto run = [&] {
+    gemm::launch_i8x2_fwd(aq, wq, Kp, scale, bias.x, M, N, K, out, out_lo, N, nullptr, nullptr, 0,
+                          nullptr, 0);
+  };
+  run();
+  TLG_CUDA(cudaDeviceSynchronize());
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  for (int i = 0; i < 5; ++i) run();
+  cudaEventRecord(e1);
+  TLG_CUDA(cudaDeviceSynchronize());
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  ms /= 5;
+  std::vector<double> hr(long(M) * N), hab(long(M) * N);
+  std::vector<float> hh(long(M) * N), hl(long(M) * N), hbias(N);
+  TLG_CUDA(cudaMemcpy(hr.data(), ref, hr.size() * 8, cudaMemcpyDeviceToHost));
+  TLG_CUDA(cudaMemcpy(hab.data(), refabs, hab.size() * 8, cudaMemcpyDeviceToHost));
+  TLG_CUDA(cudaMemcpy(hh.data(), out, hh.size() * 4, cudaMemcpyDeviceToHost));
+  TLG_CUDA(cudaMemcpy(hl.data(), out_lo, hl.size() * 4, cudaMemcpyDeviceToHost));
+  TLG_CUDA(cudaMemcpy(hbias.data(), bias.x, N * 4, cudaMemcpyDeviceToHost));
+  double worst = 0;
+  long bad = 0;
+  for (long i = 0; i < long(M) * N; ++i) {
+    const int n = int(i % N);
+    double got = hh[i];
+    uint32_t bits;
+    std::memcpy(&bits, &hh[i], 4);
+    bits &= 0xFFFFE000u;
+    float th;
+    std::memcpy(&th, &bits, 4);
+    if (hl[i] != hh[i] - th) got = 1e9;
+    const double want = std::tanh(hr[i] + hbias[n]);
+    const double err = std::fabs(got - want) / (hab[i] + 1.0);
+    if (!(err <= 2e-6)) ++bad;
+    if (!(err <= worst)) worst = std::isfinite(err) ? std::max(worst, err) : 1e30;
+  }
+  const double tflops = 2.0 * M * N * K / (ms * 1e-3) / 1e12;
+  printf("%-34s M=%6d N=%5d K=%6d split=1 : worst rel %.3e bad %ld  %.3f ms %.1f TF/s  %s\n",
+         name, M, N, K, worst, bad, ms, tflops, bad ? "FAIL" : "ok");
+  if (bad) ++failures;
+  cudaFree(A); cudaFree(ref); cudaFree(refabs); cudaFree(aq); cudaFree(wq); cudaFree(scale);
+  cudaFree(out); cudaFree(out_lo); cudaFree(B.x); cudaFree(B.hi); cudaFree(B.lo); cudaFree(bias.x);
+  cudaFree(bias.hi); cudaFree(bias.lo);
+}
+
 int main(int argc, char** argv) {
   try {
     using namespace gemm;
@@ -377,12 +474,15 @@ int main(int argc, char** argv) {
     check_i8("I8 bits fwd", 300, 256, 200);
     check_i8("I8 bits fwd N=100 K=1936", 700, 100, 1936);
     check_i8("I8 bits fwd pair", 4096, 256, 1936);
+    check_i8x2("I8x2 fwd", 512, 256, 256);
+    check_i8x2("I8x2 fwd ragged", 700, 200, 96);
     check_i8_dw("I8 bits dW", 128, 200, 1000, 2);
     check_i8_dw("I8 bits dW pair", 256, 1936, 4096, 8);
     check_i8_dw("I8 bits dW ragged", 256, 300, 1300, 4);
     if (argc > 1) {
       check_i8("perf I8 bits fwd C3 L1", 131072, 256, 1936);
       check_i8_dw("perf I8 bits dW C3 L1", 256, 1936, 131072, 114);
+      check_i8x2("perf I8x2 fwd C3 L2", 131072, 256, 256);
       g_u8 = 1;
       check("perf U8 fwd C3 L1", 131072, 256, 1936, false, false, true, kEpiFwdTanh, 1);
       g_u8 = 2;
