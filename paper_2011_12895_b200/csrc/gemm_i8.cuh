@@ -215,8 +215,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
       uint32_t uph = 0;
       long issued = 0, done = 0;
       for (int t = cl_id; t < num_tiles; t += n_cl) {
-        const int nt = t % tm.n_tiles, mt = t / tm.n_tiles;
-        const int m0 = mt * kBM * CG + int(rank) * kBM;
+        const int nt = t % tm.n_tiles;
         const int n0 = nt * BN + int(rank) * S::kBN;
         for (int kb = 0; kb < kb_total; ++kb, ++done) {
           while (bt < num_tiles && issued < done + S::kRing) {
