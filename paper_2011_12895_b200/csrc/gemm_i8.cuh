@@ -648,19 +648,19 @@ __global__ void __launch_bounds__(32 * (2 + kEpiWarps), 1)
             wsm[k * 32 + lane] = wk;
           }
           __syncwarp();
+          // j-outer / k-inner: the head_k dot products advance together (independent
+          // FMA chains hide the latency; per k the summation order is unchanged)
 #pragma unroll
-          for (int k = 0; k < kHK; ++k) {
-            if (k < p.head_k) {
-              float z = zacc[k];
+          for (int j4 = 0; j4 < 8; ++j4) {
 #pragma unroll
-              for (int j4 = 0; j4 < 8; ++j4) {
+            for (int k = 0; k < kHK; ++k) {
+              if (k < p.head_k) {
                 const float4 w4 = *reinterpret_cast<const float4*>(wsm + k * 32 + 4 * j4);
-                z = fmaf(w4.x, o[4 * j4], z);
-                z = fmaf(w4.y, o[4 * j4 + 1], z);
-                z = fmaf(w4.z, o[4 * j4 + 2], z);
-                z = fmaf(w4.w, o[4 * j4 + 3], z);
+                zacc[k] = fmaf(w4.x, o[4 * j4], zacc[k]);
+                zacc[k] = fmaf(w4.y, o[4 * j4 + 1], zacc[k]);
+                zacc[k] = fmaf(w4.z, o[4 * j4 + 2], zacc[k]);
+                zacc[k] = fmaf(w4.w, o[4 * j4 + 3], zacc[k]);
               }
-              zacc[k] = z;
             }
           }
           __syncwarp();
