@@ -172,31 +172,44 @@ __global__ void __launch_bounds__(256) quantize_cols_kernel(const float* __restr
       inv[j] = mx > 0.f ? 127.f / mx : 1.f;  // the GEMM epilogue multiplies by mx / 127
       lim[j] = 127.f;
     }
-    for (long f = f0 + lane; f < min(F, f0 + kQRows); f += lanes) {
-      const float4 z = *reinterpret_cast<const float4*>(Z + f * ldz + m);
-      const float zv[4] = {z.x, z.y, z.z, z.w};
-      uint32_t w0 = 0, w1 = 0, w2 = 0;
-      // round-to-nearest-even via the 1.5 * 2^23 magic constant: the sum's low mantissa
-      // bits are the integer in two's complement (no F2I / FRND on the quarter-rate pipe)
-      constexpr float kMagic = 12582912.f;
+    const long fend = min(F, f0 + kQRows);
+    // four rows per round: their loads are in flight together
+    for (long fb = f0 + lane; fb < fend; fb += 4L * lanes) {
+      float4 zr[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        // x = z * (127 / max) rounds once (|x| <= 127 (1 + 2^-23)); the residual steps
-        // are exact (Sterbenz, power-of-two scaling)
-        const float x = fminf(fmaxf(zv[j] * inv[j], -lim[j]), lim[j]);
-        const float m0 = x + kMagic;
-        const float x1 = (x - (m0 - kMagic)) * 128.f;
-        const float m1 = x1 + kMagic;
-        const float x2 = (x1 - (m1 - kMagic)) * 128.f;
-        const float m2 = x2 + kMagic;
-        w0 |= (__float_as_uint(m0) & 0xFFu) << (8 * j);
-        w1 |= (__float_as_uint(m1) & 0xFFu) << (8 * j);
-        w2 |= (__float_as_uint(m2) & 0xFFu) << (8 * j);
+      for (int u = 0; u < 4; ++u) {
+        const long f = fb + long(u) * lanes;
+        zr[u] = f < fend ? *reinterpret_cast<const float4*>(Z + f * ldz + m)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      const long o = f * M + m;
-      *reinterpret_cast<uint32_t*>(P + o) = w0;
-      *reinterpret_cast<uint32_t*>(P + plane + o) = w1;
-      *reinterpret_cast<uint32_t*>(P + 2 * plane + o) = w2;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const long f = fb + long(u) * lanes;
+        if (f >= fend) break;
+        const float zv[4] = {zr[u].x, zr[u].y, zr[u].z, zr[u].w};
+        uint32_t w0 = 0, w1 = 0, w2 = 0;
+        // round-to-nearest-even via the 1.5 * 2^23 magic constant: the sum's low mantissa
+        // bits are the integer in two's complement (no F2I / FRND on the quarter-rate pipe)
+        constexpr float kMagic = 12582912.f;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          // x = z * (127 / max) rounds once (|x| <= 127 (1 + 2^-23)); the residual steps
+          // are exact (Sterbenz, power-of-two scaling)
+          const float x = fminf(fmaxf(zv[j] * inv[j], -lim[j]), lim[j]);
+          const float m0 = x + kMagic;
+          const float x1 = (x - (m0 - kMagic)) * 128.f;
+          const float m1 = x1 + kMagic;
+          const float x2 = (x1 - (m1 - kMagic)) * 128.f;
+          const float m2 = x2 + kMagic;
+          w0 |= (__float_as_uint(m0) & 0xFFu) << (8 * j);
+          w1 |= (__float_as_uint(m1) & 0xFFu) << (8 * j);
+          w2 |= (__float_as_uint(m2) & 0xFFu) << (8 * j);
+        }
+        const long o = f * M + m;
+        *reinterpret_cast<uint32_t*>(P + o) = w0;
+        *reinterpret_cast<uint32_t*>(P + plane + o) = w1;
+        *reinterpret_cast<uint32_t*>(P + 2 * plane + o) = w2;
+      }
     }
   }
 }

@@ -24,21 +24,40 @@ __global__ void expand_u8_kernel(const uchar4* __restrict__ in, float4* __restri
   }
 }
 
-// Bit rows of rowb bytes -> rows of `pitch` bytes (zero padded), 8 output bytes per thread.
-__global__ void repitch_bits_kernel(const uint8_t* __restrict__ bits, long rowb, long F,
-                                    uint8_t* __restrict__ out, long pitch) {
-  const long per_row = pitch / 8;
-  for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < F * per_row;
-       i += long(gridDim.x) * blockDim.x) {
-    const long f = i / per_row, j = (i % per_row) * 8;
-    const uint8_t* src = bits + f * rowb + j;
-    uint32_t lo = 0, hi = 0;
+// Bit rows of rowb bytes -> rows of `pitch` bytes (zero padded).  A block stages
+// kRepitchRows consecutive rows through shared memory with aligned 16-byte loads (the
+// source rows are only 2-byte aligned in general), then writes 16-byte chunks.
+constexpr int kRepitchRows = 64;
+__global__ void __launch_bounds__(256) repitch_bits_kernel(const uint8_t* __restrict__ bits,
+                                                           long rowb, long F,
+                                                           uint8_t* __restrict__ out, long pitch) {
+  extern __shared__ uint4 rp_smem[];
+  uint8_t* sb = reinterpret_cast<uint8_t*>(rp_smem);
+  const long f0 = long(blockIdx.x) * kRepitchRows;
+  const int rows = int(F - f0 < kRepitchRows ? F - f0 : long(kRepitchRows));
+  const uint8_t* src = bits + f0 * rowb;
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(src) & ~uintptr_t(15);
+  const int lead = int(reinterpret_cast<uintptr_t>(src) - a0);
+  const int n16 = (lead + rows * int(rowb) + 15) / 16;
+  // (the aligned 16-byte chunks stay inside the allocation's 256-byte granules)
+  for (int i = threadIdx.x; i < n16; i += blockDim.x)
+    rp_smem[i] = __ldg(reinterpret_cast<const uint4*>(a0) + i);
+  __syncthreads();
+  const int per_row = int(pitch / 16);
+  for (int i = threadIdx.x; i < rows * per_row; i += blockDim.x) {
+    const int r = i / per_row, j = (i % per_row) * 16;
+    uint32_t w[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      if (j + q < rowb) lo |= uint32_t(src[q]) << (8 * q);
-      if (j + 4 + q < rowb) hi |= uint32_t(src[4 + q]) << (8 * q);
+      uint32_t v = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int col = j + 4 * q + b;
+        if (col < rowb) v |= uint32_t(sb[lead + r * int(rowb) + col]) << (8 * b);
+      }
+      w[q] = v;
     }
-    *reinterpret_cast<uint2*>(out + f * pitch + j) = make_uint2(lo, hi);
+    *reinterpret_cast<uint4*>(out + (f0 + r) * pitch + j) = make_uint4(w[0], w[1], w[2], w[3]);
   }
 }
 
@@ -867,8 +886,11 @@ void launch_unpack_bits(const uint8_t* bits, long rowb, long F, long D, uint8_t*
                         uint8_t* pitched, long pitch,
                         cudaStream_t s) {
   if (out == nullptr) {  // only the re-pitched bit rows
-    if (pitch % 8 != 0) throw CudaError("bit-row pitch must be a multiple of 8");
-    repitch_bits_kernel<<<grid_for(F * (pitch / 8), 256), 256, 0, s>>>(bits, rowb, F, pitched, pitch);
+    if (pitch % 16 != 0) throw CudaError("bit-row pitch must be a multiple of 16");
+    const size_t smem = size_t(kRepitchRows * rowb + 32);
+    if (smem > 48 * 1024) throw CudaError("bit rows too long for the repitch kernel");
+    repitch_bits_kernel<<<ceil_div(F, kRepitchRows), 256, smem, s>>>(bits, rowb, F, pitched,
+                                                                     pitch);
     TLG_CHECK_LAUNCH();
     return;
   }
