@@ -108,6 +108,9 @@ typedef struct tlg_segment_batch {
   const uint8_t* done;          /* [S][T] */
   const float* bootstrap;       /* [S] */
   const int32_t* valid_steps;   /* [S] */
+  uint32_t obs_pitch;           /* TLG_OBS_BITS: bytes per frame row, >= ceil(obs_dim / 8);
+                                   0 = ceil(obs_dim / 8).  A multiple of 16 lets a device-
+                                   resident batch feed the int8 GEMM without re-pitching. */
 } tlg_segment_batch;
 
 /* rlmath::LossStats (rlmath.hpp:52-57) plus the loss itself (mean over the shard's

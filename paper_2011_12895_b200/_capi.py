@@ -77,7 +77,7 @@ class SegmentBatchC(C.Structure):
                 ("obs_dtype", C.c_uint32), ("obs", C.c_void_p), ("action", C.c_void_p),
                 ("reward", C.c_void_p), ("behavior_logp", C.c_void_p),
                 ("value_est", C.c_void_p), ("done", C.c_void_p), ("bootstrap", C.c_void_p),
-                ("valid_steps", C.c_void_p)]
+                ("valid_steps", C.c_void_p), ("obs_pitch", C.c_uint32)]
 
 
 class StepStats(C.Structure):
@@ -194,10 +194,17 @@ class SegmentBatchView:
 class DeviceSegmentBatch:
     """The same batch resident in HBM (torch tensors as device allocations)."""
 
-    def __init__(self, b, device=0, bits=False, obs_dim=None):
+    def __init__(self, b, device=0, bits=False, obs_dim=None, pitch=0):
+        """bits=True: b.obs holds bit-packed rows; pitch > 0 pads each frame row to `pitch`
+        bytes (a multiple of 16 feeds the int8 GEMM without re-pitching)."""
         import torch
         dev = torch.device("cuda", device)
         v = SegmentBatchView(b, bits=bits, obs_dim=obs_dim)
+        if bits and pitch:
+            o = v.arrs["obs"]
+            padded = np.zeros(o.shape[:-1] + (pitch,), np.uint8)
+            padded[..., :o.shape[-1]] = o
+            v.arrs["obs"] = padded
         self.t = {k: torch.from_numpy(a).to(dev) for k, a in v.arrs.items()}
         o = self.t["obs"]
         S, T = self.t["action"].shape
@@ -205,7 +212,7 @@ class DeviceSegmentBatch:
                                2 if bits else (1 if o.dtype == torch.uint8 else 0),
                                *(self.t[k].data_ptr() for k in (
                                    "obs", "action", "reward", "behavior_logp", "value_est",
-                                   "done", "bootstrap", "valid_steps")))
+                                   "done", "bootstrap", "valid_steps")), pitch if bits else 0)
 
 
 class Learner:

@@ -373,21 +373,37 @@ struct tlg_learner {
     bd.S = int(S);
     bd.T = T;
     if (b.obs_dtype == TLG_OBS_BITS) {
-      // bit-packed 0/1 planes (LSB first, ceil(D/8) bytes per frame): unpack to uint8
-      const long rowb = (D + 7) / 8;
+      // bit-packed 0/1 planes (LSB first, obs_pitch or ceil(D/8) bytes per frame)
+      const long rowb_min = (D + 7) / 8;
+      const long rowb = b.obs_pitch ? long(b.obs_pitch) : rowb_min;
+      if (rowb != rowb_min && rowb != bits_pitch)
+        throw InvalidArg("obs_pitch must be 0, ceil(obs_dim/8) or that rounded up to 16 bytes");
       const uint8_t* bits = static_cast<const uint8_t*>(b.obs);
+      const bool pitched = rowb == bits_pitch;  // rows already 16-B multiples
       if (!on_device) {
-        TLG_CUDA(cudaMemcpyAsync(obs_bits_lin, bits, size_t(F * rowb), cudaMemcpyHostToDevice,
+        uint8_t* dst = pitched ? obs_bits : obs_bits_lin;
+        TLG_CUDA(cudaMemcpyAsync(dst, bits, size_t(F * rowb), cudaMemcpyHostToDevice, stream));
+        bits = dst;
+      } else if (pitched && (internal || (reinterpret_cast<uintptr_t>(bits) & 15) != 0)) {
+        // graph replays read the learner's own buffer
+        TLG_CUDA(cudaMemcpyAsync(obs_bits, bits, size_t(F * rowb), cudaMemcpyDeviceToDevice,
                                  stream));
-        bits = obs_bits_lin;
+        bits = obs_bits;
       }
-      // one pass: rows re-pitched to 16 B for the int8 GEMM's TMA (pad bytes zero) and
-      // expanded to the uint8 planes the layer-1 dW reads
-      // (the uint8 planes are only needed by the tf32 layer-1 dW)
-      tlg::launch_unpack_bits(bits, rowb, F, D, i8_dw1() ? nullptr : obs_u8,
-                              i8_layer1() ? obs_bits : nullptr, bits_pitch, stream);
-      if (i8_layer1()) x0_bits = obs_bits;
-      ++launches;
+      if (pitched) {
+        if (i8_layer1()) x0_bits = bits;
+        if (!i8_dw1()) {  // the tf32 layer-1 dW (or a non-MLP family) reads uint8 planes
+          tlg::launch_unpack_bits(bits, rowb, F, D, obs_u8, nullptr, 0, stream);
+          ++launches;
+        }
+      } else {
+        // one pass: rows re-pitched to 16 B for the int8 GEMM's TMA (pad bytes zero) and,
+        // when the tf32 layer-1 dW runs, expanded to the uint8 planes it reads
+        tlg::launch_unpack_bits(bits, rowb, F, D, i8_dw1() ? nullptr : obs_u8,
+                                i8_layer1() ? obs_bits : nullptr, bits_pitch, stream);
+        if (i8_layer1()) x0_bits = obs_bits;
+        ++launches;
+      }
       tlg_segment_batch u = b;
       u.obs_dtype = TLG_OBS_U8;
       u.obs = obs_u8;
@@ -730,7 +746,8 @@ struct tlg_learner {
     const long S = b.n_segments, F = S * T, D = net.D;
     const size_t ob = b.obs_dtype == TLG_OBS_F32 ? size_t(F * D) * 4
                       : b.obs_dtype == TLG_OBS_U8 ? size_t(F * D)
-                                                  : size_t(F * ((D + 7) / 8));
+                                                  : size_t(F * (b.obs_pitch ? long(b.obs_pitch)
+                                                                             : (D + 7) / 8));
     if (!sl.ready) {
       TLG_CUDA(cudaEventCreateWithFlags(&sl.ready, cudaEventDisableTiming));
       TLG_CUDA(cudaEventCreateWithFlags(&sl.consumed, cudaEventDisableTiming));

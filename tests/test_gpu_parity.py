@@ -400,7 +400,7 @@ def test_bit_packed_and_staged_inputs_match(tlg, oracle, D, hidden):
     batches = [tlg.synth.make_segments(S, T, D, A, seed=70 + k, obs_kind="binary", obs_u8=True)
                for k in range(3)]
     res = []
-    for mode in ("u8", "bits", "staged"):
+    for mode in ("u8", "bits", "staged", "device-pitched"):
         # SGD: parameter differences stay proportional to gradient differences (Adam's
         # normalised first steps turn a sign flip of a ~0 gradient into a full lr move)
         lrn = tlg.Learner("mlp", D, A, hidden, max_segments=S, unroll_len=T, obs_u8=True,
@@ -418,6 +418,10 @@ def test_bit_packed_and_staged_inputs_match(tlg, oracle, D, hidden):
                 views.append(v)
                 if mode == "bits":
                     lrn.train_step(v)
+                elif mode == "device-pitched":  # HBM-resident rows padded to 16 B
+                    pitch = ((D + 7) // 8 + 15) // 16 * 16
+                    dv = tlg.DeviceSegmentBatch(pb, 0, bits=True, obs_dim=D, pitch=pitch)
+                    lrn.train_step(dv, on_device=True)
         if mode == "staged":
             lrn.stage(views[0])
             for k in range(len(views)):
@@ -426,6 +430,7 @@ def test_bit_packed_and_staged_inputs_match(tlg, oracle, D, hidden):
                 lrn.train_staged()
         res.append(lrn.get_params())
     assert np.array_equal(res[1], res[2])
+    assert np.array_equal(res[1], res[3])
     if len(hidden) == 1:
         assert np.array_equal(res[0], res[1])
     else:
