@@ -214,7 +214,7 @@ LaunchInfo launch(const Operand& A, const Operand& B, int M, int N, int K, int e
   // else 128 (short-K fused epilogues are the critical path; narrower tiles balance).
   int BN = N > 128 ? 256 : N > 64 ? 128 : 64;
   const int kb_tile = p.kb_per_split;  // K blocks per tile
-  if (BN == 256 && epi != kEpiStore && kb_tile < 16) BN = 128;
+  if (BN == 256 && epi != kEpiStore && kb_tile < 16 && !std::getenv("TLG_GEMM_WIDE")) BN = 128;
   if (const char* e = std::getenv("TLG_GEMM_MAX_BN")) {  // tuning experiments only
     const int cap = std::atoi(e);
     while (BN > 64 && BN > cap) BN /= 2;
