@@ -295,15 +295,15 @@ def main():
 
     # ---- per-kernel CUDA-event times from separate instrumented (eager) steps
     lrn.set_timing(True)
-    kern = {"fwd1": [], "dw1": [], "fwd2": [], "dw2": [], "dx2": [], "phases": []}
+    # every trunk GEMM: (kind, layer) -> CUDA-event ms per step
+    gemms = [(k, l) for l in range(len(hidden)) for k in ("fwd", "dw", "dx")
+             if not (k == "dx" and l == 0)]
+    kern = {g: [] for g in gemms}
+    kern["phases"] = []
     for i in range(max(5, args.steps // 2)):
         lrn.train_step(dev[i % nb], on_device=True)
-        kern["fwd1"].append(lrn.kernel_ms("fwd", 0))
-        kern["dw1"].append(lrn.kernel_ms("dw", 0))
-        if len(hidden) > 1:
-            kern["fwd2"].append(lrn.kernel_ms("fwd", 1))
-            kern["dw2"].append(lrn.kernel_ms("dw", 1))
-            kern["dx2"].append(lrn.kernel_ms("dx", 1))
+        for g in gemms:
+            kern[g].append(lrn.kernel_ms(*g))
         kern["phases"].append(lrn.phase_ms())
     lrn.set_timing(False)
 
@@ -375,36 +375,50 @@ def main():
     # ---- roofline of the dominant kernel (layer-1 forward GEMM)
     peaks, peak_src = measured_peaks()
     F = S * T
-    flops_fwd1 = 2.0 * F * hidden[0] * D
-    t_fwd1 = float(np.mean(kern["fwd1"])) / 1e3
-    t_dw1 = float(np.mean(kern["dw1"])) / 1e3
+    dims = [D] + list(hidden)
+    gflops = {(k, l): 2.0 * F * dims[l] * dims[l + 1] for (k, l) in gemms}
+    gms = {g: float(np.mean(kern[g])) for g in gemms}
+    flops_fwd1 = gflops[("fwd", 0)]
+    t_fwd1 = gms[("fwd", 0)] / 1e3
+    t_dw1 = gms[("dw", 0)] / 1e3
     peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
     ph = np.mean(np.array(kern["phases"]), axis=0)
     step_ms = float(ph[6])
-    # the dominant kernel of the step: the layer-1 forward or the layer-1 weight gradient
-    # (same algorithmic FLOPs, 2 F h1 D)
-    dom = "dw1" if t_dw1 >= t_fwd1 else "fwd1"
-    t_dom = max(t_dw1, t_fwd1)
-    achieved = flops_fwd1 / t_dom / 1e12
+    # the dominant kernel of the step: the trunk GEMM with the longest CUDA-event time
+    dom_g = max(gemms, key=lambda g: gms[g])
+    dom = {("fwd", 0): "fwd1", ("dw", 0): "dw1"}.get(dom_g, f"{dom_g[0]}{dom_g[1] + 1}")
+    t_dom = gms[dom_g] / 1e3
+    achieved = gflops[dom_g] / t_dom / 1e12
     desc = {
         "fwd1": ("gemm_i8_bits_fwd_kernel layer-1 forward (tcgen05.mma kind::i8: bit-packed "
                  "binary planes x 3 fixed-point int8 weight pieces, exact int32 accumulate)"
                  if obs_bits else
                  "gemm_tf32x3_kernel layer-1 forward (tcgen05.mma kind::tf32, obs exact -> "
                  "2 MMA passes)"),
-        "dw1": "gemm_tf32x3_kernel layer-1 dW = dZ1^T X (tcgen05.mma kind::tf32, MN-major "
-               "operands, uint8 planes converted in smem, 2 MMA passes, split-K)",
-    }[dom]
-    bytes_dom = (F * D // (8 if obs_bits else 1) + 3 * hidden[0] * D + 2 * 4 * F * hidden[0]
-                 if dom == "fwd1" else
-                 2 * 4 * F * hidden[0] + F * D + 4 * hidden[0] * D)
+        "dw1": ("gemm_i8_bits_dw_kernel layer-1 dW = dZ1^T X (tcgen05.mma kind::i8: "
+                "fixed-point dZ1 pieces x bit-packed planes, split-K)" if obs_bits else
+                "gemm_tf32x3_kernel layer-1 dW = dZ1^T X (tcgen05.mma kind::tf32, MN-major "
+                "operands, split-K)"),
+    }.get(dom, f"gemm_tf32x3_kernel layer-{dom_g[1] + 1} {dom_g[0]} (tcgen05.mma kind::tf32, "
+               f"3xTF32, {dims[dom_g[1]]}->{dims[dom_g[1] + 1]})")
+    li, lo_ = dims[dom_g[1]], dims[dom_g[1] + 1]
+    if dom == "fwd1":
+        bytes_dom = F * D // (8 if obs_bits else 1) + 3 * hidden[0] * D + 2 * 4 * F * hidden[0]
+    elif dom == "dw1":
+        bytes_dom = 3 * F * hidden[0] + F * D // (8 if obs_bits else 1) + 4 * hidden[0] * D
+    elif dom_g[0] == "fwd":
+        bytes_dom = 8 * F * li + 8 * F * lo_ + 8 * li * lo_
+    elif dom_g[0] == "dx":
+        bytes_dom = 8 * F * lo_ + 4 * F * li + 8 * F * li + 8 * li * lo_
+    else:
+        bytes_dom = 8 * F * lo_ + 8 * F * li + 4 * li * lo_
     roofline = {
         "kernel": desc,
         "algorithmic_bytes_per_launch": bytes_dom,
         "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
         "frac": achieved / peak, "traffic": _ncu_traffic(dom),
         "peak_source": f"{peak_src} bf16_tflops_sustained (MEASURED_PEAKS.json)",
-        "algorithmic_flops_per_launch": flops_fwd1,
+        "algorithmic_flops_per_launch": gflops[dom_g],
         "ms_per_launch": t_dom * 1e3,
         "share_of_step": t_dom * 1e3 / step_ms,
         "note": "fp32-exact: 3xTF32 split (tf32 dense ceiling = half the bf16 peak, 2-3 MMA "
@@ -417,9 +431,7 @@ def main():
                       "bwd": float(ph[3]), "allreduce": float(ph[4]), "optimizer": float(ph[5]),
                       "step": step_ms},
     }
-    if kern["fwd2"]:
-        kernels.update(fwd2_ms=float(np.mean(kern["fwd2"])), dw2_ms=float(np.mean(kern["dw2"])),
-                       dx2_ms=float(np.mean(kern["dx2"])))
+    kernels["gemm_ms"] = {f"{k}{l + 1}": gms[(k, l)] for (k, l) in gemms}
     total_flops = cfg.flops_per_frame() * F
     kernels["step_tflops"] = total_flops / (ms_per_step / 1e3) / 1e12
 

@@ -535,15 +535,16 @@ struct tlg_learner {
         p.head_k = int(net.A) + 1;
         p.head_part = head_part;
       }
+      if (l == 0 && sg.x0_bits != nullptr && !wq_fresh) {
+        // this step's layer-1 weights -> int8 pieces (once per step)
+        tlg::gemm::launch_quantize_rows(params + net.w_off[0], outw, in, in, wq, wq_kp, wq_scale,
+                                        stream);
+        wq_fresh = true;
+        ++launches;
+      }
       if (shard == 0) kmark(0, int(l), 0);
       int bn;
       if (l == 0 && sg.x0_bits != nullptr) {
-        if (!wq_fresh) {  // this step's layer-1 weights -> pieces (once per step)
-          tlg::gemm::launch_quantize_rows(params + net.w_off[0], outw, in, in, wq, wq_kp, wq_scale,
-                                          stream);
-          wq_fresh = true;
-          ++launches;
-        }
         // binary planes x int8 weight pieces: exact integer tensor-core GEMM (+ the
         // activations as int8 pieces when layer 2 takes the int8 path too)
         bn = tlg::gemm::launch_i8_bits_fwd(sg.x0_bits, bits_pitch, wq, wq_kp, wq_scale, p.bias,
