@@ -137,6 +137,12 @@ void tlg_learner_destroy(tlg_learner* l);
 size_t tlg_learner_param_count(const tlg_learner* l);
 /* f64 -> device f32; also resets the optimizer state (StartPeriod). */
 int tlg_learner_set_params(tlg_learner* l, const double* values, size_t n);
+/* Teacher policy for the PPO KL penalty (rlmath.cpp:116-185, PpoLossAndGrad's `teacher`;
+ * hyper kl_teacher_coef): f64 flat blob of the same shape; NULL clears it.  Without a
+ * teacher, kl_teacher_coef > 0 fails the step with TLG_INVALID_ARGUMENT
+ * ("teacher params required when kl_teacher_coef > 0", rlmath.cpp:119-120).  The V-trace
+ * (PG) loss has no KL term, as in the reference. */
+int tlg_learner_set_teacher(tlg_learner* l, const double* values, size_t n);
 int tlg_learner_get_params(tlg_learner* l, double* values, size_t n);
 int tlg_learner_set_hyper(tlg_learner* l, const tlg_hyper* hp);
 /* Multi-GPU: join an NCCL communicator of `nranks` learner shards (one process or

@@ -105,7 +105,8 @@ def lib():
         L.tlg_learner_destroy.argtypes = [C.c_void_p]
         L.tlg_learner_param_count.restype = C.c_size_t
         L.tlg_learner_param_count.argtypes = [C.c_void_p]
-        for fn in ("tlg_learner_set_params", "tlg_learner_get_params", "tlg_learner_get_grad"):
+        for fn in ("tlg_learner_set_params", "tlg_learner_get_params", "tlg_learner_get_grad",
+                   "tlg_learner_set_teacher"):
             getattr(L, fn).argtypes = [C.c_void_p, C.c_void_p, C.c_size_t]
         L.tlg_learner_set_hyper.argtypes = [C.c_void_p, C.POINTER(Hyper)]
         L.tlg_comm_unique_id.argtypes = [C.c_void_p]
@@ -152,6 +153,7 @@ def check(rc):
 EXPORTS = [
     "tlg_last_error", "tlg_version", "tlg_host_alloc", "tlg_host_free", "tlg_learner_create", "tlg_learner_destroy",
     "tlg_learner_param_count", "tlg_learner_set_params", "tlg_learner_get_params",
+    "tlg_learner_set_teacher",
     "tlg_learner_set_hyper", "tlg_comm_unique_id", "tlg_learner_comm_init",
     "tlg_learner_train_step", "tlg_learner_train_step_shards", "tlg_learner_get_grad",
     "tlg_learner_stage", "tlg_learner_train_staged", "tlg_learner_get_returns",
@@ -246,6 +248,14 @@ class Learner:
         out = np.zeros(self.n_params)
         check(lib().tlg_learner_get_params(self.h, out.ctypes.data, out.size))
         return out
+
+    def set_teacher(self, values):
+        """Teacher policy for the PPO KL term (None clears it)."""
+        if values is None:
+            check(lib().tlg_learner_set_teacher(self.h, None, 0))
+            return
+        v = np.ascontiguousarray(values, np.float64)
+        check(lib().tlg_learner_set_teacher(self.h, v.ctypes.data, v.size))
 
     def get_grad(self):
         out = np.zeros(self.n_params)

@@ -187,6 +187,14 @@ struct tlg_learner {
   // activations
   std::vector<float*> act, act_lo, dz, dz_lo;
   float *head_out, *head_part, *tlogp, *adv, *target, *dzh;
+  // teacher policy for the PPO KL term (rlmath.cpp:145-155; tlg_learner_set_teacher)
+  float* teacher = nullptr;
+  float* teacher_lo = nullptr;
+  float* t_head_out = nullptr;
+  bool has_teacher = false;
+  // the reference's learner passes no teacher (learner.cpp:127); with one set, PPO losses
+  // carry the KL term (V-trace's PgLossAndGrad has none, rlmath.cpp:187-222)
+  bool teacher_active() const { return has_teacher && cfg.algo != TLG_ALGO_VTRACE; }
   double* seg_partial;
   tlg::StepStatsDev* stats;
   int* err;
@@ -499,6 +507,72 @@ struct tlg_learner {
     compute_shard(stage_shard(b, on_device, false), shard, gtarget);
   }
 
+  // Trunk forward + policy/value heads with the parameter set P (the student's, or a
+  // teacher's for the KL term, rlmath.cpp:145-155): head outputs [F][A+1] -> out,
+  // log-prob of the taken action -> out_tlogp (may be null).
+  void forward_heads(const Staged& sg, const float* P, const float* P_lo, const float* x0,
+                     const float* x0_lo, float* out, float* out_tlogp, bool timed) {
+    const tlg::BatchDev bd = sg.bd;
+    const long F = long(bd.S) * T;
+    // ---- forward trunk
+    using tlg::gemm::Operand;
+    for (uint32_t l = 0; l < net.L; ++l) {
+      const int in = int(net.dims[l]), outw = int(net.dims[l + 1]);
+      Operand A{l == 0 ? x0 : act[l - 1], l == 0 ? x0_lo : act_lo[l - 1], in, false,
+                l == 0 ? x0_u8 : nullptr};
+      Operand B{P + net.w_off[l], P_lo + net.w_off[l], in, false};
+      tlg::gemm::Params p{};
+      p.out_hi = act[l];
+      // the top layer's residual plane has no reader (heads and loss read the full plane)
+      p.out_lo = l + 1 == net.L ? nullptr : act_lo[l];
+      p.ldo = outw;
+      p.bias = P + net.b_off[l];
+      const bool fuse_head = l + 1 == net.L && fused_head();
+      if (fuse_head) {  // policy/value heads in the last trunk GEMM's epilogue
+        p.head_w = P + net.head.wpi;
+        p.head_wv = P + net.head.wv;
+        p.head_k = int(net.A) + 1;
+        p.head_part = head_part;
+      }
+      if (l == 0 && sg.x0_bits != nullptr && !wq_fresh) {
+        // this step's layer-1 weights -> int8 pieces (once per step)
+        tlg::gemm::launch_quantize_rows(P + net.w_off[0], outw, in, in, wq, wq_kp, wq_scale,
+                                        stream);
+        wq_fresh = true;
+        ++launches;
+      }
+      if (timed) kmark(0, int(l), 0);
+      int bn;
+      if (l == 0 && sg.x0_bits != nullptr) {
+        // binary planes x int8 weight pieces: exact integer tensor-core GEMM (+ the
+        // activations as int8 pieces when layer 2 takes the int8 path too)
+        bn = tlg::gemm::launch_i8_bits_fwd(sg.x0_bits, bits_pitch, wq, wq_kp, wq_scale, p.bias,
+                                           int(F), outw, in, act[0], act_lo[0], outw, stream,
+                                           i8_fwd2(F) ? act_q : nullptr).bn;
+      } else if (l == 1 && sg.x0_bits != nullptr && i8_fwd2(F)) {
+        tlg::gemm::launch_quantize_rows(P + net.w_off[1], outw, in, in, w2q, in, w2_scale,
+                                        stream);
+        ++launches;
+        bn = tlg::gemm::launch_i8x2_fwd(act_q, w2q, in, w2_scale, p.bias, int(F), outw, in,
+                                        act[1], p.out_lo, outw, p.head_w, p.head_wv, p.head_k,
+                                        p.head_part, stream).bn;
+      } else {
+        bn = tlg::gemm::launch(A, B, int(F), outw, in, tlg::gemm::kEpiFwdTanh, p, 1, stream).bn;
+      }
+      if (timed) kmark(0, int(l), 1);
+      if (fuse_head) head_tiles = (outw + bn - 1) / bn;
+      ++launches;
+    }
+    const float* hL = net.L ? act[net.L - 1] : x0;
+    const long ldh = net.head.H;
+    if (net.L > 0 && fused_head())
+      tlg::launch_head_finalize(net.head, P, head_part, head_tiles, F, &bd, out, out_tlogp,
+                                nullptr, nullptr, nullptr, err, stream);
+    else
+      tlg::launch_head_forward(net.head, P, hL, ldh, &bd, F, out, out_tlogp, nullptr, err, stream);
+    launches += 1;
+  }
+
   void compute_shard(const Staged& sg, int shard, float* gtarget) {
     tlg::StepStatsDev* st = stats + shard;
     const tlg::BatchDev bd = sg.bd;
@@ -515,67 +589,19 @@ struct tlg_learner {
       x0_lo = obs_lo;
     }
     if (shard == 0) mark(1);
-    // ---- forward trunk
-    using tlg::gemm::Operand;
-    for (uint32_t l = 0; l < net.L; ++l) {
-      const int in = int(net.dims[l]), outw = int(net.dims[l + 1]);
-      Operand A{l == 0 ? x0 : act[l - 1], l == 0 ? x0_lo : act_lo[l - 1], in, false,
-                l == 0 ? x0_u8 : nullptr};
-      Operand B{params + net.w_off[l], params_lo + net.w_off[l], in, false};
-      tlg::gemm::Params p{};
-      p.out_hi = act[l];
-      // the top layer's residual plane has no reader (heads and loss read the full plane)
-      p.out_lo = l + 1 == net.L ? nullptr : act_lo[l];
-      p.ldo = outw;
-      p.bias = params + net.b_off[l];
-      const bool fuse_head = l + 1 == net.L && fused_head();
-      if (fuse_head) {  // policy/value heads in the last trunk GEMM's epilogue
-        p.head_w = params + net.head.wpi;
-        p.head_wv = params + net.head.wv;
-        p.head_k = int(net.A) + 1;
-        p.head_part = head_part;
-      }
-      if (l == 0 && sg.x0_bits != nullptr && !wq_fresh) {
-        // this step's layer-1 weights -> int8 pieces (once per step)
-        tlg::gemm::launch_quantize_rows(params + net.w_off[0], outw, in, in, wq, wq_kp, wq_scale,
-                                        stream);
-        wq_fresh = true;
-        ++launches;
-      }
-      if (shard == 0) kmark(0, int(l), 0);
-      int bn;
-      if (l == 0 && sg.x0_bits != nullptr) {
-        // binary planes x int8 weight pieces: exact integer tensor-core GEMM (+ the
-        // activations as int8 pieces when layer 2 takes the int8 path too)
-        bn = tlg::gemm::launch_i8_bits_fwd(sg.x0_bits, bits_pitch, wq, wq_kp, wq_scale, p.bias,
-                                           int(F), outw, in, act[0], act_lo[0], outw, stream,
-                                           i8_fwd2(F) ? act_q : nullptr).bn;
-      } else if (l == 1 && sg.x0_bits != nullptr && i8_fwd2(F)) {
-        tlg::gemm::launch_quantize_rows(params + net.w_off[1], outw, in, in, w2q, in, w2_scale,
-                                        stream);
-        ++launches;
-        bn = tlg::gemm::launch_i8x2_fwd(act_q, w2q, in, w2_scale, p.bias, int(F), outw, in,
-                                        act[1], p.out_lo, outw, p.head_w, p.head_wv, p.head_k,
-                                        p.head_part, stream).bn;
-      } else {
-        bn = tlg::gemm::launch(A, B, int(F), outw, in, tlg::gemm::kEpiFwdTanh, p, 1, stream).bn;
-      }
-      if (shard == 0) kmark(0, int(l), 1);
-      if (fuse_head) head_tiles = (outw + bn - 1) / bn;
-      ++launches;
+    if (teacher_active()) {
+      // the teacher's head outputs first (the student's forward then reuses the buffers)
+      forward_heads(sg, teacher, teacher_lo, x0, x0_lo, t_head_out, nullptr, false);
+      wq_fresh = false;  // layer-1 int8 pieces must be rebuilt from the student's weights
     }
+    forward_heads(sg, params, params_lo, x0, x0_lo, head_out, tlogp, shard == 0);
     if (shard == 0) mark(2);
     // ---- heads, returns, loss
     const float* hL = net.L ? act[net.L - 1] : x0;
     const long ldh = net.head.H;
-    if (net.L > 0 && fused_head())
-      tlg::launch_head_finalize(net.head, params, head_part, head_tiles, F, &bd, head_out, tlogp,
-                                nullptr, nullptr, nullptr, err, stream);
-    else
-      tlg::launch_head_forward(net.head, params, hL, ldh, &bd, F, head_out, tlogp, nullptr, err,
-                               stream);
     tlg::HyperDev hd{float(hp.gamma), float(hp.lam), float(hp.clip_eps), float(hp.vf_coef),
-                     float(hp.ent_coef), float(hp.rho_bar), float(hp.c_bar), hp.adv_norm};
+                     float(hp.ent_coef), float(hp.rho_bar), float(hp.c_bar), hp.adv_norm,
+                     float(hp.kl_teacher_coef)};
     const int algo = int(cfg.algo);
     tlg::launch_returns(bd, algo, hd, tlogp, adv, target, seg_partial, err, stream);
     tlg::launch_finalize_adv(seg_partial, bd, hp.adv_norm, st, err, stream);
@@ -583,9 +609,9 @@ struct tlg_learner {
     const tlg::LossLaunch ll = tlg::launch_loss_backward(
         net.head, params, hL, ldh, bd, head_out, adv, target, st, hd, loss_kind, dzh,
         net.L ? dz[net.L - 1] : nullptr, net.L ? dz_lo[net.L - 1] : nullptr, hg_partial,
-        loss_partial, col_partial, stream);
+        loss_partial, col_partial, stream, teacher_active() ? t_head_out : nullptr);
     tlg::launch_head_grad_reduce(net.head, hg_partial, loss_partial, ll, gtarget, st, stream);
-    launches += 7;
+    launches += 6;
     if (net.L > 0) {  // db of the top trunk layer from the loss kernel's column partials
       tlg::launch_rows_reduce(col_partial, ll.stream_blocks, net.head.H, net.head.H,
                               gtarget + net.b_off[net.L - 1], stream);
@@ -593,6 +619,7 @@ struct tlg_learner {
     }
     if (shard == 0) mark(3);
     // ---- backward trunk
+    using tlg::gemm::Operand;
     for (int l = int(net.L) - 1; l >= 0; --l) {
       const int in = int(net.dims[l]), outw = int(net.dims[l + 1]);
       const float* xin = l == 0 ? x0 : act[l - 1];
@@ -685,6 +712,9 @@ struct tlg_learner {
   void step(const tlg_segment_batch* bs, int n, int on_device, tlg_step_stats* out,
             cudaEvent_t consumed = nullptr) {
     if (!hp_set) throw InvalidArg("hyperparameters not set");
+    // PpoLossAndGrad (rlmath.cpp:119-120); the PG (V-trace) loss takes no teacher
+    if (hp.kl_teacher_coef > 0.0 && cfg.algo != TLG_ALGO_VTRACE && !has_teacher)
+      throw InvalidArg("teacher params required when kl_teacher_coef > 0");
     if (n < 1 || n > kMaxLocalShards) throw InvalidArg("1..64 local shards per call");
     launches = 0;
     TLG_CUDA(cudaSetDevice(cfg.device));
@@ -1091,6 +1121,25 @@ int tlg_learner_set_params(tlg_learner* l, const double* values, size_t n) {
   });
 }
 
+int tlg_learner_set_teacher(tlg_learner* l, const double* values, size_t n) {
+  return Guard([&] {
+    TLG_CUDA(cudaSetDevice(l->cfg.device));
+    if (values == nullptr) {
+      l->has_teacher = false;
+    } else {
+      if (!l->teacher) {
+        l->teacher = l->mem.add<float>(l->P_pad);
+        l->teacher_lo = l->mem.add<float>(l->P_pad);
+        l->t_head_out = l->mem.add<float>(l->F_max * (l->net.A + 1));
+      }
+      set_params_common(l->teacher, l->teacher_lo, l->net.P, l->P_pad, values, n, l->stream);
+      TLG_CUDA(cudaStreamSynchronize(l->stream));
+      l->has_teacher = true;
+    }
+    ++l->hyper_version;  // captured graphs include (or not) the teacher pass
+  });
+}
+
 int tlg_learner_get_params(tlg_learner* l, double* values, size_t n) {
   return Guard([&] {
     if (long(n) != l->net.P) throw InvalidArg("parameter count mismatch");
@@ -1134,8 +1183,7 @@ int tlg_learner_set_hyper(tlg_learner* l, const tlg_hyper* hp) {
     if (!(hp->clip_eps > 0)) throw InvalidArg("hyperparams: clip_eps must be > 0");
     if (!(hp->rho_bar > 0) || !(hp->c_bar > 0) || hp->c_bar > hp->rho_bar)
       throw InvalidArg("hyperparams: need 0 < c_bar <= rho_bar");
-    if (hp->kl_teacher_coef > 0)
-      throw InvalidArg("teacher params required when kl_teacher_coef > 0");
+    if (!(hp->kl_teacher_coef >= 0)) throw InvalidArg("kl_teacher_coef must be >= 0");
     l->hp = *hp;
     l->hp_set = true;
     ++l->hyper_version;

@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(256) loss_math_kernel(
     HeadDesc hd, BatchDev b, const float* __restrict__ head_out, const float* __restrict__ adv,
     const float* __restrict__ target, const StepStatsDev* __restrict__ st, HyperDev hp,
     int loss_kind, float* __restrict__ dzh, double* __restrict__ loss_partial,
-    float* __restrict__ bias_partial) {
+    float* __restrict__ bias_partial, const float* __restrict__ teacher_out) {
   __shared__ double red[5][8];
   __shared__ float bred[kMaxA1][8];
   const int A = hd.A, A1 = A + 1;
@@ -454,6 +454,28 @@ __global__ void __launch_bounds__(256) loss_math_kernel(
       if (k < A && pk[k] > 0.f) ent -= pk[k] * lpk[k];  // Entropy (rlmath.cpp:36-41)
     }
     const int a = min(max(b.action[f], 0), A - 1);  // out-of-range is flagged by K3a
+    // teacher KL (rlmath.cpp:145-155, 177-178): KL(p || q) with q the teacher's policy
+    float lq[kMaxA1], kl = 0.f;
+    const bool kl_on = loss_kind == 0 && teacher_out != nullptr;
+    if (kl_on) {
+      float tz[kMaxA1];
+#pragma unroll
+      for (int k = 0; k < kMaxA1; ++k) tz[k] = k < A ? teacher_out[f * A1 + k] : 0.f;
+      float tmx = -INFINITY;
+#pragma unroll
+      for (int k = 0; k < kMaxA1; ++k)
+        if (k < A) tmx = fmaxf(tmx, tz[k]);
+      float tse = 0.f;
+#pragma unroll
+      for (int k = 0; k < kMaxA1; ++k)
+        if (k < A) tse += expf(tz[k] - tmx);
+      const float tlse = tmx + logf(tse);
+#pragma unroll
+      for (int k = 0; k < kMaxA1; ++k) {
+        lq[k] = tz[k] - tlse;
+        if (k < A && pk[k] > 0.f) kl += pk[k] * (lpk[k] - lq[k]);
+      }
+    }
     float logp = 0.f, V = 0.f;
 #pragma unroll
     for (int k = 0; k < kMaxA1; ++k) {
@@ -468,13 +490,16 @@ __global__ void __launch_bounds__(256) loss_math_kernel(
       const float clipped = fminf(fmaxf(ratio, 1.f - hp.clip_eps), 1.f + hp.clip_eps);
       const float t1 = ratio * ad, t2 = clipped * ad;
       loss_i = -fminf(t1, t2) + hp.vf_coef * verr * verr - hp.ent_coef * ent;
+      if (kl_on) loss_i += hp.kl_coef * kl;
       if (t2 < t1) l_clip = 1.0;
       const bool surr = t1 <= t2;  // gradient only when the unclipped term is active
 #pragma unroll
       for (int k = 0; k < kMaxA1; ++k)
         if (k < A) {
-          float g = hp.ent_coef * pk[k] * ((pk[k] > 0.f ? lpk[k] : 0.f) + ent);
+          const float lpz = pk[k] > 0.f ? lpk[k] : 0.f;
+          float g = hp.ent_coef * pk[k] * (lpz + ent);
           if (surr) g += -ad * ratio * ((k == a ? 1.f : 0.f) - pk[k]);
+          if (kl_on) g += hp.kl_coef * pk[k] * (lpz - lq[k] - kl);
           d[k] = g * inv_n;
         }
     } else {
@@ -952,7 +977,7 @@ LossLaunch launch_loss_backward(const HeadDesc& hd, const float* params, const f
                                 const float* adv, const float* target, const StepStatsDev* st,
                                 const HyperDev& hp, int loss_kind, float* dzh, float* dz,
                                 float* dz_lo, float* hg_partial, double* loss_partial,
-                                float* db_partial, cudaStream_t s) {
+                                float* db_partial, cudaStream_t s, const float* teacher_out) {
   const long F = long(b.S) * b.T;
   const int A1 = hd.A + 1;
   const long nw = long(A1) * hd.H;
@@ -968,11 +993,12 @@ LossLaunch launch_loss_backward(const HeadDesc& hd, const float* params, const f
   float* bias_partial = hg_partial + long(ll.stream_blocks) * nw;
   if (A1 <= 8)
     loss_math_kernel<8><<<ll.math_blocks, 256, 0, s>>>(hd, b, head_out, adv, target, st, hp,
-                                                       loss_kind, dzh, loss_partial, bias_partial);
+                                                       loss_kind, dzh, loss_partial, bias_partial,
+                                                       teacher_out);
   else
     loss_math_kernel<32><<<ll.math_blocks, 256, 0, s>>>(hd, b, head_out, adv, target, st, hp,
                                                         loss_kind, dzh, loss_partial,
-                                                        bias_partial);
+                                                        bias_partial, teacher_out);
   TLG_CHECK_LAUNCH();
   if (vec) {
     loss_stream4_kernel<8><<<dim3(ll.stream_blocks, slabs), 256, 0, s>>>(

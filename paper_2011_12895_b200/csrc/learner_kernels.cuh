@@ -53,6 +53,7 @@ struct BatchDev {
 struct HyperDev {
   float gamma, lam, clip_eps, vf_coef, ent_coef, rho_bar, c_bar;
   int adv_norm;
+  float kl_coef;  // kl_teacher_coef (PPO with a teacher)
 };
 
 // Device-side per-step statistics (written by finalize kernels, read once by host).
@@ -96,7 +97,8 @@ LossLaunch launch_loss_backward(const HeadDesc& hd, const float* params, const f
                                 const float* adv, const float* target, const StepStatsDev* st,
                                 const HyperDev& hp, int loss_kind, float* dzh, float* dz,
                                 float* dz_lo, float* hg_partial, double* loss_partial,
-                                float* db_partial, cudaStream_t s);
+                                float* db_partial, cudaStream_t s,
+                                const float* teacher_out = nullptr);
 void launch_head_grad_reduce(const HeadDesc& hd, const float* hg_partial,
                              const double* loss_partial, const LossLaunch& ll, float* grad,
                              StepStatsDev* st, cudaStream_t s);

@@ -513,3 +513,55 @@ def test_staged_f32_inputs_match_train_step(tlg, oracle, monkeypatch, no_graph):
         res.append((lrn.get_params(), stats))
     assert np.array_equal(res[0][0], res[1][0])
     assert res[0][1] == res[1][1]
+
+
+@pytest.mark.parametrize("case", [("mlp", 16, (32, 32), "gauss"), ("linear", 10, (), "gauss"),
+                                  ("mlp", 200, (64, 32), "bits")],
+                         ids=["mlp", "linear", "mlp-bits-int8"])
+def test_teacher_kl_term_matches_oracle(tlg, oracle, case):
+    """PPO with a teacher policy (PpoLossAndGrad's KL penalty, rlmath.cpp:145-155, 177-178):
+    loss and gradient against the fp64 oracle's loss over the same returns."""
+    from paper_2011_12895_b200._capi import SegmentBatchView
+    family, D, hidden, obs_kind = case
+    S, T, A = 12, 8, 6
+    shape = Shape(FAM[family], D, A, hidden)
+    hp = dict(learning_rate=0.05, batch_size=S, unroll_len=T, kl_teacher_coef=0.7,
+              ent_coef=0.02)
+    lrn = tlg.Learner(family, D, A, hidden, optimizer="sgd", max_segments=S, unroll_len=T,
+                      obs_u8=obs_kind == "bits")
+    lrn.set_hyper(**hp)
+    p = init_params(oracle, shape, seed=21)
+    teacher = init_params(oracle, shape, seed=22)
+    lrn.set_params(p)
+    if obs_kind == "bits":
+        b = tlg.synth.make_segments(S, T, D, A, seed=77, obs_kind="binary", obs_u8=True)
+        pb = b.slice(0, S)
+        pb.obs = tlg.synth.pack_bits(b.obs)
+        view = SegmentBatchView(pb, bits=True, obs_dim=D)
+    else:
+        b = make_batch(tlg, S, T, D, A, seed=77, family=family)
+        view = b
+    with pytest.raises(tlg.InvalidArgument, match="teacher params required"):
+        lrn.train_step(view)
+    lrn.set_teacher(teacher)
+    st = lrn.train_step(view)
+    g = lrn.get_grad()
+    ohp = OHyper(**hp)
+    ob = to_oracle(b)
+    adv, tgt = oracle.shard_returns(shape, p, ohp, ALGO["ppo"], ob)
+    sel = [(s, t) for s in range(S) for t in range(int(b.valid_steps[s]))]
+    obs = np.stack([np.asarray(b.obs[s, t], np.float64) for s, t in sel])
+    act = np.array([b.action[s, t] for s, t in sel])
+    blogp = np.array([b.behavior_logp[s, t] for s, t in sel], np.float64)
+    ost, og = oracle.ppo_loss_grad(shape, p, obs, act, blogp, np.array([adv[s, t] for s, t in sel]),
+                                   np.array([tgt[s, t] for s, t in sel]), ohp, teacher=teacher)
+    for k in ("loss", "entropy", "value_loss", "mean_ratio", "clip_fraction"):
+        assert close(st[k], ost[k], 1e-4), (k, st[k], ost[k])
+    gscale = max(1e-30, float(np.max(np.abs(og))))
+    assert np.max(np.abs(g - og)) <= 1e-4 * gscale, np.max(np.abs(g - og)) / gscale
+    # the KL term is live: the same step without the teacher's penalty differs
+    lrn.set_teacher(None)
+    lrn.set_hyper(**dict(hp, kl_teacher_coef=0.0))
+    lrn.set_params(p)
+    lrn.train_step(view)
+    assert np.max(np.abs(lrn.get_grad() - og)) > 1e-3 * gscale
