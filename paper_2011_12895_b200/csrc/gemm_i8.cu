@@ -39,10 +39,10 @@ CUtensorMap make_f32_out_map(float* base, long n, long m, long ld) {
   return t;
 }
 
-template <int BN, int CG>
+template <int BN, int CG, int MC = 1>
 void run_i8_fwd(const CUtensorMap& tb, const CUtensorMap& tq, const CUtensorMap& to,
                 const CUtensorMap& tl, const I8Params& p, const TileMap& tm, cudaStream_t stream) {
-  auto kern = gemm_i8_bits_fwd_kernel<BN, CG>;
+  auto kern = gemm_i8_bits_fwd_kernel<BN, CG, MC>;
   constexpr int bytes = SmemI8<BN, CG>::kBytes;
   static_assert(bytes <= 227 * 1024, "shared memory budget");
   static bool attr = false;
@@ -55,13 +55,14 @@ void run_i8_fwd(const CUtensorMap& tb, const CUtensorMap& tq, const CUtensorMap&
     kern<<<std::min(tiles, num_sms()), kThreadsI8, bytes, stream>>>(tb, tq, to, tl, p, tm);
   } else {
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(2 * std::min(tiles, num_sms() / 2));
+    constexpr int kCl = CG * MC;
+    cfg.gridDim = dim3(kCl * std::min(tiles, num_sms() / kCl));
     cfg.blockDim = dim3(kThreadsI8);
     cfg.dynamicSmemBytes = bytes;
     cfg.stream = stream;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.x = kCl;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
@@ -338,19 +339,27 @@ LaunchInfo launch_i8_bits_fwd(const uint8_t* bits, long rowb, const int8_t* q, l
   // CTA pairs (256-row tiles) whenever there are enough of them to fill the GPU
   int cg = (M >= 2 * kBM && long(ceil_div(M, 2 * kBM)) * ceil_div(N, BN) >= num_sms() / 2) ? 2 : 1;
   if (const char* e = std::getenv("TLG_I8_CG")) cg = std::atoi(e) == 2 ? 2 : 1;
+  // TLG_I8_MC=2: two CTA pairs per cluster share the weight-piece tiles (TMA multicast).
+  // Correct, but measured 1.9x slower at C3 (the pairs run in lockstep on the shared
+  // stages), so single pairs stay the default.
+  int mc = 1;
+  if (const char* e = std::getenv("TLG_I8_MC"))
+    mc = cg == 2 && std::atoi(e) == 2 && M >= 4 * kBM ? 2 : 1;
   if (out_q != nullptr && (N % 32 != 0 || (reinterpret_cast<uintptr_t>(out_q) & 15) != 0))
     throw CudaError("gemm_i8: int8 activation pieces need N % 32 == 0 and 16-B alignment");
   I8Params p{M, N, K, scale, bias, N, out_q};
-  const TileMap tm{ceil_div(M, kBM * cg), ceil_div(N, BN), 1};
+  const TileMap tm{ceil_div(M, kBM * cg * mc), ceil_div(N, BN), 1};
   // bit rows: box {16 bytes = 128 elements, 128 rows}; pieces: box {128, BN / cg}, SW128
   const CUtensorMap tb = make_bytes_map(bits, rowb, M, rowb, kBKi / 8, kBM, CU_TENSOR_MAP_SWIZZLE_NONE);
   const CUtensorMap tq = make_bytes_map(q, Kp, 3L * N, Kp, kBKi, BN / cg, CU_TENSOR_MAP_SWIZZLE_128B);
   const CUtensorMap to = make_f32_out_map(out, N, M, ldo);
   const CUtensorMap tl = make_f32_out_map(out_lo, N, M, ldo);
-  if (cg == 2) run_i8_fwd<BN, 2>(tb, tq, to, tl, p, tm, stream);
+  if (mc == 2) run_i8_fwd<BN, 2, 2>(tb, tq, to, tl, p, tm, stream);
+  else if (cg == 2) run_i8_fwd<BN, 2>(tb, tq, to, tl, p, tm, stream);
   else run_i8_fwd<BN, 1>(tb, tq, to, tl, p, tm, stream);
   const int tiles = tm.m_tiles * tm.n_tiles;
-  return {BN, cg == 2 ? 2 * std::min(tiles, num_sms() / 2) : std::min(tiles, num_sms())};
+  const int cl = cg * mc;
+  return {BN, cl * std::min(tiles, num_sms() / cl)};
 }
 
 }  // namespace tlg::gemm

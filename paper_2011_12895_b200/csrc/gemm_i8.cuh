@@ -115,6 +115,30 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t a, uint64_t b, 
         "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
+// shared::cluster address of the same smem offset in CTA `r` of the cluster
+__device__ __forceinline__ uint32_t map_rank(uint32_t addr, uint32_t r) {
+  uint32_t out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(addr), "r"(r));
+  return out;
+}
+// TMA into this smem offset of every CTA in `mask`, each completion counted on the
+// destination pair leader's mbarrier (cta_group::2)
+__device__ __forceinline__ void tma_load_2d_pair_mc(uint32_t dst, const CUtensorMap* map, int x,
+                                                    int y, uint32_t leader_bar, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(leader_bar), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_pair_mask(uint32_t bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(bar),
+      "h"(mask)
+      : "memory");
+}
+
 // 4 bits (LSB first) -> 4 bytes of 0/1
 __device__ __forceinline__ uint32_t spread4(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
 
@@ -137,7 +161,10 @@ __device__ __forceinline__ void expand_bit_row(const uint8_t* src, uint8_t* x_ti
   }
 }
 
-template <int BN, int CG>
+// MC == 2 (CG == 2 only): clusters of two CTA pairs stacked along M (512-row tiles)
+// sharing each weight-piece tile: pair 0 TMA-multicasts it into both pairs' smem, halving
+// the L2->SM piece traffic that bounds this kernel.
+template <int BN, int CG, int MC = 1>
 __global__ void __launch_bounds__(kThreadsI8, 1)
     gemm_i8_bits_fwd_kernel(const __grid_constant__ CUtensorMap tmBits,
                             const __grid_constant__ CUtensorMap tmQ,
@@ -145,9 +172,16 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                             const __grid_constant__ CUtensorMap tmOutLo, const I8Params p,
                             const TileMap tm) {
   using S = SmemI8<BN, CG>;
-  const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
-  const int cl_id = CG == 2 ? int(blockIdx.x >> 1) : int(blockIdx.x);
-  const int n_cl = CG == 2 ? int(gridDim.x >> 1) : int(gridDim.x);
+  static_assert(MC == 1 || CG == 2, "multicast pairs need CTA pairs");
+  constexpr int kCl = CG * MC;                      // CTAs per cluster
+  const uint32_t crank = CG == 2 ? cluster_rank() : 0u;
+  const uint32_t rank = crank & 1u;                 // rank within the pair
+  const uint32_t pair = crank >> 1;                 // pair within the cluster (MC == 2)
+  const uint32_t leader = crank & ~1u;              // this pair's leader CTA
+  const int cl_id = int(blockIdx.x) / kCl;
+  const int n_cl = int(gridDim.x) / kCl;
+  constexpr int kRowsT = kBM * CG * MC;             // rows per tile
+  auto to_leader = [&](uint32_t a) { return MC == 2 ? map_rank(a, leader) : map_rank0(a); };
   extern __shared__ uint8_t smem_raw[];
   // 1 KB-aligned base by pointer arithmetic on the __shared__ array (an integer round
   // trip would turn every staging access into a generic LD/ST)
@@ -174,7 +208,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
     for (int s = 0; s < S::kStages; ++s) {
       mbar_init(bar_full + 8 * s, 1);
       mbar_init(bar_conv + 8 * s, kConvWarps * CG);
-      mbar_init(bar_empty + 8 * s, 1);
+      mbar_init(bar_empty + 8 * s, MC);  // every pair whose MMAs read the shared pieces
     }
     for (int u = 0; u < S::kRing; ++u) {
       mbar_init(bar_ufull + 8 * u, 1);
@@ -221,7 +255,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
           while (bt < num_tiles && issued < done + S::kRing) {
             mbar_wait(bar_uempty + 8 * ui, uph ^ 1);
             mbar_expect_tx(bar_ufull + 8 * ui, S::kBits);
-            const int bm0 = (bt / tm.n_tiles) * kBM * CG + int(rank) * kBM;
+            const int bm0 = (bt / tm.n_tiles) * kRowsT + int(pair) * kBM * CG + int(rank) * kBM;
             tma_load_2d(sbase + S::kRingOff + ui * S::kBits, &tmBits, bkb * (kBKi / 8), bm0,
                         bar_ufull + 8 * ui);
             ++issued;
@@ -236,13 +270,20 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
           }
           mbar_wait(bar_empty + 8 * stage, phase ^ 1);
           const uint32_t st = sbase + stage * S::kStage;
-          const uint32_t full = CG == 2 ? map_rank0(bar_full + 8 * stage) : bar_full + 8 * stage;
+          const uint32_t full = CG == 2 ? to_leader(bar_full + 8 * stage) : bar_full + 8 * stage;
           if (rank == 0) mbar_expect_tx(bar_full + 8 * stage, 3 * S::kQ * CG);
+          if (MC == 1 || pair == 0) {
 #pragma unroll
-          for (int pc = 0; pc < 3; ++pc) {
-            const int row = pc * int(p.q_rows) + n0;
-            if (CG == 2) tma_load_2d_pair(st + kOffQ + pc * S::kQ, &tmQ, kb * kBKi, row, full);
-            else tma_load_2d(st + kOffQ + pc * S::kQ, &tmQ, kb * kBKi, row, full);
+            for (int pc = 0; pc < 3; ++pc) {
+              const int row = pc * int(p.q_rows) + n0;
+              if (MC == 2)
+                tma_load_2d_pair_mc(st + kOffQ + pc * S::kQ, &tmQ, kb * kBKi, row, full,
+                                    uint16_t((1u << rank) | (1u << (rank + 2))));
+              else if (CG == 2)
+                tma_load_2d_pair(st + kOffQ + pc * S::kQ, &tmQ, kb * kBKi, row, full);
+              else
+                tma_load_2d(st + kOffQ + pc * S::kQ, &tmQ, kb * kBKi, row, full);
+            }
           }
           if (++stage == S::kStages) {
             stage = 0;
@@ -282,14 +323,16 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
             mma_i8<CG>(tacc_a, dx, dq1, idesc, 1u);
             mma_i8<CG>(tacc_b, dx, dq2, idesc, acc);
           }
-          if (CG == 2) mma_commit_pair(bar_empty + 8 * stage);
+          if (MC == 2) mma_commit_pair_mask(bar_empty + 8 * stage, uint16_t(0xF));
+          else if (CG == 2) mma_commit_pair(bar_empty + 8 * stage);
           else mma_commit(bar_empty + 8 * stage);
           if (++stage == S::kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        if (CG == 2) mma_commit_pair(bar_tfull + 8 * acc_buf);
+        if (MC == 2) mma_commit_pair_mask(bar_tfull + 8 * acc_buf, uint16_t(3u << leader));
+        else if (CG == 2) mma_commit_pair(bar_tfull + 8 * acc_buf);
         else mma_commit(bar_tfull + 8 * acc_buf);
       }
     }
@@ -309,7 +352,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
         fence_async_smem();
         __syncwarp();
         if (lane == 0) {
-          if (CG == 2) mbar_arrive_cluster(map_rank0(bar_conv + 8 * stage));
+          if (CG == 2) mbar_arrive_cluster(to_leader(bar_conv + 8 * stage));
           else mbar_arrive(bar_conv + 8 * stage);
           mbar_arrive(bar_uempty + 8 * ui);
         }
@@ -332,7 +375,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
     int it = 0;
     for (int t = cl_id; t < num_tiles; t += n_cl, ++it) {
       const int nt = t % tm.n_tiles, mt = t / tm.n_tiles;
-      const int m0 = mt * kBM * CG + int(rank) * kBM, n0 = nt * BN;
+      const int m0 = mt * kRowsT + int(pair) * kBM * CG + int(rank) * kBM, n0 = nt * BN;
       const int rbase = m0 + q * 32;
       const int acc_buf = it & 1;
       mbar_wait(bar_tfull + 8 * acc_buf, (it >> 1) & 1);
@@ -394,7 +437,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if (CG == 2) mbar_arrive_cluster(map_rank0(bar_tempty + 8 * acc_buf));
+        if (CG == 2) mbar_arrive_cluster(to_leader(bar_tempty + 8 * acc_buf));
         else mbar_arrive(bar_tempty + 8 * acc_buf);
       }
     }
