@@ -170,6 +170,22 @@ int tlg_learner_train_step_shards(tlg_learner* l, const tlg_segment_batch* shard
  * overlaps step k; tlg_learner_train_staged runs one step on the oldest staged batch. */
 int tlg_learner_stage(tlg_learner* l, const tlg_segment_batch* host_batch);
 int tlg_learner_train_staged(tlg_learner* l, tlg_step_stats* stats);
+
+/* Device-resident replay: segments are copied to HBM once, at ingest,
+ * into `capacity` slots; a training step then names its segments by slot and the batch
+ * is gathered on the device (replay_mem.cpp:14-49 keeps the draw decisions on the host:
+ * the caller maps its draw to slots).  obs_dtype: TLG_OBS_F32 or TLG_OBS_BITS (rows
+ * stored 16-byte pitched).  tlg_replay_put copies b->n_segments host segments into
+ * slots[0..n); tlg_learner_train_step_replay runs one step over n_shards shards of
+ * `per_shard` slots each (slots[r * per_shard + i], the reference's shard slices,
+ * learner.cpp:122-124) and writes stats[n_shards]; results equal
+ * tlg_learner_train_step_shards on the same segments. */
+typedef struct tlg_replay tlg_replay;
+int tlg_replay_create(tlg_learner* l, uint32_t capacity, uint32_t obs_dtype, tlg_replay** out);
+void tlg_replay_destroy(tlg_replay* r);
+int tlg_replay_put(tlg_replay* r, const uint32_t* slots, const tlg_segment_batch* host_batch);
+int tlg_learner_train_step_replay(tlg_learner* l, tlg_replay* r, const uint32_t* slots,
+                                  uint32_t n_shards, uint32_t per_shard, tlg_step_stats* stats);
 /* The averaged gradient of the last step (f32 -> f64), for parity checks. */
 int tlg_learner_get_grad(tlg_learner* l, double* out, size_t n);
 /* Per-frame advantages / value targets of the last step ([S][T], f32, padding = 0). */

@@ -109,6 +109,11 @@ def lib():
                    "tlg_learner_set_teacher"):
             getattr(L, fn).argtypes = [C.c_void_p, C.c_void_p, C.c_size_t]
         L.tlg_learner_set_hyper.argtypes = [C.c_void_p, C.POINTER(Hyper)]
+        L.tlg_replay_create.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.POINTER(C.c_void_p)]
+        L.tlg_replay_destroy.argtypes = [C.c_void_p]
+        L.tlg_replay_put.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(SegmentBatchC)]
+        L.tlg_learner_train_step_replay.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p,
+                                                    C.c_uint32, C.c_uint32, C.c_void_p]
         L.tlg_comm_unique_id.argtypes = [C.c_void_p]
         L.tlg_learner_comm_init.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int]
         L.tlg_learner_train_step.argtypes = [C.c_void_p, C.POINTER(SegmentBatchC), C.c_int,
@@ -153,7 +158,8 @@ def check(rc):
 EXPORTS = [
     "tlg_last_error", "tlg_version", "tlg_host_alloc", "tlg_host_free", "tlg_learner_create", "tlg_learner_destroy",
     "tlg_learner_param_count", "tlg_learner_set_params", "tlg_learner_get_params",
-    "tlg_learner_set_teacher",
+    "tlg_learner_set_teacher", "tlg_replay_create", "tlg_replay_destroy", "tlg_replay_put",
+    "tlg_learner_train_step_replay",
     "tlg_learner_set_hyper", "tlg_comm_unique_id", "tlg_learner_comm_init",
     "tlg_learner_train_step", "tlg_learner_train_step_shards", "tlg_learner_get_grad",
     "tlg_learner_stage", "tlg_learner_train_staged", "tlg_learner_get_returns",
@@ -323,6 +329,38 @@ class Learner:
         check(lib().tlg_learner_kernel_ms(self.h, {"fwd": 0, "dw": 1, "dx": 2}[kind], layer,
                                           C.byref(ms)))
         return ms.value
+
+
+class Replay:
+    """Device-resident replay ring of `capacity` segment slots (tlg_replay_*)."""
+
+    def __init__(self, learner, capacity, bits=False):
+        h = C.c_void_p()
+        check(lib().tlg_replay_create(learner.h, capacity, 2 if bits else 0, C.byref(h)))
+        self.h = h
+        self.learner = learner  # keeps the learner alive
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().tlg_replay_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def put(self, slots, batch):
+        """Copy the batch's segments (a SegmentBatchView or SegmentBatch) into `slots`."""
+        view = batch if isinstance(batch, SegmentBatchView) else SegmentBatchView(batch)
+        sl = np.ascontiguousarray(slots, np.uint32)
+        check(lib().tlg_replay_put(self.h, sl.ctypes.data, C.byref(view.c)))
+
+    def train_step(self, slots, n_shards=1):
+        """One learner step over n_shards shards of len(slots) // n_shards slots each;
+        returns the per-shard statistics."""
+        sl = np.ascontiguousarray(slots, np.uint32)
+        sts = (StepStats * n_shards)()
+        check(lib().tlg_learner_train_step_replay(self.learner.h, self.h, sl.ctypes.data,
+                                                  n_shards, sl.size // n_shards, sts))
+        return [s.as_dict() for s in sts]
 
 
 def comm_unique_id() -> bytes:

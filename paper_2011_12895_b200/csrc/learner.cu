@@ -1218,6 +1218,145 @@ int tlg_learner_comm_init(tlg_learner* l, const uint8_t unique_id[128], int nran
   });
 }
 
+// ---------------------------------------------------------------------------
+// Device-resident replay ring
+struct tlg_replay {
+  tlg_learner* l = nullptr;
+  uint32_t cap = 0, dtype = 0;
+  long rowb = 0;  // bytes per frame row in the ring and the gathered batches
+  DevFree mem;
+  tlg::SegArrays ring{}, stage{}, gath{};
+  long stage_segs = 0, stage_rowb = 0, gath_segs = 0;
+  uint32_t *d_put_slots = nullptr, *d_gather_slots = nullptr;
+  long put_slots_cap = 0, gather_slots_cap = 0;
+
+  tlg::SegArrays alloc(long segs, long rb) {
+    const int T = l->T;
+    tlg::SegArrays a{};
+    a.obs = mem.add<uint8_t>(segs * T * rb + 16);
+    a.action = mem.add<int32_t>(segs * T);
+    a.reward = mem.add<float>(segs * T);
+    a.blogp = mem.add<float>(segs * T);
+    a.value = mem.add<float>(segs * T);
+    a.done = mem.add<uint8_t>(segs * T);
+    a.boot = mem.add<float>(segs);
+    a.valid = mem.add<int32_t>(segs);
+    return a;
+  }
+  uint32_t* slots_to_device(uint32_t*& buf, long& capn, const uint32_t* h, long n) {
+    for (long i = 0; i < n; ++i)
+      if (h[i] >= cap) throw InvalidArg("replay slot out of range");
+    if (capn < n) {
+      buf = mem.add<uint32_t>(n);
+      capn = n;
+    }
+    TLG_CUDA(cudaMemcpyAsync(buf, h, n * 4, cudaMemcpyHostToDevice, l->stream));
+    return buf;
+  }
+};
+
+int tlg_replay_create(tlg_learner* l, uint32_t capacity, uint32_t obs_dtype, tlg_replay** out) {
+  return Guard([&] {
+    if (!l || !out) throw InvalidArg("null argument");
+    if (capacity == 0) throw InvalidArg("replay capacity must be >= 1");
+    if (obs_dtype != TLG_OBS_F32 && obs_dtype != TLG_OBS_BITS)
+      throw InvalidArg("device replay stores fp32 or bit-packed observations");
+    if (obs_dtype == TLG_OBS_BITS && l->obs_bits == nullptr)
+      throw InvalidArg("learner not configured for bit-packed observations");
+    TLG_CUDA(cudaSetDevice(l->cfg.device));
+    auto r = std::make_unique<tlg_replay>();
+    r->l = l;
+    r->cap = capacity;
+    r->dtype = obs_dtype;
+    r->rowb = obs_dtype == TLG_OBS_BITS ? l->bits_pitch : long(l->net.D) * 4;
+    r->ring = r->alloc(capacity, r->rowb);
+    *out = r.release();
+  });
+}
+
+void tlg_replay_destroy(tlg_replay* r) {
+  if (r && r->l && r->l->stream) cudaStreamSynchronize(r->l->stream);
+  delete r;
+}
+
+int tlg_replay_put(tlg_replay* r, const uint32_t* slots, const tlg_segment_batch* b) {
+  return Guard([&] {
+    if (!r || !slots || !b) throw InvalidArg("null argument");
+    tlg_learner* l = r->l;
+    TLG_CUDA(cudaSetDevice(l->cfg.device));
+    const int T = l->T;
+    const long n = b->n_segments, D = l->net.D;
+    if (n == 0) return;
+    if (int(b->unroll_len) != T) throw InvalidArg("unroll_len mismatch");
+    if (b->obs_dim != l->net.D) throw InvalidArg("observation size does not match policy shape");
+    if (b->obs_dtype != r->dtype) throw InvalidArg("observation format differs from the replay's");
+    const long src_rowb = r->dtype == TLG_OBS_BITS
+                              ? (b->obs_pitch ? long(b->obs_pitch) : (D + 7) / 8)
+                              : D * 4;
+    if (r->dtype == TLG_OBS_BITS && (src_rowb < (D + 7) / 8 || src_rowb > r->rowb))
+      throw InvalidArg("bad obs_pitch");
+    if (r->stage_segs < n || r->stage_rowb < src_rowb) {
+      r->stage = r->alloc(n, std::max(src_rowb, r->rowb));
+      r->stage_segs = n;
+      r->stage_rowb = std::max(src_rowb, r->rowb);
+    }
+    const long F = n * T;
+    auto h2d = [&](void* dst, const void* src, size_t bytes) {
+      TLG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, l->stream));
+    };
+    h2d(r->stage.obs, b->obs, size_t(F * src_rowb));
+    h2d(r->stage.action, b->action, F * 4);
+    h2d(r->stage.reward, b->reward, F * 4);
+    h2d(r->stage.blogp, b->behavior_logp, F * 4);
+    h2d(r->stage.value, b->value_est, F * 4);
+    h2d(r->stage.done, b->done, F);
+    h2d(r->stage.boot, b->bootstrap, n * 4);
+    h2d(r->stage.valid, b->valid_steps, n * 4);
+    const uint32_t* ds = r->slots_to_device(r->d_put_slots, r->put_slots_cap, slots, n);
+    tlg::launch_replay_move(r->stage, src_rowb, r->ring, r->rowb, ds, int(n), T, true, l->stream);
+    TLG_CUDA(cudaStreamSynchronize(l->stream));  // the host batch may be reused on return
+  });
+}
+
+int tlg_learner_train_step_replay(tlg_learner* l, tlg_replay* r, const uint32_t* slots,
+                                  uint32_t n_shards, uint32_t per_shard, tlg_step_stats* stats) {
+  return Guard([&] {
+    if (!l || !r || !slots) throw InvalidArg("null argument");
+    if (r->l != l) throw InvalidArg("replay belongs to another learner");
+    if (n_shards == 0 || per_shard == 0) throw InvalidArg("empty minibatch");
+    if (int(per_shard) > l->S_max) throw InvalidArg("batch exceeds the learner's max_segments");
+    TLG_CUDA(cudaSetDevice(l->cfg.device));
+    const long total = long(n_shards) * per_shard;
+    const int T = l->T;
+    if (r->gath_segs < total) {
+      r->gath = r->alloc(total, r->rowb);
+      r->gath_segs = total;
+    }
+    const uint32_t* ds = r->slots_to_device(r->d_gather_slots, r->gather_slots_cap, slots, total);
+    tlg::launch_replay_move(r->ring, r->rowb, r->gath, r->rowb, ds, int(total), T, false,
+                            l->stream);
+    std::vector<tlg_segment_batch> bs(n_shards);
+    for (uint32_t k = 0; k < n_shards; ++k) {
+      const long s0 = long(k) * per_shard, f0 = s0 * T;
+      tlg_segment_batch& b = bs[k];
+      b.n_segments = per_shard;
+      b.unroll_len = T;
+      b.obs_dim = l->net.D;
+      b.obs_dtype = r->dtype;
+      b.obs_pitch = r->dtype == TLG_OBS_BITS ? uint32_t(r->rowb) : 0;
+      b.obs = r->gath.obs + f0 * r->rowb;
+      b.action = r->gath.action + f0;
+      b.reward = r->gath.reward + f0;
+      b.behavior_logp = r->gath.blogp + f0;
+      b.value_est = r->gath.value + f0;
+      b.done = r->gath.done + f0;
+      b.bootstrap = r->gath.boot + s0;
+      b.valid_steps = r->gath.valid + s0;
+    }
+    l->step(bs.data(), int(n_shards), /*on_device=*/1, stats);
+  });
+}
+
 int tlg_learner_train_step(tlg_learner* l, const tlg_segment_batch* batch, int on_device,
                            tlg_step_stats* stats) {
   return Guard([&] {

@@ -907,6 +907,47 @@ void launch_expand_u8(const uint8_t* in, float* out, long n, cudaStream_t s) {
   TLG_CHECK_LAUNCH();
 }
 
+// block per segment: scatter (contiguous i -> slot[i]) or gather (slot[i] -> contiguous i)
+__global__ void __launch_bounds__(256) replay_move_kernel(SegArrays src, long src_rowb,
+                                                          SegArrays dst, long dst_rowb,
+                                                          const uint32_t* __restrict__ slots,
+                                                          int T, int scatter) {
+  const long i = blockIdx.x;
+  const long si = scatter ? i : long(slots[i]);
+  const long di = scatter ? long(slots[i]) : i;
+  const uint8_t* so = src.obs + si * T * src_rowb;
+  uint8_t* d_o = dst.obs + di * T * dst_rowb;
+  if (src_rowb == dst_rowb && (src_rowb & 15) == 0 &&
+      ((reinterpret_cast<uintptr_t>(so) | reinterpret_cast<uintptr_t>(d_o)) & 15) == 0) {
+    const long n16 = T * src_rowb / 16;
+    for (long k = threadIdx.x; k < n16; k += blockDim.x)
+      reinterpret_cast<uint4*>(d_o)[k] = reinterpret_cast<const uint4*>(so)[k];
+  } else {
+    for (long k = threadIdx.x; k < T * dst_rowb; k += blockDim.x) {
+      const long t = k / dst_rowb, j = k % dst_rowb;
+      d_o[k] = j < src_rowb ? so[t * src_rowb + j] : uint8_t(0);
+    }
+  }
+  for (int t = threadIdx.x; t < T; t += blockDim.x) {
+    dst.action[di * T + t] = src.action[si * T + t];
+    dst.reward[di * T + t] = src.reward[si * T + t];
+    dst.blogp[di * T + t] = src.blogp[si * T + t];
+    dst.value[di * T + t] = src.value[si * T + t];
+    dst.done[di * T + t] = src.done[si * T + t];
+  }
+  if (threadIdx.x == 0) {
+    dst.boot[di] = src.boot[si];
+    dst.valid[di] = src.valid[si];
+  }
+}
+
+void launch_replay_move(const SegArrays& src, long src_rowb, const SegArrays& dst, long dst_rowb,
+                        const uint32_t* slots, int n, int T, bool scatter, cudaStream_t s) {
+  if (n <= 0) return;
+  replay_move_kernel<<<n, 256, 0, s>>>(src, src_rowb, dst, dst_rowb, slots, T, scatter ? 1 : 0);
+  TLG_CHECK_LAUNCH();
+}
+
 void launch_unpack_bits(const uint8_t* bits, long rowb, long F, long D, uint8_t* out,
                         uint8_t* pitched, long pitch,
                         cudaStream_t s) {

@@ -70,6 +70,20 @@ constexpr int kLossBlocks = 444;  // persistent loss_backward blocks (3 per SM):
 
 void launch_expand_u8(const uint8_t* in, float* out, long n, cudaStream_t s);
 void launch_split_lo(const float* x, float* lo, long n, cudaStream_t s);
+// Device-resident replay (learner.cu tlg_replay): scatter n segments of a contiguous
+// staged batch into ring slots, or gather slots into a contiguous batch.  obs rows are
+// copied byte-exactly (src_rowb -> dst_rowb bytes per frame, zero padded).
+struct SegArrays {
+  uint8_t* obs;
+  int32_t* action;
+  float *reward, *blogp, *value;
+  uint8_t* done;
+  float* boot;
+  int32_t* valid;
+};
+void launch_replay_move(const SegArrays& src, long src_rowb, const SegArrays& dst, long dst_rowb,
+                        const uint32_t* slots, int n, int T, bool scatter, cudaStream_t s);
+
 void launch_unpack_bits(const uint8_t* bits, long rowb, long F, long D, uint8_t* out,
                         uint8_t* pitched, long pitch,
                         cudaStream_t s);

@@ -565,3 +565,62 @@ def test_teacher_kl_term_matches_oracle(tlg, oracle, case):
     lrn.set_params(p)
     lrn.train_step(view)
     assert np.max(np.abs(lrn.get_grad() - og)) > 1e-3 * gscale
+
+
+@pytest.mark.parametrize("fmt", ["f32", "bits"])
+def test_device_replay_matches_host_batches(tlg, oracle, fmt):
+    """Segments ingested once into the device replay ring and gathered by slot give
+    bit-identical steps to the same segments passed as host shard batches."""
+    from paper_2011_12895_b200._capi import SegmentBatchView
+    S, T, A = 16, 8, 6
+    D, hidden = (64, (32, 32)) if fmt == "f32" else (200, (64, 32))
+    bits = fmt == "bits"
+    p = init_params(oracle, Shape(2, D, A, hidden), 31)
+    rng = np.random.default_rng(5)
+    pool = [tlg.synth.make_segments(S, T, D, A, seed=900 + k,
+                                    obs_kind="binary" if bits else "gauss", obs_u8=bits)
+            for k in range(3)]
+
+    def view(b):
+        if not bits:
+            return SegmentBatchView(b)
+        pb = b.slice(0, b.n_segments)
+        pb.obs = tlg.synth.pack_bits(b.obs)
+        return SegmentBatchView(pb, bits=True, obs_dim=D)
+
+    def concat(parts):
+        return tlg.synth.SegmentBatch(*(np.concatenate([getattr(q, k) for q in parts]) for k in (
+            "obs", "action", "reward", "behavior_logp", "value_est", "done", "bootstrap",
+            "valid_steps")))
+
+    allsegs = concat(pool)                      # 3 S segments
+    cap = 4 * S
+    slot_of = rng.permutation(cap)[:3 * S]      # where each segment lives in the ring
+    draws = [rng.permutation(3 * S)[:2 * S] for _ in range(3)]
+    fields = ("obs", "action", "reward", "behavior_logp", "value_est", "done", "bootstrap",
+              "valid_steps")
+    res = []
+    for mode in ("host", "replay"):
+        lrn = tlg.Learner("mlp", D, A, hidden, max_segments=S, unroll_len=T, optimizer="adam",
+                          obs_u8=bits)
+        lrn.set_hyper(learning_rate=1e-3, batch_size=S, unroll_len=T)
+        lrn.set_params(p)
+        rep = None
+        if mode == "replay":
+            rep = tlg.Replay(lrn, cap, bits=bits)
+            for k in range(3):                  # ingest in three puts
+                rep.put(slot_of[k * S:(k + 1) * S], view(pool[k]))
+        stats = []
+        for draw in draws:
+            if mode == "host":
+                shards = [view(tlg.synth.SegmentBatch(*(getattr(allsegs, k)[draw[r * S:(r + 1) * S]]
+                                                        for k in fields)))
+                          for r in range(2)]
+                stats.append(lrn.train_step_shards(shards))
+            else:
+                stats.append(rep.train_step(slot_of[draw], n_shards=2))
+        res.append((lrn.get_params(), stats))
+        if rep is not None:
+            rep.close()
+    assert np.array_equal(res[0][0], res[1][0])
+    assert res[0][1] == res[1][1]
