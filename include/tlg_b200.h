@@ -179,7 +179,9 @@ int tlg_learner_train_staged(tlg_learner* l, tlg_step_stats* stats);
  * slots[0..n); tlg_learner_train_step_replay runs one step over n_shards shards of
  * `per_shard` slots each (slots[r * per_shard + i], the reference's shard slices,
  * learner.cpp:122-124) and writes stats[n_shards]; results equal
- * tlg_learner_train_step_shards on the same segments. */
+ * tlg_learner_train_step_shards on the same segments.  Puts run on the replay's own
+ * stream and may overlap a step on another host thread (puts themselves must be
+ * serialised, and must not target slots of a step in flight). */
 typedef struct tlg_replay tlg_replay;
 int tlg_replay_create(tlg_learner* l, uint32_t capacity, uint32_t obs_dtype, tlg_replay** out);
 void tlg_replay_destroy(tlg_replay* r);

@@ -51,6 +51,12 @@ struct LearnerConfig {
   // Non-empty: the blob is an MLP (flat [W_1,b_1,...,W_L,b_L | W_pi,b_pi | w_v,b_v])
   // over ParamBlob::shape {obs_dim, n_actions}.
   std::vector<std::uint32_t> mlp_hidden;
+  // Device-resident replay: PushSegment copies each segment into an HBM slot once; the
+  // host ReplayMem keeps making the (bit-identical) draw decisions over entries whose
+  // observations are dropped, and TrainStep gathers the drawn slots on the device (no
+  // per-step packing or observation H2D).  Within a period all observations must be
+  // 0/1 planes or all fp32 values, fixed by the first segment.
+  bool device_replay = false;
 };
 
 struct ThroughputStats {
@@ -73,7 +79,7 @@ class Learner : public SegmentSink {
   bool TrainStep();
   std::string FinishPeriod();
   std::string RunPeriod();
-  void Shutdown() { replay_.Shutdown(); }
+  void Shutdown();
 
   const std::string& current_key() const { return current_key_; }
   // Host fp64 mirror of the device parameters, refreshed lazily after updates.
@@ -88,6 +94,7 @@ class Learner : public SegmentSink {
  private:
   struct Gpu;
   void Publish();
+  bool TrainStepDeviceReplay(std::size_t per_shard);
   void SyncParams() const;
 
   LearnerConfig config_;

@@ -6,10 +6,14 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <condition_variable>
 #include <cstdio>
 #include <cstring>
+#include <deque>
 #include <stdexcept>
 #include <thread>
+#include <unordered_map>
+#include <unordered_set>
 
 #include "tlg_b200.h"
 
@@ -61,7 +65,133 @@ struct Learner::Gpu {
   std::vector<tlg_segment_batch> batches;
   std::vector<tlg_step_stats> stats;
 
-  ~Gpu() { tlg_learner_destroy(h); }
+  // ---- device-resident replay (LearnerConfig::device_replay)
+  // The host ReplayMem holds observation-less copies tagged with a private id (their
+  // segment_seq); `live` mirrors its FIFO (Push evicts the oldest live entry exactly when
+  // ReplayMem pops its front) and its reuse counts (an entry leaves after max_reuse
+  // draws), so every live entry's HBM slot is known.  Pushes and draws are serialised
+  // under `mu`; slots of the step in flight are pinned and freed after it.
+  struct Live {
+    std::uint32_t slot, uses;
+  };
+  tlg_replay* ring = nullptr;
+  std::uint32_t ring_dtype = 0, ring_cap = 0;
+  bool ring_decided = false;
+  std::mutex mu;
+  std::condition_variable cv;
+  bool shutting_down = false;
+  std::uint64_t next_id = 0;
+  std::deque<std::uint64_t> fifo;                   // ids in push order (lazy deletion)
+  std::unordered_map<std::uint64_t, Live> live;     // id -> slot, draws so far
+  std::vector<std::uint32_t> free_slots, deferred;  // deferred: freed while pinned
+  std::unordered_set<std::uint32_t> pinned;
+  Pinned<float> one_obs, one_f;
+  Pinned<std::int32_t> one_i;
+  Pinned<std::uint8_t> one_b;
+
+  void ResetRing(std::size_t capacity) {
+    if (ring) tlg_replay_destroy(ring);
+    ring = nullptr;
+    ring_decided = false;
+    ring_cap = std::uint32_t(capacity);
+    fifo.clear();
+    live.clear();
+    pinned.clear();
+    deferred.clear();
+    free_slots.clear();
+    for (std::uint32_t i = ring_cap; i-- > 0;) free_slots.push_back(i);
+  }
+  void Release(std::uint32_t slot) {
+    if (pinned.count(slot)) deferred.push_back(slot);
+    else free_slots.push_back(slot);
+  }
+  // mirrors ReplayMem::Push (replay_mem.cpp:14-20) before the stripped copy is pushed
+  std::uint32_t Admit(std::size_t capacity) {
+    if (live.size() == capacity) {
+      while (!fifo.empty() && !live.count(fifo.front())) fifo.pop_front();
+      Release(live.at(fifo.front()).slot);
+      live.erase(fifo.front());
+      fifo.pop_front();
+    }
+    if (free_slots.empty()) throw std::runtime_error("device replay ring exhausted");
+    const std::uint32_t slot = free_slots.back();
+    free_slots.pop_back();
+    return slot;
+  }
+  // one segment -> SoA (the same packing as Pack) -> its HBM slot
+  void Put(const TrajectorySegment& seg, std::uint32_t slot) {
+    const std::size_t D = shape.obs_dim, rowb = (D + 7) / 8;
+    const bool bitsfmt = ring_dtype == TLG_OBS_BITS;
+    if (bitsfmt) {
+      one_b.ensure(std::size_t(T) * (rowb + 1));
+      std::memset(one_b.p, 0, std::size_t(T) * (rowb + 1));
+    } else {
+      one_obs.ensure(std::size_t(T) * D);
+      std::memset(one_obs.p, 0, std::size_t(T) * D * sizeof(float));
+    }
+    one_f.ensure(3 * std::size_t(T) + 1);
+    one_i.ensure(std::size_t(T) + 1);
+    float* rw = one_f.p;
+    float* bl = rw + T;
+    float* va = bl + T;
+    float* bo = va + T;
+    std::uint8_t* dn = bitsfmt ? one_b.p + std::size_t(T) * rowb : nullptr;
+    std::vector<std::uint8_t> done_host;
+    if (!bitsfmt) {
+      done_host.assign(T, 0);
+      dn = done_host.data();
+    }
+    if (seg.valid_steps > T || seg.valid_steps > seg.steps.size())
+      throw std::invalid_argument("segment valid_steps exceeds its steps / unroll_len");
+    for (std::uint32_t t = 0; t < T; ++t) {
+      if (t < seg.valid_steps) {
+        const SegmentStep& st = seg.steps[t];
+        if (st.obs.size() != D)
+          throw std::invalid_argument("observation size does not match policy shape");
+        if (bitsfmt) {
+          std::uint8_t* row = one_b.p + std::size_t(t) * rowb;
+          for (std::size_t j = 0; j < D; ++j) {
+            if (st.obs[j] == 1.0) row[j >> 3] |= std::uint8_t(1u << (j & 7));
+            else if (st.obs[j] != 0.0)
+              throw std::invalid_argument("device replay: non-binary observation in a "
+                                          "bit-packed period");
+          }
+        } else {
+          for (std::size_t j = 0; j < D; ++j) one_obs.p[std::size_t(t) * D + j] = float(st.obs[j]);
+        }
+        one_i.p[t] = std::int32_t(st.action);
+        rw[t] = float(st.reward);
+        bl[t] = float(st.behavior_logp);
+        va[t] = float(st.value_est);
+        dn[t] = st.done ? 1 : 0;
+      } else {
+        one_i.p[t] = 0;
+        rw[t] = bl[t] = va[t] = 0.f;
+        dn[t] = 0;
+      }
+    }
+    *bo = float(seg.bootstrap_value);
+    one_i.p[T] = std::int32_t(seg.valid_steps);
+    tlg_segment_batch b{};
+    b.n_segments = 1;
+    b.unroll_len = T;
+    b.obs_dim = shape.obs_dim;
+    b.obs_dtype = ring_dtype;
+    b.obs = bitsfmt ? static_cast<const void*>(one_b.p) : static_cast<const void*>(one_obs.p);
+    b.action = one_i.p;
+    b.reward = rw;
+    b.behavior_logp = bl;
+    b.value_est = va;
+    b.done = dn;
+    b.bootstrap = bo;
+    b.valid_steps = one_i.p + T;
+    Check(tlg_replay_put(ring, &slot, &b));
+  }
+
+  ~Gpu() {
+    if (ring) tlg_replay_destroy(ring);
+    tlg_learner_destroy(h);
+  }
 
   bool Matches(const tlg_policy_shape& s, std::uint32_t S_, std::uint32_t T_,
                std::uint32_t sh) const {
@@ -186,6 +316,11 @@ void Learner::StartPeriod() {
   if (s.n_hidden > 8) throw std::invalid_argument("at most 8 hidden layers");
   for (std::uint32_t l = 0; l < s.n_hidden; ++l) s.hidden[l] = config_.mlp_hidden[l];
   const std::uint32_t S = hyper_.batch_size, T = hyper_.unroll_len;
+  if (gpu_->ring) {  // the ring belongs to the device learner: drop it first
+    std::lock_guard dl(gpu_->mu);
+    tlg_replay_destroy(gpu_->ring);
+    gpu_->ring = nullptr;
+  }
   if (!gpu_->Matches(s, S, T, config_.num_shards)) {
     tlg_learner_destroy(gpu_->h);
     gpu_->h = nullptr;
@@ -214,6 +349,18 @@ void Learner::StartPeriod() {
                hyper_.adv_norm ? 1 : 0};
   Check(tlg_learner_set_hyper(gpu_->h, &hp));
   Check(tlg_learner_set_params(gpu_->h, params_.values.data(), params_.values.size()));
+  if (config_.device_replay) {
+    std::lock_guard dl(gpu_->mu);
+    // replay_capacity live entries + the slots pinned by one draw
+    gpu_->ResetRing(config_.replay_capacity + std::size_t(S) * config_.num_shards);
+  }
+}
+
+void Learner::Shutdown() {
+  replay_.Shutdown();
+  std::lock_guard dl(gpu_->mu);
+  gpu_->shutting_down = true;
+  gpu_->cv.notify_all();
 }
 
 void Learner::PushSegment(const TrajectorySegment& segment) {
@@ -224,13 +371,50 @@ void Learner::PushSegment(const TrajectorySegment& segment) {
       return;
     }
   }
-  replay_.Push(segment);
+  if (!config_.device_replay) {
+    replay_.Push(segment);
+    return;
+  }
+  Gpu& g = *gpu_;
+  std::lock_guard dl(g.mu);
+  if (!g.ring_decided) {  // the period's first segment fixes the ring's format
+    bool binary = true;
+    const std::uint32_t n = std::min<std::uint32_t>(segment.valid_steps,
+                                                    std::uint32_t(segment.steps.size()));
+    for (std::uint32_t t = 0; t < n && binary; ++t)
+      for (double x : segment.steps[t].obs)
+        if (x != 0.0 && x != 1.0) {
+          binary = false;
+          break;
+        }
+    g.ring_dtype = binary ? TLG_OBS_BITS : TLG_OBS_F32;
+    Check(tlg_replay_create(g.h, g.ring_cap, g.ring_dtype, &g.ring));
+    g.ring_decided = true;
+  }
+  const std::uint32_t slot = g.Admit(config_.replay_capacity);
+  try {
+    g.Put(segment, slot);
+  } catch (...) {
+    g.free_slots.push_back(slot);
+    throw;
+  }
+  TrajectorySegment stripped = segment;
+  for (SegmentStep& st : stripped.steps) {
+    st.obs.clear();
+    st.obs.shrink_to_fit();
+  }
+  stripped.segment_seq = g.next_id;
+  g.live.emplace(g.next_id, Gpu::Live{slot, 0});
+  g.fifo.push_back(g.next_id++);
+  replay_.Push(std::move(stripped));
+  g.cv.notify_all();
 }
 
 bool Learner::TrainStep() {
   if (config_.step_delay_ms > 0)
     std::this_thread::sleep_for(std::chrono::milliseconds(config_.step_delay_ms));
   const std::size_t per_shard = hyper_.batch_size;
+  if (config_.device_replay) return TrainStepDeviceReplay(per_shard);
   auto segments = replay_.SampleBlocking(per_shard * config_.num_shards);
   if (segments.empty()) return false;
   gpu_->Pack(segments);
@@ -239,6 +423,45 @@ bool Learner::TrainStep() {
   // back as the reference's exception types; on failure the parameters are unchanged.
   Check(tlg_learner_train_step_shards(gpu_->h, gpu_->batches.data(), int(config_.num_shards),
                                       /*on_device=*/0, gpu_->stats.data()));
+  ++update_steps_;
+  params_stale_ = true;
+  if (config_.publish_interval > 0 && update_steps_ % config_.publish_interval == 0) Publish();
+  return true;
+}
+
+// TrainStep over the device-resident ring: the same ReplayMem draw (pushes are held off
+// while it happens, so the live-entry mirror stays exact), then a device gather by slot.
+bool Learner::TrainStepDeviceReplay(std::size_t per_shard) {
+  Gpu& g = *gpu_;
+  const std::size_t n = per_shard * config_.num_shards;
+  std::vector<std::uint32_t> slots;
+  {
+    std::unique_lock dl(g.mu);
+    g.cv.wait(dl, [&] { return g.shutting_down || replay_.size() >= n; });
+    if (g.shutting_down) return false;
+    auto segments = replay_.SampleBlocking(n);  // cannot block: pushes are held off
+    if (segments.empty()) return false;
+    slots.reserve(n);
+    for (const TrajectorySegment& seg : segments) {
+      Gpu::Live& e = g.live.at(seg.segment_seq);
+      slots.push_back(e.slot);
+      g.pinned.insert(e.slot);
+      if (++e.uses >= hyper_.max_reuse) {  // ReplayMem erased it (replay_mem.cpp:41-44)
+        g.Release(e.slot);
+        g.live.erase(seg.segment_seq);
+      }
+    }
+  }
+  g.stats.assign(config_.num_shards, tlg_step_stats{});
+  int rc = tlg_learner_train_step_replay(g.h, g.ring, slots.data(), config_.num_shards,
+                                         std::uint32_t(per_shard), g.stats.data());
+  {
+    std::lock_guard dl(g.mu);
+    g.pinned.clear();
+    g.free_slots.insert(g.free_slots.end(), g.deferred.begin(), g.deferred.end());
+    g.deferred.clear();
+  }
+  Check(rc);
   ++update_steps_;
   params_stale_ = true;
   if (config_.publish_interval > 0 && update_steps_ % config_.publish_interval == 0) Publish();

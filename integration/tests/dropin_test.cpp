@@ -468,6 +468,41 @@ TEST(constructing_against_a_missing_key_fails_fast) {
   CHECK_THROWS_AS(infserver::InfServer({"absent:0000"}, pool, "127.0.0.1", 0), std::exception);
 }
 
+TEST(device_resident_replay_matches_the_host_replay_path) {
+  // LearnerConfig::device_replay: segments live in HBM slots from PushSegment on and the
+  // draw is gathered on the device; draws (the reference ReplayMem's) and parameters must
+  // equal the host-packing path exactly, through FIFO eviction and reuse.
+  for (auto algo : {learner::Algo::kPpo, learner::Algo::kVtrace}) {
+    HyperParams hyper = TestHyper();
+    hyper.max_reuse = algo == learner::Algo::kVtrace ? 2 : 1;
+    Rig rig_a(hyper), rig_b(hyper);
+    learner::LearnerConfig cfg;
+    cfg.num_shards = 2;
+    cfg.algo = algo;
+    cfg.publish_interval = 1;
+    cfg.seed = 5;
+    cfg.replay_capacity = 12;  // small: pushes evict through the FIFO
+    learner::LearnerConfig cfg_dev = cfg;
+    cfg_dev.device_replay = true;
+    learner::Learner host(cfg, rig_a.league, rig_a.pool);
+    learner::Learner dev(cfg_dev, rig_b.league, rig_b.pool);
+    std::mt19937_64 feed_a(77), feed_b(77);
+    std::uint64_t seq = 0;
+    for (int step = 0; step < 20; ++step) {
+      const int pushes = 8 + step % 5;  // >= one draw (2 shards x 4 segments)
+      for (int i = 0; i < pushes; ++i, ++seq) {
+        host.PushSegment(MakeSegment(host.current_key(), feed_a, seq));
+        dev.PushSegment(MakeSegment(dev.current_key(), feed_b, seq));
+      }
+      CHECK(host.replay().size() == dev.replay().size());
+      CHECK(host.TrainStep());
+      CHECK(dev.TrainStep());
+      CHECK(host.params().values == dev.params().values);
+      CHECK(host.replay().consumed_steps() == dev.replay().consumed_steps());
+    }
+  }
+}
+
 TEST(reference_run_bench_runs_on_the_b200_learner) {
   // run::RunBench (bench.cpp:60-162) builds learner::Learner -- here the B200 drop-in --
   // next to the reference's own actors, league and pool.

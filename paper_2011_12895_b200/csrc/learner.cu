@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -1222,6 +1223,10 @@ int tlg_learner_comm_init(tlg_learner* l, const uint8_t unique_id[128], int nran
 // Device-resident replay ring
 struct tlg_replay {
   tlg_learner* l = nullptr;
+  // ingest runs on its own stream (a put does not wait for an in-flight step); a step's
+  // gather waits for the last put through `ready`
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ready = nullptr;
   uint32_t cap = 0, dtype = 0;
   long rowb = 0;  // bytes per frame row in the ring and the gathered batches
   DevFree mem;
@@ -1230,7 +1235,10 @@ struct tlg_replay {
   uint32_t *d_put_slots = nullptr, *d_gather_slots = nullptr;
   long put_slots_cap = 0, gather_slots_cap = 0;
 
+  std::mutex alloc_mu;  // puts (ingest thread) and steps (trainer thread) both allocate
+
   tlg::SegArrays alloc(long segs, long rb) {
+    std::lock_guard<std::mutex> g(alloc_mu);
     const int T = l->T;
     tlg::SegArrays a{};
     a.obs = mem.add<uint8_t>(segs * T * rb + 16);
@@ -1243,15 +1251,24 @@ struct tlg_replay {
     a.valid = mem.add<int32_t>(segs);
     return a;
   }
-  uint32_t* slots_to_device(uint32_t*& buf, long& capn, const uint32_t* h, long n) {
+  uint32_t* slots_to_device(uint32_t*& buf, long& capn, const uint32_t* h, long n,
+                            cudaStream_t st) {
     for (long i = 0; i < n; ++i)
       if (h[i] >= cap) throw InvalidArg("replay slot out of range");
     if (capn < n) {
+      std::lock_guard<std::mutex> g(alloc_mu);
       buf = mem.add<uint32_t>(n);
       capn = n;
     }
-    TLG_CUDA(cudaMemcpyAsync(buf, h, n * 4, cudaMemcpyHostToDevice, l->stream));
+    TLG_CUDA(cudaMemcpyAsync(buf, h, n * 4, cudaMemcpyHostToDevice, st));
     return buf;
+  }
+  ~tlg_replay() {
+    if (stream) {
+      cudaStreamSynchronize(stream);
+      cudaStreamDestroy(stream);
+    }
+    if (ready) cudaEventDestroy(ready);
   }
 };
 
@@ -1270,12 +1287,14 @@ int tlg_replay_create(tlg_learner* l, uint32_t capacity, uint32_t obs_dtype, tlg
     r->dtype = obs_dtype;
     r->rowb = obs_dtype == TLG_OBS_BITS ? l->bits_pitch : long(l->net.D) * 4;
     r->ring = r->alloc(capacity, r->rowb);
+    TLG_CUDA(cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking));
+    TLG_CUDA(cudaEventCreateWithFlags(&r->ready, cudaEventDisableTiming));
     *out = r.release();
   });
 }
 
 void tlg_replay_destroy(tlg_replay* r) {
-  if (r && r->l && r->l->stream) cudaStreamSynchronize(r->l->stream);
+  if (r && r->l && r->l->stream) cudaStreamSynchronize(r->l->stream);  // no gather in flight
   delete r;
 }
 
@@ -1302,7 +1321,7 @@ int tlg_replay_put(tlg_replay* r, const uint32_t* slots, const tlg_segment_batch
     }
     const long F = n * T;
     auto h2d = [&](void* dst, const void* src, size_t bytes) {
-      TLG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, l->stream));
+      TLG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, r->stream));
     };
     h2d(r->stage.obs, b->obs, size_t(F * src_rowb));
     h2d(r->stage.action, b->action, F * 4);
@@ -1312,9 +1331,11 @@ int tlg_replay_put(tlg_replay* r, const uint32_t* slots, const tlg_segment_batch
     h2d(r->stage.done, b->done, F);
     h2d(r->stage.boot, b->bootstrap, n * 4);
     h2d(r->stage.valid, b->valid_steps, n * 4);
-    const uint32_t* ds = r->slots_to_device(r->d_put_slots, r->put_slots_cap, slots, n);
-    tlg::launch_replay_move(r->stage, src_rowb, r->ring, r->rowb, ds, int(n), T, true, l->stream);
-    TLG_CUDA(cudaStreamSynchronize(l->stream));  // the host batch may be reused on return
+    const uint32_t* ds =
+        r->slots_to_device(r->d_put_slots, r->put_slots_cap, slots, n, r->stream);
+    tlg::launch_replay_move(r->stage, src_rowb, r->ring, r->rowb, ds, int(n), T, true, r->stream);
+    TLG_CUDA(cudaEventRecord(r->ready, r->stream));
+    TLG_CUDA(cudaStreamSynchronize(r->stream));  // the host batch may be reused on return
   });
 }
 
@@ -1332,7 +1353,9 @@ int tlg_learner_train_step_replay(tlg_learner* l, tlg_replay* r, const uint32_t*
       r->gath = r->alloc(total, r->rowb);
       r->gath_segs = total;
     }
-    const uint32_t* ds = r->slots_to_device(r->d_gather_slots, r->gather_slots_cap, slots, total);
+    const uint32_t* ds =
+        r->slots_to_device(r->d_gather_slots, r->gather_slots_cap, slots, total, l->stream);
+    TLG_CUDA(cudaStreamWaitEvent(l->stream, r->ready, 0));
     tlg::launch_replay_move(r->ring, r->rowb, r->gath, r->rowb, ds, int(total), T, false,
                             l->stream);
     std::vector<tlg_segment_batch> bs(n_shards);
