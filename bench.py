@@ -372,6 +372,38 @@ def main():
                    "h2d_bytes_per_step": sum(a.nbytes for a in pu[0].arrs.values()),
                    "d2h_bytes_per_step": 48 + 8, "obs_format": "uint8 planes"}
 
+    # ---- device-resident replay: segments ingested once into HBM
+    # slots, each step gathers a random draw of S slots on the device
+    replay = None
+    if obs_bits or not obs_u8:
+        rep = tlg.Replay(lrn, 2 * S, bits=obs_bits)
+        for k in range(2):  # (the first put also allocates the staging buffers)
+            rep.put(np.arange(k * S, (k + 1) * S, dtype=np.uint32), pinned[k])
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for k in range(2):
+            rep.put(np.arange(k * S, (k + 1) * S, dtype=np.uint32), pinned[k])
+        ingest_s = time.perf_counter() - t0
+        rng = np.random.default_rng(rank)
+        draws = [rng.permutation(2 * S)[:S].astype(np.uint32) for _ in range(args.steps + 2)]
+        for i in range(2):
+            rep.train_step(draws[i])
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        fr = 0
+        for i in range(args.steps):
+            st = rep.train_step(draws[i + 2])
+            fr += int(st[0]["n_samples"])
+        dt = max_over_ranks(time.perf_counter() - t0)
+        replay = {"value": sum_over_ranks(fr) / dt, "unit": "frames/s",
+                  "ring_segments": 2 * S,
+                  "ingest_gbs": 2 * h2d / ingest_s / 1e9,
+                  "note": "tlg_learner_train_step_replay: random draws of S slots from a "
+                          "2S-segment HBM ring (gathered on the device each step); ingest "
+                          "= tlg_replay_put of two host batches"}
+        rep.close()
+
     # ---- roofline of the dominant kernel (layer-1 forward GEMM)
     peaks, peak_src = measured_peaks()
     F = S * T
@@ -513,6 +545,7 @@ def main():
                     "note": "pinned host SoA batch H2D each step (same obs format as value), "
                             "pipelined one step ahead on a copy stream; stats D2H each step"},
             "e2e_alt_format": e2e_alt,
+            "device_replay": replay,
             "gpu_launches": launches,
             "roofline": roofline,
             "kernels": kernels,
