@@ -495,14 +495,19 @@ def main():
         e1.record(pstream)
         torch.cuda.synchronize()
         ims = max_over_ranks(e0.elapsed_time(e1) / reps)
-        obs_pin_t = torch.from_numpy(obs).pin_memory()  # kept alive while the view is used
+        # pinned host buffers on both sides (kept alive while their views are used)
+        obs_pin_t = torch.from_numpy(obs).pin_memory()
         obs_pin = obs_pin_t.numpy()
-        pol.forward(obs_pin)
+        outs_t = [torch.empty(c4.batch_size, c4.n_actions, pin_memory=True),
+                  torch.empty(c4.batch_size, c4.n_actions, pin_memory=True),
+                  torch.empty(c4.batch_size, pin_memory=True)]
+        outs = tuple(t.numpy() for t in outs_t)
+        pol.forward(obs_pin, out=outs)
         barrier()
         t0 = time.perf_counter()
-        for _ in range(3):
-            pol.forward(obs_pin)
-        idt = max_over_ranks((time.perf_counter() - t0) / 3)
+        for _ in range(10):
+            pol.forward(obs_pin, out=outs)
+        idt = max_over_ranks((time.perf_counter() - t0) / 10)
         infer = {"metric": "InferenceServer actions/sec", "config": c4.name, "note": c4.note,
                  "value": world * c4.batch_size / (ims / 1e3), "unit": "actions/s",
                  "ms_per_batch": ims,

@@ -390,12 +390,17 @@ class Policy:
         v = np.ascontiguousarray(values, np.float64)
         check(lib().tlg_policy_set_params(self.h, v.ctypes.data, v.size))
 
-    def forward(self, obs):
+    def forward(self, obs, out=None):
+        """Host batch in, host results out.  `out` = (logits, probs, value) arrays to fill
+        (e.g. views of pinned buffers); new arrays otherwise."""
         obs = np.ascontiguousarray(obs, np.float32)
         n = obs.shape[0]
-        lg = np.zeros((n, self.A), np.float32)
-        pr = np.zeros((n, self.A), np.float32)
-        v = np.zeros(n, np.float32)
+        if out is None:
+            lg = np.zeros((n, self.A), np.float32)
+            pr = np.zeros((n, self.A), np.float32)
+            v = np.zeros(n, np.float32)
+        else:
+            lg, pr, v = out
         check(lib().tlg_policy_forward(self.h, obs.ctypes.data, n, lg.ctypes.data, pr.ctypes.data,
                                        v.ctypes.data, 0))
         return lg, pr, v
