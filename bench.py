@@ -310,10 +310,14 @@ def main():
     # ---- end to end through the C ABI with pinned host buffers: every step's batch is
     # copied H2D inside the timed region (pipelined: the copy of step k+1 overlaps step
     # k through tlg_learner_stage / tlg_learner_train_staged) and its statistics D2H'd.
-    def pinned_view(h, bits=False):
+    def pinned_view(h, bits=False, pitch=0):
         hb = h.slice(0, h.n_segments)
         if bits:
             hb.obs = tlg.synth.pack_bits(h.obs)
+            if pitch:  # bit rows padded to `pitch` bytes on the host already
+                padded = np.zeros(hb.obs.shape[:-1] + (pitch,), np.uint8)
+                padded[..., :hb.obs.shape[-1]] = hb.obs
+                hb.obs = padded
         pv = tlg.SegmentBatchView(hb, bits=bits, obs_dim=D)
         pv.pinned = []  # the pinned tensors must outlive the numpy views handed to the C ABI
         for k, a in pv.arrs.items():
@@ -325,7 +329,7 @@ def main():
             h.n_segments, h.unroll_len, D, 2 if bits else (1 if obs_u8 else 0),
             *(pv.arrs[k].ctypes.data for k in ("obs", "action", "reward", "behavior_logp",
                                                  "value_est", "done", "bootstrap",
-                                                 "valid_steps")))
+                                                 "valid_steps")), pitch)
         return pv
 
     def e2e_run(views):
@@ -349,9 +353,18 @@ def main():
         return sum_over_ranks(fr) / dt
 
     # main e2e in the run's obs format; binary planes also reported as uint8 planes
-    pinned = [pinned_view(h, bits=obs_bits) for h in host[:2]]
+    # bit rows padded to 16 B on the host (obs_pitch; +6 % bytes, no device re-pitch)
+    host_pitch = ((D + 7) // 8 + 15) // 16 * 16 if obs_bits else 0
+    pinned = [pinned_view(h, bits=obs_bits, pitch=host_pitch) for h in host[:2]]
     h2d = sum(a.nbytes for a in pinned[0].arrs.values())
     e2e_value = e2e_run(pinned)
+    e2e_unpitched = None
+    if obs_bits:  # dense ceil(D/8)-byte rows, re-pitched on the device
+        pp = [pinned_view(h, bits=True) for h in host[:2]]
+        e2e_unpitched = {"value": e2e_run(pp), "unit": "frames/s",
+                         "h2d_bytes_per_step": sum(a.nbytes for a in pp[0].arrs.values()),
+                         "d2h_bytes_per_step": 48 + 8,
+                         "obs_format": "bit-packed planes, dense rows (re-pitched on device)"}
 
     # this box's pinned host->device bandwidth for the same bytes (PCIe; it bounds e2e)
     def h2d_gbs():
@@ -547,9 +560,11 @@ def main():
                              f"{resident_bytes / 1e6:.0f} MB in total"},
             "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": 48 + 8, "h2d_gbs_measured": h2d_bw,
-                    "note": "pinned host SoA batch H2D each step (same obs format as value), "
-                            "pipelined one step ahead on a copy stream; stats D2H each step"},
+                    "note": "pinned host SoA batch H2D each step (same obs format as value; "
+                            "bit rows padded to 16 B), pipelined one step ahead on a copy "
+                            "stream; stats D2H each step"},
             "e2e_alt_format": e2e_alt,
+            "e2e_dense_rows": e2e_unpitched,
             "device_replay": replay,
             "gpu_launches": launches,
             "roofline": roofline,
