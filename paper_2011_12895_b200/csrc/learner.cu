@@ -511,8 +511,15 @@ struct tlg_learner {
   // Trunk forward + policy/value heads with the parameter set P (the student's, or a
   // teacher's for the KL term, rlmath.cpp:145-155): head outputs [F][A+1] -> out,
   // log-prob of the taken action -> out_tlogp (may be null).
+  // PPO with fused heads: the loss kernel reads the head partial sums directly (no target
+  // log-prob is needed, so head_finalize_kernel is skipped)
+  bool loss_reads_parts() const {
+    return cfg.algo == TLG_ALGO_PPO && net.L > 0 && fused_head();
+  }
+
   void forward_heads(const Staged& sg, const float* P, const float* P_lo, const float* x0,
-                     const float* x0_lo, float* out, float* out_tlogp, bool timed) {
+                     const float* x0_lo, float* out, float* out_tlogp, bool timed,
+                     bool finalize = true) {
     const tlg::BatchDev bd = sg.bd;
     const long F = long(bd.S) * T;
     // ---- forward trunk
@@ -566,11 +573,13 @@ struct tlg_learner {
     }
     const float* hL = net.L ? act[net.L - 1] : x0;
     const long ldh = net.head.H;
-    if (net.L > 0 && fused_head())
+    if (net.L > 0 && fused_head()) {
+      if (!finalize) return;
       tlg::launch_head_finalize(net.head, P, head_part, head_tiles, F, &bd, out, out_tlogp,
                                 nullptr, nullptr, nullptr, err, stream);
-    else
+    } else {
       tlg::launch_head_forward(net.head, P, hL, ldh, &bd, F, out, out_tlogp, nullptr, err, stream);
+    }
     launches += 1;
   }
 
@@ -595,7 +604,8 @@ struct tlg_learner {
       forward_heads(sg, teacher, teacher_lo, x0, x0_lo, t_head_out, nullptr, false);
       wq_fresh = false;  // layer-1 int8 pieces must be rebuilt from the student's weights
     }
-    forward_heads(sg, params, params_lo, x0, x0_lo, head_out, tlogp, shard == 0);
+    const bool parts = loss_reads_parts();
+    forward_heads(sg, params, params_lo, x0, x0_lo, head_out, tlogp, shard == 0, !parts);
     if (shard == 0) mark(2);
     // ---- heads, returns, loss
     const float* hL = net.L ? act[net.L - 1] : x0;
@@ -610,7 +620,8 @@ struct tlg_learner {
     const tlg::LossLaunch ll = tlg::launch_loss_backward(
         net.head, params, hL, ldh, bd, head_out, adv, target, st, hd, loss_kind, dzh,
         net.L ? dz[net.L - 1] : nullptr, net.L ? dz_lo[net.L - 1] : nullptr, hg_partial,
-        loss_partial, col_partial, stream, teacher_active() ? t_head_out : nullptr);
+        loss_partial, col_partial, stream, teacher_active() ? t_head_out : nullptr,
+        parts ? head_part : nullptr, head_tiles, err);
     tlg::launch_head_grad_reduce(net.head, hg_partial, loss_partial, ll, gtarget, st, stream);
     launches += 6;
     if (net.L > 0) {  // db of the top trunk layer from the loss kernel's column partials

@@ -410,12 +410,16 @@ __global__ void __launch_bounds__(1024) finalize_adv_kernel(const double* __rest
 // K3b, part 1 (thread per frame): the per-sample PPO / PG body (rlmath.cpp:129-182 /
 // 196-220) -> dlogits, dvalue [F][A1]; per-block fp64 loss/stat sums and per-block
 // bias-gradient sums (fixed-order warp trees).
-template <int kMaxA1>
+// kParts: the logits come straight from the fused-head partial sums of the last trunk
+// GEMM (head_finalize_kernel skipped: PPO needs no target log-prob), and the action range
+// check (rlmath.cpp:133) happens here.  kKL: teacher KL term compiled in.
+template <int kMaxA1, bool kKL, bool kParts>
 __global__ void __launch_bounds__(256) loss_math_kernel(
     HeadDesc hd, BatchDev b, const float* __restrict__ head_out, const float* __restrict__ adv,
     const float* __restrict__ target, const StepStatsDev* __restrict__ st, HyperDev hp,
     int loss_kind, float* __restrict__ dzh, double* __restrict__ loss_partial,
-    float* __restrict__ bias_partial, const float* __restrict__ teacher_out) {
+    float* __restrict__ bias_partial, const float* __restrict__ teacher_out, int n_tiles,
+    const float* __restrict__ params, int* __restrict__ err) {
   __shared__ double red[5][8];
   __shared__ float bred[kMaxA1][8];
   const int A = hd.A, A1 = A + 1;
@@ -434,8 +438,23 @@ __global__ void __launch_bounds__(256) loss_math_kernel(
   }
   if (valid) {
     float z[kMaxA1];
+    if (kParts) {
 #pragma unroll
-    for (int k = 0; k < kMaxA1; ++k) z[k] = k < A1 ? head_out[f * A1 + k] : 0.f;
+      for (int k = 0; k < kMaxA1; ++k) {
+        float acc = 0.f;
+        if (k < A1) {
+          for (int t = 0; t < n_tiles; ++t) acc += head_out[(long(t) * F + f) * A1 + k];
+          const long boff = k < A ? (hd.bpi >= 0 ? hd.bpi + k : -1) : hd.bv;
+          if (boff >= 0) acc += params[boff];
+        }
+        z[k] = acc;
+      }
+      const int ar = b.action[f];
+      if (ar < 0 || ar >= A) atomicOr(err, kErrActionRange);
+    } else {
+#pragma unroll
+      for (int k = 0; k < kMaxA1; ++k) z[k] = k < A1 ? head_out[f * A1 + k] : 0.f;
+    }
     float mx = -INFINITY;
 #pragma unroll
     for (int k = 0; k < kMaxA1; ++k)
@@ -456,7 +475,7 @@ __global__ void __launch_bounds__(256) loss_math_kernel(
     const int a = min(max(b.action[f], 0), A - 1);  // out-of-range is flagged by K3a
     // teacher KL (rlmath.cpp:145-155, 177-178): KL(p || q) with q the teacher's policy
     float lq[kMaxA1], kl = 0.f;
-    const bool kl_on = loss_kind == 0 && teacher_out != nullptr;
+    const bool kl_on = kKL && loss_kind == 0 && teacher_out != nullptr;
     if (kl_on) {
       float tz[kMaxA1];
 #pragma unroll
@@ -1018,7 +1037,8 @@ LossLaunch launch_loss_backward(const HeadDesc& hd, const float* params, const f
                                 const float* adv, const float* target, const StepStatsDev* st,
                                 const HyperDev& hp, int loss_kind, float* dzh, float* dz,
                                 float* dz_lo, float* hg_partial, double* loss_partial,
-                                float* db_partial, cudaStream_t s, const float* teacher_out) {
+                                float* db_partial, cudaStream_t s, const float* teacher_out,
+                                const float* head_part, int n_tiles, int* err) {
   const long F = long(b.S) * b.T;
   const int A1 = hd.A + 1;
   const long nw = long(A1) * hd.H;
@@ -1032,14 +1052,26 @@ LossLaunch launch_loss_backward(const HeadDesc& hd, const float* params, const f
                          : int(std::min<long>(nchunks, kLossBlocks));
   ll.math_blocks = ceil_div(F, 256);
   float* bias_partial = hg_partial + long(ll.stream_blocks) * nw;
-  if (A1 <= 8)
-    loss_math_kernel<8><<<ll.math_blocks, 256, 0, s>>>(hd, b, head_out, adv, target, st, hp,
-                                                       loss_kind, dzh, loss_partial, bias_partial,
-                                                       teacher_out);
-  else
-    loss_math_kernel<32><<<ll.math_blocks, 256, 0, s>>>(hd, b, head_out, adv, target, st, hp,
-                                                        loss_kind, dzh, loss_partial,
-                                                        bias_partial, teacher_out);
+  const float* src = head_part ? head_part : head_out;
+#define TLG_MATH(MA, KL, PARTS)                                                              \
+  loss_math_kernel<MA, KL, PARTS><<<ll.math_blocks, 256, 0, s>>>(                           \
+      hd, b, src, adv, target, st, hp, loss_kind, dzh, loss_partial, bias_partial, teacher_out, \
+      n_tiles, params, err)
+  const bool kl = teacher_out != nullptr;
+  if (A1 <= 8) {
+    if (head_part) {
+      if (kl) TLG_MATH(8, true, true);
+      else TLG_MATH(8, false, true);
+    } else {
+      if (kl) TLG_MATH(8, true, false);
+      else TLG_MATH(8, false, false);
+    }
+  } else {
+    if (head_part) throw CudaError("fused-head partials need n_actions + 1 <= 8");
+    if (kl) TLG_MATH(32, true, false);
+    else TLG_MATH(32, false, false);
+  }
+#undef TLG_MATH
   TLG_CHECK_LAUNCH();
   if (vec) {
     loss_stream4_kernel<8><<<dim3(ll.stream_blocks, slabs), 256, 0, s>>>(

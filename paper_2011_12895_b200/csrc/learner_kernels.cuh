@@ -112,7 +112,9 @@ LossLaunch launch_loss_backward(const HeadDesc& hd, const float* params, const f
                                 const HyperDev& hp, int loss_kind, float* dzh, float* dz,
                                 float* dz_lo, float* hg_partial, double* loss_partial,
                                 float* db_partial, cudaStream_t s,
-                                const float* teacher_out = nullptr);
+                                const float* teacher_out = nullptr,
+                                const float* head_part = nullptr, int n_tiles = 0,
+                                int* err = nullptr);
 void launch_head_grad_reduce(const HeadDesc& hd, const float* hg_partial,
                              const double* loss_partial, const LossLaunch& ll, float* grad,
                              StepStatsDev* st, cudaStream_t s);
