@@ -756,26 +756,30 @@ __global__ void __launch_bounds__(256, 2) loss_stream4_kernel(
   }
 }
 
+// 32 columns per block, nw = blockDim/32 warps each summing rows w, w + nw, ... in order,
+// then the warps' partial sums in warp order (deterministic for a given block size: 32
+// warps when few columns must cover many rows, 8 when the grid is already wide)
+constexpr int kRowWarps = 32;
 template <typename Store>
 __device__ __forceinline__ void rows_reduce_block(const float* __restrict__ partial, int rows,
                                                   long cols, long stride, Store store) {
-  __shared__ float sh[8][33];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __shared__ float sh[kRowWarps][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = int(blockDim.x >> 5);
   const long c = long(blockIdx.x) * 32 + lane;
   float acc = 0.f;
   if (c < cols)
-    for (int r = w; r < rows; r += 8) acc += partial[long(r) * stride + c];
+    for (int r = w; r < rows; r += nw) acc += partial[long(r) * stride + c];
   sh[w][lane] = acc;
   __syncthreads();
   if (w == 0 && c < cols) {
     float t = 0.f;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) t += sh[i][lane];
+    for (int i = 0; i < nw; ++i) t += sh[i][lane];
     store(c, t);
   }
 }
+inline int rows_reduce_threads(long cols) { return cols >= 8192 ? 256 : 32 * kRowWarps; }
 
-__global__ void __launch_bounds__(256) rows_reduce_kernel(const float* __restrict__ partial,
+__global__ void __launch_bounds__(1024) rows_reduce_kernel(const float* __restrict__ partial,
                                                           int rows, long cols, long stride,
                                                           float* __restrict__ out) {
   rows_reduce_block(partial, rows, cols, stride, [&](long c, float v) { out[c] = v; });
@@ -783,7 +787,7 @@ __global__ void __launch_bounds__(256) rows_reduce_kernel(const float* __restric
 
 // Head-gradient partials [nblk][A1][H] -> flat gradient (layout-aware, AccumulateGrad
 // order of the families, policy.cpp:122-141).
-__global__ void __launch_bounds__(256) head_grad_reduce_kernel(HeadDesc hd,
+__global__ void __launch_bounds__(1024) head_grad_reduce_kernel(HeadDesc hd,
                                                                const float* __restrict__ hg_partial,
                                                                int nblocks,
                                                                float* __restrict__ grad) {
@@ -1104,8 +1108,8 @@ void launch_head_grad_reduce(const HeadDesc& hd, const float* hg_partial,
                              const double* loss_partial, const LossLaunch& ll, float* grad,
                              StepStatsDev* st, cudaStream_t s) {
   const long nw = long(hd.A + 1) * hd.H;
-  head_grad_reduce_kernel<<<ceil_div(nw, 32), 256, 0, s>>>(hd, hg_partial, ll.stream_blocks,
-                                                           grad);
+  head_grad_reduce_kernel<<<ceil_div(nw, 32), rows_reduce_threads(nw), 0, s>>>(
+      hd, hg_partial, ll.stream_blocks, grad);
   TLG_CHECK_LAUNCH();
   head_bias_stats_kernel<<<1, 32 * (hd.A + 1 + 5), 0, s>>>(
       hd, hg_partial + long(ll.stream_blocks) * nw, loss_partial, ll.math_blocks, grad, st);
@@ -1114,7 +1118,8 @@ void launch_head_grad_reduce(const HeadDesc& hd, const float* hg_partial,
 
 void launch_rows_reduce(const float* partial, int rows, long cols, long stride, float* out,
                         cudaStream_t s) {
-  rows_reduce_kernel<<<ceil_div(cols, 32), 256, 0, s>>>(partial, rows, cols, stride, out);
+  rows_reduce_kernel<<<ceil_div(cols, 32), rows_reduce_threads(cols), 0, s>>>(partial, rows, cols,
+                                                                             stride, out);
   TLG_CHECK_LAUNCH();
 }
 
