@@ -92,25 +92,26 @@ __global__ void __launch_bounds__(256) quantize_rows_kernel(const float* __restr
   }
   __syncthreads();
   const float s = red[0] > 0.f ? red[0] / 127.f : 1.f;
+  const float inv = red[0] > 0.f ? 127.f / red[0] : 1.f;  // the epilogue multiplies by s
   if (threadIdx.x == 0) scale[n] = s;
-  const double inv = 1.0 / double(s);
   int8_t* q0 = q + long(n) * Kp;
+  constexpr float kMagic = 12582912.f;  // round-to-nearest-even via 1.5 * 2^23
   for (long k = threadIdx.x; k < Kp; k += blockDim.x) {
-    int a = 0, b = 0, c = 0;
+    uint32_t a = 0, b = 0, c = 0;
     if (k < K) {
-      const double x = double(w[k]) * inv;  // |x| <= 127 (+ rounding of s)
-      const double r0 = rint(x);
-      const double x1 = (x - r0) * 128.0;  // |x1| <= 64
-      const double r1 = rint(x1);
-      const double x2 = (x1 - r1) * 128.0;
-      a = int(r0);
-      b = int(r1);
-      c = int(rint(x2));
-      a = a > 127 ? 127 : a < -127 ? -127 : a;
+      // x = w * 127 / max rounds once; the residual steps are exact
+      const float x = fminf(fmaxf(w[k] * inv, -127.f), 127.f);
+      const float m0 = x + kMagic;
+      const float x1 = (x - (m0 - kMagic)) * 128.f;  // |x1| <= 64
+      const float m1 = x1 + kMagic;
+      const float m2 = (x1 - (m1 - kMagic)) * 128.f + kMagic;
+      a = __float_as_uint(m0);
+      b = __float_as_uint(m1);
+      c = __float_as_uint(m2);
     }
-    q0[k] = int8_t(a);
-    q0[plane + k] = int8_t(b);
-    q0[2 * plane + k] = int8_t(c);
+    q0[k] = int8_t(a & 0xFFu);
+    q0[plane + k] = int8_t(b & 0xFFu);
+    q0[2 * plane + k] = int8_t(c & 0xFFu);
   }
 }
 
