@@ -624,3 +624,35 @@ def test_device_replay_matches_host_batches(tlg, oracle, fmt):
             rep.close()
     assert np.array_equal(res[0][0], res[1][0])
     assert res[0][1] == res[1][1]
+
+
+def test_boundary_errors_match_reference_exception_types(tlg, oracle):
+    """Misuse of the newer entry points fails with TLG_INVALID_ARGUMENT (the reference's
+    std::invalid_argument), never silently."""
+    from paper_2011_12895_b200._capi import SegmentBatchView
+    S, T, D, A, hidden = 4, 8, 40, 5, (32, 32)
+    lrn = tlg.Learner("mlp", D, A, hidden, max_segments=S, unroll_len=T, obs_u8=True,
+                      optimizer="sgd")
+    lrn.set_hyper(learning_rate=0.05, batch_size=S, unroll_len=T)
+    lrn.set_params(init_params(oracle, Shape(2, D, A, hidden), 3))
+    b = tlg.synth.make_segments(S, T, D, A, seed=1, obs_kind="binary", obs_u8=True)
+    pb = b.slice(0, S)
+    pb.obs = tlg.synth.pack_bits(b.obs)
+    v = SegmentBatchView(pb, bits=True, obs_dim=D)
+    v.c.obs_pitch = 3  # shorter than ceil(40 / 8) = 5 bytes
+    with pytest.raises(tlg.InvalidArgument, match="obs_pitch"):
+        lrn.train_step(v)
+    rep = tlg.Replay(lrn, 8, bits=True)
+    good = SegmentBatchView(pb, bits=True, obs_dim=D)
+    with pytest.raises(tlg.InvalidArgument, match="slot out of range"):
+        rep.put(np.arange(4, 8) + 4, good)
+    with pytest.raises(tlg.InvalidArgument, match="format"):
+        rep.put(np.arange(4), b)  # uint8 planes into a bit-packed ring
+    rep.put(np.arange(4), good)
+    with pytest.raises(tlg.InvalidArgument, match="max_segments"):
+        rep.train_step(np.arange(8), n_shards=1)
+    st = rep.train_step(np.arange(4))
+    assert np.isfinite(st[0]["loss"])
+    with pytest.raises(tlg.InvalidArgument, match="parameter count"):
+        lrn.set_teacher(np.zeros(3))
+    rep.close()
