@@ -171,6 +171,9 @@ void dispatch_bn(bool a_mn, bool b_mn, bool a_lo, bool b_lo, int epi, int u8,
     if (a_lo) return run_if_fits<BN, false, false, true, true, kEpiFwdTanh>(ah, al, bh, bl, em, p, grid, s);
     return run_if_fits<BN, false, false, false, true, kEpiFwdTanh>(ah, al, bh, bl, em, p, grid, s);
   }
+  // fused top layer + heads + PPO loss + dZ_L (A = activations, B = W, both 3-pass)
+  if (epi == kEpiFwdLoss && !a_mn && !b_mn && a_lo && b_lo)
+    return run_if_fits<BN, false, false, true, true, kEpiFwdLoss>(ah, al, bh, bl, em, p, grid, s);
   // dX: A = dZ (K-major), B = W (MN-major)
   if (!a_mn && b_mn && a_lo && b_lo && epi == kEpiBwdTanh)
     return run_if_fits<BN, false, true, true, true, kEpiBwdTanh>(ah, al, bh, bl, em, p, grid, s);
@@ -214,7 +217,14 @@ LaunchInfo launch(const Operand& A, const Operand& B, int M, int N, int K, int e
   // else 128 (short-K fused epilogues are the critical path; narrower tiles balance).
   int BN = N > 128 ? 256 : N > 64 ? 128 : 64;
   const int kb_tile = p.kb_per_split;  // K blocks per tile
-  if (BN == 256 && epi != kEpiStore && kb_tile < 16 && !std::getenv("TLG_GEMM_WIDE")) BN = 128;
+  if (BN == 256 && epi != kEpiStore && epi != kEpiFwdLoss && kb_tile < 16 &&
+      !std::getenv("TLG_GEMM_WIDE"))
+    BN = 128;
+  if (epi == kEpiFwdLoss) {  // whole rows per tile, CTA pairs (the only plan that fits)
+    if (N > 256 || M < 2 * kBM || p.head_k < 2 || p.head_k > 8)
+      throw CudaError("gemm: fused loss epilogue needs N <= 256, M >= 256, 2 <= A+1 <= 8");
+    BN = 256;
+  }
   if (const char* e = std::getenv("TLG_GEMM_MAX_BN")) {  // tuning experiments only
     const int cap = std::atoi(e);
     while (BN > 64 && BN > cap) BN /= 2;
@@ -227,9 +237,12 @@ LaunchInfo launch(const Operand& A, const Operand& B, int M, int N, int K, int e
     const long tiles2 = long(ceil_div(M, 2 * kBM)) * ceil_div(N, BN) * splits;
     if (BN >= 128 && M >= 2 * kBM && tiles2 >= num_sms() / 2 && kb_tile >= 8) cg = 2;
     if (const char* e = std::getenv("TLG_GEMM_CG")) cg = std::atoi(e) == 2 && BN >= 128 ? 2 : 1;
+    if (epi == kEpiFwdLoss) cg = 2;
     if (const char* e = std::getenv("TLG_GEMM_CG_U8"))  // tuning experiments only
       if ((A.u8 || B.u8) && std::atoi(e) == 2 && BN >= 128) cg = 2;
-    if (BN == 64 || smem_plan(BN, a_lo0, b_lo0, epi, u8_0, cg).bytes <= 227 * 1024) break;
+    if (BN == 64 || epi == kEpiFwdLoss ||
+        smem_plan(BN, a_lo0, b_lo0, epi, u8_0, cg).bytes <= 227 * 1024)
+      break;
     BN /= 2;
   }
   const int u8 = A.u8 ? 1 : B.u8 ? 2 : 0;

@@ -33,6 +33,32 @@ enum Epi : int {
   kEpiFwdTanh = 0,   // out = tanh(acc + bias[n])          -> out (full) / out_lo planes
   kEpiBwdTanh = 1,   // out = acc * (1 - h[m][n]^2)         -> out (full) / out_lo planes
   kEpiStore = 2,     // ws[split][m][n] = acc               (split-K partials, fp32)
+  kEpiFwdLoss = 3,   // last trunk layer + heads + PPO loss: writes dZ_L, not h_L (below)
+};
+
+// kEpiFwdLoss: the top trunk layer's forward fused with the policy/value heads, the PPO
+// loss (rlmath.cpp:116-185) and dZ_L = (dlogits . W_head) * (1 - h^2), per row of the
+// tile (BN = N: the whole row is in TMEM).  Pass 1 over the row's chunks: h = tanh(acc+b)
+// and the head dot products; the per-row loss math; pass 2: h again, dZ_L (full + tf32
+// residual planes, TMA-stored), and per-CTA partial sums of the head weight gradient
+// sum_f d_k h_j, of the top bias gradient sum_f dZ_L and of the head bias gradient and
+// loss statistics -- fixed order, one partial row per CTA.  h_L never reaches HBM.
+struct LossEpi {
+  const int* action;
+  const float* blogp;
+  const int* valid;
+  int T;
+  const float* adv;
+  const float* target;
+  const double* stats;  // StepStatsDev: mean [2], sd [3], inv_n [4]
+  float clip_eps, vf_coef, ent_coef;
+  long bpi, bv;          // head bias offsets in `params` (-1: none)
+  const float* params;
+  float* hg_partial;     // [ctas][A1][N]
+  float* db_partial;     // [ctas][N]
+  double* loss_partial;  // [ctas][5]
+  float* bias_partial;   // [ctas][A1]
+  int* err;
 };
 
 constexpr int kBM = 128;
@@ -69,6 +95,7 @@ struct Params {
   // U8 == 1: also write the expanded fp32 A operand (exact) to this [M][K] buffer
   // (tmAct map) from the n_tile == 0 CTAs, so a later GEMM can read it as plain fp32
   float* a_expand;
+  LossEpi loss;  // kEpiFwdLoss only
 };
 
 // ---------------------------------------------------------------------------
@@ -263,14 +290,17 @@ constexpr SmemPlan smem_plan(int BN, bool a_lo, bool b_lo, int epi, int u8, int 
   // TMA-prefetched activation block (bwd), + 1 KB of head weights (fwd).  out and out_lo
   // share one block (stores serialised) when that buys the pipeline a third stage: the
   // uint8-input forward and the wide 3-pass tiles, whose long K loops hide it.
-  q.extra = epi == kEpiBwdTanh ? kEpiWarps * BN * 4 + kColMax * 4 : 0;
-  const int head = epi == kEpiFwdTanh ? 1024 : 0;
+  q.extra = epi == kEpiBwdTanh   ? kEpiWarps * BN * 4 + kColMax * 4
+            : epi == kEpiFwdLoss ? kEpiWarps * (8 * BN + BN) * 4  // per-warp hg [8][BN], db [BN]
+                                 : 0;
+  const int head = epi == kEpiFwdTanh ? 1024 : epi == kEpiFwdLoss ? 2048 : 0;
   const int ring = q.u8_ring * q.u8_slot;
   auto epi_bytes = [&](int blocks) { return kEpiWarps * (blocks * 4096 + head) + q.extra; };
-  const int sep_blocks = epi == kEpiStore ? 1 : 2 + (epi == kEpiBwdTanh ? 1 : 0);
+  // blocks: out (+ out_lo) (+ act for bwd, + h staging for the fused loss)
+  const int sep_blocks = epi == kEpiStore ? 1 : 2 + (epi == kEpiBwdTanh || epi == kEpiFwdLoss ? 1 : 0);
   const int sep = plan_stages(q.stage, epi_bytes(sep_blocks), ring);
   const int shr = plan_stages(q.stage, epi_bytes(sep_blocks - 1), ring);
-  q.share_lo = epi != kEpiStore && (u8 == 1 || (sep < 3 && shr > sep));
+  q.share_lo = epi != kEpiStore && epi != kEpiFwdLoss && (u8 == 1 || (sep < 3 && shr > sep));
   q.epi_blocks = q.share_lo ? sep_blocks - 1 : sep_blocks;
   q.warp_epi = q.epi_blocks * 4096 + head;
   q.stages = q.share_lo ? shr : sep;
@@ -696,6 +726,265 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
       }
     }
     if (expand && ct == 0) bulk_wait_all();
+  } else if (EPI == kEpiFwdLoss) {
+    // ===== fused forward + heads + PPO loss + dZ_L epilogue (see LossEpi) =====
+    const int q = warp & 3;
+    const int ew = warp - 2;
+    const uint32_t blk = sbase + S::kEpiOff + uint32_t(ew * S::kWarpEpi);
+    uint8_t* bp = smem + S::kEpiOff + ew * S::kWarpEpi;  // [out][lo][h][wsm 1K][dsm 1K]
+    float* wsm = reinterpret_cast<float*>(bp + 3 * 4096);         // head weights [8][32]
+    float* dsm = reinterpret_cast<float*>(bp + 3 * 4096 + 1024);  // d [32 rows][8]
+    float* hgw = reinterpret_cast<float*>(smem + S::kEpiOff + kEpiWarps * S::kWarpEpi) +
+                 long(ew) * 9 * BN;  // this warp's head-grad [8][BN] then db [BN]
+    float* dbw = hgw + 8 * BN;
+    const LossEpi& L = p.loss;
+    const int A1 = p.head_k, A = A1 - 1;
+    for (int i = lane; i < 9 * BN; i += 32) hgw[i] = 0.f;
+    const double mean = L.stats[2], sd = L.stats[3];
+    const float inv_n = float(L.stats[4]);
+    double sl[5] = {0, 0, 0, 0, 0};  // loss, ratio, entropy, value loss, clipped (this warp)
+    float sb[8];                      // head bias gradient partials (this warp, lane 0)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) sb[k] = 0.f;
+    auto load_w = [&](int nb) {       // head weights of one 32-column chunk -> wsm
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        float wk = 0.f;
+        if (k < A1 && nb + lane < p.N) {
+          const float* wrow = k < A ? p.head_w + long(k) * p.N : p.head_wv;
+          wk = __ldg(wrow + nb + lane);
+        }
+        wsm[k * 32 + lane] = wk;
+      }
+      __syncwarp();
+    };
+    int it = 0;
+    for (int t = cl_id; t < num_tiles; t += n_cl, ++it) {
+      int mt, nt, sp;
+      tm.decode(t, mt, nt, sp);
+      const int m0 = mt * kBM * CG + int(rank) * kBM;
+      const int rbase = m0 + q * 32;
+      const long f = rbase + lane;  // this thread's frame (row)
+      const int acc_buf = it & 1;
+      mbar_wait(bar_tfull + 8 * acc_buf, (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + uint32_t(acc_buf * S::kAccCols) + (uint32_t(q * 32) << 16);
+      // ---- pass 1: h and the head dot products
+      float z[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) z[k] = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(tbase + uint32_t(c), r);
+        const float bl = (c + lane < p.N) ? __ldg(p.bias + c + lane) : 0.f;
+        float h[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) h[j] = tanhf(__uint_as_float(r[j]) + __shfl_sync(0xffffffffu, bl, j));
+        load_w(c);
+#pragma unroll
+        for (int j4 = 0; j4 < 8; ++j4) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            if (k < A1) {
+              const float4 w4 = *reinterpret_cast<const float4*>(wsm + k * 32 + 4 * j4);
+              z[k] = fmaf(w4.x, h[4 * j4], z[k]);
+              z[k] = fmaf(w4.y, h[4 * j4 + 1], z[k]);
+              z[k] = fmaf(w4.z, h[4 * j4 + 2], z[k]);
+              z[k] = fmaf(w4.w, h[4 * j4 + 3], z[k]);
+            }
+          }
+        }
+        __syncwarp();
+      }
+      // ---- the per-row PPO loss (rlmath.cpp:129-182), as loss_math_kernel
+      float d[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) d[k] = 0.f;
+      bool valid = false;
+      if (f < p.M) {
+        const int sg = int(f / L.T), tt = int(f % L.T);
+        valid = tt < L.valid[sg];
+      }
+      if (valid) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (k < A1) {
+            const long boff = k < A ? (L.bpi >= 0 ? L.bpi + k : -1) : L.bv;
+            if (boff >= 0) z[k] += L.params[boff];
+          }
+        float mx = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (k < A) mx = fmaxf(mx, z[k]);
+        float se = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (k < A) se += expf(z[k] - mx);
+        const float lse = mx + logf(se);
+        float pk[8], lpk[8], ent = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          lpk[k] = z[k] - lse;
+          pk[k] = k < A ? expf(lpk[k]) : 0.f;
+          if (k < A && pk[k] > 0.f) ent -= pk[k] * lpk[k];
+        }
+        const int ar = L.action[f];
+        if (ar < 0 || ar >= A) atomicOr(L.err, 2 /* kErrActionRange */);
+        const int a = min(max(ar, 0), A - 1);
+        float logp = 0.f, V = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          if (k == a) logp = lpk[k];
+          if (k == A) V = z[k];
+        }
+        const float verr = V - L.target[f];
+        const float ad = float((double(L.adv[f]) - mean) / sd);
+        const float ratio = expf(logp - L.blogp[f]);
+        const float clipped = fminf(fmaxf(ratio, 1.f - L.clip_eps), 1.f + L.clip_eps);
+        const float t1 = ratio * ad, t2 = clipped * ad;
+        const float loss_i = -fminf(t1, t2) + L.vf_coef * verr * verr - L.ent_coef * ent;
+        const bool surr = t1 <= t2;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (k < A) {
+            float g = L.ent_coef * pk[k] * ((pk[k] > 0.f ? lpk[k] : 0.f) + ent);
+            if (surr) g += -ad * ratio * ((k == a ? 1.f : 0.f) - pk[k]);
+            d[k] = g * inv_n;
+          }
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (k == A) d[k] = 2.f * L.vf_coef * verr * inv_n;
+        sl[0] += loss_i;
+        sl[1] += ratio;
+        sl[2] += ent;
+        sl[3] += double(verr) * double(verr);
+        if (t2 < t1) sl[4] += 1.0;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        dsm[lane * 8 + k] = d[k];
+        const float t = warp_sum(d[k]);
+        if (lane == 0) sb[k] += t;
+      }
+      __syncwarp();
+      // ---- pass 2: dZ_L and the gradient partials
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        const int nb = c;
+        uint32_t r[32];
+        tmem_ld32(tbase + uint32_t(c), r);
+        const float bl = (c + lane < p.N) ? __ldg(p.bias + c + lane) : 0.f;
+        float h[32], o[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) h[j] = tanhf(__uint_as_float(r[j]) + __shfl_sync(0xffffffffu, bl, j));
+        load_w(c);
+#pragma unroll
+        for (int j4 = 0; j4 < 8; ++j4) {
+          float dh[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            if (k < A1) {
+              const float4 w4 = *reinterpret_cast<const float4*>(wsm + k * 32 + 4 * j4);
+              dh[0] = fmaf(d[k], w4.x, dh[0]);
+              dh[1] = fmaf(d[k], w4.y, dh[1]);
+              dh[2] = fmaf(d[k], w4.z, dh[2]);
+              dh[3] = fmaf(d[k], w4.w, dh[3]);
+            }
+          }
+#pragma unroll
+          for (int e = 0; e < 4; ++e) o[4 * j4 + e] = dh[e] * (1.f - h[4 * j4 + e] * h[4 * j4 + e]);
+        }
+        // staging: dZ (full, residual) for the TMA store, h for the head-gradient sums
+        if (lane == 0) bulk_wait_read();
+        __syncwarp();
+#pragma unroll
+        for (int j4 = 0; j4 < 8; ++j4) {
+          *reinterpret_cast<float4*>(bp + swz(lane, j4)) =
+              make_float4(o[4 * j4], o[4 * j4 + 1], o[4 * j4 + 2], o[4 * j4 + 3]);
+          *reinterpret_cast<float4*>(bp + 4096 + swz(lane, j4)) =
+              make_float4(o[4 * j4] - tf32_hi(o[4 * j4]), o[4 * j4 + 1] - tf32_hi(o[4 * j4 + 1]),
+                          o[4 * j4 + 2] - tf32_hi(o[4 * j4 + 2]),
+                          o[4 * j4 + 3] - tf32_hi(o[4 * j4 + 3]));
+          *reinterpret_cast<float4*>(bp + 8192 + swz(lane, j4)) =
+              make_float4(h[4 * j4], h[4 * j4 + 1], h[4 * j4 + 2], h[4 * j4 + 3]);
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tmOut, nb, rbase, blk);
+          tma_store_2d(&tmOutLo, nb, rbase, blk + 4096);
+          bulk_commit();
+        }
+        // lane = column j: sum over this warp's 32 rows (rows past M carry d = 0, and
+        // their dZ is 0 since d = 0)
+        float hgs[8], dbs = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) hgs[k] = 0.f;
+#pragma unroll 4
+        for (int rr = 0; rr < 32; ++rr) {
+          const float hv = *reinterpret_cast<const float*>(bp + 8192 + swz(rr, lane >> 2) + (lane & 3) * 4);
+          const float ov = *reinterpret_cast<const float*>(bp + swz(rr, lane >> 2) + (lane & 3) * 4);
+          dbs += ov;
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (k < A1) hgs[k] = fmaf(dsm[rr * 8 + k], hv, hgs[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (k < A1) hgw[k * BN + c + lane] += hgs[k];
+        dbw[c + lane] += dbs;
+        __syncwarp();
+      }
+      // TMEM buffer drained
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (CG == 2) mbar_arrive_cluster(map_rank0(bar_tempty + 8 * acc_buf));
+        else mbar_arrive(bar_tempty + 8 * acc_buf);
+      }
+    }
+    if (lane == 0) bulk_wait_all();
+    // ---- this CTA's partial rows: the 4 warps in order (deterministic)
+    double* sld = reinterpret_cast<double*>(wsm);  // 5 doubles + 8 floats per warp
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+      const double v = warp_sum(sl[i]);
+      if (lane == 0) sld[i] = v;
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) wsm[10 + k] = sb[k];
+    }
+    named_bar(1, kEpiWarps * 32);
+    const int tid = threadIdx.x - 64;
+    const float* hg0 = reinterpret_cast<float*>(smem + S::kEpiOff + kEpiWarps * S::kWarpEpi);
+    for (int i = tid; i < A1 * p.N; i += kEpiWarps * 32) {
+      const int k = i / p.N, j = i % p.N;
+      float v = 0.f;
+      for (int w = 0; w < kEpiWarps; ++w) v += hg0[long(w) * 9 * BN + k * BN + j];
+      L.hg_partial[long(blockIdx.x) * A1 * p.N + i] = v;
+    }
+    for (int j = tid; j < p.N; j += kEpiWarps * 32) {
+      float v = 0.f;
+      for (int w = 0; w < kEpiWarps; ++w) v += hg0[long(w) * 9 * BN + 8 * BN + j];
+      L.db_partial[long(blockIdx.x) * p.N + j] = v;
+    }
+    if (tid < 5 + A1) {
+      auto wbase = [&](int w) {
+        return reinterpret_cast<const uint8_t*>(smem + S::kEpiOff + w * S::kWarpEpi + 3 * 4096);
+      };
+      if (tid < 5) {
+        double v = 0.0;
+        for (int w = 0; w < kEpiWarps; ++w) v += reinterpret_cast<const double*>(wbase(w))[tid];
+        L.loss_partial[long(blockIdx.x) * 5 + tid] = v;
+      } else {
+        const int k = tid - 5;
+        float v = 0.f;
+        for (int w = 0; w < kEpiWarps; ++w) v += reinterpret_cast<const float*>(wbase(w))[10 + k];
+        L.bias_partial[long(blockIdx.x) * A1 + k] = v;
+      }
+    }
   } else {
     // ===== Epilogue: warps 2..5 own TMEM lane quadrants (warp % 4) =====
     // Per 32-column chunk each warp handles a 32x32 block: TMEM -> registers (thread =

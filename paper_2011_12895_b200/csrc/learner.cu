@@ -282,7 +282,9 @@ struct tlg_learner {
     seg_partial = mem.add<double>(2 * S_max);
     stats = mem.add<tlg::StepStatsDev>(kMaxLocalShards);
     err = mem.add<int>(4);
-    const long nblk = (F_max + tlg::kLossFrames - 1) / tlg::kLossFrames;
+    // partial rows: one per loss block, or one per persistent CTA of the fused loss GEMM
+    const long nblk = std::max<long>((F_max + tlg::kLossFrames - 1) / tlg::kLossFrames,
+                                     tlg::gemm::num_sms());
     hg_partial = mem.add<float>(nblk * A1 * long(net.head.H) + nblk * A1);
     loss_partial = mem.add<double>(nblk * 5);
     dzh = mem.add<float>(F_max * A1);
@@ -516,6 +518,17 @@ struct tlg_learner {
   bool loss_reads_parts() const {
     return cfg.algo == TLG_ALGO_PPO && net.L > 0 && fused_head();
   }
+  // PPO without a teacher: the top trunk GEMM's epilogue also runs the loss and writes
+  // dZ_L directly (gemm kEpiFwdLoss; h_L never reaches HBM).  Opt-in (TLG_FUSED_LOSS=1):
+  // correct, but at C3 the two-pass epilogue makes that GEMM epilogue-bound (276 us vs
+  // 208 us for forward + loss kernels, profiles/r01_fused_loss.md).
+  const bool fused_loss_disabled = std::getenv("TLG_FUSED_LOSS") == nullptr;
+  bool fused_loss_ok(long F) const {
+    return loss_reads_parts() && !teacher_active() && !fused_loss_disabled &&
+           net.head.H <= 256 && F >= 256;
+  }
+  const tlg::gemm::LossEpi* fuse_loss_epi = nullptr;  // set while the fused step runs
+  int fused_ctas = 0;
 
   void forward_heads(const Staged& sg, const float* P, const float* P_lo, const float* x0,
                      const float* x0_lo, float* out, float* out_tlogp, bool timed,
@@ -542,6 +555,12 @@ struct tlg_learner {
         p.head_k = int(net.A) + 1;
         p.head_part = head_part;
       }
+      const bool fuse_loss = fuse_head && fuse_loss_epi != nullptr;
+      if (fuse_loss) {  // ... and the PPO loss: the epilogue writes dZ_L instead of h_L
+        p.loss = *fuse_loss_epi;
+        p.out_hi = dz[l];
+        p.out_lo = dz_lo[l];
+      }
       if (l == 0 && sg.x0_bits != nullptr && !wq_fresh) {
         // this step's layer-1 weights -> int8 pieces (once per step)
         tlg::gemm::launch_quantize_rows(P + net.w_off[0], outw, in, in, wq, wq_kp, wq_scale,
@@ -564,6 +583,11 @@ struct tlg_learner {
         bn = tlg::gemm::launch_i8x2_fwd(act_q, w2q, in, w2_scale, p.bias, int(F), outw, in,
                                         act[1], p.out_lo, outw, p.head_w, p.head_wv, p.head_k,
                                         p.head_part, stream).bn;
+      } else if (fuse_loss) {
+        const tlg::gemm::LaunchInfo li =
+            tlg::gemm::launch(A, B, int(F), outw, in, tlg::gemm::kEpiFwdLoss, p, 1, stream);
+        bn = li.bn;
+        fused_ctas = li.ctas;
       } else {
         bn = tlg::gemm::launch(A, B, int(F), outw, in, tlg::gemm::kEpiFwdTanh, p, 1, stream).bn;
       }
@@ -583,53 +607,10 @@ struct tlg_learner {
     launches += 1;
   }
 
-  void compute_shard(const Staged& sg, int shard, float* gtarget) {
-    tlg::StepStatsDev* st = stats + shard;
-    const tlg::BatchDev bd = sg.bd;
-    const float* x0 = sg.x0;
-    const bool obs_exact = sg.exact;
-    x0_u8 = sg.x0_u8;
-    S_last = bd.S;
-    const long F = long(bd.S) * T;
-    const long D = net.D;
-    const float* x0_lo = nullptr;
-    if (net.L > 0 && !obs_exact) {
-      tlg::launch_split_lo(x0, obs_lo, F * D, stream);
-      ++launches;
-      x0_lo = obs_lo;
-    }
-    if (shard == 0) mark(1);
-    if (teacher_active()) {
-      // the teacher's head outputs first (the student's forward then reuses the buffers)
-      forward_heads(sg, teacher, teacher_lo, x0, x0_lo, t_head_out, nullptr, false);
-      wq_fresh = false;  // layer-1 int8 pieces must be rebuilt from the student's weights
-    }
-    const bool parts = loss_reads_parts();
-    forward_heads(sg, params, params_lo, x0, x0_lo, head_out, tlogp, shard == 0, !parts);
-    if (shard == 0) mark(2);
-    // ---- heads, returns, loss
-    const float* hL = net.L ? act[net.L - 1] : x0;
-    const long ldh = net.head.H;
-    tlg::HyperDev hd{float(hp.gamma), float(hp.lam), float(hp.clip_eps), float(hp.vf_coef),
-                     float(hp.ent_coef), float(hp.rho_bar), float(hp.c_bar), hp.adv_norm,
-                     float(hp.kl_teacher_coef)};
-    const int algo = int(cfg.algo);
-    tlg::launch_returns(bd, algo, hd, tlogp, adv, target, seg_partial, err, stream);
-    tlg::launch_finalize_adv(seg_partial, bd, hp.adv_norm, st, err, stream);
-    const int loss_kind = algo == TLG_ALGO_VTRACE ? 1 : 0;
-    const tlg::LossLaunch ll = tlg::launch_loss_backward(
-        net.head, params, hL, ldh, bd, head_out, adv, target, st, hd, loss_kind, dzh,
-        net.L ? dz[net.L - 1] : nullptr, net.L ? dz_lo[net.L - 1] : nullptr, hg_partial,
-        loss_partial, col_partial, stream, teacher_active() ? t_head_out : nullptr,
-        parts ? head_part : nullptr, head_tiles, err);
-    tlg::launch_head_grad_reduce(net.head, hg_partial, loss_partial, ll, gtarget, st, stream);
-    launches += 6;
-    if (net.L > 0) {  // db of the top trunk layer from the loss kernel's column partials
-      tlg::launch_rows_reduce(col_partial, ll.stream_blocks, net.head.H, net.head.H,
-                              gtarget + net.b_off[net.L - 1], stream);
-      ++launches;
-    }
-    if (shard == 0) mark(3);
+  // Trunk backward from dZ_L: dW / db per layer (split-K, fixed-order reductions), dX with
+  // tanh' for the layer below, then the rank-ordered shard accumulation and failure guard.
+  void backward_trunk(const Staged& sg, int shard, float* gtarget, const float* x0,
+                      const float* x0_lo, long F) {
     // ---- backward trunk
     using tlg::gemm::Operand;
     for (int l = int(net.L) - 1; l >= 0; --l) {
@@ -710,6 +691,96 @@ struct tlg_learner {
       accumulate_grad();  // grad += shard gradient, in rank order (learner.cpp:145-147)
     }
     set_guard(shard);
+  }
+
+  void compute_shard(const Staged& sg, int shard, float* gtarget) {
+    tlg::StepStatsDev* st = stats + shard;
+    const tlg::BatchDev bd = sg.bd;
+    const float* x0 = sg.x0;
+    const bool obs_exact = sg.exact;
+    x0_u8 = sg.x0_u8;
+    S_last = bd.S;
+    const long F = long(bd.S) * T;
+    const long D = net.D;
+    const float* x0_lo = nullptr;
+    if (net.L > 0 && !obs_exact) {
+      tlg::launch_split_lo(x0, obs_lo, F * D, stream);
+      ++launches;
+      x0_lo = obs_lo;
+    }
+    if (shard == 0) mark(1);
+    if (teacher_active()) {
+      // the teacher's head outputs first (the student's forward then reuses the buffers)
+      forward_heads(sg, teacher, teacher_lo, x0, x0_lo, t_head_out, nullptr, false);
+      wq_fresh = false;  // layer-1 int8 pieces must be rebuilt from the student's weights
+    }
+    const bool parts = loss_reads_parts();
+    tlg::HyperDev hd{float(hp.gamma), float(hp.lam), float(hp.clip_eps), float(hp.vf_coef),
+                     float(hp.ent_coef), float(hp.rho_bar), float(hp.c_bar), hp.adv_norm,
+                     float(hp.kl_teacher_coef)};
+    const int algo = int(cfg.algo);
+    if (fused_loss_ok(F)) {
+      // GAE + advantage statistics need no forward output (rlmath.cpp:62-78, 18-34)
+      tlg::launch_returns(bd, algo, hd, tlogp, adv, target, seg_partial, err, stream);
+      tlg::launch_finalize_adv(seg_partial, bd, hp.adv_norm, st, err, stream);
+      tlg::gemm::LossEpi le{};
+      le.action = bd.action;
+      le.blogp = bd.blogp;
+      le.valid = bd.valid;
+      le.T = T;
+      le.adv = adv;
+      le.target = target;
+      le.stats = reinterpret_cast<const double*>(st);
+      le.clip_eps = hd.clip_eps;
+      le.vf_coef = hd.vf_coef;
+      le.ent_coef = hd.ent_coef;
+      le.bpi = net.head.bpi;
+      le.bv = net.head.bv;
+      le.params = params;
+      le.hg_partial = hg_partial;
+      le.db_partial = col_partial;
+      le.loss_partial = loss_partial;
+      le.err = err;
+      // the CTA count is known only at launch: bias partials follow the weight partials of
+      // at most num_sms() rows
+      const long nw = long(net.A + 1) * net.head.H;
+      le.bias_partial = hg_partial + long(tlg::gemm::num_sms()) * nw;
+      fuse_loss_epi = &le;
+      forward_heads(sg, params, params_lo, x0, x0_lo, head_out, tlogp, shard == 0, false);
+      fuse_loss_epi = nullptr;
+      if (shard == 0) mark(2);
+      tlg::LossLaunch ll{fused_ctas, fused_ctas};
+      tlg::launch_head_grad_reduce(net.head, hg_partial, loss_partial, ll, gtarget, st, stream,
+                                   le.bias_partial);
+      tlg::launch_rows_reduce(col_partial, fused_ctas, net.head.H, net.head.H,
+                              gtarget + net.b_off[net.L - 1], stream);
+      launches += 5;
+      if (shard == 0) mark(3);
+      backward_trunk(sg, shard, gtarget, x0, x0_lo, F);
+      return;
+    }
+    forward_heads(sg, params, params_lo, x0, x0_lo, head_out, tlogp, shard == 0, !parts);
+    if (shard == 0) mark(2);
+    // ---- heads, returns, loss
+    const float* hL = net.L ? act[net.L - 1] : x0;
+    const long ldh = net.head.H;
+    tlg::launch_returns(bd, algo, hd, tlogp, adv, target, seg_partial, err, stream);
+    tlg::launch_finalize_adv(seg_partial, bd, hp.adv_norm, st, err, stream);
+    const int loss_kind = algo == TLG_ALGO_VTRACE ? 1 : 0;
+    const tlg::LossLaunch ll = tlg::launch_loss_backward(
+        net.head, params, hL, ldh, bd, head_out, adv, target, st, hd, loss_kind, dzh,
+        net.L ? dz[net.L - 1] : nullptr, net.L ? dz_lo[net.L - 1] : nullptr, hg_partial,
+        loss_partial, col_partial, stream, teacher_active() ? t_head_out : nullptr,
+        parts ? head_part : nullptr, head_tiles, err);
+    tlg::launch_head_grad_reduce(net.head, hg_partial, loss_partial, ll, gtarget, st, stream);
+    launches += 6;
+    if (net.L > 0) {  // db of the top trunk layer from the loss kernel's column partials
+      tlg::launch_rows_reduce(col_partial, ll.stream_blocks, net.head.H, net.head.H,
+                              gtarget + net.b_off[net.L - 1], stream);
+      ++launches;
+    }
+    if (shard == 0) mark(3);
+    backward_trunk(sg, shard, gtarget, x0, x0_lo, F);
   }
 
   // Learner::TrainStep over `n` local shards (+ the communicator's other ranks).

@@ -1106,13 +1106,14 @@ LossLaunch launch_loss_backward(const HeadDesc& hd, const float* params, const f
 
 void launch_head_grad_reduce(const HeadDesc& hd, const float* hg_partial,
                              const double* loss_partial, const LossLaunch& ll, float* grad,
-                             StepStatsDev* st, cudaStream_t s) {
+                             StepStatsDev* st, cudaStream_t s, const float* bias_partial) {
   const long nw = long(hd.A + 1) * hd.H;
   head_grad_reduce_kernel<<<ceil_div(nw, 32), rows_reduce_threads(nw), 0, s>>>(
       hd, hg_partial, ll.stream_blocks, grad);
   TLG_CHECK_LAUNCH();
   head_bias_stats_kernel<<<1, 32 * (hd.A + 1 + 5), 0, s>>>(
-      hd, hg_partial + long(ll.stream_blocks) * nw, loss_partial, ll.math_blocks, grad, st);
+      hd, bias_partial ? bias_partial : hg_partial + long(ll.stream_blocks) * nw, loss_partial,
+      ll.math_blocks, grad, st);
   TLG_CHECK_LAUNCH();
 }
 

@@ -437,15 +437,19 @@ def test_bit_packed_and_staged_inputs_match(tlg, oracle, D, hidden):
         assert close(res[0], res[1], 1e-5), worst(res[0], res[1])
 
 
+@pytest.mark.parametrize("fused_loss", [False, True], ids=["", "fused-loss"])
 @pytest.mark.parametrize("optimizer", ["sgd", "adam"])
 @pytest.mark.parametrize("shape_case", [(1936, (256, 256), 32, 16), (200, (64, 32), 8, 24)],
                          ids=["c3-like", "small"])
-def test_bit_planes_int8_layer1_match_oracle(tlg, oracle, shape_case, optimizer):
+def test_bit_planes_int8_layer1_match_oracle(tlg, oracle, shape_case, optimizer, fused_loss,
+                                            monkeypatch):
     """Bit-packed binary planes: layer 1 runs on the int8 tensor cores (fixed-point
     weight pieces, gemm_i8.cuh); losses, gradients and parameters stay within the
     north-star tolerances of the fp64 oracle over several steps."""
     from paper_2011_12895_b200._capi import SegmentBatchView
     D, hidden, T, S = shape_case
+    if fused_loss:  # the top GEMM's epilogue runs the PPO loss (gemm kEpiFwdLoss)
+        monkeypatch.setenv("TLG_FUSED_LOSS", "1")
     A = 6
     shape = Shape(2, D, A, hidden)
     lr = 0.05 if optimizer == "sgd" else 3e-3
