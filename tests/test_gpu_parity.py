@@ -319,6 +319,39 @@ def test_local_shards_match_oracle(tlg, oracle, algo):
         lrn.set_params(p)
 
 
+@pytest.mark.parametrize("algo", ["ppo", "ppo_vtrace"])
+def test_local_shards_bit_planes_int8_match_oracle(tlg, oracle, algo):
+    """Several local shards through the int8 layer-1 path (per-shard dZ_1 maxima and
+    pieces, rank-ordered gradient sum) against the oracle's multi-shard step."""
+    from paper_2011_12895_b200._capi import SegmentBatchView
+    S, T, D, A, hidden = 8, 32, 200, 6, (64, 32)
+    shape = Shape(2, D, A, hidden)
+    hp = dict(learning_rate=0.05, batch_size=S, unroll_len=T)
+    lrn = tlg.Learner("mlp", D, A, hidden, algo=algo, optimizer="sgd", max_segments=S,
+                      unroll_len=T, obs_u8=True)
+    lrn.set_hyper(**hp)
+    p = init_params(oracle, shape, 23)
+    lrn.set_params(p)
+    for step in range(2):
+        shards = [tlg.synth.make_segments(S, T, D, A, seed=2000 + 10 * step + r,
+                                          obs_kind="binary", obs_u8=True) for r in range(3)]
+        views = []
+        for b in shards:
+            pb = b.slice(0, S)
+            pb.obs = tlg.synth.pack_bits(b.obs)
+            views.append(SegmentBatchView(pb, bits=True, obs_dim=D))
+        sts = lrn.train_step_shards(views)
+        p_new, g, osts, _ = oracle.learner_step(shape, p, OHyper(**hp), ALGO[algo],
+                                                [to_oracle(b) for b in shards])
+        for st, ost in zip(sts, osts):
+            assert close(st["loss"], ost["loss"], 1e-4)
+        gscale = max(1e-30, float(np.max(np.abs(g))))
+        assert np.max(np.abs(lrn.get_grad() - g)) <= 1e-4 * gscale
+        assert close(lrn.get_params(), p_new, 1e-4), worst(lrn.get_params(), p_new)
+        p = p_new.astype(np.float32).astype(np.float64)
+        lrn.set_params(p)
+
+
 def _golden_batches(g, name, s, B):
     from paper_2011_12895_b200.synth import SegmentBatch
     return SegmentBatch(*(g[f"{name}_s{s}_{k}"] for k in (
