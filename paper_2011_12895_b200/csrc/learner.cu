@@ -786,10 +786,56 @@ struct tlg_learner {
   // Learner::TrainStep over `n` local shards (+ the communicator's other ranks).
   // Small steps are launch-bound: after staging into the learner's own buffers, the
   // whole device step (kernels, allreduce, optimizer, stats D2H) replays as one CUDA graph.
-  bool use_graph(const tlg_segment_batch* bs, int n) const {
-    if (cfg.timing || n != 1 || graph_disabled) return false;
-    const long F = long(bs[0].n_segments) * T;
-    return F * long(net.D) <= (8L << 20);
+  bool use_graph(const tlg_segment_batch*, int n) const {
+    return !cfg.timing && n == 1 && !graph_disabled;
+  }
+  // graph of a step over an external device-resident batch, keyed by its pointers
+  struct ExtGraph {
+    const void* ptrs[8] = {};
+    uint32_t S = 0, dtype = 0, pitch = 0;
+    int slot = 0;  // index into graphs[]
+    uint64_t last_use = 0;
+  };
+  static void batch_ptrs(const tlg_segment_batch& b, const void* out[8]) {
+    out[0] = b.obs;
+    out[1] = b.action;
+    out[2] = b.reward;
+    out[3] = b.behavior_logp;
+    out[4] = b.value_est;
+    out[5] = b.done;
+    out[6] = b.bootstrap;
+    out[7] = b.valid_steps;
+  }
+  // graphs[] slot for this external batch (LRU over kExtGraphs entries)
+  int ext_graph_slot(const tlg_segment_batch& b) {
+    const void* ptrs[8];
+    batch_ptrs(b, ptrs);
+    ++graph_clock;
+    for (auto& e : ext)
+      if (std::equal(ptrs, ptrs + 8, e.ptrs) && e.S == b.n_segments && e.dtype == b.obs_dtype &&
+          e.pitch == b.obs_pitch) {
+        e.last_use = graph_clock;
+        return e.slot;
+      }
+    ExtGraph* v = nullptr;
+    if (int(ext.size()) < kExtGraphs) {
+      ext.push_back(ExtGraph{});
+      v = &ext.back();
+      v->slot = 3 + int(ext.size()) - 1;
+    } else {
+      v = &*std::min_element(ext.begin(), ext.end(), [](const ExtGraph& x, const ExtGraph& y) {
+        return x.last_use < y.last_use;
+      });
+      Graph& g = graphs[v->slot];
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+      g = Graph{};
+    }
+    std::copy(ptrs, ptrs + 8, v->ptrs);
+    v->S = b.n_segments;
+    v->dtype = b.obs_dtype;
+    v->pitch = b.obs_pitch;
+    v->last_use = graph_clock;
+    return v->slot;
   }
 
   void step(const tlg_segment_batch* bs, int n, int on_device, tlg_step_stats* out,
@@ -802,12 +848,15 @@ struct tlg_learner {
     launches = 0;
     TLG_CUDA(cudaSetDevice(cfg.device));
     if (use_graph(bs, n)) {
-      // a batch staged by stage_async is read in place (its slot's graph); any other batch
-      // is first copied into the learner's own buffers (binding 0)
+      // a batch staged by stage_async is read in place (its slot's graph), as is any other
+      // device-resident batch (a graph per batch address, LRU); host batches are copied
+      // into the learner's own buffers first (binding 0)
       int bind = 0;
-      if (on_device)
+      if (on_device) {
         for (int k = 0; k < 2; ++k)
           if (slots[k].ready && bs[0].action == slots[k].action) bind = 1 + k;
+        if (bind == 0) bind = ext_graph_slot(bs[0]);
+      }
       const Staged sg = stage_shard(bs[0], on_device, /*internal=*/bind == 0);
       const long key = long(sg.bd.S) * 8 + (sg.x0_u8 ? 1 : 0) + (sg.exact ? 2 : 0) +
                        (sg.x0_bits ? 4 : 0);
@@ -990,7 +1039,11 @@ struct tlg_learner {
     int launches = 0;
     const void* obs = nullptr;  // slot obs buffer the graph reads (slot bindings)
   };
-  Graph graphs[3];  // learner's own buffers, staging slot 0, staging slot 1
+  static constexpr int kExtGraphs = 8;
+  // learner's own buffers, staging slot 0, staging slot 1, external device batches
+  Graph graphs[3 + kExtGraphs];
+  std::vector<ExtGraph> ext;
+  uint64_t graph_clock = 0;
   uint64_t hyper_version = 0;
   bool graph_disabled = std::getenv("TLG_NO_GRAPH") != nullptr;
   uint64_t* adam_t_dev = nullptr;
