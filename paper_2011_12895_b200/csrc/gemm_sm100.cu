@@ -177,6 +177,9 @@ void dispatch_bn(bool a_mn, bool b_mn, bool a_lo, bool b_lo, int epi, int u8,
   // dX: A = dZ (K-major), B = W (MN-major)
   if (!a_mn && b_mn && a_lo && b_lo && epi == kEpiBwdTanh)
     return run_if_fits<BN, false, true, true, true, kEpiBwdTanh>(ah, al, bh, bl, em, p, grid, s);
+  // dX with a transposed copy of W (B K-major)
+  if (!a_mn && !b_mn && a_lo && b_lo && epi == kEpiBwdTanh)
+    return run_if_fits<BN, false, false, true, true, kEpiBwdTanh>(ah, al, bh, bl, em, p, grid, s);
   // dW: A = dZ^T (MN-major), B = H (MN-major), split-K partials
   if (a_mn && b_mn && a_lo && epi == kEpiStore) {
     if (b_lo) return run_if_fits<BN, true, true, true, true, kEpiStore>(ah, al, bh, bl, em, p, grid, s);
@@ -191,11 +194,37 @@ void dispatch_bn(bool a_mn, bool b_mn, bool a_lo, bool b_lo, int epi, int u8,
 }  // namespace
 
 int pick_splits(int M, int N, int K, int max_splits) {
-  const int tiles = ceil_div(M, kBM) * ceil_div(N, N > 128 ? 256 : N > 64 ? 128 : 64);
+  // Split-K count for the dW GEMMs (K = frames): minimise a simple cost model of
+  //   waves(s) x K-blocks per split  (+ the workspace round trip of the fixed-order reduce),
+  // with the launcher's own tile plan (256-wide tiles; CTA pairs once there are enough
+  // 256-row tiles to occupy every pair).  Without the pair term a 2048x2048 dW picked one
+  // split and ran 128 single-CTA tiles on 148 SMs (C5: 4.8 ms vs 3.6 ms at 8 splits).
+  const int BN = N > 128 ? 256 : N > 64 ? 128 : 64;
   const int kb = ceil_div(K, kBK);
-  int s = std::max(1, std::min(max_splits, 148 / std::max(1, tiles)));
-  s = std::min(s, std::max(1, kb / 4));  // keep >= 4 K blocks per split
-  return s;
+  const int units2 = num_sms() / 2;
+  const int s_max = std::max(1, std::min(max_splits, kb / 4));  // keep >= 4 K blocks per split
+  const double kblock_us = 1.33 * BN / 256.0;  // one 128xBN x 32 3xTF32 K block per SM
+  const double ws_us_per_elem = 2.0 * 4.0 / 6.0e6;  // write + read back at ~6 TB/s
+  double best = 0;
+  int best_s = 1;
+  for (int s = 1; s <= s_max; ++s) {
+    const int per = ceil_div(kb, s);
+    const int se = ceil_div(kb, per);  // launch() drops empty splits the same way
+    if (se != s) continue;
+    const long t2 = long(ceil_div(M, 2 * kBM)) * ceil_div(N, BN) * s;
+    long waves;
+    if (BN >= 128 && M >= 2 * kBM && t2 >= units2 && per >= 8)
+      waves = (t2 + units2 - 1) / units2;
+    else
+      waves = (long(ceil_div(M, kBM)) * ceil_div(N, BN) * s + num_sms() - 1) / num_sms();
+    const double t = double(waves) * per * kblock_us + ws_us_per_elem * s * double(M) * N +
+                     (s > 1 ? 3.0 : 0.0);
+    if (s == 1 || t < 0.98 * best) {
+      best = t;
+      best_s = s;
+    }
+  }
+  return best_s;
 }
 
 LaunchInfo launch(const Operand& A, const Operand& B, int M, int N, int K, int epi, Params p,

@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <cstring>
 #include <random>
+#include <string>
 #include <vector>
 
 #include "../gemm_i8.cuh"
@@ -61,6 +62,7 @@ static bool g_fullhi = false;  // feed the full fp32 plane as "hi" (tests HW tf3
 static int g_u8 = 0;           // 1: A as uint8 planes, 2: B as uint8 planes
 static int g_heads = 0;        // > 0: fused head width (fwd), timing only
 static bool g_nolo = false;    // fwd/bwd: no residual output plane, timing only
+static bool g_noref = false;   // timing only: skip the fp64 reference and the check
 
 uint8_t* to_u8(const float* d, long n) {
   std::vector<float> h(n);
@@ -87,8 +89,9 @@ void check(const char* name, int M, int N, int K, bool a_mn, bool b_mn, bool a_e
   double *ref, *refabs;
   TLG_CUDA(cudaMalloc(&ref, long(M) * N * 8));
   TLG_CUDA(cudaMalloc(&refabs, long(M) * N * 8));
-  ref_gemm<<<dim3((M + 127) / 128, N), 128>>>(A.x, lda, a_mn, B.x, ldb, b_mn, M, N, K, ref,
-                                              refabs);
+  if (!g_noref)
+    ref_gemm<<<dim3((M + 127) / 128, N), 128>>>(A.x, lda, a_mn, B.x, ldb, b_mn, M, N, K, ref,
+                                                refabs);
   float *out_hi, *out_lo, *ws, *colsum;
   const int mt = std::max((M + 127) / 128, 160);  // rows: one per CTA (<= #SMs)
   TLG_CUDA(cudaMalloc(&colsum, long(mt) * N * 4));
@@ -157,6 +160,16 @@ void check(const char* name, int M, int N, int K, bool a_mn, bool b_mn, bool a_e
   TLG_CUDA(cudaMemcpy(hws.data(), ws, hws.size() * 4, cudaMemcpyDeviceToHost));
   double worst = 0;
   long bad = 0;
+  if (g_noref) {
+    const double tf = 2.0 * M * N * K / (ms * 1e-3) / 1e12;
+    printf("%-34s M=%6d N=%5d K=%6d split=%d : (timing only)  %.3f ms %.1f TF/s\n", name, M, N,
+           K, splits, ms, tf);
+    cudaFree(colsum); cudaFree(ref); cudaFree(refabs); cudaFree(out_hi); cudaFree(out_lo); cudaFree(ws);
+    cudaFree(A.x); cudaFree(A.hi); cudaFree(A.lo); cudaFree(B.x); cudaFree(B.hi); cudaFree(B.lo);
+    cudaFree(act.x); cudaFree(act.hi); cudaFree(act.lo); cudaFree(bias.x); cudaFree(bias.hi);
+    cudaFree(bias.lo);
+    return;
+  }
   if (expand) {  // the converter's fp32 copy of the uint8 A operand must be exact
     std::vector<float> he(long(M) * K), ha(long(M) * K);
     TLG_CUDA(cudaMemcpy(he.data(), expand, he.size() * 4, cudaMemcpyDeviceToHost));
@@ -467,6 +480,7 @@ int main(int argc, char** argv) {
     check("fwd tanh K/K N=64", 128, 64, 64, false, false, false, kEpiFwdTanh, 1);
     check("dX bwd K/MN", 300, 256, 256, false, true, false, kEpiBwdTanh, 1);
     check("dX bwd K/MN N=64", 200, 64, 256, false, true, false, kEpiBwdTanh, 1);
+    check("dX bwd K/K", 300, 256, 256, false, false, false, kEpiBwdTanh, 1);
     check("dW store MN/MN", 256, 200, 1000, true, true, false, kEpiStore, 1);
     check("dW store MN/MN split4", 256, 200, 1000, true, true, false, kEpiStore, 4);
     check("dW store MN/MN exactB", 256, 1936, 2048, true, true, false, kEpiStore, 2);
@@ -491,7 +505,15 @@ int main(int argc, char** argv) {
     check_i8_dw("I8 bits dW", 128, 200, 1000, 2);
     check_i8_dw("I8 bits dW pair", 256, 1936, 4096, 8);
     check_i8_dw("I8 bits dW ragged", 256, 300, 1300, 4);
-    if (argc > 1) {
+    if (argc > 1 && std::string(argv[1]) == "c5") {
+      g_noref = true;  // C5 trunk shapes (4x2048, 131,072 frames per shard)
+      check("perf fwd C5", 131072, 2048, 2048, false, false, false, kEpiFwdTanh, 1);
+      check("perf dX C5 K/MN", 131072, 2048, 2048, false, true, false, kEpiBwdTanh, 1);
+      check("perf dX C5 K/K", 131072, 2048, 2048, false, false, false, kEpiBwdTanh, 1);
+      for (int sp : {1, 2, 4, 8, 15, 37})
+        check("perf dW C5", 2048, 2048, 131072, true, true, false, kEpiStore, sp);
+      g_noref = false;
+    } else if (argc > 1) {
       check_i8("perf I8 bits fwd C3 L1", 131072, 256, 1936);
       check_i8_dw("perf I8 bits dW C3 L1", 256, 1936, 131072, 114);
       check_i8x2("perf I8x2 fwd C3 L2", 131072, 256, 256);
