@@ -223,6 +223,9 @@ struct tlg_learner {
     if (c.max_segments == 0 || c.unroll_len == 0)
       throw InvalidArg("max_segments and unroll_len must be >= 1");
     if (c.algo > TLG_ALGO_PPO_VTRACE) throw InvalidArg("unknown algo");
+    for (uint32_t l = 1; l < net.L; ++l)  // dZ column sums are fused into the dX epilogue
+      if (net.dims[l] > uint32_t(tlg::gemm::kColMax))
+        throw InvalidArg("mlp hidden widths below the top layer must be <= 2048 on the GPU path");
     TLG_CUDA(cudaSetDevice(c.device));
     S_max = int(c.max_segments);
     T = int(c.unroll_len);
@@ -279,7 +282,7 @@ struct tlg_learner {
     tlogp = mem.add<float>(F_max);
     adv = mem.add<float>(F_max);
     target = mem.add<float>(F_max);
-    seg_partial = mem.add<double>(2 * S_max);
+    seg_partial = mem.add<double>(3 * ((S_max + 7) / 8));  // one {s1, s2, n} per returns block
     stats = mem.add<tlg::StepStatsDev>(kMaxLocalShards);
     err = mem.add<int>(4);
     // partial rows: one per loss block, or one per persistent CTA of the fused loss GEMM
@@ -1673,18 +1676,36 @@ int tlg_returns(uint32_t algo, const tlg_hyper* hp, uint32_t n_segments, uint32_
     bd.blogp = behavior_logp;
     tlg::HyperDev hd{float(hp->gamma), float(hp->lam), float(hp->clip_eps), float(hp->vf_coef),
                      float(hp->ent_coef), float(hp->rho_bar), float(hp->c_bar), hp->adv_norm};
-    double* part = nullptr;
-    int* err = nullptr;
-    TLG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part), 16 * size_t(n_segments), s));
-    TLG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&err), 4, s));
+    // per-device scratch, grown on demand (a per-call allocation costs more than the
+    // kernels at small sizes); calls on one device are serialised by its mutex
+    struct Scratch {
+      std::mutex mu;
+      void* buf = nullptr;
+      size_t bytes = 0;
+      int* host_err = nullptr;
+    };
+    static Scratch scratch[64];
+    int dev = 0;
+    TLG_CUDA(cudaGetDevice(&dev));
+    Scratch& sc = scratch[dev & 63];
+    std::lock_guard<std::mutex> lk(sc.mu);
+    const size_t need = 64 + 24 * ((size_t(n_segments) + 7) / 8);
+    if (sc.bytes < need) {
+      if (sc.buf) TLG_CUDA(cudaFree(sc.buf));
+      sc.buf = nullptr;
+      sc.bytes = 0;
+      TLG_CUDA(cudaMalloc(&sc.buf, need));
+      sc.bytes = need;
+    }
+    if (!sc.host_err) TLG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&sc.host_err), 4));
+    int* err = static_cast<int*>(sc.buf);
+    double* part = reinterpret_cast<double*>(static_cast<char*>(sc.buf) + 64);
     TLG_CUDA(cudaMemsetAsync(err, 0, 4, s));
     tlg::launch_returns(bd, int(algo == TLG_ALGO_PPO ? tlg::kAlgoPpo : tlg::kAlgoVtrace), hd,
                         target_logp, adv, target, part, err, s);
-    int e = 0;
-    TLG_CUDA(cudaMemcpyAsync(&e, err, 4, cudaMemcpyDeviceToHost, s));
-    TLG_CUDA(cudaFreeAsync(part, s));
-    TLG_CUDA(cudaFreeAsync(err, s));
+    TLG_CUDA(cudaMemcpyAsync(sc.host_err, err, 4, cudaMemcpyDeviceToHost, s));
     TLG_CUDA(cudaStreamSynchronize(s));
+    const int e = *sc.host_err;
     if (e & tlg::kErrNonFiniteLogp) throw InvalidArg("non-finite log probability");
     if (e & tlg::kErrValidSteps) throw InvalidArg("valid_steps exceeds unroll_len");
   });

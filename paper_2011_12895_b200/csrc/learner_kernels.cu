@@ -261,103 +261,123 @@ __device__ __forceinline__ Aff suffix_scan(Aff m, int lane) {
   return m;
 }
 
+// 8 segments (one per warp) per block; the block writes one partial of the adv statistics
+constexpr int kRetSegsPerBlock = 8;
+
 __global__ void __launch_bounds__(256) returns_kernel(BatchDev b, int algo, HyperDev hp,
                                                       const float* __restrict__ tlogp,
                                                       float* __restrict__ adv,
                                                       float* __restrict__ target,
                                                       double* __restrict__ seg_partial,
                                                       int* __restrict__ err) {
-  const int lane = threadIdx.x & 31;
-  const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (s >= b.S) return;
-  const int T = b.T;
-  int n = b.valid[s];
-  if (n > T || n < 0) {
-    if (lane == 0) atomicOr(err, kErrValidSteps);
-    n = min(max(n, 0), T);
-  }
-  const long base = long(s) * T;
-  const float boot = b.boot[s];
-  const float g = hp.gamma, gl = hp.gamma * hp.lam;
-  const int nblk = (T + 31) / 32;
-  // carries from the block after the current one (t = (jb+1)*32)
-  float carry_v = boot;    // V_{t+1} for lane 31 (bootstrap when t+1 >= n)
-  float carry_x = 0.f;     // GAE A / V-trace u at the block start after
-  float carry_g = boot;    // lambda-return G
-  float carry_vs = boot;   // V-trace vs_{t+1}
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int s = blockIdx.x * kRetSegsPerBlock + w;
   double s1 = 0.0, s2 = 0.0;
-  bool bad_adv = false, bad_logp = false;
-  for (int jb = nblk - 1; jb >= 0; --jb) {
-    const int t = jb * 32 + lane;
-    const bool in = t < n;
-    const long f = base + t;
-    const float r = in ? b.reward[f] : 0.f;
-    const float v = in ? b.value[f] : 0.f;
-    const float nt = (in && b.done[f]) ? 0.f : 1.f;
-    float v_next = __shfl_down_sync(0xffffffffu, v, 1);
-    if (lane == 31) v_next = carry_v;
-    if (t + 1 >= n) v_next = boot;
-    if (algo == kAlgoPpo) {
-      // GaeAdvantages (rlmath.cpp:62-78) and LambdaReturn (:45-60)
-      Aff ma{in ? gl * nt : 0.f, in ? (r + g * nt * v_next - v) : 0.f};
-      Aff mg{in ? gl * nt : 0.f, in ? (r + g * nt * (1.f - hp.lam) * v_next) : boot};
-      ma = suffix_scan(ma, lane);
-      mg = suffix_scan(mg, lane);
-      const float A_t = fmaf(ma.a, carry_x, ma.b);
-      const float G_t = fmaf(mg.a, carry_g, mg.b);
-      if (t < T) {
-        adv[f] = in ? A_t : 0.f;
-        target[f] = in ? G_t : 0.f;
-      }
-      if (in) {
-        bad_adv |= !isfinite(A_t);
-        s1 += double(A_t);
-        s2 += double(A_t) * double(A_t);
-      }
-      carry_x = __shfl_sync(0xffffffffu, A_t, 0);
-      carry_g = __shfl_sync(0xffffffffu, G_t, 0);
-    } else {
-      // VtraceTargets (rlmath.cpp:80-114): truncated importance weights fused in
-      float rho = 0.f, c = 0.f;
-      if (in) {
-        const float bl = b.blogp[f], tl = tlogp[f];
-        if (!isfinite(bl) || !isfinite(tl)) bad_logp = true;
-        const float w = expf(tl - bl);
-        rho = fminf(hp.rho_bar, w);
-        c = fminf(hp.c_bar, w);
-      }
-      const float delta = rho * (r + g * nt * v_next - v);
-      Aff mu{in ? g * nt * c : 0.f, in ? delta : 0.f};
-      mu = suffix_scan(mu, lane);
-      const float u = fmaf(mu.a, carry_x, mu.b);
-      const float vs = v + u;
-      float vs_next = __shfl_down_sync(0xffffffffu, vs, 1);
-      if (lane == 31) vs_next = carry_vs;
-      if (t + 1 >= n) vs_next = boot;
-      const float pg = rho * (r + g * nt * vs_next - v);
-      if (t < T) {
-        adv[f] = in ? pg : 0.f;
-        target[f] = in ? vs : 0.f;
-      }
-      if (in) {
-        bad_adv |= !isfinite(pg);
-        s1 += double(pg);
-        s2 += double(pg) * double(pg);
-      }
-      carry_x = __shfl_sync(0xffffffffu, u, 0);
-      carry_vs = __shfl_sync(0xffffffffu, vs, 0);
+  int nv = 0;
+  if (s < b.S) {
+    const int T = b.T;
+    int n = b.valid[s];
+    if (n > T || n < 0) {
+      if (lane == 0) atomicOr(err, kErrValidSteps);
+      n = min(max(n, 0), T);
     }
-    carry_v = __shfl_sync(0xffffffffu, v, 0);
+    const long base = long(s) * T;
+    const float boot = b.boot[s];
+    nv = n;
+    const float g = hp.gamma, gl = hp.gamma * hp.lam;
+    const int nblk = (T + 31) / 32;
+    // carries from the block after the current one (t = (jb+1)*32)
+    float carry_v = boot;    // V_{t+1} for lane 31 (bootstrap when t+1 >= n)
+    float carry_x = 0.f;     // GAE A / V-trace u at the block start after
+    float carry_g = boot;    // lambda-return G
+    float carry_vs = boot;   // V-trace vs_{t+1}
+    bool bad_adv = false, bad_logp = false;
+    for (int jb = nblk - 1; jb >= 0; --jb) {
+      const int t = jb * 32 + lane;
+      const bool in = t < n;
+      const long f = base + t;
+      const float r = in ? b.reward[f] : 0.f;
+      const float v = in ? b.value[f] : 0.f;
+      const float nt = (in && b.done[f]) ? 0.f : 1.f;
+      float v_next = __shfl_down_sync(0xffffffffu, v, 1);
+      if (lane == 31) v_next = carry_v;
+      if (t + 1 >= n) v_next = boot;
+      if (algo == kAlgoPpo) {
+        // GaeAdvantages (rlmath.cpp:62-78) and LambdaReturn (:45-60)
+        Aff ma{in ? gl * nt : 0.f, in ? (r + g * nt * v_next - v) : 0.f};
+        Aff mg{in ? gl * nt : 0.f, in ? (r + g * nt * (1.f - hp.lam) * v_next) : boot};
+        ma = suffix_scan(ma, lane);
+        mg = suffix_scan(mg, lane);
+        const float A_t = fmaf(ma.a, carry_x, ma.b);
+        const float G_t = fmaf(mg.a, carry_g, mg.b);
+        if (t < T) {
+          adv[f] = in ? A_t : 0.f;
+          target[f] = in ? G_t : 0.f;
+        }
+        if (in) {
+          bad_adv |= !isfinite(A_t);
+          s1 += double(A_t);
+          s2 += double(A_t) * double(A_t);
+        }
+        carry_x = __shfl_sync(0xffffffffu, A_t, 0);
+        carry_g = __shfl_sync(0xffffffffu, G_t, 0);
+      } else {
+        // VtraceTargets (rlmath.cpp:80-114): truncated importance weights fused in
+        float rho = 0.f, c = 0.f;
+        if (in) {
+          const float bl = b.blogp[f], tl = tlogp[f];
+          if (!isfinite(bl) || !isfinite(tl)) bad_logp = true;
+          const float w = expf(tl - bl);
+          rho = fminf(hp.rho_bar, w);
+          c = fminf(hp.c_bar, w);
+        }
+        const float delta = rho * (r + g * nt * v_next - v);
+        Aff mu{in ? g * nt * c : 0.f, in ? delta : 0.f};
+        mu = suffix_scan(mu, lane);
+        const float u = fmaf(mu.a, carry_x, mu.b);
+        const float vs = v + u;
+        float vs_next = __shfl_down_sync(0xffffffffu, vs, 1);
+        if (lane == 31) vs_next = carry_vs;
+        if (t + 1 >= n) vs_next = boot;
+        const float pg = rho * (r + g * nt * vs_next - v);
+        if (t < T) {
+          adv[f] = in ? pg : 0.f;
+          target[f] = in ? vs : 0.f;
+        }
+        if (in) {
+          bad_adv |= !isfinite(pg);
+          s1 += double(pg);
+          s2 += double(pg) * double(pg);
+        }
+        carry_x = __shfl_sync(0xffffffffu, u, 0);
+        carry_vs = __shfl_sync(0xffffffffu, vs, 0);
+      }
+      carry_v = __shfl_sync(0xffffffffu, v, 0);
+    }
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    const unsigned anybad = __ballot_sync(0xffffffffu, bad_adv);
+    const unsigned anylogp = __ballot_sync(0xffffffffu, bad_logp);
+    if (lane == 0) {
+      if (anylogp) atomicOr(err, kErrNonFiniteLogp);
+      if (anybad) atomicOr(err, kErrNonFiniteAdv);
+    }
   }
-  s1 = warp_sum(s1);
-  s2 = warp_sum(s2);
-  const unsigned anybad = __ballot_sync(0xffffffffu, bad_adv);
-  const unsigned anylogp = __ballot_sync(0xffffffffu, bad_logp);
+  // per-block partial {sum A, sum A^2, valid frames}, warps added in fixed order, so the
+  // statistics pass reads S/8 partials instead of S (and no valid_steps)
+  __shared__ double red[3][kRetSegsPerBlock];
   if (lane == 0) {
-    seg_partial[2 * s] = s1;
-    seg_partial[2 * s + 1] = s2;
-    if (anylogp) atomicOr(err, kErrNonFiniteLogp);
-    if (anybad) atomicOr(err, kErrNonFiniteAdv);
+    red[0][w] = s1;
+    red[1][w] = s2;
+    red[2][w] = double(nv);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, c = 0.0, m = 0.0;
+    for (int i = 0; i < kRetSegsPerBlock; ++i) { a += red[0][i]; c += red[1][i]; m += red[2][i]; }
+    seg_partial[3 * blockIdx.x] = a;
+    seg_partial[3 * blockIdx.x + 1] = c;
+    seg_partial[3 * blockIdx.x + 2] = m;
   }
 }
 
@@ -369,10 +389,11 @@ __global__ void __launch_bounds__(1024) finalize_adv_kernel(const double* __rest
   __shared__ long long shn[32];
   double s1 = 0.0, s2 = 0.0;
   long long n = 0;
-  for (int s = threadIdx.x; s < b.S; s += blockDim.x) {
-    s1 += seg_partial[2 * s];
-    s2 += seg_partial[2 * s + 1];
-    n += min(max(b.valid[s], 0), b.T);
+  const int nblk = (b.S + kRetSegsPerBlock - 1) / kRetSegsPerBlock;
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x) {
+    s1 += seg_partial[3 * i];
+    s2 += seg_partial[3 * i + 1];
+    n += (long long)seg_partial[3 * i + 2];
   }
   s1 = warp_sum(s1);
   s2 = warp_sum(s2);
@@ -1025,7 +1046,7 @@ void launch_head_finalize(const HeadDesc& hd, const float* params, const float* 
 
 void launch_returns(const BatchDev& b, int algo, const HyperDev& hp, const float* tlogp,
                     float* adv, float* target, double* seg_partial, int* err, cudaStream_t s) {
-  returns_kernel<<<ceil_div(b.S, 8), 256, 0, s>>>(b, algo, hp, tlogp, adv, target, seg_partial,
+  returns_kernel<<<ceil_div(b.S, kRetSegsPerBlock), 32 * kRetSegsPerBlock, 0, s>>>(b, algo, hp, tlogp, adv, target, seg_partial,
                                                   err);
   TLG_CHECK_LAUNCH();
 }
