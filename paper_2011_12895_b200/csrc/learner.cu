@@ -724,8 +724,8 @@ struct tlg_learner {
     const int algo = int(cfg.algo);
     if (fused_loss_ok(F)) {
       // GAE + advantage statistics need no forward output (rlmath.cpp:62-78, 18-34)
-      tlg::launch_returns(bd, algo, hd, tlogp, adv, target, seg_partial, err, stream);
-      tlg::launch_finalize_adv(seg_partial, bd, hp.adv_norm, st, err, stream);
+      const int rpb = tlg::launch_returns(bd, algo, hd, tlogp, adv, target, seg_partial, err, stream);
+      tlg::launch_finalize_adv(seg_partial, bd, hp.adv_norm, st, err, stream, rpb);
       tlg::gemm::LossEpi le{};
       le.action = bd.action;
       le.blogp = bd.blogp;
@@ -767,8 +767,8 @@ struct tlg_learner {
     // ---- heads, returns, loss
     const float* hL = net.L ? act[net.L - 1] : x0;
     const long ldh = net.head.H;
-    tlg::launch_returns(bd, algo, hd, tlogp, adv, target, seg_partial, err, stream);
-    tlg::launch_finalize_adv(seg_partial, bd, hp.adv_norm, st, err, stream);
+    const int rpb = tlg::launch_returns(bd, algo, hd, tlogp, adv, target, seg_partial, err, stream);
+    tlg::launch_finalize_adv(seg_partial, bd, hp.adv_norm, st, err, stream, rpb);
     const int loss_kind = algo == TLG_ALGO_VTRACE ? 1 : 0;
     const tlg::LossLaunch ll = tlg::launch_loss_backward(
         net.head, params, hL, ldh, bd, head_out, adv, target, st, hd, loss_kind, dzh,

@@ -1,5 +1,6 @@
 // Non-GEMM kernels of the B200 learner step (see learner_kernels.cuh).
 #include <cmath>
+#include <cstdlib>
 
 #include "learner_kernels.cuh"
 
@@ -296,9 +297,22 @@ __global__ void __launch_bounds__(256) returns_kernel(BatchDev b, int algo, Hype
       const int t = jb * 32 + lane;
       const bool in = t < n;
       const long f = base + t;
-      const float r = in ? b.reward[f] : 0.f;
-      const float v = in ? b.value[f] : 0.f;
-      const float nt = (in && b.done[f]) ? 0.f : 1.f;
+      // the row loads depend only on T, not on valid_steps: all of a warp's loads are in
+      // flight together (the valid_steps load no longer serialises them); padding masked after
+      float r = 0.f, v = 0.f, bl = 0.f, tl = 0.f;
+      uint8_t dn = 0;
+      if (t < T) {
+        r = b.reward[f];
+        v = b.value[f];
+        dn = b.done[f];
+        if (algo != kAlgoPpo) {
+          bl = b.blogp[f];
+          tl = tlogp[f];
+        }
+      }
+      r = in ? r : 0.f;
+      v = in ? v : 0.f;
+      const float nt = (in && dn) ? 0.f : 1.f;
       float v_next = __shfl_down_sync(0xffffffffu, v, 1);
       if (lane == 31) v_next = carry_v;
       if (t + 1 >= n) v_next = boot;
@@ -325,7 +339,6 @@ __global__ void __launch_bounds__(256) returns_kernel(BatchDev b, int algo, Hype
         // VtraceTargets (rlmath.cpp:80-114): truncated importance weights fused in
         float rho = 0.f, c = 0.f;
         if (in) {
-          const float bl = b.blogp[f], tl = tlogp[f];
           if (!isfinite(bl) || !isfinite(tl)) bad_logp = true;
           const float w = expf(tl - bl);
           rho = fminf(hp.rho_bar, w);
@@ -381,15 +394,218 @@ __global__ void __launch_bounds__(256) returns_kernel(BatchDev b, int algo, Hype
   }
 }
 
+// K1, vectorised (T % 4 == 0, 16-B aligned rows): 8 lanes per segment, 4 consecutive steps
+// per lane (float4 / uchar4 loads and stores), so a warp instruction covers 128 frames.
+// Each lane composes its 4 steps' affine maps serially, the 8 lanes of a segment suffix-scan
+// the composites (3 shuffle rounds), then each lane expands its 4 values backwards.  Same
+// recursions and masking as returns_kernel (rlmath.cpp:45-114), fewer instructions per
+// frame: the scalar kernel was issue-bound at ~20 % of HBM bandwidth once the data streams.
+constexpr int kRetVecSegsPerBlock = 32;  // 8 warps x 4 segments
+
+struct Aff4 {
+  float a[4], b[4];
+};
+
+// lane composite of its 4 maps (x_t = a_t x_{t+1} + b_t), suffix scan over the segment's
+// 8 lanes; returns x at the lane's first step and at the step after its last (x_next)
+__device__ __forceinline__ float scan4(const Aff4& m, float carry, float& x_next) {
+  float A = m.a[3], B = m.b[3];
+#pragma unroll
+  for (int q = 2; q >= 0; --q) {
+    B = fmaf(m.a[q], B, m.b[q]);
+    A = m.a[q] * A;
+  }
+  const int j = threadIdx.x & 7;
+#pragma unroll
+  for (int d = 1; d < 8; d <<= 1) {
+    const float a2 = __shfl_down_sync(0xffffffffu, A, d, 8);
+    const float b2 = __shfl_down_sync(0xffffffffu, B, d, 8);
+    if (j + d < 8) {
+      B = fmaf(A, b2, B);
+      A = A * a2;
+    }
+  }
+  const float x0 = fmaf(A, carry, B);
+  float xn = __shfl_down_sync(0xffffffffu, x0, 1, 8);
+  if (j == 7) xn = carry;
+  x_next = xn;
+  return x0;
+}
+
+__global__ void __launch_bounds__(256) returns_vec_kernel(BatchDev b, int algo, HyperDev hp,
+                                                          const float* __restrict__ tlogp,
+                                                          float* __restrict__ adv,
+                                                          float* __restrict__ target,
+                                                          double* __restrict__ seg_partial,
+                                                          int* __restrict__ err) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, j = lane & 7;
+  const int s = blockIdx.x * kRetVecSegsPerBlock + w * 4 + (lane >> 3);
+  const bool active = s < b.S;
+  const int T = b.T;
+  int n = 0;
+  float boot = 0.f;
+  if (active) {
+    n = b.valid[s];
+    boot = b.boot[s];
+    if (n > T || n < 0) {
+      if (j == 0) atomicOr(err, kErrValidSteps);
+      n = min(max(n, 0), T);
+    }
+  }
+  const long base = long(s) * T;
+  const float g = hp.gamma, gl = hp.gamma * hp.lam;
+  const int nchunk = (T + 31) / 32;
+  float carry_v = boot, carry_x = 0.f, carry_g = boot, carry_vs = boot;
+  double s1 = 0.0, s2 = 0.0;
+  bool bad_adv = false, bad_logp = false;
+  for (int c = nchunk - 1; c >= 0; --c) {
+    const int t0 = c * 32 + j * 4;
+    const bool row = active && t0 < T;
+    float r[4] = {0.f, 0.f, 0.f, 0.f}, v[4] = {0.f, 0.f, 0.f, 0.f};
+    float bl[4] = {0.f, 0.f, 0.f, 0.f}, tl[4] = {0.f, 0.f, 0.f, 0.f};
+    uchar4 dn = make_uchar4(0, 0, 0, 0);
+    if (row) {
+      const float4 r4 = *reinterpret_cast<const float4*>(b.reward + base + t0);
+      const float4 v4 = *reinterpret_cast<const float4*>(b.value + base + t0);
+      dn = *reinterpret_cast<const uchar4*>(b.done + base + t0);
+      r[0] = r4.x; r[1] = r4.y; r[2] = r4.z; r[3] = r4.w;
+      v[0] = v4.x; v[1] = v4.y; v[2] = v4.z; v[3] = v4.w;
+      if (algo != kAlgoPpo) {
+        const float4 b4 = *reinterpret_cast<const float4*>(b.blogp + base + t0);
+        const float4 l4 = *reinterpret_cast<const float4*>(tlogp + base + t0);
+        bl[0] = b4.x; bl[1] = b4.y; bl[2] = b4.z; bl[3] = b4.w;
+        tl[0] = l4.x; tl[1] = l4.y; tl[2] = l4.z; tl[3] = l4.w;
+      }
+    }
+    const unsigned char dd[4] = {dn.x, dn.y, dn.z, dn.w};
+    bool in[4];
+    float nt[4], vn[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      in[q] = t0 + q < n;
+      r[q] = in[q] ? r[q] : 0.f;
+      v[q] = in[q] ? v[q] : 0.f;
+      nt[q] = (in[q] && dd[q]) ? 0.f : 1.f;
+    }
+    // V_{t+1}: within the lane, then the next lane's first value, then the next chunk's
+    float v_after = __shfl_down_sync(0xffffffffu, v[0], 1, 8);
+    if (j == 7) v_after = carry_v;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      vn[q] = q < 3 ? v[q + 1] : v_after;
+      if (t0 + q + 1 >= n) vn[q] = boot;
+    }
+    float out_a[4], out_t[4];
+    if (algo == kAlgoPpo) {
+      // GaeAdvantages (rlmath.cpp:62-78) and LambdaReturn (:45-60)
+      Aff4 ma, mg;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        ma.a[q] = in[q] ? gl * nt[q] : 0.f;
+        ma.b[q] = in[q] ? (r[q] + g * nt[q] * vn[q] - v[q]) : 0.f;
+        mg.a[q] = ma.a[q];
+        mg.b[q] = in[q] ? (r[q] + g * nt[q] * (1.f - hp.lam) * vn[q]) : boot;
+      }
+      float xa, xg;
+      const float a0 = scan4(ma, carry_x, xa);
+      const float g0 = scan4(mg, carry_g, xg);
+#pragma unroll
+      for (int q = 3; q >= 0; --q) {
+        xa = fmaf(ma.a[q], xa, ma.b[q]);
+        xg = fmaf(mg.a[q], xg, mg.b[q]);
+        out_a[q] = in[q] ? xa : 0.f;
+        out_t[q] = in[q] ? xg : 0.f;
+        if (in[q]) {
+          bad_adv |= !isfinite(xa);
+          s1 += double(xa);
+          s2 += double(xa) * double(xa);
+        }
+      }
+      carry_x = __shfl_sync(0xffffffffu, a0, 0, 8);
+      carry_g = __shfl_sync(0xffffffffu, g0, 0, 8);
+    } else {
+      // VtraceTargets (rlmath.cpp:80-114): truncated importance weights fused in
+      Aff4 mu;
+      float rho[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float rh = 0.f, cc = 0.f;
+        if (in[q]) {
+          if (!isfinite(bl[q]) || !isfinite(tl[q])) bad_logp = true;
+          const float wq = expf(tl[q] - bl[q]);
+          rh = fminf(hp.rho_bar, wq);
+          cc = fminf(hp.c_bar, wq);
+        }
+        rho[q] = rh;
+        mu.a[q] = in[q] ? g * nt[q] * cc : 0.f;
+        mu.b[q] = in[q] ? rh * (r[q] + g * nt[q] * vn[q] - v[q]) : 0.f;
+      }
+      float xu;
+      const float u0 = scan4(mu, carry_x, xu);
+      float vs[4];
+#pragma unroll
+      for (int q = 3; q >= 0; --q) {
+        xu = fmaf(mu.a[q], xu, mu.b[q]);
+        vs[q] = v[q] + xu;
+      }
+      float vs_after = __shfl_down_sync(0xffffffffu, vs[0], 1, 8);
+      if (j == 7) vs_after = carry_vs;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float vsn = q < 3 ? vs[q + 1] : vs_after;
+        if (t0 + q + 1 >= n) vsn = boot;
+        const float pg = rho[q] * (r[q] + g * nt[q] * vsn - v[q]);
+        out_a[q] = in[q] ? pg : 0.f;
+        out_t[q] = in[q] ? vs[q] : 0.f;
+        if (in[q]) {
+          bad_adv |= !isfinite(pg);
+          s1 += double(pg);
+          s2 += double(pg) * double(pg);
+        }
+      }
+      carry_x = __shfl_sync(0xffffffffu, u0, 0, 8);
+      carry_vs = __shfl_sync(0xffffffffu, vs[0], 0, 8);
+    }
+    if (row) {
+      *reinterpret_cast<float4*>(adv + base + t0) = make_float4(out_a[0], out_a[1], out_a[2], out_a[3]);
+      *reinterpret_cast<float4*>(target + base + t0) = make_float4(out_t[0], out_t[1], out_t[2], out_t[3]);
+    }
+    carry_v = __shfl_sync(0xffffffffu, v[0], 0, 8);
+  }
+  s1 = warp_sum(s1);
+  s2 = warp_sum(s2);
+  int nv = j == 0 ? n : 0;
+  for (int o = 16; o > 0; o >>= 1) nv += __shfl_xor_sync(0xffffffffu, nv, o);
+  const unsigned anybad = __ballot_sync(0xffffffffu, bad_adv);
+  const unsigned anylogp = __ballot_sync(0xffffffffu, bad_logp);
+  __shared__ double red[3][8];
+  if (lane == 0) {
+    if (anylogp) atomicOr(err, kErrNonFiniteLogp);
+    if (anybad) atomicOr(err, kErrNonFiniteAdv);
+    red[0][w] = s1;
+    red[1][w] = s2;
+    red[2][w] = double(nv);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, c = 0.0, m = 0.0;
+    for (int i = 0; i < 8; ++i) { a += red[0][i]; c += red[1][i]; m += red[2][i]; }
+    seg_partial[3 * blockIdx.x] = a;
+    seg_partial[3 * blockIdx.x + 1] = c;
+    seg_partial[3 * blockIdx.x + 2] = m;
+  }
+}
+
 // EffectiveAdvantages statistics (rlmath.cpp:18-34), fixed-order fp64 reduction.
 __global__ void __launch_bounds__(1024) finalize_adv_kernel(const double* __restrict__ seg_partial,
                                                             BatchDev b, int adv_norm,
-                                                            StepStatsDev* st, int* err) {
+                                                            StepStatsDev* st, int* err,
+                                                            int segs_per_block) {
   __shared__ double sh1[32], sh2[32];
   __shared__ long long shn[32];
   double s1 = 0.0, s2 = 0.0;
   long long n = 0;
-  const int nblk = (b.S + kRetSegsPerBlock - 1) / kRetSegsPerBlock;
+  const int nblk = (b.S + segs_per_block - 1) / segs_per_block;
   for (int i = threadIdx.x; i < nblk; i += blockDim.x) {
     s1 += seg_partial[3 * i];
     s2 += seg_partial[3 * i + 1];
@@ -1044,16 +1260,36 @@ void launch_head_finalize(const HeadDesc& hd, const float* params, const float* 
   TLG_CHECK_LAUNCH();
 }
 
-void launch_returns(const BatchDev& b, int algo, const HyperDev& hp, const float* tlogp,
-                    float* adv, float* target, double* seg_partial, int* err, cudaStream_t s) {
-  returns_kernel<<<ceil_div(b.S, kRetSegsPerBlock), 32 * kRetSegsPerBlock, 0, s>>>(b, algo, hp, tlogp, adv, target, seg_partial,
-                                                  err);
+static bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
+
+static bool returns_vec_ok(const BatchDev& b, int algo, const float* tlogp, const float* adv,
+                           const float* target) {
+  if (b.T % 4 != 0 || std::getenv("TLG_RETURNS_SCALAR")) return false;
+  if (!aligned(b.reward, 16) || !aligned(b.value, 16) || !aligned(b.done, 4) ||
+      !aligned(adv, 16) || !aligned(target, 16))
+    return false;
+  return algo == kAlgoPpo || (aligned(b.blogp, 16) && aligned(tlogp, 16));
+}
+
+int launch_returns(const BatchDev& b, int algo, const HyperDev& hp, const float* tlogp,
+                   float* adv, float* target, double* seg_partial, int* err, cudaStream_t s) {
+  int per;
+  if (returns_vec_ok(b, algo, tlogp, adv, target)) {
+    per = kRetVecSegsPerBlock;
+    returns_vec_kernel<<<ceil_div(b.S, per), 256, 0, s>>>(b, algo, hp, tlogp, adv, target,
+                                                           seg_partial, err);
+  } else {
+    per = kRetSegsPerBlock;
+    returns_kernel<<<ceil_div(b.S, per), 32 * per, 0, s>>>(b, algo, hp, tlogp, adv, target,
+                                                           seg_partial, err);
+  }
   TLG_CHECK_LAUNCH();
+  return per;
 }
 
 void launch_finalize_adv(const double* seg_partial, const BatchDev& b, int adv_norm,
-                         StepStatsDev* st, int* err, cudaStream_t s) {
-  finalize_adv_kernel<<<1, 1024, 0, s>>>(seg_partial, b, adv_norm, st, err);
+                         StepStatsDev* st, int* err, cudaStream_t s, int segs_per_block) {
+  finalize_adv_kernel<<<1, 1024, 0, s>>>(seg_partial, b, adv_norm, st, err, segs_per_block);
   TLG_CHECK_LAUNCH();
 }
 

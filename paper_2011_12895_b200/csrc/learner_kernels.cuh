@@ -97,10 +97,11 @@ void launch_head_finalize(const HeadDesc& hd, const float* params, const float* 
                           int n_tiles, long F, const BatchDev* b, float* head_out, float* tlogp,
                           float* logits_out, float* probs_out, float* value_out, int* err,
                           cudaStream_t s);
-void launch_returns(const BatchDev& b, int algo, const HyperDev& hp, const float* tlogp,
-                    float* adv, float* target, double* seg_partial, int* err, cudaStream_t s);
+// returns the segments per block of the kernel it chose (the layout of seg_partial)
+int launch_returns(const BatchDev& b, int algo, const HyperDev& hp, const float* tlogp,
+                   float* adv, float* target, double* seg_partial, int* err, cudaStream_t s);
 void launch_finalize_adv(const double* seg_partial, const BatchDev& b, int adv_norm,
-                         StepStatsDev* st, int* err, cudaStream_t s);
+                         StepStatsDev* st, int* err, cudaStream_t s, int segs_per_block);
 struct LossLaunch {
   int stream_blocks;  // rows of the head-weight / last-layer-bias partials
   int math_blocks;    // rows of the loss/stat and head-bias partials

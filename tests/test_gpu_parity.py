@@ -52,10 +52,15 @@ def init_params(oracle, shape, seed, scale=0.3):
 
 
 # ---------------------------------------------------------------------------
-@pytest.mark.parametrize("T", [1, 7, 32, 33, 80])
+@pytest.mark.parametrize("T", [1, 4, 7, 12, 32, 33, 64, 80])
 @pytest.mark.parametrize("algo", ["ppo", "vtrace"])
-def test_returns_kernel_matches_oracle(tlg, oracle, T, algo):
+@pytest.mark.parametrize("kernel", ["auto", "scalar"])
+def test_returns_kernel_matches_oracle(tlg, oracle, T, algo, kernel, monkeypatch):
+    """auto: the vectorised K1 (8 lanes x 4 steps per segment) whenever T % 4 == 0,
+    else the warp-per-segment kernel; scalar: the latter forced."""
     import ctypes as C
+    if kernel == "scalar":
+        monkeypatch.setenv("TLG_RETURNS_SCALAR", "1")
     import torch
     from paper_2011_12895_b200._capi import Hyper, check, lib
     S = 257

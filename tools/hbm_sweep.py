@@ -27,14 +27,14 @@ def peaks():
         return 7700.0, "nominal fallback"
 
 
-def sweep_returns(torch, reps=20):
+def sweep_returns(torch, reps=20, sizes=(4096, 65536, 524288, 1048576)):
     from paper_2011_12895_b200._capi import Hyper, check, lib
     dev = torch.device("cuda", 0)
     stream = torch.cuda.Stream(dev)
     out = []
     l2 = torch.cuda.get_device_properties(0).L2_cache_size
     for algo, name, b_frame in ((0, "ppo", 17), (1, "vtrace", 25)):
-        for S in (4096, 65536, 524288, 1048576):
+        for S in sizes:
             T = 32
             g = torch.Generator(device=dev).manual_seed(S + algo)
             r = torch.rand(S, T, device=dev, generator=g) * 2 - 1
@@ -109,8 +109,14 @@ def sweep_optimizer(torch, steps=10):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default="gpurun_out/hbm_sweep.json")
+    ap.add_argument("--profile-returns", type=int, default=0,
+                    help="only K1 at this many segments, 2 reps (for an ncu capture)")
     a = ap.parse_args()
     import torch
+    if a.profile_returns:
+        for r in sweep_returns(torch, reps=2, sizes=(a.profile_returns,)):
+            print(r["algo"], r["ms"])
+        return
     peak, src = peaks()
     rows = sweep_returns(torch) + sweep_optimizer(torch)
     for r in rows:
