@@ -211,6 +211,13 @@ int tlg_policy_create(const tlg_policy_shape* shape, int32_t device, uint32_t ma
                       tlg_policy** out);
 void tlg_policy_destroy(tlg_policy* p);
 int tlg_policy_set_params(tlg_policy* p, const double* values, size_t n);
+/* Co-located refresh (replaces the fp64 blob round trip of
+ * InfServer::RefreshNow, inf_server.cpp:41-48, when learner and server share a node):
+ * copies the learner's fp32 parameter planes device-to-device (peer-to-peer across
+ * GPUs), stream-ordered after the learner's last step and before its next one; no host
+ * synchronisation.  Same result as tlg_policy_set_params(tlg_learner_get_params(l)).
+ * Shapes must match (else TLG_INVALID_ARGUMENT). */
+int tlg_policy_set_params_from_learner(tlg_policy* p, tlg_learner* l);
 /* obs [n][obs_dim] f32; logits/probs [n][A] f32; value [n] f32.  Host pointers
  * when on_device == 0 (copied on the policy's stream), else device pointers.
  * Each row is evaluated independently of the others (batch-invariant). */

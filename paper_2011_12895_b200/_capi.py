@@ -134,6 +134,7 @@ def lib():
                                         C.POINTER(C.c_void_p)]
         L.tlg_policy_destroy.argtypes = [C.c_void_p]
         L.tlg_policy_set_params.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t]
+        L.tlg_policy_set_params_from_learner.argtypes = [C.c_void_p, C.c_void_p]
         L.tlg_policy_forward.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p,
                                          C.c_void_p, C.c_void_p, C.c_int]
         L.tlg_policy_stream.restype = C.c_void_p
@@ -166,6 +167,7 @@ EXPORTS = [
     "tlg_learner_stream", "tlg_learner_phase_ms", "tlg_learner_last_launches",
     "tlg_learner_kernel_ms", "tlg_learner_set_timing",
     "tlg_policy_create", "tlg_policy_destroy", "tlg_policy_set_params", "tlg_policy_forward",
+    "tlg_policy_set_params_from_learner",
     "tlg_policy_stream", "tlg_returns",
 ]
 
@@ -389,6 +391,10 @@ class Policy:
     def set_params(self, values):
         v = np.ascontiguousarray(values, np.float64)
         check(lib().tlg_policy_set_params(self.h, v.ctypes.data, v.size))
+
+    def refresh_from(self, learner):
+        """Device-to-device refresh from a co-located Learner (no fp64 host round trip)."""
+        check(lib().tlg_policy_set_params_from_learner(self.h, learner.h))
 
     def forward(self, obs, out=None):
         """Host batch in, host results out.  `out` = (logits, probs, value) arrays to fill

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <stdexcept>
 #include <string>
 
@@ -25,6 +26,21 @@ struct CudaError : std::runtime_error {
 #define TLG_CHECK_LAUNCH() TLG_CUDA(cudaGetLastError())
 
 inline int ceil_div(long a, long b) { return int((a + b - 1) / b); }
+
+// Function attributes are per device: raise a kernel's dynamic shared-memory limit once
+// on every device it is launched on (one bit per device in `done`).
+template <typename Kernel>
+inline void ensure_smem_attr(Kernel kern, int bytes, std::atomic<unsigned long long>& done) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) throw CudaError("cudaGetDevice failed");
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return;
+  const cudaError_t e =
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess)
+    throw CudaError(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+  done.fetch_or(bit, std::memory_order_acq_rel);
+}
 
 // ---------------------------------------------------------------------------
 // TF32 hi/lo split.  hi keeps the 10 explicit mantissa bits a tcgen05 kind::tf32

@@ -45,11 +45,8 @@ void run_i8_fwd(const CUtensorMap& tb, const CUtensorMap& tq, const CUtensorMap&
   auto kern = gemm_i8_bits_fwd_kernel<BN, CG, MC>;
   constexpr int bytes = SmemI8<BN, CG>::kBytes;
   static_assert(bytes <= 227 * 1024, "shared memory budget");
-  static bool attr = false;
-  if (!attr) {
-    TLG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};  // per device
+  ensure_smem_attr(kern, bytes, attr);
   const int tiles = tm.m_tiles * tm.n_tiles;
   if (CG == 1) {
     kern<<<std::min(tiles, num_sms()), kThreadsI8, bytes, stream>>>(tb, tq, to, tl, p, tm);
@@ -121,11 +118,8 @@ void run_i8_dw(const CUtensorMap& tp, const CUtensorMap& tb, const CUtensorMap& 
   auto kern = gemm_i8_bits_dw_kernel<CG>;
   constexpr int bytes = SmemI8Dw<CG>::kBytes;
   static_assert(bytes <= 227 * 1024, "shared memory budget");
-  static bool attr = false;
-  if (!attr) {
-    TLG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};  // per device
+  ensure_smem_attr(kern, bytes, attr);
   const int tiles = tm.m_tiles * tm.n_tiles * tm.splits;
   if (CG == 1) {
     kern<<<std::min(tiles, num_sms()), kThreadsI8, bytes, stream>>>(tp, tb, tw, p, tm);
@@ -267,11 +261,8 @@ void run_i8x2_fwd(const CUtensorMap& ta, const CUtensorMap& tq, const CUtensorMa
   auto kern = gemm_i8x2_fwd_kernel<BN, CG>;
   constexpr int bytes = SmemI8x2<BN, CG>::kBytes;
   static_assert(bytes <= 227 * 1024, "shared memory budget");
-  static bool attr = false;
-  if (!attr) {
-    TLG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};  // per device
+  ensure_smem_attr(kern, bytes, attr);
   const int tiles = tm.m_tiles * tm.n_tiles;
   constexpr int threads = 32 * (2 + kEpiWarps);
   if (CG == 1) {

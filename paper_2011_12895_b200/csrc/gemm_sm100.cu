@@ -112,11 +112,8 @@ void run(const CUtensorMap& ah, const CUtensorMap& al, const CUtensorMap& bh,
   auto kern = gemm_tf32x3_kernel<BN, A_MN, B_MN, A_LO, B_LO, EPI, U8, CG>;
   constexpr int bytes = Smem<BN, A_LO, B_LO, EPI, U8, CG>::kBytes;
   static_assert(bytes <= 227 * 1024, "shared memory budget");
-  static bool attr = false;  // one-time per instantiation
-  if (!attr) {
-    TLG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};  // per device
+  ensure_smem_attr(kern, bytes, attr);
   const TileMap tm{int(grid.x), int(grid.y), int(grid.z)};  // grid.x counts (128*CG)-row tiles
   const int tiles = tm.m_tiles * tm.n_tiles * tm.splits;
   if (CG == 1) {

@@ -1589,6 +1589,42 @@ int tlg_policy_set_params(tlg_policy* p, const double* values, size_t n) {
   });
 }
 
+int tlg_policy_set_params_from_learner(tlg_policy* p, tlg_learner* l) {
+  return Guard([&] {
+    if (!p || !l) throw InvalidArg("null argument");
+    if (p->net.P != l->net.P || p->net.dims != l->net.dims || p->net.A != l->net.A ||
+        p->net.family != l->net.family)
+      throw InvalidArg("policy and learner shapes differ");
+    // learner stream -> policy stream: the copy sees the learner's last step; policy
+    // stream -> learner stream: the learner's next optimizer step waits for the copy.
+    // No host synchronisation; the planes (params and their tf32 residuals, kept in step
+    // by the optimizer) cross NVLink peer-to-peer when the devices differ.
+    cudaEvent_t ev_l, ev_p;
+    TLG_CUDA(cudaSetDevice(l->cfg.device));
+    TLG_CUDA(cudaEventCreateWithFlags(&ev_l, cudaEventDisableTiming));
+    TLG_CUDA(cudaEventRecord(ev_l, l->stream));
+    TLG_CUDA(cudaSetDevice(p->device));
+    TLG_CUDA(cudaEventCreateWithFlags(&ev_p, cudaEventDisableTiming));
+    TLG_CUDA(cudaStreamWaitEvent(p->stream, ev_l, 0));
+    const size_t bytes = size_t(p->P_pad) * 4;
+    if (p->device == int(l->cfg.device)) {
+      TLG_CUDA(cudaMemcpyAsync(p->params, l->params, bytes, cudaMemcpyDeviceToDevice, p->stream));
+      TLG_CUDA(cudaMemcpyAsync(p->params_lo, l->params_lo, bytes, cudaMemcpyDeviceToDevice,
+                               p->stream));
+    } else {
+      TLG_CUDA(cudaMemcpyPeerAsync(p->params, p->device, l->params, int(l->cfg.device), bytes,
+                                   p->stream));
+      TLG_CUDA(cudaMemcpyPeerAsync(p->params_lo, p->device, l->params_lo, int(l->cfg.device),
+                                   bytes, p->stream));
+    }
+    TLG_CUDA(cudaEventRecord(ev_p, p->stream));
+    TLG_CUDA(cudaSetDevice(l->cfg.device));
+    TLG_CUDA(cudaStreamWaitEvent(l->stream, ev_p, 0));
+    TLG_CUDA(cudaEventDestroy(ev_l));  // destruction is deferred until the event completes
+    TLG_CUDA(cudaEventDestroy(ev_p));
+  });
+}
+
 int tlg_policy_forward(tlg_policy* p, const float* obs, size_t n, float* logits, float* probs,
                        float* value, int on_device) {
   return Guard([&] {

@@ -698,3 +698,42 @@ def test_boundary_errors_match_reference_exception_types(tlg, oracle):
     with pytest.raises(tlg.InvalidArgument, match="parameter count"):
         lrn.set_teacher(np.zeros(3))
     rep.close()
+
+
+# ---------------------------------------------------------------------------
+# co-located InfServer refresh, device to device
+@pytest.mark.parametrize("devices", [(0, 0), (0, 1)])
+def test_policy_refresh_from_learner_matches_host_refresh(tlg, oracle, devices):
+    """tlg_policy_set_params_from_learner gives bit-identical forwards to the fp64 host
+    round trip, and is stream-ordered against the learner's steps on both sides."""
+    import torch
+    from paper_2011_12895_b200._capi import InvalidArgument
+    ldev, pdev = devices
+    if max(devices) >= torch.cuda.device_count():
+        pytest.skip("needs 2 GPUs")
+    S, T, D, A, hidden = 16, 8, 64, 6, (64, 32)
+    lrn = tlg.Learner("mlp", D, A, hidden, max_segments=S, unroll_len=T, device=ldev)
+    lrn.set_hyper(learning_rate=1e-2, batch_size=S, unroll_len=T)
+    lrn.set_params(init_params(oracle, Shape(2, D, A, hidden), 77))
+    batches = [tlg.synth.make_segments(S, T, D, A, seed=40 + k) for k in range(3)]
+    lrn.train_step(batches[0])
+    snap = lrn.get_params()                 # params after step 1
+    d2d = tlg.Policy("mlp", D, A, hidden, device=pdev, max_batch=512)
+    host = tlg.Policy("mlp", D, A, hidden, device=pdev, max_batch=512)
+    d2d.refresh_from(lrn)                   # async: ordered after step 1 ...
+    lrn.train_step(batches[1])              # ... and before step 2's update
+    host.set_params(snap)
+    obs = np.random.default_rng(3).standard_normal((300, D)).astype(np.float32)
+    a, b = d2d.forward(obs), host.forward(obs)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+    # a second refresh picks up step 2
+    d2d.refresh_from(lrn)
+    host.set_params(lrn.get_params())
+    for x, y in zip(d2d.forward(obs), host.forward(obs)):
+        assert np.array_equal(x, y)
+    other = tlg.Policy("mlp", D, A, (64, 64), device=pdev, max_batch=16)
+    with pytest.raises(InvalidArgument, match="shapes differ"):
+        other.refresh_from(lrn)
+    for o in (d2d, host, other, lrn):
+        o.close()
