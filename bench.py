@@ -347,9 +347,8 @@ def main():
         fr = 0
         lrn.stage(views[0])
         for i in range(nsteps):
-            if i + 1 < nsteps:
-                lrn.stage(views[(i + 1) % 2])
-            lrn.train_staged()
+            # step i runs while batch i+1's H2D is issued (tlg_learner_train_staged_next)
+            lrn.train_staged(views[(i + 1) % 2] if i + 1 < nsteps else None)
             fr += frames_per_step[i % 2]
         dt = max_over_ranks(time.perf_counter() - t0)
         return sum_over_ranks(fr) / dt

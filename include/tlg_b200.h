@@ -170,6 +170,11 @@ int tlg_learner_train_step_shards(tlg_learner* l, const tlg_segment_batch* shard
  * overlaps step k; tlg_learner_train_staged runs one step on the oldest staged batch. */
 int tlg_learner_stage(tlg_learner* l, const tlg_segment_batch* host_batch);
 int tlg_learner_train_staged(tlg_learner* l, tlg_step_stats* stats);
+/* tlg_learner_train_staged, and — when next_host_batch is not NULL — tlg_learner_stage of
+ * that batch issued while the step runs (after its launch, before its results are read),
+ * so the host-side staging work leaves the critical path: one call per step. */
+int tlg_learner_train_staged_next(tlg_learner* l, const tlg_segment_batch* next_host_batch,
+                                  tlg_step_stats* stats);
 
 /* Device-resident replay: segments are copied to HBM once, at ingest,
  * into `capacity` slots; a training step then names its segments by slot and the batch

@@ -122,6 +122,8 @@ def lib():
                                                     C.c_int, C.POINTER(StepStats)]
         L.tlg_learner_stage.argtypes = [C.c_void_p, C.POINTER(SegmentBatchC)]
         L.tlg_learner_train_staged.argtypes = [C.c_void_p, C.POINTER(StepStats)]
+        L.tlg_learner_train_staged_next.argtypes = [C.c_void_p, C.POINTER(SegmentBatchC),
+                                                    C.POINTER(StepStats)]
         L.tlg_learner_get_returns.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t]
         L.tlg_learner_stream.restype = C.c_void_p
         L.tlg_learner_stream.argtypes = [C.c_void_p]
@@ -163,7 +165,8 @@ EXPORTS = [
     "tlg_learner_train_step_replay",
     "tlg_learner_set_hyper", "tlg_comm_unique_id", "tlg_learner_comm_init",
     "tlg_learner_train_step", "tlg_learner_train_step_shards", "tlg_learner_get_grad",
-    "tlg_learner_stage", "tlg_learner_train_staged", "tlg_learner_get_returns",
+    "tlg_learner_stage", "tlg_learner_train_staged", "tlg_learner_train_staged_next",
+    "tlg_learner_get_returns",
     "tlg_learner_stream", "tlg_learner_phase_ms", "tlg_learner_last_launches",
     "tlg_learner_kernel_ms", "tlg_learner_set_timing",
     "tlg_policy_create", "tlg_policy_destroy", "tlg_policy_set_params", "tlg_policy_forward",
@@ -300,9 +303,14 @@ class Learner:
         """Queue the async H2D of a host batch (keep `batch_view` alive until trained)."""
         check(lib().tlg_learner_stage(self.h, C.byref(batch_view.c)))
 
-    def train_staged(self):
+    def train_staged(self, next_view=None):
+        """Train the oldest staged batch; `next_view` (kept alive by the caller) is staged
+        while that step runs."""
         st = StepStats()
-        check(lib().tlg_learner_train_staged(self.h, C.byref(st)))
+        if next_view is None:
+            check(lib().tlg_learner_train_staged(self.h, C.byref(st)))
+        else:
+            check(lib().tlg_learner_train_staged_next(self.h, C.byref(next_view.c), C.byref(st)))
         return st.as_dict()
 
     def get_returns(self, n_frames):

@@ -842,7 +842,7 @@ struct tlg_learner {
   }
 
   void step(const tlg_segment_batch* bs, int n, int on_device, tlg_step_stats* out,
-            cudaEvent_t consumed = nullptr) {
+            cudaEvent_t consumed = nullptr, const tlg_segment_batch* stage_next = nullptr) {
     if (!hp_set) throw InvalidArg("hyperparameters not set");
     // PpoLossAndGrad (rlmath.cpp:119-120); the PG (V-trace) loss takes no teacher
     if (hp.kl_teacher_coef > 0.0 && cfg.algo != TLG_ALGO_VTRACE && !has_teacher)
@@ -885,6 +885,8 @@ struct tlg_learner {
       enqueue_device_step(nullptr, n, bs, on_device);
     }
     if (consumed) TLG_CUDA(cudaEventRecord(consumed, stream));
+    // host-side staging of the next batch while this step runs on the device
+    if (stage_next) stage_async(*stage_next);
     finish(n, out);
   }
 
@@ -903,10 +905,14 @@ struct tlg_learner {
   int slot_next = 0, slot_count = 0, slot_head = 0;
   cudaStream_t copy_stream = nullptr;
 
-  void stage_async(const tlg_segment_batch& b) {
-    if (slot_count == 2) throw InvalidArg("both staging slots hold untrained batches");
+  void check_stage(const tlg_segment_batch& b) const {
     if (int(b.n_segments) > S_max || b.n_segments == 0) throw InvalidArg("bad batch size");
     if (int(b.unroll_len) != T) throw InvalidArg("unroll_len mismatch");
+  }
+
+  void stage_async(const tlg_segment_batch& b) {
+    if (slot_count == 2) throw InvalidArg("both staging slots hold untrained batches");
+    check_stage(b);
     if (!copy_stream) TLG_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
     Slot& sl = slots[slot_next];
     const long S = b.n_segments, F = S * T, D = net.D;
@@ -955,13 +961,14 @@ struct tlg_learner {
     ++slot_count;
   }
 
-  void train_staged(tlg_step_stats* out) {
+  void train_staged(tlg_step_stats* out, const tlg_segment_batch* next = nullptr) {
     if (slot_count == 0) throw InvalidArg("no staged batch");
+    if (next) check_stage(*next);  // fail before the step is launched
     Slot& sl = slots[slot_head];
     slot_head ^= 1;
     --slot_count;
     TLG_CUDA(cudaStreamWaitEvent(stream, sl.ready, 0));
-    step(&sl.dev, 1, /*on_device=*/1, out, sl.consumed);
+    step(&sl.dev, 1, /*on_device=*/1, out, sl.consumed, next);
   }
 
 
@@ -1545,6 +1552,14 @@ int tlg_learner_train_staged(tlg_learner* l, tlg_step_stats* stats) {
   return Guard([&] {
     TLG_CUDA(cudaSetDevice(l->cfg.device));
     l->train_staged(stats);
+  });
+}
+
+int tlg_learner_train_staged_next(tlg_learner* l, const tlg_segment_batch* next_host_batch,
+                                  tlg_step_stats* stats) {
+  return Guard([&] {
+    TLG_CUDA(cudaSetDevice(l->cfg.device));
+    l->train_staged(stats, next_host_batch);
   });
 }
 

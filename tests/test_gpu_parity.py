@@ -535,12 +535,18 @@ def test_staged_f32_inputs_match_train_step(tlg, oracle, monkeypatch, no_graph):
     p = init_params(oracle, Shape(2, D, A, hidden), 11)
     batches = [make_batch(tlg, S, T, D, A, seed=300 + k) for k in range(4)]
     res = []
-    for mode in ("plain", "staged"):
+    for mode in ("plain", "staged", "staged_next"):
         lrn = tlg.Learner("mlp", D, A, hidden, max_segments=S, unroll_len=T, optimizer="sgd")
         lrn.set_hyper(learning_rate=0.05, batch_size=S, unroll_len=T)
         lrn.set_params(p)
         if mode == "plain":
             stats = [lrn.train_step(b) for b in batches]
+        elif mode == "staged_next":  # one call per step, staging overlapped with the step
+            from paper_2011_12895_b200._capi import SegmentBatchView
+            views = [SegmentBatchView(b) for b in batches]
+            lrn.stage(views[0])
+            stats = [lrn.train_staged(views[k + 1] if k + 1 < len(views) else None)
+                     for k in range(len(views))]
         else:
             from paper_2011_12895_b200._capi import SegmentBatchView
             views = [SegmentBatchView(b) for b in batches]
@@ -553,8 +559,9 @@ def test_staged_f32_inputs_match_train_step(tlg, oracle, monkeypatch, no_graph):
                 stats.append(lrn.train_staged())
             stats.append(lrn.train_staged())
         res.append((lrn.get_params(), stats))
-    assert np.array_equal(res[0][0], res[1][0])
-    assert res[0][1] == res[1][1]
+    for r in res[1:]:
+        assert np.array_equal(res[0][0], r[0])
+        assert res[0][1] == r[1]
 
 
 @pytest.mark.parametrize("case", [("mlp", 16, (32, 32), "gauss"), ("linear", 10, (), "gauss"),
