@@ -1,4 +1,5 @@
 // Host side of the exact-integer binary-plane GEMM (gemm_i8.cuh) + the weight quantizer.
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -53,7 +54,6 @@ void run_i8_fwd(const CUtensorMap& tb, const CUtensorMap& tq, const CUtensorMap&
   } else {
     cudaLaunchConfig_t cfg{};
     constexpr int kCl = CG * MC;
-    cfg.gridDim = dim3(kCl * std::min(tiles, num_sms() / kCl));
     cfg.blockDim = dim3(kThreadsI8);
     cfg.dynamicSmemBytes = bytes;
     cfg.stream = stream;
@@ -64,6 +64,27 @@ void run_i8_fwd(const CUtensorMap& tb, const CUtensorMap& tq, const CUtensorMap&
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
+    // persistent grid = the clusters that are co-resident (GPCs need not hold a multiple of
+    // kCl SMs; a second partial wave of persistent clusters would double the time)
+    // (pairs: every GPC holds an even number of SMs, and the occupancy query under-reports
+    // them — 74 pairs measured faster than the queried count)
+    static std::atomic<int> max_cl{0};
+    if (max_cl.load() == 0) {
+      int n = num_sms() / kCl;
+      if (MC == 2) {
+        cfg.gridDim = dim3(kCl * n);
+        TLG_CUDA(cudaOccupancyMaxActiveClusters(&n, kern, &cfg));
+      }
+      if (std::getenv("TLG_DEBUG_CLUSTERS")) {
+        int q = 0;
+        cfg.gridDim = dim3(kCl * (num_sms() / kCl));
+        cudaOccupancyMaxActiveClusters(&q, kern, &cfg);
+        fprintf(stderr, "i8 fwd: cluster %d, persistent clusters %d, occupancy query %d\n",
+                kCl, n, q);
+      }
+      max_cl.store(std::max(1, std::min(n, num_sms() / kCl)));
+    }
+    cfg.gridDim = dim3(kCl * std::min(tiles, max_cl.load()));
     TLG_CUDA(cudaLaunchKernelEx(&cfg, kern, tb, tq, to, tl, p, tm));
   }
   TLG_CHECK_LAUNCH();
@@ -351,7 +372,7 @@ LaunchInfo launch_i8_bits_fwd(const uint8_t* bits, long rowb, const int8_t* q, l
   else run_i8_fwd<BN, 1>(tb, tq, to, tl, p, tm, stream);
   const int tiles = tm.m_tiles * tm.n_tiles;
   const int cl = cg * mc;
-  return {BN, cl * std::min(tiles, num_sms() / cl)};
+  return {BN, cl * std::min(tiles, num_sms() / cl)};  // upper bound on the CTAs launched
 }
 
 }  // namespace tlg::gemm

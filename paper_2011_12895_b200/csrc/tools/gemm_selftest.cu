@@ -505,7 +505,10 @@ int main(int argc, char** argv) {
     check_i8_dw("I8 bits dW", 128, 200, 1000, 2);
     check_i8_dw("I8 bits dW pair", 256, 1936, 4096, 8);
     check_i8_dw("I8 bits dW ragged", 256, 300, 1300, 4);
-    if (argc > 1 && std::string(argv[1]) == "c5") {
+    if (argc > 1 && std::string(argv[1]) == "i8") {
+      check_i8("perf I8 bits fwd C3 L1", 131072, 256, 1936);
+      check_i8("perf I8 bits fwd C3 L1", 131072, 256, 1936);
+    } else if (argc > 1 && std::string(argv[1]) == "c5") {
       g_noref = true;  // C5 trunk shapes (4x2048, 131,072 frames per shard)
       check("perf fwd C5", 131072, 2048, 2048, false, false, false, kEpiFwdTanh, 1);
       check("perf dX C5 K/MN", 131072, 2048, 2048, false, true, false, kEpiBwdTanh, 1);
