@@ -54,10 +54,11 @@ def init_params(oracle, shape, seed, scale=0.3):
 # ---------------------------------------------------------------------------
 @pytest.mark.parametrize("T", [1, 4, 7, 12, 32, 33, 64, 80])
 @pytest.mark.parametrize("algo", ["ppo", "vtrace"])
-@pytest.mark.parametrize("kernel", ["auto", "scalar"])
+@pytest.mark.parametrize("kernel", ["auto", "scalar", "misaligned"])
 def test_returns_kernel_matches_oracle(tlg, oracle, T, algo, kernel, monkeypatch):
     """auto: the vectorised K1 (8 lanes x 4 steps per segment) whenever T % 4 == 0,
-    else the warp-per-segment kernel; scalar: the latter forced."""
+    else the warp-per-segment kernel; scalar: the latter forced; misaligned: rows that
+    are not 16-B aligned (caller buffers at a 4-B offset) take the scalar kernel."""
     import ctypes as C
     if kernel == "scalar":
         monkeypatch.setenv("TLG_RETURNS_SCALAR", "1")
@@ -75,6 +76,13 @@ def test_returns_kernel_matches_oracle(tlg, oracle, T, algo, kernel, monkeypatch
         bl=b.behavior_logp, tl=tl).items()}
     adv = torch.zeros(S, T, device=dev)
     tgt = torch.zeros(S, T, device=dev)
+    if kernel == "misaligned":
+        def shifted(x):
+            y = torch.zeros(x.numel() + 1, dtype=x.dtype, device=dev)[1:].view(x.shape)
+            y.copy_(x)
+            return y
+        t["r"], t["v"] = shifted(t["r"]), shifted(t["v"])
+        adv, tgt = shifted(adv), shifted(tgt)
     h = Hyper.make(**hp)
     torch.cuda.synchronize()
     check(lib().tlg_returns(ALGO[algo], C.byref(h), S, T, t["r"].data_ptr(), t["v"].data_ptr(),
