@@ -26,6 +26,8 @@
 #include "tleague/pool/pool_iface.hpp"
 #include "tleague/types.hpp"
 
+struct tlg_segment_batch;  // include/tlg_b200.h (SoA segment batch of the C ABI)
+
 namespace tleague::learner {
 
 enum class Algo { kPpo, kVtrace, kPpoVtrace };
@@ -76,6 +78,12 @@ class Learner : public SegmentSink {
 
   void StartPeriod();
   void PushSegment(const TrajectorySegment& segment) override;
+  // Bulk SoA ingest (an extension): `batch.n_segments` segments of one
+  // model key in the C ABI's SoA layout (TLG_OBS_F32 or TLG_OBS_BITS) — what a bulk
+  // segment message would carry.  Same replay bookkeeping and draws as that many
+  // PushSegment calls in order; with device_replay the observations go to their HBM
+  // slots in one copy instead of one per segment.  At most replay_capacity segments.
+  void PushSegmentBatch(const std::string& model_key, const tlg_segment_batch& batch);
   bool TrainStep();
   std::string FinishPeriod();
   std::string RunPeriod();

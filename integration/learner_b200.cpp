@@ -410,6 +410,92 @@ void Learner::PushSegment(const TrajectorySegment& segment) {
   g.cv.notify_all();
 }
 
+namespace {
+// one SoA segment -> a TrajectorySegment (observations widened exactly to f64)
+TrajectorySegment SegmentFromSoa(const tlg_segment_batch& b, std::uint32_t i,
+                                 const std::string& key) {
+  const std::uint32_t T = b.unroll_len, D = b.obs_dim;
+  const std::size_t rowb = b.obs_pitch ? b.obs_pitch : (D + 7) / 8;
+  TrajectorySegment seg;
+  seg.model_key = key;
+  seg.valid_steps = std::uint32_t(b.valid_steps[i]);
+  seg.bootstrap_value = b.bootstrap[i];
+  seg.steps.resize(seg.valid_steps);
+  for (std::uint32_t t = 0; t < seg.valid_steps; ++t) {
+    const std::size_t f = std::size_t(i) * T + t;
+    SegmentStep& st = seg.steps[t];
+    st.obs.resize(D);
+    if (b.obs_dtype == TLG_OBS_BITS) {
+      const auto* row = static_cast<const std::uint8_t*>(b.obs) + f * rowb;
+      for (std::uint32_t j = 0; j < D; ++j) st.obs[j] = (row[j >> 3] >> (j & 7)) & 1u;
+    } else {
+      const float* row = static_cast<const float*>(b.obs) + f * D;
+      for (std::uint32_t j = 0; j < D; ++j) st.obs[j] = row[j];
+    }
+    st.action = std::uint32_t(b.action[f]);
+    st.reward = b.reward[f];
+    st.behavior_logp = b.behavior_logp[f];
+    st.value_est = b.value_est[f];
+    st.done = b.done[f] != 0;
+  }
+  return seg;
+}
+}  // namespace
+
+void Learner::PushSegmentBatch(const std::string& model_key, const tlg_segment_batch& b) {
+  if (b.obs_dtype != TLG_OBS_F32 && b.obs_dtype != TLG_OBS_BITS)
+    throw std::invalid_argument("PushSegmentBatch: observations must be f32 or bit planes");
+  if (b.n_segments == 0) return;
+  if (b.n_segments > config_.replay_capacity)
+    throw std::invalid_argument("PushSegmentBatch: more segments than replay_capacity");
+  for (std::uint32_t i = 0; i < b.n_segments; ++i)
+    if (b.valid_steps[i] < 0 || std::uint32_t(b.valid_steps[i]) > b.unroll_len)
+      throw std::invalid_argument("segment valid_steps exceeds its steps / unroll_len");
+  {
+    std::lock_guard lock(task_mu_);
+    if (model_key != current_key_) {
+      stale_dropped_.fetch_add(b.n_segments, std::memory_order_relaxed);
+      return;
+    }
+  }
+  if (!config_.device_replay) {
+    for (std::uint32_t i = 0; i < b.n_segments; ++i) replay_.Push(SegmentFromSoa(b, i, model_key));
+    return;
+  }
+  Gpu& g = *gpu_;
+  std::lock_guard dl(g.mu);
+  if (b.unroll_len != g.T || b.obs_dim != g.shape.obs_dim)
+    throw std::invalid_argument("PushSegmentBatch: unroll_len / obs_dim do not match");
+  if (!g.ring_decided) {
+    g.ring_dtype = b.obs_dtype;
+    Check(tlg_replay_create(g.h, g.ring_cap, g.ring_dtype, &g.ring));
+    g.ring_decided = true;
+  }
+  if (b.obs_dtype != g.ring_dtype)
+    throw std::invalid_argument("PushSegmentBatch: observation format differs from the period's");
+  // admit in order (mirrors n ReplayMem::Push evictions), one device copy, then the
+  // observation-less entries in the same order
+  std::vector<std::uint32_t> slots(b.n_segments);
+  std::vector<std::uint64_t> ids(b.n_segments);
+  for (std::uint32_t i = 0; i < b.n_segments; ++i) {
+    slots[i] = g.Admit(config_.replay_capacity);
+    ids[i] = g.next_id;
+    g.live.emplace(g.next_id, Gpu::Live{slots[i], 0});
+    g.fifo.push_back(g.next_id++);
+  }
+  Check(tlg_replay_put(g.ring, slots.data(), &b));
+  for (std::uint32_t i = 0; i < b.n_segments; ++i) {
+    TrajectorySegment stripped = SegmentFromSoa(b, i, model_key);
+    for (SegmentStep& st : stripped.steps) {
+      st.obs.clear();
+      st.obs.shrink_to_fit();
+    }
+    stripped.segment_seq = ids[i];
+    replay_.Push(std::move(stripped));
+  }
+  g.cv.notify_all();
+}
+
 bool Learner::TrainStep() {
   if (config_.step_delay_ms > 0)
     std::this_thread::sleep_for(std::chrono::milliseconds(config_.step_delay_ms));

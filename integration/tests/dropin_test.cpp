@@ -503,6 +503,124 @@ TEST(device_resident_replay_matches_the_host_replay_path) {
   }
 }
 
+// the SoA layout of the C ABI for a group of segments (what a bulk message would carry)
+struct SoaBatch {
+  std::vector<std::uint8_t> obs8, done;
+  std::vector<float> obs32, reward, blogp, value, boot;
+  std::vector<std::int32_t> action, valid;
+  tlg_segment_batch c{};
+};
+
+std::unique_ptr<SoaBatch> ToSoa(const std::vector<TrajectorySegment>& segs, std::uint32_t T,
+                                std::uint32_t D, bool bits) {
+  auto b = std::make_unique<SoaBatch>();
+  const std::size_t n = segs.size(), rowb = (D + 7) / 8;
+  if (bits) b->obs8.assign(n * T * rowb, 0);
+  else b->obs32.assign(n * T * D, 0.f);
+  b->done.assign(n * T, 0);
+  b->reward.assign(n * T, 0.f);
+  b->blogp.assign(n * T, 0.f);
+  b->value.assign(n * T, 0.f);
+  b->action.assign(n * T, 0);
+  for (std::size_t i = 0; i < n; ++i) {
+    const TrajectorySegment& sg = segs[i];
+    b->boot.push_back(float(sg.bootstrap_value));
+    b->valid.push_back(std::int32_t(sg.valid_steps));
+    for (std::uint32_t t = 0; t < sg.valid_steps; ++t) {
+      const std::size_t f = i * T + t;
+      const SegmentStep& st = sg.steps[t];
+      for (std::uint32_t j = 0; j < D; ++j) {
+        if (bits) b->obs8[f * rowb + j / 8] |= std::uint8_t((st.obs[j] == 1.0) << (j % 8));
+        else b->obs32[f * D + j] = float(st.obs[j]);
+      }
+      b->action[f] = std::int32_t(st.action);
+      b->reward[f] = float(st.reward);
+      b->blogp[f] = float(st.behavior_logp);
+      b->value[f] = float(st.value_est);
+      b->done[f] = st.done ? 1 : 0;
+    }
+  }
+  tlg_segment_batch& c = b->c;
+  c.n_segments = std::uint32_t(n);
+  c.unroll_len = T;
+  c.obs_dim = D;
+  c.obs_dtype = bits ? TLG_OBS_BITS : TLG_OBS_F32;
+  c.obs = bits ? static_cast<const void*>(b->obs8.data()) : static_cast<const void*>(b->obs32.data());
+  c.action = b->action.data();
+  c.reward = b->reward.data();
+  c.behavior_logp = b->blogp.data();
+  c.value_est = b->value.data();
+  c.done = b->done.data();
+  c.bootstrap = b->boot.data();
+  c.valid_steps = b->valid.data();
+  return b;
+}
+
+TEST(bulk_soa_ingest_matches_per_segment_pushes) {
+  // Learner::PushSegmentBatch (one SoA copy into the device ring per group) draws and
+  // trains exactly like the same segments pushed one by one; in host-replay mode too.
+  for (auto algo : {learner::Algo::kPpo, learner::Algo::kVtrace}) {
+    HyperParams hyper = TestHyper();
+    hyper.max_reuse = algo == learner::Algo::kVtrace ? 2 : 1;
+    Rig rig_a(hyper), rig_b(hyper), rig_c(hyper);
+    learner::LearnerConfig cfg;
+    cfg.num_shards = 2;
+    cfg.algo = algo;
+    cfg.publish_interval = 1;
+    cfg.seed = 9;
+    cfg.replay_capacity = 12;
+    cfg.device_replay = true;
+    learner::LearnerConfig cfg_host = cfg;
+    cfg_host.device_replay = false;
+    learner::Learner one(cfg, rig_a.league, rig_a.pool);
+    learner::Learner bulk(cfg, rig_b.league, rig_b.pool);
+    learner::Learner bulk_host(cfg_host, rig_c.league, rig_c.pool);
+    std::mt19937_64 feed(123);
+    std::uint64_t seq = 0;
+    for (int step = 0; step < 16; ++step) {
+      const int pushes = 8 + step % 4;
+      std::vector<TrajectorySegment> group;
+      for (int i = 0; i < pushes; ++i, ++seq) {
+        TrajectorySegment sg = MakeSegment(one.current_key(), feed, seq);
+        if (seq % 3 == 1) {  // ragged
+          sg.valid_steps = 2;
+          sg.steps.resize(2);
+        }
+        one.PushSegment(sg);
+        group.push_back(std::move(sg));
+      }
+      auto soa_bits = ToSoa(group, hyper.unroll_len, 1, true);
+      auto soa_f32 = ToSoa(group, hyper.unroll_len, 1, false);
+      bulk.PushSegmentBatch(bulk.current_key(), soa_bits->c);
+      bulk_host.PushSegmentBatch(bulk_host.current_key(), soa_f32->c);
+      CHECK(one.replay().size() == bulk.replay().size());
+      CHECK(one.replay().size() == bulk_host.replay().size());
+      CHECK(one.TrainStep());
+      CHECK(bulk.TrainStep());
+      CHECK(bulk_host.TrainStep());
+      CHECK(one.params().values == bulk.params().values);
+      CHECK(one.params().values == bulk_host.params().values);
+      CHECK(one.replay().consumed_steps() == bulk.replay().consumed_steps());
+    }
+    // stale keys are dropped as a whole, oversize groups rejected
+    std::vector<TrajectorySegment> stale{MakeSegment("other:0000", feed, 0)};
+    auto st = ToSoa(stale, hyper.unroll_len, 1, true);
+    const auto before = bulk.Counters().stale_dropped;
+    bulk.PushSegmentBatch("other:0000", st->c);
+    CHECK(bulk.Counters().stale_dropped == before + 1);
+    std::vector<TrajectorySegment> big;
+    for (int i = 0; i < 13; ++i) big.push_back(MakeSegment(bulk.current_key(), feed, 0));
+    auto bg = ToSoa(big, hyper.unroll_len, 1, true);
+    bool threw = false;
+    try {
+      bulk.PushSegmentBatch(bulk.current_key(), bg->c);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    CHECK(threw);
+  }
+}
+
 TEST(reference_run_bench_runs_on_the_b200_learner) {
   // run::RunBench (bench.cpp:60-162) builds learner::Learner -- here the B200 drop-in --
   // next to the reference's own actors, league and pool.
