@@ -432,7 +432,12 @@ __device__ __forceinline__ float scan4(const Aff4& m, float carry, float& x_next
   return x0;
 }
 
-__global__ void __launch_bounds__(256) returns_vec_kernel(BatchDev b, int algo, HyperDev hp,
+// Each lane has only ~36-52 B of loads in flight (one chunk at T=32), so bytes in flight per
+// SM scale with resident CTAs: PPO is capped at 32 registers (8 CTAs/SM, 20 B spilled to L1),
+// V-trace at 40 (6 CTAs/SM).  At 1 M segments (>= 4x L2) this took the kernel from 157 to
+// 114 us (PPO) and 180 to 159 us (V-trace) in ncu (profiles/r01_k1_occupancy.md).
+template <int kAlgo>
+__global__ void __launch_bounds__(256, kAlgo == kAlgoPpo ? 8 : 6) returns_vec_kernel(BatchDev b, HyperDev hp,
                                                           const float* __restrict__ tlogp,
                                                           float* __restrict__ adv,
                                                           float* __restrict__ target,
@@ -470,7 +475,7 @@ __global__ void __launch_bounds__(256) returns_vec_kernel(BatchDev b, int algo, 
       dn = *reinterpret_cast<const uchar4*>(b.done + base + t0);
       r[0] = r4.x; r[1] = r4.y; r[2] = r4.z; r[3] = r4.w;
       v[0] = v4.x; v[1] = v4.y; v[2] = v4.z; v[3] = v4.w;
-      if (algo != kAlgoPpo) {
+      if (kAlgo != kAlgoPpo) {
         const float4 b4 = *reinterpret_cast<const float4*>(b.blogp + base + t0);
         const float4 l4 = *reinterpret_cast<const float4*>(tlogp + base + t0);
         bl[0] = b4.x; bl[1] = b4.y; bl[2] = b4.z; bl[3] = b4.w;
@@ -496,7 +501,7 @@ __global__ void __launch_bounds__(256) returns_vec_kernel(BatchDev b, int algo, 
       if (t0 + q + 1 >= n) vn[q] = boot;
     }
     float out_a[4], out_t[4];
-    if (algo == kAlgoPpo) {
+    if constexpr (kAlgo == kAlgoPpo) {
       // GaeAdvantages (rlmath.cpp:62-78) and LambdaReturn (:45-60)
       Aff4 ma, mg;
 #pragma unroll
@@ -1276,8 +1281,14 @@ int launch_returns(const BatchDev& b, int algo, const HyperDev& hp, const float*
   int per;
   if (returns_vec_ok(b, algo, tlogp, adv, target)) {
     per = kRetVecSegsPerBlock;
-    returns_vec_kernel<<<ceil_div(b.S, per), 256, 0, s>>>(b, algo, hp, tlogp, adv, target,
-                                                           seg_partial, err);
+    // one instantiation per algorithm: the PPO kernel drops the V-trace state (56 -> fewer
+    // registers, more resident segments per SM for the HBM stream)
+    if (algo == kAlgoPpo)
+      returns_vec_kernel<kAlgoPpo><<<ceil_div(b.S, per), 256, 0, s>>>(b, hp, tlogp, adv, target,
+                                                                    seg_partial, err);
+    else
+      returns_vec_kernel<kAlgoVtrace><<<ceil_div(b.S, per), 256, 0, s>>>(b, hp, tlogp, adv,
+                                                                       target, seg_partial, err);
   } else {
     per = kRetSegsPerBlock;
     returns_kernel<<<ceil_div(b.S, per), 32 * per, 0, s>>>(b, algo, hp, tlogp, adv, target,
