@@ -8,6 +8,6 @@ L=paper_2011_12895_b200/_lib
 for v in ${VARIANTS:-cur}; do
   if [ "$v" = cur ]; then cp /tmp/libtlg_b200.cur.so $L/libtlg_b200.so; else cp $L/variants/lib_$v.so $L/libtlg_b200.so; fi
   timeout 300 python tools/hbm_sweep.py --out gpurun_out/sweep_$v.json > gpurun_out/sweep_$v.log 2>&1
-  timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:returns --csv --log-file gpurun_out/ncu_k1_$v.csv python tools/hbm_sweep.py --profile-returns 1048576 > gpurun_out/ncu_k1_$v.log 2>&1
+  timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:${KREGEX:-returns} --csv --log-file gpurun_out/ncu_k1_$v.csv python tools/hbm_sweep.py ${PROFILE_ARGS:---profile-returns 1048576} > gpurun_out/ncu_k1_$v.log 2>&1
 done
 cp /tmp/libtlg_b200.cur.so $L/libtlg_b200.so
