@@ -87,7 +87,7 @@ struct Learner::Gpu {
   std::unordered_set<std::uint32_t> pinned;
   Pinned<float> one_obs, one_f;
   Pinned<std::int32_t> one_i;
-  Pinned<std::uint8_t> one_b;
+  Pinned<std::uint8_t> one_b, one_d;
 
   void ResetRing(std::size_t capacity) {
     if (ring) tlg_replay_destroy(ring);
@@ -105,21 +105,70 @@ struct Learner::Gpu {
     if (pinned.count(slot)) deferred.push_back(slot);
     else free_slots.push_back(slot);
   }
+  // Undo log of a group of admissions: the mirror changes only when ReplayMem::Push
+  // really happens, so a push that fails after Admit (a bad segment, a failed copy) is
+  // rolled back before the error reaches the caller.
+  struct Undo {
+    std::vector<std::pair<std::uint64_t, Live>> evicted;  // in eviction order
+    std::vector<std::uint32_t> taken;                      // slots handed out
+    std::uint64_t first_id = 0;                            // ids >= this were added
+  };
+  Undo BeginAdmit() const {
+    Undo u;
+    u.first_id = next_id;
+    return u;
+  }
   // mirrors ReplayMem::Push (replay_mem.cpp:14-20) before the stripped copy is pushed
-  std::uint32_t Admit(std::size_t capacity) {
+  std::uint32_t Admit(std::size_t capacity, Undo& u) {
     if (live.size() == capacity) {
       while (!fifo.empty() && !live.count(fifo.front())) fifo.pop_front();
-      Release(live.at(fifo.front()).slot);
-      live.erase(fifo.front());
+      const std::uint64_t id = fifo.front();
+      const Live e = live.at(id);
+      u.evicted.emplace_back(id, e);
+      Release(e.slot);
+      live.erase(id);
       fifo.pop_front();
     }
     if (free_slots.empty()) throw std::runtime_error("device replay ring exhausted");
     const std::uint32_t slot = free_slots.back();
     free_slots.pop_back();
+    u.taken.push_back(slot);
     return slot;
   }
-  // one segment -> SoA (the same packing as Pack) -> its HBM slot
-  void Put(const TrajectorySegment& seg, std::uint32_t slot) {
+  // Register an admitted segment under a fresh id (after its slot holds the data).
+  std::uint64_t Enter(std::uint32_t slot) {
+    live.emplace(next_id, Live{slot, 0});
+    fifo.push_back(next_id);
+    return next_id++;
+  }
+  static void Unfree(std::vector<std::uint32_t>& v, std::uint32_t slot) {
+    for (std::size_t i = v.size(); i-- > 0;)
+      if (v[i] == slot) {
+        v.erase(v.begin() + std::ptrdiff_t(i));
+        return;
+      }
+  }
+  // Restore the mirror to its state before BeginAdmit.
+  void Rollback(Undo& u) {
+    while (next_id > u.first_id) {
+      --next_id;
+      live.erase(next_id);
+      if (!fifo.empty() && fifo.back() == next_id) fifo.pop_back();
+    }
+    for (std::size_t i = u.taken.size(); i-- > 0;) free_slots.push_back(u.taken[i]);
+    for (std::size_t i = u.evicted.size(); i-- > 0;) {
+      const auto& [id, e] = u.evicted[i];
+      Unfree(free_slots, e.slot);
+      Unfree(deferred, e.slot);
+      live.emplace(id, e);
+      fifo.push_front(id);
+    }
+    u = Undo{};
+  }
+  // one segment -> SoA in the pinned single-segment buffers (the same packing as Pack);
+  // validates the segment, so it runs before any admission.  Commit copies it to a slot.
+  tlg_segment_batch one{};
+  void Prepare(const TrajectorySegment& seg) {
     const std::size_t D = shape.obs_dim, rowb = (D + 7) / 8;
     const bool bitsfmt = ring_dtype == TLG_OBS_BITS;
     if (bitsfmt) {
@@ -136,10 +185,10 @@ struct Learner::Gpu {
     float* va = bl + T;
     float* bo = va + T;
     std::uint8_t* dn = bitsfmt ? one_b.p + std::size_t(T) * rowb : nullptr;
-    std::vector<std::uint8_t> done_host;
-    if (!bitsfmt) {
-      done_host.assign(T, 0);
-      dn = done_host.data();
+    if (!bitsfmt) {  // kept until Commit: a member buffer, not a local
+      one_d.ensure(T);
+      std::memset(one_d.p, 0, T);
+      dn = one_d.p;
     }
     if (seg.valid_steps > T || seg.valid_steps > seg.steps.size())
       throw std::invalid_argument("segment valid_steps exceeds its steps / unroll_len");
@@ -185,8 +234,9 @@ struct Learner::Gpu {
     b.done = dn;
     b.bootstrap = bo;
     b.valid_steps = one_i.p + T;
-    Check(tlg_replay_put(ring, &slot, &b));
+    one = b;
   }
+  void Commit(std::uint32_t slot) { Check(tlg_replay_put(ring, &slot, &one)); }
 
   ~Gpu() {
     if (ring) tlg_replay_destroy(ring);
@@ -391,22 +441,22 @@ void Learner::PushSegment(const TrajectorySegment& segment) {
     Check(tlg_replay_create(g.h, g.ring_cap, g.ring_dtype, &g.ring));
     g.ring_decided = true;
   }
-  const std::uint32_t slot = g.Admit(config_.replay_capacity);
-  try {
-    g.Put(segment, slot);
-  } catch (...) {
-    g.free_slots.push_back(slot);
-    throw;
-  }
+  g.Prepare(segment);  // throws on a bad segment before the mirror changes
   TrajectorySegment stripped = segment;
   for (SegmentStep& st : stripped.steps) {
     st.obs.clear();
     st.obs.shrink_to_fit();
   }
-  stripped.segment_seq = g.next_id;
-  g.live.emplace(g.next_id, Gpu::Live{slot, 0});
-  g.fifo.push_back(g.next_id++);
-  replay_.Push(std::move(stripped));
+  Gpu::Undo undo = g.BeginAdmit();
+  try {
+    const std::uint32_t slot = g.Admit(config_.replay_capacity, undo);
+    g.Commit(slot);
+    stripped.segment_seq = g.Enter(slot);
+    replay_.Push(std::move(stripped));
+  } catch (...) {
+    g.Rollback(undo);
+    throw;
+  }
   g.cv.notify_all();
 }
 
@@ -473,26 +523,31 @@ void Learner::PushSegmentBatch(const std::string& model_key, const tlg_segment_b
   }
   if (b.obs_dtype != g.ring_dtype)
     throw std::invalid_argument("PushSegmentBatch: observation format differs from the period's");
-  // admit in order (mirrors n ReplayMem::Push evictions), one device copy, then the
-  // observation-less entries in the same order
-  std::vector<std::uint32_t> slots(b.n_segments);
-  std::vector<std::uint64_t> ids(b.n_segments);
+  if (b.obs_dtype == TLG_OBS_BITS && b.obs_pitch != 0 &&
+      (b.obs_pitch < (b.obs_dim + 7) / 8 || b.obs_pitch > ((b.obs_dim + 7) / 8 + 15) / 16 * 16))
+    throw std::invalid_argument("PushSegmentBatch: bad obs_pitch");
+  // observation-less entries first (nothing below can fail on the caller's data)
+  std::vector<TrajectorySegment> stripped(b.n_segments);
   for (std::uint32_t i = 0; i < b.n_segments; ++i) {
-    slots[i] = g.Admit(config_.replay_capacity);
-    ids[i] = g.next_id;
-    g.live.emplace(g.next_id, Gpu::Live{slots[i], 0});
-    g.fifo.push_back(g.next_id++);
-  }
-  Check(tlg_replay_put(g.ring, slots.data(), &b));
-  for (std::uint32_t i = 0; i < b.n_segments; ++i) {
-    TrajectorySegment stripped = SegmentFromSoa(b, i, model_key);
-    for (SegmentStep& st : stripped.steps) {
+    stripped[i] = SegmentFromSoa(b, i, model_key);
+    for (SegmentStep& st : stripped[i].steps) {
       st.obs.clear();
       st.obs.shrink_to_fit();
     }
-    stripped.segment_seq = ids[i];
-    replay_.Push(std::move(stripped));
   }
+  // admit in order (mirrors n ReplayMem::Push evictions), one device copy, then the
+  // entries in the same order; any failure restores the mirror
+  std::vector<std::uint32_t> slots(b.n_segments);
+  Gpu::Undo undo = g.BeginAdmit();
+  try {
+    for (std::uint32_t i = 0; i < b.n_segments; ++i) slots[i] = g.Admit(config_.replay_capacity, undo);
+    Check(tlg_replay_put(g.ring, slots.data(), &b));
+    for (std::uint32_t i = 0; i < b.n_segments; ++i) stripped[i].segment_seq = g.Enter(slots[i]);
+  } catch (...) {
+    g.Rollback(undo);
+    throw;
+  }
+  for (std::uint32_t i = 0; i < b.n_segments; ++i) replay_.Push(std::move(stripped[i]));
   g.cv.notify_all();
 }
 

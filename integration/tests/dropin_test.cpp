@@ -621,6 +621,46 @@ TEST(bulk_soa_ingest_matches_per_segment_pushes) {
   }
 }
 
+TEST(a_rejected_push_leaves_the_device_replay_mirror_in_step) {
+  // A push that fails (a non-binary observation in a bit-packed period, a bad obs_pitch)
+  // must leave the HBM slot map exactly in step with the reference ReplayMem, which never
+  // saw the segment: later draws and parameters equal a host-replay learner's that was
+  // never offered the bad pushes.
+  HyperParams hyper = TestHyper();
+  Rig rig_a(hyper), rig_b(hyper);
+  learner::LearnerConfig cfg;
+  cfg.num_shards = 2;
+  cfg.publish_interval = 1;
+  cfg.seed = 3;
+  cfg.replay_capacity = 12;
+  learner::LearnerConfig cfg_dev = cfg;
+  cfg_dev.device_replay = true;
+  learner::Learner host(cfg, rig_a.league, rig_a.pool);
+  learner::Learner dev(cfg_dev, rig_b.league, rig_b.pool);
+  std::mt19937_64 feed_a(31), feed_b(31), junk(5);
+  std::uint64_t seq = 0;
+  for (int step = 0; step < 8; ++step) {
+    for (int i = 0; i < 10; ++i, ++seq) {  // the ring is full from step 1 on: pushes evict
+      host.PushSegment(MakeSegment(host.current_key(), feed_a, seq));
+      dev.PushSegment(MakeSegment(dev.current_key(), feed_b, seq));
+      if (i % 4 == 1) {
+        TrajectorySegment bad = MakeSegment(dev.current_key(), junk, 0);
+        bad.steps[1].obs = {0.5};  // not a 0/1 plane: rejected in a bit-packed period
+        CHECK_THROWS_AS(dev.PushSegment(bad), std::invalid_argument);
+        std::vector<TrajectorySegment> grp{MakeSegment(dev.current_key(), junk, 0)};
+        auto soa = ToSoa(grp, hyper.unroll_len, 1, true);
+        soa->c.obs_pitch = 64;  // wider than a 16-B padded row
+        CHECK_THROWS_AS(dev.PushSegmentBatch(dev.current_key(), soa->c), std::invalid_argument);
+      }
+    }
+    CHECK(host.replay().size() == dev.replay().size());
+    CHECK(host.TrainStep());
+    CHECK(dev.TrainStep());
+    CHECK(host.params().values == dev.params().values);
+    CHECK(host.replay().consumed_steps() == dev.replay().consumed_steps());
+  }
+}
+
 TEST(reference_run_bench_runs_on_the_b200_learner) {
   // run::RunBench (bench.cpp:60-162) builds learner::Learner -- here the B200 drop-in --
   // next to the reference's own actors, league and pool.

@@ -172,7 +172,10 @@ struct tlg_learner {
   int8_t* dzq = nullptr;
   unsigned* colmax = nullptr;
   static constexpr int kMaxI8Splits = 148;
-  bool wq_fresh = false;
+  // parameter plane the int8 pieces in wq were quantized from during this step (the
+  // student's or the teacher's); null = stale.  Shards alternate teacher and student
+  // forwards, so the pieces are rebuilt whenever the plane differs.
+  const float* wq_src = nullptr;
   // layer 2 on int8 x int8 (tanh activations as pieces, W_2 as row pieces).  Opt-in
   // (TLG_I8X2=1): measured at C3 its forward is L2->SM-bound at 64-column tiles and the
   // extra piece plane costs layer 1 more than layer 2 saves (profiles/r01_ncu_i8x2.md)
@@ -564,11 +567,11 @@ struct tlg_learner {
         p.out_hi = dz[l];
         p.out_lo = dz_lo[l];
       }
-      if (l == 0 && sg.x0_bits != nullptr && !wq_fresh) {
-        // this step's layer-1 weights -> int8 pieces (once per step)
+      if (l == 0 && sg.x0_bits != nullptr && wq_src != P) {
+        // this step's layer-1 weights of plane P -> int8 pieces (once per step and plane)
         tlg::gemm::launch_quantize_rows(P + net.w_off[0], outw, in, in, wq, wq_kp, wq_scale,
                                         stream);
-        wq_fresh = true;
+        wq_src = P;
         ++launches;
       }
       if (timed) kmark(0, int(l), 0);
@@ -715,7 +718,6 @@ struct tlg_learner {
     if (teacher_active()) {
       // the teacher's head outputs first (the student's forward then reuses the buffers)
       forward_heads(sg, teacher, teacher_lo, x0, x0_lo, t_head_out, nullptr, false);
-      wq_fresh = false;  // layer-1 int8 pieces must be rebuilt from the student's weights
     }
     const bool parts = loss_reads_parts();
     tlg::HyperDev hd{float(hp.gamma), float(hp.lam), float(hp.clip_eps), float(hp.vf_coef),
@@ -864,8 +866,9 @@ struct tlg_learner {
       const long key = long(sg.bd.S) * 8 + (sg.x0_u8 ? 1 : 0) + (sg.exact ? 2 : 0) +
                        (sg.x0_bits ? 4 : 0);
       Graph& gr = graphs[bind];
+      const bool slot_bind = bind == 1 || bind == 2;  // staging slots (3.. = external)
       if (!gr.exec || key != gr.key || gr.hyper != hyper_version ||
-          (bind && gr.obs != slots[bind - 1].obs)) {
+          (slot_bind && gr.obs != slots[bind - 1].obs)) {
         if (gr.exec) cudaGraphExecDestroy(gr.exec);
         gr.exec = nullptr;
         cudaGraph_t g;
@@ -877,16 +880,26 @@ struct tlg_learner {
         gr.key = key;
         gr.hyper = hyper_version;
         gr.launches = launches;
-        gr.obs = bind ? slots[bind - 1].obs : nullptr;
+        gr.obs = slot_bind ? slots[bind - 1].obs : nullptr;
       }
       TLG_CUDA(cudaGraphLaunch(gr.exec, stream));
       launches = gr.launches;
+      S_last = sg.bd.S;  // host code of the captured step ran only at capture
     } else {
       enqueue_device_step(nullptr, n, bs, on_device);
     }
     if (consumed) TLG_CUDA(cudaEventRecord(consumed, stream));
-    // host-side staging of the next batch while this step runs on the device
-    if (stage_next) stage_async(*stage_next);
+    // host-side staging of the next batch while this step runs on the device; the step
+    // has already been launched, so its results are checked before a staging error is
+    // reported (the parameters have moved: the caller must see the step's own outcome)
+    if (stage_next) {
+      try {
+        stage_async(*stage_next);
+      } catch (...) {
+        finish(n, out);
+        throw;
+      }
+    }
     finish(n, out);
   }
 
@@ -905,9 +918,19 @@ struct tlg_learner {
   int slot_next = 0, slot_count = 0, slot_head = 0;
   cudaStream_t copy_stream = nullptr;
 
+  // everything stage() would reject, checked before any copy is queued (the copy sizes
+  // derive from obs_dim / obs_dtype / obs_pitch, so a mismatch would over-read the host)
   void check_stage(const tlg_segment_batch& b) const {
     if (int(b.n_segments) > S_max || b.n_segments == 0) throw InvalidArg("bad batch size");
     if (int(b.unroll_len) != T) throw InvalidArg("unroll_len mismatch");
+    if (b.obs_dim != net.D) throw InvalidArg("observation size does not match policy shape");
+    if (b.obs_dtype != TLG_OBS_F32 && b.obs_dtype != TLG_OBS_U8 && b.obs_dtype != TLG_OBS_BITS)
+      throw InvalidArg("unknown obs dtype");
+    if (b.obs_dtype != TLG_OBS_F32 && obs_u8 == nullptr)
+      throw InvalidArg("learner not configured for uint8 / bit-packed observations");
+    if (b.obs_dtype == TLG_OBS_BITS && b.obs_pitch != 0 &&
+        long(b.obs_pitch) != (long(net.D) + 7) / 8 && long(b.obs_pitch) != bits_pitch)
+      throw InvalidArg("obs_pitch must be 0, ceil(obs_dim/8) or that rounded up to 16 bytes");
   }
 
   void stage_async(const tlg_segment_batch& b) {
@@ -976,7 +999,7 @@ struct tlg_learner {
   void enqueue_device_step(const Staged* staged, int n, const tlg_segment_batch* bs = nullptr,
                            int on_device = 0) {
     launches = 0;
-    wq_fresh = false;
+    wq_src = nullptr;  // the parameters changed since the last step
     mark(0);
     TLG_CUDA(cudaMemsetAsync(err, 0, 16, stream));
     TLG_CUDA(cudaMemsetAsync(grad + P_pad, 0, 16, stream));

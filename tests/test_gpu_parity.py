@@ -624,6 +624,48 @@ def test_teacher_kl_term_matches_oracle(tlg, oracle, case):
     assert np.max(np.abs(lrn.get_grad() - og)) > 1e-3 * gscale
 
 
+def test_teacher_kl_two_local_shards_of_bit_planes(tlg, oracle):
+    """The teacher's and the student's layer-1 weights take turns in the int8 pieces
+    buffer: with two local shards of bit-packed planes, shard 1's teacher forward must
+    re-quantize the teacher's W1 (not reuse the student's pieces left by shard 0)."""
+    from paper_2011_12895_b200._capi import SegmentBatchView
+    S, T, A, D, hidden = 12, 8, 6, 200, (64, 32)
+    shape = Shape(2, D, A, hidden)
+    hp = dict(learning_rate=0.05, batch_size=S, unroll_len=T, kl_teacher_coef=0.7,
+              ent_coef=0.02)
+    lrn = tlg.Learner("mlp", D, A, hidden, optimizer="sgd", max_segments=S, unroll_len=T,
+                      obs_u8=True)
+    lrn.set_hyper(**hp)
+    p = init_params(oracle, shape, seed=41)
+    teacher = init_params(oracle, shape, seed=42)
+    lrn.set_params(p)
+    lrn.set_teacher(teacher)
+    raw, views = [], []
+    for k in range(2):
+        b = tlg.synth.make_segments(S, T, D, A, seed=300 + k, obs_kind="binary", obs_u8=True)
+        pb = b.slice(0, S)
+        pb.obs = tlg.synth.pack_bits(b.obs)
+        raw.append(b)
+        views.append(SegmentBatchView(pb, bits=True, obs_dim=D))
+    sts = lrn.train_step_shards(views)
+    g = lrn.get_grad()
+    ohp = OHyper(**hp)
+    want = np.zeros_like(p)
+    for b, st in zip(raw, sts):
+        adv, tgt = oracle.shard_returns(shape, p, ohp, ALGO["ppo"], to_oracle(b))
+        sel = [(s, t) for s in range(S) for t in range(int(b.valid_steps[s]))]
+        obs = np.stack([np.asarray(b.obs[s, t], np.float64) for s, t in sel])
+        ost, og = oracle.ppo_loss_grad(
+            shape, p, obs, np.array([b.action[s, t] for s, t in sel]),
+            np.array([b.behavior_logp[s, t] for s, t in sel], np.float64),
+            np.array([adv[s, t] for s, t in sel]), np.array([tgt[s, t] for s, t in sel]), ohp,
+            teacher=teacher)
+        assert close(st["loss"], ost["loss"], 1e-4), (st["loss"], ost["loss"])
+        want += og / 2
+    gscale = max(1e-30, float(np.max(np.abs(want))))
+    assert np.max(np.abs(g - want)) <= 1e-4 * gscale, np.max(np.abs(g - want)) / gscale
+
+
 @pytest.mark.parametrize("fmt", ["f32", "bits"])
 def test_device_replay_matches_host_batches(tlg, oracle, fmt):
     """Segments ingested once into the device replay ring and gathered by slot give
