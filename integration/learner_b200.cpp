@@ -540,9 +540,12 @@ void Learner::PushSegmentBatch(const std::string& model_key, const tlg_segment_b
   std::vector<std::uint32_t> slots(b.n_segments);
   Gpu::Undo undo = g.BeginAdmit();
   try {
-    for (std::uint32_t i = 0; i < b.n_segments; ++i) slots[i] = g.Admit(config_.replay_capacity, undo);
+    // each admission sees the previous ones (the FIFO evicts as n single pushes would)
+    for (std::uint32_t i = 0; i < b.n_segments; ++i) {
+      slots[i] = g.Admit(config_.replay_capacity, undo);
+      stripped[i].segment_seq = g.Enter(slots[i]);
+    }
     Check(tlg_replay_put(g.ring, slots.data(), &b));
-    for (std::uint32_t i = 0; i < b.n_segments; ++i) stripped[i].segment_seq = g.Enter(slots[i]);
   } catch (...) {
     g.Rollback(undo);
     throw;

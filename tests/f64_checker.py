@@ -164,7 +164,7 @@ def returns(algo, hp, reward, value, done, boot, valid, blogp=None, tlogp=None):
 def shard_step(net: Net, p, hp, algo, b, dev, chunk=1 << 15):
     """One shard: BuildMinibatch + loss/grad (learner.cpp:117-128).  b is a synth
     SegmentBatch (fp32-representable arrays; obs may be uint8 planes).  Returns
-    (stats dict, grad [P] f64 tensor, adv [S,T], target [S,T])."""
+    (stats dict, grad [P] f64 tensor, adv [S,T], target [S,T], target logp [S,T] | None)."""
     S, T = b.action.shape
     D = net.d
     obs = _t(np.asarray(b.obs).reshape(S * T, D), dev)
@@ -240,22 +240,22 @@ def shard_step(net: Net, p, hp, algo, b, dev, chunk=1 << 15):
         del acts, z
     st["clip_fraction"] = clip * inv_n if algo != 1 else 0.0
     st["n_samples"] = n
-    return st, grad, adv, tgt
+    return st, grad, adv, tgt, tlogp
 
 
 def learner_step(net: Net, p, hp, algo, shards, dev):
-    """Rank-ordered shard mean (learner.cpp:138-149): (stats list, avg grad, adv/tgt of
-    the last shard)."""
+    """Rank-ordered shard mean (learner.cpp:138-149): (stats list, avg grad,
+    (adv, target, target logp) of the last shard)."""
     avg = torch.zeros(net.P, dtype=F64, device=dev)
     stats = []
     ret = None
     for b in shards:
-        st, g, adv, tgt = shard_step(net, p, hp, algo, b, dev)
+        st, g, adv, tgt, tl = shard_step(net, p, hp, algo, b, dev)
         if not np.isfinite(st["loss"]):
             raise RuntimeError("non-finite loss")
         avg += g
         stats.append(st)
-        ret = (adv, tgt)
+        ret = (adv, tgt, tl)
     avg *= 1.0 / len(shards)
     return stats, avg, ret
 

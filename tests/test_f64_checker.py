@@ -48,7 +48,7 @@ def test_checker_matches_oracle(oracle, algo, case):
     shards[1].obs[3] = 0; shards[1].done[3] = 0; shards[1].action[3] = 0
     dev = torch.device("cpu")
     pt = torch.tensor(p, dtype=torch.float64)
-    stats, g, (adv, tgt) = fc.learner_step(net, pt, hpd, ALGO[algo], shards, dev)
+    stats, g, (adv, tgt, _) = fc.learner_step(net, pt, hpd, ALGO[algo], shards, dev)
     p_new, g_want, st_want, _ = oracle.learner_step(shape, p, Hyper(**hpd), ALGO[algo],
                                                     [_segments(b) for b in shards])
     assert rel(g.numpy(), g_want) < 1e-10
