@@ -4,11 +4,13 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
 
 Workload (BASELINE.json): config C3 -- Pommerman-shaped obs (11x11x16 = 1936 binary
-planes), MLP 1936-256-256-(6,1), PPO + GAE, T=32, B=4096 segments per learner shard
-(HyperParams::batch_size is per shard, learner.cpp:108), Adam.  One step = one
-Learner::TrainStep on every rank: returns, loss fwd/bwd, NCCL gradient allreduce,
-optimizer.  N>1 is launched by torchrun, one rank per GPU (weak scaling: per-GPU
-work fixed).
+planes), MLP 1936-256-256-(6,1), PPO + GAE, T=32, a draw of B=4096 segments, Adam.  One
+step = one Learner::TrainStep on every rank: returns, loss fwd/bwd, NCCL gradient
+allreduce (per-layer buckets overlapped with the backward), optimizer.  N>1 is launched
+by torchrun, one rank per GPU.  --scaling strong (default): the 4096-
+segment draw is split over the G ranks (4096/G segments = HyperParams::batch_size per
+shard, learner.cpp:108,119-125); at N>1 the weak-scaling figure (4096 segments per GPU)
+is measured in the same run and reported beside it.
 
 * value   : frames/s with the batch already resident in HBM (whole job, all ranks),
             timed with CUDA events on the learner's stream, max over ranks.
@@ -98,7 +100,39 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-def reference_cpu(cfg, seconds=12.0, steps=None, warmup=0, segs_per_shard=None):
+def oracle_mlp_cpu(cfg, segments=64, reps=2):
+    """The same model on the CPU: the fp64 oracle's learner step (oracle/tlg_oracle.cpp --
+    the reference's rlmath/policy arithmetic extended to the MLP family, std::thread over
+    16 fixed sample chunks) on a `segments` x T slice of the config (>= 2048 frames).
+    A port, not the reference (which has no MLP family, types.hpp:14)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_ffi import Hyper, Oracle, Segments, Shape
+    from paper_2011_12895_b200.synth import make_segments
+    orc = Oracle()
+    T, D, A = cfg.unroll_len, cfg.obs_dim, cfg.n_actions
+    shape = Shape(2, D, A, cfg.hidden)
+    p = orc.init_params(shape, 0.05, 3)
+    hp = Hyper(learning_rate=3e-4, batch_size=segments, unroll_len=T)
+    algo = {"ppo": 0, "vtrace": 1, "ppo_vtrace": 2}[cfg.algo]
+    b = make_segments(segments, T, D, A, seed=77, obs_kind=cfg.obs_kind)
+    seg = Segments(b.obs.astype(np.float64), b.action.astype(np.uint32),
+                   b.reward.astype(np.float64), b.behavior_logp.astype(np.float64),
+                   b.value_est.astype(np.float64), b.done, b.bootstrap.astype(np.float64),
+                   b.valid_steps.astype(np.uint32))
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        orc.learner_step(shape, p, hp, algo, [seg])
+        ts.append(time.perf_counter() - t0)
+    frames = int(b.valid_steps.sum())
+    return {"value": frames / min(ts), "unit": "frames/s",
+            "cores": min(16, os.cpu_count() or 1), "kind": "port",
+            "sample": f"fp64 oracle learner step (same MLP {D}-{'-'.join(map(str, cfg.hidden))}"
+                      f"-({A},1), {cfg.algo}) on {segments} segments x T={T} = {frames} "
+                      f"frames, best of {reps}"}
+
+
+def reference_cpu(cfg, seconds=12.0, steps=None, warmup=0, segs_per_shard=None, shards=None):
     """The reference's own Learner::TrainStep (linear_softmax: the only policy family the
     reference has, types.hpp:14) at the config's obs/A/T, num_shards = host cores, on a
     bounded sample (segs_per_shard segments per shard per step)."""
@@ -106,7 +140,7 @@ def reference_cpu(cfg, seconds=12.0, steps=None, warmup=0, segs_per_shard=None):
     from oracle_ffi import Hyper, RefLearner, RefLib, Segments
     from paper_2011_12895_b200.synth import make_segments
     ref = RefLib()
-    cores = os.cpu_count() or 1
+    cores = shards or os.cpu_count() or 1
     T, D, A = cfg.unroll_len, cfg.obs_dim, cfg.n_actions
     if segs_per_shard is None:
         # keep one step's fp64 AoS segments around ~64 MB
@@ -199,6 +233,8 @@ def main():
     ap.add_argument("--obs", default="bits", choices=["bits", "u8", "f32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-infer", action="store_true")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: the config's B segments split over the ranks; weak: B per rank")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -218,34 +254,50 @@ def main():
 
     obs_u8 = args.obs in ("u8", "bits") and cfg.obs_kind == "binary"
     obs_bits = obs_u8 and args.obs == "bits"
-    S, T, D, A, hidden = cfg.batch_size, cfg.unroll_len, cfg.obs_dim, cfg.n_actions, cfg.hidden
-    lrn = tlg.Learner("mlp", D, A, hidden, algo=cfg.algo, optimizer=cfg.optimizer,
-                      max_segments=S, unroll_len=T, device=local, obs_u8=obs_u8, timing=False)
-    lrn.set_hyper(learning_rate=3e-4, batch_size=S, unroll_len=T)
-    params = tlg.synth.init_params_f32(lrn.n_params, 0.05, seed=cfg.seed).astype(np.float64)
-    lrn.set_params(params)
-    if world > 1:
-        uid = [tlg.comm_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        lrn.comm_init(uid[0], world, rank)
+    T, D, A, hidden = cfg.unroll_len, cfg.obs_dim, cfg.n_actions, cfg.hidden
+    if args.scaling == "strong" and cfg.batch_size % world:
+        raise SystemExit(f"{cfg.batch_size} segments do not split over {world} ranks")
+    S = cfg.batch_size // world if args.scaling == "strong" else cfg.batch_size
+
+    def make_learner(S_):
+        l_ = tlg.Learner("mlp", D, A, hidden, algo=cfg.algo, optimizer=cfg.optimizer,
+                         max_segments=S_, unroll_len=T, device=local, obs_u8=obs_u8,
+                         timing=False)
+        l_.set_hyper(learning_rate=3e-4, batch_size=S_, unroll_len=T)
+        l_.set_params(tlg.synth.init_params_f32(l_.n_params, 0.05,
+                                                seed=cfg.seed).astype(np.float64))
+        if world > 1:
+            uid = [tlg.comm_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            l_.comm_init(uid[0], world, rank)
+        return l_
+    lrn = make_learner(S)
 
     # distinct resident batches per rank, cycled so the inputs exceed L2 (126 MB): two
-    # u8/f32 batches (obs >= 254 MB each) or four bit-packed ones (34 MB each)
-    nb = 4 if obs_bits else 2
-    host = [tlg.synth.make_segments(S, T, D, A, seed=cfg.seed * 100 + rank * 10 + i,
-                                    obs_kind=cfg.obs_kind, obs_u8=obs_u8) for i in range(nb)]
-    if obs_bits:
-        packed = []
-        for h in host:
-            hb = h.slice(0, h.n_segments)
-            hb.obs = tlg.synth.pack_bits(h.obs)
-            packed.append(hb)
-        # rows padded to 16-byte multiples in HBM: they feed the int8 GEMM's TMA directly
-        pitch = ((D + 7) // 8 + 15) // 16 * 16
-        dev = [tlg.DeviceSegmentBatch(h, local, bits=True, obs_dim=D, pitch=pitch)
-               for h in packed]
-    else:
-        dev = [tlg.DeviceSegmentBatch(h, local) for h in host]
+    # u8/f32 batches (obs >= 254 MB each) or four bit-packed ones (34 MB each at S=4096;
+    # more batches at smaller per-rank shards, >= 136 MB resident per rank)
+    def make_batches(S_):
+        per = S_ * T * ((((D + 7) // 8 + 15) // 16 * 16 if obs_bits else
+                         D * (1 if obs_u8 else 4)) + 17)  # + action/reward/blogp/value/done
+        nb_ = max(4 if obs_bits else 2, -(-136_000_000 // per)) if obs_bits else 2
+        host_ = [tlg.synth.make_segments(S_, T, D, A, seed=cfg.seed * 100 + rank * 10 + i,
+                                         obs_kind=cfg.obs_kind, obs_u8=obs_u8)
+                 for i in range(nb_)]
+        if obs_bits:
+            packed = []
+            for h in host_:
+                hb = h.slice(0, h.n_segments)
+                hb.obs = tlg.synth.pack_bits(h.obs)
+                packed.append(hb)
+            # rows padded to 16-byte multiples in HBM: they feed the int8 GEMM's TMA directly
+            pitch = ((D + 7) // 8 + 15) // 16 * 16
+            dev_ = [tlg.DeviceSegmentBatch(h, local, bits=True, obs_dim=D, pitch=pitch)
+                    for h in packed]
+        else:
+            dev_ = [tlg.DeviceSegmentBatch(h, local) for h in host_]
+        return host_, dev_
+    host, dev = make_batches(S)
+    nb = len(dev)
     frames_per_step = [int(h.valid_steps.sum()) for h in host]
     resident_bytes = sum(sum(t.numel() * t.element_size() for t in d.t.values()) for d in dev)
 
@@ -294,6 +346,33 @@ def main():
     frames_all = sum_over_ranks(frames)
     value = frames_all / (ms_total / 1e3)
     ms_per_step = ms_total / args.steps
+
+    # ---- at N>1 under strong scaling: the weak-scaling figure (the config's B per rank)
+    weak = None
+    if world > 1 and args.scaling == "strong":
+        lw = make_learner(cfg.batch_size)
+        hw, dw = make_batches(cfg.batch_size)
+        fw = [int(h.valid_steps.sum()) for h in hw]
+        for i in range(max(args.warmup, 2 * len(dw))):
+            lw.train_step(dw[i % len(dw)], on_device=True)
+        sw = torch.cuda.ExternalStream(lw.stream(), device=local)
+        barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(sw)
+        frw = 0
+        for i in range(args.steps):
+            lw.train_step(dw[i % len(dw)], on_device=True)
+            frw += fw[i % len(dw)]
+        e1.record(sw)
+        torch.cuda.synchronize()
+        msw = max_over_ranks(e0.elapsed_time(e1))
+        weak = {"value": sum_over_ranks(frw) / (msw / 1e3), "unit": "frames/s",
+                "segments_per_gpu": cfg.batch_size, "ms_per_step": msw / args.steps}
+        lw.close()
+        del dw, hw
+        torch.cuda.empty_cache()
 
     # ---- per-kernel CUDA-event times from separate instrumented (eager) steps
     lrn.set_timing(True)
@@ -427,7 +506,9 @@ def main():
     flops_fwd1 = gflops[("fwd", 0)]
     t_fwd1 = gms[("fwd", 0)] / 1e3
     t_dw1 = gms[("dw", 0)] / 1e3
-    peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+    # burst peak: the kernel is timed over a handful of instrumented steps, not a
+    # seconds-long run (the sustained figure is reported beside it)
+    peak = peaks.get("bf16_tflops", peaks.get("bf16_tflops_sustained"))
     ph = np.mean(np.array(kern["phases"]), axis=0)
     step_ms = float(ph[6])
     # the dominant kernel of the step: the trunk GEMM with the longest CUDA-event time
@@ -463,7 +544,8 @@ def main():
         "algorithmic_bytes_per_launch": bytes_dom,
         "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
         "frac": achieved / peak, "traffic": _ncu_traffic(dom),
-        "peak_source": f"{peak_src} bf16_tflops_sustained (MEASURED_PEAKS.json)",
+        "peak_source": f"{peak_src} bf16_tflops (burst, MEASURED_PEAKS.json)",
+        "frac_of_sustained": achieved / peaks.get("bf16_tflops_sustained", peak),
         "algorithmic_flops_per_launch": gflops[dom_g],
         "ms_per_launch": t_dom * 1e3,
         "share_of_step": t_dom * 1e3 / step_ms,
@@ -540,16 +622,31 @@ def main():
         except Exception as e:
             cpu = {"value": None, "unit": "frames/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {type(e).__name__}: {e}"}
+        # the reference learner at num_shards = 1 too, and the same MLP on the
+        # CPU (the fp64 oracle port; the reference cannot run an MLP)
+        others = []
+        try:
+            fps1, c1, sample1, _ = reference_cpu(cfg, seconds=5.0, shards=1)
+            others.append({"value": fps1, "unit": "frames/s", "cores": c1, "kind": "reference",
+                           "sample": sample1})
+        except Exception as e:
+            others.append({"value": None, "kind": "reference", "sample": f"unavailable: {e}"})
+        try:
+            others.append(oracle_mlp_cpu(cfg))
+        except Exception as e:
+            others.append({"value": None, "kind": "port", "sample": f"unavailable: {e}"})
+        cpu["others"] = others
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
             "config": {"workload": cfg.name, "note": cfg.note, "algo": cfg.algo,
                        "optimizer": cfg.optimizer, "obs_dim": D, "hidden": list(hidden),
                        "n_actions": A, "unroll_len": T, "segments_per_gpu": S,
+                       "global_batch_segments": S * world,
                        "frames_per_gpu_step": F,
                        "obs_format": ("bit-packed binary planes (rows padded to 16 B in HBM)"
                                       if obs_bits else "u8 planes" if obs_u8 else "f32"),
@@ -564,6 +661,7 @@ def main():
                     "note": "pinned host SoA batch H2D each step (same obs format as value; "
                             "bit rows padded to 16 B), pipelined one step ahead on a copy "
                             "stream; stats D2H each step"},
+            "weak_scaling": weak,
             "e2e_alt_format": e2e_alt,
             "e2e_dense_rows": e2e_unpitched,
             "device_replay": replay,

@@ -150,6 +150,15 @@ int tlg_learner_set_hyper(tlg_learner* l, const tlg_hyper* hp);
  * tlg_comm_unique_id on rank 0, distributed by the caller. */
 int tlg_comm_unique_id(uint8_t out[128]);
 int tlg_learner_comm_init(tlg_learner* l, const uint8_t unique_id[128], int nranks, int rank);
+/* In-process data parallelism (one host thread per GPU, the reference's shard threads of
+ * learner.cpp:117-134 mapped onto devices): one ncclCommInitAll over n learners created
+ * on n distinct devices; learners[i] becomes rank i.  Steps must then be issued for all
+ * n learners concurrently (one host thread each).  With one local shard per rank, each
+ * layer's gradient bucket is allreduced on a high-priority comm stream as soon as the
+ * backward has produced it, overlapping the layers below; NCCL_ALGO / NCCL_PROTO are
+ * pinned (Ring; LL128,Simple) for run-to-run determinism unless already set or
+ * TLG_NCCL_PIN=0. */
+int tlg_learner_comm_init_all(tlg_learner* const* learners, int n);
 /* One synchronized update over this rank's shard.  `batch` pointers are host
  * memory (copied in on the learner's stream; pinned memory is used as-is) when
  * on_device == 0, else device memory.  The gradient is averaged over the

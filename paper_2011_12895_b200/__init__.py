@@ -10,9 +10,9 @@ the library is missing, importing ``_capi`` users fails loudly.
 from . import configs, synth  # noqa: F401
 from ._capi import (  # noqa: F401
     CudaError, DeviceSegmentBatch, InvalidArgument, Learner, LearnerRuntimeError, Policy,
-    Replay, SegmentBatchView, comm_unique_id, lib,
+    Replay, SegmentBatchView, comm_init_all, comm_unique_id, lib,
 )
 
 __all__ = ["Learner", "Policy", "lib", "configs", "synth", "InvalidArgument",
-           "LearnerRuntimeError", "CudaError", "comm_unique_id", "SegmentBatchView",
+           "LearnerRuntimeError", "CudaError", "comm_unique_id", "comm_init_all", "SegmentBatchView",
            "DeviceSegmentBatch", "Replay"]

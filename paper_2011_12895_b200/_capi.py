@@ -116,6 +116,7 @@ def lib():
                                                     C.c_uint32, C.c_uint32, C.c_void_p]
         L.tlg_comm_unique_id.argtypes = [C.c_void_p]
         L.tlg_learner_comm_init.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int]
+        L.tlg_learner_comm_init_all.argtypes = [C.c_void_p, C.c_int]
         L.tlg_learner_train_step.argtypes = [C.c_void_p, C.POINTER(SegmentBatchC), C.c_int,
                                              C.POINTER(StepStats)]
         L.tlg_learner_train_step_shards.argtypes = [C.c_void_p, C.POINTER(SegmentBatchC), C.c_int,
@@ -164,6 +165,7 @@ EXPORTS = [
     "tlg_learner_set_teacher", "tlg_replay_create", "tlg_replay_destroy", "tlg_replay_put",
     "tlg_learner_train_step_replay",
     "tlg_learner_set_hyper", "tlg_comm_unique_id", "tlg_learner_comm_init",
+    "tlg_learner_comm_init_all",
     "tlg_learner_train_step", "tlg_learner_train_step_shards", "tlg_learner_get_grad",
     "tlg_learner_stage", "tlg_learner_train_staged", "tlg_learner_train_staged_next",
     "tlg_learner_get_returns",
@@ -371,6 +373,12 @@ class Replay:
         check(lib().tlg_learner_train_step_replay(self.learner.h, self.h, sl.ctypes.data,
                                                   n_shards, sl.size // n_shards, sts))
         return [s.as_dict() for s in sts]
+
+
+def comm_init_all(learners):
+    """One ncclCommInitAll over learners on distinct devices (learners[i] = rank i)."""
+    arr = (C.c_void_p * len(learners))(*[l.h.value for l in learners])
+    check(lib().tlg_learner_comm_init_all(arr, len(learners)))
 
 
 def comm_unique_id() -> bytes:

@@ -56,6 +56,16 @@ int Guard(F&& f) {
   }
 }
 
+// Run-to-run determinism of the gradient sum (the reference's determinism contract,
+// docs/architecture.md:83-89): NCCL's per-size algorithm / protocol choice is
+// pinned unless the caller set it (TLG_NCCL_PIN=0 leaves NCCL's tuner alone).
+void pin_nccl() {
+  const char* pin = std::getenv("TLG_NCCL_PIN");
+  if (pin && std::strcmp(pin, "0") == 0) return;
+  setenv("NCCL_ALGO", "Ring", 0);
+  setenv("NCCL_PROTO", "LL128,Simple", 0);
+}
+
 #define NCCL_CHECK(expr)                                                              \
   do {                                                                                \
     ncclResult_t _r = (expr);                                                         \
@@ -214,6 +224,32 @@ struct tlg_learner {
   uint64_t steps_done = 0;
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
+  // ---- gradient buckets (nranks > 1, one local shard per rank): each layer's dW/db
+  // region of the flat gradient is sum-allreduced on comm_stream as soon as the backward
+  // has written it, overlapping the layers below (learner.cpp:138-149).  The
+  // last bucket travels in one NCCL group with the failure guard; the optimizer waits
+  // for comm_done.  TLG_NO_OVERLAP=1: one allreduce after the whole backward instead.
+  cudaStream_t comm_stream = nullptr;
+  static constexpr int kMaxBuckets = 12;
+  cudaEvent_t bucket_ev[kMaxBuckets]{};
+  cudaEvent_t comm_done = nullptr;
+  int n_buckets = 0;
+  bool overlap_active = false;
+  long pend_off = 0, pend_count = 0;
+  const bool overlap_disabled = std::getenv("TLG_NO_OVERLAP") != nullptr;
+  void issue_bucket(long off, long count, bool with_guard);
+  // grad[off, off + count) is final on `stream`: allreduce it now, or (the last bucket of
+  // the step) together with the guard in bucket_flush()
+  void bucket_ready(long off, long count, bool last) {
+    if (!overlap_active) return;
+    if (last) {
+      pend_off = off;
+      pend_count = count;
+    } else {
+      issue_bucket(off, count, false);
+    }
+  }
+  void bucket_flush();
   tlg::StepStatsDev* h_stats = nullptr;
   int* h_flags = nullptr;  // [0] err bits, [1..] guard as float bits
   cudaEvent_t ev[8]{};
@@ -329,6 +365,13 @@ struct tlg_learner {
       if (sl.ready) cudaEventDestroy(sl.ready);
       if (sl.consumed) cudaEventDestroy(sl.consumed);
     }
+    if (comm_stream) {
+      cudaStreamSynchronize(comm_stream);
+      cudaStreamDestroy(comm_stream);
+    }
+    for (auto& e : bucket_ev)
+      if (e) cudaEventDestroy(e);
+    if (comm_done) cudaEventDestroy(comm_done);
     if (comm) tlg::nccl::api().CommDestroy(comm);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
@@ -339,6 +382,14 @@ struct tlg_learner {
     if (h_stats) cudaFreeHost(h_stats);
     if (h_flags) cudaFreeHost(h_flags);
     if (stream) cudaStreamDestroy(stream);
+  }
+
+  void make_comm_stream() {
+    if (comm_stream) return;
+    int lo = 0, hi = 0;
+    TLG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    // highest priority: a bucket's NCCL kernel is scheduled as soon as SMs free up
+    TLG_CUDA(cudaStreamCreateWithPriority(&comm_stream, cudaStreamNonBlocking, hi));
   }
 
   void mark(int i) {
@@ -640,6 +691,7 @@ struct tlg_learner {
           ++launches;
         }
         launches += 3;
+        bucket_ready(net.w_off[0], long(outw) * in + outw, true);
         continue;
       }
       // dW_l = dZ_l^T . X_{l-1}   (K = frames, split-K partials reduced in fixed order)
@@ -666,6 +718,9 @@ struct tlg_learner {
         ++launches;
       }
       launches += 2;
+      // W_l and b_l are contiguous in the flat layout: one bucket, allreduced while the
+      // dX GEMM below (and the layers under it) run
+      bucket_ready(net.w_off[l], long(outw) * in + outw, l == 0);
       if (l > 0) {
         // dZ_{l-1} = (dZ_l . W_l) * (1 - X_{l-1}^2)
         Operand A2{dz[l], dz_lo[l], outw, false};
@@ -757,6 +812,7 @@ struct tlg_learner {
       tlg::LossLaunch ll{fused_ctas, fused_ctas};
       tlg::launch_head_grad_reduce(net.head, hg_partial, loss_partial, ll, gtarget, st, stream,
                                    le.bias_partial);
+      bucket_ready(net.head.wpi, net.P - net.head.wpi, net.L == 0);
       tlg::launch_rows_reduce(col_partial, fused_ctas, net.head.H, net.head.H,
                               gtarget + net.b_off[net.L - 1], stream);
       launches += 5;
@@ -778,6 +834,7 @@ struct tlg_learner {
         loss_partial, col_partial, stream, teacher_active() ? t_head_out : nullptr,
         parts ? head_part : nullptr, head_tiles, err);
     tlg::launch_head_grad_reduce(net.head, hg_partial, loss_partial, ll, gtarget, st, stream);
+    bucket_ready(net.head.wpi, net.P - net.head.wpi, net.L == 0);
     launches += 6;
     if (net.L > 0) {  // db of the top trunk layer from the loss kernel's column partials
       tlg::launch_rows_reduce(col_partial, ll.stream_blocks, net.head.H, net.head.H,
@@ -1000,6 +1057,9 @@ struct tlg_learner {
                            int on_device = 0) {
     launches = 0;
     wq_src = nullptr;  // the parameters changed since the last step
+    overlap_active = nranks > 1 && n == 1 && !overlap_disabled;
+    n_buckets = 0;
+    pend_count = 0;
     mark(0);
     TLG_CUDA(cudaMemsetAsync(err, 0, 16, stream));
     TLG_CUDA(cudaMemsetAsync(grad + P_pad, 0, 16, stream));
@@ -1010,7 +1070,12 @@ struct tlg_learner {
     mark(4);
     // ---- allreduce over ranks (learner.cpp:138-149); the guard slot rides along
     if (nranks > 1) {
-      NCCL_CHECK(tlg::nccl::api().AllReduce(grad, grad, size_t(P_pad + 4), ncclFloat, ncclSum, comm, stream));
+      if (overlap_active) {
+        bucket_flush();
+      } else {
+        NCCL_CHECK(tlg::nccl::api().AllReduce(grad, grad, size_t(P_pad + 4), ncclFloat, ncclSum,
+                                              comm, stream));
+      }
     }
     mark(5);
     // ---- optimizer (skipped on device when any shard of any rank failed); the Adam step
@@ -1072,7 +1137,7 @@ struct tlg_learner {
     int launches = 0;
     const void* obs = nullptr;  // slot obs buffer the graph reads (slot bindings)
   };
-  static constexpr int kExtGraphs = 8;
+  static constexpr int kExtGraphs = 64;
   // learner's own buffers, staging slot 0, staging slot 1, external device batches
   Graph graphs[3 + kExtGraphs];
   std::vector<ExtGraph> ext;
@@ -1158,6 +1223,31 @@ void tlg_learner::set_guard(int shard) {
   set_guard_kernel<<<1, 1, 0, stream>>>(err, stats + shard, grad + P_pad);
   TLG_CHECK_LAUNCH();
   ++launches;
+}
+
+void tlg_learner::issue_bucket(long off, long count, bool with_guard) {
+  if (n_buckets >= kMaxBuckets) throw RuntimeErr("too many gradient buckets");
+  cudaEvent_t& e = bucket_ev[n_buckets++];
+  if (!e) TLG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  TLG_CUDA(cudaEventRecord(e, stream));
+  TLG_CUDA(cudaStreamWaitEvent(comm_stream, e, 0));
+  const auto& nc = tlg::nccl::api();
+  if (with_guard) NCCL_CHECK(nc.GroupStart());
+  if (count > 0)
+    NCCL_CHECK(nc.AllReduce(grad + off, grad + off, size_t(count), ncclFloat, ncclSum, comm,
+                            comm_stream));
+  if (with_guard) {
+    NCCL_CHECK(nc.AllReduce(grad + P_pad, grad + P_pad, 4, ncclFloat, ncclSum, comm,
+                            comm_stream));
+    NCCL_CHECK(nc.GroupEnd());
+  }
+}
+
+void tlg_learner::bucket_flush() {
+  issue_bucket(pend_off, pend_count, true);
+  if (!comm_done) TLG_CUDA(cudaEventCreateWithFlags(&comm_done, cudaEventDisableTiming));
+  TLG_CUDA(cudaEventRecord(comm_done, comm_stream));
+  TLG_CUDA(cudaStreamWaitEvent(stream, comm_done, 0));  // joins the capture, if any
 }
 
 void tlg_learner::accumulate_grad() {
@@ -1380,9 +1470,46 @@ int tlg_learner_comm_init(tlg_learner* l, const uint8_t unique_id[128], int nran
     l->rank = rank;
     ++l->hyper_version;  // re-capture: the step graph embeds the communicator
     if (nranks > 1) {
+      pin_nccl();
       ncclUniqueId id;
       std::memcpy(&id, unique_id, 128);
       NCCL_CHECK(tlg::nccl::api().CommInitRank(&l->comm, nranks, id, rank));
+      l->make_comm_stream();
+    }
+  });
+}
+
+int tlg_learner_comm_init_all(tlg_learner* const* learners, int n) {
+  return Guard([&] {
+    if (!learners || n < 1 || n > 64) throw InvalidArg("1..64 learners");
+    std::vector<int> devs(n);
+    for (int i = 0; i < n; ++i) {
+      if (!learners[i]) throw InvalidArg("null learner");
+      devs[i] = learners[i]->cfg.device;
+      for (int j = 0; j < i; ++j)
+        if (devs[j] == devs[i]) throw InvalidArg("learners must be on distinct devices");
+      if (learners[i]->net.P != learners[0]->net.P)
+        throw InvalidArg("learners must share one policy shape");
+    }
+    for (int i = 0; i < n; ++i) {
+      tlg_learner* l = learners[i];
+      TLG_CUDA(cudaSetDevice(l->cfg.device));
+      if (l->comm) {
+        tlg::nccl::api().CommDestroy(l->comm);
+        l->comm = nullptr;
+      }
+      l->nranks = n;
+      l->rank = i;
+      ++l->hyper_version;
+    }
+    if (n == 1) return;
+    pin_nccl();
+    std::vector<ncclComm_t> comms(n);
+    NCCL_CHECK(tlg::nccl::api().CommInitAll(comms.data(), n, devs.data()));
+    for (int i = 0; i < n; ++i) {
+      learners[i]->comm = comms[i];
+      TLG_CUDA(cudaSetDevice(learners[i]->cfg.device));
+      learners[i]->make_comm_stream();
     }
   });
 }
