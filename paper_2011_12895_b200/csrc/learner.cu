@@ -63,7 +63,6 @@ void pin_nccl() {
   const char* pin = std::getenv("TLG_NCCL_PIN");
   if (pin && std::strcmp(pin, "0") == 0) return;
   setenv("NCCL_ALGO", "Ring", 0);
-  setenv("NCCL_PROTO", "LL128,Simple", 0);
 }
 
 #define NCCL_CHECK(expr)                                                              \
@@ -236,17 +235,19 @@ struct tlg_learner {
   int n_buckets = 0;
   bool overlap_active = false;
   long pend_off = 0, pend_count = 0;
+  bool pend_guard = false;
   const bool overlap_disabled = std::getenv("TLG_NO_OVERLAP") != nullptr;
   void issue_bucket(long off, long count, bool with_guard);
-  // grad[off, off + count) is final on `stream`: allreduce it now, or (the last bucket of
-  // the step) together with the guard in bucket_flush()
-  void bucket_ready(long off, long count, bool last) {
+  // grad[off, off + count) (and the failure guard, with_guard) is final on `stream`:
+  // allreduce it now, or -- the last bucket of the step -- in bucket_flush()
+  void bucket_ready(long off, long count, bool last, bool with_guard = false) {
     if (!overlap_active) return;
     if (last) {
       pend_off = off;
       pend_count = count;
+      pend_guard = with_guard;
     } else {
-      issue_bucket(off, count, false);
+      issue_bucket(off, count, with_guard);
     }
   }
   void bucket_flush();
@@ -666,15 +667,48 @@ struct tlg_learner {
 
   // Trunk backward from dZ_L: dW / db per layer (split-K, fixed-order reductions), dX with
   // tanh' for the layer below, then the rank-ordered shard accumulation and failure guard.
+  // Trunk backward from dZ_L.  (1) the dX chain top down -- dZ_{l-1} = (dZ_l . W_l) *
+  // (1 - X_{l-1}^2) -- with db_{l-1} reduced right after each dX from the column partials
+  // its epilogue wrote; (2) the weight gradients bottom up (dW split-K + fixed-order
+  // reduce), so the widest bucket (layer 1 holds ~88 % of C3's parameters) reaches the
+  // comm stream first and its allreduce runs under the remaining dW GEMMs; then the
+  // rank-ordered shard accumulation.
   void backward_trunk(const Staged& sg, int shard, float* gtarget, const float* x0,
                       const float* x0_lo, long F) {
-    // ---- backward trunk
     using tlg::gemm::Operand;
-    for (int l = int(net.L) - 1; l >= 0; --l) {
+    const bool i8dw = sg.x0_bits != nullptr && i8_dw1();
+    for (int l = int(net.L) - 1; l >= 1; --l) {
       const int in = int(net.dims[l]), outw = int(net.dims[l + 1]);
-      const float* xin = l == 0 ? x0 : act[l - 1];
-      const float* xin_lo = l == 0 ? x0_lo : act_lo[l - 1];
-      if (l == 0 && sg.x0_bits != nullptr && i8_dw1()) {
+      Operand A2{dz[l], dz_lo[l], outw, false};
+      Operand B2{params + net.w_off[l], params_lo + net.w_off[l], in, true};
+      tlg::gemm::Params p2{};
+      p2.out_hi = dz[l - 1];
+      p2.out_lo = dz_lo[l - 1];
+      p2.ldo = in;
+      p2.act_hi = act[l - 1];
+      p2.ld_act = in;
+      p2.colsum = col_partial;
+      if (l == 1 && i8dw) {
+        // dZ_1 feeds only the int8 dW: column maxima per split instead of a residual plane
+        int sp_i8, kbps;
+        i8_dw_plan(F, sp_i8, kbps);
+        TLG_CUDA(cudaMemsetAsync(colmax, 0, size_t(sp_i8) * in * sizeof(unsigned), stream));
+        p2.colmax = colmax;
+        p2.colmax_rows = kbps * 128;
+        p2.out_lo = nullptr;
+      }
+      if (shard == 0) kmark(2, l, 0);
+      colsum_rows = tlg::gemm::launch(A2, B2, int(F), in, outw, tlg::gemm::kEpiBwdTanh, p2, 1,
+                                      stream).ctas;
+      if (shard == 0) kmark(2, l, 1);
+      // db_{l-1} = column sums of dZ_{l-1} (col_partial is reused by the next dX)
+      tlg::launch_rows_reduce(col_partial, colsum_rows, in, in, gtarget + net.b_off[l - 1],
+                              stream);
+      launches += 2;
+    }
+    for (int l = 0; l < int(net.L); ++l) {
+      const int in = int(net.dims[l]), outw = int(net.dims[l + 1]);
+      if (l == 0 && i8dw) {
         // dW_1 = dZ_1^T . X on the int8 tensor cores (exact int32 per split)
         int sp_i8, kbps;
         i8_dw_plan(F, sp_i8, kbps);
@@ -685,73 +719,35 @@ struct tlg_learner {
                                      ws, stream);
         if (shard == 0) kmark(1, l, 1);
         tlg::launch_dw_reduce(ws, sp_i8, long(outw) * in, gtarget + net.w_off[0], stream);
-        if (net.L > 1) {
-          tlg::launch_rows_reduce(col_partial, colsum_rows, outw, outw, gtarget + net.b_off[0],
-                                  stream);
-          ++launches;
-        }
         launches += 3;
-        bucket_ready(net.w_off[0], long(outw) * in + outw, true);
-        continue;
+      } else {
+        // dW_l = dZ_l^T . X_{l-1}   (K = frames, split-K partials reduced in fixed order)
+        const float* xin = l == 0 ? x0 : act[l - 1];
+        const float* xin_lo = l == 0 ? x0_lo : act_lo[l - 1];
+        int sp = tlg::gemm::pick_splits(outw, in, int(F), kMaxSplits);
+        while (long(sp) * outw * in > ws_elems && sp > 1) --sp;
+        Operand A{dz[l], dz_lo[l], outw, true};
+        // layer 1 reads the uint8 planes directly (converted in smem, exact, no residual)
+        Operand B{xin, xin_lo, in, true, l == 0 ? x0_u8 : nullptr};
+        tlg::gemm::Params p{};
+        p.ws = ws;
+        p.ws_split_stride = long(outw) * in;
+        const int kb = (int(F) + tlg::gemm::kBK - 1) / tlg::gemm::kBK;
+        const int per = (kb + sp - 1) / sp;
+        const int sp_eff = (kb + per - 1) / per;  // launch() drops empty splits the same way
+        if (shard == 0) kmark(1, l, 0);
+        tlg::gemm::launch(A, B, outw, in, int(F), tlg::gemm::kEpiStore, p, sp, stream);
+        if (shard == 0) kmark(1, l, 1);
+        tlg::launch_dw_reduce(ws, sp_eff, long(outw) * in, gtarget + net.w_off[l], stream);
+        launches += 2;
       }
-      // dW_l = dZ_l^T . X_{l-1}   (K = frames, split-K partials reduced in fixed order)
-      int sp = tlg::gemm::pick_splits(outw, in, int(F), kMaxSplits);
-      while (long(sp) * outw * in > ws_elems && sp > 1) --sp;
-      Operand A{dz[l], dz_lo[l], outw, true};
-      // layer 1 reads the uint8 planes directly (converted in smem, exact, no residual)
-      Operand B{xin, xin_lo, in, true, l == 0 ? x0_u8 : nullptr};
-      tlg::gemm::Params p{};
-      p.ws = ws;
-      p.ws_split_stride = long(outw) * in;
-      const int kb = (int(F) + tlg::gemm::kBK - 1) / tlg::gemm::kBK;
-      const int per = (kb + sp - 1) / sp;
-      const int sp_eff = (kb + per - 1) / per;  // launch() drops empty splits the same way
-      if (shard == 0) kmark(1, l, 0);
-      tlg::gemm::launch(A, B, outw, in, int(F), tlg::gemm::kEpiStore, p, sp, stream);
-      if (shard == 0) kmark(1, l, 1);
-      tlg::launch_dw_reduce(ws, sp_eff, long(outw) * in, gtarget + net.w_off[l], stream);
-      // db_l = column sums of dZ_l, from the per-M-tile partials the dX epilogue of
-      // layer l+1 wrote (the top layer's came from the loss kernel)
-      if (l < int(net.L) - 1) {
-        tlg::launch_rows_reduce(col_partial, colsum_rows, outw, outw, gtarget + net.b_off[l],
-                                stream);
-        ++launches;
-      }
-      launches += 2;
       // W_l and b_l are contiguous in the flat layout: one bucket, allreduced while the
-      // dX GEMM below (and the layers under it) run
-      bucket_ready(net.w_off[l], long(outw) * in + outw, l == 0);
-      if (l > 0) {
-        // dZ_{l-1} = (dZ_l . W_l) * (1 - X_{l-1}^2)
-        Operand A2{dz[l], dz_lo[l], outw, false};
-        Operand B2{params + net.w_off[l], params_lo + net.w_off[l], in, true};
-        tlg::gemm::Params p2{};
-        p2.out_hi = dz[l - 1];
-        p2.out_lo = dz_lo[l - 1];
-        p2.ldo = in;
-        p2.act_hi = act[l - 1];
-        p2.ld_act = in;
-        p2.colsum = col_partial;
-        if (l == 1 && sg.x0_bits != nullptr && i8_dw1()) {
-          // dZ_1 feeds only the int8 dW: column maxima per split instead of a residual plane
-          int sp_i8, kbps;
-          i8_dw_plan(F, sp_i8, kbps);
-          TLG_CUDA(cudaMemsetAsync(colmax, 0, size_t(sp_i8) * in * sizeof(unsigned), stream));
-          p2.colmax = colmax;
-          p2.colmax_rows = kbps * 128;
-          p2.out_lo = nullptr;
-        }
-        if (shard == 0) kmark(2, l, 0);
-        colsum_rows = tlg::gemm::launch(A2, B2, int(F), in, outw, tlg::gemm::kEpiBwdTanh, p2, 1,
-                                        stream).ctas;
-        if (shard == 0) kmark(2, l, 1);
-        ++launches;
-      }
+      // dW GEMMs of the layers above run
+      bucket_ready(net.w_off[l], long(outw) * in + outw, l + 1 == int(net.L));
     }
     if (gtarget != grad) {
       accumulate_grad();  // grad += shard gradient, in rank order (learner.cpp:145-147)
     }
-    set_guard(shard);
   }
 
   void compute_shard(const Staged& sg, int shard, float* gtarget) {
@@ -812,7 +808,8 @@ struct tlg_learner {
       tlg::LossLaunch ll{fused_ctas, fused_ctas};
       tlg::launch_head_grad_reduce(net.head, hg_partial, loss_partial, ll, gtarget, st, stream,
                                    le.bias_partial);
-      bucket_ready(net.head.wpi, net.P - net.head.wpi, net.L == 0);
+      set_guard(shard);  // the shard's loss and error flags are final here
+      bucket_ready(net.head.wpi, net.P - net.head.wpi, net.L == 0, /*with_guard=*/true);
       tlg::launch_rows_reduce(col_partial, fused_ctas, net.head.H, net.head.H,
                               gtarget + net.b_off[net.L - 1], stream);
       launches += 5;
@@ -834,7 +831,8 @@ struct tlg_learner {
         loss_partial, col_partial, stream, teacher_active() ? t_head_out : nullptr,
         parts ? head_part : nullptr, head_tiles, err);
     tlg::launch_head_grad_reduce(net.head, hg_partial, loss_partial, ll, gtarget, st, stream);
-    bucket_ready(net.head.wpi, net.P - net.head.wpi, net.L == 0);
+    set_guard(shard);  // the shard's loss and error flags are final here
+    bucket_ready(net.head.wpi, net.P - net.head.wpi, net.L == 0, /*with_guard=*/true);
     launches += 6;
     if (net.L > 0) {  // db of the top trunk layer from the loss kernel's column partials
       tlg::launch_rows_reduce(col_partial, ll.stream_blocks, net.head.H, net.head.H,
@@ -849,8 +847,11 @@ struct tlg_learner {
   // Small steps are launch-bound: after staging into the learner's own buffers, the
   // whole device step (kernels, allreduce, optimizer, stats D2H) replays as one CUDA graph.
   bool use_graph(const tlg_segment_batch*, int n) const {
-    return !cfg.timing && n == 1 && !graph_disabled;
+    return !cfg.timing && n == 1 && !graph_disabled && comm_warm;
   }
+  // NCCL connects its transports lazily at a communicator's first collectives, which
+  // must not happen under stream capture: the first step after comm init runs eagerly
+  bool comm_warm = true;
   // graph of a step over an external device-resident batch, keyed by its pointers
   struct ExtGraph {
     const void* ptrs[8] = {};
@@ -1060,6 +1061,7 @@ struct tlg_learner {
     overlap_active = nranks > 1 && n == 1 && !overlap_disabled;
     n_buckets = 0;
     pend_count = 0;
+    pend_guard = false;
     mark(0);
     TLG_CUDA(cudaMemsetAsync(err, 0, 16, stream));
     TLG_CUDA(cudaMemsetAsync(grad + P_pad, 0, 16, stream));
@@ -1111,6 +1113,7 @@ struct tlg_learner {
       throw RuntimeErr("learner shard failed on another rank at update step " + std::to_string(k));
     if (adam) ++adam_t;
     steps_done = k;
+    comm_warm = true;
     if (out) {
       for (int r = 0; r < n; ++r) {
         const tlg::StepStatsDev& h = h_stats[r];
@@ -1232,19 +1235,19 @@ void tlg_learner::issue_bucket(long off, long count, bool with_guard) {
   TLG_CUDA(cudaEventRecord(e, stream));
   TLG_CUDA(cudaStreamWaitEvent(comm_stream, e, 0));
   const auto& nc = tlg::nccl::api();
-  if (with_guard) NCCL_CHECK(nc.GroupStart());
+  if (with_guard && count > 0) NCCL_CHECK(nc.GroupStart());
   if (count > 0)
     NCCL_CHECK(nc.AllReduce(grad + off, grad + off, size_t(count), ncclFloat, ncclSum, comm,
                             comm_stream));
   if (with_guard) {
     NCCL_CHECK(nc.AllReduce(grad + P_pad, grad + P_pad, 4, ncclFloat, ncclSum, comm,
                             comm_stream));
-    NCCL_CHECK(nc.GroupEnd());
+    if (count > 0) NCCL_CHECK(nc.GroupEnd());
   }
 }
 
 void tlg_learner::bucket_flush() {
-  issue_bucket(pend_off, pend_count, true);
+  issue_bucket(pend_off, pend_count, pend_guard);
   if (!comm_done) TLG_CUDA(cudaEventCreateWithFlags(&comm_done, cudaEventDisableTiming));
   TLG_CUDA(cudaEventRecord(comm_done, comm_stream));
   TLG_CUDA(cudaStreamWaitEvent(stream, comm_done, 0));  // joins the capture, if any
@@ -1468,6 +1471,7 @@ int tlg_learner_comm_init(tlg_learner* l, const uint8_t unique_id[128], int nran
     }
     l->nranks = nranks;
     l->rank = rank;
+    l->comm_warm = nranks == 1;
     ++l->hyper_version;  // re-capture: the step graph embeds the communicator
     if (nranks > 1) {
       pin_nccl();
@@ -1500,6 +1504,7 @@ int tlg_learner_comm_init_all(tlg_learner* const* learners, int n) {
       }
       l->nranks = n;
       l->rank = i;
+      l->comm_warm = n == 1;
       ++l->hyper_version;
     }
     if (n == 1) return;
