@@ -637,6 +637,17 @@ def main():
             others.append({"value": None, "kind": "port", "sample": f"unavailable: {e}"})
         cpu["others"] = others
 
+    # ---- the drop-in C++ learner::Learner (reference-facing API) at C3, N=1
+    dropin = None
+    exe = os.path.join(ROOT, "integration", "_build", "dropin_bench")
+    if rank == 0 and world == 1 and cfg.name == "C3" and os.path.exists(exe):
+        try:
+            out = subprocess.run([exe, str(cfg.batch_size), "3"], capture_output=True, text=True,
+                                 timeout=300)
+            dropin = json.loads(out.stdout.strip().splitlines()[-1])
+        except Exception as e:  # reported, not raised
+            dropin = {"unavailable": f"{type(e).__name__}: {e}"}
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
@@ -662,6 +673,7 @@ def main():
                             "bit rows padded to 16 B), pipelined one step ahead on a copy "
                             "stream; stats D2H each step"},
             "weak_scaling": weak,
+            "dropin_e2e": dropin,
             "e2e_alt_format": e2e_alt,
             "e2e_dense_rows": e2e_unpitched,
             "device_replay": replay,

@@ -126,6 +126,8 @@ typedef struct tlg_policy tlg_policy;
 
 const char* tlg_last_error(void);
 const char* tlg_version(void);
+/* CUDA devices visible to this process (0 without a driver / GPU). */
+int tlg_device_count(void);
 /* Page-locked host staging memory for the host-pointer calls (NULL on failure). */
 void* tlg_host_alloc(size_t bytes);
 void tlg_host_free(void* p);

@@ -48,6 +48,10 @@ struct LearnerConfig {
   std::uint32_t step_delay_ms = 0;
   // ---- B200 additions
   int device = 0;
+  // More than one entry: data-parallel over these devices in this process (one learner
+  // and one host thread per device, NCCL over NVLink); num_shards must be a multiple of
+  // devices.size(), each device taking num_shards / devices.size() consecutive shards.
+  std::vector<int> devices;
   Optimizer optimizer = Optimizer::kSgd;
   double adam_beta1 = 0.9, adam_beta2 = 0.999, adam_eps = 1e-8;
   // Non-empty: the blob is an MLP (flat [W_1,b_1,...,W_L,b_L | W_pi,b_pi | w_v,b_v])

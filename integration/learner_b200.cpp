@@ -4,6 +4,8 @@
 #include "tleague/learner/learner.hpp"
 
 #include <algorithm>
+#include <atomic>
+#include <exception>
 #include <chrono>
 #include <cmath>
 #include <condition_variable>
@@ -27,6 +29,50 @@ void Check(int rc) {
   const std::string msg = tlg_last_error();
   if (rc == TLG_INVALID_ARGUMENT) throw std::invalid_argument(msg);
   throw std::runtime_error(msg);
+}
+
+// The device-side shape of a blob: PolicyFamily::kMlp carries its trunk widths in
+// PolicyShape::hidden (wire tag 2); `hidden` (the config's mlp_hidden) is the older
+// spelling for an MLP-layout blob tagged with another family, and must agree otherwise.
+tlg_policy_shape DeviceShape(const ParamBlob& b, const std::vector<std::uint32_t>& hidden) {
+  tlg_policy_shape s{};
+  const bool mlp = b.family == PolicyFamily::kMlp;
+  const std::vector<std::uint32_t>& h = mlp ? b.shape.hidden : hidden;
+  if (mlp && !hidden.empty() && hidden != b.shape.hidden)
+    throw std::invalid_argument("mlp_hidden does not match the blob's trunk widths");
+  s.family = (mlp || !hidden.empty()) ? TLG_FAMILY_MLP : std::uint32_t(b.family);
+  s.obs_dim = b.shape.obs_dim;
+  s.n_actions = b.shape.n_actions;
+  if (h.size() > 8) throw std::invalid_argument("at most 8 hidden layers");
+  s.n_hidden = std::uint32_t(h.size());
+  for (std::uint32_t l = 0; l < s.n_hidden; ++l) s.hidden[l] = h[l];
+  return s;
+}
+
+// fn(lo, hi) over [0, n) split into contiguous ranges on up to 16 host threads (fewer
+// when the work is small); the first exception (in range order) is rethrown.
+template <typename F>
+void ParallelRanges(std::size_t n, std::size_t work, F&& fn) {
+  const std::size_t nth = std::max<std::size_t>(
+      1, std::min<std::size_t>({16, std::size_t(std::max(1u, std::thread::hardware_concurrency())),
+                                work / (1u << 16) + 1, n}));
+  if (nth <= 1) {
+    fn(std::size_t(0), n);
+    return;
+  }
+  std::vector<std::thread> pool;
+  std::vector<std::exception_ptr> errs(nth);
+  for (std::size_t w = 0; w < nth; ++w)
+    pool.emplace_back([&, w] {
+      try {
+        fn(n * w / nth, n * (w + 1) / nth);
+      } catch (...) {
+        errs[w] = std::current_exception();
+      }
+    });
+  for (auto& t : pool) t.join();
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
 }
 
 template <typename T>
@@ -55,6 +101,9 @@ Algo ParseAlgo(const std::string& name) {
 // One GPU learner plus pinned SoA staging for `shards` slices of the replay draw.
 struct Learner::Gpu {
   tlg_learner* h = nullptr;
+  // LearnerConfig::devices with G > 1: one learner per device (hs[0] == h), joined by one
+  // ncclCommInitAll; each device takes num_shards / G consecutive shards of the draw
+  std::vector<tlg_learner*> hs;
   tlg_policy_shape shape{};
   std::uint32_t S = 0, T = 0, shards = 0;
   std::size_t P = 0;
@@ -85,21 +134,20 @@ struct Learner::Gpu {
   std::unordered_map<std::uint64_t, Live> live;     // id -> slot, draws so far
   std::vector<std::uint32_t> free_slots, deferred;  // deferred: freed while pinned
   std::unordered_set<std::uint32_t> pinned;
-  Pinned<float> one_obs, one_f;
-  Pinned<std::int32_t> one_i;
-  Pinned<std::uint8_t> one_b, one_d;
 
   void ResetRing(std::size_t capacity) {
     if (ring) tlg_replay_destroy(ring);
     ring = nullptr;
     ring_decided = false;
-    ring_cap = std::uint32_t(capacity);
+    ring_cap = std::uint32_t(capacity) + 1;  // + the trash slot of Flush
+    trash_slot = ring_cap - 1;
+    stg_slots.clear();
     fifo.clear();
     live.clear();
     pinned.clear();
     deferred.clear();
     free_slots.clear();
-    for (std::uint32_t i = ring_cap; i-- > 0;) free_slots.push_back(i);
+    for (std::uint32_t i = trash_slot; i-- > 0;) free_slots.push_back(i);
   }
   void Release(std::uint32_t slot) {
     if (pinned.count(slot)) deferred.push_back(slot);
@@ -165,82 +213,109 @@ struct Learner::Gpu {
     }
     u = Undo{};
   }
-  // one segment -> SoA in the pinned single-segment buffers (the same packing as Pack);
-  // validates the segment, so it runs before any admission.  Commit copies it to a slot.
-  tlg_segment_batch one{};
+  // ---- coalesced ingest: PushSegment packs each segment (SoA, the same packing as Pack)
+  // into a pinned staging batch and records its slot; the staged segments reach their HBM
+  // slots in one tlg_replay_put (one copy per array, one synchronisation) when the stage
+  // fills, before every draw and before a bulk push.  A slot staged twice (its entry was
+  // evicted and the slot handed out again before the flush) keeps only its newest
+  // segment: older copies are redirected to a trash slot past the ring's live slots.
+  static constexpr std::uint32_t kStageSegs = 512;
+  Pinned<std::uint8_t> stg_bits, stg_done;
+  Pinned<float> stg_obs, stg_f;  // f32 obs; reward | blogp | value per frame, bootstrap
+  Pinned<std::int32_t> stg_i;    // action per frame, valid_steps per segment
+  std::vector<std::uint32_t> stg_slots;
+  std::uint32_t trash_slot = 0;
+
+  // Validate and pack `seg` into the next free stage position (the caller flushes a full
+  // stage first); nothing is recorded until Commit, so a throw leaves no trace.
   void Prepare(const TrajectorySegment& seg) {
     const std::size_t D = shape.obs_dim, rowb = (D + 7) / 8;
     const bool bitsfmt = ring_dtype == TLG_OBS_BITS;
-    if (bitsfmt) {
-      one_b.ensure(std::size_t(T) * (rowb + 1));
-      std::memset(one_b.p, 0, std::size_t(T) * (rowb + 1));
-    } else {
-      one_obs.ensure(std::size_t(T) * D);
-      std::memset(one_obs.p, 0, std::size_t(T) * D * sizeof(float));
-    }
-    one_f.ensure(3 * std::size_t(T) + 1);
-    one_i.ensure(std::size_t(T) + 1);
-    float* rw = one_f.p;
-    float* bl = rw + T;
-    float* va = bl + T;
-    float* bo = va + T;
-    std::uint8_t* dn = bitsfmt ? one_b.p + std::size_t(T) * rowb : nullptr;
-    if (!bitsfmt) {  // kept until Commit: a member buffer, not a local
-      one_d.ensure(T);
-      std::memset(one_d.p, 0, T);
-      dn = one_d.p;
-    }
+    if (stg_slots.size() == kStageSegs) Flush();
+    const std::size_t k = stg_slots.size(), f0 = k * T;
+    if (bitsfmt) stg_bits.ensure(std::size_t(kStageSegs) * T * rowb);
+    else stg_obs.ensure(std::size_t(kStageSegs) * T * D);
+    stg_f.ensure(std::size_t(kStageSegs) * (3 * T + 1));
+    stg_i.ensure(std::size_t(kStageSegs) * (T + 1));
+    stg_done.ensure(std::size_t(kStageSegs) * T);
+    float* rw = stg_f.p + f0;
+    float* bl = stg_f.p + std::size_t(kStageSegs) * T + f0;
+    float* va = stg_f.p + 2 * std::size_t(kStageSegs) * T + f0;
+    float* bo = stg_f.p + 3 * std::size_t(kStageSegs) * T + k;
+    std::int32_t* ac = stg_i.p + f0;
+    std::int32_t* vs = stg_i.p + std::size_t(kStageSegs) * T + k;
+    std::uint8_t* dn = stg_done.p + f0;
     if (seg.valid_steps > T || seg.valid_steps > seg.steps.size())
       throw std::invalid_argument("segment valid_steps exceeds its steps / unroll_len");
     for (std::uint32_t t = 0; t < T; ++t) {
+      std::uint8_t* brow = bitsfmt ? stg_bits.p + (f0 + t) * rowb : nullptr;
+      float* orow = bitsfmt ? nullptr : stg_obs.p + (f0 + t) * D;
+      if (bitsfmt) std::memset(brow, 0, rowb);
       if (t < seg.valid_steps) {
         const SegmentStep& st = seg.steps[t];
         if (st.obs.size() != D)
           throw std::invalid_argument("observation size does not match policy shape");
         if (bitsfmt) {
-          std::uint8_t* row = one_b.p + std::size_t(t) * rowb;
           for (std::size_t j = 0; j < D; ++j) {
-            if (st.obs[j] == 1.0) row[j >> 3] |= std::uint8_t(1u << (j & 7));
+            if (st.obs[j] == 1.0) brow[j >> 3] |= std::uint8_t(1u << (j & 7));
             else if (st.obs[j] != 0.0)
               throw std::invalid_argument("device replay: non-binary observation in a "
                                           "bit-packed period");
           }
         } else {
-          for (std::size_t j = 0; j < D; ++j) one_obs.p[std::size_t(t) * D + j] = float(st.obs[j]);
+          for (std::size_t j = 0; j < D; ++j) orow[j] = float(st.obs[j]);
         }
-        one_i.p[t] = std::int32_t(st.action);
+        ac[t] = std::int32_t(st.action);
         rw[t] = float(st.reward);
         bl[t] = float(st.behavior_logp);
         va[t] = float(st.value_est);
         dn[t] = st.done ? 1 : 0;
       } else {
-        one_i.p[t] = 0;
+        if (!bitsfmt) std::memset(orow, 0, D * sizeof(float));
+        ac[t] = 0;
         rw[t] = bl[t] = va[t] = 0.f;
         dn[t] = 0;
       }
     }
     *bo = float(seg.bootstrap_value);
-    one_i.p[T] = std::int32_t(seg.valid_steps);
+    *vs = std::int32_t(seg.valid_steps);
+  }
+  // The prepared segment belongs in `slot`.
+  void Commit(std::uint32_t slot) { stg_slots.push_back(slot); }
+  // Staged segments -> their HBM slots (one put).  Must run before the slots are read.
+  void Flush() {
+    const std::size_t n = stg_slots.size();
+    if (n == 0) return;
+    std::vector<std::uint32_t> sl(stg_slots);
+    std::unordered_set<std::uint32_t> seen;
+    for (std::size_t i = n; i-- > 0;)
+      if (!seen.insert(sl[i]).second) sl[i] = trash_slot;  // an older copy of a reused slot
     tlg_segment_batch b{};
-    b.n_segments = 1;
+    b.n_segments = std::uint32_t(n);
     b.unroll_len = T;
     b.obs_dim = shape.obs_dim;
     b.obs_dtype = ring_dtype;
-    b.obs = bitsfmt ? static_cast<const void*>(one_b.p) : static_cast<const void*>(one_obs.p);
-    b.action = one_i.p;
-    b.reward = rw;
-    b.behavior_logp = bl;
-    b.value_est = va;
-    b.done = dn;
-    b.bootstrap = bo;
-    b.valid_steps = one_i.p + T;
-    one = b;
+    b.obs = ring_dtype == TLG_OBS_BITS ? static_cast<const void*>(stg_bits.p)
+                                       : static_cast<const void*>(stg_obs.p);
+    b.action = stg_i.p;
+    b.reward = stg_f.p;
+    b.behavior_logp = stg_f.p + std::size_t(kStageSegs) * T;
+    b.value_est = stg_f.p + 2 * std::size_t(kStageSegs) * T;
+    b.done = stg_done.p;
+    b.bootstrap = stg_f.p + 3 * std::size_t(kStageSegs) * T;
+    b.valid_steps = stg_i.p + std::size_t(kStageSegs) * T;
+    stg_slots.clear();  // cleared first: a failed copy is a device error (fail-stop)
+    Check(tlg_replay_put(ring, sl.data(), &b));
   }
-  void Commit(std::uint32_t slot) { Check(tlg_replay_put(ring, &slot, &one)); }
 
   ~Gpu() {
     if (ring) tlg_replay_destroy(ring);
-    tlg_learner_destroy(h);
+    DestroyLearners();
+  }
+  void DestroyLearners() {
+    for (tlg_learner* x : hs) tlg_learner_destroy(x);
+    hs.clear();
+    h = nullptr;
   }
 
   bool Matches(const tlg_policy_shape& s, std::uint32_t S_, std::uint32_t T_,
@@ -255,23 +330,24 @@ struct Learner::Gpu {
   void Pack(const std::vector<TrajectorySegment>& segs) {
     const std::size_t D = shape.obs_dim, F = std::size_t(S) * T * shards;
     const std::size_t rowb = (D + 7) / 8;
-    binary = true;
-    for (const TrajectorySegment& seg : segs) {
-      const std::uint32_t n = std::min<std::uint32_t>(seg.valid_steps, std::uint32_t(seg.steps.size()));
-      for (std::uint32_t t = 0; t < n && binary; ++t)
-        for (double x : seg.steps[t].obs)
-          if (x != 0.0 && x != 1.0) {
-            binary = false;
-            break;
-          }
-      if (!binary) break;
-    }
-    if (binary) {
-      bits.ensure(F * rowb);
-      std::memset(bits.p, 0, F * rowb);
-    } else {
-      obs.ensure(F * D);
-    }
+    // the format is decided over the whole draw first (a parallel scan)
+    std::atomic<bool> all_binary{true};
+    ParallelRanges(segs.size(), segs.size() * T * D, [&](std::size_t lo, std::size_t hi) {
+      for (std::size_t i = lo; i < hi && all_binary.load(std::memory_order_relaxed); ++i) {
+        const TrajectorySegment& seg = segs[i];
+        const std::uint32_t n =
+            std::min<std::uint32_t>(seg.valid_steps, std::uint32_t(seg.steps.size()));
+        for (std::uint32_t t = 0; t < n; ++t)
+          for (double x : seg.steps[t].obs)
+            if (x != 0.0 && x != 1.0) {
+              all_binary = false;
+              return;
+            }
+      }
+    });
+    binary = all_binary.load();
+    if (binary) bits.ensure(F * rowb);
+    else obs.ensure(F * D);
     reward.ensure(F);
     blogp.ensure(F);
     value.ensure(F);
@@ -279,38 +355,10 @@ struct Learner::Gpu {
     done.ensure(F);
     boot.ensure(std::size_t(S) * shards);
     valid.ensure(std::size_t(S) * shards);
-    if (!binary) std::memset(obs.p, 0, F * D * sizeof(float));
-    for (std::size_t i = 0; i < segs.size(); ++i) {
-      const TrajectorySegment& seg = segs[i];
-      if (seg.valid_steps > T || seg.valid_steps > seg.steps.size())
-        throw std::invalid_argument("segment valid_steps exceeds its steps / unroll_len");
-      boot.p[i] = float(seg.bootstrap_value);
-      valid.p[i] = std::int32_t(seg.valid_steps);
-      for (std::uint32_t t = 0; t < T; ++t) {
-        const std::size_t f = i * T + t;
-        if (t < seg.valid_steps) {
-          const SegmentStep& st = seg.steps[t];
-          if (st.obs.size() != D)
-            throw std::invalid_argument("observation size does not match policy shape");
-          if (binary) {
-            std::uint8_t* row = bits.p + f * rowb;
-            for (std::size_t j = 0; j < D; ++j)
-              if (st.obs[j] != 0.0) row[j >> 3] |= std::uint8_t(1u << (j & 7));
-          } else {
-            for (std::size_t j = 0; j < D; ++j) obs.p[f * D + j] = float(st.obs[j]);
-          }
-          action.p[f] = std::int32_t(st.action);
-          reward.p[f] = float(st.reward);
-          blogp.p[f] = float(st.behavior_logp);
-          value.p[f] = float(st.value_est);
-          done.p[f] = st.done ? 1 : 0;
-        } else {
-          action.p[f] = 0;
-          reward.p[f] = blogp.p[f] = value.p[f] = 0.f;
-          done.p[f] = 0;
-        }
-      }
-    }
+    // segments are independent: pack them on up to 16 host threads (a C3 draw is 4096
+    // segments x 32 steps x 1936 doubles = 2 GB of fp64 observations)
+    ParallelRanges(segs.size(), segs.size() * T * D,
+                   [&](std::size_t lo, std::size_t hi) { PackRange(segs, lo, hi, rowb); });
     batches.assign(shards, tlg_segment_batch{});
     for (std::uint32_t r = 0; r < shards; ++r) {
       tlg_segment_batch& b = batches[r];
@@ -330,6 +378,75 @@ struct Learner::Gpu {
       b.valid_steps = valid.p + s0;
     }
   }
+
+  void PackRange(const std::vector<TrajectorySegment>& segs, std::size_t lo, std::size_t hi,
+                 std::size_t rowb) {
+    const std::size_t D = shape.obs_dim;
+    for (std::size_t i = lo; i < hi; ++i) {
+      const TrajectorySegment& seg = segs[i];
+      if (seg.valid_steps > T || seg.valid_steps > seg.steps.size())
+        throw std::invalid_argument("segment valid_steps exceeds its steps / unroll_len");
+      boot.p[i] = float(seg.bootstrap_value);
+      valid.p[i] = std::int32_t(seg.valid_steps);
+      for (std::uint32_t t = 0; t < T; ++t) {
+        const std::size_t f = i * T + t;
+        if (t < seg.valid_steps) {
+          const SegmentStep& st = seg.steps[t];
+          if (st.obs.size() != D)
+            throw std::invalid_argument("observation size does not match policy shape");
+          if (binary) {
+            std::uint8_t* row = bits.p + f * rowb;
+            std::memset(row, 0, rowb);
+            for (std::size_t j = 0; j < D; ++j)
+              if (st.obs[j] != 0.0) row[j >> 3] |= std::uint8_t(1u << (j & 7));
+          } else {
+            for (std::size_t j = 0; j < D; ++j) obs.p[f * D + j] = float(st.obs[j]);
+          }
+          action.p[f] = std::int32_t(st.action);
+          reward.p[f] = float(st.reward);
+          blogp.p[f] = float(st.behavior_logp);
+          value.p[f] = float(st.value_est);
+          done.p[f] = st.done ? 1 : 0;
+        } else {  // padding (segmenter.cpp:26-31): all zero
+          if (binary) std::memset(bits.p + f * rowb, 0, rowb);
+          else std::memset(obs.p + f * D, 0, D * sizeof(float));
+          action.p[f] = 0;
+          reward.p[f] = blogp.p[f] = value.p[f] = 0.f;
+          done.p[f] = 0;
+        }
+      }
+    }
+  }
+
+  // One training step over the packed shards: on one device a single call; on G devices
+  // one host thread per device issues its num_shards / G shards (the reference's shard
+  // threads, learner.cpp:117-134), the gradient sum crossing NVLink in NCCL buckets.
+  // The first failure (in device order) is rethrown, as learner.cpp:134-136 does.
+  void Train() {
+    stats.assign(shards, tlg_step_stats{});
+    const int G = int(hs.size());
+    if (G <= 1) {
+      Check(tlg_learner_train_step_shards(h, batches.data(), int(shards), /*on_device=*/0,
+                                          stats.data()));
+      return;
+    }
+    const int per = int(shards) / G;
+    std::vector<int> rc(G, TLG_OK);
+    std::vector<std::string> msg(G);
+    std::vector<std::thread> th;
+    for (int g = 0; g < G; ++g)
+      th.emplace_back([&, g] {
+        rc[g] = tlg_learner_train_step_shards(hs[g], batches.data() + g * per, per, 0,
+                                              stats.data() + g * per);
+        if (rc[g] != TLG_OK) msg[g] = tlg_last_error();  // thread-local message
+      });
+    for (auto& t : th) t.join();
+    for (int g = 0; g < G; ++g)
+      if (rc[g] != TLG_OK) {
+        if (rc[g] == TLG_INVALID_ARGUMENT) throw std::invalid_argument(msg[g]);
+        throw std::runtime_error(msg[g]);
+      }
+  }
 };
 
 Learner::Learner(LearnerConfig config, league::LeagueIface& league, pool::ModelPoolIface& pool)
@@ -339,6 +456,12 @@ Learner::Learner(LearnerConfig config, league::LeagueIface& league, pool::ModelP
       replay_(config_.replay_capacity, /*max_reuse set per task*/ 1, config_.seed),
       gpu_(std::make_unique<Gpu>()) {
   if (config_.num_shards == 0) throw std::invalid_argument("num_shards must be >= 1");
+  if (config_.devices.size() > 1) {
+    if (config_.num_shards % config_.devices.size() != 0)
+      throw std::invalid_argument("num_shards must be a multiple of the number of devices");
+    if (config_.device_replay)
+      throw std::invalid_argument("device_replay runs on a single device");
+  }
   StartPeriod();
 }
 
@@ -358,13 +481,7 @@ void Learner::StartPeriod() {
   replay_.SetMaxReuse(hyper_.max_reuse);
 
   // (Re)configure the device learner for this period's blob and hyperparameters.
-  tlg_policy_shape s{};
-  s.family = config_.mlp_hidden.empty() ? std::uint32_t(params_.family) : TLG_FAMILY_MLP;
-  s.obs_dim = params_.shape.obs_dim;
-  s.n_actions = params_.shape.n_actions;
-  s.n_hidden = std::uint32_t(config_.mlp_hidden.size());
-  if (s.n_hidden > 8) throw std::invalid_argument("at most 8 hidden layers");
-  for (std::uint32_t l = 0; l < s.n_hidden; ++l) s.hidden[l] = config_.mlp_hidden[l];
+  const tlg_policy_shape s = DeviceShape(params_, config_.mlp_hidden);
   const std::uint32_t S = hyper_.batch_size, T = hyper_.unroll_len;
   if (gpu_->ring) {  // the ring belongs to the device learner: drop it first
     std::lock_guard dl(gpu_->mu);
@@ -372,8 +489,7 @@ void Learner::StartPeriod() {
     gpu_->ring = nullptr;
   }
   if (!gpu_->Matches(s, S, T, config_.num_shards)) {
-    tlg_learner_destroy(gpu_->h);
-    gpu_->h = nullptr;
+    gpu_->DestroyLearners();
     tlg_learner_config c{};
     c.algo = config_.algo == Algo::kPpo      ? TLG_ALGO_PPO
              : config_.algo == Algo::kVtrace ? TLG_ALGO_VTRACE
@@ -384,9 +500,18 @@ void Learner::StartPeriod() {
     c.adam_eps = config_.adam_eps;
     c.max_segments = S;
     c.unroll_len = T;
-    c.device = config_.device;
     c.obs_dtype = TLG_OBS_BITS;  // accepts fp32 and bit-packed batches
-    Check(tlg_learner_create(&c, &s, &gpu_->h));
+    const std::vector<int> devs =
+        config_.devices.size() > 1 ? config_.devices : std::vector<int>{config_.device};
+    for (int d : devs) {
+      c.device = d;
+      tlg_learner* x = nullptr;
+      Check(tlg_learner_create(&c, &s, &x));
+      gpu_->hs.push_back(x);
+    }
+    gpu_->h = gpu_->hs[0];
+    if (gpu_->hs.size() > 1)
+      Check(tlg_learner_comm_init_all(gpu_->hs.data(), int(gpu_->hs.size())));
     gpu_->shape = s;
     gpu_->S = S;
     gpu_->T = T;
@@ -397,8 +522,10 @@ void Learner::StartPeriod() {
                hyper_.vf_coef, hyper_.ent_coef, hyper_.kl_teacher_coef, hyper_.rho_bar,
                hyper_.c_bar, hyper_.batch_size, hyper_.unroll_len, hyper_.max_reuse,
                hyper_.adv_norm ? 1 : 0};
-  Check(tlg_learner_set_hyper(gpu_->h, &hp));
-  Check(tlg_learner_set_params(gpu_->h, params_.values.data(), params_.values.size()));
+  for (tlg_learner* x : gpu_->hs) {  // identical parameters and optimizer state everywhere
+    Check(tlg_learner_set_hyper(x, &hp));
+    Check(tlg_learner_set_params(x, params_.values.data(), params_.values.size()));
+  }
   if (config_.device_replay) {
     std::lock_guard dl(gpu_->mu);
     // replay_capacity live entries + the slots pinned by one draw
@@ -523,6 +650,7 @@ void Learner::PushSegmentBatch(const std::string& model_key, const tlg_segment_b
   }
   if (b.obs_dtype != g.ring_dtype)
     throw std::invalid_argument("PushSegmentBatch: observation format differs from the period's");
+  g.Flush();  // staged single pushes land first: this batch may reuse their slots
   if (b.obs_dtype == TLG_OBS_BITS && b.obs_pitch != 0 &&
       (b.obs_pitch < (b.obs_dim + 7) / 8 || b.obs_pitch > ((b.obs_dim + 7) / 8 + 15) / 16 * 16))
     throw std::invalid_argument("PushSegmentBatch: bad obs_pitch");
@@ -562,11 +690,9 @@ bool Learner::TrainStep() {
   auto segments = replay_.SampleBlocking(per_shard * config_.num_shards);
   if (segments.empty()) return false;
   gpu_->Pack(segments);
-  gpu_->stats.assign(config_.num_shards, tlg_step_stats{});
-  // Per-shard gradients, rank-ordered mean, optimizer: one device call.  Errors come
-  // back as the reference's exception types; on failure the parameters are unchanged.
-  Check(tlg_learner_train_step_shards(gpu_->h, gpu_->batches.data(), int(config_.num_shards),
-                                      /*on_device=*/0, gpu_->stats.data()));
+  // Per-shard gradients, rank-ordered mean, optimizer.  Errors come back as the
+  // reference's exception types; on failure the parameters are unchanged.
+  gpu_->Train();
   ++update_steps_;
   params_stale_ = true;
   if (config_.publish_interval > 0 && update_steps_ % config_.publish_interval == 0) Publish();
@@ -583,6 +709,7 @@ bool Learner::TrainStepDeviceReplay(std::size_t per_shard) {
     std::unique_lock dl(g.mu);
     g.cv.wait(dl, [&] { return g.shutting_down || replay_.size() >= n; });
     if (g.shutting_down) return false;
+    g.Flush();  // every live entry's observations are in HBM before the gather
     auto segments = replay_.SampleBlocking(n);  // cannot block: pushes are held off
     if (segments.empty()) return false;
     slots.reserve(n);

@@ -7,6 +7,8 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <filesystem>
+#include <cstdio>
 #include <functional>
 #include <limits>
 #include <memory>
@@ -23,6 +25,9 @@
 #include "tleague/pool/model_store.hpp"
 #include "tleague/rlmath/rlmath.hpp"
 #include "tleague/run/bench.hpp"
+#include "tleague/run/config.hpp"
+#include "tleague/run/local_run.hpp"
+#include "tleague/run/model_io.hpp"
 #include "tlg_b200.h"
 
 using namespace tleague;
@@ -659,6 +664,238 @@ TEST(a_rejected_push_leaves_the_device_replay_mirror_in_step) {
     CHECK(host.params().values == dev.params().values);
     CHECK(host.replay().consumed_steps() == dev.replay().consumed_steps());
   }
+}
+
+TEST(devices_spread_the_shards_over_gpus_like_local_shards) {
+  // LearnerConfig::devices: num_shards shards over G GPUs in this process (one host thread
+  // per device, NCCL allreduce in per-layer buckets).  With 2 ranks the NCCL sum a + b is
+  // the same fp32 operation as the single-GPU rank-ordered local sum, so parameters match
+  // the 2-local-shard learner bit for bit, step after step.
+  if (tlg_device_count() < 2) {
+    std::printf("  skipped: needs 2 GPUs\n");
+    return;
+  }
+  for (auto algo : {learner::Algo::kPpo, learner::Algo::kVtrace}) {
+    HyperParams hyper = TestHyper();
+    Rig rig_a(hyper), rig_b(hyper);
+    learner::LearnerConfig cfg;
+    cfg.num_shards = 2;
+    cfg.algo = algo;
+    cfg.publish_interval = 1;
+    cfg.seed = 11;
+    cfg.optimizer = learner::Optimizer::kAdam;
+    learner::LearnerConfig cfg2 = cfg;
+    cfg2.devices = {0, 1};
+    learner::Learner one(cfg, rig_a.league, rig_a.pool);
+    learner::Learner two(cfg2, rig_b.league, rig_b.pool);
+    std::mt19937_64 feed_a(8), feed_b(8);
+    std::uint64_t seq = 0;
+    for (int step = 0; step < 12; ++step) {
+      for (int i = 0; i < 8; ++i, ++seq) {
+        one.PushSegment(MakeSegment(one.current_key(), feed_a, seq));
+        two.PushSegment(MakeSegment(two.current_key(), feed_b, seq));
+      }
+      CHECK(one.TrainStep());
+      CHECK(two.TrainStep());
+      CHECK(one.params().values == two.params().values);
+    }
+  }
+  learner::LearnerConfig bad;
+  bad.num_shards = 3;
+  bad.devices = {0, 1};
+  Rig rig(TestHyper());
+  CHECK_THROWS_AS(learner::Learner(bad, rig.league, rig.pool), std::invalid_argument);
+}
+
+// ---------------------------------------------------------------------------
+// The MLP policy family registered at the reference's extension seam (wire tag 2,
+// integration/patches/mlp_family.py + integration/policy_mlp.cpp).
+namespace {
+const PolicyShape kGridMlp{50, 6, {256, 256}};  // grid_duel's obs/actions, 2x256 trunk
+
+league::LearnerGroupConfig MlpGroup(HyperParams hyper, PolicyShape shape) {
+  league::LearnerGroupConfig cfg;
+  cfg.family = PolicyFamily::kMlp;
+  cfg.shape = shape;
+  cfg.init_scale = 0.1;
+  cfg.hyper = hyper;
+  return cfg;
+}
+
+TrajectorySegment MakeSegmentD(const std::string& key, std::mt19937_64& rng, std::uint64_t seq,
+                               std::uint32_t D, std::uint32_t A, std::uint32_t T, bool binary) {
+  TrajectorySegment seg;
+  seg.model_key = key;
+  seg.segment_seq = seq;
+  seg.valid_steps = T - (seq % 5 == 2 ? 1 : 0);  // some ragged
+  seg.steps.resize(seg.valid_steps);
+  std::uniform_real_distribution<double> real(-1.0, 1.0);
+  std::normal_distribution<double> gauss(0.0, 1.0);
+  for (auto& step : seg.steps) {
+    step.obs.resize(D);
+    for (double& x : step.obs) x = binary ? double(rng() % 10 == 0) : double(float(gauss(rng)));
+    step.action = static_cast<std::uint32_t>(rng() % A);
+    step.reward = double(float(real(rng)));
+    step.behavior_logp = double(float(std::log(1.0 / A) + 0.1 * real(rng)));
+    step.value_est = double(float(real(rng)));
+  }
+  seg.bootstrap_value = double(float(real(rng)));
+  return seg;
+}
+}  // namespace
+
+TEST(mlp_family_learner_matches_the_fp64_reference_on_grid_duel_shape) {
+  // A league seeded with MLP blobs (InitParams of the registered family), the B200 learner
+  // training them through StartPeriod / PushSegment / TrainStep, against the reference's
+  // own fp64 rlmath losses back-propagated through policy::mlp; obs 50 is not a multiple
+  // of 4, so the device pads its rows internally.  Gaussian observations ship as fp32,
+  // 0/1 planes bit-packed (int8 layer-1 kernels).
+  for (bool binary : {false, true})
+    for (auto algo : {learner::Algo::kPpo, learner::Algo::kVtrace}) {
+      HyperParams hyper = TestHyper();
+      hyper.unroll_len = 5;
+      const bool vtrace = algo == learner::Algo::kVtrace;
+      pool::ModelStore store;
+      pool::DirectPool pool(store);
+      league::LeagueState league({MlpGroup(hyper, kGridMlp)}, pool, 42);
+      learner::LearnerConfig cfg;
+      cfg.num_shards = 2;
+      cfg.algo = algo;
+      cfg.publish_interval = 1;
+      cfg.seed = 99;
+      learner::Learner lrn(cfg, league, pool);
+      learner::ReplayMem oracle_replay(cfg.replay_capacity, hyper.max_reuse, cfg.seed);
+      ParamBlob oracle = store.Get(lrn.current_key())->params;
+      CHECK(oracle.family == PolicyFamily::kMlp);
+      CHECK(oracle.values.size() == policy::ParamCount(PolicyFamily::kMlp, kGridMlp));
+      CHECK(oracle == lrn.params());
+      std::mt19937_64 feed_a(2025), feed_b(2025);
+      std::uint64_t seq = 0;
+      const std::size_t draw = hyper.batch_size * 2;
+      double worst_all = 0;
+      for (int step = 0; step < 8; ++step) {
+        for (std::size_t i = 0; i < draw; ++i) {
+          lrn.PushSegment(MakeSegmentD(lrn.current_key(), feed_a, seq + i, 50, 6, 5, binary));
+          oracle_replay.Push(MakeSegmentD(lrn.current_key(), feed_b, seq + i, 50, 6, 5, binary));
+        }
+        seq += draw;
+        CHECK(lrn.TrainStep());
+        auto segs = oracle_replay.SampleBlocking(draw);
+        std::vector<double> avg(oracle.values.size(), 0.0);
+        for (int r = 0; r < 2; ++r) {
+          std::vector<TrajectorySegment> slice(segs.begin() + r * hyper.batch_size,
+                                               segs.begin() + (r + 1) * hyper.batch_size);
+          auto batch = OracleBatch(slice, vtrace, oracle, hyper);
+          auto res = vtrace ? rlmath::PgLossAndGrad(oracle, batch, hyper)
+                            : rlmath::PpoLossAndGrad(oracle, nullptr, batch, hyper);
+          for (std::size_t i = 0; i < avg.size(); ++i) avg[i] += res.grad[i];
+        }
+        for (double& g : avg) g *= 0.5;
+        oracle = rlmath::SgdStep(oracle, avg, hyper.learning_rate);
+        double worst = 0;
+        CHECK(AllClose(lrn.params().values, oracle.values, 1e-4, &worst));
+        worst_all = std::max(worst_all, worst);
+        CHECK(store.Get(lrn.current_key())->params.family == PolicyFamily::kMlp);
+      }
+      std::printf("  %s %s obs: 8 steps, worst Close() error vs fp64 reference %.2e\n",
+                  vtrace ? "vtrace" : "ppo", binary ? "0/1" : "gaussian", worst_all);
+    }
+}
+
+TEST(mlp_blobs_travel_as_wire_tag_2_and_serve_from_the_b200_infserver) {
+  // ParamBlob of family kMlp: codec round trip (model files are ParamPut frames,
+  // docs/protocol.md:91-93), remote == local GPU inference bit for bit, and within 1e-5 of
+  // the fp64 host family (what actors use for frozen MLP opponents, actor_loop.cpp:81-84).
+  ModelRecord rec;
+  rec.model_key = "mlp:0000";
+  rec.params = policy::InitParams(PolicyFamily::kMlp, kGridMlp, 0.1, 5);
+  for (double& v : rec.params.values) v = double(float(v));
+  const std::string path = "/tmp/tlg_dropin_mlp.model";
+  run::SaveModel(path, rec);
+  ModelRecord back = run::LoadModel(path);
+  CHECK(back.params == rec.params);
+  CHECK(back.params.shape.hidden == kGridMlp.hidden);
+  std::remove(path.c_str());
+  pool::ModelStore store;
+  pool::DirectPool pool(store);
+  pool.PutModel(rec);
+  infserver::InfServer server({"mlp:0000"}, pool, "127.0.0.1", 0);
+  infserver::InferenceClient client(server.endpoint());
+  std::mt19937_64 rng(3);
+  std::normal_distribution<double> n(0.0, 1.0);
+  double worst = 0;
+  for (int i = 0; i < 300; ++i) {
+    std::vector<double> obs(50);
+    for (double& x : obs) x = double(float(n(rng)));
+    auto reply = client.Infer(obs);
+    auto local = server.EvaluateLocal(obs);
+    CHECK(reply.logits == local.logits);
+    CHECK(reply.probs == local.probs);
+    auto ref = policy::Distribution(rec.params, obs);
+    double w1 = 0, w2 = 0;
+    CHECK(AllClose(reply.logits, ref.logits, 1e-5, &w1));
+    CHECK(AllClose(reply.probs, ref.probs, 1e-5, &w2));
+    CHECK(Close(reply.value, policy::ValueEstimate(rec.params, obs), 1e-5));
+    worst = std::max({worst, w1, w2});
+  }
+  std::printf("  MLP 50-256-256-(6,1): worst Close() error vs fp64 policy::mlp %.2e\n", worst);
+  server.Stop();
+}
+
+TEST(mlp_host_gradient_matches_central_finite_differences) {
+  // policy::mlp::AccumulateGrad in the reference's FD pattern (policy_test.cpp:144-194):
+  // d(c . logits + c_v * value)/d(theta) at h = 1e-6.
+  const PolicyShape shape{7, 4, {5, 6}};
+  ParamBlob p = policy::InitParams(PolicyFamily::kMlp, shape, 0.5, 11);
+  std::mt19937_64 rng(1);
+  std::normal_distribution<double> n(0.0, 1.0);
+  std::vector<double> obs(7), c(4);
+  for (double& x : obs) x = n(rng);
+  for (double& x : c) x = n(rng);
+  const double cv = 0.7;
+  auto f = [&](const ParamBlob& q) {
+    auto d = policy::Distribution(q, obs);
+    double s = cv * policy::ValueEstimate(q, obs);
+    for (int k = 0; k < 4; ++k) s += c[k] * d.logits[k];
+    return s;
+  };
+  std::vector<double> g(p.values.size(), 0.0);
+  policy::AccumulateGrad(p, obs, c, cv, g);
+  double worst = 0;
+  for (std::size_t i = 0; i < p.values.size(); ++i) {
+    ParamBlob a = p, b = p;
+    a.values[i] += 1e-6;
+    b.values[i] -= 1e-6;
+    const double fd = (f(a) - f(b)) / 2e-6;
+    worst = std::max(worst, std::abs(fd - g[i]) / std::max(1.0, std::abs(fd)));
+  }
+  CHECK(worst < 1e-5);
+  std::printf("  %zu parameters, worst FD error %.2e\n", p.values.size(), worst);
+}
+
+TEST(local_run_trains_an_mlp_league_on_grid_duel) {
+  // run::LocalRun (lockstep) on grid_duel with `family: mlp`: actors act with the MLP
+  // family against frozen MLP opponents, the B200 learner trains, frozen models are
+  // written as tag-2 model files.
+  const std::string text =
+      "env: grid_duel\nmode: lockstep\nalgo: ppo\nseed: 5\nperiods: 3\nperiod_steps: 4\n"
+      "publish_interval: 2\nactors: 2\nshards: 1\ninit_scale: 0.1\nfamily: mlp\n"
+      "hidden: 64,32\nbatch_size: 4\nunroll_len: 8\nlearning_rate: 0.01\n";
+  run::RunConfig cfg = run::ParseRunConfigText(text, "mlp.conf");
+  CHECK(cfg.groups.at(0).family == PolicyFamily::kMlp);
+  const std::string dir = "/tmp/tlg_dropin_mlp_run";
+  std::filesystem::remove_all(dir);
+  auto res = run::LocalRun(cfg, dir);
+  CHECK(res.frozen_keys.size() == 3);
+  for (const auto& key : res.frozen_keys) {
+    auto rec = run::LoadModel(dir + "/models/" + run::ModelFileName(key));
+    CHECK(rec.params.family == PolicyFamily::kMlp);
+    CHECK((rec.params.shape.hidden == std::vector<std::uint32_t>{64, 32}));
+    CHECK(rec.params.shape.obs_dim == 50);
+    CHECK(rec.frozen);
+  }
+  CHECK(!res.group_counters.empty() && res.group_counters[0].update_steps > 0);
+  std::filesystem::remove_all(dir);
 }
 
 TEST(reference_run_bench_runs_on_the_b200_learner) {

@@ -160,7 +160,7 @@ def check(rc):
 
 
 EXPORTS = [
-    "tlg_last_error", "tlg_version", "tlg_host_alloc", "tlg_host_free", "tlg_learner_create", "tlg_learner_destroy",
+    "tlg_last_error", "tlg_version", "tlg_device_count", "tlg_host_alloc", "tlg_host_free", "tlg_learner_create", "tlg_learner_destroy",
     "tlg_learner_param_count", "tlg_learner_set_params", "tlg_learner_get_params",
     "tlg_learner_set_teacher", "tlg_replay_create", "tlg_replay_destroy", "tlg_replay_put",
     "tlg_learner_train_step_replay",

@@ -75,6 +75,10 @@ void pin_nccl() {
 // Parameter layout of the three families (policy.cpp:23-27,78-104).
 struct Net {
   uint32_t family, D, A, L;
+  // GEMM row length of the observations: D rounded up to 4 floats (16-B rows for TMA).
+  // The flat parameters keep the reference layout [h_1 x D]; when D_pad != D the first
+  // trunk layer runs on zero-padded copies (obs rows, W_1) and its dW is compacted back.
+  uint32_t D_pad;
   std::vector<uint32_t> dims;
   std::vector<long> w_off, b_off;
   long P = 0;
@@ -87,6 +91,7 @@ struct Net {
     if (s.n_actions + 1 > 32) throw InvalidArg("n_actions > 31 is not supported on the GPU path");
     family = s.family;
     D = s.obs_dim;
+    D_pad = family == TLG_FAMILY_MLP ? (D + 3) / 4 * 4 : D;
     A = s.n_actions;
     L = family == TLG_FAMILY_MLP ? s.n_hidden : 0;
     if (L > 8) throw InvalidArg("at most 8 hidden layers");
@@ -95,8 +100,8 @@ struct Net {
     for (uint32_t l = 0; l < L; ++l) {
       const uint32_t h = s.hidden[l];
       if (h == 0) throw InvalidArg("hidden width must be positive");
-      if (h % 4 != 0 || dims.back() % 4 != 0)
-        throw InvalidArg("mlp widths (obs_dim and hidden) must be multiples of 4 on the GPU path");
+      if (h % 4 != 0)
+        throw InvalidArg("mlp hidden widths must be multiples of 4 on the GPU path");
       w_off.push_back(off);
       off += long(h) * dims.back();
       b_off.push_back(off);
@@ -123,7 +128,29 @@ struct Net {
     }
     P = off;
   }
+  bool padded() const { return L > 0 && D_pad != D; }
+  // K extent of trunk layer l's GEMMs (its input width, padded for layer 0)
+  int gin(uint32_t l) const { return l == 0 ? int(D_pad) : int(dims[l]); }
 };
+
+// Zero-padded copy of a row-major [rows x cols] matrix into [rows x cols_pad].
+__global__ void pad_rows_kernel(const float* __restrict__ src, long rows, int cols, int cols_pad,
+                                float* __restrict__ dst) {
+  const long n = rows * cols_pad;
+  for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n;
+       i += long(gridDim.x) * blockDim.x) {
+    const long r = i / cols_pad;
+    const int c = int(i - r * cols_pad);
+    dst[i] = c < cols ? src[r * cols + c] : 0.f;
+  }
+}
+
+void pad_rows(const float* src, long rows, int cols, int cols_pad, float* dst, cudaStream_t st) {
+  const long n = rows * cols_pad;
+  pad_rows_kernel<<<int(std::min<long>((n + 255) / 256, 148L * 8)), 256, 0, st>>>(src, rows, cols,
+                                                                               cols_pad, dst);
+  TLG_CHECK_LAUNCH();
+}
 
 template <typename T>
 T* dalloc(size_t n) {
@@ -167,6 +194,9 @@ struct tlg_learner {
   float grad_scale = 1.f;
   // batch
   float *obs, *obs_lo;
+  // net.padded(): observation rows, W_1 (student / teacher) and dW_1 at D_pad columns
+  float *obs_pad = nullptr, *w1p = nullptr, *w1p_lo = nullptr, *tw1p = nullptr,
+        *tw1p_lo = nullptr, *dw1p = nullptr;
   uint8_t* obs_u8;
   uint8_t* obs_bits;       // bit planes, row pitch bits_pitch (16-B aligned rows)
   long bits_pitch = 0;
@@ -281,7 +311,13 @@ struct tlg_learner {
     adam_t_dev = mem.add<uint64_t>(1);
     const long D = net.D;
     obs = mem.add<float>(F_max * D);
-    obs_lo = mem.add<float>(F_max * D);
+    obs_lo = mem.add<float>(F_max * long(net.D_pad));
+    if (net.padded()) {
+      obs_pad = mem.add<float>(F_max * long(net.D_pad));
+      w1p = mem.add<float>(long(net.dims[1]) * net.D_pad);
+      w1p_lo = mem.add<float>(long(net.dims[1]) * net.D_pad);
+      dw1p = mem.add<float>(long(net.dims[1]) * net.D_pad);
+    }
     obs_u8 = cfg.obs_dtype != TLG_OBS_F32 ? mem.add<uint8_t>(F_max * D + 16) : nullptr;
     bits_pitch = ((D + 7) / 8 + 15) / 16 * 16;
     obs_bits = cfg.obs_dtype != TLG_OBS_F32 ? mem.add<uint8_t>(F_max * bits_pitch + 16) : nullptr;
@@ -334,7 +370,7 @@ struct tlg_learner {
     ws_elems = 0;
     long max_cols = 1;
     for (uint32_t l = 0; l < net.L; ++l) {
-      const int out = int(net.dims[l + 1]), in = int(net.dims[l]);
+      const int out = int(net.dims[l + 1]), in = net.gin(l);
       const int sp = tlg::gemm::pick_splits(out, in, int(F_max), kMaxSplits);
       ws_elems = std::max(ws_elems, long(sp) * out * in);
       max_cols = std::max<long>(max_cols, out);
@@ -596,10 +632,14 @@ struct tlg_learner {
     // ---- forward trunk
     using tlg::gemm::Operand;
     for (uint32_t l = 0; l < net.L; ++l) {
-      const int in = int(net.dims[l]), outw = int(net.dims[l + 1]);
+      const int in = net.gin(l), outw = int(net.dims[l + 1]);
       Operand A{l == 0 ? x0 : act[l - 1], l == 0 ? x0_lo : act_lo[l - 1], in, false,
                 l == 0 ? x0_u8 : nullptr};
       Operand B{P + net.w_off[l], P_lo + net.w_off[l], in, false};
+      if (l == 0 && net.padded()) {  // the padded copy of this plane's W_1
+        B.hi = P == params ? w1p : tw1p;
+        B.lo = P == params ? w1p_lo : tw1p_lo;
+      }
       tlg::gemm::Params p{};
       p.out_hi = act[l];
       // the top layer's residual plane has no reader (heads and loss read the full plane)
@@ -621,8 +661,8 @@ struct tlg_learner {
       }
       if (l == 0 && sg.x0_bits != nullptr && wq_src != P) {
         // this step's layer-1 weights of plane P -> int8 pieces (once per step and plane)
-        tlg::gemm::launch_quantize_rows(P + net.w_off[0], outw, in, in, wq, wq_kp, wq_scale,
-                                        stream);
+        tlg::gemm::launch_quantize_rows(P + net.w_off[0], outw, int(net.D), int(net.D), wq, wq_kp,
+                                        wq_scale, stream);
         wq_src = P;
         ++launches;
       }
@@ -632,7 +672,8 @@ struct tlg_learner {
         // binary planes x int8 weight pieces: exact integer tensor-core GEMM (+ the
         // activations as int8 pieces when layer 2 takes the int8 path too)
         bn = tlg::gemm::launch_i8_bits_fwd(sg.x0_bits, bits_pitch, wq, wq_kp, wq_scale, p.bias,
-                                           int(F), outw, in, act[0], act_lo[0], outw, stream,
+                                           int(F), outw, int(net.D), act[0], act_lo[0], outw,
+                                           stream,
                                            i8_fwd2(F) ? act_q : nullptr).bn;
       } else if (l == 1 && sg.x0_bits != nullptr && i8_fwd2(F)) {
         tlg::gemm::launch_quantize_rows(P + net.w_off[1], outw, in, in, w2q, in, w2_scale,
@@ -724,21 +765,28 @@ struct tlg_learner {
         // dW_l = dZ_l^T . X_{l-1}   (K = frames, split-K partials reduced in fixed order)
         const float* xin = l == 0 ? x0 : act[l - 1];
         const float* xin_lo = l == 0 ? x0_lo : act_lo[l - 1];
-        int sp = tlg::gemm::pick_splits(outw, in, int(F), kMaxSplits);
-        while (long(sp) * outw * in > ws_elems && sp > 1) --sp;
+        const bool pad = l == 0 && net.padded();
+        const int gin = net.gin(uint32_t(l));
+        int sp = tlg::gemm::pick_splits(outw, gin, int(F), kMaxSplits);
+        while (long(sp) * outw * gin > ws_elems && sp > 1) --sp;
         Operand A{dz[l], dz_lo[l], outw, true};
         // layer 1 reads the uint8 planes directly (converted in smem, exact, no residual)
-        Operand B{xin, xin_lo, in, true, l == 0 ? x0_u8 : nullptr};
+        Operand B{xin, xin_lo, gin, true, l == 0 ? x0_u8 : nullptr};
         tlg::gemm::Params p{};
         p.ws = ws;
-        p.ws_split_stride = long(outw) * in;
+        p.ws_split_stride = long(outw) * gin;
         const int kb = (int(F) + tlg::gemm::kBK - 1) / tlg::gemm::kBK;
         const int per = (kb + sp - 1) / sp;
         const int sp_eff = (kb + per - 1) / per;  // launch() drops empty splits the same way
         if (shard == 0) kmark(1, l, 0);
-        tlg::gemm::launch(A, B, outw, in, int(F), tlg::gemm::kEpiStore, p, sp, stream);
+        tlg::gemm::launch(A, B, outw, gin, int(F), tlg::gemm::kEpiStore, p, sp, stream);
         if (shard == 0) kmark(1, l, 1);
-        tlg::launch_dw_reduce(ws, sp_eff, long(outw) * in, gtarget + net.w_off[l], stream);
+        tlg::launch_dw_reduce(ws, sp_eff, long(outw) * gin, pad ? dw1p : gtarget + net.w_off[l],
+                              stream);
+        if (pad)  // [h_1 x D_pad] -> the flat layout's [h_1 x D]
+          TLG_CUDA(cudaMemcpy2DAsync(gtarget + net.w_off[0], size_t(in) * 4, dw1p,
+                                     size_t(gin) * 4, size_t(in) * 4, size_t(outw),
+                                     cudaMemcpyDeviceToDevice, stream));
         launches += 2;
       }
       // W_l and b_l are contiguous in the flat layout: one bucket, allreduced while the
@@ -760,8 +808,15 @@ struct tlg_learner {
     const long F = long(bd.S) * T;
     const long D = net.D;
     const float* x0_lo = nullptr;
+    if (net.padded() && !(sg.x0_bits != nullptr && i8_dw1())) {
+      // observation rows at D_pad floats for the tf32 GEMMs that read them (pad columns
+      // stay zero from allocation); the int8 layer-1 kernels read the bit rows instead
+      TLG_CUDA(cudaMemcpy2DAsync(obs_pad, size_t(net.D_pad) * 4, x0, size_t(D) * 4,
+                                 size_t(D) * 4, size_t(F), cudaMemcpyDeviceToDevice, stream));
+      x0 = obs_pad;
+    }
     if (net.L > 0 && !obs_exact) {
-      tlg::launch_split_lo(x0, obs_lo, F * D, stream);
+      tlg::launch_split_lo(x0, obs_lo, F * long(net.gin(0)), stream);
       ++launches;
       x0_lo = obs_lo;
     }
@@ -1058,6 +1113,11 @@ struct tlg_learner {
                            int on_device = 0) {
     launches = 0;
     wq_src = nullptr;  // the parameters changed since the last step
+    if (net.padded()) {  // this step's W_1 planes at D_pad columns
+      pad_rows(params + net.w_off[0], net.dims[1], int(net.D), int(net.D_pad), w1p, stream);
+      pad_rows(params_lo + net.w_off[0], net.dims[1], int(net.D), int(net.D_pad), w1p_lo, stream);
+      launches += 2;
+    }
     overlap_active = nranks > 1 && n == 1 && !overlap_disabled;
     n_buckets = 0;
     pend_count = 0;
@@ -1285,6 +1345,13 @@ struct tlg_policy {
   DevFree mem;
   float *params, *params_lo, *obs, *obs_lo, *head_out, *head_part, *logits, *probs, *value;
   std::vector<float*> act, act_lo;
+  // net.padded(): observation rows and W_1 at D_pad columns (see Net)
+  float *obs_pad = nullptr, *w1p = nullptr, *w1p_lo = nullptr;
+  void pad_w1() {
+    if (!net.padded()) return;
+    pad_rows(params + net.w_off[0], net.dims[1], int(net.D), int(net.D_pad), w1p, stream);
+    pad_rows(params_lo + net.w_off[0], net.dims[1], int(net.D), int(net.D_pad), w1p_lo, stream);
+  }
   int* err;
   long P_pad;
   int head_tiles = 1;
@@ -1297,7 +1364,12 @@ struct tlg_policy {
     params = mem.add<float>(P_pad);
     params_lo = mem.add<float>(P_pad);
     obs = mem.add<float>(mb * net.D);
-    obs_lo = mem.add<float>(mb * net.D);
+    obs_lo = mem.add<float>(mb * net.D_pad);
+    if (net.padded()) {
+      obs_pad = mem.add<float>(mb * net.D_pad);
+      w1p = mem.add<float>(long(net.dims[1]) * net.D_pad);
+      w1p_lo = mem.add<float>(long(net.dims[1]) * net.D_pad);
+    }
     head_out = mem.add<float>(mb * (net.A + 1));
     head_part = mem.add<float>(mb * (net.A + 1) * ((net.head.H + 63) / 64));
     logits = mem.add<float>(mb * net.A);
@@ -1344,7 +1416,16 @@ void set_params_common(float* params, float* params_lo, long P, long P_pad, cons
 extern "C" {
 
 const char* tlg_last_error(void) { return g_err.c_str(); }
-const char* tlg_version(void) { return "tlg_b200 0.1 (sm_100a, tcgen05 3xTF32)"; }
+const char* tlg_version(void) { return "tlg_b200 0.2 (sm_100a, tcgen05 3xTF32 / int8)"; }
+
+int tlg_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
 
 void* tlg_host_alloc(size_t bytes) {
   void* p = nullptr;
@@ -1395,6 +1476,17 @@ int tlg_learner_set_teacher(tlg_learner* l, const double* values, size_t n) {
         l->t_head_out = l->mem.add<float>(l->F_max * (l->net.A + 1));
       }
       set_params_common(l->teacher, l->teacher_lo, l->net.P, l->P_pad, values, n, l->stream);
+      if (l->net.padded()) {
+        const long n1 = long(l->net.dims[1]) * l->net.D_pad;
+        if (!l->tw1p) {
+          l->tw1p = l->mem.add<float>(n1);
+          l->tw1p_lo = l->mem.add<float>(n1);
+        }
+        pad_rows(l->teacher + l->net.w_off[0], l->net.dims[1], int(l->net.D), int(l->net.D_pad),
+                 l->tw1p, l->stream);
+        pad_rows(l->teacher_lo + l->net.w_off[0], l->net.dims[1], int(l->net.D),
+                 int(l->net.D_pad), l->tw1p_lo, l->stream);
+      }
       TLG_CUDA(cudaStreamSynchronize(l->stream));
       l->has_teacher = true;
     }
@@ -1756,6 +1848,8 @@ int tlg_policy_set_params(tlg_policy* p, const double* values, size_t n) {
   return Guard([&] {
     TLG_CUDA(cudaSetDevice(p->device));
     set_params_common(p->params, p->params_lo, p->net.P, p->P_pad, values, n, p->stream);
+    p->pad_w1();
+    TLG_CUDA(cudaStreamSynchronize(p->stream));
   });
 }
 
@@ -1787,6 +1881,8 @@ int tlg_policy_set_params_from_learner(tlg_policy* p, tlg_learner* l) {
       TLG_CUDA(cudaMemcpyPeerAsync(p->params_lo, p->device, l->params_lo, int(l->cfg.device),
                                    bytes, p->stream));
     }
+    TLG_CUDA(cudaSetDevice(p->device));
+    p->pad_w1();
     TLG_CUDA(cudaEventRecord(ev_p, p->stream));
     TLG_CUDA(cudaSetDevice(l->cfg.device));
     TLG_CUDA(cudaStreamWaitEvent(l->stream, ev_p, 0));
@@ -1808,15 +1904,24 @@ int tlg_policy_forward(tlg_policy* p, const float* obs, size_t n, float* logits,
       x0 = p->obs;
     }
     const float* x0_lo = nullptr;
+    if (p->net.padded()) {
+      TLG_CUDA(cudaMemcpy2DAsync(p->obs_pad, size_t(p->net.D_pad) * 4, x0, size_t(D) * 4,
+                                 size_t(D) * 4, n, cudaMemcpyDeviceToDevice, p->stream));
+      x0 = p->obs_pad;
+    }
     if (p->net.L > 0) {
-      tlg::launch_split_lo(x0, p->obs_lo, long(n) * D, p->stream);
+      tlg::launch_split_lo(x0, p->obs_lo, long(n) * p->net.gin(0), p->stream);
       x0_lo = p->obs_lo;
     }
     using tlg::gemm::Operand;
     for (uint32_t l = 0; l < p->net.L; ++l) {
-      const int in = int(p->net.dims[l]), outw = int(p->net.dims[l + 1]);
+      const int in = p->net.gin(l), outw = int(p->net.dims[l + 1]);
       Operand Aop{l == 0 ? x0 : p->act[l - 1], l == 0 ? x0_lo : p->act_lo[l - 1], in, false};
       Operand Bop{p->params + p->net.w_off[l], p->params_lo + p->net.w_off[l], in, false};
+      if (l == 0 && p->net.padded()) {
+        Bop.hi = p->w1p;
+        Bop.lo = p->w1p_lo;
+      }
       tlg::gemm::Params gp{};
       gp.out_hi = p->act[l];
       gp.out_lo = l + 1 == p->net.L ? nullptr : p->act_lo[l];

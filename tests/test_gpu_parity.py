@@ -128,6 +128,8 @@ CASES = [
     ("mlp", 16, 6, (32, 32), 8, 12),
     ("mlp", 64, 6, (256, 256), 32, 8),
     ("mlp", 36, 5, (64,), 5, 20),
+    ("mlp", 50, 6, (64, 32), 7, 9),    # grid_duel's obs 50: rows padded to 52 internally
+    ("mlp", 13, 3, (16, 8, 12), 4, 6),  # odd obs, 3 trunk layers
     ("linear", 10, 4, (), 6, 10),
     ("tabular", 5, 3, (), 4, 16),
 ]
@@ -275,6 +277,7 @@ def test_action_out_of_range_and_tabular_one_hot(tlg, oracle):
 
 # ---------------------------------------------------------------------------
 @pytest.mark.parametrize("case", [("mlp", 64, 6, (1024, 1024)), ("mlp", 36, 5, (64, 32)),
+                                  ("mlp", 50, 6, (64, 64)), ("mlp", 7, 3, (8,)),
                                   ("linear", 9, 4, ()), ("tabular", 6, 3, ())],
                          ids=lambda c: c[0] + "-" + str(c[1]))
 def test_policy_forward_matches_oracle_and_is_batch_invariant(tlg, oracle, case):
@@ -485,8 +488,9 @@ def test_bit_packed_and_staged_inputs_match(tlg, oracle, D, hidden):
 
 @pytest.mark.parametrize("fused_loss", [False, True], ids=["", "fused-loss"])
 @pytest.mark.parametrize("optimizer", ["sgd", "adam"])
-@pytest.mark.parametrize("shape_case", [(1936, (256, 256), 32, 16), (200, (64, 32), 8, 24)],
-                         ids=["c3-like", "small"])
+@pytest.mark.parametrize("shape_case", [(1936, (256, 256), 32, 16), (200, (64, 32), 8, 24),
+                                        (50, (64, 32), 8, 12), (50, (36, 32), 8, 12)],
+                         ids=["c3-like", "small", "obs50", "obs50-tf32dw"])
 def test_bit_planes_int8_layer1_match_oracle(tlg, oracle, shape_case, optimizer, fused_loss,
                                             monkeypatch):
     """Bit-packed binary planes: layer 1 runs on the int8 tensor cores (fixed-point
