@@ -38,7 +38,7 @@ def test_version_and_no_device_error(L):
     assert b"sm_100a" in L.tlg_version()
     from paper_2011_12895_b200._capi import LearnerConfig, PolicyShape
     cfg = LearnerConfig(0, 1, 0.9, 0.999, 1e-8, 4, 3, 0, 0, 0)
-    shape = PolicyShape.make("mlp", 3, 2, (8,))  # obs_dim not a multiple of 4
+    shape = PolicyShape.make("mlp", 3, 2, (6,))  # hidden width not a multiple of 4
     h = C.c_void_p()
     rc = L.tlg_learner_create(C.byref(cfg), C.byref(shape), C.byref(h))
     assert rc == 1  # TLG_INVALID_ARGUMENT raised before any device work
