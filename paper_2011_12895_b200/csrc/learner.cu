@@ -375,7 +375,7 @@ struct tlg_learner {
       ws_elems = std::max(ws_elems, long(sp) * out * in);
       max_cols = std::max<long>(max_cols, out);
     }
-    if (dzq) ws_elems = std::max(ws_elems, long(kMaxI8Splits) * net.dims[1] * net.D);
+    if (dzq) ws_elems = std::max(ws_elems, long(kMaxI8Splits) * net.dims[1] * net.D_pad);
     ws = ws_elems ? mem.add<float>(ws_elems) : nullptr;
     // rows: the loss kernel's blocks, or one per persistent GEMM CTA (the dX epilogue's
     // fused column sums), whichever is more
@@ -755,11 +755,18 @@ struct tlg_learner {
         i8_dw_plan(F, sp_i8, kbps);
         tlg::gemm::launch_quantize_cols(dz[0], F, outw, outw, colmax, long(kbps) * 128, dzq,
                                         stream);
+        // N = D_pad: the bit rows are zero past obs_dim, so the pad columns come out zero
+        const int gin = net.gin(0);
         if (shard == 0) kmark(1, l, 0);
-        tlg::gemm::launch_i8_bits_dw(dzq, sg.x0_bits, bits_pitch, colmax, outw, in, int(F), kbps,
+        tlg::gemm::launch_i8_bits_dw(dzq, sg.x0_bits, bits_pitch, colmax, outw, gin, int(F), kbps,
                                      ws, stream);
         if (shard == 0) kmark(1, l, 1);
-        tlg::launch_dw_reduce(ws, sp_i8, long(outw) * in, gtarget + net.w_off[0], stream);
+        tlg::launch_dw_reduce(ws, sp_i8, long(outw) * gin,
+                              net.padded() ? dw1p : gtarget + net.w_off[0], stream);
+        if (net.padded())  // [h_1 x D_pad] -> the flat layout's [h_1 x D]
+          TLG_CUDA(cudaMemcpy2DAsync(gtarget + net.w_off[0], size_t(in) * 4, dw1p,
+                                     size_t(gin) * 4, size_t(in) * 4, size_t(outw),
+                                     cudaMemcpyDeviceToDevice, stream));
         launches += 3;
       } else {
         // dW_l = dZ_l^T . X_{l-1}   (K = frames, split-K partials reduced in fixed order)
@@ -986,7 +993,16 @@ struct tlg_learner {
         gr.exec = nullptr;
         cudaGraph_t g;
         TLG_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
-        enqueue_device_step(&sg, 1);
+        try {
+          enqueue_device_step(&sg, 1);
+        } catch (...) {
+          // leave the stream usable: end (and drop) the partial capture before reporting
+          cudaGraph_t partial = nullptr;
+          cudaStreamEndCapture(stream, &partial);
+          if (partial) cudaGraphDestroy(partial);
+          cudaGetLastError();
+          throw;
+        }
         TLG_CUDA(cudaStreamEndCapture(stream, &g));
         TLG_CUDA(cudaGraphInstantiate(&gr.exec, g, 0));
         cudaGraphDestroy(g);
