@@ -360,13 +360,13 @@ LaunchInfo launch_i8_bits_fwd(const uint8_t* bits, long rowb, const int8_t* q, l
     mc = cg == 2 && std::atoi(e) == 2 && M >= 4 * kBM ? 2 : 1;
   if (out_q != nullptr && (N % 32 != 0 || (reinterpret_cast<uintptr_t>(out_q) & 15) != 0))
     throw CudaError("gemm_i8: int8 activation pieces need N % 32 == 0 and 16-B alignment");
-  I8Params p{M, N, K, scale, bias, N, out_q};
+  I8Params p{M, N, K, scale, bias, N, out_q, out_lo != nullptr ? 1 : 0};
   const TileMap tm{ceil_div(M, kBM * cg * mc), ceil_div(N, BN), 1};
   // bit rows: box {16 bytes = 128 elements, 128 rows}; pieces: box {128, BN / cg}, SW128
   const CUtensorMap tb = make_bytes_map(bits, rowb, M, rowb, kBKi / 8, kBM, CU_TENSOR_MAP_SWIZZLE_NONE);
   const CUtensorMap tq = make_bytes_map(q, Kp, 3L * N, Kp, kBKi, BN / cg, CU_TENSOR_MAP_SWIZZLE_128B);
   const CUtensorMap to = make_f32_out_map(out, N, M, ldo);
-  const CUtensorMap tl = make_f32_out_map(out_lo, N, M, ldo);
+  const CUtensorMap tl = out_lo ? make_f32_out_map(out_lo, N, M, ldo) : CUtensorMap{};
   if (mc == 2) run_i8_fwd<BN, 2, 2>(tb, tq, to, tl, p, tm, stream);
   else if (cg == 2) run_i8_fwd<BN, 2>(tb, tq, to, tl, p, tm, stream);
   else run_i8_fwd<BN, 1>(tb, tq, to, tl, p, tm, stream);

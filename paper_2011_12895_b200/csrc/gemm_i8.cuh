@@ -42,6 +42,7 @@ struct I8Params {
   const float* bias;   // [N]
   long q_rows;         // rows per piece in the stacked [3][q_rows][Kp] piece array
   int8_t* out_q;       // optional: tanh outputs as int8 pieces [3][M][N] (scale 1/127)
+  int write_lo;        // store the tf32 residual plane (0: the consumers derive it)
 };
 
 // tanh output o in (-1, 1) -> three int8 pieces of o * 127 (fixed scale 1/127), packed
@@ -421,16 +422,16 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
         for (int j4 = 0; j4 < 8; ++j4) {
           *reinterpret_cast<float4*>(blk_ptr + swz(lane, j4)) =
               make_float4(o[4 * j4], o[4 * j4 + 1], o[4 * j4 + 2], o[4 * j4 + 3]);
-          *reinterpret_cast<float4*>(blk_ptr + 4096 + swz(lane, j4)) =
-              make_float4(o[4 * j4] - tf32_hi(o[4 * j4]), o[4 * j4 + 1] - tf32_hi(o[4 * j4 + 1]),
-                          o[4 * j4 + 2] - tf32_hi(o[4 * j4 + 2]),
-                          o[4 * j4 + 3] - tf32_hi(o[4 * j4 + 3]));
+          if (p.write_lo)
+            *reinterpret_cast<float4*>(blk_ptr + 4096 + swz(lane, j4)) = make_float4(
+                o[4 * j4] - tf32_hi(o[4 * j4]), o[4 * j4 + 1] - tf32_hi(o[4 * j4 + 1]),
+                o[4 * j4 + 2] - tf32_hi(o[4 * j4 + 2]), o[4 * j4 + 3] - tf32_hi(o[4 * j4 + 3]));
         }
         fence_async_smem();
         __syncwarp();
         if (lane == 0) {
           tma_store_2d(&tmOut, nb, rbase, blk);
-          tma_store_2d(&tmOutLo, nb, rbase, blk + 4096);
+          if (p.write_lo) tma_store_2d(&tmOutLo, nb, rbase, blk + 4096);
           bulk_commit();
         }
       }

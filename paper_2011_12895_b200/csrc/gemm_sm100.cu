@@ -105,24 +105,26 @@ struct EpiMaps {
   CUtensorMap out, out_lo, act;
 };
 
-template <int BN, bool A_MN, bool B_MN, bool A_LO, bool B_LO, int EPI, int U8 = 0, int CG = 1>
+template <int BN, bool A_MN, bool B_MN, bool A_LO, bool B_LO, int EPI, int U8 = 0, int CG = 1,
+          int LOD = 0>
 void run(const CUtensorMap& ah, const CUtensorMap& al, const CUtensorMap& bh,
          const CUtensorMap& bl, const EpiMaps& em, const Params& p, dim3 grid,
          cudaStream_t stream) {
-  auto kern = gemm_tf32x3_kernel<BN, A_MN, B_MN, A_LO, B_LO, EPI, U8, CG>;
-  constexpr int bytes = Smem<BN, A_LO, B_LO, EPI, U8, CG>::kBytes;
+  auto kern = gemm_tf32x3_kernel<BN, A_MN, B_MN, A_LO, B_LO, EPI, U8, CG, LOD>;
+  constexpr int bytes = Smem<BN, A_LO, B_LO, EPI, U8, CG, LOD>::kBytes;
+  constexpr int threads = (U8 || LOD) ? kThreadsU8 : kThreads;
   static_assert(bytes <= 227 * 1024, "shared memory budget");
   static std::atomic<unsigned long long> attr{0};  // per device
   ensure_smem_attr(kern, bytes, attr);
   const TileMap tm{int(grid.x), int(grid.y), int(grid.z)};  // grid.x counts (128*CG)-row tiles
   const int tiles = tm.m_tiles * tm.n_tiles * tm.splits;
   if (CG == 1) {
-    kern<<<std::min(tiles, num_sms()), U8 ? kThreadsU8 : kThreads, bytes, stream>>>(
+    kern<<<std::min(tiles, num_sms()), threads, bytes, stream>>>(
         ah, al, bh, bl, em.out, em.out_lo, em.act, p, tm);
   } else {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(2 * std::min(tiles, num_sms() / 2));
-    cfg.blockDim = dim3(U8 ? kThreadsU8 : kThreads);
+    cfg.blockDim = dim3(threads);
     cfg.dynamicSmemBytes = bytes;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
@@ -137,26 +139,41 @@ void run(const CUtensorMap& ah, const CUtensorMap& al, const CUtensorMap& bh,
   TLG_CHECK_LAUNCH();
 }
 
-template <int BN, bool A_MN, bool B_MN, bool A_LO, bool B_LO, int EPI, int U8 = 0>
+template <int BN, bool A_MN, bool B_MN, bool A_LO, bool B_LO, int EPI, int U8 = 0, int LOD = 0>
 void run_if_fits(const CUtensorMap& ah, const CUtensorMap& al, const CUtensorMap& bh,
                  const CUtensorMap& bl, const EpiMaps& em, const Params& p, dim3 grid,
                  cudaStream_t s) {
   if (g_cg == 2) {
-    if constexpr (Smem<BN, A_LO, B_LO, EPI, U8, 2>::kFits && BN >= 128)
-      return run<BN, A_MN, B_MN, A_LO, B_LO, EPI, U8, 2>(ah, al, bh, bl, em, p, grid, s);
+    if constexpr (Smem<BN, A_LO, B_LO, EPI, U8, 2, LOD>::kFits && BN >= 128)
+      return run<BN, A_MN, B_MN, A_LO, B_LO, EPI, U8, 2, LOD>(ah, al, bh, bl, em, p, grid, s);
     throw CudaError("gemm: pair tile does not fit shared memory");
   }
-  if constexpr (Smem<BN, A_LO, B_LO, EPI, U8>::kFits)
-    run<BN, A_MN, B_MN, A_LO, B_LO, EPI, U8>(ah, al, bh, bl, em, p, grid, s);
+  if constexpr (Smem<BN, A_LO, B_LO, EPI, U8, 1, LOD>::kFits)
+    run<BN, A_MN, B_MN, A_LO, B_LO, EPI, U8, 1, LOD>(ah, al, bh, bl, em, p, grid, s);
   else
     throw CudaError("gemm: tile does not fit shared memory");
 }
 
 template <int BN>
-void dispatch_bn(bool a_mn, bool b_mn, bool a_lo, bool b_lo, int epi, int u8,
+void dispatch_bn(bool a_mn, bool b_mn, bool a_lo, bool b_lo, int epi, int u8, int lod,
                  const CUtensorMap& ah, const CUtensorMap& al, const CUtensorMap& bh,
                  const CUtensorMap& bl, const EpiMaps& em, const Params& p, dim3 grid,
                  cudaStream_t s) {
+  // derived lo planes (Operand::lo_smem): the learner's activations / dZ / observations
+  if (lod) {
+    if (u8) throw CudaError("gemm: derived lo planes need fp32 operands");
+    if (!a_mn && !b_mn && a_lo && b_lo && epi == kEpiFwdTanh && lod == 1)
+      return run_if_fits<BN, false, false, true, true, kEpiFwdTanh, 0, 1>(ah, al, bh, bl, em, p, grid, s);
+    if (!a_mn && !b_mn && a_lo && b_lo && epi == kEpiFwdLoss && lod == 1)
+      return run_if_fits<BN, false, false, true, true, kEpiFwdLoss, 0, 1>(ah, al, bh, bl, em, p, grid, s);
+    if (!a_mn && b_mn && a_lo && b_lo && epi == kEpiBwdTanh && lod == 1)
+      return run_if_fits<BN, false, true, true, true, kEpiBwdTanh, 0, 1>(ah, al, bh, bl, em, p, grid, s);
+    if (a_mn && b_mn && a_lo && b_lo && epi == kEpiStore && lod == 3)
+      return run_if_fits<BN, true, true, true, true, kEpiStore, 0, 3>(ah, al, bh, bl, em, p, grid, s);
+    if (a_mn && b_mn && a_lo && !b_lo && epi == kEpiStore && lod == 1)
+      return run_if_fits<BN, true, true, true, false, kEpiStore, 0, 1>(ah, al, bh, bl, em, p, grid, s);
+    throw CudaError("gemm: unsupported derived-lo operand combination");
+  }
   // uint8 observation planes: forward (A = obs) and dW of layer 1 (B = obs)
   if (u8 == 1 && !a_mn && !b_mn && b_lo && epi == kEpiFwdTanh)
     return run_if_fits<BN, false, false, false, true, kEpiFwdTanh, 1>(ah, al, bh, bl, em, p, grid, s);
@@ -227,7 +244,9 @@ int pick_splits(int M, int N, int K, int max_splits) {
 LaunchInfo launch(const Operand& A, const Operand& B, int M, int N, int K, int epi, Params p,
                   int splits, cudaStream_t stream) {
   if (M <= 0 || N <= 0 || K <= 0) throw CudaError("gemm: empty problem");
-  const bool a_lo0 = A.lo != nullptr && !A.u8, b_lo0 = B.lo != nullptr && !B.u8;
+  const bool a_lo0 = (A.lo != nullptr || A.lo_smem) && !A.u8,
+             b_lo0 = (B.lo != nullptr || B.lo_smem) && !B.u8;
+  const int lod = (A.lo_smem && !A.u8 ? 1 : 0) | (B.lo_smem && !B.u8 ? 2 : 0);
   const int u8_0 = A.u8 ? 1 : B.u8 ? 2 : 0;
   if (epi == kEpiBwdTanh && p.colsum != nullptr && N > kColMax)
     throw CudaError("gemm: fused column sums need N <= 2048");
@@ -267,7 +286,7 @@ LaunchInfo launch(const Operand& A, const Operand& B, int M, int N, int K, int e
     if (const char* e = std::getenv("TLG_GEMM_CG_U8"))  // tuning experiments only
       if ((A.u8 || B.u8) && std::atoi(e) == 2 && BN >= 128) cg = 2;
     if (BN == 64 || epi == kEpiFwdLoss ||
-        smem_plan(BN, a_lo0, b_lo0, epi, u8_0, cg).bytes <= 227 * 1024)
+        smem_plan(BN, a_lo0, b_lo0, epi, u8_0, cg, lod).bytes <= 227 * 1024)
       break;
     BN /= 2;
   }
@@ -275,13 +294,13 @@ LaunchInfo launch(const Operand& A, const Operand& B, int M, int N, int K, int e
   if (A.u8 && (A.mn_major || A.ld % 16)) throw CudaError("gemm: uint8 A must be K-major, ld % 16 == 0");
   if (B.u8 && (!B.mn_major || B.ld % 16)) throw CudaError("gemm: uint8 B must be MN-major, ld % 16 == 0");
   const CUtensorMap ah = A.u8 ? make_u8_map(A.u8, K, M, A.ld, 32, kBM) : operand_map(A.hi, A, M, K, kBM);
-  const CUtensorMap al = operand_map(A.lo, A, M, K, kBM);
+  const CUtensorMap al = operand_map(A.lo_smem ? nullptr : A.lo, A, M, K, kBM);
   const CUtensorMap bh = B.u8 ? make_u8_map(B.u8, N, K, B.ld, BN / cg, 32)
                               : operand_map(B.hi, B, N, K, BN / cg);
-  const CUtensorMap bl = operand_map(B.lo, B, N, K, BN / cg);
+  const CUtensorMap bl = operand_map(B.lo_smem ? nullptr : B.lo, B, N, K, BN / cg);
   dim3 grid(ceil_div(M, kBM * cg), ceil_div(N, BN), splits);
   g_cg = cg;
-  const bool a_lo = A.lo != nullptr && !A.u8, b_lo = B.lo != nullptr && !B.u8;
+  const bool a_lo = a_lo0, b_lo = b_lo0;
   // epilogue maps: 32x32 fp32 blocks with the 128-B swizzle
   EpiMaps em;
   std::memset(&em, 0, sizeof(em));
@@ -294,9 +313,9 @@ LaunchInfo launch(const Operand& A, const Operand& B, int M, int N, int K, int e
     if (A.u8 && p.a_expand) em.act = make_map(p.a_expand, K, M, A.ld, kBM, CU_TENSOR_MAP_SWIZZLE_128B);
   }
   switch (BN) {
-    case 256: dispatch_bn<256>(A.mn_major, B.mn_major, a_lo, b_lo, epi, u8, ah, al, bh, bl, em, p, grid, stream); break;
-    case 128: dispatch_bn<128>(A.mn_major, B.mn_major, a_lo, b_lo, epi, u8, ah, al, bh, bl, em, p, grid, stream); break;
-    default: dispatch_bn<64>(A.mn_major, B.mn_major, a_lo, b_lo, epi, u8, ah, al, bh, bl, em, p, grid, stream); break;
+    case 256: dispatch_bn<256>(A.mn_major, B.mn_major, a_lo, b_lo, epi, u8, lod, ah, al, bh, bl, em, p, grid, stream); break;
+    case 128: dispatch_bn<128>(A.mn_major, B.mn_major, a_lo, b_lo, epi, u8, lod, ah, al, bh, bl, em, p, grid, stream); break;
+    default: dispatch_bn<64>(A.mn_major, B.mn_major, a_lo, b_lo, epi, u8, lod, ah, al, bh, bl, em, p, grid, stream); break;
   }
   const int tiles = int(grid.x * grid.y * grid.z);
   return {BN, cg == 2 ? 2 * std::min(tiles, num_sms() / 2) : std::min(tiles, num_sms())};

@@ -274,12 +274,16 @@ constexpr int plan_stages(int stage, int epi_bytes, int ring_bytes) {
   const int b = (225 * 1024 - epi_bytes - ring_bytes - 1024 - 256) / stage;
   return b < 2 ? 2 : b > 8 ? 8 : b;
 }
-constexpr SmemPlan smem_plan(int BN, bool a_lo, bool b_lo, int epi, int u8, int cg) {
+// lod: bit 0 / bit 1 = the lo plane of A / B is derived in shared memory from the hi tile
+// (lo = x - trunc_tf32(x), elementwise, so any swizzled layout) by the converter warps
+// instead of being TMA-loaded from a residual plane in HBM.
+constexpr SmemPlan smem_plan(int BN, bool a_lo, bool b_lo, int epi, int u8, int cg, int lod = 0) {
   SmemPlan q{};
   const int kA = kBM * kBK * 4;          // 16 KB
   const int kB = (BN / cg) * kBK * 4;    // B rows held by this CTA (a pair splits N)
   q.stage = kA * (a_lo ? 2 : 1) + kB * (b_lo ? 2 : 1);
-  q.tma_bytes = q.stage - (u8 == 1 ? kA : u8 == 2 ? kB : 0);
+  q.tma_bytes = q.stage - (u8 == 1 ? kA : u8 == 2 ? kB : 0) - ((lod & 1) ? kA : 0) -
+                ((lod & 2) ? kB : 0);
   // a uint8 operand's byte tiles stream through their own ring (u8_ring slots), filled
   // by the producer up to u8_ring k-blocks ahead of the fp32 stages, so only the
   // conversion itself sits on the MMA's critical path.
@@ -308,7 +312,8 @@ constexpr SmemPlan smem_plan(int BN, bool a_lo, bool b_lo, int epi, int u8, int 
   q.bar_off = q.ring_off + ring;
   // full/empty per stage, tmem full/empty x2, act-block full x4, converted per stage,
   // u8 ring full/empty per slot
-  q.num_bars = 2 * q.stages + 4 + kEpiWarps + (u8 ? q.stages + 2 * q.u8_ring : 0);
+  q.num_bars = 2 * q.stages + 4 + kEpiWarps + (u8 ? q.stages + 2 * q.u8_ring : 0) +
+               (lod ? 2 * q.stages : 0);  // lod: converted + local hi-landed per stage
   q.epi_off = (q.bar_off + q.num_bars * 8 + 16 + 1023) / 1024 * 1024;
   q.bytes = q.epi_off + kEpiWarps * q.warp_epi + q.extra + 1024;  // + 1 KB alignment slack
   return q;
@@ -317,9 +322,9 @@ constexpr SmemPlan smem_plan(int BN, bool a_lo, bool b_lo, int epi, int u8, int 
 // U8: 0 = fp32 operands; 1 = A arrives as uint8 planes (K-major); 2 = B arrives as uint8
 // planes (MN-major).  A uint8 operand is TMA-loaded into a byte staging tile and expanded
 // to fp32 in the MMA's swizzled layout by 4 converter warps (exact: 0..255).
-template <int BN, bool A_LO, bool B_LO, int EPI, int U8 = 0, int CG = 1>
+template <int BN, bool A_LO, bool B_LO, int EPI, int U8 = 0, int CG = 1, int LOD = 0>
 struct Smem {
-  static constexpr SmemPlan P = smem_plan(BN, A_LO, B_LO, EPI, U8, CG);
+  static constexpr SmemPlan P = smem_plan(BN, A_LO, B_LO, EPI, U8, CG, LOD);
   static constexpr int kA = kBM * kBK * 4;
   static constexpr int kBN = BN / CG;
   static constexpr int kB = kBN * kBK * 4;
@@ -425,8 +430,8 @@ __device__ __forceinline__ float4 u8x4_to_f32(uint32_t v) {
 // byte offset of element (row r, col c) in a 32x32 fp32 block with the 128-B TMA swizzle
 __device__ __forceinline__ uint32_t swz(int r, int c4) { return uint32_t(r * 128 + ((c4 ^ (r & 7)) << 4)); }
 
-template <int BN, bool A_MN, bool B_MN, bool A_LO, bool B_LO, int EPI, int U8, int CG>
-__global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
+template <int BN, bool A_MN, bool B_MN, bool A_LO, bool B_LO, int EPI, int U8, int CG, int LOD>
+__global__ void __launch_bounds__((U8 || LOD) ? kThreadsU8 : kThreads, 1)
     gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap tmA_hi,
                        const __grid_constant__ CUtensorMap tmA_lo,
                        const __grid_constant__ CUtensorMap tmB_hi,
@@ -435,7 +440,10 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
                        const __grid_constant__ CUtensorMap tmOutLo,
                        const __grid_constant__ CUtensorMap tmAct, const Params p,
                        const TileMap tm) {
-  using S = Smem<BN, A_LO, B_LO, EPI, U8, CG>;
+  using S = Smem<BN, A_LO, B_LO, EPI, U8, CG, LOD>;
+  static_assert(!(U8 && LOD), "derived lo planes and uint8 operands do not mix");
+  static_assert(!(LOD & 1) || A_LO, "A lo derived needs the A lo slot");
+  static_assert(!(LOD & 2) || B_LO, "B lo derived needs the B lo slot");
   // CG == 2: a cluster of two CTAs shares each (256 x BN) tile; rank r owns rows
   // [128 r, 128 r + 128) of A / D and B rows [r BN/2, (r+1) BN/2).  Only rank 0 issues
   // the MMAs (cta_group::2), reading both CTAs' smem and writing both CTAs' TMEM.
@@ -456,6 +464,7 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
   const uint32_t bar_conv = bar_act + 8 * kEpiWarps;        // [stages] (U8)
   const uint32_t bar_ufull = bar_conv + 8 * S::kStages;     // [ring] (U8)
   const uint32_t bar_uempty = bar_ufull + 8 * S::kU8Ring;   // [ring] (U8)
+  const uint32_t bar_hfull = bar_uempty + 8 * S::kU8Ring;   // [stages] (LOD): local tiles landed
   float* colpart = reinterpret_cast<float*>(smem + S::kEpiOff + kEpiWarps * S::kWarpEpi);
 
   const int warp = threadIdx.x >> 5;
@@ -466,8 +475,8 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA_hi);
     prefetch_tmap(&tmB_hi);
-    if (A_LO) prefetch_tmap(&tmA_lo);
-    if (B_LO) prefetch_tmap(&tmB_lo);
+    if (A_LO && !(LOD & 1)) prefetch_tmap(&tmA_lo);
+    if (B_LO && !(LOD & 2)) prefetch_tmap(&tmB_lo);
     for (int s = 0; s < S::kStages; ++s) {
       mbar_init(bar_full + 8 * s, 1);
       mbar_init(bar_empty + 8 * s, 1);
@@ -477,6 +486,12 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
       mbar_init(bar_tempty + 8 * a, kEpiWarps * CG);  // both CTAs' epilogues drain
     }
     for (int w = 0; w < kEpiWarps; ++w) mbar_init(bar_act + 8 * w, 1);
+    if (LOD) {
+      for (int st = 0; st < S::kStages; ++st) {
+        mbar_init(bar_conv + 8 * st, 4 * CG);  // one arrive per converter warp (x CTAs)
+        mbar_init(bar_hfull + 8 * st, 1);      // this CTA's tiles (local tx count)
+      }
+    }
     if (U8) {
       for (int st = 0; st < S::kStages; ++st)
         mbar_init(bar_conv + 8 * st, 4 * CG);  // one arrive per converter warp (x CTAs)
@@ -511,7 +526,7 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
       // ===== TMA producer =====
 #define TMA_FP32(dst, map, x, y, bar)                                   \
   do {                                                                 \
-    if (CG == 2) tma_load_2d_pair(dst, map, x, y, bar);                \
+    if (CG == 2 && !LOD) tma_load_2d_pair(dst, map, x, y, bar);        \
     else tma_load_2d(dst, map, x, y, bar);                             \
   } while (0)
       int stage = 0;
@@ -550,21 +565,26 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
         {
           mbar_wait(bar_empty + 8 * stage, phase ^ 1);
           const uint32_t st = sbase + stage * S::kStage;
-          // CG == 2: both CTAs' fp32 tiles complete on the leader's full barrier
-          const uint32_t full = CG == 2 ? map_rank0(bar_full + 8 * stage) : bar_full + 8 * stage;
-          if (rank == 0) mbar_expect_tx(bar_full + 8 * stage, S::kTmaBytes * CG);
+          // CG == 2: both CTAs' fp32 tiles complete on the leader's full barrier; with
+          // derived lo planes each CTA's tiles complete locally (its converters go next)
+          const uint32_t full = LOD        ? bar_hfull + 8 * stage
+                                : CG == 2 ? map_rank0(bar_full + 8 * stage)
+                                          : bar_full + 8 * stage;
+          if (LOD) mbar_expect_tx(bar_hfull + 8 * stage, S::kTmaBytes);
+          else if (rank == 0) mbar_expect_tx(bar_full + 8 * stage, S::kTmaBytes * CG);
           const int k0 = kb * kBK;
           uint32_t off = st;
           if (U8 == 1) {
             // converted by the converter warps
           } else if (!A_MN) {
             TMA_FP32(off, &tmA_hi, k0, m0, full);
-            if (A_LO) TMA_FP32(off + S::kA, &tmA_lo, k0, m0, full);
+            if (A_LO && !(LOD & 1)) TMA_FP32(off + S::kA, &tmA_lo, k0, m0, full);
           } else {
 #pragma unroll
             for (int j = 0; j < kBM / 32; ++j) {
               TMA_FP32(off + j * 4096, &tmA_hi, m0 + 32 * j, k0, full);
-              if (A_LO) TMA_FP32(off + S::kA + j * 4096, &tmA_lo, m0 + 32 * j, k0, full);
+              if (A_LO && !(LOD & 1))
+                TMA_FP32(off + S::kA + j * 4096, &tmA_lo, m0 + 32 * j, k0, full);
             }
           }
           off += S::kA * (A_LO ? 2 : 1);
@@ -572,12 +592,13 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
             // converted by the converter warps
           } else if (!B_MN) {
             TMA_FP32(off, &tmB_hi, k0, n0, full);
-            if (B_LO) TMA_FP32(off + S::kB, &tmB_lo, k0, n0, full);
+            if (B_LO && !(LOD & 2)) TMA_FP32(off + S::kB, &tmB_lo, k0, n0, full);
           } else {
 #pragma unroll
             for (int j = 0; j < S::kBN / 32; ++j) {
               TMA_FP32(off + j * 4096, &tmB_hi, n0 + 32 * j, k0, full);
-              if (B_LO) TMA_FP32(off + S::kB + j * 4096, &tmB_lo, n0 + 32 * j, k0, full);
+              if (B_LO && !(LOD & 2))
+                TMA_FP32(off + S::kB + j * 4096, &tmB_lo, n0 + 32 * j, k0, full);
             }
           }
           if (++stage == S::kStages) {
@@ -605,8 +626,8 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + uint32_t(acc_buf * S::kAccCols);
         for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(bar_full + 8 * stage, phase);
-          if (U8) mbar_wait(bar_conv + 8 * stage, phase);
+          if (!LOD) mbar_wait(bar_full + 8 * stage, phase);
+          if (U8 || LOD) mbar_wait(bar_conv + 8 * stage, phase);
           tc_fence_after();
           const uint32_t a_hi = sbase + stage * S::kStage;
           const uint32_t a_lo = a_hi + S::kA;
@@ -642,6 +663,38 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
         }
         if (CG == 2) mma_commit_pair(bar_tfull + 8 * acc_buf);
         else mma_commit(bar_tfull + 8 * acc_buf);
+      }
+    }
+  } else if (LOD && warp >= 2 + kEpiWarps) {
+    // ===== Converter warps 6..9: lo = x - trunc_tf32(x) of the landed hi tiles =====
+    // Elementwise over the tile bytes, so the swizzled K- or MN-major layout is kept.
+    const int ct = threadIdx.x - (2 + kEpiWarps) * 32;  // 0..127
+    int stage = 0;
+    uint32_t phase = 0;
+    KCursor cc;
+    cc.init(cl_id, n_cl, num_tiles, tm, p.kb_per_split, kb_total);
+    auto derive = [&](uint8_t* hi, int bytes) {
+      for (int o = ct * 16; o < bytes; o += 128 * 16) {
+        const float4 x = *reinterpret_cast<const float4*>(hi + o);
+        *reinterpret_cast<float4*>(hi + bytes + o) =
+            make_float4(x.x - tf32_hi(x.x), x.y - tf32_hi(x.y), x.z - tf32_hi(x.z),
+                        x.w - tf32_hi(x.w));
+      }
+    };
+    for (; cc.valid(num_tiles); cc.next(n_cl, num_tiles, tm, p.kb_per_split, kb_total)) {
+      mbar_wait(bar_hfull + 8 * stage, phase);  // this CTA's tiles landed
+      uint8_t* st = smem + stage * S::kStage;
+      if (LOD & 1) derive(st, S::kA);
+      if (LOD & 2) derive(st + S::kA * (A_LO ? 2 : 1), S::kB);
+      fence_async_smem();  // generic-proxy writes -> visible to the tensor core
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) {
+        if (CG == 2) mbar_arrive_cluster(map_rank0(bar_conv + 8 * stage));
+        else mbar_arrive(bar_conv + 8 * stage);
+      }
+      if (++stage == S::kStages) {
+        stage = 0;
+        phase ^= 1;
       }
     }
   } else if (U8 && warp >= 2 + kEpiWarps) {
@@ -902,10 +955,10 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
         for (int j4 = 0; j4 < 8; ++j4) {
           *reinterpret_cast<float4*>(bp + swz(lane, j4)) =
               make_float4(o[4 * j4], o[4 * j4 + 1], o[4 * j4 + 2], o[4 * j4 + 3]);
-          *reinterpret_cast<float4*>(bp + 4096 + swz(lane, j4)) =
-              make_float4(o[4 * j4] - tf32_hi(o[4 * j4]), o[4 * j4 + 1] - tf32_hi(o[4 * j4 + 1]),
-                          o[4 * j4 + 2] - tf32_hi(o[4 * j4 + 2]),
-                          o[4 * j4 + 3] - tf32_hi(o[4 * j4 + 3]));
+          if (p.out_lo != nullptr)
+            *reinterpret_cast<float4*>(bp + 4096 + swz(lane, j4)) = make_float4(
+                o[4 * j4] - tf32_hi(o[4 * j4]), o[4 * j4 + 1] - tf32_hi(o[4 * j4 + 1]),
+                o[4 * j4 + 2] - tf32_hi(o[4 * j4 + 2]), o[4 * j4 + 3] - tf32_hi(o[4 * j4 + 3]));
           *reinterpret_cast<float4*>(bp + 8192 + swz(lane, j4)) =
               make_float4(h[4 * j4], h[4 * j4 + 1], h[4 * j4 + 2], h[4 * j4 + 3]);
         }
@@ -913,7 +966,7 @@ __global__ void __launch_bounds__(U8 ? kThreadsU8 : kThreads, 1)
         __syncwarp();
         if (lane == 0) {
           tma_store_2d(&tmOut, nb, rbase, blk);
-          tma_store_2d(&tmOutLo, nb, rbase, blk + 4096);
+          if (p.out_lo != nullptr) tma_store_2d(&tmOutLo, nb, rbase, blk + 4096);
           bulk_commit();
         }
         // lane = column j: sum over this warp's 32 rows (rows past M carry d = 0, and
@@ -1202,6 +1255,9 @@ struct Operand {
   bool mn_major = false;      // false: stored [MN rows][K cols]; true: stored [K rows][MN cols]
   const uint8_t* u8 = nullptr;  // set: the operand is uint8 planes (exact), hi/lo unused;
                                 // A must be K-major, B must be MN-major; ld % 16 == 0
+  bool lo_smem = false;         // the lo pass runs, on lo = hi - trunc_tf32(hi) derived in
+                                // shared memory from the hi tile (lo ignored): no residual
+                                // plane in HBM (fp32 operands only)
 };
 
 struct LaunchInfo {

@@ -229,6 +229,23 @@ struct tlg_learner {
   int32_t* valid;
   // activations
   std::vector<float*> act, act_lo, dz, dz_lo;
+  // tf32 residual (lo = x - trunc_tf32(x)) of the fp32 GEMM operands: derived in shared
+  // memory by the consuming GEMM (Operand::lo_smem, the default), or -- TLG_LO_HBM=1, the
+  // round-1 scheme kept for A/B runs -- planes written by each producer and re-read from
+  // HBM.  Only dZ_1 keeps a plane when layer 1's dW runs on uint8 planes (that kernel's
+  // converter warps expand the bytes, so it reads the residual plane).
+  const bool lo_hbm = std::getenv("TLG_LO_HBM") != nullptr;
+  bool x0_has_lo = false;  // this shard's observations are inexact in tf32 (fp32 values)
+  tlg::gemm::Operand lo_op(const float* hi, const float* plane, long ld, bool mn) const {
+    tlg::gemm::Operand o{hi, nullptr, ld, mn};
+    if (lo_hbm) o.lo = plane;
+    else o.lo_smem = true;
+    return o;
+  }
+  // dZ_l's residual plane has a reader: the tf32 layer-1 dW over uint8 planes
+  bool dz_lo_plane(int l, const uint8_t* x0u8) const {
+    return lo_hbm || (l == 0 && x0u8 != nullptr);
+  }
   float *head_out, *head_part, *tlogp, *adv, *target, *dzh;
   // teacher policy for the PPO KL term (rlmath.cpp:145-155; tlg_learner_set_teacher)
   float* teacher = nullptr;
@@ -311,7 +328,7 @@ struct tlg_learner {
     adam_t_dev = mem.add<uint64_t>(1);
     const long D = net.D;
     obs = mem.add<float>(F_max * D);
-    obs_lo = mem.add<float>(F_max * long(net.D_pad));
+    obs_lo = lo_hbm ? mem.add<float>(F_max * long(net.D_pad)) : nullptr;
     if (net.padded()) {
       obs_pad = mem.add<float>(F_max * long(net.D_pad));
       w1p = mem.add<float>(long(net.dims[1]) * net.D_pad);
@@ -348,9 +365,10 @@ struct tlg_learner {
     for (uint32_t l = 0; l < net.L; ++l) {
       const long n = F_max * net.dims[l + 1];
       act.push_back(mem.add<float>(n));
-      act_lo.push_back(mem.add<float>(n));
+      act_lo.push_back(lo_hbm ? mem.add<float>(n) : nullptr);
       dz.push_back(mem.add<float>(n));
-      dz_lo.push_back(mem.add<float>(n));
+      dz_lo.push_back(lo_hbm || (l == 0 && cfg.obs_dtype != TLG_OBS_F32) ? mem.add<float>(n)
+                                                                         : nullptr);
     }
     const int A1 = int(net.A) + 1;
     head_out = mem.add<float>(F_max * A1);
@@ -633,8 +651,9 @@ struct tlg_learner {
     using tlg::gemm::Operand;
     for (uint32_t l = 0; l < net.L; ++l) {
       const int in = net.gin(l), outw = int(net.dims[l + 1]);
-      Operand A{l == 0 ? x0 : act[l - 1], l == 0 ? x0_lo : act_lo[l - 1], in, false,
-                l == 0 ? x0_u8 : nullptr};
+      Operand A = l > 0       ? lo_op(act[l - 1], act_lo[l - 1], in, false)
+                  : x0_has_lo ? lo_op(x0, x0_lo, in, false)
+                              : Operand{x0, nullptr, in, false, x0_u8};
       Operand B{P + net.w_off[l], P_lo + net.w_off[l], in, false};
       if (l == 0 && net.padded()) {  // the padded copy of this plane's W_1
         B.hi = P == params ? w1p : tw1p;
@@ -643,7 +662,7 @@ struct tlg_learner {
       tlg::gemm::Params p{};
       p.out_hi = act[l];
       // the top layer's residual plane has no reader (heads and loss read the full plane)
-      p.out_lo = l + 1 == net.L ? nullptr : act_lo[l];
+      p.out_lo = l + 1 == net.L ? nullptr : act_lo[l];  // null unless TLG_LO_HBM
       p.ldo = outw;
       p.bias = P + net.b_off[l];
       const bool fuse_head = l + 1 == net.L && fused_head();
@@ -657,7 +676,7 @@ struct tlg_learner {
       if (fuse_loss) {  // ... and the PPO loss: the epilogue writes dZ_L instead of h_L
         p.loss = *fuse_loss_epi;
         p.out_hi = dz[l];
-        p.out_lo = dz_lo[l];
+        p.out_lo = dz_lo_plane(int(l), x0_u8) ? dz_lo[l] : nullptr;
       }
       if (l == 0 && sg.x0_bits != nullptr && wq_src != P) {
         // this step's layer-1 weights of plane P -> int8 pieces (once per step and plane)
@@ -672,7 +691,8 @@ struct tlg_learner {
         // binary planes x int8 weight pieces: exact integer tensor-core GEMM (+ the
         // activations as int8 pieces when layer 2 takes the int8 path too)
         bn = tlg::gemm::launch_i8_bits_fwd(sg.x0_bits, bits_pitch, wq, wq_kp, wq_scale, p.bias,
-                                           int(F), outw, int(net.D), act[0], act_lo[0], outw,
+                                           int(F), outw, int(net.D), act[0],
+                                           net.L > 1 ? act_lo[0] : nullptr, outw,
                                            stream,
                                            i8_fwd2(F) ? act_q : nullptr).bn;
       } else if (l == 1 && sg.x0_bits != nullptr && i8_fwd2(F)) {
@@ -720,11 +740,11 @@ struct tlg_learner {
     const bool i8dw = sg.x0_bits != nullptr && i8_dw1();
     for (int l = int(net.L) - 1; l >= 1; --l) {
       const int in = int(net.dims[l]), outw = int(net.dims[l + 1]);
-      Operand A2{dz[l], dz_lo[l], outw, false};
+      Operand A2 = lo_op(dz[l], dz_lo[l], outw, false);
       Operand B2{params + net.w_off[l], params_lo + net.w_off[l], in, true};
       tlg::gemm::Params p2{};
       p2.out_hi = dz[l - 1];
-      p2.out_lo = dz_lo[l - 1];
+      p2.out_lo = dz_lo_plane(l - 1, sg.x0_u8) ? dz_lo[l - 1] : nullptr;
       p2.ldo = in;
       p2.act_hi = act[l - 1];
       p2.ld_act = in;
@@ -776,9 +796,12 @@ struct tlg_learner {
         const int gin = net.gin(uint32_t(l));
         int sp = tlg::gemm::pick_splits(outw, gin, int(F), kMaxSplits);
         while (long(sp) * outw * gin > ws_elems && sp > 1) --sp;
-        Operand A{dz[l], dz_lo[l], outw, true};
-        // layer 1 reads the uint8 planes directly (converted in smem, exact, no residual)
-        Operand B{xin, xin_lo, gin, true, l == 0 ? x0_u8 : nullptr};
+        // layer 1 over uint8 planes (converted in smem, exact): dZ_1's residual plane
+        const bool u8b = l == 0 && x0_u8 != nullptr;
+        Operand A = u8b ? Operand{dz[0], dz_lo[0], outw, true} : lo_op(dz[l], dz_lo[l], outw, true);
+        Operand B = u8b ? Operand{nullptr, nullptr, gin, true, x0_u8}
+                    : (l > 0 || x0_has_lo) ? lo_op(xin, xin_lo, gin, true)
+                                           : Operand{xin, nullptr, gin, true};
         tlg::gemm::Params p{};
         p.ws = ws;
         p.ws_split_stride = long(outw) * gin;
@@ -815,6 +838,7 @@ struct tlg_learner {
     const long F = long(bd.S) * T;
     const long D = net.D;
     const float* x0_lo = nullptr;
+    x0_has_lo = net.L > 0 && !obs_exact;
     if (net.padded() && !(sg.x0_bits != nullptr && i8_dw1())) {
       // observation rows at D_pad floats for the tf32 GEMMs that read them (pad columns
       // stay zero from allocation); the int8 layer-1 kernels read the bit rows instead
@@ -822,7 +846,7 @@ struct tlg_learner {
                                  size_t(D) * 4, size_t(F), cudaMemcpyDeviceToDevice, stream));
       x0 = obs_pad;
     }
-    if (net.L > 0 && !obs_exact) {
+    if (x0_has_lo && lo_hbm) {
       tlg::launch_split_lo(x0, obs_lo, F * long(net.gin(0)), stream);
       ++launches;
       x0_lo = obs_lo;
@@ -889,7 +913,8 @@ struct tlg_learner {
     const int loss_kind = algo == TLG_ALGO_VTRACE ? 1 : 0;
     const tlg::LossLaunch ll = tlg::launch_loss_backward(
         net.head, params, hL, ldh, bd, head_out, adv, target, st, hd, loss_kind, dzh,
-        net.L ? dz[net.L - 1] : nullptr, net.L ? dz_lo[net.L - 1] : nullptr, hg_partial,
+        net.L ? dz[net.L - 1] : nullptr,
+        net.L && dz_lo_plane(int(net.L) - 1, x0_u8) ? dz_lo[net.L - 1] : nullptr, hg_partial,
         loss_partial, col_partial, stream, teacher_active() ? t_head_out : nullptr,
         parts ? head_part : nullptr, head_tiles, err);
     tlg::launch_head_grad_reduce(net.head, hg_partial, loss_partial, ll, gtarget, st, stream);
@@ -1380,7 +1405,7 @@ struct tlg_policy {
     params = mem.add<float>(P_pad);
     params_lo = mem.add<float>(P_pad);
     obs = mem.add<float>(mb * net.D);
-    obs_lo = mem.add<float>(mb * net.D_pad);
+    obs_lo = nullptr;
     if (net.padded()) {
       obs_pad = mem.add<float>(mb * net.D_pad);
       w1p = mem.add<float>(long(net.dims[1]) * net.D_pad);
@@ -1394,7 +1419,7 @@ struct tlg_policy {
     err = mem.add<int>(4);
     for (uint32_t l = 0; l < net.L; ++l) {
       act.push_back(mem.add<float>(mb * net.dims[l + 1]));
-      act_lo.push_back(mem.add<float>(mb * net.dims[l + 1]));
+      act_lo.push_back(nullptr);
     }
   }
   ~tlg_policy() {
@@ -1919,20 +1944,18 @@ int tlg_policy_forward(tlg_policy* p, const float* obs, size_t n, float* logits,
       TLG_CUDA(cudaMemcpyAsync(p->obs, obs, n * D * 4, cudaMemcpyHostToDevice, p->stream));
       x0 = p->obs;
     }
-    const float* x0_lo = nullptr;
     if (p->net.padded()) {
       TLG_CUDA(cudaMemcpy2DAsync(p->obs_pad, size_t(p->net.D_pad) * 4, x0, size_t(D) * 4,
                                  size_t(D) * 4, n, cudaMemcpyDeviceToDevice, p->stream));
       x0 = p->obs_pad;
     }
-    if (p->net.L > 0) {
-      tlg::launch_split_lo(x0, p->obs_lo, long(n) * p->net.gin(0), p->stream);
-      x0_lo = p->obs_lo;
-    }
+    // the tf32 residuals of the observations and activations are derived in the GEMMs'
+    // shared memory (Operand::lo_smem): no residual planes
     using tlg::gemm::Operand;
     for (uint32_t l = 0; l < p->net.L; ++l) {
       const int in = p->net.gin(l), outw = int(p->net.dims[l + 1]);
-      Operand Aop{l == 0 ? x0 : p->act[l - 1], l == 0 ? x0_lo : p->act_lo[l - 1], in, false};
+      Operand Aop{l == 0 ? x0 : p->act[l - 1], nullptr, in, false};
+      Aop.lo_smem = true;
       Operand Bop{p->params + p->net.w_off[l], p->params_lo + p->net.w_off[l], in, false};
       if (l == 0 && p->net.padded()) {
         Bop.hi = p->w1p;
@@ -1940,7 +1963,7 @@ int tlg_policy_forward(tlg_policy* p, const float* obs, size_t n, float* logits,
       }
       tlg::gemm::Params gp{};
       gp.out_hi = p->act[l];
-      gp.out_lo = l + 1 == p->net.L ? nullptr : p->act_lo[l];
+      gp.out_lo = nullptr;
       gp.ldo = outw;
       gp.bias = p->params + p->net.b_off[l];
       const bool fuse = l + 1 == p->net.L && p->net.A + 1 <= 8;

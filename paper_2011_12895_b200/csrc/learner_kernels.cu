@@ -872,7 +872,7 @@ __global__ void __launch_bounds__(256) loss_stream_kernel(
           if (dz) {
             const float o = dh * (1.f - x * x);
             dz[f * hd.H + j] = o;
-            dz_lo[f * hd.H + j] = o - tf32_hi(o);
+            if (dz_lo) dz_lo[f * hd.H + j] = o - tf32_hi(o);
             dbacc[c] += o;
           }
         }
@@ -970,9 +970,10 @@ __global__ void __launch_bounds__(256, 2) loss_stream4_kernel(
         if (dz) {
           const long off = (f0 + i) * hd.H + j0;
           *reinterpret_cast<float4*>(dz + off) = make_float4(o[0], o[1], o[2], o[3]);
-          *reinterpret_cast<float4*>(dz_lo + off) =
-              make_float4(o[0] - tf32_hi(o[0]), o[1] - tf32_hi(o[1]), o[2] - tf32_hi(o[2]),
-                          o[3] - tf32_hi(o[3]));
+          if (dz_lo)
+            *reinterpret_cast<float4*>(dz_lo + off) =
+                make_float4(o[0] - tf32_hi(o[0]), o[1] - tf32_hi(o[1]), o[2] - tf32_hi(o[2]),
+                            o[3] - tf32_hi(o[3]));
         }
       }
     }
