@@ -1096,6 +1096,10 @@ __global__ void __launch_bounds__((U8 || LOD) ? kThreadsU8 : kThreads, 1)
             const float4 v = *reinterpret_cast<const float4*>(blk_ptr + act_off + swz(lane, j4));
             h[4 * j4] = v.x; h[4 * j4 + 1] = v.y; h[4 * j4 + 2] = v.z; h[4 * j4 + 3] = v.w;
           }
+          // the generic-proxy reads of this block are ordered before the TMA (async
+          // proxy) refill below: without the proxy fence the refill can overtake loads
+          // still in flight (a rare write-after-read race on the act block)
+          fence_async_smem();
           __syncwarp();
           if (c + 32 < BN) act_issue(t, c + 32);
           else act_issue(t + n_cl, 0);

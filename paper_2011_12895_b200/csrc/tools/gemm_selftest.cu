@@ -471,6 +471,56 @@ void check_i8x2(const char* name, int M, int N, int K) {
   cudaFree(bias.hi); cudaFree(bias.lo);
 }
 
+// Derived lo planes (Operand::lo_smem): the GEMM computes lo = x - trunc_tf32(x) in shared
+// memory; the result must equal, bit for bit, the same GEMM fed the residual planes from
+// HBM, and must not vary across repeats.
+void check_lod(const char* name, int M, int N, int K, bool a_mn, bool b_mn, int epi, int splits,
+               int lod) {
+  std::mt19937 rng(M * 31 + N * 17 + K + lod);
+  Buf A, B, act, bias;
+  A.init(long(M) * K, rng);
+  B.init(long(N) * K, rng);
+  act.init(long(M) * N, rng);
+  bias.init(N, rng);
+  const long lda = a_mn ? M : K, ldb = b_mn ? N : K;
+  const long outn = epi == gemm::kEpiStore ? long(splits) * M * N : long(M) * N;
+  float* outs[7];
+  for (auto& o : outs) {
+    TLG_CUDA(cudaMalloc(&o, outn * 4));
+    TLG_CUDA(cudaMemset(o, 0, outn * 4));
+  }
+  auto run = [&](bool derive, float* out) {
+    gemm::Operand oa{A.x, A.lo, lda, a_mn};
+    gemm::Operand ob{B.x, B.lo, ldb, b_mn};
+    if (derive && (lod & 1)) { oa.lo = nullptr; oa.lo_smem = true; }
+    if (derive && (lod & 2)) { ob.lo = nullptr; ob.lo_smem = true; }
+    gemm::Params p{};
+    p.out_hi = out;
+    p.ldo = N;
+    p.bias = bias.x;
+    p.act_hi = act.x;
+    p.ld_act = N;
+    p.ws = out;
+    p.ws_split_stride = long(M) * N;
+    gemm::launch(oa, ob, M, N, K, epi, p, splits, 0);
+  };
+  run(false, outs[0]);
+  for (int r = 1; r < 7; ++r) run(true, outs[r]);
+  TLG_CUDA(cudaDeviceSynchronize());
+  std::vector<float> ref(outn), got(outn);
+  TLG_CUDA(cudaMemcpy(ref.data(), outs[0], outn * 4, cudaMemcpyDeviceToHost));
+  long bad = 0;
+  for (int r = 1; r < 7; ++r) {
+    TLG_CUDA(cudaMemcpy(got.data(), outs[r], outn * 4, cudaMemcpyDeviceToHost));
+    for (long i = 0; i < outn; ++i)
+      if (std::memcmp(&ref[i], &got[i], 4) != 0) ++bad;
+  }
+  printf("%-34s M=%6d N=%5d K=%6d split=%d lod=%d : %s (%ld mismatching words over 6 runs)\n",
+         name, M, N, K, splits, lod, bad ? "FAIL" : "ok", bad);
+  if (bad) ++failures;
+  for (auto& o : outs) cudaFree(o);
+}
+
 int main(int argc, char** argv) {
   try {
     using namespace gemm;
@@ -485,6 +535,13 @@ int main(int argc, char** argv) {
     check("dW store MN/MN split4", 256, 200, 1000, true, true, false, kEpiStore, 4);
     check("dW store MN/MN exactB", 256, 1936, 2048, true, true, false, kEpiStore, 2);
     check("store K/K", 256, 256, 512, false, false, false, kEpiStore, 1);
+    check_lod("LOD fwd tanh K/K", 300, 256, 200, false, false, kEpiFwdTanh, 1, 1);
+    check_lod("LOD fwd tanh K/K pair", 4096, 256, 512, false, false, kEpiFwdTanh, 1, 1);
+    check_lod("LOD dX bwd K/MN", 300, 256, 256, false, true, kEpiBwdTanh, 1, 1);
+    check_lod("LOD dX bwd K/MN pair", 20480, 512, 512, false, true, kEpiBwdTanh, 1, 1);
+    check_lod("LOD dW store MN/MN", 256, 200, 1000, true, true, kEpiStore, 1, 3);
+    check_lod("LOD dW store MN/MN split4", 512, 512, 20480, true, true, kEpiStore, 4, 3);
+    check_lod("LOD dW store MN/MN split1 pair", 512, 512, 20480, true, true, kEpiStore, 1, 3);
     g_fullhi = true;
     check("FULLHI fwd tanh K/K", 300, 256, 200, false, false, false, kEpiFwdTanh, 1);
     check("FULLHI dX bwd K/MN", 300, 256, 256, false, true, false, kEpiBwdTanh, 1);

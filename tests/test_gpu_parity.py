@@ -216,19 +216,27 @@ def test_uint8_observations_match_f32(tlg, oracle):
     assert close(outs[0][0]["loss"], outs[1][0]["loss"], 1e-6)
 
 
-def test_learner_is_deterministic(tlg, oracle):
-    S, T, D, A = 16, 16, 64, 6
-    shape = Shape(2, D, A, (128, 128))
+@pytest.mark.parametrize("case", [(16, 16, 64, (128, 128), "ppo"),
+                                  (256, 80, 64, (512, 512), "vtrace")],  # C2: CTA pairs
+                         ids=["small", "c2"])
+def test_learner_is_deterministic(tlg, oracle, case):
+    """Bit-identical parameters and gradients run to run (fixed-order reductions; the
+    GEMMs' smem hand-offs between the TMA and the generic proxy are fenced)."""
+    S, T, D, hidden, algo = case
+    A = 6
+    shape = Shape(2, D, A, hidden)
     p = init_params(oracle, shape, 8)
     res = []
-    for _ in range(2):
-        lrn = tlg.Learner("mlp", D, A, (128, 128), max_segments=S, unroll_len=T)
+    for _ in range(3):
+        lrn = tlg.Learner("mlp", D, A, hidden, algo=algo, max_segments=S, unroll_len=T)
         lrn.set_hyper(learning_rate=3e-4, batch_size=S, unroll_len=T)
         lrn.set_params(p)
         for step in range(3):
             lrn.train_step(make_batch(tlg, S, T, D, A, seed=step))
-        res.append(lrn.get_params())
-    assert np.array_equal(res[0], res[1])
+        res.append((lrn.get_params(), lrn.get_grad()))
+    for pr, g in res[1:]:
+        assert np.array_equal(res[0][0], pr)
+        assert np.array_equal(res[0][1], g)
 
 
 # ---------------------------------------------------------------------------
