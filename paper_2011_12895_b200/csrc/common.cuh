@@ -6,6 +6,8 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <cstdlib>
+#include <utility>
 #include <stdexcept>
 #include <string>
 
@@ -24,6 +26,87 @@ struct CudaError : std::runtime_error {
   } while (0)
 
 #define TLG_CHECK_LAUNCH() TLG_CUDA(cudaGetLastError())
+
+// ---------------------------------------------------------------------------
+// Programmatic dependent launch (PDL).  Every kernel of this library is launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, so it may be scheduled while its
+// predecessor on the stream drains (launch latency and the prologue -- barrier init,
+// TMEM allocation, tensor-map prefetch -- overlap the predecessor's tail, also inside
+// captured CUDA graphs).  Each kernel therefore calls pdl_wait() before it touches memory
+// a predecessor wrote (griddepcontrol.wait returns once the preceding grid has completed
+// and its writes are visible; it is a no-op without a programmatic dependency) and then
+// pdl_trigger() to let its own successor launch early.  Because every kernel waits, the
+// completion order along a stream is transitive as with ordinary launches.
+// TLG_NO_PDL=1 launches without the attribute (A/B runs).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+#define TLG_PDL_ENTRY()     \
+  do {                      \
+    ::tlg::pdl_wait();      \
+    ::tlg::pdl_trigger();   \
+  } while (0)
+
+inline bool pdl_enabled() {
+  static const bool on = std::getenv("TLG_NO_PDL") == nullptr;
+  return on;
+}
+
+// Append the PDL attribute to a launch configuration whose attribute array has room.
+inline void add_pdl(cudaLaunchConfig_t& cfg, cudaLaunchAttribute* at) {
+  if (!pdl_enabled()) return;
+  at[cfg.numAttrs].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[cfg.numAttrs].val.programmaticStreamSerializationAllowed = 1;
+  cfg.numAttrs += 1;
+}
+
+// cudaLaunchKernelEx with the PDL attribute.
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                     cudaStream_t stream, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  int na = 0;
+  if (pdl_enabled()) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  TLG_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
+
+// The same with a thread-block cluster of `cluster_x` CTAs.
+template <typename... KArgs, typename... Args>
+inline void launch_k_cluster(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                             cudaStream_t stream, int cluster_x, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  at[na].id = cudaLaunchAttributeClusterDimension;
+  at[na].val.clusterDim.x = unsigned(cluster_x);
+  at[na].val.clusterDim.y = 1;
+  at[na].val.clusterDim.z = 1;
+  ++na;
+  if (pdl_enabled()) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  TLG_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
 
 inline int ceil_div(long a, long b) { return int((a + b - 1) / b); }
 

@@ -50,14 +50,14 @@ void run_i8_fwd(const CUtensorMap& tb, const CUtensorMap& tq, const CUtensorMap&
   ensure_smem_attr(kern, bytes, attr);
   const int tiles = tm.m_tiles * tm.n_tiles;
   if (CG == 1) {
-    kern<<<std::min(tiles, num_sms()), kThreadsI8, bytes, stream>>>(tb, tq, to, tl, p, tm);
+    ::tlg::launch_k(kern, dim3(std::min(tiles, num_sms())), dim3(kThreadsI8), size_t(bytes), stream, tb, tq, to, tl, p, tm);
   } else {
     cudaLaunchConfig_t cfg{};
     constexpr int kCl = CG * MC;
     cfg.blockDim = dim3(kThreadsI8);
     cfg.dynamicSmemBytes = bytes;
     cfg.stream = stream;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = kCl;
     at[0].val.clusterDim.y = 1;
@@ -85,6 +85,7 @@ void run_i8_fwd(const CUtensorMap& tb, const CUtensorMap& tq, const CUtensorMap&
       max_cl.store(std::max(1, std::min(n, num_sms() / kCl)));
     }
     cfg.gridDim = dim3(kCl * std::min(tiles, max_cl.load()));
+    add_pdl(cfg, cfg.attrs);
     TLG_CUDA(cudaLaunchKernelEx(&cfg, kern, tb, tq, to, tl, p, tm));
   }
   TLG_CHECK_LAUNCH();
@@ -95,6 +96,7 @@ __global__ void __launch_bounds__(256) quantize_rows_kernel(const float* __restr
                                                             long ldw, int8_t* __restrict__ q,
                                                             long Kp, long plane,
                                                             float* __restrict__ scale) {
+  TLG_PDL_ENTRY();
   __shared__ float red[8];
   const int n = blockIdx.x;
   const float* w = W + long(n) * ldw;
@@ -143,20 +145,21 @@ void run_i8_dw(const CUtensorMap& tp, const CUtensorMap& tb, const CUtensorMap& 
   ensure_smem_attr(kern, bytes, attr);
   const int tiles = tm.m_tiles * tm.n_tiles * tm.splits;
   if (CG == 1) {
-    kern<<<std::min(tiles, num_sms()), kThreadsI8, bytes, stream>>>(tp, tb, tw, p, tm);
+    ::tlg::launch_k(kern, dim3(std::min(tiles, num_sms())), dim3(kThreadsI8), size_t(bytes), stream, tp, tb, tw, p, tm);
   } else {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(2 * std::min(tiles, num_sms() / 2));
     cfg.blockDim = dim3(kThreadsI8);
     cfg.dynamicSmemBytes = bytes;
     cfg.stream = stream;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = 2;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
+    add_pdl(cfg, cfg.attrs);
     TLG_CUDA(cudaLaunchKernelEx(&cfg, kern, tp, tb, tw, p, tm));
   }
   TLG_CHECK_LAUNCH();
@@ -171,6 +174,7 @@ __global__ void __launch_bounds__(256) quantize_cols_kernel(const float* __restr
                                                             const unsigned* __restrict__ colmax,
                                                             long rows_per_split,
                                                             int8_t* __restrict__ P) {
+  TLG_PDL_ENTRY();
   const int quads = M / 4;
   const int lanes = max(1, 256 / quads);
   const int per_pass = (256 / quads) > 0 ? quads : 256;  // quads handled per pass
@@ -252,7 +256,7 @@ void launch_quantize_cols(const float* Z, long F, int M, long ldz, const unsigne
                           long rows_per_split, int8_t* P, cudaStream_t stream) {
   if (M % 4 != 0 || ldz % 4 != 0) throw CudaError("quantize_cols: M and ldz must be multiples of 4");
   if (rows_per_split % kQRows != 0) throw CudaError("quantize_cols: split rows % 64 != 0");
-  quantize_cols_kernel<<<ceil_div(F, kQRows), 256, 0, stream>>>(Z, F, M, ldz, colmax,
+  ::tlg::launch_k(quantize_cols_kernel, dim3(ceil_div(F, kQRows)), dim3(256), size_t(0), stream, Z, F, M, ldz, colmax,
                                                                 rows_per_split, P);
   TLG_CHECK_LAUNCH();
 }
@@ -287,20 +291,21 @@ void run_i8x2_fwd(const CUtensorMap& ta, const CUtensorMap& tq, const CUtensorMa
   const int tiles = tm.m_tiles * tm.n_tiles;
   constexpr int threads = 32 * (2 + kEpiWarps);
   if (CG == 1) {
-    kern<<<std::min(tiles, num_sms()), threads, bytes, stream>>>(ta, tq, to, tl, p, tm);
+    ::tlg::launch_k(kern, dim3(std::min(tiles, num_sms())), dim3(threads), size_t(bytes), stream, ta, tq, to, tl, p, tm);
   } else {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(2 * std::min(tiles, num_sms() / 2));
     cfg.blockDim = dim3(threads);
     cfg.dynamicSmemBytes = bytes;
     cfg.stream = stream;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = 2;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
+    add_pdl(cfg, cfg.attrs);
     TLG_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tq, to, tl, p, tm));
   }
   TLG_CHECK_LAUNCH();
@@ -338,7 +343,7 @@ LaunchInfo launch_i8x2_fwd(const int8_t* a, const int8_t* q, long Kp, const floa
 void launch_quantize_rows(const float* W, int N, int K, long ldw, int8_t* q, long Kp, float* s,
                           cudaStream_t stream) {
   if (Kp % 16 != 0 || Kp < K) throw CudaError("quantize_rows: Kp must be >= K and a multiple of 16");
-  quantize_rows_kernel<<<N, 256, 0, stream>>>(W, K, ldw, q, Kp, long(N) * Kp, s);
+  ::tlg::launch_k(quantize_rows_kernel, dim3(N), dim3(256), size_t(0), stream, W, K, ldw, q, Kp, long(N) * Kp, s);
   TLG_CHECK_LAUNCH();
 }
 

@@ -239,6 +239,9 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // prologue done (barriers, TMEM, tensor maps): wait for the predecessor's writes
+  pdl_wait();
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -566,6 +569,9 @@ __global__ void __launch_bounds__(32 * (2 + kEpiWarps), 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // prologue done (barriers, TMEM, tensor maps): wait for the predecessor's writes
+  pdl_wait();
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -865,6 +871,9 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // prologue done (barriers, TMEM, tensor maps): wait for the predecessor's writes
+  pdl_wait();
+  pdl_trigger();
 
   auto decode = [&](int t, int& mt, int& nt, int& sp) {
     nt = t % tm.n_tiles;

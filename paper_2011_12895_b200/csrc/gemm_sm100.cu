@@ -119,7 +119,7 @@ void run(const CUtensorMap& ah, const CUtensorMap& al, const CUtensorMap& bh,
   const TileMap tm{int(grid.x), int(grid.y), int(grid.z)};  // grid.x counts (128*CG)-row tiles
   const int tiles = tm.m_tiles * tm.n_tiles * tm.splits;
   if (CG == 1) {
-    kern<<<std::min(tiles, num_sms()), threads, bytes, stream>>>(
+    ::tlg::launch_k(kern, dim3(std::min(tiles, num_sms())), dim3(threads), size_t(bytes), stream, 
         ah, al, bh, bl, em.out, em.out_lo, em.act, p, tm);
   } else {
     cudaLaunchConfig_t cfg{};
@@ -127,13 +127,14 @@ void run(const CUtensorMap& ah, const CUtensorMap& al, const CUtensorMap& bh,
     cfg.blockDim = dim3(threads);
     cfg.dynamicSmemBytes = bytes;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    add_pdl(cfg, cfg.attrs);
     TLG_CUDA(cudaLaunchKernelEx(&cfg, kern, ah, al, bh, bl, em.out, em.out_lo, em.act, p, tm));
   }
   TLG_CHECK_LAUNCH();

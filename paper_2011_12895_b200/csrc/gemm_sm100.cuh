@@ -520,6 +520,9 @@ __global__ void __launch_bounds__((U8 || LOD) ? kThreadsU8 : kThreads, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // prologue done (barriers, TMEM, tensor maps): wait for the predecessor's writes
+  pdl_wait();
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {

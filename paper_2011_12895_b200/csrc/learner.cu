@@ -136,6 +136,7 @@ struct Net {
 // Zero-padded copy of a row-major [rows x cols] matrix into [rows x cols_pad].
 __global__ void pad_rows_kernel(const float* __restrict__ src, long rows, int cols, int cols_pad,
                                 float* __restrict__ dst) {
+  TLG_PDL_ENTRY();
   const long n = rows * cols_pad;
   for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n;
        i += long(gridDim.x) * blockDim.x) {
@@ -147,7 +148,7 @@ __global__ void pad_rows_kernel(const float* __restrict__ src, long rows, int co
 
 void pad_rows(const float* src, long rows, int cols, int cols_pad, float* dst, cudaStream_t st) {
   const long n = rows * cols_pad;
-  pad_rows_kernel<<<int(std::min<long>((n + 255) / 256, 148L * 8)), 256, 0, st>>>(src, rows, cols,
+  ::tlg::launch_k(pad_rows_kernel, dim3(int(std::min<long>((n + 255) / 256, 148L * 8))), dim3(256), size_t(0), st, src, rows, cols,
                                                                                cols_pad, dst);
   TLG_CHECK_LAUNCH();
 }
@@ -1256,11 +1257,13 @@ namespace {
 // guard[0] > 0 iff some shard raised an error bit or produced a non-finite loss; it is
 // summed by the allreduce together with the gradient, so every rank agrees to skip.
 __global__ void set_guard_kernel(const int* err, const tlg::StepStatsDev* st, float* guard) {
+  TLG_PDL_ENTRY();
   const bool bad = (*err != 0) || !isfinite(st->loss);
   if (bad) guard[0] = 1.f;
 }
 
 __global__ void accumulate_kernel(float4* __restrict__ g, const float4* __restrict__ t, long n4) {
+  TLG_PDL_ENTRY();
   for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n4;
        i += long(gridDim.x) * blockDim.x) {
     float4 a = g[i];
@@ -1276,6 +1279,7 @@ __global__ void optimizer_guarded_kernel(float4* __restrict__ p, float4* __restr
                                          float grad_scale, int adam, float lr,
                                          const uint64_t* adam_t, double b1d, double b2d,
                                          float eps) {
+  TLG_PDL_ENTRY();
   if (*guard != 0.f) return;  // some shard failed: parameters stay untouched
   // torch.optim.Adam bias corrections for step t = (completed steps) + 1
   const double t = double(*adam_t + 1);
@@ -1313,10 +1317,12 @@ __global__ void optimizer_guarded_kernel(float4* __restrict__ p, float4* __restr
 }
 
 __global__ void advance_step_kernel(const float* guard, uint64_t* adam_t) {
+  TLG_PDL_ENTRY();
   if (*guard == 0.f) *adam_t += 1;
 }
 
 __global__ void split_lo_flat(const float* x, float* lo, long n) {
+  TLG_PDL_ENTRY();
   long i = blockIdx.x * long(blockDim.x) + threadIdx.x;
   if (i < n) lo[i] = x[i] - tlg::tf32_hi(x[i]);
 }
@@ -1324,7 +1330,7 @@ __global__ void split_lo_flat(const float* x, float* lo, long n) {
 }  // namespace
 
 void tlg_learner::set_guard(int shard) {
-  set_guard_kernel<<<1, 1, 0, stream>>>(err, stats + shard, grad + P_pad);
+  ::tlg::launch_k(set_guard_kernel, dim3(1), dim3(1), size_t(0), stream, err, stats + shard, grad + P_pad);
   TLG_CHECK_LAUNCH();
   ++launches;
 }
@@ -1356,8 +1362,7 @@ void tlg_learner::bucket_flush() {
 
 void tlg_learner::accumulate_grad() {
   const long n4 = P_pad / 4;
-  accumulate_kernel<<<int(std::max<long>(1, std::min<long>((n4 + 255) / 256, 148L * 4))), 256, 0,
-                      stream>>>(reinterpret_cast<float4*>(grad),
+  ::tlg::launch_k(accumulate_kernel, dim3(int(std::max<long>(1, std::min<long>((n4 + 255) / 256, 148L * 4)))), dim3(256), size_t(0), stream, reinterpret_cast<float4*>(grad),
                                 reinterpret_cast<const float4*>(grad_tmp), n4);
   TLG_CHECK_LAUNCH();
   ++launches;
@@ -1366,13 +1371,13 @@ void tlg_learner::accumulate_grad() {
 void tlg_learner::launch_guarded_optimizer(bool adam, float lr) {
   const long n4 = P_pad / 4;
   const int blocks = int(std::max<long>(1, std::min<long>((n4 + 255) / 256, 148L * 4)));
-  optimizer_guarded_kernel<<<blocks, 256, 0, stream>>>(
+  ::tlg::launch_k(optimizer_guarded_kernel, dim3(blocks), dim3(256), size_t(0), stream, 
       reinterpret_cast<float4*>(params), reinterpret_cast<float4*>(params_lo),
       reinterpret_cast<const float4*>(grad), reinterpret_cast<float4*>(adam_m),
       reinterpret_cast<float4*>(adam_v), n4, grad + P_pad, grad_scale, adam ? 1 : 0, lr,
       adam_t_dev, cfg.adam_beta1, cfg.adam_beta2, float(cfg.adam_eps));
   TLG_CHECK_LAUNCH();
-  advance_step_kernel<<<1, 1, 0, stream>>>(grad + P_pad, adam_t_dev);
+  ::tlg::launch_k(advance_step_kernel, dim3(1), dim3(1), size_t(0), stream, grad + P_pad, adam_t_dev);
   TLG_CHECK_LAUNCH();
   launches += 2;
 }
@@ -1434,6 +1439,7 @@ namespace {
 
 __global__ void unpack_head_kernel(const float* head_out, int A, long n, float* logits,
                                    float* value) {
+  TLG_PDL_ENTRY();
   const long i = blockIdx.x * long(blockDim.x) + threadIdx.x;
   if (i >= n) return;
   for (int k = 0; k < A; ++k) logits[i * A + k] = head_out[i * (A + 1) + k];
@@ -1446,7 +1452,7 @@ void set_params_common(float* params, float* params_lo, long P, long P_pad, cons
   std::vector<float> h(P_pad, 0.f);
   for (long i = 0; i < P; ++i) h[i] = float(values[i]);
   TLG_CUDA(cudaMemcpyAsync(params, h.data(), P_pad * 4, cudaMemcpyHostToDevice, stream));
-  split_lo_flat<<<int((P_pad + 255) / 256), 256, 0, stream>>>(params, params_lo, P_pad);
+  ::tlg::launch_k(split_lo_flat, dim3(int((P_pad + 255) / 256)), dim3(256), size_t(0), stream, params, params_lo, P_pad);
   TLG_CHECK_LAUNCH();
   TLG_CUDA(cudaStreamSynchronize(stream));
 }
@@ -1988,7 +1994,7 @@ int tlg_policy_forward(tlg_policy* p, const float* obs, size_t n, float* logits,
     } else {
       tlg::launch_head_forward(p->net.head, p->params, hL, p->net.head.H, nullptr, long(n),
                                p->head_out, nullptr, pr, p->err, p->stream);
-      unpack_head_kernel<<<int((n + 255) / 256), 256, 0, p->stream>>>(p->head_out, int(A),
+      ::tlg::launch_k(unpack_head_kernel, dim3(int((n + 255) / 256)), dim3(256), size_t(0), p->stream, p->head_out, int(A),
                                                                        long(n), lg, vv);
       TLG_CHECK_LAUNCH();
     }

@@ -19,6 +19,7 @@ __device__ __forceinline__ bool frame_valid(const BatchDev* b, long f, int* t_ou
 
 // ---------------------------------------------------------------------------
 __global__ void expand_u8_kernel(const uchar4* __restrict__ in, float4* __restrict__ out, long n4) {
+  TLG_PDL_ENTRY();
   for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n4; i += long(gridDim.x) * blockDim.x) {
     const uchar4 u = in[i];
     out[i] = make_float4(u.x, u.y, u.z, u.w);
@@ -32,6 +33,7 @@ constexpr int kRepitchRows = 64;
 __global__ void __launch_bounds__(256) repitch_bits_kernel(const uint8_t* __restrict__ bits,
                                                            long rowb, long F,
                                                            uint8_t* __restrict__ out, long pitch) {
+  TLG_PDL_ENTRY();
   extern __shared__ uint4 rp_smem[];
   uint8_t* sb = reinterpret_cast<uint8_t*>(rp_smem);
   const long f0 = long(blockIdx.x) * kRepitchRows;
@@ -67,6 +69,7 @@ __global__ void __launch_bounds__(256) repitch_bits_kernel(const uint8_t* __rest
 __global__ void unpack_bits_kernel(const uint8_t* __restrict__ bits, long rowb, long F, long D,
                                    uint8_t* __restrict__ out, uint8_t* __restrict__ pitched,
                                    long pitch) {
+  TLG_PDL_ENTRY();
   for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < F * rowb;
        i += long(gridDim.x) * blockDim.x) {
     const long f = i / rowb, j = i % rowb;
@@ -86,6 +89,7 @@ __global__ void unpack_bits_kernel(const uint8_t* __restrict__ bits, long rowb, 
 }
 
 __global__ void split_lo_kernel(const float4* __restrict__ x, float4* __restrict__ lo, long n4) {
+  TLG_PDL_ENTRY();
   for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n4; i += long(gridDim.x) * blockDim.x) {
     const float4 v = x[i];
     lo[i] = make_float4(v.x - tf32_hi(v.x), v.y - tf32_hi(v.y), v.z - tf32_hi(v.z),
@@ -105,6 +109,7 @@ __global__ void __launch_bounds__(256) head_forward_kernel(HeadDesc hd, const fl
                                                          float* __restrict__ tlogp,
                                                          float* __restrict__ probs_out,
                                                          int* __restrict__ err) {
+  TLG_PDL_ENTRY();
   const BatchDev* b = has_batch ? &bd : nullptr;
   const int lane = threadIdx.x & 31;
   const long warps = long(gridDim.x) * (blockDim.x >> 5);
@@ -188,6 +193,7 @@ __global__ void head_finalize_kernel(HeadDesc hd, const float* __restrict__ para
                                      float* __restrict__ tlogp, float* __restrict__ logits_out,
                                      float* __restrict__ probs_out, float* __restrict__ value_out,
                                      int* __restrict__ err) {
+  TLG_PDL_ENTRY();
   const long f = blockIdx.x * long(blockDim.x) + threadIdx.x;
   if (f >= F) return;
   const int A = hd.A, A1 = A + 1;
@@ -271,6 +277,7 @@ __global__ void __launch_bounds__(256) returns_kernel(BatchDev b, int algo, Hype
                                                       float* __restrict__ target,
                                                       double* __restrict__ seg_partial,
                                                       int* __restrict__ err) {
+  TLG_PDL_ENTRY();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int s = blockIdx.x * kRetSegsPerBlock + w;
   double s1 = 0.0, s2 = 0.0;
@@ -443,6 +450,7 @@ __global__ void __launch_bounds__(256, kAlgo == kAlgoPpo ? 8 : 6) returns_vec_ke
                                                           float* __restrict__ target,
                                                           double* __restrict__ seg_partial,
                                                           int* __restrict__ err) {
+  TLG_PDL_ENTRY();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, j = lane & 7;
   const int s = blockIdx.x * kRetVecSegsPerBlock + w * 4 + (lane >> 3);
   const bool active = s < b.S;
@@ -606,6 +614,7 @@ __global__ void __launch_bounds__(1024) finalize_adv_kernel(const double* __rest
                                                             BatchDev b, int adv_norm,
                                                             StepStatsDev* st, int* err,
                                                             int segs_per_block) {
+  TLG_PDL_ENTRY();
   __shared__ double sh1[32], sh2[32];
   __shared__ long long shn[32];
   double s1 = 0.0, s2 = 0.0;
@@ -662,6 +671,7 @@ __global__ void __launch_bounds__(256) loss_math_kernel(
     int loss_kind, float* __restrict__ dzh, double* __restrict__ loss_partial,
     float* __restrict__ bias_partial, const float* __restrict__ teacher_out, int n_tiles,
     const float* __restrict__ params, int* __restrict__ err) {
+  TLG_PDL_ENTRY();
   __shared__ double red[5][8];
   __shared__ float bred[kMaxA1][8];
   const int A = hd.A, A1 = A + 1;
@@ -819,6 +829,7 @@ __global__ void __launch_bounds__(256) loss_stream_kernel(
     HeadDesc hd, const float* __restrict__ params, const float* __restrict__ h, long ldh,
     long F, const float* __restrict__ dzh, float* __restrict__ dz, float* __restrict__ dz_lo,
     float* __restrict__ hg_partial, float* __restrict__ db_partial) {
+  TLG_PDL_ENTRY();
   extern __shared__ float sdz[];  // [kLossFrames][A1]
   const int A = hd.A, A1 = A + 1;
   const long nchunks = (F + kLossFrames - 1) / kLossFrames;
@@ -905,6 +916,7 @@ __global__ void __launch_bounds__(256, 2) loss_stream4_kernel(
     HeadDesc hd, const float* __restrict__ params, const float* __restrict__ h, long ldh,
     long F, const float* __restrict__ dzh, float* __restrict__ dz, float* __restrict__ dz_lo,
     float* __restrict__ hg_partial, float* __restrict__ db_partial) {
+  TLG_PDL_ENTRY();
   constexpr int kA1 = 8;
   __shared__ float sdz[kLossFrames * kA1];
   __shared__ float red[256 * 4];
@@ -1025,6 +1037,7 @@ inline int rows_reduce_threads(long cols) { return cols >= 8192 ? 256 : 32 * kRo
 __global__ void __launch_bounds__(1024) rows_reduce_kernel(const float* __restrict__ partial,
                                                           int rows, long cols, long stride,
                                                           float* __restrict__ out) {
+  TLG_PDL_ENTRY();
   rows_reduce_block(partial, rows, cols, stride, [&](long c, float v) { out[c] = v; });
 }
 
@@ -1034,6 +1047,7 @@ __global__ void __launch_bounds__(1024) head_grad_reduce_kernel(HeadDesc hd,
                                                                const float* __restrict__ hg_partial,
                                                                int nblocks,
                                                                float* __restrict__ grad) {
+  TLG_PDL_ENTRY();
   const int A = hd.A, A1 = A + 1;
   const long nw = long(A1) * hd.H;
   rows_reduce_block(hg_partial, nblocks, nw, nw, [&](long idx, float v) {
@@ -1051,6 +1065,7 @@ __global__ void __launch_bounds__(1024) head_grad_reduce_kernel(HeadDesc hd,
 __global__ void head_bias_stats_kernel(HeadDesc hd, const float* __restrict__ bias_partial,
                                        const double* __restrict__ loss_partial, int nblocks,
                                        float* __restrict__ grad, StepStatsDev* st) {
+  TLG_PDL_ENTRY();
   const int A = hd.A, A1 = A + 1;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (w < A1) {
@@ -1079,6 +1094,7 @@ __global__ void head_bias_stats_kernel(HeadDesc hd, const float* __restrict__ bi
 
 __global__ void dw_reduce_kernel(const float4* __restrict__ ws, int splits, long n4, long stride4,
                                  float4* __restrict__ out) {
+  TLG_PDL_ENTRY();
   for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n4; i += long(gridDim.x) * blockDim.x) {
     float4 a = ws[i];
     for (int s = 1; s < splits; ++s) {
@@ -1091,6 +1107,7 @@ __global__ void dw_reduce_kernel(const float4* __restrict__ ws, int splits, long
 
 __global__ void dw_reduce_scalar_kernel(const float* __restrict__ ws, int splits, long n,
                                         float* __restrict__ out) {
+  TLG_PDL_ENTRY();
   for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
     float a = ws[i];
     for (int s = 1; s < splits; ++s) a += ws[s * n + i];
@@ -1102,6 +1119,7 @@ constexpr int kColRows = 256;  // rows per colsum chunk
 
 __global__ void colsum_partial_kernel(const float* __restrict__ x, long ld, long rows, int cols,
                                       float* __restrict__ partial) {
+  TLG_PDL_ENTRY();
   const long r0 = long(blockIdx.y) * kColRows;
   const long r1 = min(rows, r0 + kColRows);
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < cols; j += gridDim.x * blockDim.x) {
@@ -1113,6 +1131,7 @@ __global__ void colsum_partial_kernel(const float* __restrict__ x, long ld, long
 
 __global__ void colsum_reduce_kernel(const float* __restrict__ partial, int chunks, int cols,
                                      float* __restrict__ out) {
+  TLG_PDL_ENTRY();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= cols) return;
   float acc = 0.f;
@@ -1131,6 +1150,7 @@ __global__ void optimizer_kernel(float4* __restrict__ p, float4* __restrict__ pl
                                  float4* __restrict__ v, long n4, float grad_scale, int adam,
                                  float lr, float step_size, float bc2_sqrt, float b1, float b2,
                                  float eps) {
+  TLG_PDL_ENTRY();
   for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n4; i += long(gridDim.x) * blockDim.x) {
     float4 pp = p[i];
     float4 gg = g[i];
@@ -1168,7 +1188,7 @@ int grid_for(long n, int threads, int per_sm = 8) {
 }  // namespace
 
 void launch_expand_u8(const uint8_t* in, float* out, long n, cudaStream_t s) {
-  expand_u8_kernel<<<grid_for(n / 4, 256), 256, 0, s>>>(reinterpret_cast<const uchar4*>(in),
+  ::tlg::launch_k(expand_u8_kernel, dim3(grid_for(n / 4, 256)), dim3(256), size_t(0), s, reinterpret_cast<const uchar4*>(in),
                                                         reinterpret_cast<float4*>(out), n / 4);
   TLG_CHECK_LAUNCH();
 }
@@ -1178,6 +1198,7 @@ __global__ void __launch_bounds__(256) replay_move_kernel(SegArrays src, long sr
                                                           SegArrays dst, long dst_rowb,
                                                           const uint32_t* __restrict__ slots,
                                                           int T, int scatter) {
+  TLG_PDL_ENTRY();
   const long i = blockIdx.x;
   const long si = scatter ? i : long(slots[i]);
   const long di = scatter ? long(slots[i]) : i;
@@ -1210,7 +1231,7 @@ __global__ void __launch_bounds__(256) replay_move_kernel(SegArrays src, long sr
 void launch_replay_move(const SegArrays& src, long src_rowb, const SegArrays& dst, long dst_rowb,
                         const uint32_t* slots, int n, int T, bool scatter, cudaStream_t s) {
   if (n <= 0) return;
-  replay_move_kernel<<<n, 256, 0, s>>>(src, src_rowb, dst, dst_rowb, slots, T, scatter ? 1 : 0);
+  ::tlg::launch_k(replay_move_kernel, dim3(n), dim3(256), size_t(0), s, src, src_rowb, dst, dst_rowb, slots, T, scatter ? 1 : 0);
   TLG_CHECK_LAUNCH();
 }
 
@@ -1221,18 +1242,18 @@ void launch_unpack_bits(const uint8_t* bits, long rowb, long F, long D, uint8_t*
     if (pitch % 16 != 0) throw CudaError("bit-row pitch must be a multiple of 16");
     const size_t smem = size_t(kRepitchRows * rowb + 32);
     if (smem > 48 * 1024) throw CudaError("bit rows too long for the repitch kernel");
-    repitch_bits_kernel<<<ceil_div(F, kRepitchRows), 256, smem, s>>>(bits, rowb, F, pitched,
+    ::tlg::launch_k(repitch_bits_kernel, dim3(ceil_div(F, kRepitchRows)), dim3(256), size_t(smem), s, bits, rowb, F, pitched,
                                                                      pitch);
     TLG_CHECK_LAUNCH();
     return;
   }
-  unpack_bits_kernel<<<grid_for(F * rowb, 256), 256, 0, s>>>(bits, rowb, F, D, out, pitched,
+  ::tlg::launch_k(unpack_bits_kernel, dim3(grid_for(F * rowb, 256)), dim3(256), size_t(0), s, bits, rowb, F, D, out, pitched,
                                                              pitch);
   TLG_CHECK_LAUNCH();
 }
 
 void launch_split_lo(const float* x, float* lo, long n, cudaStream_t s) {
-  split_lo_kernel<<<grid_for(n / 4, 256), 256, 0, s>>>(reinterpret_cast<const float4*>(x),
+  ::tlg::launch_k(split_lo_kernel, dim3(grid_for(n / 4, 256)), dim3(256), size_t(0), s, reinterpret_cast<const float4*>(x),
                                                        reinterpret_cast<float4*>(lo), n / 4);
   TLG_CHECK_LAUNCH();
 }
@@ -1245,10 +1266,10 @@ void launch_head_forward(const HeadDesc& hd, const float* params, const float* h
   if (b) bd = *b;
   const int blocks = int(std::max<long>(1, std::min<long>((F + 7) / 8, 148L * 16)));
   if (hd.A + 1 <= 8)
-    head_forward_kernel<8><<<blocks, 256, 0, s>>>(hd, params, h, ldh, bd, b ? 1 : 0, F, head_out,
+    ::tlg::launch_k(head_forward_kernel<8>, dim3(blocks), dim3(256), size_t(0), s, hd, params, h, ldh, bd, b ? 1 : 0, F, head_out,
                                                   tlogp, probs_out, err);
   else
-    head_forward_kernel<32><<<blocks, 256, 0, s>>>(hd, params, h, ldh, bd, b ? 1 : 0, F,
+    ::tlg::launch_k(head_forward_kernel<32>, dim3(blocks), dim3(256), size_t(0), s, hd, params, h, ldh, bd, b ? 1 : 0, F,
                                                    head_out, tlogp, probs_out, err);
   TLG_CHECK_LAUNCH();
 }
@@ -1260,7 +1281,7 @@ void launch_head_finalize(const HeadDesc& hd, const float* params, const float* 
   if (hd.A + 1 > 8) throw CudaError("fused head supports n_actions <= 7");
   BatchDev bd{};
   if (b) bd = *b;
-  head_finalize_kernel<<<ceil_div(F, 256), 256, 0, s>>>(hd, params, part, n_tiles, F, bd,
+  ::tlg::launch_k(head_finalize_kernel, dim3(ceil_div(F, 256)), dim3(256), size_t(0), s, hd, params, part, n_tiles, F, bd,
                                                         b ? 1 : 0, head_out, tlogp, logits_out,
                                                         probs_out, value_out, err);
   TLG_CHECK_LAUNCH();
@@ -1285,14 +1306,14 @@ int launch_returns(const BatchDev& b, int algo, const HyperDev& hp, const float*
     // one instantiation per algorithm: the PPO kernel drops the V-trace state (56 -> fewer
     // registers, more resident segments per SM for the HBM stream)
     if (algo == kAlgoPpo)
-      returns_vec_kernel<kAlgoPpo><<<ceil_div(b.S, per), 256, 0, s>>>(b, hp, tlogp, adv, target,
+      ::tlg::launch_k(returns_vec_kernel<kAlgoPpo>, dim3(ceil_div(b.S, per)), dim3(256), size_t(0), s, b, hp, tlogp, adv, target,
                                                                     seg_partial, err);
     else
-      returns_vec_kernel<kAlgoVtrace><<<ceil_div(b.S, per), 256, 0, s>>>(b, hp, tlogp, adv,
+      ::tlg::launch_k(returns_vec_kernel<kAlgoVtrace>, dim3(ceil_div(b.S, per)), dim3(256), size_t(0), s, b, hp, tlogp, adv,
                                                                        target, seg_partial, err);
   } else {
     per = kRetSegsPerBlock;
-    returns_kernel<<<ceil_div(b.S, per), 32 * per, 0, s>>>(b, algo, hp, tlogp, adv, target,
+    ::tlg::launch_k(returns_kernel, dim3(ceil_div(b.S, per)), dim3(32 * per), size_t(0), s, b, algo, hp, tlogp, adv, target,
                                                            seg_partial, err);
   }
   TLG_CHECK_LAUNCH();
@@ -1301,7 +1322,7 @@ int launch_returns(const BatchDev& b, int algo, const HyperDev& hp, const float*
 
 void launch_finalize_adv(const double* seg_partial, const BatchDev& b, int adv_norm,
                          StepStatsDev* st, int* err, cudaStream_t s, int segs_per_block) {
-  finalize_adv_kernel<<<1, 1024, 0, s>>>(seg_partial, b, adv_norm, st, err, segs_per_block);
+  ::tlg::launch_k(finalize_adv_kernel, dim3(1), dim3(1024), size_t(0), s, seg_partial, b, adv_norm, st, err, segs_per_block);
   TLG_CHECK_LAUNCH();
 }
 
@@ -1327,7 +1348,7 @@ LossLaunch launch_loss_backward(const HeadDesc& hd, const float* params, const f
   float* bias_partial = hg_partial + long(ll.stream_blocks) * nw;
   const float* src = head_part ? head_part : head_out;
 #define TLG_MATH(MA, KL, PARTS)                                                              \
-  loss_math_kernel<MA, KL, PARTS><<<ll.math_blocks, 256, 0, s>>>(                           \
+  ::tlg::launch_k(loss_math_kernel<MA, KL, PARTS>, dim3(ll.math_blocks), dim3(256), size_t(0), s,                            \
       hd, b, src, adv, target, st, hp, loss_kind, dzh, loss_partial, bias_partial, teacher_out, \
       n_tiles, params, err)
   const bool kl = teacher_out != nullptr;
@@ -1347,14 +1368,14 @@ LossLaunch launch_loss_backward(const HeadDesc& hd, const float* params, const f
 #undef TLG_MATH
   TLG_CHECK_LAUNCH();
   if (vec) {
-    loss_stream4_kernel<8><<<dim3(ll.stream_blocks, slabs), 256, 0, s>>>(
+    ::tlg::launch_k(loss_stream4_kernel<8>, dim3(dim3(ll.stream_blocks, slabs)), dim3(256), size_t(0), s, 
         hd, params, h, ldh, F, dzh, dz, dz_lo, hg_partial, db_partial);
     TLG_CHECK_LAUNCH();
     return ll;
   }
   const size_t smem = size_t(kLossFrames) * A1 * sizeof(float);
 #define TLG_LOSS(MA, CPT)                                                                  \
-  loss_stream_kernel<MA, CPT><<<ll.stream_blocks, 256, smem, s>>>(hd, params, h, ldh, F, dzh, dz, \
+  ::tlg::launch_k(loss_stream_kernel<MA, CPT>, dim3(ll.stream_blocks), dim3(256), size_t(smem), s, hd, params, h, ldh, F, dzh, dz, \
                                                                  dz_lo, hg_partial, db_partial)
   const int cpt = (hd.H + 255) / 256;
   if (A1 <= 8) {
@@ -1377,10 +1398,10 @@ void launch_head_grad_reduce(const HeadDesc& hd, const float* hg_partial,
                              const double* loss_partial, const LossLaunch& ll, float* grad,
                              StepStatsDev* st, cudaStream_t s, const float* bias_partial) {
   const long nw = long(hd.A + 1) * hd.H;
-  head_grad_reduce_kernel<<<ceil_div(nw, 32), rows_reduce_threads(nw), 0, s>>>(
+  ::tlg::launch_k(head_grad_reduce_kernel, dim3(ceil_div(nw, 32)), dim3(rows_reduce_threads(nw)), size_t(0), s, 
       hd, hg_partial, ll.stream_blocks, grad);
   TLG_CHECK_LAUNCH();
-  head_bias_stats_kernel<<<1, 32 * (hd.A + 1 + 5), 0, s>>>(
+  ::tlg::launch_k(head_bias_stats_kernel, dim3(1), dim3(32 * (hd.A + 1 + 5)), size_t(0), s, 
       hd, bias_partial ? bias_partial : hg_partial + long(ll.stream_blocks) * nw, loss_partial,
       ll.math_blocks, grad, st);
   TLG_CHECK_LAUNCH();
@@ -1388,7 +1409,7 @@ void launch_head_grad_reduce(const HeadDesc& hd, const float* hg_partial,
 
 void launch_rows_reduce(const float* partial, int rows, long cols, long stride, float* out,
                         cudaStream_t s) {
-  rows_reduce_kernel<<<ceil_div(cols, 32), rows_reduce_threads(cols), 0, s>>>(partial, rows, cols,
+  ::tlg::launch_k(rows_reduce_kernel, dim3(ceil_div(cols, 32)), dim3(rows_reduce_threads(cols)), size_t(0), s, partial, rows, cols,
                                                                              stride, out);
   TLG_CHECK_LAUNCH();
 }
@@ -1401,11 +1422,11 @@ void launch_dw_reduce(const float* ws, int splits, long n, float* grad, cudaStre
     return;
   }
   if ((n & 3) == 0 && (reinterpret_cast<uintptr_t>(grad) & 15) == 0) {
-    dw_reduce_kernel<<<grid_for(n / 4, 256), 256, 0, s>>>(reinterpret_cast<const float4*>(ws),
+    ::tlg::launch_k(dw_reduce_kernel, dim3(grid_for(n / 4, 256)), dim3(256), size_t(0), s, reinterpret_cast<const float4*>(ws),
                                                           splits, n / 4, n / 4,
                                                           reinterpret_cast<float4*>(grad));
   } else {
-    dw_reduce_scalar_kernel<<<grid_for(n, 256), 256, 0, s>>>(ws, splits, n, grad);
+    ::tlg::launch_k(dw_reduce_scalar_kernel, dim3(grid_for(n, 256)), dim3(256), size_t(0), s, ws, splits, n, grad);
   }
   TLG_CHECK_LAUNCH();
 }
@@ -1414,9 +1435,9 @@ void launch_colsum(const float* x, long ld, long rows, int cols, float* partial,
                    cudaStream_t s) {
   const int chunks = ceil_div(rows, kColRows);
   dim3 grid(ceil_div(cols, 256), chunks);
-  colsum_partial_kernel<<<grid, 256, 0, s>>>(x, ld, rows, cols, partial);
+  ::tlg::launch_k(colsum_partial_kernel, dim3(grid), dim3(256), size_t(0), s, x, ld, rows, cols, partial);
   TLG_CHECK_LAUNCH();
-  colsum_reduce_kernel<<<ceil_div(cols, 256), 256, 0, s>>>(partial, chunks, cols, grad);
+  ::tlg::launch_k(colsum_reduce_kernel, dim3(ceil_div(cols, 256)), dim3(256), size_t(0), s, partial, chunks, cols, grad);
   TLG_CHECK_LAUNCH();
 }
 
@@ -1424,7 +1445,7 @@ void launch_optimizer(float* params, float* params_lo, const float* grad, float*
                       long n, float grad_scale, int adam, float lr, float step_size,
                       float bc2_sqrt, float b1, float b2, float eps, cudaStream_t s) {
   // n is padded to a multiple of 4 by the allocator
-  optimizer_kernel<<<grid_for(n / 4, 256, 4), 256, 0, s>>>(
+  ::tlg::launch_k(optimizer_kernel, dim3(grid_for(n / 4, 256, 4)), dim3(256), size_t(0), s, 
       reinterpret_cast<float4*>(params), reinterpret_cast<float4*>(params_lo),
       reinterpret_cast<const float4*>(grad), reinterpret_cast<float4*>(m),
       reinterpret_cast<float4*>(v), n / 4, grad_scale, adam, lr, step_size, bc2_sqrt, b1, b2,
