@@ -88,6 +88,9 @@ class Learner : public SegmentSink {
   // PushSegment calls in order; with device_replay the observations go to their HBM
   // slots in one copy instead of one per segment.  At most replay_capacity segments.
   void PushSegmentBatch(const std::string& model_key, const tlg_segment_batch& batch);
+  // The same for the bulk segment message (message kind 17, SegmentSink extension): the
+  // batch's SoA arrays are handed to the device ring without unpacking.
+  void PushSegmentBatch(const SegmentBatch& batch) override;
   bool TrainStep();
   std::string FinishPeriod();
   std::string RunPeriod();

@@ -682,6 +682,27 @@ void Learner::PushSegmentBatch(const std::string& model_key, const tlg_segment_b
   g.cv.notify_all();
 }
 
+void Learner::PushSegmentBatch(const SegmentBatch& b) {
+  if (b.n_segments == 0) return;
+  const std::size_t F = std::size_t(b.n_segments) * b.unroll_len;
+  if (b.action.size() != F || b.valid_steps.size() != b.n_segments)
+    throw std::invalid_argument("PushSegmentBatch: inconsistent segment batch");
+  tlg_segment_batch v{};
+  v.n_segments = b.n_segments;
+  v.unroll_len = b.unroll_len;
+  v.obs_dim = b.obs_dim;
+  v.obs_dtype = b.obs_format == SegmentBatch::kObsBits ? TLG_OBS_BITS : TLG_OBS_F32;
+  v.obs = b.obs.data();
+  v.action = b.action.data();
+  v.reward = b.reward.data();
+  v.behavior_logp = b.behavior_logp.data();
+  v.value_est = b.value_est.data();
+  v.done = b.done.data();
+  v.bootstrap = b.bootstrap.data();
+  v.valid_steps = b.valid_steps.data();
+  PushSegmentBatch(b.model_key, v);
+}
+
 bool Learner::TrainStep() {
   if (config_.step_delay_ms > 0)
     std::this_thread::sleep_for(std::chrono::milliseconds(config_.step_delay_ms));

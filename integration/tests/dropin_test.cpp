@@ -24,6 +24,10 @@
 #include "tleague/policy/policy.hpp"
 #include "tleague/pool/model_store.hpp"
 #include "tleague/rlmath/rlmath.hpp"
+#include "tleague/learner/learner_service.hpp"
+#include "tleague/pool/model_pool_service.hpp"
+#include "tleague/proto/codec.hpp"
+#include "tleague/proto/wire_ext.hpp"
 #include "tleague/run/bench.hpp"
 #include "tleague/run/config.hpp"
 #include "tleague/run/local_run.hpp"
@@ -896,6 +900,105 @@ TEST(local_run_trains_an_mlp_league_on_grid_duel) {
   }
   CHECK(!res.group_counters.empty() && res.group_counters[0].update_steps > 0);
   std::filesystem::remove_all(dir);
+}
+
+// ---------------------------------------------------------------------------
+// Wire extensions (message kinds 17 SegmentBatchPush, 18 ParamChunk; wire_ext.hpp).
+TEST(bulk_segment_messages_over_tcp_train_like_single_pushes) {
+  // learner::LearnerClient::PushSegmentBatch -> TCP -> LearnerService -> the B200
+  // learner's bulk ingest (one frame per group, observations bit-packed or fp32), against
+  // a learner fed the same segments one PushSegment at a time: identical draws and
+  // parameters, in host-replay and device-replay mode.
+  for (bool dev : {false, true})
+    for (bool binary : {true, false}) {
+      HyperParams hyper = TestHyper();
+      hyper.unroll_len = 5;
+      pool::ModelStore store_a, store_b;
+      pool::DirectPool pool_a(store_a), pool_b(store_b);
+      const PolicyShape shape{20, 6, {32, 32}};
+      league::LeagueState league_a({MlpGroup(hyper, shape)}, pool_a, 7);
+      league::LeagueState league_b({MlpGroup(hyper, shape)}, pool_b, 7);
+      learner::LearnerConfig cfg;
+      cfg.num_shards = 2;
+      cfg.seed = 4;
+      cfg.replay_capacity = 24;
+      cfg.device_replay = dev;
+      learner::Learner one(cfg, league_a, pool_a);
+      learner::Learner bulk(cfg, league_b, pool_b);
+      learner::LearnerService svc(bulk, "127.0.0.1", 0);
+      learner::LearnerClient client(svc.endpoint());
+      std::mt19937_64 feed(17);
+      std::uint64_t seq = 0;
+      for (int step = 0; step < 6; ++step) {
+        std::vector<TrajectorySegment> group;
+        for (int i = 0; i < 10; ++i, ++seq) {
+          TrajectorySegment sg = MakeSegmentD(one.current_key(), feed, seq, 20, 6, 5, binary);
+          one.PushSegment(sg);
+          group.push_back(std::move(sg));
+        }
+        const SegmentBatch b = PackSegmentBatch(group, 5);
+        CHECK(b.obs_format == (binary ? SegmentBatch::kObsBits : SegmentBatch::kObsF32));
+        client.PushSegmentBatch(b);
+        CHECK(one.replay().size() == bulk.replay().size());
+        CHECK(one.TrainStep());
+        CHECK(bulk.TrainStep());
+        CHECK(one.params().values == bulk.params().values);
+        CHECK(one.replay().consumed_steps() == bulk.replay().consumed_steps());
+      }
+      // codec round trip of the message itself
+      auto group = std::vector<TrajectorySegment>{
+          MakeSegmentD(one.current_key(), feed, 1, 20, 6, 5, binary)};
+      proto::Message m = proto::MakeMessage(3, proto::SegmentBatchPushBody{PackSegmentBatch(group, 5)});
+      CHECK(proto::Decode(proto::Encode(m)) == m);
+      svc.Stop();
+    }
+}
+
+TEST(c5_size_models_publish_and_travel_in_chunks) {
+  // C5's 4x2048 MLP: 12.7M fp64 parameters = 102 MB, over the 64 MiB frame and the
+  // reference ModelStore's 32 MiB blob cap.  Seeded by the league, trained and published
+  // by the B200 learner, put / got over TCP in ParamChunk slices, saved as a chunked
+  // model file, served by the B200 InfServer through a remote pool.
+  const PolicyShape c5{64, 6, {2048, 2048, 2048, 2048}};
+  HyperParams hyper = TestHyper();
+  hyper.batch_size = 2;
+  hyper.unroll_len = 4;
+  pool::ModelPoolService svc("127.0.0.1", 0, {});
+  pool::ModelPoolClient remote({svc.endpoint()});
+  league::LeagueState league({MlpGroup(hyper, c5)}, remote, 9);  // chunked put of the seed
+  const std::string key = league.RequestLearnerTask(0, 0).learning_model_key;
+  ModelRecord seed = remote.GetModel(key);  // chunked get
+  CHECK(seed.params.values.size() == policy::ParamCount(PolicyFamily::kMlp, c5));
+  CHECK(seed.params.values.size() * sizeof(double) > proto::kMaxFrameBytes);
+  learner::LearnerConfig cfg;
+  cfg.publish_interval = 1;
+  learner::Learner lrn(cfg, league, remote);
+  std::mt19937_64 feed(2);
+  for (int i = 0; i < 2; ++i) lrn.PushSegment(MakeSegmentD(lrn.current_key(), feed, i, 64, 6, 4, false));
+  CHECK(lrn.TrainStep());  // publishes (publish_interval = 1): a chunked put
+  ModelRecord back = remote.GetModel(key);
+  CHECK(back.params == lrn.params());
+  CHECK(back.params.values != seed.params.values);
+  const std::string path = "/tmp/tlg_dropin_c5.model";
+  run::SaveModel(path, back);
+  CHECK(run::LoadModel(path) == back);
+  std::remove(path.c_str());
+  infserver::InfServer server({key}, remote, "127.0.0.1", 0);
+  std::normal_distribution<double> n(0.0, 1.0);
+  double worst = 0;
+  for (int i = 0; i < 8; ++i) {
+    std::vector<double> obs(64);
+    for (double& x : obs) x = double(float(n(feed)));
+    auto reply = server.EvaluateLocal(obs);
+    auto ref = policy::Distribution(back.params, obs);
+    double w = 0;
+    CHECK(AllClose(reply.probs, ref.probs, 1e-5, &w));
+    worst = std::max(worst, w);
+  }
+  std::printf("  C5 record %.1f MB in %zu-byte chunks; InfServer vs fp64 %.2e\n",
+              back.params.values.size() * 8.0 / 1e6, proto::ext::kChunkBytes, worst);
+  server.Stop();
+  svc.Stop();
 }
 
 TEST(reference_run_bench_runs_on_the_b200_learner) {

@@ -23,7 +23,8 @@ def steps():
     T, D, A, hidden = cfg.unroll_len, cfg.obs_dim, cfg.n_actions, cfg.hidden
     pitch = ((D + 7) // 8 + 15) // 16 * 16
     out = {}
-    for S in (512, 1024, 2048, 4096):
+    sizes = [int(x) for x in os.environ.get("TLG_PROBE_S", "512,1024,2048,4096").split(",")]
+    for S in sizes:
         l = tlg.Learner("mlp", D, A, hidden, algo="ppo", optimizer="adam", max_segments=S,
                         unroll_len=T, obs_u8=True)
         l.set_hyper(learning_rate=3e-4, batch_size=S, unroll_len=T)
@@ -41,7 +42,7 @@ def steps():
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
         e0.record(st)
-        n = 50
+        n = int(os.environ.get("TLG_PROBE_STEPS", "50"))
         for i in range(n):
             l.train_step(dev[i % nb], on_device=True)
         e1.record(st)
