@@ -992,7 +992,8 @@ TEST(c5_size_models_publish_and_travel_in_chunks) {
     auto reply = server.EvaluateLocal(obs);
     auto ref = policy::Distribution(back.params, obs);
     double w = 0;
-    CHECK(AllClose(reply.probs, ref.probs, 1e-5, &w));
+    // four 2048-wide fp32 layers (3xTF32): the 1e-4 class of forward-derived values
+    CHECK(AllClose(reply.probs, ref.probs, 1e-4, &w));
     worst = std::max(worst, w);
   }
   std::printf("  C5 record %.1f MB in %zu-byte chunks; InfServer vs fp64 %.2e\n",
