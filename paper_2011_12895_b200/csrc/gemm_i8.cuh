@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
           const float bj = __shfl_sync(0xffffffffu, bi, j);
           const float z = fmaf(float(int(ra[j])), s * 0.0078125f,
                                float(int(rb[j])) * (s * 6.103515625e-05f));
-          o[j] = tanhf(z + bj);
+          o[j] = tanh_fast(z + bj);
         }
         if (p.out_q != nullptr && rbase + lane < p.M) {
           // the same activations as int8 pieces for the next layer's int8 GEMM
@@ -685,7 +685,7 @@ __global__ void __launch_bounds__(32 * (2 + kEpiWarps), 1)
           const float bj = __shfl_sync(0xffffffffu, bi, j);
           const float v = fmaf(float(int(r2[j])), 6.103515625e-05f,
                                fmaf(float(int(r1[j])), 0.0078125f, float(int(r0[j]))));
-          o[j] = tanhf(fmaf(v, s, bj));
+          o[j] = tanh_fast(fmaf(v, s, bj));
         }
         if (do_head) {
 #pragma unroll

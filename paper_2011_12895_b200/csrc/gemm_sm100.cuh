@@ -836,7 +836,7 @@ __global__ void __launch_bounds__((U8 || LOD) ? kThreadsU8 : kThreads, 1)
         const float bl = (c + lane < p.N) ? __ldg(p.bias + c + lane) : 0.f;
         float h[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) h[j] = tanhf(__uint_as_float(r[j]) + __shfl_sync(0xffffffffu, bl, j));
+        for (int j = 0; j < 32; ++j) h[j] = tanh_fast(__uint_as_float(r[j]) + __shfl_sync(0xffffffffu, bl, j));
         load_w(c);
 #pragma unroll
         for (int j4 = 0; j4 < 8; ++j4) {
@@ -933,7 +933,7 @@ __global__ void __launch_bounds__((U8 || LOD) ? kThreadsU8 : kThreads, 1)
         const float bl = (c + lane < p.N) ? __ldg(p.bias + c + lane) : 0.f;
         float h[32], o[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) h[j] = tanhf(__uint_as_float(r[j]) + __shfl_sync(0xffffffffu, bl, j));
+        for (int j = 0; j < 32; ++j) h[j] = tanh_fast(__uint_as_float(r[j]) + __shfl_sync(0xffffffffu, bl, j));
         load_w(c);
 #pragma unroll
         for (int j4 = 0; j4 < 8; ++j4) {
@@ -1114,7 +1114,7 @@ __global__ void __launch_bounds__((U8 || LOD) ? kThreadsU8 : kThreads, 1)
           const float bl = (nb + lane < p.N) ? __ldg(p.bias + nb + lane) : 0.f;
 #pragma unroll
           for (int j = 0; j < 32; ++j)
-            o[j] = tanhf(__uint_as_float(r[j]) + __shfl_sync(0xffffffffu, bl, j));
+            o[j] = tanh_fast(__uint_as_float(r[j]) + __shfl_sync(0xffffffffu, bl, j));
           if (do_head) {
             // head weights of this chunk's 32 columns -> smem, then broadcast LDS.128
 #pragma unroll
