@@ -214,9 +214,9 @@ METRIC = "learner frames/sec at 1/2/4/8 B200 + InferenceServer actions/sec vs CP
 
 def _ncu_traffic(kernel="fwd1"):
     """dram__bytes_read + dram__bytes_write of the dominant kernel per launch, from the
-    committed ncu --set full capture (profiles/r01_<kernel>_ncu.json)."""
+    committed ncu --set full capture (profiles/r02_<kernel>_ncu.json)."""
     try:
-        with open(os.path.join(ROOT, "profiles", f"r01_{kernel}_ncu.json")) as f:
+        with open(os.path.join(ROOT, "profiles", f"r02_{kernel}_ncu.json")) as f:
             return json.load(f)["traffic_bytes_per_launch"]
     except Exception:
         return None

@@ -353,9 +353,13 @@ LaunchInfo launch_i8_bits_fwd(const uint8_t* bits, long rowb, const int8_t* q, l
                               int8_t* out_q) {
   if (M <= 0 || N <= 0 || K <= 0) throw CudaError("gemm_i8: empty problem");
   if (rowb * 8 < K || Kp < K) throw CudaError("gemm_i8: K exceeds the operand rows");
-  constexpr int BN = 128;
+  // 128-wide tiles (double-buffered accumulators); TLG_I8_BN=256 (experiment): one tile
+  // spans N = 256 (the x tiles are expanded once per M tile, accumulators single-buffered)
+  const int BN = std::getenv("TLG_I8_BN") && std::atoi(std::getenv("TLG_I8_BN")) == 256 && N > 128
+                     ? 256 : 128;
   // CTA pairs (256-row tiles) whenever there are enough of them to fill the GPU
   int cg = (M >= 2 * kBM && long(ceil_div(M, 2 * kBM)) * ceil_div(N, BN) >= num_sms() / 2) ? 2 : 1;
+  if (BN == 256) cg = 2;
   if (const char* e = std::getenv("TLG_I8_CG")) cg = std::atoi(e) == 2 ? 2 : 1;
   // TLG_I8_MC=2: two CTA pairs per cluster share the weight-piece tiles (TMA multicast).
   // Correct, but measured 1.9x slower at C3 (the pairs run in lockstep on the shared
@@ -372,9 +376,10 @@ LaunchInfo launch_i8_bits_fwd(const uint8_t* bits, long rowb, const int8_t* q, l
   const CUtensorMap tq = make_bytes_map(q, Kp, 3L * N, Kp, kBKi, BN / cg, CU_TENSOR_MAP_SWIZZLE_128B);
   const CUtensorMap to = make_f32_out_map(out, N, M, ldo);
   const CUtensorMap tl = out_lo ? make_f32_out_map(out_lo, N, M, ldo) : CUtensorMap{};
-  if (mc == 2) run_i8_fwd<BN, 2, 2>(tb, tq, to, tl, p, tm, stream);
-  else if (cg == 2) run_i8_fwd<BN, 2>(tb, tq, to, tl, p, tm, stream);
-  else run_i8_fwd<BN, 1>(tb, tq, to, tl, p, tm, stream);
+  if (BN == 256) run_i8_fwd<256, 2>(tb, tq, to, tl, p, tm, stream);
+  else if (mc == 2) run_i8_fwd<128, 2, 2>(tb, tq, to, tl, p, tm, stream);
+  else if (cg == 2) run_i8_fwd<128, 2>(tb, tq, to, tl, p, tm, stream);
+  else run_i8_fwd<128, 1>(tb, tq, to, tl, p, tm, stream);
   const int tiles = tm.m_tiles * tm.n_tiles;
   const int cl = cg * mc;
   return {BN, cl * std::min(tiles, num_sms() / cl)};  // upper bound on the CTAs launched

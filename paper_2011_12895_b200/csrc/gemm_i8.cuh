@@ -84,7 +84,10 @@ struct SmemI8 {
   static constexpr int kNumBars = 3 * kStages + 2 * kRing + 4;
   static constexpr int kEpiOff = (kBarOff + kNumBars * 8 + 16 + 1023) / 1024 * 1024;
   static constexpr int kBytes = kEpiOff + kEpi + 1024;
-  static constexpr int kTmemCols = 4 * BN;  // 2 accumulators x double buffer
+  // 2 accumulators, double-buffered while they fit TMEM's 512 columns (BN <= 128); a
+  // 256-wide tile keeps one buffer (the epilogue then drains before the next tile's MMAs)
+  static constexpr int kBufs = 4 * BN <= 512 ? 2 : 1;
+  static constexpr int kTmemCols = 2 * BN * kBufs;
   static_assert(kStage % 1024 == 0, "stages must keep the 1 KB swizzle alignment");
   static_assert(kStages >= 2, "pipeline needs two stages");
   static_assert(kTmemCols <= 512, "TMEM has 512 columns");
@@ -304,8 +307,8 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
       uint32_t phase = 0;
       int it = 0;
       for (int t = cl_id; t < num_tiles; t += n_cl, ++it) {
-        const int acc_buf = it & 1;
-        mbar_wait(bar_tempty + 8 * acc_buf, ((it >> 1) & 1) ^ 1);
+        const int acc_buf = it % S::kBufs;
+        mbar_wait(bar_tempty + 8 * acc_buf, ((it / S::kBufs) & 1) ^ 1);
         tc_fence_after();
         const uint32_t tacc_a = tmem_base + uint32_t(acc_buf * 2 * BN);
         const uint32_t tacc_b = tacc_a + uint32_t(BN);
@@ -381,8 +384,8 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
       const int nt = t % tm.n_tiles, mt = t / tm.n_tiles;
       const int m0 = mt * kRowsT + int(pair) * kBM * CG + int(rank) * kBM, n0 = nt * BN;
       const int rbase = m0 + q * 32;
-      const int acc_buf = it & 1;
-      mbar_wait(bar_tfull + 8 * acc_buf, (it >> 1) & 1);
+      const int acc_buf = it % S::kBufs;
+      mbar_wait(bar_tfull + 8 * acc_buf, (it / S::kBufs) & 1);
       tc_fence_after();
       const uint32_t ta = tmem_base + uint32_t(acc_buf * 2 * BN) + (uint32_t(q * 32) << 16);
       const uint32_t tb = ta + uint32_t(BN);
