@@ -75,6 +75,18 @@ void ParallelRanges(std::size_t n, std::size_t work, F&& fn) {
     if (e) std::rethrow_exception(e);
 }
 
+// The device-replay entry the reference ReplayMem holds for a segment whose data lives in
+// an HBM slot: ReplayMem reads only valid_steps (received / consumed counters,
+// replay_mem.cpp:16,40), so the steps themselves are not copied; segment_seq carries the
+// private id of the slot mirror.
+TrajectorySegment ReplayEntry(const std::string& key, std::uint32_t valid_steps, double boot) {
+  TrajectorySegment e;
+  e.model_key = key;
+  e.valid_steps = valid_steps;
+  e.bootstrap_value = boot;
+  return e;
+}
+
 template <typename T>
 struct Pinned {
   T* p = nullptr;
@@ -569,11 +581,8 @@ void Learner::PushSegment(const TrajectorySegment& segment) {
     g.ring_decided = true;
   }
   g.Prepare(segment);  // throws on a bad segment before the mirror changes
-  TrajectorySegment stripped = segment;
-  for (SegmentStep& st : stripped.steps) {
-    st.obs.clear();
-    st.obs.shrink_to_fit();
-  }
+  TrajectorySegment stripped = ReplayEntry(segment.model_key, segment.valid_steps,
+                                           segment.bootstrap_value);
   Gpu::Undo undo = g.BeginAdmit();
   try {
     const std::uint32_t slot = g.Admit(config_.replay_capacity, undo);
@@ -657,11 +666,7 @@ void Learner::PushSegmentBatch(const std::string& model_key, const tlg_segment_b
   // observation-less entries first (nothing below can fail on the caller's data)
   std::vector<TrajectorySegment> stripped(b.n_segments);
   for (std::uint32_t i = 0; i < b.n_segments; ++i) {
-    stripped[i] = SegmentFromSoa(b, i, model_key);
-    for (SegmentStep& st : stripped[i].steps) {
-      st.obs.clear();
-      st.obs.shrink_to_fit();
-    }
+    stripped[i] = ReplayEntry(model_key, std::uint32_t(b.valid_steps[i]), b.bootstrap[i]);
   }
   // admit in order (mirrors n ReplayMem::Push evictions), one device copy, then the
   // entries in the same order; any failure restores the mirror
