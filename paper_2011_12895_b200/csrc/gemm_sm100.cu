@@ -163,17 +163,10 @@ void dispatch_bn(bool a_mn, bool b_mn, bool a_lo, bool b_lo, int epi, int u8, in
   // derived lo planes (Operand::lo_smem): the learner's activations / dZ / observations
   if (lod) {
     if (u8) throw CudaError("gemm: derived lo planes need fp32 operands");
-    // K-major A with a derived lo: its hi tiles stream through the A ring (lod 5)
-    if (!a_mn && !b_mn && a_lo && b_lo && epi == kEpiFwdTanh && lod == 5)
-      return run_if_fits<BN, false, false, true, true, kEpiFwdTanh, 0, 5>(ah, al, bh, bl, em, p, grid, s);
     if (!a_mn && !b_mn && a_lo && b_lo && epi == kEpiFwdTanh && lod == 1)
       return run_if_fits<BN, false, false, true, true, kEpiFwdTanh, 0, 1>(ah, al, bh, bl, em, p, grid, s);
-    if (!a_mn && !b_mn && a_lo && b_lo && epi == kEpiFwdLoss && lod == 5)
-      return run_if_fits<BN, false, false, true, true, kEpiFwdLoss, 0, 5>(ah, al, bh, bl, em, p, grid, s);
     if (!a_mn && !b_mn && a_lo && b_lo && epi == kEpiFwdLoss && lod == 1)
       return run_if_fits<BN, false, false, true, true, kEpiFwdLoss, 0, 1>(ah, al, bh, bl, em, p, grid, s);
-    if (!a_mn && b_mn && a_lo && b_lo && epi == kEpiBwdTanh && lod == 5)
-      return run_if_fits<BN, false, true, true, true, kEpiBwdTanh, 0, 5>(ah, al, bh, bl, em, p, grid, s);
     if (!a_mn && b_mn && a_lo && b_lo && epi == kEpiBwdTanh && lod == 1)
       return run_if_fits<BN, false, true, true, true, kEpiBwdTanh, 0, 1>(ah, al, bh, bl, em, p, grid, s);
     if (a_mn && b_mn && a_lo && b_lo && epi == kEpiStore && lod == 3)
@@ -254,9 +247,7 @@ LaunchInfo launch(const Operand& A, const Operand& B, int M, int N, int K, int e
   if (M <= 0 || N <= 0 || K <= 0) throw CudaError("gemm: empty problem");
   const bool a_lo0 = (A.lo != nullptr || A.lo_smem) && !A.u8,
              b_lo0 = (B.lo != nullptr || B.lo_smem) && !B.u8;
-  int lod = (A.lo_smem && !A.u8 ? 1 : 0) | (B.lo_smem && !B.u8 ? 2 : 0);
-  // a streamed K-major A with a derived residual: A ring (TLG_NO_ARING=1: in the stages)
-  if (lod == 1 && !A.mn_major && epi != kEpiStore && !std::getenv("TLG_NO_ARING")) lod = 5;
+  const int lod = (A.lo_smem && !A.u8 ? 1 : 0) | (B.lo_smem && !B.u8 ? 2 : 0);
   const int u8_0 = A.u8 ? 1 : B.u8 ? 2 : 0;
   if (epi == kEpiBwdTanh && p.colsum != nullptr && N > kColMax)
     throw CudaError("gemm: fused column sums need N <= 2048");

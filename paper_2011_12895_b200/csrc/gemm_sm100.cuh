@@ -277,24 +277,19 @@ constexpr int plan_stages(int stage, int epi_bytes, int ring_bytes) {
 // lod: bit 0 / bit 1 = the lo plane of A / B is derived in shared memory from the hi tile
 // (lo = x - trunc_tf32(x), elementwise, so any swizzled layout) by the converter warps
 // instead of being TMA-loaded from a residual plane in HBM.
-// lod bit 2 (with bit 0, K-major A): the A hi tiles stream through their own ring of
-// slots, TMA'd up to that many k-blocks ahead of the stages (HBM latency hiding for the
-// streamed activation / dZ operand), and a stage holds only A lo (derived) and B.
 constexpr SmemPlan smem_plan(int BN, bool a_lo, bool b_lo, int epi, int u8, int cg, int lod = 0) {
   SmemPlan q{};
   const int kA = kBM * kBK * 4;          // 16 KB
   const int kB = (BN / cg) * kBK * 4;    // B rows held by this CTA (a pair splits N)
-  const bool ar = (lod & 4) != 0;
-  q.stage = kA * (a_lo ? 2 : 1) + kB * (b_lo ? 2 : 1) - (ar ? kA : 0);
-  q.tma_bytes = q.stage - (u8 == 1 ? kA : u8 == 2 ? kB : 0) - ((lod & 1) && !ar ? kA : 0) -
-                ((lod & 1) && ar ? kA : 0) - ((lod & 2) ? kB : 0);
+  q.stage = kA * (a_lo ? 2 : 1) + kB * (b_lo ? 2 : 1);
+  q.tma_bytes = q.stage - (u8 == 1 ? kA : u8 == 2 ? kB : 0) - ((lod & 1) ? kA : 0) -
+                ((lod & 2) ? kB : 0);
   // a uint8 operand's byte tiles stream through their own ring (u8_ring slots), filled
   // by the producer up to u8_ring k-blocks ahead of the fp32 stages, so only the
   // conversion itself sits on the MMA's critical path.
-  q.u8_slot = ar ? kA : u8 == 1 ? kBM * kBK : u8 == 2 ? (BN / cg) * kBK : 0;
-  q.u8_ring = ar ? 4
-              : u8 == 0 ? 0 : (16384 / q.u8_slot) < 2 ? 2 : (16384 / q.u8_slot) > 8 ? 8
-                                                                                : (16384 / q.u8_slot);
+  q.u8_slot = u8 == 1 ? kBM * kBK : u8 == 2 ? (BN / cg) * kBK : 0;
+  q.u8_ring = u8 == 0 ? 0 : (16384 / q.u8_slot) < 2 ? 2 : (16384 / q.u8_slot) > 8 ? 8
+                                                                                 : (16384 / q.u8_slot);
   // per epilogue warp: 4 KB TMA-store staging for out, another for out_lo, + a 4 KB
   // TMA-prefetched activation block (bwd), + 1 KB of head weights (fwd).  out and out_lo
   // share one block (stores serialised) when that buys the pipeline a third stage: the
@@ -318,8 +313,7 @@ constexpr SmemPlan smem_plan(int BN, bool a_lo, bool b_lo, int epi, int u8, int 
   // full/empty per stage, tmem full/empty x2, act-block full x4, converted per stage,
   // u8 ring full/empty per slot
   q.num_bars = 2 * q.stages + 4 + kEpiWarps + (u8 ? q.stages + 2 * q.u8_ring : 0) +
-               (lod ? 2 * q.stages : 0) +  // lod: converted + local hi-landed per stage
-               (ar ? 2 * q.u8_ring : 0);   // A ring full / empty
+               (lod ? 2 * q.stages : 0);  // lod: converted + local hi-landed per stage
   q.epi_off = (q.bar_off + q.num_bars * 8 + 16 + 1023) / 1024 * 1024;
   q.bytes = q.epi_off + kEpiWarps * q.warp_epi + q.extra + 1024;  // + 1 KB alignment slack
   return q;
@@ -450,11 +444,6 @@ __global__ void __launch_bounds__((U8 || LOD) ? kThreadsU8 : kThreads, 1)
   static_assert(!(U8 && LOD), "derived lo planes and uint8 operands do not mix");
   static_assert(!(LOD & 1) || A_LO, "A lo derived needs the A lo slot");
   static_assert(!(LOD & 2) || B_LO, "B lo derived needs the B lo slot");
-  constexpr bool AR = (LOD & 4) != 0;  // A hi through its own ring (K-major A, lo derived)
-  static_assert(!AR || ((LOD & 1) && !A_MN), "the A ring serves a K-major A with derived lo");
-  // offsets inside a stage
-  constexpr int kOffALo = AR ? 0 : S::kA;
-  constexpr int kOffBHi = AR ? S::kA : S::kA * (A_LO ? 2 : 1);
   // CG == 2: a cluster of two CTAs shares each (256 x BN) tile; rank r owns rows
   // [128 r, 128 r + 128) of A / D and B rows [r BN/2, (r+1) BN/2).  Only rank 0 issues
   // the MMAs (cta_group::2), reading both CTAs' smem and writing both CTAs' TMEM.
@@ -485,11 +474,6 @@ __global__ void __launch_bounds__((U8 || LOD) ? kThreadsU8 : kThreads, 1)
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA_hi);
-    if (AR)
-      for (int u = 0; u < S::kU8Ring; ++u) {
-        mbar_init(bar_ufull + 8 * u, 1);   // A hi landed (local tx count)
-        mbar_init(bar_uempty + 8 * u, 1);  // the MMAs that read it completed (commit)
-      }
     prefetch_tmap(&tmB_hi);
     if (A_LO && !(LOD & 1)) prefetch_tmap(&tmA_lo);
     if (B_LO && !(LOD & 2)) prefetch_tmap(&tmB_lo);
@@ -559,12 +543,12 @@ __global__ void __launch_bounds__((U8 || LOD) ? kThreadsU8 : kThreads, 1)
       KCursor cf;
       cf.init(cl_id, n_cl, num_tiles, tm, p.kb_per_split, kb_total);
       for (; cf.valid(num_tiles); cf.next(n_cl, num_tiles, tm, p.kb_per_split, kb_total), ++done_fp32) {
-        if (U8 || AR) {
+        if (U8) {
           while (cu.valid(num_tiles) && issued_u8 < done_fp32 + S::kU8Ring) {
             mbar_wait(bar_uempty + 8 * ui, uph ^ 1);
             mbar_expect_tx(bar_ufull + 8 * ui, S::kU8);
             const uint32_t dst = sbase + S::kRingOff + ui * S::kU8;
-            if (U8 == 1 || AR)  // u8 box {32 k, 128 m}, or the fp32 A hi tile
+            if (U8 == 1)  // u8 box {32 k, 128 m}
               tma_load_2d(dst, &tmA_hi, cu.kb * kBK, cu.mt * kBM * CG + int(rank) * kBM,
                           bar_ufull + 8 * ui);
             else          // u8 box {BN/CG n, 32 k}
@@ -593,8 +577,8 @@ __global__ void __launch_bounds__((U8 || LOD) ? kThreadsU8 : kThreads, 1)
           else if (rank == 0) mbar_expect_tx(bar_full + 8 * stage, S::kTmaBytes * CG);
           const int k0 = kb * kBK;
           uint32_t off = st;
-          if (U8 == 1 || AR) {
-            // converted by the converter warps / streamed through the A ring
+          if (U8 == 1) {
+            // converted by the converter warps
           } else if (!A_MN) {
             TMA_FP32(off, &tmA_hi, k0, m0, full);
             if (A_LO && !(LOD & 1)) TMA_FP32(off + S::kA, &tmA_lo, k0, m0, full);
@@ -606,7 +590,7 @@ __global__ void __launch_bounds__((U8 || LOD) ? kThreadsU8 : kThreads, 1)
                 TMA_FP32(off + S::kA + j * 4096, &tmA_lo, m0 + 32 * j, k0, full);
             }
           }
-          off = st + kOffBHi;
+          off += S::kA * (A_LO ? 2 : 1);
           if (U8 == 2) {
             // converted by the converter warps
           } else if (!B_MN) {
@@ -634,7 +618,6 @@ __global__ void __launch_bounds__((U8 || LOD) ? kThreadsU8 : kThreads, 1)
       constexpr uint32_t idesc = make_idesc<BN, A_MN, B_MN, CG>();
       int stage = 0;
       uint32_t phase = 0;
-      int ri = 0;  // A ring slot (AR)
       int it = 0;
       for (int t = cl_id; t < num_tiles; t += n_cl, ++it) {
         int mt, nt, sp;
@@ -649,10 +632,9 @@ __global__ void __launch_bounds__((U8 || LOD) ? kThreadsU8 : kThreads, 1)
           if (!LOD) mbar_wait(bar_full + 8 * stage, phase);
           if (U8 || LOD) mbar_wait(bar_conv + 8 * stage, phase);
           tc_fence_after();
-          const uint32_t st = sbase + stage * S::kStage;
-          const uint32_t a_hi = AR ? sbase + S::kRingOff + ri * S::kU8 : st;
-          const uint32_t a_lo = st + kOffALo;
-          const uint32_t b_hi = st + kOffBHi;
+          const uint32_t a_hi = sbase + stage * S::kStage;
+          const uint32_t a_lo = a_hi + S::kA;
+          const uint32_t b_hi = a_hi + S::kA * (A_LO ? 2 : 1);
           const uint32_t b_lo = b_hi + S::kB;
 #pragma unroll
           for (int k = 0; k < kBK / 8; ++k) {
@@ -677,11 +659,6 @@ __global__ void __launch_bounds__((U8 || LOD) ? kThreadsU8 : kThreads, 1)
           }
           if (CG == 2) mma_commit_pair(bar_empty + 8 * stage);
           else mma_commit(bar_empty + 8 * stage);
-          if (AR) {  // the A hi slot goes back to the producer
-            if (CG == 2) mma_commit_pair(bar_uempty + 8 * ri);
-            else mma_commit(bar_uempty + 8 * ri);
-            if (++ri == S::kU8Ring) ri = 0;
-          }
           if (++stage == S::kStages) {
             stage = 0;
             phase ^= 1;
@@ -699,27 +676,19 @@ __global__ void __launch_bounds__((U8 || LOD) ? kThreadsU8 : kThreads, 1)
     uint32_t phase = 0;
     KCursor cc;
     cc.init(cl_id, n_cl, num_tiles, tm, p.kb_per_split, kb_total);
-    auto derive = [&](const uint8_t* hi, uint8_t* lo, int bytes) {
+    auto derive = [&](uint8_t* hi, int bytes) {
       for (int o = ct * 16; o < bytes; o += 128 * 16) {
         const float4 x = *reinterpret_cast<const float4*>(hi + o);
-        *reinterpret_cast<float4*>(lo + o) =
+        *reinterpret_cast<float4*>(hi + bytes + o) =
             make_float4(x.x - tf32_hi(x.x), x.y - tf32_hi(x.y), x.z - tf32_hi(x.z),
                         x.w - tf32_hi(x.w));
       }
     };
-    int ri = 0;
-    uint32_t rph = 0;
     for (; cc.valid(num_tiles); cc.next(n_cl, num_tiles, tm, p.kb_per_split, kb_total)) {
-      if (AR) mbar_wait(bar_ufull + 8 * ri, rph);  // this k-block's A hi landed
-      mbar_wait(bar_hfull + 8 * stage, phase);     // this CTA's stage tiles landed
+      mbar_wait(bar_hfull + 8 * stage, phase);  // this CTA's tiles landed
       uint8_t* st = smem + stage * S::kStage;
-      if (AR) derive(smem + S::kRingOff + ri * S::kU8, st + kOffALo, S::kA);
-      else if (LOD & 1) derive(st, st + S::kA, S::kA);
-      if (LOD & 2) derive(st + kOffBHi, st + kOffBHi + S::kB, S::kB);
-      if (AR && ++ri == S::kU8Ring) {
-        ri = 0;
-        rph ^= 1;
-      }
+      if (LOD & 1) derive(st, S::kA);
+      if (LOD & 2) derive(st + S::kA * (A_LO ? 2 : 1), S::kB);
       fence_async_smem();  // generic-proxy writes -> visible to the tensor core
       __syncwarp();
       if ((threadIdx.x & 31) == 0) {
