@@ -7,10 +7,11 @@ Workload (BASELINE.json): config C3 -- Pommerman-shaped obs (11x11x16 = 1936 bin
 planes), MLP 1936-256-256-(6,1), PPO + GAE, T=32, a draw of B=4096 segments, Adam.  One
 step = one Learner::TrainStep on every rank: returns, loss fwd/bwd, NCCL gradient
 allreduce (per-layer buckets overlapped with the backward), optimizer.  N>1 is launched
-by torchrun, one rank per GPU.  --scaling strong (default): the 4096-
-segment draw is split over the G ranks (4096/G segments = HyperParams::batch_size per
-shard, learner.cpp:108,119-125); at N>1 the weak-scaling figure (4096 segments per GPU)
-is measured in the same run and reported beside it.
+by torchrun, one rank per GPU.  --scaling weak (default): B=4096 segments per learner
+shard, HyperParams::batch_size being per shard in the reference (learner.cpp:108), so G
+ranks consume a G x 4096-segment draw per step; at N>1 the strong-scaling figure (one
+4096-segment draw split over the G ranks) is measured in the same run and
+reported beside it (`strong_scaling`).  --scaling strong makes the split draw the value.
 
 * value   : frames/s with the batch already resident in HBM (whole job, all ranks),
             timed with CUDA events on the learner's stream, max over ranks.
@@ -233,8 +234,8 @@ def main():
     ap.add_argument("--obs", default="bits", choices=["bits", "u8", "f32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-infer", action="store_true")
-    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
-                    help="strong: the config's B segments split over the ranks; weak: B per rank")
+    ap.add_argument("--scaling", default="weak", choices=["strong", "weak"],
+                    help="weak: the config's B segments per rank; strong: B split over the ranks")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -347,11 +348,12 @@ def main():
     value = frames_all / (ms_total / 1e3)
     ms_per_step = ms_total / args.steps
 
-    # ---- at N>1 under strong scaling: the weak-scaling figure (the config's B per rank)
-    weak = None
-    if world > 1 and args.scaling == "strong":
-        lw = make_learner(cfg.batch_size)
-        hw, dw = make_batches(cfg.batch_size)
+    # ---- at N>1: the other scaling mode's figure, measured in the same run
+    other = None
+    if world > 1:
+        S_o = cfg.batch_size if args.scaling == "strong" else cfg.batch_size // world
+        lw = make_learner(S_o)
+        hw, dw = make_batches(S_o)
         fw = [int(h.valid_steps.sum()) for h in hw]
         for i in range(max(args.warmup, 2 * len(dw))):
             lw.train_step(dw[i % len(dw)], on_device=True)
@@ -368,8 +370,9 @@ def main():
         e1.record(sw)
         torch.cuda.synchronize()
         msw = max_over_ranks(e0.elapsed_time(e1))
-        weak = {"value": sum_over_ranks(frw) / (msw / 1e3), "unit": "frames/s",
-                "segments_per_gpu": cfg.batch_size, "ms_per_step": msw / args.steps}
+        other = {"value": sum_over_ranks(frw) / (msw / 1e3), "unit": "frames/s",
+                 "segments_per_gpu": S_o, "global_batch_segments": S_o * world,
+                 "ms_per_step": msw / args.steps}
         lw.close()
         del dw, hw
         torch.cuda.empty_cache()
@@ -603,14 +606,33 @@ def main():
         t0 = time.perf_counter()
         for _ in range(10):
             pol.forward(obs_pin, out=outs)
-        idt = max_over_ranks((time.perf_counter() - t0) / 10)
+        idt_sync = max_over_ranks((time.perf_counter() - t0) / 10)
+        # pipelined stream of batches (tlg_policy_forward_async): batch k+1's H2D and batch
+        # k-1's D2H overlap batch k's forward; each batch's results are waited for
+        obs_pins = [obs_pin, torch.from_numpy(obs.copy()).pin_memory().numpy()]
+        outs2 = [outs, tuple(torch.empty_like(t, pin_memory=True).numpy() for t in outs_t)]
+        tk = [pol.forward_async(obs_pins[0], outs2[0])]
+        pol.wait(tk[0])
+        barrier()
+        reps_p = 20
+        t0 = time.perf_counter()
+        tk = []
+        for k in range(reps_p):
+            tk.append(pol.forward_async(obs_pins[k % 2], outs2[k % 2]))
+            if k >= 1:
+                pol.wait(tk[k - 1])
+        pol.wait(tk[-1])
+        idt = max_over_ranks((time.perf_counter() - t0) / reps_p)
         infer = {"metric": "InferenceServer actions/sec", "config": c4.name, "note": c4.note,
                  "value": world * c4.batch_size / (ims / 1e3), "unit": "actions/s",
                  "ms_per_batch": ims,
                  "tflops": 2.2426e6 * c4.batch_size / (ims / 1e3) / 1e12,
                  "e2e": {"value": world * c4.batch_size / idt, "unit": "actions/s",
                          "h2d_bytes_per_batch": obs.nbytes,
-                         "d2h_bytes_per_batch": c4.batch_size * (2 * c4.n_actions + 1) * 4}}
+                         "d2h_bytes_per_batch": c4.batch_size * (2 * c4.n_actions + 1) * 4,
+                         "note": "pinned host batches through tlg_policy_forward_async, two in "
+                                 "flight (H2D / forward / D2H overlapped), every batch waited for",
+                         "synchronous": world * c4.batch_size / idt_sync}}
 
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None
@@ -672,7 +694,7 @@ def main():
                     "note": "pinned host SoA batch H2D each step (same obs format as value; "
                             "bit rows padded to 16 B), pipelined one step ahead on a copy "
                             "stream; stats D2H each step"},
-            "weak_scaling": weak,
+            ("weak_scaling" if args.scaling == "strong" else "strong_scaling"): other,
             "dropin_e2e": dropin,
             "e2e_alt_format": e2e_alt,
             "e2e_dense_rows": e2e_unpitched,

@@ -239,6 +239,16 @@ int tlg_policy_set_params_from_learner(tlg_policy* p, tlg_learner* l);
  * Each row is evaluated independently of the others (batch-invariant). */
 int tlg_policy_forward(tlg_policy* p, const float* obs, size_t n, float* logits, float* probs,
                        float* value, int on_device);
+/* Pipelined batches from host memory (the InfServer's stream of request batches): enqueue
+ * one batch -- H2D on a copy stream, the forward on the policy's stream, D2H on a second
+ * copy stream -- and return at once with a ticket; batch k+1's H2D overlaps batch k's
+ * forward and batch k-1's D2H (page-locked host buffers overlap; pageable ones still
+ * work).  Two batches are in flight at most (enqueuing a third waits for the oldest).  A
+ * batch's host buffers must stay valid until tlg_policy_wait(ticket) returns; results are
+ * the same as tlg_policy_forward's. */
+int tlg_policy_forward_async(tlg_policy* p, const float* obs, size_t n, float* logits,
+                             float* probs, float* value, uint64_t* ticket);
+int tlg_policy_wait(tlg_policy* p, uint64_t ticket);
 void* tlg_policy_stream(tlg_policy* p);
 
 /* ---- returns (K1) standalone -------------------------------------------- */

@@ -138,6 +138,9 @@ def lib():
         L.tlg_policy_destroy.argtypes = [C.c_void_p]
         L.tlg_policy_set_params.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t]
         L.tlg_policy_set_params_from_learner.argtypes = [C.c_void_p, C.c_void_p]
+        L.tlg_policy_forward_async.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p,
+                                               C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64)]
+        L.tlg_policy_wait.argtypes = [C.c_void_p, C.c_uint64]
         L.tlg_policy_forward.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p,
                                          C.c_void_p, C.c_void_p, C.c_int]
         L.tlg_policy_stream.restype = C.c_void_p
@@ -172,6 +175,7 @@ EXPORTS = [
     "tlg_learner_stream", "tlg_learner_phase_ms", "tlg_learner_last_launches",
     "tlg_learner_kernel_ms", "tlg_learner_set_timing",
     "tlg_policy_create", "tlg_policy_destroy", "tlg_policy_set_params", "tlg_policy_forward",
+    "tlg_policy_forward_async", "tlg_policy_wait",
     "tlg_policy_set_params_from_learner",
     "tlg_policy_stream", "tlg_returns",
 ]
@@ -426,6 +430,19 @@ class Policy:
         check(lib().tlg_policy_forward(self.h, obs.ctypes.data, n, lg.ctypes.data, pr.ctypes.data,
                                        v.ctypes.data, 0))
         return lg, pr, v
+
+    def forward_async(self, obs, out):
+        """Enqueue a host batch (obs and the (logits, probs, value) arrays must stay alive,
+        page-locked for overlap, until wait(ticket)); returns the ticket."""
+        t = C.c_uint64()
+        lg, pr, v = out
+        check(lib().tlg_policy_forward_async(self.h, obs.ctypes.data, obs.shape[0],
+                                             lg.ctypes.data, pr.ctypes.data, v.ctypes.data,
+                                             C.byref(t)))
+        return t.value
+
+    def wait(self, ticket):
+        check(lib().tlg_policy_wait(self.h, ticket))
 
     def forward_device(self, obs_t, logits_t, probs_t, value_t):
         check(lib().tlg_policy_forward(self.h, obs_t.data_ptr(), obs_t.shape[0],

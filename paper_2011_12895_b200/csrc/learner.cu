@@ -1401,6 +1401,17 @@ struct tlg_policy {
   int* err;
   long P_pad;
   int head_tiles = 1;
+  // pipelined batches (tlg_policy_forward_async): two slots of device inputs / outputs, an
+  // H2D and a D2H stream around the compute stream, events ordering slot reuse
+  struct Slot {
+    float *obs = nullptr, *logits = nullptr, *probs = nullptr, *value = nullptr;
+    cudaEvent_t h2d = nullptr, computed = nullptr, d2h = nullptr;
+    uint64_t ticket = 0;
+  };
+  Slot pipe[2];
+  cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
+  uint64_t next_ticket = 1, done_ticket = 0;
+  int* h_err = nullptr;
 
   tlg_policy(const tlg_policy_shape& s, int dev, long mb) : net(s), device(dev), max_batch(mb) {
     if (mb <= 0) throw InvalidArg("max_batch must be >= 1");
@@ -1427,7 +1438,32 @@ struct tlg_policy {
       act_lo.push_back(nullptr);
     }
   }
+  // Enqueue one forward of n device-resident observations on `stream` (err accumulates).
+  void enqueue(const float* x0, long n, float* lg, float* pr, float* vv);
+  void open_pipe() {
+    if (h2d_stream) return;
+    TLG_CUDA(cudaStreamCreateWithFlags(&h2d_stream, cudaStreamNonBlocking));
+    TLG_CUDA(cudaStreamCreateWithFlags(&d2h_stream, cudaStreamNonBlocking));
+    for (Slot& sl : pipe) {
+      sl.obs = mem.add<float>(max_batch * net.D);
+      sl.logits = mem.add<float>(max_batch * net.A);
+      sl.probs = mem.add<float>(max_batch * net.A);
+      sl.value = mem.add<float>(max_batch);
+      TLG_CUDA(cudaEventCreateWithFlags(&sl.h2d, cudaEventDisableTiming));
+      TLG_CUDA(cudaEventCreateWithFlags(&sl.computed, cudaEventDisableTiming));
+      TLG_CUDA(cudaEventCreateWithFlags(&sl.d2h, cudaEventDisableTiming));
+    }
+    TLG_CUDA(cudaMallocHost(&h_err, 16));
+  }
   ~tlg_policy() {
+    for (Slot& sl : pipe) {
+      if (sl.h2d) cudaEventSynchronize(sl.d2h), cudaEventDestroy(sl.h2d);
+      if (sl.computed) cudaEventDestroy(sl.computed);
+      if (sl.d2h) cudaEventDestroy(sl.d2h);
+    }
+    if (h2d_stream) cudaStreamDestroy(h2d_stream);
+    if (d2h_stream) cudaStreamDestroy(d2h_stream);
+    if (h_err) cudaFreeHost(h_err);
     if (stream) {
       cudaStreamSynchronize(stream);
       cudaStreamDestroy(stream);
@@ -1458,6 +1494,53 @@ void set_params_common(float* params, float* params_lo, long P, long P_pad, cons
 }
 
 }  // namespace
+
+void tlg_policy::enqueue(const float* x0, long n, float* lg, float* pr, float* vv) {
+  const long D = net.D, A = net.A;
+  if (net.padded()) {
+    TLG_CUDA(cudaMemcpy2DAsync(obs_pad, size_t(net.D_pad) * 4, x0, size_t(D) * 4, size_t(D) * 4,
+                               size_t(n), cudaMemcpyDeviceToDevice, stream));
+    x0 = obs_pad;
+  }
+  // the tf32 residuals of the observations and activations are derived in the GEMMs'
+  // shared memory (Operand::lo_smem): no residual planes
+  using tlg::gemm::Operand;
+  for (uint32_t l = 0; l < net.L; ++l) {
+    const int in = net.gin(l), outw = int(net.dims[l + 1]);
+    Operand Aop{l == 0 ? x0 : act[l - 1], nullptr, in, false};
+    Aop.lo_smem = true;
+    Operand Bop{params + net.w_off[l], params_lo + net.w_off[l], in, false};
+    if (l == 0 && net.padded()) {
+      Bop.hi = w1p;
+      Bop.lo = w1p_lo;
+    }
+    tlg::gemm::Params gp{};
+    gp.out_hi = act[l];
+    gp.out_lo = nullptr;
+    gp.ldo = outw;
+    gp.bias = params + net.b_off[l];
+    const bool fuse = l + 1 == net.L && net.A + 1 <= 8;
+    if (fuse) {
+      gp.head_w = params + net.head.wpi;
+      gp.head_wv = params + net.head.wv;
+      gp.head_k = int(A) + 1;
+      gp.head_part = head_part;
+    }
+    const int bn =
+        tlg::gemm::launch(Aop, Bop, int(n), outw, in, tlg::gemm::kEpiFwdTanh, gp, 1, stream).bn;
+    if (fuse) head_tiles = (outw + bn - 1) / bn;
+  }
+  const float* hL = net.L ? act[net.L - 1] : x0;
+  if (net.L > 0 && net.A + 1 <= 8) {
+    tlg::launch_head_finalize(net.head, params, head_part, head_tiles, n, nullptr, nullptr,
+                              nullptr, lg, pr, vv, err, stream);
+  } else {
+    tlg::launch_head_forward(net.head, params, hL, net.head.H, nullptr, n, head_out, nullptr, pr,
+                             err, stream);
+    ::tlg::launch_k(unpack_head_kernel, dim3(int((n + 255) / 256)), dim3(256), size_t(0), stream,
+                    head_out, int(A), n, lg, vv);
+  }
+}
 
 // ===========================================================================
 extern "C" {
@@ -1950,54 +2033,11 @@ int tlg_policy_forward(tlg_policy* p, const float* obs, size_t n, float* logits,
       TLG_CUDA(cudaMemcpyAsync(p->obs, obs, n * D * 4, cudaMemcpyHostToDevice, p->stream));
       x0 = p->obs;
     }
-    if (p->net.padded()) {
-      TLG_CUDA(cudaMemcpy2DAsync(p->obs_pad, size_t(p->net.D_pad) * 4, x0, size_t(D) * 4,
-                                 size_t(D) * 4, n, cudaMemcpyDeviceToDevice, p->stream));
-      x0 = p->obs_pad;
-    }
-    // the tf32 residuals of the observations and activations are derived in the GEMMs'
-    // shared memory (Operand::lo_smem): no residual planes
-    using tlg::gemm::Operand;
-    for (uint32_t l = 0; l < p->net.L; ++l) {
-      const int in = p->net.gin(l), outw = int(p->net.dims[l + 1]);
-      Operand Aop{l == 0 ? x0 : p->act[l - 1], nullptr, in, false};
-      Aop.lo_smem = true;
-      Operand Bop{p->params + p->net.w_off[l], p->params_lo + p->net.w_off[l], in, false};
-      if (l == 0 && p->net.padded()) {
-        Bop.hi = p->w1p;
-        Bop.lo = p->w1p_lo;
-      }
-      tlg::gemm::Params gp{};
-      gp.out_hi = p->act[l];
-      gp.out_lo = nullptr;
-      gp.ldo = outw;
-      gp.bias = p->params + p->net.b_off[l];
-      const bool fuse = l + 1 == p->net.L && p->net.A + 1 <= 8;
-      if (fuse) {
-        gp.head_w = p->params + p->net.head.wpi;
-        gp.head_wv = p->params + p->net.head.wv;
-        gp.head_k = int(A) + 1;
-        gp.head_part = p->head_part;
-      }
-      const int bn = tlg::gemm::launch(Aop, Bop, int(n), outw, in, tlg::gemm::kEpiFwdTanh, gp, 1,
-                                       p->stream).bn;
-      if (fuse) p->head_tiles = (outw + bn - 1) / bn;
-    }
-    const float* hL = p->net.L ? p->act[p->net.L - 1] : x0;
     float* lg = on_device ? logits : p->logits;
     float* pr = on_device ? probs : p->probs;
     float* vv = on_device ? value : p->value;
     TLG_CUDA(cudaMemsetAsync(p->err, 0, 4, p->stream));
-    if (p->net.L > 0 && p->net.A + 1 <= 8) {
-      tlg::launch_head_finalize(p->net.head, p->params, p->head_part, p->head_tiles, long(n),
-                                nullptr, nullptr, nullptr, lg, pr, vv, p->err, p->stream);
-    } else {
-      tlg::launch_head_forward(p->net.head, p->params, hL, p->net.head.H, nullptr, long(n),
-                               p->head_out, nullptr, pr, p->err, p->stream);
-      ::tlg::launch_k(unpack_head_kernel, dim3(int((n + 255) / 256)), dim3(256), size_t(0), p->stream, p->head_out, int(A),
-                                                                       long(n), lg, vv);
-      TLG_CHECK_LAUNCH();
-    }
+    p->enqueue(x0, long(n), lg, pr, vv);
     if (!on_device) {
       TLG_CUDA(cudaMemcpyAsync(logits, p->logits, n * A * 4, cudaMemcpyDeviceToHost, p->stream));
       TLG_CUDA(cudaMemcpyAsync(probs, p->probs, n * A * 4, cudaMemcpyDeviceToHost, p->stream));
@@ -2007,6 +2047,56 @@ int tlg_policy_forward(tlg_policy* p, const float* obs, size_t n, float* logits,
     TLG_CUDA(cudaMemcpyAsync(&e, p->err, 4, cudaMemcpyDeviceToHost, p->stream));
     TLG_CUDA(cudaStreamSynchronize(p->stream));
     if (e & tlg::kErrNotOneHot) throw InvalidArg("tabular observation must be one-hot");
+  });
+}
+
+int tlg_policy_forward_async(tlg_policy* p, const float* obs, size_t n, float* logits,
+                             float* probs, float* value, uint64_t* ticket) {
+  return Guard([&] {
+    if (!p || !obs || !logits || !probs || !value || !ticket) throw InvalidArg("null argument");
+    if (n == 0 || long(n) > p->max_batch) throw InvalidArg("batch must hold 1..max_batch rows");
+    TLG_CUDA(cudaSetDevice(p->device));
+    p->open_pipe();
+    const uint64_t t = p->next_ticket;
+    tlg_policy::Slot& sl = p->pipe[t & 1];
+    // the slot's previous batch must have drained (its D2H read the slot's outputs)
+    if (sl.ticket != 0) TLG_CUDA(cudaEventSynchronize(sl.d2h));
+    const long D = p->net.D, A = p->net.A;
+    if (t == 1) TLG_CUDA(cudaMemsetAsync(p->err, 0, 4, p->stream));
+    // H2D (page-locked host memory overlaps the forward of the previous batch)
+    TLG_CUDA(cudaStreamWaitEvent(p->h2d_stream, sl.computed, 0));  // the slot's obs are free
+    TLG_CUDA(cudaMemcpyAsync(sl.obs, obs, n * D * 4, cudaMemcpyHostToDevice, p->h2d_stream));
+    TLG_CUDA(cudaEventRecord(sl.h2d, p->h2d_stream));
+    // forward on the policy stream
+    TLG_CUDA(cudaStreamWaitEvent(p->stream, sl.h2d, 0));
+    p->enqueue(sl.obs, long(n), sl.logits, sl.probs, sl.value);
+    TLG_CUDA(cudaEventRecord(sl.computed, p->stream));
+    // D2H overlaps the next batch's forward
+    TLG_CUDA(cudaStreamWaitEvent(p->d2h_stream, sl.computed, 0));
+    TLG_CUDA(cudaMemcpyAsync(logits, sl.logits, n * A * 4, cudaMemcpyDeviceToHost, p->d2h_stream));
+    TLG_CUDA(cudaMemcpyAsync(probs, sl.probs, n * A * 4, cudaMemcpyDeviceToHost, p->d2h_stream));
+    TLG_CUDA(cudaMemcpyAsync(value, sl.value, n * 4, cudaMemcpyDeviceToHost, p->d2h_stream));
+    TLG_CUDA(cudaEventRecord(sl.d2h, p->d2h_stream));
+    sl.ticket = t;
+    p->next_ticket = t + 1;
+    *ticket = t;
+  });
+}
+
+int tlg_policy_wait(tlg_policy* p, uint64_t ticket) {
+  return Guard([&] {
+    if (!p) throw InvalidArg("null argument");
+    if (ticket == 0 || ticket >= p->next_ticket) throw InvalidArg("unknown ticket");
+    if (ticket <= p->done_ticket) return;
+    if (ticket + 2 < p->next_ticket) throw InvalidArg("ticket no longer tracked (2 in flight)");
+    TLG_CUDA(cudaSetDevice(p->device));
+    tlg_policy::Slot& sl = p->pipe[ticket & 1];
+    if (sl.ticket != ticket) throw InvalidArg("ticket no longer tracked");
+    TLG_CUDA(cudaEventSynchronize(sl.d2h));
+    TLG_CUDA(cudaMemcpyAsync(p->h_err, p->err, 4, cudaMemcpyDeviceToHost, p->stream));
+    TLG_CUDA(cudaStreamSynchronize(p->stream));
+    p->done_ticket = ticket;
+    if (p->h_err[0] & tlg::kErrNotOneHot) throw InvalidArg("tabular observation must be one-hot");
   });
 }
 

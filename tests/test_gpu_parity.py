@@ -678,6 +678,29 @@ def test_teacher_kl_two_local_shards_of_bit_planes(tlg, oracle):
     assert np.max(np.abs(g - want)) <= 1e-4 * gscale, np.max(np.abs(g - want)) / gscale
 
 
+def test_pipelined_policy_batches_match_synchronous_forward(tlg, oracle):
+    """tlg_policy_forward_async / tlg_policy_wait: a stream of host batches with two in
+    flight returns exactly the synchronous forward's results, batch by batch."""
+    import torch
+    D, A, hidden = 64, 6, (256, 128)
+    p = init_params(oracle, Shape(2, D, A, hidden), 13)
+    pol = tlg.Policy("mlp", D, A, hidden, max_batch=4096)
+    pol.set_params(p)
+    batches = [tlg.synth.make_obs(n, D, seed=40 + i) for i, n in enumerate((4096, 1000, 4096, 7, 2500))]
+    want = [pol.forward(o) for o in batches]
+    pins = [torch.from_numpy(o).pin_memory() for o in batches]
+    outs = [(np.zeros((o.shape[0], A), np.float32), np.zeros((o.shape[0], A), np.float32),
+             np.zeros(o.shape[0], np.float32)) for o in batches]
+    tickets = []
+    for k, (o, out) in enumerate(zip(pins, outs)):
+        tickets.append(pol.forward_async(o.numpy(), out))
+        if k >= 1:
+            pol.wait(tickets[k - 1])
+    pol.wait(tickets[-1])
+    for (lg, pr, v), (wl, wp, wv) in zip(outs, want):
+        assert np.array_equal(lg, wl) and np.array_equal(pr, wp) and np.array_equal(v, wv)
+
+
 @pytest.mark.parametrize("fmt", ["f32", "bits"])
 def test_device_replay_matches_host_batches(tlg, oracle, fmt):
     """Segments ingested once into the device replay ring and gathered by slot give
