@@ -542,8 +542,24 @@ def main():
         bytes_dom = 8 * F * lo_ + 4 * F * li + 8 * F * li + 8 * li * lo_
     else:
         bytes_dom = 8 * F * lo_ + 8 * F * li + 4 * li * lo_
+    # the dominant kernel's own instruction ceiling (tools/mma_peak.cu: back-to-back
+    # tcgen05.mma from smem on every SM pair, profiles/r02_mma_peak.json)
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_mma_peak.json")) as f:
+            mp = json.load(f)
+        if obs_bits and dom in ("fwd1", "dw1"):  # 3 kind::i8 MMAs per fp32-equivalent MAC
+            own = {"kind": "tcgen05.mma kind::i8", "peak": mp["i8_tops"], "unit": "TOPS",
+                   "achieved": 3 * achieved, "frac": 3 * achieved / mp["i8_tops"]}
+        else:  # 3xTF32: 3 kind::tf32 MMAs per fp32 MAC (2 when one operand is exact)
+            own = {"kind": "tcgen05.mma kind::tf32", "peak": mp["tf32_tflops"],
+                   "unit": "TFLOP/s", "achieved": 3 * achieved,
+                   "frac": 3 * achieved / mp["tf32_tflops"]}
+        own["source"] = "profiles/r02_mma_peak.json"
+    except Exception:
+        own = None
     roofline = {
         "kernel": desc,
+        "own_instruction_ceiling": own,
         "algorithmic_bytes_per_launch": bytes_dom,
         "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
         "frac": achieved / peak, "traffic": _ncu_traffic(dom),
