@@ -314,8 +314,10 @@ void run_i8x2_fwd(const CUtensorMap& ta, const CUtensorMap& tq, const CUtensorMa
 LaunchInfo launch_i8x2_fwd(const int8_t* a, const int8_t* q, long Kp, const float* scale,
                            const float* bias, int M, int N, int K, float* out, float* out_lo,
                            int ldo, const float* head_w, const float* head_wv, int head_k,
-                           float* head_part, cudaStream_t stream) {
+                           float* head_part, cudaStream_t stream, int8_t* out_q) {
   if (M <= 0 || N <= 0 || K <= 0) throw CudaError("gemm_i8x2: empty problem");
+  if (out_q != nullptr && (N % 32 != 0 || (reinterpret_cast<uintptr_t>(out_q) & 15) != 0))
+    throw CudaError("gemm_i8x2: int8 activation pieces need N % 32 == 0 and 16-B alignment");
   if (K % 16 != 0 || Kp < K) throw CudaError("gemm_i8x2: K must be a multiple of 16");
   if (head_k > 8) throw CudaError("gemm_i8x2: fused heads need n_actions + 1 <= 8");
   // 64-column tiles: three accumulators double-buffered in TMEM (the epilogue of one tile
@@ -326,11 +328,15 @@ LaunchInfo launch_i8x2_fwd(const int8_t* a, const int8_t* q, long Kp, const floa
   if (M < 2 * kBM) throw CudaError("gemm_i8x2: needs M >= 256");
   constexpr int cg = 2;
   I8x2Params p{M, N, K, scale, bias, long(M), long(N), head_w, head_wv, head_k, head_part,
-               out_lo != nullptr ? 1 : 0};
+               out_lo != nullptr ? 1 : 0, out_q, out != nullptr ? 1 : 0};
   const TileMap tm{ceil_div(M, kBM * cg), ceil_div(N, BN), 1};
   const CUtensorMap ta = make_bytes_map(a, K, 3L * M, K, kBKi, kBM, CU_TENSOR_MAP_SWIZZLE_128B);
   const CUtensorMap tq = make_bytes_map(q, Kp, 3L * N, Kp, kBKi, BN / cg, CU_TENSOR_MAP_SWIZZLE_128B);
-  const CUtensorMap to = make_f32_out_map(out, N, M, ldo);
+  if (out == nullptr && (out_lo != nullptr || (out_q == nullptr && head_k <= 0)))
+    throw CudaError("gemm_i8x2: missing output plane");
+  CUtensorMap to;
+  if (out) to = make_f32_out_map(out, N, M, ldo);
+  else std::memset(&to, 0, sizeof(to));
   CUtensorMap tl;
   if (out_lo) tl = make_f32_out_map(out_lo, N, M, ldo);
   else std::memset(&tl, 0, sizeof(tl));

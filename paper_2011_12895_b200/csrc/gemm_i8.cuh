@@ -45,25 +45,6 @@ struct I8Params {
   int write_lo;        // store the tf32 residual plane (0: the consumers derive it)
 };
 
-// tanh output o in (-1, 1) -> three int8 pieces of o * 127 (fixed scale 1/127), packed
-// four columns per word; magic-constant rounding (exact residual steps)
-__device__ __forceinline__ void act_pieces4(const float* o, uint32_t& w0, uint32_t& w1,
-                                            uint32_t& w2) {
-  constexpr float kMagic = 12582912.f;
-  w0 = w1 = w2 = 0u;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const float x = o[j] * 127.f;
-    const float m0 = x + kMagic;
-    const float x1 = (x - (m0 - kMagic)) * 128.f;
-    const float m1 = x1 + kMagic;
-    const float m2 = (x1 - (m1 - kMagic)) * 128.f + kMagic;
-    w0 |= (__float_as_uint(m0) & 0xFFu) << (8 * j);
-    w1 |= (__float_as_uint(m1) & 0xFFu) << (8 * j);
-    w2 |= (__float_as_uint(m2) & 0xFFu) << (8 * j);
-  }
-}
-
 template <int BN, int CG>
 struct SmemI8 {
   static constexpr int kX = kBM * kBKi;         // 16 KB operand tile (x, x<<7)
@@ -407,21 +388,9 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                                float(int(rb[j])) * (s * 6.103515625e-05f));
           o[j] = tanh_fast(z + bj);
         }
-        if (p.out_q != nullptr && rbase + lane < p.M) {
-          // the same activations as int8 pieces for the next layer's int8 GEMM
-          const long plane = long(p.M) * p.N;
-          int8_t* q = p.out_q + long(rbase + lane) * p.N + nb;
-#pragma unroll
-          for (int j16 = 0; j16 < 2; ++j16) {
-            uint32_t a[4], b[4], c4[4];
-#pragma unroll
-            for (int w = 0; w < 4; ++w) act_pieces4(o + 16 * j16 + 4 * w, a[w], b[w], c4[w]);
-            *reinterpret_cast<uint4*>(q + 16 * j16) = make_uint4(a[0], a[1], a[2], a[3]);
-            *reinterpret_cast<uint4*>(q + plane + 16 * j16) = make_uint4(b[0], b[1], b[2], b[3]);
-            *reinterpret_cast<uint4*>(q + 2 * plane + 16 * j16) =
-                make_uint4(c4[0], c4[1], c4[2], c4[3]);
-          }
-        }
+        // the same activations as int8 pieces for the next layer's int8 GEMM
+        if (p.out_q != nullptr && nb < p.N && rbase + lane < p.M)
+          write_act_pieces(o, p.out_q, long(p.M) * p.N, long(rbase + lane) * p.N + nb);
         if (lane == 0) bulk_wait_read();
         __syncwarp();
 #pragma unroll
@@ -485,6 +454,8 @@ struct I8x2Params {
   int head_k;
   float* head_part;
   int has_lo;
+  int8_t* out_q;  // optional: tanh outputs as int8 pieces [3][M][N] for the next int8 layer
+  int has_out;    // 0: no fp32 plane (the pieces or the fused heads are what is read)
 };
 
 template <int BN_, int CG>
@@ -690,6 +661,8 @@ __global__ void __launch_bounds__(32 * (2 + kEpiWarps), 1)
                                fmaf(float(int(r1[j])), 0.0078125f, float(int(r0[j]))));
           o[j] = tanh_fast(fmaf(v, s, bj));
         }
+        if (p.out_q != nullptr && nb < p.N && rbase + lane < p.M)
+          write_act_pieces(o, p.out_q, long(p.M) * p.N, long(rbase + lane) * p.N + nb);
         if (do_head) {
 #pragma unroll
           for (int k = 0; k < kHK; ++k) {
@@ -718,6 +691,7 @@ __global__ void __launch_bounds__(32 * (2 + kEpiWarps), 1)
           }
           __syncwarp();
         }
+        if (!p.has_out) continue;
         if (lane == 0) bulk_wait_read();
         __syncwarp();
 #pragma unroll
@@ -1070,10 +1044,11 @@ LaunchInfo launch_i8_bits_fwd(const uint8_t* bits, long rowb, const int8_t* q, l
 // out = tanh(A . W^T + b) with A given as int8 pieces [3][M][K] (scale 1/127, e.g. the
 // out_q of launch_i8_bits_fwd) and W as launch_quantize_rows pieces.  Optional fused
 // heads (Params::head_* semantics) and residual plane (out_lo may be null).  K % 16 == 0.
+// out may be null (out_lo then null too) when out_q or the fused heads carry the result.
 LaunchInfo launch_i8x2_fwd(const int8_t* a, const int8_t* q, long Kp, const float* scale,
                            const float* bias, int M, int N, int K, float* out, float* out_lo,
                            int ldo, const float* head_w, const float* head_wv, int head_k,
-                           float* head_part, cudaStream_t stream);
+                           float* head_part, cudaStream_t stream, int8_t* out_q = nullptr);
 
 // dZ [F][M] (row pitch ldz floats) -> pieces P [3][F][M] int8 with one scale per
 // (split, column): s = colmax[f / rows_per_split][m] / 127.  M % 4 == 0.

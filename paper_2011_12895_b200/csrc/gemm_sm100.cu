@@ -249,6 +249,14 @@ LaunchInfo launch(const Operand& A, const Operand& B, int M, int N, int K, int e
              b_lo0 = (B.lo != nullptr || B.lo_smem) && !B.u8;
   const int lod = (A.lo_smem && !A.u8 ? 1 : 0) | (B.lo_smem && !B.u8 ? 2 : 0);
   const int u8_0 = A.u8 ? 1 : B.u8 ? 2 : 0;
+  // the tanh forward may drop its fp32 plane when the int8 pieces or the fused heads are
+  // what the caller reads
+  if (p.out_hi == nullptr && epi != kEpiStore &&
+      !(epi == kEpiFwdTanh && p.out_lo == nullptr && (p.out_q != nullptr || p.head_k > 0)))
+    throw CudaError("gemm: missing output plane");
+  if (p.out_q != nullptr &&
+      (epi != kEpiFwdTanh || N % 32 != 0 || (reinterpret_cast<uintptr_t>(p.out_q) & 15) != 0))
+    throw CudaError("gemm: int8 activation pieces need the tanh forward, N % 32 == 0, 16-B alignment");
   if (epi == kEpiBwdTanh && p.colsum != nullptr && N > kColMax)
     throw CudaError("gemm: fused column sums need N <= 2048");
   const int kb_total = ceil_div(K, kBK);

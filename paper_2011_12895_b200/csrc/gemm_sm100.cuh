@@ -95,6 +95,9 @@ struct Params {
   // U8 == 1: also write the expanded fp32 A operand (exact) to this [M][K] buffer
   // (tmAct map) from the n_tile == 0 CTAs, so a later GEMM can read it as plain fp32
   float* a_expand;
+  // kEpiFwdTanh: also write the tanh outputs as fixed-scale int8 pieces [3][M][N] (scale
+  // 1/127) for a following int8 x int8 layer (gemm_i8x2_fwd_kernel); N % 32 == 0
+  int8_t* out_q;
   LossEpi loss;  // kEpiFwdLoss only
 };
 
@@ -304,7 +307,10 @@ constexpr SmemPlan smem_plan(int BN, bool a_lo, bool b_lo, int epi, int u8, int 
   const int sep_blocks = epi == kEpiStore ? 1 : 2 + (epi == kEpiBwdTanh || epi == kEpiFwdLoss ? 1 : 0);
   const int sep = plan_stages(q.stage, epi_bytes(sep_blocks), ring);
   const int shr = plan_stages(q.stage, epi_bytes(sep_blocks - 1), ring);
-  q.share_lo = epi != kEpiStore && epi != kEpiFwdLoss && (u8 == 1 || (sep < 3 && shr > sep));
+  // The tanh forward shares whenever that buys a stage: its consumers derive the tf32
+  // residual in their own shared memory, so out_lo is normally null (TLG_LO_HBM only).
+  q.share_lo = epi != kEpiStore && epi != kEpiFwdLoss &&
+               (u8 == 1 || (sep < 3 && shr > sep) || (epi == kEpiFwdTanh && shr > sep));
   q.epi_blocks = q.share_lo ? sep_blocks - 1 : sep_blocks;
   q.warp_epi = q.epi_blocks * 4096 + head;
   q.stages = q.share_lo ? shr : sep;
@@ -429,6 +435,40 @@ __device__ __forceinline__ float4 u8x4_to_f32(uint32_t v) {
 
 // byte offset of element (row r, col c) in a 32x32 fp32 block with the 128-B TMA swizzle
 __device__ __forceinline__ uint32_t swz(int r, int c4) { return uint32_t(r * 128 + ((c4 ^ (r & 7)) << 4)); }
+
+// tanh output o in (-1, 1) -> three int8 pieces of o * 127 (fixed scale 1/127), packed
+// four columns per word; magic-constant rounding (exact residual steps)
+__device__ __forceinline__ void act_pieces4(const float* o, uint32_t& w0, uint32_t& w1,
+                                            uint32_t& w2) {
+  constexpr float kMagic = 12582912.f;
+  w0 = w1 = w2 = 0u;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float x = o[j] * 127.f;
+    const float m0 = x + kMagic;
+    const float x1 = (x - (m0 - kMagic)) * 128.f;
+    const float m1 = x1 + kMagic;
+    const float m2 = (x1 - (m1 - kMagic)) * 128.f + kMagic;
+    w0 |= (__float_as_uint(m0) & 0xFFu) << (8 * j);
+    w1 |= (__float_as_uint(m1) & 0xFFu) << (8 * j);
+    w2 |= (__float_as_uint(m2) & 0xFFu) << (8 * j);
+  }
+}
+
+// One thread's 32 consecutive columns of one row (starting at element `at` of a [M][N]
+// plane, 16-B aligned) -> the three piece planes (plane stride `plane`).
+__device__ __forceinline__ void write_act_pieces(const float* o, int8_t* q, long plane, long at) {
+  q += at;
+#pragma unroll
+  for (int j16 = 0; j16 < 2; ++j16) {
+    uint32_t a[4], b[4], c4[4];
+#pragma unroll
+    for (int w = 0; w < 4; ++w) act_pieces4(o + 16 * j16 + 4 * w, a[w], b[w], c4[w]);
+    *reinterpret_cast<uint4*>(q + 16 * j16) = make_uint4(a[0], a[1], a[2], a[3]);
+    *reinterpret_cast<uint4*>(q + plane + 16 * j16) = make_uint4(b[0], b[1], b[2], b[3]);
+    *reinterpret_cast<uint4*>(q + 2 * plane + 16 * j16) = make_uint4(c4[0], c4[1], c4[2], c4[3]);
+  }
+}
 
 template <int BN, bool A_MN, bool B_MN, bool A_LO, bool B_LO, int EPI, int U8, int CG, int LOD>
 __global__ void __launch_bounds__((U8 || LOD) ? kThreadsU8 : kThreads, 1)
@@ -1074,6 +1114,24 @@ __global__ void __launch_bounds__((U8 || LOD) ? kThreadsU8 : kThreads, 1)
     }
     constexpr int kHK = 8;  // fused head width limit (n_actions + 1)
     const bool do_head = EPI == kEpiFwdTanh && p.head_k > 0;
+    // kEpiFwdTanh with fused heads: the bias and head weights of the next 32-column chunk
+    // are loaded one chunk ahead (registers), so their latency overlaps this chunk's math
+    float bnext = 0.f, wnext[kHK];
+    auto fetch = [&](int t_next, int c_next) {
+      if (EPI != kEpiFwdTanh || t_next >= num_tiles) return;
+      int mt_, nt_, sp_;
+      tm.decode(t_next, mt_, nt_, sp_);
+      const int col = nt_ * BN + c_next + lane;
+      const bool ok = col < p.N;
+      bnext = ok ? __ldg(p.bias + col) : 0.f;
+#pragma unroll
+      for (int k = 0; k < kHK; ++k) {
+        wnext[k] = 0.f;
+        if (do_head && k < p.head_k && ok)
+          wnext[k] = __ldg((k < p.head_k - 1 ? p.head_w + long(k) * p.N : p.head_wv) + col);
+      }
+    };
+    if (do_head) fetch(cl_id, 0);
     int it = 0;
     for (int t = cl_id; t < num_tiles; t += n_cl, ++it) {
       int mt, nt, sp;
@@ -1111,22 +1169,26 @@ __global__ void __launch_bounds__((U8 || LOD) ? kThreadsU8 : kThreads, 1)
         tmem_ld32(tbase + uint32_t(c), r);
         float o[32];
         if (EPI == kEpiFwdTanh) {
-          const float bl = (nb + lane < p.N) ? __ldg(p.bias + nb + lane) : 0.f;
+          float bl;
+          if (do_head) {
+            bl = bnext;
+            // this chunk's head weights -> smem (read back as broadcast LDS.128 below)
+#pragma unroll
+            for (int k = 0; k < kHK; ++k) wsm[k * 32 + lane] = wnext[k];
+            if (c + 32 < BN) fetch(t, c + 32);
+            else fetch(t + n_cl, 0);
+          } else {
+            // (measured: the one-chunk-ahead loads slow the head-less, epilogue-bound
+            // short-K forward, e.g. C4 layer 1, by 15 %)
+            bl = (nb + lane < p.N) ? __ldg(p.bias + nb + lane) : 0.f;
+          }
 #pragma unroll
           for (int j = 0; j < 32; ++j)
             o[j] = tanh_fast(__uint_as_float(r[j]) + __shfl_sync(0xffffffffu, bl, j));
+          if (p.out_q != nullptr && nb < p.N && rbase + lane < p.M)
+            write_act_pieces(o, p.out_q, long(p.M) * p.N, long(rbase + lane) * p.N + nb);
           if (do_head) {
-            // head weights of this chunk's 32 columns -> smem, then broadcast LDS.128
-#pragma unroll
-            for (int k = 0; k < kHK; ++k) {
-              float wk = 0.f;
-              if (k < p.head_k && nb + lane < p.N) {
-                const float* wrow = k < p.head_k - 1 ? p.head_w + long(k) * p.N : p.head_wv;
-                wk = __ldg(wrow + nb + lane);
-              }
-              wsm[k * 32 + lane] = wk;
-            }
-            __syncwarp();
+            __syncwarp();  // the chunk's head weights are in wsm
             // j-outer / k-inner: the head_k dot products advance together (independent
             // FMA chains hide the latency; per k the summation order is unchanged)
 #pragma unroll
@@ -1151,6 +1213,8 @@ __global__ void __launch_bounds__((U8 || LOD) ? kThreadsU8 : kThreads, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) o[j] = __uint_as_float(r[j]);
         }
+        // kEpiFwdTanh with out_hi null: the int8 pieces are the only output
+        if (EPI != kEpiFwdTanh || p.out_hi != nullptr) {
         // staging buffers are free once the previous chunk's bulk store has read them
         if (lane == 0) bulk_wait_read();
         __syncwarp();
@@ -1174,6 +1238,7 @@ __global__ void __launch_bounds__((U8 || LOD) ? kThreadsU8 : kThreads, 1)
             if (!S::kShareLo && p.out_lo != nullptr) tma_store_2d(&tmOutLo, nb, rbase, st_lo);
           }
           bulk_commit();
+        }
         }
         if (EPI == kEpiBwdTanh) {
           // column sums of this warp's 32 rows (rows past M are exact zeros)

@@ -1401,6 +1401,40 @@ struct tlg_policy {
   int* err;
   long P_pad;
   int head_tiles = 1;
+  // Layers >= 2 as exact int8 x int8 tensor-core GEMMs (gemm_i8x2_fwd_kernel): each
+  // layer's tanh outputs leave its epilogue as three fixed-scale int8 pieces (1/127) and the
+  // weights of layers >= 2 as per-row-scaled pieces (quantized when the parameters are
+  // set), so the 1024-wide layers run at the int8 instruction rate instead of three tf32
+  // passes.  The pair kernel tiles 256 rows: batches are evaluated on at least kMinRows
+  // rows (the extra rows are scratch), so every batch size takes the same path and a row's
+  // outputs do not depend on the batch it came in.  Opt-in (TLG_POLICY_I8=1): at C4 the
+  // int8 x int8 kernel streams its operands from L2 at 64-column tiles (three accumulators
+  // fill TMEM) and the layer-1 epilogue pays for the piece stores, 0.73 ms per batch
+  // against 0.62 ms for 3xTF32.
+  static constexpr long kMinRows = 256;
+  bool i8 = false;
+  long rows_cap = 0;                // max(max_batch, kMinRows)
+  int8_t* act_q[2] = {nullptr, nullptr};  // ping-pong [3][rows][h_l]
+  std::vector<int8_t*> wq;          // [l] pieces [3][h_{l+1}][h_l], l >= 1
+  std::vector<float*> wscale;       // [l] row scales [h_{l+1}]
+  bool i8_eligible() const {
+    if (net.L < 2) return false;
+    const char* e = std::getenv("TLG_POLICY_I8");
+    if (!e || std::atoi(e) != 1) return false;
+    for (uint32_t l = 1; l < net.L; ++l)  // pieces need 32-column chunks, K % 16
+      if (net.dims[l] % 32 != 0) return false;
+    return true;
+  }
+  // parameters changed: padded W_1 and the int8 weight pieces of layers >= 2
+  void prepare_params() {
+    pad_w1();
+    if (!i8) return;
+    for (uint32_t l = 1; l < net.L; ++l) {
+      const int in = int(net.dims[l]), outw = int(net.dims[l + 1]);
+      tlg::gemm::launch_quantize_rows(params + net.w_off[l], outw, in, in, wq[l], in, wscale[l],
+                                      stream);
+    }
+  }
   // pipelined batches (tlg_policy_forward_async): two slots of device inputs / outputs, an
   // H2D and a D2H stream around the compute stream, events ordering slot reuse
   struct Slot {
@@ -1420,21 +1454,40 @@ struct tlg_policy {
     P_pad = pad4(net.P);
     params = mem.add<float>(P_pad);
     params_lo = mem.add<float>(P_pad);
-    obs = mem.add<float>(mb * net.D);
+    i8 = i8_eligible();
+    rows_cap = i8 ? std::max(mb, kMinRows) : mb;
+    obs = mem.add<float>(rows_cap * net.D);
     obs_lo = nullptr;
+    if (i8) {
+      long widest = 0;
+      for (uint32_t l = 1; l < net.L; ++l) widest = std::max(widest, long(net.dims[l]));
+      for (int8_t*& q : act_q) q = mem.add<int8_t>(3 * rows_cap * widest);
+      wq.assign(net.L, nullptr);
+      wscale.assign(net.L, nullptr);
+      for (uint32_t l = 1; l < net.L; ++l) {
+        wq[l] = mem.add<int8_t>(3 * long(net.dims[l + 1]) * net.dims[l]);
+        wscale[l] = mem.add<float>(net.dims[l + 1]);
+      }
+      // scratch rows start as zeros (finite); they never reach a caller's outputs
+      TLG_CUDA(cudaMemsetAsync(obs, 0, size_t(rows_cap * net.D) * 4, stream));
+    }
     if (net.padded()) {
-      obs_pad = mem.add<float>(mb * net.D_pad);
+      obs_pad = mem.add<float>(rows_cap * net.D_pad);
+      if (i8) TLG_CUDA(cudaMemsetAsync(obs_pad, 0, size_t(rows_cap * net.D_pad) * 4, stream));
       w1p = mem.add<float>(long(net.dims[1]) * net.D_pad);
       w1p_lo = mem.add<float>(long(net.dims[1]) * net.D_pad);
     }
     head_out = mem.add<float>(mb * (net.A + 1));
-    head_part = mem.add<float>(mb * (net.A + 1) * ((net.head.H + 63) / 64));
+    head_part = mem.add<float>(rows_cap * (net.A + 1) * ((net.head.H + 63) / 64));
     logits = mem.add<float>(mb * net.A);
     probs = mem.add<float>(mb * net.A);
     value = mem.add<float>(mb);
     err = mem.add<int>(4);
     for (uint32_t l = 0; l < net.L; ++l) {
-      act.push_back(mem.add<float>(mb * net.dims[l + 1]));
+      // int8 layers keep their activations as pieces only; the top layer's fp32 plane is
+      // only read when the heads are not fused
+      const bool plane = !i8 || (l + 1 == net.L && net.A + 1 > 8);
+      act.push_back(plane ? mem.add<float>(mb * net.dims[l + 1]) : nullptr);
       act_lo.push_back(nullptr);
     }
   }
@@ -1445,7 +1498,7 @@ struct tlg_policy {
     TLG_CUDA(cudaStreamCreateWithFlags(&h2d_stream, cudaStreamNonBlocking));
     TLG_CUDA(cudaStreamCreateWithFlags(&d2h_stream, cudaStreamNonBlocking));
     for (Slot& sl : pipe) {
-      sl.obs = mem.add<float>(max_batch * net.D);
+      sl.obs = mem.add<float>(rows_cap * net.D);
       sl.logits = mem.add<float>(max_batch * net.A);
       sl.probs = mem.add<float>(max_batch * net.A);
       sl.value = mem.add<float>(max_batch);
@@ -1497,10 +1550,15 @@ void set_params_common(float* params, float* params_lo, long P, long P_pad, cons
 
 void tlg_policy::enqueue(const float* x0, long n, float* lg, float* pr, float* vv) {
   const long D = net.D, A = net.A;
+  // rows the GEMMs evaluate: the int8 pair kernels tile 256 rows (see kMinRows)
+  const long m = i8 ? std::max(n, kMinRows) : n;
   if (net.padded()) {
     TLG_CUDA(cudaMemcpy2DAsync(obs_pad, size_t(net.D_pad) * 4, x0, size_t(D) * 4, size_t(D) * 4,
                                size_t(n), cudaMemcpyDeviceToDevice, stream));
     x0 = obs_pad;
+  } else if (m > n && x0 != obs) {
+    TLG_CUDA(cudaMemcpyAsync(obs, x0, size_t(n * D) * 4, cudaMemcpyDeviceToDevice, stream));
+    x0 = obs;
   }
   // the tf32 residuals of the observations and activations are derived in the GEMMs'
   // shared memory (Operand::lo_smem): no residual planes
@@ -1515,25 +1573,36 @@ void tlg_policy::enqueue(const float* x0, long n, float* lg, float* pr, float* v
       Bop.lo = w1p_lo;
     }
     tlg::gemm::Params gp{};
-    gp.out_hi = act[l];
+    const bool fuse = l + 1 == net.L && net.A + 1 <= 8;
+    // with fused heads nothing reads the top layer's plane
+    gp.out_hi = fuse ? nullptr : act[l];
     gp.out_lo = nullptr;
     gp.ldo = outw;
     gp.bias = params + net.b_off[l];
-    const bool fuse = l + 1 == net.L && net.A + 1 <= 8;
     if (fuse) {
       gp.head_w = params + net.head.wpi;
       gp.head_wv = params + net.head.wv;
       gp.head_k = int(A) + 1;
       gp.head_part = head_part;
     }
-    const int bn =
-        tlg::gemm::launch(Aop, Bop, int(n), outw, in, tlg::gemm::kEpiFwdTanh, gp, 1, stream).bn;
+    int8_t* q_out = i8 && l + 1 < net.L ? act_q[l & 1] : nullptr;
+    int bn;
+    if (i8 && l >= 1) {
+      bn = tlg::gemm::launch_i8x2_fwd(act_q[(l - 1) & 1], wq[l], in, wscale[l], gp.bias, int(m),
+                                      outw, in, gp.out_hi, nullptr, outw, gp.head_w, gp.head_wv,
+                                      gp.head_k, gp.head_part, stream, q_out)
+               .bn;
+    } else {
+      gp.out_q = q_out;
+      if (q_out) gp.out_hi = nullptr;  // the next layer reads the pieces
+      bn = tlg::gemm::launch(Aop, Bop, int(m), outw, in, tlg::gemm::kEpiFwdTanh, gp, 1, stream).bn;
+    }
     if (fuse) head_tiles = (outw + bn - 1) / bn;
   }
   const float* hL = net.L ? act[net.L - 1] : x0;
   if (net.L > 0 && net.A + 1 <= 8) {
     tlg::launch_head_finalize(net.head, params, head_part, head_tiles, n, nullptr, nullptr,
-                              nullptr, lg, pr, vv, err, stream);
+                              nullptr, lg, pr, vv, err, stream, m);
   } else {
     tlg::launch_head_forward(net.head, params, hL, net.head.H, nullptr, n, head_out, nullptr, pr,
                              err, stream);
@@ -1978,7 +2047,7 @@ int tlg_policy_set_params(tlg_policy* p, const double* values, size_t n) {
   return Guard([&] {
     TLG_CUDA(cudaSetDevice(p->device));
     set_params_common(p->params, p->params_lo, p->net.P, p->P_pad, values, n, p->stream);
-    p->pad_w1();
+    p->prepare_params();
     TLG_CUDA(cudaStreamSynchronize(p->stream));
   });
 }
@@ -2012,7 +2081,7 @@ int tlg_policy_set_params_from_learner(tlg_policy* p, tlg_learner* l) {
                                    bytes, p->stream));
     }
     TLG_CUDA(cudaSetDevice(p->device));
-    p->pad_w1();
+    p->prepare_params();
     TLG_CUDA(cudaEventRecord(ev_p, p->stream));
     TLG_CUDA(cudaSetDevice(l->cfg.device));
     TLG_CUDA(cudaStreamWaitEvent(l->stream, ev_p, 0));

@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(256) head_forward_kernel(HeadDesc hd, const fl
 // products; add them in tile order, add the biases, log-softmax.  Thread per frame.
 __global__ void head_finalize_kernel(HeadDesc hd, const float* __restrict__ params,
                                      const float* __restrict__ part, int n_tiles, long F,
-                                     BatchDev bd, int has_batch, float* __restrict__ head_out,
+                                     long part_rows, BatchDev bd, int has_batch, float* __restrict__ head_out,
                                      float* __restrict__ tlogp, float* __restrict__ logits_out,
                                      float* __restrict__ probs_out, float* __restrict__ value_out,
                                      int* __restrict__ err) {
@@ -208,7 +208,7 @@ __global__ void head_finalize_kernel(HeadDesc hd, const float* __restrict__ para
   for (int k = 0; k < 8; ++k) {
     if (k < A1) {
       float acc = 0.f;
-      for (int t = 0; t < n_tiles; ++t) acc += part[(long(t) * F + f) * A1 + k];
+      for (int t = 0; t < n_tiles; ++t) acc += part[(long(t) * part_rows + f) * A1 + k];
       const long boff = k < A ? (hd.bpi >= 0 ? hd.bpi + k : -1) : hd.bv;
       z[k] = acc + (boff >= 0 ? params[boff] : 0.f);
     }
@@ -1277,11 +1277,12 @@ void launch_head_forward(const HeadDesc& hd, const float* params, const float* h
 void launch_head_finalize(const HeadDesc& hd, const float* params, const float* part,
                           int n_tiles, long F, const BatchDev* b, float* head_out, float* tlogp,
                           float* logits_out, float* probs_out, float* value_out, int* err,
-                          cudaStream_t s) {
+                          cudaStream_t s, long part_rows) {
   if (hd.A + 1 > 8) throw CudaError("fused head supports n_actions <= 7");
+  if (part_rows < F) part_rows = F;  // rows of the GEMM that left the partials
   BatchDev bd{};
   if (b) bd = *b;
-  ::tlg::launch_k(head_finalize_kernel, dim3(ceil_div(F, 256)), dim3(256), size_t(0), s, hd, params, part, n_tiles, F, bd,
+  ::tlg::launch_k(head_finalize_kernel, dim3(ceil_div(F, 256)), dim3(256), size_t(0), s, hd, params, part, n_tiles, F, part_rows, bd,
                                                         b ? 1 : 0, head_out, tlogp, logits_out,
                                                         probs_out, value_out, err);
   TLG_CHECK_LAUNCH();

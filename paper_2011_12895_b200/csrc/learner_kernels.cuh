@@ -96,7 +96,7 @@ void launch_head_forward(const HeadDesc& hd, const float* params, const float* h
 void launch_head_finalize(const HeadDesc& hd, const float* params, const float* part,
                           int n_tiles, long F, const BatchDev* b, float* head_out, float* tlogp,
                           float* logits_out, float* probs_out, float* value_out, int* err,
-                          cudaStream_t s);
+                          cudaStream_t s, long part_rows = 0);
 // returns the segments per block of the kernel it chose (the layout of seg_partial)
 int launch_returns(const BatchDev& b, int algo, const HyperDev& hp, const float* tlogp,
                    float* adv, float* target, double* seg_partial, int* err, cudaStream_t s);

@@ -317,6 +317,34 @@ def test_policy_forward_matches_oracle_and_is_batch_invariant(tlg, oracle, case)
     assert np.array_equal(lg3, lg[5:6]) and np.array_equal(v3, v[5:6])
 
 
+@pytest.mark.parametrize("hidden", [(1024, 1024), (64, 32), (96, 64, 32)],
+                         ids=lambda h: "x".join(map(str, h)))
+def test_policy_int8_layers_match_oracle_and_are_batch_invariant(tlg, oracle, hidden,
+                                                                 monkeypatch):
+    """Opt-in serving path (TLG_POLICY_I8=1): layers >= 2 as exact int8 x int8 tensor-core
+    GEMMs over three fixed-scale activation pieces and per-row weight pieces."""
+    monkeypatch.setenv("TLG_POLICY_I8", "1")
+    D, A = 64, 6
+    shape = Shape(FAM["mlp"], D, A, hidden)
+    p = init_params(oracle, shape, 11, scale=0.1)
+    pol = tlg.Policy("mlp", D, A, hidden, max_batch=4096)
+    pol.set_params(p)
+    rng = np.random.default_rng(1)
+    obs = rng.standard_normal((1000, D)).astype(np.float32)
+    lg, pr, v = pol.forward(obs)
+    wl, wp, wv = oracle.forward(shape, p, obs.astype(np.float64))
+    assert close(lg, wl, 1e-4), worst(lg, wl)
+    assert close(pr, wp, 1e-4), worst(pr, wp)
+    assert close(v, wv, 1e-4), worst(v, wv)
+    # batches below the pair kernel's 256 rows run on padded scratch rows: same outputs
+    idx = rng.permutation(1000)[:333]
+    lg2, pr2, v2 = pol.forward(obs[idx])
+    assert np.array_equal(lg2, lg[idx]) and np.array_equal(v2, v[idx])
+    lg3, pr3, v3 = pol.forward(obs[7:9])
+    assert np.array_equal(lg3, lg[7:9]) and np.array_equal(pr3, pr[7:9])
+    assert np.array_equal(v3, v[7:9])
+
+
 # ---------------------------------------------------------------------------
 # Multi-shard semantics (learner.cpp:117-149): per-shard normalisation and 1/n,
 # rank-ordered sum, 1/num_shards.
