@@ -112,7 +112,7 @@ void run(const CUtensorMap& ah, const CUtensorMap& al, const CUtensorMap& bh,
          cudaStream_t stream) {
   auto kern = gemm_tf32x3_kernel<BN, A_MN, B_MN, A_LO, B_LO, EPI, U8, CG, LOD>;
   constexpr int bytes = Smem<BN, A_LO, B_LO, EPI, U8, CG, LOD>::kBytes;
-  constexpr int threads = (U8 || LOD) ? kThreadsU8 : kThreads;
+  constexpr int threads = kernel_threads(BN, EPI, U8, LOD);
   static_assert(bytes <= 227 * 1024, "shared memory budget");
   static std::atomic<unsigned long long> attr{0};  // per device
   ensure_smem_attr(kern, bytes, attr);
@@ -327,7 +327,8 @@ LaunchInfo launch(const Operand& A, const Operand& B, int M, int N, int K, int e
     default: dispatch_bn<64>(A.mn_major, B.mn_major, a_lo, b_lo, epi, u8, lod, ah, al, bh, bl, em, p, grid, stream); break;
   }
   const int tiles = int(grid.x * grid.y * grid.z);
-  return {BN, cg == 2 ? 2 * std::min(tiles, num_sms() / 2) : std::min(tiles, num_sms())};
+  return {BN / epi_groups(BN, epi, u8, lod),
+          cg == 2 ? 2 * std::min(tiles, num_sms() / 2) : std::min(tiles, num_sms())};
 }
 
 }  // namespace tlg::gemm

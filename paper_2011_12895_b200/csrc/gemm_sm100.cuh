@@ -260,6 +260,17 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 
 // ---------------------------------------------------------------------------
 constexpr int kEpiWarps = 4;
+// Epilogue warp groups: the tanh forward on a derived-residual operand (short K: the
+// per-element tanh + fused head dot products are the critical path) runs two groups of 4
+// epilogue warps (warps 2..5 and 10..13) that take alternate 32-column chunks, so every
+// scheduler holds two epilogue warps.  128-column tiles only: launch() picks them for
+// short K loops (the wide tiles' long K loops hide the epilogue, and their pipeline
+// would lose a stage to the extra staging); each group's head partials cover 64 columns
+// (LaunchInfo::bn).
+__host__ __device__ constexpr int epi_groups(int bn, int epi, int u8, int lod) {
+  // (the dX epilogue is written for either count; measured no faster with two groups)
+  return epi == 0 /* kEpiFwdTanh */ && lod != 0 && u8 == 0 && bn == 128 ? 2 : 1;
+}
 constexpr int kColMax = 2048;  // widest N with fused column sums
 constexpr int kStageBuf = 32 * 33;  // per-warp 32x32 transpose buffer (+1 pad: no bank conflicts)
 
@@ -302,7 +313,8 @@ constexpr SmemPlan smem_plan(int BN, bool a_lo, bool b_lo, int epi, int u8, int 
                                  : 0;
   const int head = epi == kEpiFwdTanh ? 1024 : epi == kEpiFwdLoss ? 2048 : 0;
   const int ring = q.u8_ring * q.u8_slot;
-  auto epi_bytes = [&](int blocks) { return kEpiWarps * (blocks * 4096 + head) + q.extra; };
+  const int ew = kEpiWarps * epi_groups(BN, epi, u8, lod);
+  auto epi_bytes = [&](int blocks) { return ew * (blocks * 4096 + head) + q.extra; };
   // blocks: out (+ out_lo) (+ act for bwd, + h staging for the fused loss)
   const int sep_blocks = epi == kEpiStore ? 1 : 2 + (epi == kEpiBwdTanh || epi == kEpiFwdLoss ? 1 : 0);
   const int sep = plan_stages(q.stage, epi_bytes(sep_blocks), ring);
@@ -318,10 +330,10 @@ constexpr SmemPlan smem_plan(int BN, bool a_lo, bool b_lo, int epi, int u8, int 
   q.bar_off = q.ring_off + ring;
   // full/empty per stage, tmem full/empty x2, act-block full x4, converted per stage,
   // u8 ring full/empty per slot
-  q.num_bars = 2 * q.stages + 4 + kEpiWarps + (u8 ? q.stages + 2 * q.u8_ring : 0) +
+  q.num_bars = 2 * q.stages + 4 + ew + (u8 ? q.stages + 2 * q.u8_ring : 0) +
                (lod ? 2 * q.stages : 0);  // lod: converted + local hi-landed per stage
   q.epi_off = (q.bar_off + q.num_bars * 8 + 16 + 1023) / 1024 * 1024;
-  q.bytes = q.epi_off + kEpiWarps * q.warp_epi + q.extra + 1024;  // + 1 KB alignment slack
+  q.bytes = q.epi_off + ew * q.warp_epi + q.extra + 1024;  // + 1 KB alignment slack
   return q;
 }
 
@@ -470,8 +482,12 @@ __device__ __forceinline__ void write_act_pieces(const float* o, int8_t* q, long
   }
 }
 
+__host__ __device__ constexpr int kernel_threads(int bn, int epi, int u8, int lod) {
+  return ((u8 || lod) ? kThreadsU8 : kThreads) + 32 * kEpiWarps * (epi_groups(bn, epi, u8, lod) - 1);
+}
+
 template <int BN, bool A_MN, bool B_MN, bool A_LO, bool B_LO, int EPI, int U8, int CG, int LOD>
-__global__ void __launch_bounds__((U8 || LOD) ? kThreadsU8 : kThreads, 1)
+__global__ void __launch_bounds__(kernel_threads(BN, EPI, U8, LOD), 1)
     gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap tmA_hi,
                        const __grid_constant__ CUtensorMap tmA_lo,
                        const __grid_constant__ CUtensorMap tmB_hi,
@@ -484,6 +500,7 @@ __global__ void __launch_bounds__((U8 || LOD) ? kThreadsU8 : kThreads, 1)
   static_assert(!(U8 && LOD), "derived lo planes and uint8 operands do not mix");
   static_assert(!(LOD & 1) || A_LO, "A lo derived needs the A lo slot");
   static_assert(!(LOD & 2) || B_LO, "B lo derived needs the B lo slot");
+  constexpr int kEG = epi_groups(BN, EPI, U8, LOD);
   // CG == 2: a cluster of two CTAs shares each (256 x BN) tile; rank r owns rows
   // [128 r, 128 r + 128) of A / D and B rows [r BN/2, (r+1) BN/2).  Only rank 0 issues
   // the MMAs (cta_group::2), reading both CTAs' smem and writing both CTAs' TMEM.
@@ -500,12 +517,12 @@ __global__ void __launch_bounds__((U8 || LOD) ? kThreadsU8 : kThreads, 1)
   const uint32_t bar_tfull = bar_empty + S::kStages * 8;  // [2]
   const uint32_t bar_tempty = bar_tfull + 16;               // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + S::kBarOff + S::kNumBars * 8);
-  const uint32_t bar_act = bar_tempty + 16;                 // [4]
-  const uint32_t bar_conv = bar_act + 8 * kEpiWarps;        // [stages] (U8)
+  const uint32_t bar_act = bar_tempty + 16;                 // [epilogue warps]
+  const uint32_t bar_conv = bar_act + 8 * kEpiWarps * kEG;  // [stages] (U8)
   const uint32_t bar_ufull = bar_conv + 8 * S::kStages;     // [ring] (U8)
   const uint32_t bar_uempty = bar_ufull + 8 * S::kU8Ring;   // [ring] (U8)
   const uint32_t bar_hfull = bar_uempty + 8 * S::kU8Ring;   // [stages] (LOD): local tiles landed
-  float* colpart = reinterpret_cast<float*>(smem + S::kEpiOff + kEpiWarps * S::kWarpEpi);
+  float* colpart = reinterpret_cast<float*>(smem + S::kEpiOff + kEpiWarps * kEG * S::kWarpEpi);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -523,9 +540,9 @@ __global__ void __launch_bounds__((U8 || LOD) ? kThreadsU8 : kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(bar_tfull + 8 * a, 1);
-      mbar_init(bar_tempty + 8 * a, kEpiWarps * CG);  // both CTAs' epilogues drain
+      mbar_init(bar_tempty + 8 * a, kEpiWarps * kEG * CG);  // both CTAs' epilogues drain
     }
-    for (int w = 0; w < kEpiWarps; ++w) mbar_init(bar_act + 8 * w, 1);
+    for (int w = 0; w < kEpiWarps * kEG; ++w) mbar_init(bar_act + 8 * w, 1);
     if (LOD) {
       for (int st = 0; st < S::kStages; ++st) {
         mbar_init(bar_conv + 8 * st, 4 * CG);  // one arrive per converter warp (x CTAs)
@@ -708,7 +725,7 @@ __global__ void __launch_bounds__((U8 || LOD) ? kThreadsU8 : kThreads, 1)
         else mma_commit(bar_tfull + 8 * acc_buf);
       }
     }
-  } else if (LOD && warp >= 2 + kEpiWarps) {
+  } else if (LOD && warp >= 2 + kEpiWarps && warp < 2 + 2 * kEpiWarps) {
     // ===== Converter warps 6..9: lo = x - trunc_tf32(x) of the landed hi tiles =====
     // Elementwise over the tile bytes, so the swizzled K- or MN-major layout is kept.
     const int ct = threadIdx.x - (2 + kEpiWarps) * 32;  // 0..127
@@ -1087,7 +1104,8 @@ __global__ void __launch_bounds__((U8 || LOD) ? kThreadsU8 : kThreads, 1)
     // row) -> fused op -> 128-B-swizzled smem staging -> TMA bulk store.  The bwd
     // activation block is TMA-prefetched one chunk ahead into its own swizzled buffer.
     const int q = warp & 3;
-    const int ew = warp - 2;
+    const int grp = warp >= 2 + 2 * kEpiWarps ? 1 : 0;  // epilogue group (kEG == 2)
+    const int ew = grp ? warp - 2 - kEpiWarps : warp - 2;
     const uint32_t blk = sbase + S::kEpiOff + uint32_t(ew * S::kWarpEpi);
     const uint32_t st_out = blk, st_lo = S::kShareLo ? blk : blk + 4096;
     const uint32_t st_act = blk + (S::kEpiBlocks - 1) * 4096;
@@ -1107,10 +1125,13 @@ __global__ void __launch_bounds__((U8 || LOD) ? kThreadsU8 : kThreads, 1)
         tma_load_2d(st_act, &tmAct, nt2 * BN + c, mt2 * kBM * CG + int(rank) * kBM + q * 32, abar);
       }
     };
-    act_issue(cl_id, 0);
+    act_issue(cl_id, 32 * grp);
+    // column partials: slot q (the groups write disjoint chunks of the same slots)
     float* csacc = colpart + kEpiWarps * BN;  // [kColMax] CTA-level column sums
+    const int etid = ew * 32 + lane;          // 0 .. 32 * kEpiWarps * kEG - 1
+    constexpr int kEpiThreads = 32 * kEpiWarps * kEG;
     if (EPI == kEpiBwdTanh && p.colsum != nullptr) {
-      for (int i = threadIdx.x - 64; i < p.N; i += kEpiWarps * 32) csacc[i] = 0.f;
+      for (int i = etid; i < p.N; i += kEpiThreads) csacc[i] = 0.f;
     }
     constexpr int kHK = 8;  // fused head width limit (n_actions + 1)
     const bool do_head = EPI == kEpiFwdTanh && p.head_k > 0;
@@ -1131,7 +1152,7 @@ __global__ void __launch_bounds__((U8 || LOD) ? kThreadsU8 : kThreads, 1)
           wnext[k] = __ldg((k < p.head_k - 1 ? p.head_w + long(k) * p.N : p.head_wv) + col);
       }
     };
-    if (do_head) fetch(cl_id, 0);
+    if (do_head) fetch(cl_id, 32 * grp);
     int it = 0;
     for (int t = cl_id; t < num_tiles; t += n_cl, ++it) {
       int mt, nt, sp;
@@ -1146,7 +1167,7 @@ __global__ void __launch_bounds__((U8 || LOD) ? kThreadsU8 : kThreads, 1)
 #pragma unroll
       for (int k = 0; k < kHK; ++k) zacc[k] = 0.f;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = 32 * grp; c < BN; c += 32 * kEG) {
         const int nb = n0 + c;
         float h[32];
         if (EPI == kEpiBwdTanh) {
@@ -1162,8 +1183,8 @@ __global__ void __launch_bounds__((U8 || LOD) ? kThreadsU8 : kThreads, 1)
           // still in flight (a rare write-after-read race on the act block)
           fence_async_smem();
           __syncwarp();
-          if (c + 32 < BN) act_issue(t, c + 32);
-          else act_issue(t + n_cl, 0);
+          if (c + 32 * kEG < BN) act_issue(t, c + 32 * kEG);
+          else act_issue(t + n_cl, 32 * grp);
         }
         uint32_t r[32];
         tmem_ld32(tbase + uint32_t(c), r);
@@ -1175,8 +1196,8 @@ __global__ void __launch_bounds__((U8 || LOD) ? kThreadsU8 : kThreads, 1)
             // this chunk's head weights -> smem (read back as broadcast LDS.128 below)
 #pragma unroll
             for (int k = 0; k < kHK; ++k) wsm[k * 32 + lane] = wnext[k];
-            if (c + 32 < BN) fetch(t, c + 32);
-            else fetch(t + n_cl, 0);
+            if (c + 32 * kEG < BN) fetch(t, c + 32 * kEG);
+            else fetch(t + n_cl, 32 * grp);
           } else {
             // (measured: the one-chunk-ahead loads slow the head-less, epilogue-bound
             // short-K forward, e.g. C4 layer 1, by 15 %)
@@ -1279,26 +1300,26 @@ __global__ void __launch_bounds__((U8 || LOD) ? kThreadsU8 : kThreads, 1)
         else mbar_arrive(bar_tempty + 8 * acc_buf);
       }
       if (do_head && rbase + lane < p.M) {
-        float* hp = p.head_part + (long(nt) * p.M + rbase + lane) * p.head_k;
+        // kEG groups: one partial slice per group (BN / kEG columns, LaunchInfo::bn)
+        float* hp = p.head_part + (long(nt * kEG + grp) * p.M + rbase + lane) * p.head_k;
 #pragma unroll
         for (int k = 0; k < kHK; ++k)
           if (k < p.head_k) hp[k] = zacc[k];
       }
       if (EPI == kEpiBwdTanh && p.colsum != nullptr) {
         // fixed-order sum of the 4 warps' column partials into the CTA accumulator
-        named_bar(1, kEpiWarps * 32);
-        const int tid = threadIdx.x - 64;
-        for (int cidx = tid; cidx < BN; cidx += kEpiWarps * 32) {
+        named_bar(1, kEpiThreads);
+        for (int cidx = etid; cidx < BN; cidx += kEpiThreads) {
           const int n = n0 + cidx;
           if (n < p.N)
             csacc[n] += colpart[cidx] + colpart[BN + cidx] + colpart[2 * BN + cidx] +
                         colpart[3 * BN + cidx];
         }
-        named_bar(1, kEpiWarps * 32);
+        named_bar(1, kEpiThreads);
       }
     }
     if (EPI == kEpiBwdTanh && p.colsum != nullptr) {
-      for (int i = threadIdx.x - 64; i < p.N; i += kEpiWarps * 32)
+      for (int i = etid; i < p.N; i += kEpiThreads)
         p.colsum[long(blockIdx.x) * p.N + i] = csacc[i];
     }
     if (lane == 0) bulk_wait_all();
@@ -1333,7 +1354,8 @@ struct Operand {
 };
 
 struct LaunchInfo {
-  int bn;    // N tile width (the fused head writes ceil(N / bn) partial rows)
+  int bn;    // N width of one fused-head partial slice (the tile width / epilogue groups):
+             // the fused head writes ceil(N / bn) partial rows
   int ctas;  // persistent CTAs (the fused column sums write this many rows)
 };
 

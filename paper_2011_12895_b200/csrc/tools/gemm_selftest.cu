@@ -537,8 +537,12 @@ int main(int argc, char** argv) {
     check("store K/K", 256, 256, 512, false, false, false, kEpiStore, 1);
     check_lod("LOD fwd tanh K/K", 300, 256, 200, false, false, kEpiFwdTanh, 1, 1);
     check_lod("LOD fwd tanh K/K pair", 4096, 256, 512, false, false, kEpiFwdTanh, 1, 1);
+    // 128-column tiles (short K): two epilogue warp groups on alternate chunks
+    check_lod("LOD fwd tanh K/K pair short-K", 4096, 256, 256, false, false, kEpiFwdTanh, 1, 1);
+    check_lod("LOD fwd tanh K/K short-K N=1024", 1000, 1024, 64, false, false, kEpiFwdTanh, 1, 1);
     check_lod("LOD dX bwd K/MN", 300, 256, 256, false, true, kEpiBwdTanh, 1, 1);
     check_lod("LOD dX bwd K/MN pair", 20480, 512, 512, false, true, kEpiBwdTanh, 1, 1);
+    check_lod("LOD dX bwd K/MN pair short-K", 20480, 256, 256, false, true, kEpiBwdTanh, 1, 1);
     check_lod("LOD dW store MN/MN", 256, 200, 1000, true, true, kEpiStore, 1, 3);
     check_lod("LOD dW store MN/MN split4", 512, 512, 20480, true, true, kEpiStore, 4, 3);
     check_lod("LOD dW store MN/MN split1 pair", 512, 512, 20480, true, true, kEpiStore, 1, 3);
