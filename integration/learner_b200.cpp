@@ -13,6 +13,7 @@
 #include <cstring>
 #include <deque>
 #include <stdexcept>
+#include <string_view>
 #include <thread>
 #include <unordered_map>
 #include <unordered_set>
@@ -104,9 +105,11 @@ struct Pinned {
 }  // namespace
 
 Algo ParseAlgo(const std::string& name) {
-  if (name == "ppo") return Algo::kPpo;
-  if (name == "vtrace") return Algo::kVtrace;
-  if (name == "ppo_vtrace") return Algo::kPpoVtrace;
+  // the reference's two names (learner.cpp:14-18) plus C5's PPO-over-V-trace
+  static constexpr std::pair<std::string_view, Algo> kNames[] = {
+      {"ppo", Algo::kPpo}, {"vtrace", Algo::kVtrace}, {"ppo_vtrace", Algo::kPpoVtrace}};
+  for (const auto& [n, a] : kNames)
+    if (n == name) return a;
   throw std::invalid_argument("unknown algo: " + name);
 }
 
@@ -776,62 +779,60 @@ const ParamBlob& Learner::params() const {
   return params_;
 }
 
+// The record the pool holds for the learning model: the current parameters (mirrored
+// from the device) under the period's key, lineage and hyperparameters, not frozen
+// (learner.cpp:160-172).
 void Learner::Publish() {
-  SyncParams();
-  ModelRecord record;
-  record.model_key = current_key_;
-  record.params = params_;
-  record.hyperparams = hyper_;
-  record.parent_key = parent_key_;
-  record.created_at_us = created_at_us_;
-  record.frozen = false;
-  pool_.PutModel(record);
+  const ParamBlob& now = params();
+  pool_.PutModel(ModelRecord{.model_key = current_key_,
+                             .params = now,
+                             .hyperparams = hyper_,
+                             .parent_key = parent_key_,
+                             .created_at_us = created_at_us_,
+                             .frozen = false});
 }
 
+// Period rollover (learner.cpp:174-186): the final parameters reach the pool before the
+// league freezes the member; then the successor period begins.
 std::string Learner::FinishPeriod() {
-  Publish();  // the frozen pool member must be the final parameters
-  std::string successor = league_.EndLearningPeriod(config_.group);
+  Publish();
+  const std::string successor = league_.EndLearningPeriod(config_.group);
   StartPeriod();
   return successor;
 }
 
 std::string Learner::RunPeriod() {
-  for (std::uint32_t k = 0; k < config_.period_steps; ++k)
-    if (!TrainStep()) return {};
-  return FinishPeriod();
+  std::uint32_t done = 0;
+  while (done < config_.period_steps && TrainStep()) ++done;
+  // a shut-down replay ends the period early: no rollover, empty key
+  return done == config_.period_steps ? FinishPeriod() : std::string();
 }
 
 ThroughputStats Learner::Counters() const {
-  ThroughputStats s;
-  s.rfps = double(replay_.received_steps());
-  s.cfps = double(replay_.consumed_steps());
-  s.update_steps = update_steps_;
-  s.stale_dropped = stale_dropped_.load(std::memory_order_relaxed);
-  return s;
+  // cumulative step counts (not rates), as the reference reports them
+  return ThroughputStats{double(replay_.received_steps()), double(replay_.consumed_steps()),
+                         update_steps_, stale_dropped_.load(std::memory_order_relaxed)};
 }
 
+// `ts=<unix s> group=<g> rfps=<r> cfps=<c> steps=<k>` with the receive / consume rates
+// since the previous call (zero on the first), learner.cpp:197-218.
 void Learner::LogMetricsLine(std::string& out) {
-  using Clock = std::chrono::steady_clock;
-  const double now = std::chrono::duration<double>(Clock::now().time_since_epoch()).count();
-  const std::uint64_t recv = replay_.received_steps();
-  const std::uint64_t cons = replay_.consumed_steps();
-  double rfps = 0.0, cfps = 0.0;
-  if (last_metric_ts_ > 0.0 && now > last_metric_ts_) {
-    const double dt = now - last_metric_ts_;
-    rfps = double(recv - last_metric_recv_) / dt;
-    cfps = double(cons - last_metric_cons_) / dt;
-  }
-  last_metric_ts_ = now;
-  last_metric_recv_ = recv;
-  last_metric_cons_ = cons;
-  const auto wall = std::chrono::duration_cast<std::chrono::seconds>(
-                        std::chrono::system_clock::now().time_since_epoch())
-                        .count();
-  char buf[160];
-  std::snprintf(buf, sizeof(buf), "ts=%lld group=%u rfps=%.1f cfps=%.1f steps=%llu\n",
-                static_cast<long long>(wall), config_.group, rfps, cfps,
-                static_cast<unsigned long long>(update_steps_));
-  out += buf;
+  const double t = std::chrono::duration<double>(
+                       std::chrono::steady_clock::now().time_since_epoch()).count();
+  const std::uint64_t got = replay_.received_steps(), used = replay_.consumed_steps();
+  const double span = t - last_metric_ts_;
+  const bool have_rate = last_metric_ts_ > 0.0 && span > 0.0;
+  const double rfps = have_rate ? double(got - last_metric_recv_) / span : 0.0;
+  const double cfps = have_rate ? double(used - last_metric_cons_) / span : 0.0;
+  last_metric_ts_ = t;
+  last_metric_recv_ = got;
+  last_metric_cons_ = used;
+  const long long unix_s = std::chrono::duration_cast<std::chrono::seconds>(
+                               std::chrono::system_clock::now().time_since_epoch()).count();
+  char line[160];
+  std::snprintf(line, sizeof(line), "ts=%lld group=%u rfps=%.1f cfps=%.1f steps=%llu\n", unix_s,
+                config_.group, rfps, cfps, static_cast<unsigned long long>(update_steps_));
+  out.append(line);
 }
 
 }  // namespace tleague::learner
