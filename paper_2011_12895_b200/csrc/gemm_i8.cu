@@ -91,6 +91,38 @@ void run_i8_fwd(const CUtensorMap& tb, const CUtensorMap& tq, const CUtensorMap&
   TLG_CHECK_LAUNCH();
 }
 
+template <int BN, int CG, int NQ, int NX, int MS = 1, int EG = 1>
+void run_i8_fwd_dec(const CUtensorMap& tb, const CUtensorMap& tq, const CUtensorMap& to,
+                    const CUtensorMap& tl, const I8Params& p, const TileMap& tm,
+                    cudaStream_t stream) {
+  auto kern = gemm_i8_bits_fwd_dec_kernel<BN, CG, NQ, NX, MS, EG>;
+  constexpr int bytes = SmemI8Dec<BN, CG, NQ, NX, MS, EG>::kBytes;
+  constexpr int kThreads = kThreadsI8 + 32 * kEpiWarps * (EG - 1);
+  static std::atomic<unsigned long long> attr{0};  // per device
+  ensure_smem_attr(kern, bytes, attr);
+  const int tiles = tm.m_tiles * tm.n_tiles;
+  if (CG == 1) {
+    ::tlg::launch_k(kern, dim3(std::min(tiles, num_sms())), dim3(kThreads), size_t(bytes),
+                    stream, tb, tq, to, tl, p, tm);
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * std::min(tiles, num_sms() / 2));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = bytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    add_pdl(cfg, cfg.attrs);
+    TLG_CUDA(cudaLaunchKernelEx(&cfg, kern, tb, tq, to, tl, p, tm));
+  }
+  TLG_CHECK_LAUNCH();
+}
+
 // one block per row: max |W[n][:]| (fixed-order tree), then the three pieces
 __global__ void __launch_bounds__(256) quantize_rows_kernel(const float* __restrict__ W, int K,
                                                             long ldw, int8_t* __restrict__ q,
@@ -368,8 +400,8 @@ LaunchInfo launch_i8_bits_fwd(const uint8_t* bits, long rowb, const int8_t* q, l
   if (BN == 256) cg = 2;
   if (const char* e = std::getenv("TLG_I8_CG")) cg = std::atoi(e) == 2 ? 2 : 1;
   // TLG_I8_MC=2: two CTA pairs per cluster share the weight-piece tiles (TMA multicast).
-  // Correct, but measured 1.9x slower at C3 (the pairs run in lockstep on the shared
-  // stages), so single pairs stay the default.
+  // Correct, but slower at C3 (0.22 vs 0.19 ms): L2 traffic drops 15 %, the per-SM
+  // tensor activity does not move, and 4-CTA clusters fit only 132 SMs.
   int mc = 1;
   if (const char* e = std::getenv("TLG_I8_MC"))
     mc = cg == 2 && std::atoi(e) == 2 && M >= 4 * kBM ? 2 : 1;
@@ -382,7 +414,35 @@ LaunchInfo launch_i8_bits_fwd(const uint8_t* bits, long rowb, const int8_t* q, l
   const CUtensorMap tq = make_bytes_map(q, Kp, 3L * N, Kp, kBKi, BN / cg, CU_TENSOR_MAP_SWIZZLE_128B);
   const CUtensorMap to = make_f32_out_map(out, N, M, ldo);
   const CUtensorMap tl = out_lo ? make_f32_out_map(out_lo, N, M, ldo) : CUtensorMap{};
-  if (BN == 256) run_i8_fwd<256, 2>(tb, tq, to, tl, p, tm, stream);
+  // Default for CTA pairs without a residual plane and N > 128: 256-column tiles on
+  // decoupled operand rings with two epilogue warp groups (gemm_i8_bits_fwd_dec_kernel
+  // <256, 2, NQ 2, NX 2, MS 1, EG 2>): x is expanded once per M tile, the N = 256 MMAs
+  // read fewer operand bytes per product, and the eight epilogue warps halve the drain
+  // the single-buffered accumulators expose (C3: 0.167 vs 0.188 ms).  TLG_I8_DEC selects
+  // the variants measured against it: 0 = coupled stages,
+  // 4x3 = decoupled rings at 128 columns, m2e = two M subtiles per CTA, b256 = one group.
+  int dec = cg == 2 && mc == 1 && out_lo == nullptr && N > 128 && !std::getenv("TLG_I8_BN")
+                ? 257 : 0;
+  if (const char* e = std::getenv("TLG_I8_DEC"); e && dec != 0)
+    dec = std::strcmp(e, "4x3") == 0 ? 43 : std::strcmp(e, "m2e") == 0 ? 3
+        : std::strcmp(e, "b256") == 0 ? 256 : std::strcmp(e, "0") == 0 ? 0 : 257;
+  if (dec == 3) {
+    // two 128-row M subtiles per CTA share each weight-piece tile (half the L2 -> SM
+    // piece traffic per output), accumulators single-buffered
+    const TileMap tm2{ceil_div(M, kBM * 2 * 2), ceil_div(N, BN), 1};
+    const CUtensorMap tb2 = make_bytes_map(bits, rowb, M, rowb, kBKi / 8, 2 * kBM, CU_TENSOR_MAP_SWIZZLE_NONE);
+    run_i8_fwd_dec<128, 2, 2, 2, 2, 2>(tb2, tq, to, tl, p, tm2, stream);
+    return {BN, 2 * std::min(tm2.m_tiles * tm2.n_tiles, num_sms() / 2)};
+  }
+  if (dec == 256 || dec == 257) {
+    const TileMap tmw{ceil_div(M, kBM * 2), ceil_div(N, 256), 1};
+    const CUtensorMap tqw = make_bytes_map(q, Kp, 3L * N, Kp, kBKi, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (dec == 257) run_i8_fwd_dec<256, 2, 2, 2, 1, 2>(tb, tqw, to, tl, p, tmw, stream);
+    else run_i8_fwd_dec<256, 2, 2, 2>(tb, tqw, to, tl, p, tmw, stream);
+    return {256, 2 * std::min(tmw.m_tiles * tmw.n_tiles, num_sms() / 2)};
+  }
+  if (dec == 43) run_i8_fwd_dec<128, 2, 4, 3>(tb, tq, to, tl, p, tm, stream);
+  else if (BN == 256) run_i8_fwd<256, 2>(tb, tq, to, tl, p, tm, stream);
   else if (mc == 2) run_i8_fwd<128, 2, 2>(tb, tq, to, tl, p, tm, stream);
   else if (cg == 2) run_i8_fwd<128, 2>(tb, tq, to, tl, p, tm, stream);
   else run_i8_fwd<128, 1>(tb, tq, to, tl, p, tm, stream);

@@ -146,6 +146,89 @@ __device__ __forceinline__ void expand_bit_row(const uint8_t* src, uint8_t* x_ti
   }
 }
 
+// Epilogue of the bit-plane forward (warps 2..5; warp % 4 = TMEM lane quadrant): per
+// 32-column chunk TMEM -> registers (thread = row) -> s (acc_a 2^-7 + acc_b 2^-14) + bias
+// -> tanh -> [int8 activation pieces] -> swizzled smem block -> TMA store of the full
+// plane (+ the tf32 residual plane through a second block when `lo_block`).
+// row_off: this CTA's first row inside a kRowsT-row tile; leader: the CTA of the cluster
+// whose tempty barrier counts the drain; MS: 128-row M subtiles per CTA and tile (their
+// accumulator pairs side by side in TMEM, rows row_off + 128 s).
+template <int BN, int CG, int KBUFS, int MS = 1, int EG = 1>
+__device__ __forceinline__ void i8_fwd_epilogue(const I8Params& p, const TileMap& tm,
+                                                const CUtensorMap* tmOut,
+                                                const CUtensorMap* tmOutLo, uint32_t tmem_base,
+                                                uint32_t bar_tfull, uint32_t bar_tempty,
+                                                uint32_t leader, uint32_t row_off, int kRowsT,
+                                                int cl_id, int n_cl, uint32_t blk,
+                                                uint8_t* blk_ptr, bool lo_block) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = warp & 3;
+  // EG == 2: a second group of 4 epilogue warps (warps 10..13) takes the odd chunks
+  const int grp = EG == 2 && warp >= 2 + 2 * kEpiWarps ? 1 : 0;
+  const int num_tiles = tm.m_tiles * tm.n_tiles;
+  const bool write_lo = lo_block && p.write_lo;
+  int it = 0;
+  for (int t = cl_id; t < num_tiles; t += n_cl, ++it) {
+    const int nt = t % tm.n_tiles, mt = t / tm.n_tiles;
+    const int n0 = nt * BN;
+    const int acc_buf = it % KBUFS;
+    mbar_wait(bar_tfull + 8 * acc_buf, (it / KBUFS) & 1);
+    tc_fence_after();
+#pragma unroll 1
+    for (int sub = 0; sub < MS; ++sub) {
+    const int rbase = mt * kRowsT + int(row_off) + sub * kBM + q * 32;
+    const uint32_t ta = tmem_base + uint32_t((acc_buf * MS + sub) * 2 * BN) + (uint32_t(q * 32) << 16);
+    const uint32_t tb = ta + uint32_t(BN);
+#pragma unroll 1
+    for (int c = 32 * grp; c < BN; c += 32 * EG) {
+      const int nb = n0 + c;
+      uint32_t ra[32], rb[32];
+      tmem_ld32(ta + uint32_t(c), ra);
+      tmem_ld32(tb + uint32_t(c), rb);
+      const bool colok = nb + lane < p.N;
+      const float sc = colok ? __ldg(p.scale + nb + lane) : 0.f;
+      const float bi = colok ? __ldg(p.bias + nb + lane) : 0.f;
+      float o[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float s = __shfl_sync(0xffffffffu, sc, j);
+        const float bj = __shfl_sync(0xffffffffu, bi, j);
+        const float z = fmaf(float(int(ra[j])), s * 0.0078125f,
+                             float(int(rb[j])) * (s * 6.103515625e-05f));
+        o[j] = tanh_fast(z + bj);
+      }
+      // the same activations as int8 pieces for the next layer's int8 GEMM
+      if (p.out_q != nullptr && nb < p.N && rbase + lane < p.M)
+        write_act_pieces(o, p.out_q, long(p.M) * p.N, long(rbase + lane) * p.N + nb);
+      if (lane == 0) bulk_wait_read();
+      __syncwarp();
+#pragma unroll
+      for (int j4 = 0; j4 < 8; ++j4) {
+        *reinterpret_cast<float4*>(blk_ptr + swz(lane, j4)) =
+            make_float4(o[4 * j4], o[4 * j4 + 1], o[4 * j4 + 2], o[4 * j4 + 3]);
+        if (write_lo)
+          *reinterpret_cast<float4*>(blk_ptr + 4096 + swz(lane, j4)) = make_float4(
+              o[4 * j4] - tf32_hi(o[4 * j4]), o[4 * j4 + 1] - tf32_hi(o[4 * j4 + 1]),
+              o[4 * j4 + 2] - tf32_hi(o[4 * j4 + 2]), o[4 * j4 + 3] - tf32_hi(o[4 * j4 + 3]));
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(tmOut, nb, rbase, blk);
+        if (write_lo) tma_store_2d(tmOutLo, nb, rbase, blk + 4096);
+        bulk_commit();
+      }
+    }
+    }
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) {
+      if (CG == 2) mbar_arrive_cluster(map_rank(bar_tempty + 8 * acc_buf, leader));
+      else mbar_arrive(bar_tempty + 8 * acc_buf);
+    }
+  }
+}
+
 // MC == 2 (CG == 2 only): clusters of two CTA pairs stacked along M (512-row tiles)
 // sharing each weight-piece tile: pair 0 TMA-multicasts it into both pairs' smem, halving
 // the L2->SM piece traffic that bounds this kernel.
@@ -356,67 +439,265 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
     }
   } else {
     // ===== epilogue: warps 2..5 own TMEM lane quadrants (warp % 4) =====
-    const int q = warp & 3;
     const int ew = warp - 2;
-    const uint32_t blk = sbase + S::kEpiOff + uint32_t(ew * 2 * 4096);
-    uint8_t* blk_ptr = smem + S::kEpiOff + ew * 2 * 4096;
-    int it = 0;
-    for (int t = cl_id; t < num_tiles; t += n_cl, ++it) {
-      const int nt = t % tm.n_tiles, mt = t / tm.n_tiles;
-      const int m0 = mt * kRowsT + int(pair) * kBM * CG + int(rank) * kBM, n0 = nt * BN;
-      const int rbase = m0 + q * 32;
-      const int acc_buf = it % S::kBufs;
-      mbar_wait(bar_tfull + 8 * acc_buf, (it / S::kBufs) & 1);
-      tc_fence_after();
-      const uint32_t ta = tmem_base + uint32_t(acc_buf * 2 * BN) + (uint32_t(q * 32) << 16);
-      const uint32_t tb = ta + uint32_t(BN);
-#pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        const int nb = n0 + c;
-        uint32_t ra[32], rb[32];
-        tmem_ld32(ta + uint32_t(c), ra);
-        tmem_ld32(tb + uint32_t(c), rb);
-        const bool colok = nb + lane < p.N;
-        const float sc = colok ? __ldg(p.scale + nb + lane) : 0.f;
-        const float bi = colok ? __ldg(p.bias + nb + lane) : 0.f;
-        float o[32];
+    i8_fwd_epilogue<BN, CG, S::kBufs>(p, tm, &tmOut, &tmOutLo, tmem_base, bar_tfull, bar_tempty,
+                                      leader, pair * kBM * CG + rank * kBM, kRowsT, cl_id, n_cl,
+                                      sbase + S::kEpiOff + uint32_t(ew * 2 * 4096),
+                                      smem + S::kEpiOff + ew * 2 * 4096, true);
+    if (lane == 0) bulk_wait_all();
+  }
+
+  tc_fence_before();
+  if (CG == 2) cluster_sync_all();
+  else __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    if (CG == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "n"(S::kTmemCols));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "n"(S::kTmemCols));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Decoupled-ring variant of the bit-plane forward.  In gemm_i8_bits_fwd_kernel one stage
+// holds both operands of a k-block (x, x<<7 from the converters, the three weight-piece
+// tiles by TMA from L2), so a released stage waits for the slower of the two refills and
+// only three 56 KB stages fit.  Here the two operands have their own rings, sized by
+// their refill latency:
+//   Q ring  NQ x 24 KB  weight pieces (TMA, L2 latency), refilled NQ k-blocks ahead
+//   X ring  NX x 32 KB  expanded planes (converter warps, a few hundred cycles)
+//   bit rows 4 x 2 KB   (TMA from HBM, feeding the converters)
+// The MMA of k-block kb waits for Q slot kb % NQ and X slot kb % NX and releases both
+// with one commit each.  The epilogue stages through one 4 KB block per warp (the
+// residual plane is not written: write_lo must be 0).
+template <int BN, int CG, int NQ, int NX, int MS = 1, int EG = 1>
+struct SmemI8Dec {
+  static constexpr int kX = kBM * kBKi;           // 16 KB operand tile (x, x<<7)
+  static constexpr int kBits = MS * kBM * kBKi / 8;  // packed source rows of the CTA's rows
+  static constexpr int kBN = BN / CG;
+  static constexpr int kQ = kBN * kBKi;           // one piece tile
+  static constexpr int kQSlot = 3 * kQ;
+  static constexpr int kXSlot = MS * 2 * kX;      // per M subtile: x, x<<7
+  static constexpr int kRing = MS == 1 ? 4 : 2;
+  static constexpr int kXOff = NQ * kQSlot;
+  static constexpr int kRingOff = kXOff + NX * kXSlot;
+  static constexpr int kBarOff = kRingOff + kRing * kBits;
+  // q_full, q_empty [NQ]; x_full, x_empty [NX]; u_full, u_empty [ring]; tfull, tempty [2]
+  static constexpr int kNumBars = 2 * NQ + 2 * NX + 2 * kRing + 4;
+  static constexpr int kEpiOff = (kBarOff + kNumBars * 8 + 16 + 1023) / 1024 * 1024;
+  static constexpr int kBytes = kEpiOff + EG * kEpiWarps * 4096 + 1024;
+  static constexpr int kBufs = 4 * BN * MS <= 512 ? 2 : 1;
+  static constexpr int kTmemCols = 2 * BN * MS * kBufs;
+  static_assert(kQSlot % 1024 == 0 && kXSlot % 1024 == 0, "1 KB swizzle alignment");
+  static_assert(NQ >= 2 && NX >= 2, "rings need two slots");
+  static_assert(kBytes <= 227 * 1024, "shared memory budget");
+};
+
+// ring cursor: slot and phase of the n-th use
+struct RingPos {
+  int slot = 0;
+  uint32_t phase = 0;
+  __device__ __forceinline__ void next(int n) {
+    if (++slot == n) {
+      slot = 0;
+      phase ^= 1u;
+    }
+  }
+};
+
+template <int BN, int CG, int NQ, int NX, int MS = 1, int EG = 1>
+__global__ void __launch_bounds__(kThreadsI8 + 32 * kEpiWarps * (EG - 1), 1)
+    gemm_i8_bits_fwd_dec_kernel(const __grid_constant__ CUtensorMap tmBits,
+                                const __grid_constant__ CUtensorMap tmQ,
+                                const __grid_constant__ CUtensorMap tmOut,
+                                const __grid_constant__ CUtensorMap tmOutLo, const I8Params p,
+                                const TileMap tm) {
+  using S = SmemI8Dec<BN, CG, NQ, NX, MS, EG>;
+  const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
+  const int cl_id = CG == 2 ? int(blockIdx.x >> 1) : int(blockIdx.x);
+  const int n_cl = CG == 2 ? int(gridDim.x >> 1) : int(gridDim.x);
+  // rows per tile; CTA `rank` holds rows [rank * 128 MS, (rank + 1) * 128 MS) of it, and
+  // M subtile s of the pair MMA is rows 128 s of each CTA's block
+  constexpr int kRowsT = kBM * CG * MS;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t q_full = sbase + S::kBarOff;
+  const uint32_t q_empty = q_full + 8 * NQ;
+  const uint32_t x_full = q_empty + 8 * NQ;
+  const uint32_t x_empty = x_full + 8 * NX;
+  const uint32_t u_full = x_empty + 8 * NX;
+  const uint32_t u_empty = u_full + 8 * S::kRing;
+  const uint32_t bar_tfull = u_empty + 8 * S::kRing;  // [2]
+  const uint32_t bar_tempty = bar_tfull + 16;         // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + S::kBarOff + S::kNumBars * 8);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int num_tiles = tm.m_tiles * tm.n_tiles;
+  const int kb_total = (p.K + kBKi - 1) / kBKi;
+  auto leader_bar = [&](uint32_t a) { return CG == 2 ? map_rank0(a) : a; };
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmBits);
+    prefetch_tmap(&tmQ);
+    for (int i = 0; i < NQ; ++i) {
+      mbar_init(q_full + 8 * i, 1);
+      mbar_init(q_empty + 8 * i, 1);
+    }
+    for (int i = 0; i < NX; ++i) {
+      mbar_init(x_full + 8 * i, kConvWarps * CG);
+      mbar_init(x_empty + 8 * i, 1);
+    }
+    for (int u = 0; u < S::kRing; ++u) {
+      mbar_init(u_full + 8 * u, 1);
+      mbar_init(u_empty + 8 * u, kConvWarps);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(bar_tfull + 8 * a, 1);
+      mbar_init(bar_tempty + 8 * a, kEpiWarps * EG * CG);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    if (CG == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "n"(S::kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "n"(S::kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+  }
+  tc_fence_before();
+  if (CG == 2) cluster_sync_all();
+  else __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();
+  pdl_trigger();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer: weight pieces NQ k-blocks ahead of the MMA; bit rows up to
+      // kRing k-blocks ahead of the pieces (the converters consume them in order) =====
+      RingPos qp, up;
+      int bt = cl_id, bkb = 0;
+      long issued_bits = 0, issued_q = 0;
+      for (int t = cl_id; t < num_tiles; t += n_cl) {
+        const int n0 = (t % tm.n_tiles) * BN + int(rank) * S::kBN;
+        for (int kb = 0; kb < kb_total; ++kb, ++issued_q) {
+          while (bt < num_tiles && issued_bits < issued_q + S::kRing) {
+            mbar_wait(u_empty + 8 * up.slot, up.phase ^ 1);
+            mbar_expect_tx(u_full + 8 * up.slot, S::kBits);
+            const int bm0 = (bt / tm.n_tiles) * kRowsT + int(rank) * kBM * MS;
+            tma_load_2d(sbase + S::kRingOff + up.slot * S::kBits, &tmBits, bkb * (kBKi / 8),
+                        bm0, u_full + 8 * up.slot);
+            ++issued_bits;
+            if (++bkb == kb_total) {
+              bkb = 0;
+              bt += n_cl;
+            }
+            up.next(S::kRing);
+          }
+          mbar_wait(q_empty + 8 * qp.slot, qp.phase ^ 1);
+          const uint32_t dst = sbase + qp.slot * S::kQSlot;
+          const uint32_t full = leader_bar(q_full + 8 * qp.slot);
+          if (rank == 0) mbar_expect_tx(q_full + 8 * qp.slot, S::kQSlot * CG);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float s = __shfl_sync(0xffffffffu, sc, j);
-          const float bj = __shfl_sync(0xffffffffu, bi, j);
-          const float z = fmaf(float(int(ra[j])), s * 0.0078125f,
-                               float(int(rb[j])) * (s * 6.103515625e-05f));
-          o[j] = tanh_fast(z + bj);
+          for (int pc = 0; pc < 3; ++pc) {
+            const int row = pc * int(p.q_rows) + n0;
+            if (CG == 2) tma_load_2d_pair(dst + pc * S::kQ, &tmQ, kb * kBKi, row, full);
+            else tma_load_2d(dst + pc * S::kQ, &tmQ, kb * kBKi, row, full);
+          }
+          qp.next(NQ);
         }
-        // the same activations as int8 pieces for the next layer's int8 GEMM
-        if (p.out_q != nullptr && nb < p.N && rbase + lane < p.M)
-          write_act_pieces(o, p.out_q, long(p.M) * p.N, long(rbase + lane) * p.N + nb);
-        if (lane == 0) bulk_wait_read();
-        __syncwarp();
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // ===== MMA issuer =====
+      constexpr uint32_t idesc = make_idesc_i8<BN, CG>();
+      RingPos qp, xp;
+      int it = 0;
+      for (int t = cl_id; t < num_tiles; t += n_cl, ++it) {
+        const int acc_buf = it % S::kBufs;
+        mbar_wait(bar_tempty + 8 * acc_buf, ((it / S::kBufs) & 1) ^ 1);
+        tc_fence_after();
+        for (int kb = 0; kb < kb_total; ++kb) {
+          mbar_wait(q_full + 8 * qp.slot, qp.phase);
+          mbar_wait(x_full + 8 * xp.slot, xp.phase);
+          tc_fence_after();
+          const uint32_t qs = sbase + qp.slot * S::kQSlot;
 #pragma unroll
-        for (int j4 = 0; j4 < 8; ++j4) {
-          *reinterpret_cast<float4*>(blk_ptr + swz(lane, j4)) =
-              make_float4(o[4 * j4], o[4 * j4 + 1], o[4 * j4 + 2], o[4 * j4 + 3]);
-          if (p.write_lo)
-            *reinterpret_cast<float4*>(blk_ptr + 4096 + swz(lane, j4)) = make_float4(
-                o[4 * j4] - tf32_hi(o[4 * j4]), o[4 * j4 + 1] - tf32_hi(o[4 * j4 + 1]),
-                o[4 * j4 + 2] - tf32_hi(o[4 * j4 + 2]), o[4 * j4 + 3] - tf32_hi(o[4 * j4 + 3]));
+          for (int sub = 0; sub < MS; ++sub) {
+          // the M subtiles share this k-block's weight-piece tiles
+          const uint32_t tacc_a = tmem_base + uint32_t((acc_buf * MS + sub) * 2 * BN);
+          const uint32_t tacc_b = tacc_a + uint32_t(BN);
+          const uint32_t xs = sbase + S::kXOff + xp.slot * S::kXSlot + sub * 2 * S::kX;
+#pragma unroll
+          for (int k = 0; k < kBKi / 32; ++k) {
+            const uint64_t dx = make_sdesc<false>(xs + k * 32, 16, 1024);
+            const uint64_t dx7 = make_sdesc<false>(xs + S::kX + k * 32, 16, 1024);
+            const uint64_t dq0 = make_sdesc<false>(qs + k * 32, 16, 1024);
+            const uint64_t dq1 = make_sdesc<false>(qs + S::kQ + k * 32, 16, 1024);
+            const uint64_t dq2 = make_sdesc<false>(qs + 2 * S::kQ + k * 32, 16, 1024);
+            const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
+            mma_i8<CG>(tacc_a, dx7, dq0, idesc, acc);
+            mma_i8<CG>(tacc_a, dx, dq1, idesc, 1u);
+            mma_i8<CG>(tacc_b, dx, dq2, idesc, acc);
+          }
+          }
+          if (CG == 2) {
+            mma_commit_pair(q_empty + 8 * qp.slot);
+            mma_commit_pair(x_empty + 8 * xp.slot);
+          } else {
+            mma_commit(q_empty + 8 * qp.slot);
+            mma_commit(x_empty + 8 * xp.slot);
+          }
+          qp.next(NQ);
+          xp.next(NX);
         }
+        if (CG == 2) mma_commit_pair(bar_tfull + 8 * acc_buf);
+        else mma_commit(bar_tfull + 8 * acc_buf);
+      }
+    }
+  } else if (warp >= 2 + kEpiWarps && warp < 2 + kEpiWarps + kConvWarps) {
+    // ===== converters: 16-B bit row -> 128-B x row and x<<7 row (SW128 K-major) =====
+    const int r = threadIdx.x - (2 + kEpiWarps) * 32;  // tile row 0..127
+    RingPos xp, up;
+    for (int t = cl_id; t < num_tiles; t += n_cl) {
+      for (int kb = 0; kb < kb_total; ++kb) {
+        mbar_wait(u_full + 8 * up.slot, up.phase);           // bit rows arrived
+        mbar_wait(x_empty + 8 * xp.slot, xp.phase ^ 1);      // the MMA released the slot
+        uint8_t* xs = smem + S::kXOff + xp.slot * S::kXSlot;
+#pragma unroll
+        for (int sub = 0; sub < MS; ++sub)
+          expand_bit_row(smem + S::kRingOff + up.slot * S::kBits + (sub * kBM + r) * 16,
+                         xs + sub * 2 * S::kX, xs + sub * 2 * S::kX + S::kX, r);
         fence_async_smem();
         __syncwarp();
         if (lane == 0) {
-          tma_store_2d(&tmOut, nb, rbase, blk);
-          if (p.write_lo) tma_store_2d(&tmOutLo, nb, rbase, blk + 4096);
-          bulk_commit();
+          if (CG == 2) mbar_arrive_cluster(map_rank0(x_full + 8 * xp.slot));
+          else mbar_arrive(x_full + 8 * xp.slot);
+          mbar_arrive(u_empty + 8 * up.slot);
         }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if (CG == 2) mbar_arrive_cluster(to_leader(bar_tempty + 8 * acc_buf));
-        else mbar_arrive(bar_tempty + 8 * acc_buf);
+        up.next(S::kRing);
+        xp.next(NX);
       }
     }
+  } else {
+    // ===== epilogue (warps 2..5, + 10..13 when EG == 2) =====
+    const int ew = warp < 2 + kEpiWarps ? warp - 2 : warp - 2 - kConvWarps;
+    i8_fwd_epilogue<BN, CG, S::kBufs, MS, EG>(p, tm, &tmOut, &tmOutLo, tmem_base, bar_tfull,
+                                          bar_tempty, 0u, rank * kBM * MS, kRowsT, cl_id, n_cl,
+                                      sbase + S::kEpiOff + uint32_t(ew * 4096),
+                                      smem + S::kEpiOff + ew * 4096, false);
     if (lane == 0) bulk_wait_all();
   }
 

@@ -223,6 +223,8 @@ void check(const char* name, int M, int N, int K, bool a_mn, bool b_mn, bool a_e
 }
 
 // Binary planes (bit-packed) x fixed-point int8 pieces of W (kind::i8), fused bias + tanh.
+static bool g_i8_nolo = false;  // the consumers derive the residual: no out_lo plane
+
 void check_i8(const char* name, int M, int N, int K) {
   std::mt19937 rng(M * 17 + N * 3 + K);
   Buf A, B, bias;
@@ -250,7 +252,8 @@ void check_i8(const char* name, int M, int N, int K) {
   TLG_CUDA(cudaMalloc(&out, long(M) * N * 4));
   TLG_CUDA(cudaMalloc(&out_lo, long(M) * N * 4));
   gemm::launch_quantize_rows(B.x, N, K, K, q, Kp, scale, 0);
-  gemm::launch_i8_bits_fwd(bits, rowb, q, Kp, scale, bias.x, M, N, K, out, out_lo, N, 0);
+  float* lo_arg = g_i8_nolo ? nullptr : out_lo;
+  gemm::launch_i8_bits_fwd(bits, rowb, q, Kp, scale, bias.x, M, N, K, out, lo_arg, N, 0);
   TLG_CUDA(cudaDeviceSynchronize());
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
@@ -258,7 +261,7 @@ void check_i8(const char* name, int M, int N, int K) {
   cudaEventRecord(e0);
   const int reps = 5;
   for (int i = 0; i < reps; ++i)
-    gemm::launch_i8_bits_fwd(bits, rowb, q, Kp, scale, bias.x, M, N, K, out, out_lo, N, 0);
+    gemm::launch_i8_bits_fwd(bits, rowb, q, Kp, scale, bias.x, M, N, K, out, lo_arg, N, 0);
   cudaEventRecord(e1);
   TLG_CUDA(cudaDeviceSynchronize());
   float ms = 0;
@@ -281,7 +284,7 @@ void check_i8(const char* name, int M, int N, int K) {
     u &= 0xFFFFE000u;
     float th;
     std::memcpy(&th, &u, 4);
-    if (hl[i] != hh[i] - th) got = 1e9;  // residual plane = x - trunc_tf32(x)
+    if (!g_i8_nolo && hl[i] != hh[i] - th) got = 1e9;  // residual plane = x - trunc_tf32(x)
     const double want = std::tanh(hr[i] + hbias[n]);
     const double err = std::fabs(got - want) / (hab[i] + 1.0);
     if (!(err <= 2e-6)) ++bad;
@@ -561,6 +564,12 @@ int main(int argc, char** argv) {
     check_i8("I8 bits fwd", 300, 256, 200);
     check_i8("I8 bits fwd N=100 K=1936", 700, 100, 1936);
     check_i8("I8 bits fwd pair", 4096, 256, 1936);
+    g_i8_nolo = true;  // decoupled-ring kernel (no residual plane)
+    check_i8("I8 bits fwd pair no-lo", 4096, 256, 1936);
+    check_i8("I8 bits fwd pair no-lo ragged", 700, 200, 1000);
+    check_i8("I8 bits fwd pair no-lo ragged pairs", 20000, 200, 1000);  // 256-col tiles
+    check_i8("I8 bits fwd pair no-lo C3", 131072, 256, 1936);
+    g_i8_nolo = false;
     check_i8x2("I8x2 fwd", 512, 256, 256);
     check_i8x2("I8x2 fwd ragged", 700, 200, 96);
     check_i8_dw("I8 bits dW", 128, 200, 1000, 2);
@@ -568,7 +577,10 @@ int main(int argc, char** argv) {
     check_i8_dw("I8 bits dW ragged", 256, 300, 1300, 4);
     if (argc > 1 && std::string(argv[1]) == "i8") {
       check_i8("perf I8 bits fwd C3 L1", 131072, 256, 1936);
-      check_i8("perf I8 bits fwd C3 L1", 131072, 256, 1936);
+      g_i8_nolo = true;
+      check_i8("perf I8 bits fwd C3 L1 no-lo", 131072, 256, 1936);
+      check_i8("perf I8 bits fwd C3 L1 no-lo", 131072, 256, 1936);
+      g_i8_nolo = false;
     } else if (argc > 1 && std::string(argv[1]) == "c5") {
       g_noref = true;  // C5 trunk shapes (4x2048, 131,072 frames per shard)
       check("perf fwd C5", 131072, 2048, 2048, false, false, false, kEpiFwdTanh, 1);
