@@ -520,8 +520,9 @@ def main():
     t_dom = gms[dom_g] / 1e3
     achieved = gflops[dom_g] / t_dom / 1e12
     desc = {
-        "fwd1": ("gemm_i8_bits_fwd_kernel layer-1 forward (tcgen05.mma kind::i8: bit-packed "
-                 "binary planes x 3 fixed-point int8 weight pieces, exact int32 accumulate)"
+        "fwd1": ("gemm_i8_bits_fwd_dec_kernel layer-1 forward (tcgen05.mma kind::i8: "
+                 "bit-packed binary planes x 3 fixed-point int8 weight pieces, exact int32 "
+                 "accumulate; 256-column tiles, decoupled operand rings)"
                  if obs_bits else
                  "gemm_tf32x3_kernel layer-1 forward (tcgen05.mma kind::tf32, obs exact -> "
                  "2 MMA passes)"),
