@@ -324,8 +324,10 @@ def main():
 
     # ---- device-resident timed region (no instrumentation: small steps replay as graphs)
     # (at least two passes over the resident batches: each one's CUDA graph is captured
-    # on first use and replayed once before the timed region)
-    for i in range(max(args.warmup, 2 * nb)):
+    # on first use and replayed once before the timed region; at N > 1 at least 32 steps,
+    # since the first timed region on a fresh multi-GPU box has read up to 1.7x slow)
+    n_warm = max(args.warmup, 2 * nb, 32 if world > 1 else 0)
+    for i in range(n_warm):
         lrn.train_step(dev[i % nb], on_device=True)
     barrier()
     torch.cuda.synchronize()
@@ -355,7 +357,7 @@ def main():
         lw = make_learner(S_o)
         hw, dw = make_batches(S_o)
         fw = [int(h.valid_steps.sum()) for h in hw]
-        for i in range(max(args.warmup, 2 * len(dw))):
+        for i in range(max(args.warmup, 2 * len(dw), 32)):
             lw.train_step(dw[i % len(dw)], on_device=True)
         sw = torch.cuda.ExternalStream(lw.stream(), device=local)
         barrier()
@@ -690,7 +692,8 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "steps": args.steps, "warmup": args.warmup, "warmup_steps_run": n_warm,
+            "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
             "config": {"workload": cfg.name, "note": cfg.note, "algo": cfg.algo,
