@@ -245,7 +245,9 @@ int tlg_policy_forward(tlg_policy* p, const float* obs, size_t n, float* logits,
  * forward and batch k-1's D2H (page-locked host buffers overlap; pageable ones still
  * work).  Two batches are in flight at most (enqueuing a third waits for the oldest).  A
  * batch's host buffers must stay valid until tlg_policy_wait(ticket) returns; results are
- * the same as tlg_policy_forward's. */
+ * the same as tlg_policy_forward's.  tlg_policy_wait reports that batch's own errors
+ * (TLG_INVALID_ARGUMENT: a tabular observation that is not one-hot) and never waits for
+ * the batch enqueued after it. */
 int tlg_policy_forward_async(tlg_policy* p, const float* obs, size_t n, float* logits,
                              float* probs, float* value, uint64_t* ticket);
 int tlg_policy_wait(tlg_policy* p, uint64_t ticket);

@@ -1439,13 +1439,14 @@ struct tlg_policy {
   // H2D and a D2H stream around the compute stream, events ordering slot reuse
   struct Slot {
     float *obs = nullptr, *logits = nullptr, *probs = nullptr, *value = nullptr;
+    int* err = nullptr;       // this batch's error flags (device), read back with its outputs
+    int* err_host = nullptr;  // pinned
     cudaEvent_t h2d = nullptr, computed = nullptr, d2h = nullptr;
     uint64_t ticket = 0;
   };
   Slot pipe[2];
   cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
   uint64_t next_ticket = 1, done_ticket = 0;
-  int* h_err = nullptr;
 
   tlg_policy(const tlg_policy_shape& s, int dev, long mb) : net(s), device(dev), max_batch(mb) {
     if (mb <= 0) throw InvalidArg("max_batch must be >= 1");
@@ -1491,8 +1492,9 @@ struct tlg_policy {
       act_lo.push_back(nullptr);
     }
   }
-  // Enqueue one forward of n device-resident observations on `stream` (err accumulates).
-  void enqueue(const float* x0, long n, float* lg, float* pr, float* vv);
+  // Enqueue one forward of n device-resident observations on `stream`; error flags are
+  // or-ed into errp (default: `err`).
+  void enqueue(const float* x0, long n, float* lg, float* pr, float* vv, int* errp = nullptr);
   void open_pipe() {
     if (h2d_stream) return;
     TLG_CUDA(cudaStreamCreateWithFlags(&h2d_stream, cudaStreamNonBlocking));
@@ -1502,21 +1504,22 @@ struct tlg_policy {
       sl.logits = mem.add<float>(max_batch * net.A);
       sl.probs = mem.add<float>(max_batch * net.A);
       sl.value = mem.add<float>(max_batch);
+      sl.err = mem.add<int>(4);
+      TLG_CUDA(cudaMallocHost(&sl.err_host, 16));
       TLG_CUDA(cudaEventCreateWithFlags(&sl.h2d, cudaEventDisableTiming));
       TLG_CUDA(cudaEventCreateWithFlags(&sl.computed, cudaEventDisableTiming));
       TLG_CUDA(cudaEventCreateWithFlags(&sl.d2h, cudaEventDisableTiming));
     }
-    TLG_CUDA(cudaMallocHost(&h_err, 16));
   }
   ~tlg_policy() {
     for (Slot& sl : pipe) {
       if (sl.h2d) cudaEventSynchronize(sl.d2h), cudaEventDestroy(sl.h2d);
       if (sl.computed) cudaEventDestroy(sl.computed);
       if (sl.d2h) cudaEventDestroy(sl.d2h);
+      if (sl.err_host) cudaFreeHost(sl.err_host);
     }
     if (h2d_stream) cudaStreamDestroy(h2d_stream);
     if (d2h_stream) cudaStreamDestroy(d2h_stream);
-    if (h_err) cudaFreeHost(h_err);
     if (stream) {
       cudaStreamSynchronize(stream);
       cudaStreamDestroy(stream);
@@ -1548,8 +1551,9 @@ void set_params_common(float* params, float* params_lo, long P, long P_pad, cons
 
 }  // namespace
 
-void tlg_policy::enqueue(const float* x0, long n, float* lg, float* pr, float* vv) {
+void tlg_policy::enqueue(const float* x0, long n, float* lg, float* pr, float* vv, int* errp) {
   const long D = net.D, A = net.A;
+  int* err = errp ? errp : this->err;
   // rows the GEMMs evaluate: the int8 pair kernels tile 256 rows (see kMinRows)
   const long m = i8 ? std::max(n, kMinRows) : n;
   if (net.padded()) {
@@ -2131,20 +2135,21 @@ int tlg_policy_forward_async(tlg_policy* p, const float* obs, size_t n, float* l
     // the slot's previous batch must have drained (its D2H read the slot's outputs)
     if (sl.ticket != 0) TLG_CUDA(cudaEventSynchronize(sl.d2h));
     const long D = p->net.D, A = p->net.A;
-    if (t == 1) TLG_CUDA(cudaMemsetAsync(p->err, 0, 4, p->stream));
     // H2D (page-locked host memory overlaps the forward of the previous batch)
     TLG_CUDA(cudaStreamWaitEvent(p->h2d_stream, sl.computed, 0));  // the slot's obs are free
     TLG_CUDA(cudaMemcpyAsync(sl.obs, obs, n * D * 4, cudaMemcpyHostToDevice, p->h2d_stream));
     TLG_CUDA(cudaEventRecord(sl.h2d, p->h2d_stream));
     // forward on the policy stream
     TLG_CUDA(cudaStreamWaitEvent(p->stream, sl.h2d, 0));
-    p->enqueue(sl.obs, long(n), sl.logits, sl.probs, sl.value);
+    TLG_CUDA(cudaMemsetAsync(sl.err, 0, 4, p->stream));
+    p->enqueue(sl.obs, long(n), sl.logits, sl.probs, sl.value, sl.err);
     TLG_CUDA(cudaEventRecord(sl.computed, p->stream));
     // D2H overlaps the next batch's forward
     TLG_CUDA(cudaStreamWaitEvent(p->d2h_stream, sl.computed, 0));
     TLG_CUDA(cudaMemcpyAsync(logits, sl.logits, n * A * 4, cudaMemcpyDeviceToHost, p->d2h_stream));
     TLG_CUDA(cudaMemcpyAsync(probs, sl.probs, n * A * 4, cudaMemcpyDeviceToHost, p->d2h_stream));
     TLG_CUDA(cudaMemcpyAsync(value, sl.value, n * 4, cudaMemcpyDeviceToHost, p->d2h_stream));
+    TLG_CUDA(cudaMemcpyAsync(sl.err_host, sl.err, 4, cudaMemcpyDeviceToHost, p->d2h_stream));
     TLG_CUDA(cudaEventRecord(sl.d2h, p->d2h_stream));
     sl.ticket = t;
     p->next_ticket = t + 1;
@@ -2161,11 +2166,12 @@ int tlg_policy_wait(tlg_policy* p, uint64_t ticket) {
     TLG_CUDA(cudaSetDevice(p->device));
     tlg_policy::Slot& sl = p->pipe[ticket & 1];
     if (sl.ticket != ticket) throw InvalidArg("ticket no longer tracked");
+    // the batch's outputs and error flags arrived together; the compute stream (already
+    // running the next batch) is not synchronised
     TLG_CUDA(cudaEventSynchronize(sl.d2h));
-    TLG_CUDA(cudaMemcpyAsync(p->h_err, p->err, 4, cudaMemcpyDeviceToHost, p->stream));
-    TLG_CUDA(cudaStreamSynchronize(p->stream));
     p->done_ticket = ticket;
-    if (p->h_err[0] & tlg::kErrNotOneHot) throw InvalidArg("tabular observation must be one-hot");
+    if (sl.err_host[0] & tlg::kErrNotOneHot)
+      throw InvalidArg("tabular observation must be one-hot");
   });
 }
 

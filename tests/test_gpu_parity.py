@@ -729,6 +729,30 @@ def test_pipelined_policy_batches_match_synchronous_forward(tlg, oracle):
         assert np.array_equal(lg, wl) and np.array_equal(pr, wp) and np.array_equal(v, wv)
 
 
+def test_pipelined_policy_reports_each_batchs_own_errors(tlg, oracle):
+    """A tabular batch with a non-one-hot row fails its own wait(); the batches around it
+    (in flight at the same time) are unaffected."""
+    D, A = 6, 3
+    p = init_params(oracle, Shape(0, D, A, ()), 3)
+    pol = tlg.Policy("tabular", D, A, (), max_batch=64)
+    pol.set_params(p)
+    good = np.zeros((50, D), np.float32)
+    good[np.arange(50), np.arange(50) % D] = 1
+    bad = good.copy()
+    bad[7, :] = 0.5
+    outs = [(np.zeros((50, A), np.float32), np.zeros((50, A), np.float32),
+             np.zeros(50, np.float32)) for _ in range(3)]
+    t0 = pol.forward_async(good, outs[0])
+    t1 = pol.forward_async(bad, outs[1])
+    pol.wait(t0)
+    t2 = pol.forward_async(good, outs[2])
+    with pytest.raises(tlg.InvalidArgument, match="one-hot"):
+        pol.wait(t1)
+    pol.wait(t2)
+    wl, wp, wv = pol.forward(good)
+    assert np.array_equal(outs[2][0], wl) and np.array_equal(outs[2][2], wv)
+
+
 @pytest.mark.parametrize("fmt", ["f32", "bits"])
 def test_device_replay_matches_host_batches(tlg, oracle, fmt):
     """Segments ingested once into the device replay ring and gathered by slot give
