@@ -29,3 +29,14 @@ def test_dropin_binary_links_the_cabi_library():
         pytest.skip("not built")
     out = subprocess.run(["ldd", BIN], capture_output=True, text=True).stdout
     assert "libtlg_b200.so" in out and "not found" not in out.split("libtlg_b200.so")[1].split("\n")[0]
+
+
+def test_dropin_replay_mem_draws_match_the_reference():
+    """CPU: the drop-in ReplayMem (O(log n) draws) against the reference's deque-based one,
+    draw for draw, over randomised push / sample / clear sequences and the C3 shape."""
+    binary = os.path.join(ROOT, "integration", "_build", "replay_mem_test")
+    if not os.path.exists(binary):
+        pytest.skip("integration/_build/replay_mem_test not built (needs the reference sources)")
+    r = subprocess.run([binary], capture_output=True, text=True, timeout=600)
+    print(r.stdout[-2000:])
+    assert r.returncode == 0 and "REPLAY MEM TEST PASSED" in r.stdout, r.stdout[-2000:]
