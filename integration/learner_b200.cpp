@@ -50,12 +50,12 @@ tlg_policy_shape DeviceShape(const ParamBlob& b, const std::vector<std::uint32_t
   return s;
 }
 
-// fn(lo, hi) over [0, n) split into contiguous ranges on up to 16 host threads (fewer
+// fn(lo, hi) over [0, n) split into contiguous ranges on up to 32 host threads (fewer
 // when the work is small); the first exception (in range order) is rethrown.
 template <typename F>
 void ParallelRanges(std::size_t n, std::size_t work, F&& fn) {
   const std::size_t nth = std::max<std::size_t>(
-      1, std::min<std::size_t>({16, std::size_t(std::max(1u, std::thread::hardware_concurrency())),
+      1, std::min<std::size_t>({32, std::size_t(std::max(1u, std::thread::hardware_concurrency())),
                                 work / (1u << 16) + 1, n}));
   if (nth <= 1) {
     fn(std::size_t(0), n);
@@ -410,10 +410,19 @@ struct Learner::Gpu {
           if (st.obs.size() != D)
             throw std::invalid_argument("observation size does not match policy shape");
           if (binary) {
+            // eight planes per byte, LSB first, without branches (vectorises)
             std::uint8_t* row = bits.p + f * rowb;
-            std::memset(row, 0, rowb);
-            for (std::size_t j = 0; j < D; ++j)
-              if (st.obs[j] != 0.0) row[j >> 3] |= std::uint8_t(1u << (j & 7));
+            const double* x = st.obs.data();
+            const std::size_t full = D / 8;
+            for (std::size_t b = 0; b < full; ++b, x += 8) {
+              unsigned v = 0;
+              for (int k = 0; k < 8; ++k) v |= unsigned(x[k] != 0.0) << k;
+              row[b] = std::uint8_t(v);
+            }
+            unsigned v = 0;
+            for (std::size_t j = full * 8; j < D; ++j) v |= unsigned(st.obs[j] != 0.0) << (j & 7);
+            if (full * 8 < D) row[full] = std::uint8_t(v);
+            std::memset(row + (D + 7) / 8, 0, rowb - (D + 7) / 8);
           } else {
             for (std::size_t j = 0; j < D; ++j) obs.p[f * D + j] = float(st.obs[j]);
           }
