@@ -327,6 +327,8 @@ struct tlg_learner {
     adam_m = mem.add<float>(P_pad);
     adam_v = mem.add<float>(P_pad);
     adam_t_dev = mem.add<uint64_t>(1);
+    opt_done = mem.add<unsigned>(4);
+    TLG_CUDA(cudaMemset(opt_done, 0, 16));
     const long D = net.D;
     obs = mem.add<float>(F_max * D);
     obs_lo = lo_hbm ? mem.add<float>(F_max * long(net.D_pad)) : nullptr;
@@ -893,9 +895,9 @@ struct tlg_learner {
       fuse_loss_epi = nullptr;
       if (shard == 0) mark(2);
       tlg::LossLaunch ll{fused_ctas, fused_ctas};
+      // (+ the failure guard: the shard's loss and error flags are final here)
       tlg::launch_head_grad_reduce(net.head, hg_partial, loss_partial, ll, gtarget, st, stream,
-                                   le.bias_partial);
-      set_guard(shard);  // the shard's loss and error flags are final here
+                                   le.bias_partial, err, grad + P_pad);
       bucket_ready(net.head.wpi, net.P - net.head.wpi, net.L == 0, /*with_guard=*/true);
       tlg::launch_rows_reduce(col_partial, fused_ctas, net.head.H, net.head.H,
                               gtarget + net.b_off[net.L - 1], stream);
@@ -918,8 +920,9 @@ struct tlg_learner {
         net.L && dz_lo_plane(int(net.L) - 1, x0_u8) ? dz_lo[net.L - 1] : nullptr, hg_partial,
         loss_partial, col_partial, stream, teacher_active() ? t_head_out : nullptr,
         parts ? head_part : nullptr, head_tiles, err);
-    tlg::launch_head_grad_reduce(net.head, hg_partial, loss_partial, ll, gtarget, st, stream);
-    set_guard(shard);  // the shard's loss and error flags are final here
+    // (+ the failure guard: the shard's loss and error flags are final here)
+    tlg::launch_head_grad_reduce(net.head, hg_partial, loss_partial, ll, gtarget, st, stream,
+                                 nullptr, err, grad + P_pad);
     bucket_ready(net.head.wpi, net.P - net.head.wpi, net.L == 0, /*with_guard=*/true);
     launches += 6;
     if (net.L > 0) {  // db of the top trunk layer from the loss kernel's column partials
@@ -1233,7 +1236,6 @@ struct tlg_learner {
   bool fused_head() const { return net.A + 1 <= 8; }
   int colsum_rows = 0;
   int head_tiles = 1;
-  void set_guard(int shard);
   void launch_guarded_optimizer(bool adam, float lr);
   struct Graph {
     cudaGraphExec_t exec = nullptr;
@@ -1250,18 +1252,13 @@ struct tlg_learner {
   uint64_t hyper_version = 0;
   bool graph_disabled = std::getenv("TLG_NO_GRAPH") != nullptr;
   uint64_t* adam_t_dev = nullptr;
+  unsigned* opt_done = nullptr;  // blocks of the optimizer launch done (the last advances t)
 };
 
 namespace {
 
 // guard[0] > 0 iff some shard raised an error bit or produced a non-finite loss; it is
 // summed by the allreduce together with the gradient, so every rank agrees to skip.
-__global__ void set_guard_kernel(const int* err, const tlg::StepStatsDev* st, float* guard) {
-  TLG_PDL_ENTRY();
-  const bool bad = (*err != 0) || !isfinite(st->loss);
-  if (bad) guard[0] = 1.f;
-}
-
 __global__ void accumulate_kernel(float4* __restrict__ g, const float4* __restrict__ t, long n4) {
   TLG_PDL_ENTRY();
   for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n4;
@@ -1273,14 +1270,32 @@ __global__ void accumulate_kernel(float4* __restrict__ g, const float4* __restri
   }
 }
 
+// The block that finishes last advances the Adam step counter (when the step applied),
+// after every block has read it: one launch instead of an optimizer + a counter kernel.
+__device__ __forceinline__ void optimizer_block_done(bool applied, uint64_t* adam_t,
+                                                     unsigned* done) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(done, 1u) == gridDim.x - 1) {
+      if (applied) *adam_t += 1;
+      *done = 0;  // ready for the next step (graph replays included)
+      __threadfence();
+    }
+  }
+}
+
 __global__ void optimizer_guarded_kernel(float4* __restrict__ p, float4* __restrict__ plo,
                                          const float4* __restrict__ g, float4* __restrict__ m,
                                          float4* __restrict__ v, long n4, const float* guard,
                                          float grad_scale, int adam, float lr,
-                                         const uint64_t* adam_t, double b1d, double b2d,
-                                         float eps) {
+                                         uint64_t* adam_t, double b1d, double b2d,
+                                         float eps, unsigned* done) {
   TLG_PDL_ENTRY();
-  if (*guard != 0.f) return;  // some shard failed: parameters stay untouched
+  if (*guard != 0.f) {  // some shard failed: parameters stay untouched
+    optimizer_block_done(false, adam_t, done);
+    return;
+  }
   // torch.optim.Adam bias corrections for step t = (completed steps) + 1
   const double t = double(*adam_t + 1);
   const float step_size = float(double(lr) / (1.0 - pow(b1d, t)));
@@ -1314,11 +1329,7 @@ __global__ void optimizer_guarded_kernel(float4* __restrict__ p, float4* __restr
     plo[i] = make_float4(pp.x - tlg::tf32_hi(pp.x), pp.y - tlg::tf32_hi(pp.y),
                          pp.z - tlg::tf32_hi(pp.z), pp.w - tlg::tf32_hi(pp.w));
   }
-}
-
-__global__ void advance_step_kernel(const float* guard, uint64_t* adam_t) {
-  TLG_PDL_ENTRY();
-  if (*guard == 0.f) *adam_t += 1;
+  optimizer_block_done(true, adam_t, done);
 }
 
 __global__ void split_lo_flat(const float* x, float* lo, long n) {
@@ -1328,12 +1339,6 @@ __global__ void split_lo_flat(const float* x, float* lo, long n) {
 }
 
 }  // namespace
-
-void tlg_learner::set_guard(int shard) {
-  ::tlg::launch_k(set_guard_kernel, dim3(1), dim3(1), size_t(0), stream, err, stats + shard, grad + P_pad);
-  TLG_CHECK_LAUNCH();
-  ++launches;
-}
 
 void tlg_learner::issue_bucket(long off, long count, bool with_guard) {
   if (n_buckets >= kMaxBuckets) throw RuntimeErr("too many gradient buckets");
@@ -1375,11 +1380,9 @@ void tlg_learner::launch_guarded_optimizer(bool adam, float lr) {
       reinterpret_cast<float4*>(params), reinterpret_cast<float4*>(params_lo),
       reinterpret_cast<const float4*>(grad), reinterpret_cast<float4*>(adam_m),
       reinterpret_cast<float4*>(adam_v), n4, grad + P_pad, grad_scale, adam ? 1 : 0, lr,
-      adam_t_dev, cfg.adam_beta1, cfg.adam_beta2, float(cfg.adam_eps));
+      adam_t_dev, cfg.adam_beta1, cfg.adam_beta2, float(cfg.adam_eps), opt_done);
   TLG_CHECK_LAUNCH();
-  ::tlg::launch_k(advance_step_kernel, dim3(1), dim3(1), size_t(0), stream, grad + P_pad, adam_t_dev);
-  TLG_CHECK_LAUNCH();
-  launches += 2;
+  launches += 1;
 }
 
 // ===========================================================================

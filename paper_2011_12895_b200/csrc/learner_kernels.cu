@@ -1062,9 +1062,12 @@ __global__ void __launch_bounds__(1024) head_grad_reduce_kernel(HeadDesc hd,
 // Bias partials [nblk][A1] and the loss/stat partials -> gradient + step statistics.
 // Warp w < A1 reduces bias column w; warps A1.. reduce the 5 loss sums; each warp sums a
 // strided subset then a fixed shuffle tree (deterministic).
+// guard (optional): set to 1 when the step failed -- error flags or a non-finite loss --
+// so that the optimizer of every rank skips the step (the flag rides the allreduce).
 __global__ void head_bias_stats_kernel(HeadDesc hd, const float* __restrict__ bias_partial,
                                        const double* __restrict__ loss_partial, int nblocks,
-                                       float* __restrict__ grad, StepStatsDev* st) {
+                                       float* __restrict__ grad, StepStatsDev* st,
+                                       const int* __restrict__ err, float* __restrict__ guard) {
   TLG_PDL_ENTRY();
   const int A = hd.A, A1 = A + 1;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1083,6 +1086,7 @@ __global__ void head_bias_stats_kernel(HeadDesc hd, const float* __restrict__ bi
     acc = warp_sum(acc);
     if (lane == 0) {
       const double v = acc * st->inv_n;
+      if (q == 0 && guard != nullptr && (*err != 0 || !isfinite(v))) guard[0] = 1.f;
       if (q == 0) st->loss = v;
       else if (q == 1) st->ratio = v;
       else if (q == 2) st->entropy = v;
@@ -1397,14 +1401,15 @@ LossLaunch launch_loss_backward(const HeadDesc& hd, const float* params, const f
 
 void launch_head_grad_reduce(const HeadDesc& hd, const float* hg_partial,
                              const double* loss_partial, const LossLaunch& ll, float* grad,
-                             StepStatsDev* st, cudaStream_t s, const float* bias_partial) {
+                             StepStatsDev* st, cudaStream_t s, const float* bias_partial,
+                             const int* err, float* guard) {
   const long nw = long(hd.A + 1) * hd.H;
   ::tlg::launch_k(head_grad_reduce_kernel, dim3(ceil_div(nw, 32)), dim3(rows_reduce_threads(nw)), size_t(0), s, 
       hd, hg_partial, ll.stream_blocks, grad);
   TLG_CHECK_LAUNCH();
   ::tlg::launch_k(head_bias_stats_kernel, dim3(1), dim3(32 * (hd.A + 1 + 5)), size_t(0), s, 
       hd, bias_partial ? bias_partial : hg_partial + long(ll.stream_blocks) * nw, loss_partial,
-      ll.math_blocks, grad, st);
+      ll.math_blocks, grad, st, err, guard);
   TLG_CHECK_LAUNCH();
 }
 

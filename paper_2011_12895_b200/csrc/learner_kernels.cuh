@@ -119,7 +119,8 @@ LossLaunch launch_loss_backward(const HeadDesc& hd, const float* params, const f
 void launch_head_grad_reduce(const HeadDesc& hd, const float* hg_partial,
                              const double* loss_partial, const LossLaunch& ll, float* grad,
                              StepStatsDev* st, cudaStream_t s,
-                             const float* bias_partial = nullptr);
+                             const float* bias_partial = nullptr, const int* err = nullptr,
+                             float* guard = nullptr);
 // out[c] = sum_r partial[r*stride + c] for c < cols, fixed order (deterministic).
 void launch_rows_reduce(const float* partial, int rows, long cols, long stride, float* out,
                         cudaStream_t s);
