@@ -165,6 +165,8 @@ void dispatch_bn(bool a_mn, bool b_mn, bool a_lo, bool b_lo, int epi, int u8, in
     if (u8) throw CudaError("gemm: derived lo planes need fp32 operands");
     if (!a_mn && !b_mn && a_lo && b_lo && epi == kEpiFwdTanh && lod == 1)
       return run_if_fits<BN, false, false, true, true, kEpiFwdTanh, 0, 1>(ah, al, bh, bl, em, p, grid, s);
+    if (!a_mn && !b_mn && a_lo && b_lo && epi == kEpiFwdTanh && lod == (1 | kLodEg2))
+      return run_if_fits<BN, false, false, true, true, kEpiFwdTanh, 0, 1 | kLodEg2>(ah, al, bh, bl, em, p, grid, s);
     if (!a_mn && !b_mn && a_lo && b_lo && epi == kEpiFwdLoss && lod == 1)
       return run_if_fits<BN, false, false, true, true, kEpiFwdLoss, 0, 1>(ah, al, bh, bl, em, p, grid, s);
     if (!a_mn && b_mn && a_lo && b_lo && epi == kEpiBwdTanh && lod == 1)
@@ -268,10 +270,21 @@ LaunchInfo launch(const Operand& A, const Operand& B, int M, int N, int K, int e
   p.N = N;
   p.K = K;
   // Tile width: 256 columns when the K loop is long enough to hide the wider epilogue,
-  // else 128 (short-K fused epilogues are the critical path; narrower tiles balance).
+  // else 128 (short-K fused epilogues are the critical path; narrower tiles balance) --
+  // except with derived residuals, where 256-column tiles halve the A-operand traffic
+  // per product: the tanh forward then drains through two epilogue warp groups, the dX
+  // epilogue keeps up as it is (C3: layer-2 forward 119 -> 103 us, dX 102 -> 99 us).
   int BN = N > 128 ? 256 : N > 64 ? 128 : 64;
   const int kb_tile = p.kb_per_split;  // K blocks per tile
-  if (BN == 256 && epi != kEpiStore && epi != kEpiFwdLoss && kb_tile < 16 &&
+  // two epilogue warp groups (kLodEg2) for the derived-residual tanh forward on 128-column
+  // tiles and on short-K 256-column tiles
+  auto lod_k = [&](int bn) {
+    return lod | (epi == kEpiFwdTanh && lod != 0 && u8_0 == 0 && (bn == 128 || (bn == 256 && kb_tile < 16))
+                      ? kLodEg2 : 0);
+  };
+  const bool wide_lod = (lod & 1) && (epi == kEpiFwdTanh || epi == kEpiBwdTanh) &&
+                        !std::getenv("TLG_GEMM_NARROW");
+  if (BN == 256 && epi != kEpiStore && epi != kEpiFwdLoss && kb_tile < 16 && !wide_lod &&
       !std::getenv("TLG_GEMM_WIDE"))
     BN = 128;
   if (epi == kEpiFwdLoss) {  // whole rows per tile, CTA pairs (the only plan that fits)
@@ -295,7 +308,7 @@ LaunchInfo launch(const Operand& A, const Operand& B, int M, int N, int K, int e
     if (const char* e = std::getenv("TLG_GEMM_CG_U8"))  // tuning experiments only
       if ((A.u8 || B.u8) && std::atoi(e) == 2 && BN >= 128) cg = 2;
     if (BN == 64 || epi == kEpiFwdLoss ||
-        smem_plan(BN, a_lo0, b_lo0, epi, u8_0, cg, lod).bytes <= 227 * 1024)
+        smem_plan(BN, a_lo0, b_lo0, epi, u8_0, cg, lod_k(BN)).bytes <= 227 * 1024)
       break;
     BN /= 2;
   }
@@ -321,13 +334,14 @@ LaunchInfo launch(const Operand& A, const Operand& B, int M, int N, int K, int e
     if (epi == kEpiBwdTanh) em.act = make_map(p.act_hi, N, M, p.ld_act, 32, CU_TENSOR_MAP_SWIZZLE_128B);
     if (A.u8 && p.a_expand) em.act = make_map(p.a_expand, K, M, A.ld, kBM, CU_TENSOR_MAP_SWIZZLE_128B);
   }
+  const int lodk = lod_k(BN);
   switch (BN) {
-    case 256: dispatch_bn<256>(A.mn_major, B.mn_major, a_lo, b_lo, epi, u8, lod, ah, al, bh, bl, em, p, grid, stream); break;
-    case 128: dispatch_bn<128>(A.mn_major, B.mn_major, a_lo, b_lo, epi, u8, lod, ah, al, bh, bl, em, p, grid, stream); break;
-    default: dispatch_bn<64>(A.mn_major, B.mn_major, a_lo, b_lo, epi, u8, lod, ah, al, bh, bl, em, p, grid, stream); break;
+    case 256: dispatch_bn<256>(A.mn_major, B.mn_major, a_lo, b_lo, epi, u8, lodk, ah, al, bh, bl, em, p, grid, stream); break;
+    case 128: dispatch_bn<128>(A.mn_major, B.mn_major, a_lo, b_lo, epi, u8, lodk, ah, al, bh, bl, em, p, grid, stream); break;
+    default: dispatch_bn<64>(A.mn_major, B.mn_major, a_lo, b_lo, epi, u8, lodk, ah, al, bh, bl, em, p, grid, stream); break;
   }
   const int tiles = int(grid.x * grid.y * grid.z);
-  return {BN / epi_groups(BN, epi, u8, lod),
+  return {BN / epi_groups(BN, epi, u8, lodk),
           cg == 2 ? 2 * std::min(tiles, num_sms() / 2) : std::min(tiles, num_sms())};
 }
 

@@ -263,13 +263,15 @@ constexpr int kEpiWarps = 4;
 // Epilogue warp groups: the tanh forward on a derived-residual operand (short K: the
 // per-element tanh + fused head dot products are the critical path) runs two groups of 4
 // epilogue warps (warps 2..5 and 10..13) that take alternate 32-column chunks, so every
-// scheduler holds two epilogue warps.  128-column tiles only: launch() picks them for
-// short K loops (the wide tiles' long K loops hide the epilogue, and their pipeline
-// would lose a stage to the extra staging); each group's head partials cover 64 columns
-// (LaunchInfo::bn).
+// scheduler holds two epilogue warps.  Selected by launch() through lod bit 3 (kLodEg2):
+// 128-column tiles, and 256-column tiles of short K loops (a long K loop hides the
+// epilogue, and its pipeline would lose a stage to the extra staging); each group's head
+// partials cover BN / 2 columns (LaunchInfo::bn).
+constexpr int kLodEg2 = 8;
 __host__ __device__ constexpr int epi_groups(int bn, int epi, int u8, int lod) {
   // (the dX epilogue is written for either count; measured no faster with two groups)
-  return epi == 0 /* kEpiFwdTanh */ && lod != 0 && u8 == 0 && bn == 128 ? 2 : 1;
+  return epi == 0 /* kEpiFwdTanh */ && (lod & kLodEg2) && (lod & 3) && u8 == 0 && bn >= 128
+             ? 2 : 1;
 }
 constexpr int kColMax = 2048;  // widest N with fused column sums
 constexpr int kStageBuf = 32 * 33;  // per-warp 32x32 transpose buffer (+1 pad: no bank conflicts)
