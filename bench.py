@@ -101,6 +101,30 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
+def oracle_policy_cpu(c4, n=2048, reps=2):
+    """The InfServer's model on the CPU: the fp64 oracle's policy forward (the reference's
+    policy::Distribution / ValueEstimate arithmetic extended to the MLP family, on the
+    oracle's thread pool) over `n` observations of the C4 shape.  A port: the reference's
+    InfServer serves linear / tabular blobs only (types.hpp:14)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_ffi import Oracle, Shape
+    orc = Oracle()
+    shape = Shape(2, c4.obs_dim, c4.n_actions, c4.hidden)
+    p = orc.init_params(shape, 0.05, 3)
+    obs = np.random.default_rng(5).standard_normal((n, c4.obs_dim))
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        orc.forward(shape, p, obs)
+        ts.append(time.perf_counter() - t0)
+    return {"value": n / min(ts), "unit": "actions/s", "cores": min(64, os.cpu_count() or 1),
+            "kind": "port",
+            "sample": f"fp64 oracle policy forward (MLP {c4.obs_dim}-"
+                      f"{'-'.join(map(str, c4.hidden))}-({c4.n_actions},1)) on {n} observations, "
+                      f"best of {reps}"}
+
+
+# ---------------------------------------------------------------------------
 def oracle_mlp_cpu(cfg, segments=64, reps=2):
     """The same model on the CPU: the fp64 oracle's learner step (oracle/tlg_oracle.cpp --
     the reference's rlmath/policy arithmetic extended to the MLP family, std::thread over
@@ -677,6 +701,11 @@ def main():
         except Exception as e:
             others.append({"value": None, "kind": "port", "sample": f"unavailable: {e}"})
         cpu["others"] = others
+        if infer is not None:
+            try:
+                infer["cpu_baseline"] = oracle_policy_cpu(CONFIGS["C4"])
+            except Exception as e:
+                infer["cpu_baseline"] = {"value": None, "kind": "port", "sample": f"unavailable: {e}"}
 
     # ---- the drop-in C++ learner::Learner (reference-facing API) at C3, N=1
     dropin = None
