@@ -415,17 +415,19 @@ LaunchInfo launch_i8_bits_fwd(const uint8_t* bits, long rowb, const int8_t* q, l
   const CUtensorMap to = make_f32_out_map(out, N, M, ldo);
   const CUtensorMap tl = out_lo ? make_f32_out_map(out_lo, N, M, ldo) : CUtensorMap{};
   // Default for CTA pairs without a residual plane and N > 128: 256-column tiles on
-  // decoupled operand rings with two epilogue warp groups (gemm_i8_bits_fwd_dec_kernel
-  // <256, 2, NQ 2, NX 2, MS 1, EG 2>): x is expanded once per M tile, the N = 256 MMAs
-  // read fewer operand bytes per product, and the eight epilogue warps halve the drain
-  // the single-buffered accumulators expose (C3: 0.167 vs 0.188 ms).  TLG_I8_DEC selects
+  // decoupled operand rings with three epilogue warp groups (gemm_i8_bits_fwd_dec_kernel
+  // <256, 2, NQ 2, NX 2, MS 1, EG 3>): x is expanded once per M tile, the N = 256 MMAs
+  // read fewer operand bytes per product, and twelve epilogue warps shorten the drain
+  // the single-buffered accumulators expose (C3: 0.157 vs 0.188 ms).  TLG_I8_DEC selects
   // the variants measured against it: 0 = coupled stages,
-  // 4x3 = decoupled rings at 128 columns, m2e = two M subtiles per CTA, b256 = one group.
+  // 4x3 = decoupled rings at 128 columns, m2e = two M subtiles per CTA, b256 / b256e =
+  // one / two epilogue groups.
   int dec = cg == 2 && mc == 1 && out_lo == nullptr && N > 128 && !std::getenv("TLG_I8_BN")
-                ? 257 : 0;
+                ? 259 : 0;
   if (const char* e = std::getenv("TLG_I8_DEC"); e && dec != 0)
     dec = std::strcmp(e, "4x3") == 0 ? 43 : std::strcmp(e, "m2e") == 0 ? 3
-        : std::strcmp(e, "b256") == 0 ? 256 : std::strcmp(e, "0") == 0 ? 0 : 257;
+        : std::strcmp(e, "b256") == 0 ? 256 : std::strcmp(e, "b256e") == 0 ? 257
+        : std::strcmp(e, "0") == 0 ? 0 : 259;
   if (dec == 3) {
     // two 128-row M subtiles per CTA share each weight-piece tile (half the L2 -> SM
     // piece traffic per output), accumulators single-buffered
@@ -434,10 +436,11 @@ LaunchInfo launch_i8_bits_fwd(const uint8_t* bits, long rowb, const int8_t* q, l
     run_i8_fwd_dec<128, 2, 2, 2, 2, 2>(tb2, tq, to, tl, p, tm2, stream);
     return {BN, 2 * std::min(tm2.m_tiles * tm2.n_tiles, num_sms() / 2)};
   }
-  if (dec == 256 || dec == 257) {
+  if (dec == 256 || dec == 257 || dec == 259) {
     const TileMap tmw{ceil_div(M, kBM * 2), ceil_div(N, 256), 1};
     const CUtensorMap tqw = make_bytes_map(q, Kp, 3L * N, Kp, kBKi, 128, CU_TENSOR_MAP_SWIZZLE_128B);
-    if (dec == 257) run_i8_fwd_dec<256, 2, 2, 2, 1, 2>(tb, tqw, to, tl, p, tmw, stream);
+    if (dec == 259) run_i8_fwd_dec<256, 2, 2, 2, 1, 3>(tb, tqw, to, tl, p, tmw, stream);
+    else if (dec == 257) run_i8_fwd_dec<256, 2, 2, 2, 1, 2>(tb, tqw, to, tl, p, tmw, stream);
     else run_i8_fwd_dec<256, 2, 2, 2>(tb, tqw, to, tl, p, tmw, stream);
     return {256, 2 * std::min(tmw.m_tiles * tmw.n_tiles, num_sms() / 2)};
   }

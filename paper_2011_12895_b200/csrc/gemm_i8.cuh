@@ -163,8 +163,9 @@ __device__ __forceinline__ void i8_fwd_epilogue(const I8Params& p, const TileMap
                                                 uint8_t* blk_ptr, bool lo_block) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = warp & 3;
-  // EG == 2: a second group of 4 epilogue warps (warps 10..13) takes the odd chunks
-  const int grp = EG == 2 && warp >= 2 + 2 * kEpiWarps ? 1 : 0;
+  // EG > 1: further groups of 4 epilogue warps (warps 10..13, 14..17) take every EG-th
+  // chunk
+  const int grp = warp < 2 + kEpiWarps ? 0 : (warp - 2 - kEpiWarps - kConvWarps) / kEpiWarps + 1;
   const int num_tiles = tm.m_tiles * tm.n_tiles;
   const bool write_lo = lo_block && p.write_lo;
   int it = 0;
@@ -692,7 +693,7 @@ __global__ void __launch_bounds__(kThreadsI8 + 32 * kEpiWarps * (EG - 1), 1)
       }
     }
   } else {
-    // ===== epilogue (warps 2..5, + 10..13 when EG == 2) =====
+    // ===== epilogue (warps 2..5, + 10..13 when EG >= 2, + 14..17 when EG == 3) =====
     const int ew = warp < 2 + kEpiWarps ? warp - 2 : warp - 2 - kConvWarps;
     i8_fwd_epilogue<BN, CG, S::kBufs, MS, EG>(p, tm, &tmOut, &tmOutLo, tmem_base, bar_tfull,
                                           bar_tempty, 0u, rank * kBM * MS, kRowsT, cl_id, n_cl,
