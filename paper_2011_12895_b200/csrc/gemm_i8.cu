@@ -375,7 +375,7 @@ LaunchInfo launch_i8x2_fwd(const int8_t* a, const int8_t* q, long Kp, const floa
   if (BN == 128) run_i8x2_fwd<128, 2>(ta, tq, to, tl, p, tm, stream);
   else run_i8x2_fwd<64, 2>(ta, tq, to, tl, p, tm, stream);
   const int tiles = tm.m_tiles * tm.n_tiles;
-  return {BN, 2 * std::min(tiles, num_sms() / 2)};
+  return {BN, 2 * std::min(tiles, num_sms() / 2), tm.n_tiles};
 }
 
 void launch_quantize_rows(const float* W, int N, int K, long ldw, int8_t* q, long Kp, float* s,
@@ -434,7 +434,7 @@ LaunchInfo launch_i8_bits_fwd(const uint8_t* bits, long rowb, const int8_t* q, l
     const TileMap tm2{ceil_div(M, kBM * 2 * 2), ceil_div(N, BN), 1};
     const CUtensorMap tb2 = make_bytes_map(bits, rowb, M, rowb, kBKi / 8, 2 * kBM, CU_TENSOR_MAP_SWIZZLE_NONE);
     run_i8_fwd_dec<128, 2, 2, 2, 2, 2>(tb2, tq, to, tl, p, tm2, stream);
-    return {BN, 2 * std::min(tm2.m_tiles * tm2.n_tiles, num_sms() / 2)};
+    return {BN, 2 * std::min(tm2.m_tiles * tm2.n_tiles, num_sms() / 2), tm2.n_tiles};
   }
   if (dec == 256 || dec == 257 || dec == 259) {
     const TileMap tmw{ceil_div(M, kBM * 2), ceil_div(N, 256), 1};
@@ -442,7 +442,7 @@ LaunchInfo launch_i8_bits_fwd(const uint8_t* bits, long rowb, const int8_t* q, l
     if (dec == 259) run_i8_fwd_dec<256, 2, 2, 2, 1, 3>(tb, tqw, to, tl, p, tmw, stream);
     else if (dec == 257) run_i8_fwd_dec<256, 2, 2, 2, 1, 2>(tb, tqw, to, tl, p, tmw, stream);
     else run_i8_fwd_dec<256, 2, 2, 2>(tb, tqw, to, tl, p, tmw, stream);
-    return {256, 2 * std::min(tmw.m_tiles * tmw.n_tiles, num_sms() / 2)};
+    return {256, 2 * std::min(tmw.m_tiles * tmw.n_tiles, num_sms() / 2), tmw.n_tiles};
   }
   if (dec == 43) run_i8_fwd_dec<128, 2, 4, 3>(tb, tq, to, tl, p, tm, stream);
   else if (BN == 256) run_i8_fwd<256, 2>(tb, tq, to, tl, p, tm, stream);
@@ -451,7 +451,7 @@ LaunchInfo launch_i8_bits_fwd(const uint8_t* bits, long rowb, const int8_t* q, l
   else run_i8_fwd<128, 1>(tb, tq, to, tl, p, tm, stream);
   const int tiles = tm.m_tiles * tm.n_tiles;
   const int cl = cg * mc;
-  return {BN, cl * std::min(tiles, num_sms() / cl)};  // upper bound on the CTAs launched
+  return {BN, cl * std::min(tiles, num_sms() / cl), tm.n_tiles};  // ctas: an upper bound
 }
 
 }  // namespace tlg::gemm

@@ -341,8 +341,9 @@ LaunchInfo launch(const Operand& A, const Operand& B, int M, int N, int K, int e
     default: dispatch_bn<64>(A.mn_major, B.mn_major, a_lo, b_lo, epi, u8, lodk, ah, al, bh, bl, em, p, grid, stream); break;
   }
   const int tiles = int(grid.x * grid.y * grid.z);
-  return {BN / epi_groups(BN, epi, u8, lodk),
-          cg == 2 ? 2 * std::min(tiles, num_sms() / 2) : std::min(tiles, num_sms())};
+  const int eg = epi_groups(BN, epi, u8, lodk);
+  return {BN / eg, cg == 2 ? 2 * std::min(tiles, num_sms() / 2) : std::min(tiles, num_sms()),
+          ceil_div(N, BN) * eg};
 }
 
 }  // namespace tlg::gemm

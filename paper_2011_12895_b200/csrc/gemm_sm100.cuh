@@ -1356,9 +1356,10 @@ struct Operand {
 };
 
 struct LaunchInfo {
-  int bn;    // N width of one fused-head partial slice (the tile width / epilogue groups):
-             // the fused head writes ceil(N / bn) partial rows
-  int ctas;  // persistent CTAs (the fused column sums write this many rows)
+  int bn;           // N tile width / epilogue groups
+  int ctas;         // persistent CTAs (the fused column sums write this many rows)
+  int head_slices;  // fused heads: partial slices written per row (N tiles x epilogue
+                    // groups) -- the n_tiles of launch_head_finalize
 };
 
 // Launch C = A . B^T with the given epilogue on `stream`.  splits > 1 only for

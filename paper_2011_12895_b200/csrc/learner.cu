@@ -72,6 +72,11 @@ void pin_nccl() {
       throw tlg::CudaError(std::string(#expr) + ": " + tlg::nccl::api().GetErrorString(_r)); \
   } while (0)
 
+// Fused-head partial slices per row a trunk GEMM can write (LaunchInfo::head_slices):
+// ceil(H / BN) tiles x epilogue groups, at most ceil(H / 64) + 2 for the tile plans of
+// gemm_sm100.cu (64-column tiles; 128 / 256 with up to 2 groups) and the int8 kernels.
+long head_slices_max(long H) { return (H + 63) / 64 + 2; }
+
 // Parameter layout of the three families (policy.cpp:23-27,78-104).
 struct Net {
   uint32_t family, D, A, L;
@@ -375,7 +380,7 @@ struct tlg_learner {
     }
     const int A1 = int(net.A) + 1;
     head_out = mem.add<float>(F_max * A1);
-    head_part = mem.add<float>(F_max * A1 * ((net.head.H + 63) / 64));
+    head_part = mem.add<float>(F_max * A1 * head_slices_max(net.head.H));
     tlogp = mem.add<float>(F_max);
     adv = mem.add<float>(F_max);
     target = mem.add<float>(F_max);
@@ -689,32 +694,33 @@ struct tlg_learner {
         ++launches;
       }
       if (timed) kmark(0, int(l), 0);
-      int bn;
+      int slices;  // fused heads: the launch's partial slices per row
       if (l == 0 && sg.x0_bits != nullptr) {
         // binary planes x int8 weight pieces: exact integer tensor-core GEMM (+ the
         // activations as int8 pieces when layer 2 takes the int8 path too)
-        bn = tlg::gemm::launch_i8_bits_fwd(sg.x0_bits, bits_pitch, wq, wq_kp, wq_scale, p.bias,
+        slices = tlg::gemm::launch_i8_bits_fwd(sg.x0_bits, bits_pitch, wq, wq_kp, wq_scale, p.bias,
                                            int(F), outw, int(net.D), act[0],
                                            net.L > 1 ? act_lo[0] : nullptr, outw,
                                            stream,
-                                           i8_fwd2(F) ? act_q : nullptr).bn;
+                                           i8_fwd2(F) ? act_q : nullptr).head_slices;
       } else if (l == 1 && sg.x0_bits != nullptr && i8_fwd2(F)) {
         tlg::gemm::launch_quantize_rows(P + net.w_off[1], outw, in, in, w2q, in, w2_scale,
                                         stream);
         ++launches;
-        bn = tlg::gemm::launch_i8x2_fwd(act_q, w2q, in, w2_scale, p.bias, int(F), outw, in,
+        slices = tlg::gemm::launch_i8x2_fwd(act_q, w2q, in, w2_scale, p.bias, int(F), outw, in,
                                         act[1], p.out_lo, outw, p.head_w, p.head_wv, p.head_k,
-                                        p.head_part, stream).bn;
+                                        p.head_part, stream).head_slices;
       } else if (fuse_loss) {
         const tlg::gemm::LaunchInfo li =
             tlg::gemm::launch(A, B, int(F), outw, in, tlg::gemm::kEpiFwdLoss, p, 1, stream);
-        bn = li.bn;
+        slices = li.head_slices;
         fused_ctas = li.ctas;
       } else {
-        bn = tlg::gemm::launch(A, B, int(F), outw, in, tlg::gemm::kEpiFwdTanh, p, 1, stream).bn;
+        slices = tlg::gemm::launch(A, B, int(F), outw, in, tlg::gemm::kEpiFwdTanh, p, 1, stream)
+                     .head_slices;
       }
       if (timed) kmark(0, int(l), 1);
-      if (fuse_head) head_tiles = (outw + bn - 1) / bn;
+      if (fuse_head) head_tiles = slices;
       ++launches;
     }
     const float* hL = net.L ? act[net.L - 1] : x0;
@@ -1482,7 +1488,7 @@ struct tlg_policy {
       w1p_lo = mem.add<float>(long(net.dims[1]) * net.D_pad);
     }
     head_out = mem.add<float>(mb * (net.A + 1));
-    head_part = mem.add<float>(rows_cap * (net.A + 1) * ((net.head.H + 63) / 64));
+    head_part = mem.add<float>(rows_cap * (net.A + 1) * head_slices_max(net.head.H));
     logits = mem.add<float>(mb * net.A);
     probs = mem.add<float>(mb * net.A);
     value = mem.add<float>(mb);
@@ -1593,18 +1599,19 @@ void tlg_policy::enqueue(const float* x0, long n, float* lg, float* pr, float* v
       gp.head_part = head_part;
     }
     int8_t* q_out = i8 && l + 1 < net.L ? act_q[l & 1] : nullptr;
-    int bn;
+    int slices;  // fused heads: the launch's partial slices per row
     if (i8 && l >= 1) {
-      bn = tlg::gemm::launch_i8x2_fwd(act_q[(l - 1) & 1], wq[l], in, wscale[l], gp.bias, int(m),
-                                      outw, in, gp.out_hi, nullptr, outw, gp.head_w, gp.head_wv,
-                                      gp.head_k, gp.head_part, stream, q_out)
-               .bn;
+      slices = tlg::gemm::launch_i8x2_fwd(act_q[(l - 1) & 1], wq[l], in, wscale[l], gp.bias,
+                                          int(m), outw, in, gp.out_hi, nullptr, outw, gp.head_w,
+                                          gp.head_wv, gp.head_k, gp.head_part, stream, q_out)
+                   .head_slices;
     } else {
       gp.out_q = q_out;
       if (q_out) gp.out_hi = nullptr;  // the next layer reads the pieces
-      bn = tlg::gemm::launch(Aop, Bop, int(m), outw, in, tlg::gemm::kEpiFwdTanh, gp, 1, stream).bn;
+      slices = tlg::gemm::launch(Aop, Bop, int(m), outw, in, tlg::gemm::kEpiFwdTanh, gp, 1, stream)
+                   .head_slices;
     }
-    if (fuse) head_tiles = (outw + bn - 1) / bn;
+    if (fuse) head_tiles = slices;
   }
   const float* hL = net.L ? act[net.L - 1] : x0;
   if (net.L > 0 && net.A + 1 <= 8) {

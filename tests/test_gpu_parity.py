@@ -130,6 +130,7 @@ CASES = [
     ("mlp", 36, 5, (64,), 5, 20),
     ("mlp", 50, 6, (64, 32), 7, 9),    # grid_duel's obs 50: rows padded to 52 internally
     ("mlp", 13, 3, (16, 8, 12), 4, 6),  # odd obs, 3 trunk layers
+    ("mlp", 32, 6, (64, 300), 8, 16),  # top width not a multiple of the tile: head slices
     ("linear", 10, 4, (), 6, 10),
     ("tabular", 5, 3, (), 4, 16),
 ]
@@ -285,6 +286,7 @@ def test_action_out_of_range_and_tabular_one_hot(tlg, oracle):
 
 # ---------------------------------------------------------------------------
 @pytest.mark.parametrize("case", [("mlp", 64, 6, (1024, 1024)), ("mlp", 36, 5, (64, 32)),
+                                  ("mlp", 64, 6, (300,)), ("mlp", 64, 6, (96, 200)),
                                   ("mlp", 50, 6, (64, 64)), ("mlp", 7, 3, (8,)),
                                   ("linear", 9, 4, ()), ("tabular", 6, 3, ())],
                          ids=lambda c: c[0] + "-" + str(c[1]))
