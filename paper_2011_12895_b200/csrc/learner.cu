@@ -927,11 +927,15 @@ struct tlg_learner {
         loss_partial, col_partial, stream, teacher_active() ? t_head_out : nullptr,
         parts ? head_part : nullptr, head_tiles, err);
     // (+ the failure guard: the shard's loss and error flags are final here)
+    // (+ db of the top trunk layer from the loss kernel's column partials, same launch)
+    const bool fuse_db = net.L > 0 && tlg::rows_reduce_threads(long(net.A + 1) * net.head.H) ==
+                                          tlg::rows_reduce_threads(net.head.H);
     tlg::launch_head_grad_reduce(net.head, hg_partial, loss_partial, ll, gtarget, st, stream,
-                                 nullptr, err, grad + P_pad);
+                                 nullptr, err, grad + P_pad, fuse_db ? col_partial : nullptr,
+                                 fuse_db ? gtarget + net.b_off[net.L - 1] : nullptr);
     bucket_ready(net.head.wpi, net.P - net.head.wpi, net.L == 0, /*with_guard=*/true);
     launches += 6;
-    if (net.L > 0) {  // db of the top trunk layer from the loss kernel's column partials
+    if (net.L > 0 && !fuse_db) {  // db of the top trunk layer from the loss kernel's partials
       tlg::launch_rows_reduce(col_partial, ll.stream_blocks, net.head.H, net.head.H,
                               gtarget + net.b_off[net.L - 1], stream);
       ++launches;

@@ -1014,13 +1014,13 @@ __global__ void __launch_bounds__(256, 2) loss_stream4_kernel(
 // 32 columns per block, nw = blockDim/32 warps each summing rows w, w + nw, ... in order,
 // then the warps' partial sums in warp order (deterministic for a given block size: 32
 // warps when few columns must cover many rows, 8 when the grid is already wide)
-constexpr int kRowWarps = 32;
 template <typename Store>
 __device__ __forceinline__ void rows_reduce_block(const float* __restrict__ partial, int rows,
-                                                  long cols, long stride, Store store) {
+                                                  long cols, long stride, Store store,
+                                                  long col_block) {
   __shared__ float sh[kRowWarps][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = int(blockDim.x >> 5);
-  const long c = long(blockIdx.x) * 32 + lane;
+  const long c = col_block * 32 + lane;
   float acc = 0.f;
   if (c < cols)
     for (int r = w; r < rows; r += nw) acc += partial[long(r) * stride + c];
@@ -1032,31 +1032,41 @@ __device__ __forceinline__ void rows_reduce_block(const float* __restrict__ part
     store(c, t);
   }
 }
-inline int rows_reduce_threads(long cols) { return cols >= 8192 ? 256 : 32 * kRowWarps; }
 
 __global__ void __launch_bounds__(1024) rows_reduce_kernel(const float* __restrict__ partial,
                                                           int rows, long cols, long stride,
                                                           float* __restrict__ out) {
   TLG_PDL_ENTRY();
-  rows_reduce_block(partial, rows, cols, stride, [&](long c, float v) { out[c] = v; });
+  rows_reduce_block(partial, rows, cols, stride, [&](long c, float v) { out[c] = v; },
+                    blockIdx.x);
 }
 
 // Head-gradient partials [nblk][A1][H] -> flat gradient (layout-aware, AccumulateGrad
 // order of the families, policy.cpp:122-141).
+// Blocks past the head columns (db_out set): the top trunk layer's bias gradient from the
+// loss kernel's column partials [nblocks][H] -- the same rows, one launch instead of two.
 __global__ void __launch_bounds__(1024) head_grad_reduce_kernel(HeadDesc hd,
                                                                const float* __restrict__ hg_partial,
                                                                int nblocks,
-                                                               float* __restrict__ grad) {
+                                                               float* __restrict__ grad,
+                                                               const float* __restrict__ db_partial,
+                                                               float* __restrict__ db_out) {
   TLG_PDL_ENTRY();
   const int A = hd.A, A1 = A + 1;
   const long nw = long(A1) * hd.H;
+  const long head_blocks = (nw + 31) / 32;
+  if (blockIdx.x >= head_blocks) {
+    rows_reduce_block(db_partial, nblocks, hd.H, hd.H, [&](long c, float v) { db_out[c] = v; },
+                      long(blockIdx.x) - head_blocks);
+    return;
+  }
   rows_reduce_block(hg_partial, nblocks, nw, nw, [&](long idx, float v) {
     const int k = int(idx / hd.H), j = int(idx % hd.H);
     if (k < A)
       grad[hd.wpi + long(k) * hd.wk + long(j) * hd.wj] = v;
     else
       grad[hd.wv + j] = v;
-  });
+  }, blockIdx.x);
 }
 
 // Bias partials [nblk][A1] and the loss/stat partials -> gradient + step statistics.
@@ -1402,10 +1412,15 @@ LossLaunch launch_loss_backward(const HeadDesc& hd, const float* params, const f
 void launch_head_grad_reduce(const HeadDesc& hd, const float* hg_partial,
                              const double* loss_partial, const LossLaunch& ll, float* grad,
                              StepStatsDev* st, cudaStream_t s, const float* bias_partial,
-                             const int* err, float* guard) {
+                             const int* err, float* guard, const float* db_partial,
+                             float* db_out) {
   const long nw = long(hd.A + 1) * hd.H;
-  ::tlg::launch_k(head_grad_reduce_kernel, dim3(ceil_div(nw, 32)), dim3(rows_reduce_threads(nw)), size_t(0), s, 
-      hd, hg_partial, ll.stream_blocks, grad);
+  // (the block size of a separate db reduce over H columns is the same: identical sums)
+  if (db_out && rows_reduce_threads(nw) != rows_reduce_threads(hd.H))
+    throw CudaError("head_grad_reduce: fused db reduce needs one block size");
+  const int blocks = int(ceil_div(nw, 32) + (db_out ? ceil_div(long(hd.H), 32) : 0));
+  ::tlg::launch_k(head_grad_reduce_kernel, dim3(blocks), dim3(rows_reduce_threads(nw)), size_t(0), s,
+      hd, hg_partial, ll.stream_blocks, grad, db_partial, db_out);
   TLG_CHECK_LAUNCH();
   ::tlg::launch_k(head_bias_stats_kernel, dim3(1), dim3(32 * (hd.A + 1 + 5)), size_t(0), s, 
       hd, bias_partial ? bias_partial : hg_partial + long(ll.stream_blocks) * nw, loss_partial,

@@ -120,7 +120,12 @@ void launch_head_grad_reduce(const HeadDesc& hd, const float* hg_partial,
                              const double* loss_partial, const LossLaunch& ll, float* grad,
                              StepStatsDev* st, cudaStream_t s,
                              const float* bias_partial = nullptr, const int* err = nullptr,
-                             float* guard = nullptr);
+                             float* guard = nullptr, const float* db_partial = nullptr,
+                             float* db_out = nullptr);
+// Fixed-order column reductions: warps of the block sum rows w, w + nw, ...; the block
+// size (so the summation order) depends on the column count only.
+constexpr int kRowWarps = 32;
+inline int rows_reduce_threads(long cols) { return cols >= 8192 ? 256 : 32 * kRowWarps; }
 // out[c] = sum_r partial[r*stride + c] for c < cols, fixed order (deterministic).
 void launch_rows_reduce(const float* partial, int rows, long cols, long stride, float* out,
                         cudaStream_t s);
