@@ -26,6 +26,8 @@
 //   warps 2..5  epilogue: TMEM -> registers -> s (a/128 + b/16384) + bias -> tanh ->
 //               hi / tf32-residual planes -> swizzled smem -> TMA store
 //   warps 6..9  converters: bits -> x, x<<7 tiles
+// (gemm_i8_bits_fwd_dec_kernel below keeps the same roles with separate operand rings and
+// up to three epilogue warp groups; it is the default for CTA pairs.)
 #pragma once
 
 #include "gemm_sm100.cuh"
@@ -473,7 +475,10 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
 //   bit rows 4 x 2 KB   (TMA from HBM, feeding the converters)
 // The MMA of k-block kb waits for Q slot kb % NQ and X slot kb % NX and releases both
 // with one commit each.  The epilogue stages through one 4 KB block per warp (the
-// residual plane is not written: write_lo must be 0).
+// residual plane is not written: write_lo must be 0).  MS: 128-row M subtiles per CTA
+// sharing each piece tile; EG: epilogue warp groups (warps 2..5, 10..13, 14..17) on
+// alternate 32-column chunks.  The default (launch_i8_bits_fwd) is <256, 2, 2, 2, 1, 3>:
+// 256-column tiles, single-buffered accumulators drained by twelve epilogue warps.
 template <int BN, int CG, int NQ, int NX, int MS = 1, int EG = 1>
 struct SmemI8Dec {
   static constexpr int kX = kBM * kBKi;           // 16 KB operand tile (x, x<<7)
