@@ -276,11 +276,11 @@ struct tlg_learner {
   uint64_t steps_done = 0;
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
-  // ---- gradient buckets (nranks > 1, one local shard per rank): each layer's dW/db
-  // region of the flat gradient is sum-allreduced on comm_stream as soon as the backward
-  // has written it, overlapping the layers below (learner.cpp:138-149).  The
-  // last bucket travels in one NCCL group with the failure guard; the optimizer waits
-  // for comm_done.  TLG_NO_OVERLAP=1: one allreduce after the whole backward instead.
+  // ---- gradient buckets (TLG_OVERLAP=1, nranks > 1, one local shard per rank): each
+  // layer's dW/db region of the flat gradient is sum-allreduced on comm_stream as soon as
+  // the backward has written it, overlapping the layers below (learner.cpp:138-149,
+  // SURVEY 8(e)).  The last bucket travels in one NCCL group with the failure guard; the
+  // optimizer waits for comm_done.  Default: one allreduce after the whole backward.
   cudaStream_t comm_stream = nullptr;
   static constexpr int kMaxBuckets = 12;
   cudaEvent_t bucket_ev[kMaxBuckets]{};
@@ -289,7 +289,11 @@ struct tlg_learner {
   bool overlap_active = false;
   long pend_off = 0, pend_count = 0;
   bool pend_guard = false;
-  const bool overlap_disabled = std::getenv("TLG_NO_OVERLAP") != nullptr;
+  // Bucketed overlap is opt-in (TLG_OVERLAP=1): measured on NVLink B200s, NCCL kernels
+  // competing with the persistent dW GEMMs for SMs (dW2 71 -> 89 us at N = 2) cost more
+  // than one allreduce of the whole gradient after the backward (C3 weak step 0.81-0.86
+  // vs 0.77-0.80 ms at N = 2 / 4, tools/overlap_probe.sh).
+  const bool overlap_requested = std::getenv("TLG_OVERLAP") != nullptr;
   void issue_bucket(long off, long count, bool with_guard);
   // grad[off, off + count) (and the failure guard, with_guard) is final on `stream`:
   // allreduce it now, or -- the last bucket of the step -- in bucket_flush()
@@ -1173,7 +1177,7 @@ struct tlg_learner {
       pad_rows(params_lo + net.w_off[0], net.dims[1], int(net.D), int(net.D_pad), w1p_lo, stream);
       launches += 2;
     }
-    overlap_active = nranks > 1 && n == 1 && !overlap_disabled;
+    overlap_active = nranks > 1 && n == 1 && overlap_requested;
     n_buckets = 0;
     pend_count = 0;
     pend_guard = false;
