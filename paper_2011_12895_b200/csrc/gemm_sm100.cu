@@ -302,7 +302,9 @@ LaunchInfo launch(const Operand& A, const Operand& B, int M, int N, int K, int e
   for (;;) {
     cg = 1;
     const long tiles2 = long(ceil_div(M, 2 * kBM)) * ceil_div(N, BN) * splits;
-    if (BN >= 128 && M >= 2 * kBM && tiles2 >= num_sms() / 2 && kb_tile >= 8) cg = 2;
+    // (short K loops too when the residual is derived: C4 layer 1, K = 64, 108 -> 98 us)
+    if (BN >= 128 && M >= 2 * kBM && tiles2 >= num_sms() / 2 && (kb_tile >= 8 || wide_lod))
+      cg = 2;
     if (const char* e = std::getenv("TLG_GEMM_CG")) cg = std::atoi(e) == 2 && BN >= 128 ? 2 : 1;
     if (epi == kEpiFwdLoss) cg = 2;
     if (const char* e = std::getenv("TLG_GEMM_CG_U8"))  // tuning experiments only
