@@ -167,6 +167,8 @@ void dispatch_bn(bool a_mn, bool b_mn, bool a_lo, bool b_lo, int epi, int u8, in
       return run_if_fits<BN, false, false, true, true, kEpiFwdTanh, 0, 1>(ah, al, bh, bl, em, p, grid, s);
     if (!a_mn && !b_mn && a_lo && b_lo && epi == kEpiFwdTanh && lod == (1 | kLodEg2))
       return run_if_fits<BN, false, false, true, true, kEpiFwdTanh, 0, 1 | kLodEg2>(ah, al, bh, bl, em, p, grid, s);
+    if (!a_mn && !b_mn && a_lo && b_lo && epi == kEpiFwdTanh && lod == (1 | kLodEg3))
+      return run_if_fits<BN, false, false, true, true, kEpiFwdTanh, 0, 1 | kLodEg3>(ah, al, bh, bl, em, p, grid, s);
     if (!a_mn && !b_mn && a_lo && b_lo && epi == kEpiFwdLoss && lod == 1)
       return run_if_fits<BN, false, false, true, true, kEpiFwdLoss, 0, 1>(ah, al, bh, bl, em, p, grid, s);
     if (!a_mn && b_mn && a_lo && b_lo && epi == kEpiBwdTanh && lod == 1)
@@ -279,8 +281,11 @@ LaunchInfo launch(const Operand& A, const Operand& B, int M, int N, int K, int e
   // two epilogue warp groups (kLodEg2) for the derived-residual tanh forward on 128-column
   // tiles and on short-K 256-column tiles
   auto lod_k = [&](int bn) {
-    return lod | (epi == kEpiFwdTanh && lod != 0 && u8_0 == 0 && (bn == 128 || (bn == 256 && kb_tile < 16))
-                      ? kLodEg2 : 0);
+    if (epi != kEpiFwdTanh || lod == 0 || u8_0 != 0) return lod;
+    // three groups where the K loop is nearly empty (K <= 64: the epilogue is the kernel)
+    if (bn == 256 && kb_tile <= 2 && !std::getenv("TLG_GEMM_EG2")) return lod | kLodEg3;
+    if (bn == 256 && kb_tile < 16) return lod | kLodEg2;
+    return bn == 128 ? lod | kLodEg2 : lod;
   };
   const bool wide_lod = (lod & 1) && (epi == kEpiFwdTanh || epi == kEpiBwdTanh) &&
                         !std::getenv("TLG_GEMM_NARROW");

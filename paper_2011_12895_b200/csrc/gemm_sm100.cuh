@@ -267,11 +267,13 @@ constexpr int kEpiWarps = 4;
 // 128-column tiles, and 256-column tiles of short K loops (a long K loop hides the
 // epilogue, and its pipeline would lose a stage to the extra staging); each group's head
 // partials cover BN / 2 columns (LaunchInfo::bn).
-constexpr int kLodEg2 = 8;
+constexpr int kLodEg2 = 8, kLodEg3 = 16;  // (kLodEg3: three groups, warps 14..17 too)
 __host__ __device__ constexpr int epi_groups(int bn, int epi, int u8, int lod) {
-  // (the dX epilogue is written for either count; measured no faster with two groups)
-  return epi == 0 /* kEpiFwdTanh */ && (lod & kLodEg2) && (lod & 3) && u8 == 0 && bn >= 128
-             ? 2 : 1;
+  // (the dX epilogue is written for any count; measured no faster with two groups)
+  return epi == 0 /* kEpiFwdTanh */ && (lod & (kLodEg2 | kLodEg3)) && (lod & 3) && u8 == 0 &&
+                 bn >= 128
+             ? ((lod & kLodEg3) ? 3 : 2)
+             : 1;
 }
 constexpr int kColMax = 2048;  // widest N with fused column sums
 constexpr int kStageBuf = 32 * 33;  // per-warp 32x32 transpose buffer (+1 pad: no bank conflicts)
@@ -324,7 +326,8 @@ constexpr SmemPlan smem_plan(int BN, bool a_lo, bool b_lo, int epi, int u8, int 
   // The tanh forward shares whenever that buys a stage: its consumers derive the tf32
   // residual in their own shared memory, so out_lo is normally null (TLG_LO_HBM only).
   q.share_lo = epi != kEpiStore && epi != kEpiFwdLoss &&
-               (u8 == 1 || (sep < 3 && shr > sep) || (epi == kEpiFwdTanh && shr > sep));
+               (u8 == 1 || (sep < 3 && shr > sep) || (epi == kEpiFwdTanh && shr > sep) ||
+                (lod & kLodEg3));  // (three groups fit only with one block per warp)
   q.epi_blocks = q.share_lo ? sep_blocks - 1 : sep_blocks;
   q.warp_epi = q.epi_blocks * 4096 + head;
   q.stages = q.share_lo ? shr : sep;
@@ -1106,7 +1109,8 @@ __global__ void __launch_bounds__(kernel_threads(BN, EPI, U8, LOD), 1)
     // row) -> fused op -> 128-B-swizzled smem staging -> TMA bulk store.  The bwd
     // activation block is TMA-prefetched one chunk ahead into its own swizzled buffer.
     const int q = warp & 3;
-    const int grp = warp >= 2 + 2 * kEpiWarps ? 1 : 0;  // epilogue group (kEG == 2)
+    // epilogue group: warps 2..5 -> 0, (converters 6..9), 10..13 -> 1, 14..17 -> 2
+    const int grp = warp < 2 + kEpiWarps ? 0 : (warp - 2 - 2 * kEpiWarps) / kEpiWarps + 1;
     const int ew = grp ? warp - 2 - kEpiWarps : warp - 2;
     const uint32_t blk = sbase + S::kEpiOff + uint32_t(ew * S::kWarpEpi);
     const uint32_t st_out = blk, st_lo = S::kShareLo ? blk : blk + 4096;
